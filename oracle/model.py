@@ -1,0 +1,130 @@
+"""Oracle steps a4-a6: k-layer GCN / GraphSAGE forward, softmax cross-entropy, backward.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Everything is float64, textbook order, on the partition-local CSR only (cut edges are
+simply absent from it -- P:141, "considers exclusively local nodes and edges").
+
+GCN layer ("averages neighbors with degree-based weights"; readings R5, R7):
+    Z = Ahat H W,  Ahat = Dt^-1/2 (A + I) Dt^-1/2,  Dt = diag(d_l + 1)  (virtual self-loop)
+SAGE layer ("aggregated (for example, by averaging) ... combined and multiplied by a
+matrix"; reading R6):
+    M = D_l^-1 A H  (row of zeros where d_l = 0),  Z = H W_self + M W_nbr
+Activation: ReLU on hidden layers, identity on the output layer; ReLU'(0) = 0 (R16).
+No biases (R7).  Loss: mean softmax cross-entropy over the partition's seeds with a
+max-subtracted log-sum-exp (R8).  Backward: exact reverse mode.
+Parameters theta = concatenation in layer order of W (GCN) or W_self, W_nbr (SAGE), each
+[d_in x d_out] row-major.
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+
+
+def adjacency(rowptr, col, n: int) -> sp.csr_matrix:
+    """A (local, unweighted, symmetric) as a sparse matrix; A[v, u] = 1 iff u in N_loc(v)."""
+    rowptr = np.asarray(rowptr, dtype=np.int64)
+    col = np.asarray(col, dtype=np.int64)
+    return sp.csr_matrix((np.ones(col.size, dtype=np.float64), col, rowptr), shape=(n, n))
+
+
+def gcn_operator(rowptr, col, n: int) -> sp.csr_matrix:
+    """Ahat = Dt^-1/2 (A + I) Dt^-1/2 with Dt = d_l + 1."""
+    A = adjacency(rowptr, col, n)
+    d_l = np.diff(np.asarray(rowptr, dtype=np.int64)).astype(np.float64)
+    nrm = 1.0 / np.sqrt(d_l + 1.0)
+    Dn = sp.diags(nrm)
+    return (Dn @ (A + sp.identity(n, format="csr")) @ Dn).tocsr()
+
+
+def sage_operator(rowptr, col, n: int) -> sp.csr_matrix:
+    """D_l^-1 A (mean over local neighbours; zero row where d_l = 0)."""
+    A = adjacency(rowptr, col, n)
+    d_l = np.diff(np.asarray(rowptr, dtype=np.int64)).astype(np.float64)
+    inv = np.where(d_l > 0, 1.0 / np.maximum(d_l, 1.0), 0.0)
+    return (sp.diags(inv) @ A).tocsr()
+
+
+def forward(arch: str, rowptr, col, X, weights):
+    """Returns (logits, cache).  weights[l] = [W] (gcn) or [W_self, W_nbr] (sage), float64."""
+    n = X.shape[0]
+    op = gcn_operator(rowptr, col, n) if arch == "gcn" else sage_operator(rowptr, col, n)
+    H = np.asarray(X, dtype=np.float64)
+    cache = dict(op=op, H=[], P=[], Z=[])
+    L = len(weights)
+    for l, Ws in enumerate(weights):
+        P = op @ H                                     # Ahat H (gcn) or M = D^-1 A H (sage)
+        if arch == "gcn":
+            Z = P @ Ws[0]
+        else:
+            Z = H @ Ws[0] + P @ Ws[1]
+        cache["H"].append(H); cache["P"].append(P); cache["Z"].append(Z)
+        H = np.maximum(Z, 0.0) if l < L - 1 else Z
+    return H, cache
+
+
+def loss_and_dlogits(Z, y, seeds):
+    """L = (1/#S) sum_{v in S} [logsumexp(Z_v) - Z_v[y_v]];  dZ = (softmax - onehot)/#S on S."""
+    seeds = np.asarray(seeds, dtype=np.int64)
+    if seeds.size == 0:
+        raise ValueError("empty seed set (S:213)")
+    Zs = Z[seeds]
+    m = Zs.max(axis=1, keepdims=True)
+    e = np.exp(Zs - m)
+    s = e.sum(axis=1, keepdims=True)
+    lse = (m + np.log(s))[:, 0]
+    ys = np.asarray(y, dtype=np.int64)[seeds]
+    if (ys >= Z.shape[1]).any() or (ys < 0).any():
+        raise ValueError("label out of range (S:280)")
+    loss = float(np.mean(lse - Zs[np.arange(seeds.size), ys]))
+    dZ = np.zeros_like(Z, dtype=np.float64)
+    g = e / s
+    g[np.arange(seeds.size), ys] -= 1.0
+    dZ[seeds] = g / seeds.size
+    return loss, dZ
+
+
+def backward(arch: str, cache, dlogits, weights):
+    """Exact reverse mode through the cached forward; returns grads shaped like weights."""
+    op = cache["op"]
+    L = len(weights)
+    grads = [None] * L
+    dZ = dlogits
+    for l in range(L - 1, -1, -1):
+        H, P, Ws = cache["H"][l], cache["P"][l], weights[l]
+        if arch == "gcn":
+            grads[l] = [P.T @ dZ]
+            dP = dZ @ Ws[0].T
+            dH = op.T @ dP
+        else:
+            grads[l] = [H.T @ dZ, P.T @ dZ]
+            dH = dZ @ Ws[0].T + op.T @ (dZ @ Ws[1].T)
+        if l > 0:
+            dZ = dH * (cache["Z"][l - 1] > 0.0)        # ReLU'(0) = 0 (R16)
+    return grads
+
+
+def flatten(mats) -> np.ndarray:
+    return np.concatenate([np.asarray(m, dtype=np.float64).ravel() for ms in mats for m in ms])
+
+
+def unflatten(theta, shapes) -> list:
+    out, off = [], 0
+    for ms in shapes:
+        row = []
+        for s in ms:
+            k = int(np.prod(s))
+            row.append(np.asarray(theta[off:off + k], dtype=np.float64).reshape(s))
+            off += k
+        out.append(row)
+    return out
+
+
+def partition_loss_grad(arch, part, X, y, weights):
+    """Loss L_p and flat gradient g_p of one isolated partition (full-graph mode).
+    X is indexed by the partition's local ids (rows = part['core'])."""
+    logits, cache = forward(arch, part["rowptr"], part["col"], X, weights)
+    loss, dZ = loss_and_dlogits(logits, y, part["seeds"])
+    grads = backward(arch, cache, dZ, weights)
+    return loss, flatten(grads), logits, cache
