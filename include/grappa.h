@@ -1,0 +1,231 @@
+/*
+ * grappa.h -- C ABI of libgrappa.so, the B200 (sm_100a) hot path of Grappa's
+ * partition-isolated, gradient-only GNN training step (arXiv 2602.01872).
+ *
+ * Citations: P:<n> = PAPER.md line n (section / equation / algorithm named beside it),
+ * S:<n> = SPEC.md line n, R<k> = reading k in DESIGN.md §2 (where the paper is silent).
+ *
+ * Conventions (all entry points)
+ *  - Plain C types only.  "dev" pointers are CUDA device pointers, "host" pointers are
+ *    host memory.  Streams are cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Tensors passed in are CALLER-OWNED; the library never frees them.  grappa_ctx and
+ *    grappa_part are LIBRARY-OWNED and released by their *_destroy call.
+ *  - Dense node tensors are row-major [rows x cols] with cols = the padded width given in
+ *    the call (every width is a multiple of 16; padded columns must be zero on input and
+ *    are kept zero on output).  Weights are fp32 row-major [f_in x f_out].
+ *  - Every call enqueues on the given stream and returns without a device sync, except
+ *    grappa_partition, grappa_repartition, grappa_part_query and grappa_check (documented).
+ *  - Argument errors are detected synchronously before anything is enqueued and return a
+ *    status != GRAPPA_OK; grappa_last_error() then returns a thread-local message.  After
+ *    an error the outputs are unspecified and nothing leaks.  One host thread per ctx.
+ *  - Determinism: results are bitwise reproducible run to run for fixed inputs, device
+ *    count and dtype (no floating-point atomics; fixed-order split-K and reductions).
+ */
+#ifndef GRAPPA_H
+#define GRAPPA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GRAPPA_OK = 0,
+    GRAPPA_E_ARG = 1,        /* invalid argument value (e.g. C<2, base==swept)            */
+    GRAPPA_E_SHAPE = 2,      /* dimension mismatch / width not a multiple of 16          */
+    GRAPPA_E_EMPTY = 3,      /* empty seed set                      */
+    GRAPPA_E_NONFINITE = 4,  /* non-finite gradient or coverage factor     */
+    GRAPPA_E_SUPPORT = 5,    /* reserved: q = 0 in the node-level variant         */
+    GRAPPA_E_NOMEM = 6,      /* device allocation failed                                  */
+    GRAPPA_E_CUDA = 7,       /* CUDA runtime error                                        */
+    GRAPPA_E_NCCL = 8        /* NCCL error                                                */
+} grappa_status;
+
+typedef enum { GRAPPA_F32 = 0, GRAPPA_BF16 = 1 } grappa_dtype;
+typedef enum { GRAPPA_GCN = 0, GRAPPA_SAGE = 1 } grappa_arch;
+
+/* Coverage-correction factor kinds (§3.4):
+ *  NONE           c = 1                         (ablation "UW")
+ *  UNIFORM        eq:correction_uniform P:303-305, the minimum-distance factor (Thm 2)
+ *  RESAMPLING     eq:resampling P:344-346 literal, with SPEC guards D<eps -> 1, cap c_max
+ *                 (S:351); the paper's deployed factor
+ *  RESAMPLING_HM  reading R13 (not the default): sum s_v / sum s_v d_g/d_l            */
+typedef enum {
+    GRAPPA_CORR_NONE = 0,
+    GRAPPA_CORR_UNIFORM = 1,
+    GRAPPA_CORR_RESAMPLING = 2,
+    GRAPPA_CORR_RESAMPLING_HM = 3
+} grappa_corr;
+
+typedef struct grappa_ctx grappa_ctx;    /* per process + GPU: NCCL comm, workspaces      */
+typedef struct grappa_part grappa_part;  /* per partition: local CSR, maps, degrees, seeds */
+
+/* Global graph in CSR (undirected, symmetric, sorted, deduplicated, no self loops;
+ * S:22-28).  Device pointers, caller-owned. */
+typedef struct {
+    int64_t num_nodes;
+    int64_t nnz;
+    const int64_t* rowptr;   /* dev [num_nodes+1] */
+    const int32_t* col;      /* dev [nnz]         */
+} grappa_csr;
+
+/* Read-only view of a partition (all pointers dev, owned by the grappa_part). */
+typedef struct {
+    int64_t n_core;             /* |base chunk| + |swept chunk|                         */
+    int64_t nnz;                /* local directed edges (cut edges dropped)             */
+    int64_t n_seeds;            /* core train nodes (reading R3)                 */
+    int32_t base, swept;        /* chunk ids                                            */
+    int32_t feat_dim;           /* padded feature width of x                            */
+    grappa_dtype dtype;         /* storage dtype of x                                   */
+    const int64_t* rowptr;      /* [n_core+1] local CSR                                 */
+    const int32_t* col;         /* [nnz] local ids, ascending per row (R14)             */
+    const int32_t* core_global; /* [n_core] global id of local id i (ascending)         */
+    const int32_t* d_l;         /* [n_core] local degree                                */
+    const int32_t* d_g;         /* [n_core] global degree                               */
+    const float* norm_gcn;      /* [n_core] (d_l+1)^-1/2  (GCN, virtual self loop, R5)  */
+    const float* norm_sage;     /* [n_core] 1/d_l, 0 where d_l = 0 (SAGE mean, R6)      */
+    const int32_t* seeds;       /* [n_seeds] local ids, ascending                       */
+    const int32_t* labels;      /* [n_core]                                             */
+    const void* x;              /* [n_core x feat_dim] core features, local order       */
+    int64_t n_heavy;            /* rows split into segments for the SpMM (d_l > seg)    */
+    int64_t n_slots;            /* partial-sum slots used by split rows                 */
+    /* coverage statistics over the seeds (full-graph mode: s_v = d_l)                  */
+    double c_uniform;           /* eq:correction_uniform                                */
+    double c_resampling;        /* eq:resampling with guards (eps 1e-9, c_max 10)       */
+    double c_resampling_hm;     /* reading R13                                          */
+    int64_t D;                  /* sum_{seeds, d_l>0} (d_g - d_l), exact integer        */
+} grappa_part_info;
+
+/* ----------------------------------------------------------------------------------- */
+const char* grappa_version(void);
+/* Thread-local message describing the most recent failure on this thread. */
+const char* grappa_last_error(void);
+
+/* NCCL bootstrap: rank 0 fills 128 bytes; the caller broadcasts them (torch.distributed)
+ * and passes them to grappa_ctx_create on every rank. */
+grappa_status grappa_nccl_unique_id(void* out128 /* host, 128 bytes */);
+
+/* Create a context on `device`.  nccl_uid == NULL or nranks == 1 -> single GPU, no NCCL.
+ * Otherwise a collective: every rank must call it with the same uid (ncclCommInitRank). */
+grappa_status grappa_ctx_create(int device, const void* nccl_uid, int rank, int nranks,
+                                grappa_ctx** out);
+void grappa_ctx_destroy(grappa_ctx* ctx);
+
+/* a1 -- random chunking, performed once (§3.3; reading R1):
+ *   chunk_of[v] = pi_seed(v) mod C, pi = 4-round Feistel bijection on [0,N), cycle-walked.
+ * chunk_of: dev int32[num_nodes] (out).  chunk_sizes: host int64[C] (out; the call syncs
+ * the stream).  Errors: E_ARG if C < 2 or C > num_nodes. */
+grappa_status grappa_partition(grappa_ctx* ctx, int64_t num_nodes, int32_t num_chunks,
+                               uint64_t seed, int32_t* chunk_of, int64_t* chunk_sizes,
+                               void* stream);
+
+/* a3 -- super-epoch repartition (§3.3, §4; S:135-143 induced-core mode):
+ * extract the partition of chunk pair {base, swept} from the replicated global CSR:
+ * core = nodes of both chunks in ascending global id (local id = rank), each core row keeps
+ * the neighbours inside the core (cut edges dropped), d_l/d_g, GCN/SAGE norms, core
+ * features gathered into local order, labels, seeds = core train nodes, coverage stats.
+ *   g         dev global CSR;  feats dev [N x feat_dim] (dtype);  chunk_of dev int32[N];
+ *   train_mask dev uint8[N];  labels dev int32[N].
+ *   *inout    NULL -> a new grappa_part is created; otherwise its buffers are reused.
+ * Syncs the stream (twice: to size outputs and to publish the coverage statistics).
+ * Errors: E_ARG base==swept or out of range; E_EMPTY if the partition has no
+ * seeds. */
+grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g, const void* feats,
+                                 int32_t feat_dim, grappa_dtype dtype, const int32_t* chunk_of,
+                                 int32_t num_chunks, int32_t base, int32_t swept,
+                                 const uint8_t* train_mask, const int32_t* labels,
+                                 grappa_part** inout, void* stream);
+grappa_status grappa_part_query(const grappa_part* part, grappa_part_info* out);
+void grappa_part_destroy(grappa_part* part);
+
+/* Workspace sizes (bytes) for one layer call on `part`; `saved` persists fwd -> bwd. */
+size_t grappa_layer_saved_bytes(const grappa_part* part, grappa_arch arch, int32_t f_in,
+                                int32_t f_out, grappa_dtype dtype);
+size_t grappa_layer_ws_bytes(const grappa_part* part, grappa_arch arch, int32_t f_in,
+                             int32_t f_out, grappa_dtype dtype);
+
+/* a4 -- one isolated message-passing layer, forward (§3.2; §5.1):
+ *   GCN  (R5):  h_out = act( Ahat h_in W ),  Ahat = Dt^-1/2 (A_loc + I) Dt^-1/2,
+ *                      Dt = d_l + 1; computed transform-first: T = h_in W (tensor-core
+ *                      GEMM), then h_out_v = act(n_v (n_v T_v + sum_{u in N_loc(v)} n_u T_u))
+ *                      (SpMM).  `saved` unused (may be NULL).
+ *   SAGE (R6):  M = D_l^-1 A_loc h_in (SpMM, zero rows where d_l = 0, kept in
+ *                      `saved`), h_out = act([h_in | M] [W_self; W_nbr]) (one GEMM, K = 2 f_in).
+ *   act = ReLU if relu != 0 else identity (output layer).
+ *   h_in dev [n_core x f_in], h_out dev [n_core x f_out] (dtype); w dev fp32: GCN
+ *   [f_in x f_out], SAGE [2 f_in x f_out] (W_self rows first).  ws: grappa_layer_ws_bytes.
+ * Errors: E_SHAPE if f_in or f_out is not a positive multiple of 16. */
+grappa_status grappa_layer_fwd(grappa_ctx* ctx, const grappa_part* part, grappa_arch arch,
+                               int32_t f_in, int32_t f_out, int relu, const void* h_in,
+                               const float* w, void* h_out, void* saved, void* ws,
+                               grappa_dtype dtype, void* stream);
+
+/* a6 -- the layer's backward (exact reverse mode; ReLU'(0) = 0, R16):
+ *   dz_out   dev [n_core x f_out]: dL/dZ of THIS layer's pre-activation output.
+ *   dw       dev fp32, same shape as w: dL/dW, combined over row splits in fixed order.
+ *   dz_in    dev [n_core x f_in] or NULL (first layer: skipped): dL/dZ of the previous
+ *            layer's pre-activation, i.e. (dL/dh_in) * 1[h_in > 0] when relu_in != 0.
+ *   GCN : dT = Ahat dz_out (SpMM; Ahat symmetric because the induced subgraph of an
+ *         undirected graph is symmetric), dW = h_in^T dT, dh_in = dT W^T.
+ *   SAGE: [dW_self; dW_nbr] = [h_in | M]^T dz_out, dh_in = dz_out W_self^T
+ *         + A_loc D_l^-1 (dz_out W_nbr^T).                                              */
+grappa_status grappa_layer_bwd(grappa_ctx* ctx, const grappa_part* part, grappa_arch arch,
+                               int32_t f_in, int32_t f_out, int relu_in, const void* dz_out,
+                               const void* h_in, const float* w, const void* saved, float* dw,
+                               void* dz_in, void* ws, grappa_dtype dtype, void* stream);
+
+/* a5 -- mean softmax cross-entropy over the partition's seeds (R8):
+ *   L = (1/#S) sum_{v in S} [logsumexp(Z_v[0:K]) - Z_v[y_v]];  dZ_v = (softmax - e_y)/#S on
+ *   seeds, 0 on every other row and on padded columns K..k_pad-1 (masked to -inf).
+ *   logits/dlogits dev [n_core x k_pad] (dtype); loss_dev dev float64[1] (out).
+ * Errors: E_ARG if num_classes > k_pad; E_EMPTY if the partition has no seeds. */
+grappa_status grappa_loss(grappa_ctx* ctx, const grappa_part* part, const void* logits,
+                          int32_t num_classes, int32_t k_pad, void* dlogits, double* loss_dev,
+                          grappa_dtype dtype, void* stream);
+
+/* a7 + a8 -- coverage-corrected aggregation and optimizer step (P:291-306 eq:batch-estimator,
+ * Alg. 1, "applied immediately before the all-reduce"):
+ *   grad <- c_p / m_active * grad (fused scale + non-finite check, device flag), then
+ *   ncclAllReduce(sum) across the context's ranks  =>  grad = (1/M) sum_p c_p g_p (R9),
+ *   then, if lr != 0, theta <- theta - lr * grad (SGD, R10).
+ *   part == NULL marks a rank with no active partition in this phase (contributes zeros).
+ *   c_p is the factor of kind `corr` computed at repartition time (grappa_part_info).
+ *   grad, theta: dev fp32 [n_params].  A COLLECTIVE when the ctx has >1 rank.           */
+grappa_status grappa_aggregate_grads(grappa_ctx* ctx, const grappa_part* part, grappa_corr corr,
+                                     float* grad, int64_t n_params, int32_t m_active, float lr,
+                                     float* theta, void* stream);
+
+/* Sync the stream and report asynchronous faults: E_NONFINITE if any aggregated gradient
+ * since the last check was non-finite, E_CUDA / E_NCCL on device or communicator errors. */
+grappa_status grappa_check(grappa_ctx* ctx, void* stream);
+
+/* Number of kernels this ctx has launched (for the bench's gpu_launches claim). */
+int64_t grappa_launch_count(const grappa_ctx* ctx);
+
+/* Per-kernel-class timing for the roofline report.  While enabled, every call of a class
+ * records a CUDA event pair on its launch stream around that class's launches, plus the
+ * call's ALGORITHMIC bytes and flops (DESIGN.md §4 gives the per-unit formulas):
+ *   SPMM     per edge 4 (col) + 4 (edge weight, GCN) + w*s (gathered row); per row 8 (rowptr)
+ *            + 8 (scales) + w*s (self row, GCN) + w*s (output) [+ w*s accumulate, + w*s mask]
+ *   GEMM     (M*K*s + K*N*4 + M*N*s [+ M*N*s mask]) bytes, 2*M*N*K flops
+ *   GEMM_TN  (M*K*s + M*N*s + K*N*4) bytes, 2*M*N*K flops (split-K partials excluded)
+ * enable(on=1) clears previous records; read() syncs and sums one class. */
+typedef enum {
+    GRAPPA_K_SPMM = 0,
+    GRAPPA_K_GEMM = 1,
+    GRAPPA_K_GEMM_TN = 2,
+    GRAPPA_K_LOSS = 3,
+    GRAPPA_K_AGG = 4,
+    GRAPPA_K_REPART = 5,
+    GRAPPA_K_NCLASS = 6
+} grappa_kclass;
+grappa_status grappa_profile_enable(grappa_ctx* ctx, int on);
+grappa_status grappa_profile_read(grappa_ctx* ctx, int kclass, double* ms, int64_t* calls,
+                                  double* bytes, double* flops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRAPPA_H */

@@ -46,21 +46,36 @@ def sage_operator(rowptr, col, n: int) -> sp.csr_matrix:
     return (sp.diags(inv) @ A).tocsr()
 
 
+def layer_forward(arch: str, op, H, Ws, relu: bool):
+    """One layer: P = op H (Ahat H or D^-1 A H); Z = P W (gcn) or H W_self + P W_nbr (sage);
+    returns (P, Z, act(Z))."""
+    P = op @ H
+    Z = P @ Ws[0] if arch == "gcn" else H @ Ws[0] + P @ Ws[1]
+    return P, Z, (np.maximum(Z, 0.0) if relu else Z)
+
+
+def layer_backward(arch: str, op, H, P, Ws, dZ):
+    """Reverse mode of layer_forward given dL/dZ: returns (weight grads, dL/dH)."""
+    if arch == "gcn":
+        return [P.T @ dZ], op.T @ (dZ @ Ws[0].T)
+    return [H.T @ dZ, P.T @ dZ], dZ @ Ws[0].T + op.T @ (dZ @ Ws[1].T)
+
+
+def operator(arch: str, rowptr, col, n: int):
+    return gcn_operator(rowptr, col, n) if arch == "gcn" else sage_operator(rowptr, col, n)
+
+
 def forward(arch: str, rowptr, col, X, weights):
     """Returns (logits, cache).  weights[l] = [W] (gcn) or [W_self, W_nbr] (sage), float64."""
     n = X.shape[0]
-    op = gcn_operator(rowptr, col, n) if arch == "gcn" else sage_operator(rowptr, col, n)
+    op = operator(arch, rowptr, col, n)
     H = np.asarray(X, dtype=np.float64)
     cache = dict(op=op, H=[], P=[], Z=[])
     L = len(weights)
     for l, Ws in enumerate(weights):
-        P = op @ H                                     # Ahat H (gcn) or M = D^-1 A H (sage)
-        if arch == "gcn":
-            Z = P @ Ws[0]
-        else:
-            Z = H @ Ws[0] + P @ Ws[1]
+        P, Z, Hn = layer_forward(arch, op, H, Ws, l < L - 1)
         cache["H"].append(H); cache["P"].append(P); cache["Z"].append(Z)
-        H = np.maximum(Z, 0.0) if l < L - 1 else Z
+        H = Hn
     return H, cache
 
 
@@ -87,19 +102,12 @@ def loss_and_dlogits(Z, y, seeds):
 
 def backward(arch: str, cache, dlogits, weights):
     """Exact reverse mode through the cached forward; returns grads shaped like weights."""
-    op = cache["op"]
     L = len(weights)
     grads = [None] * L
     dZ = dlogits
     for l in range(L - 1, -1, -1):
-        H, P, Ws = cache["H"][l], cache["P"][l], weights[l]
-        if arch == "gcn":
-            grads[l] = [P.T @ dZ]
-            dP = dZ @ Ws[0].T
-            dH = op.T @ dP
-        else:
-            grads[l] = [H.T @ dZ, P.T @ dZ]
-            dH = dZ @ Ws[0].T + op.T @ (dZ @ Ws[1].T)
+        grads[l], dH = layer_backward(arch, cache["op"], cache["H"][l], cache["P"][l],
+                                      weights[l], dZ)
         if l > 0:
             dZ = dH * (cache["Z"][l - 1] > 0.0)        # ReLU'(0) = 0 (R16)
     return grads

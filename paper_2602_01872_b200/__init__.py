@@ -1,0 +1,207 @@
+"""paper_2602_01872_b200 -- B200-native hot path of Grappa (arXiv 2602.01872).
+
+Thin Python binding over libgrappa.so (C ABI in include/grappa.h).  The functions below
+have the ABI's names and only marshal arguments; every step of the path runs in the
+sm_100a kernels behind the ABI.  PyTorch provides device memory, streams and process
+groups.  ``engine.Trainer`` is the host-side driver (Algorithm 1 phase loop, sweep
+schedule, buffers) built on these calls.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import BF16, CORR, F32, GCN, SAGE, GrappaError, load
+
+__all__ = ["Context", "Part", "grappa_partition", "grappa_repartition", "grappa_layer_fwd",
+           "grappa_layer_bwd", "grappa_loss", "grappa_aggregate_grads", "GCN", "SAGE", "F32",
+           "BF16", "CORR", "GrappaError", "load"]
+
+_TORCH_DT = {F32: torch.float32, BF16: torch.bfloat16}
+
+
+def dtype_code(dt) -> int:
+    if dt in (F32, BF16):
+        return dt
+    return {torch.float32: F32, torch.bfloat16: BF16, "f32": F32, "fp32": F32,
+            "bf16": BF16}[dt]
+
+
+def arch_code(a) -> int:
+    return {"gcn": GCN, "sage": SAGE, GCN: GCN, SAGE: SAGE}[a]
+
+
+class _DevView:
+    """Zero-copy __cuda_array_interface__ view of library-owned device memory."""
+
+    def __init__(self, ptr: int, shape, typestr: str, keepalive):
+        self.__cuda_array_interface__ = {"shape": tuple(int(s) for s in shape),
+                                         "typestr": typestr, "data": (int(ptr or 0), False),
+                                         "version": 3, "strides": None}
+        self._keep = keepalive
+
+
+def _view(ptr, shape, typestr, owner):
+    if int(shape[0]) == 0 or not ptr:
+        return torch.empty(shape, dtype={"<i4": torch.int32, "<i8": torch.int64,
+                                         "<f4": torch.float32}.get(typestr, torch.float32),
+                           device="cuda")
+    return torch.as_tensor(_DevView(ptr, shape, typestr, owner), device="cuda")
+
+
+class Context:
+    """grappa_ctx: one per process + GPU (holds the NCCL communicator when world > 1)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1, nccl_uid: bytes | None = None):
+        lib = load()
+        self.lib = lib
+        h = ctypes.c_void_p()
+        uid = None
+        if nccl_uid is not None:
+            uid = ctypes.create_string_buffer(bytes(nccl_uid), 128)
+        _lib.check("grappa_ctx_create", lib.grappa_ctx_create(device, uid, rank, nranks, ctypes.byref(h)))
+        self.h = h
+        self.device, self.rank, self.nranks = device, rank, nranks
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _lib.check("grappa_nccl_unique_id", load().grappa_nccl_unique_id(buf))
+        return buf.raw
+
+    def launches(self) -> int:
+        return int(self.lib.grappa_launch_count(self.h))
+
+    def profile(self, on: bool):
+        _lib.check("grappa_profile_enable", self.lib.grappa_profile_enable(self.h, int(on)))
+
+    def profile_read(self, kclass: str):
+        """(ms total, calls, algorithmic bytes, flops) of one kernel class since profile(True)."""
+        ms, by, fl = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        n = ctypes.c_int64()
+        _lib.check("grappa_profile_read", self.lib.grappa_profile_read(
+            self.h, _lib.KCLASS[kclass], ctypes.byref(ms), ctypes.byref(n), ctypes.byref(by),
+            ctypes.byref(fl)))
+        return ms.value, n.value, by.value, fl.value
+
+    def check(self, stream=None):
+        _lib.check("grappa_check", self.lib.grappa_check(self.h, _lib.stream_ptr(stream)))
+
+    def close(self):
+        if self.h:
+            self.lib.grappa_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Part:
+    """grappa_part handle + zero-copy tensor views of its device arrays."""
+
+    def __init__(self):
+        self.h = ctypes.c_void_p()
+        self.info = _lib.PartInfo()
+
+    def refresh(self):
+        _lib.check("grappa_part_query", load().grappa_part_query(self.h, ctypes.byref(self.info)))
+        I = self.info
+        n, m, s = I.n_core, I.nnz, I.n_seeds
+        self.n_core, self.nnz, self.n_seeds = n, m, s
+        self.rowptr = _view(I.rowptr, (n + 1,), "<i8", self)
+        self.col = _view(I.col, (m,), "<i4", self)
+        self.core_global = _view(I.core_global, (n,), "<i4", self)
+        self.d_l = _view(I.d_l, (n,), "<i4", self)
+        self.d_g = _view(I.d_g, (n,), "<i4", self)
+        self.norm_gcn = _view(I.norm_gcn, (n,), "<f4", self)
+        self.norm_sage = _view(I.norm_sage, (n,), "<f4", self)
+        self.seeds = _view(I.seeds, (s,), "<i4", self)
+        self.labels = _view(I.labels, (n,), "<i4", self)
+        if I.feat_dim:
+            if I.dtype == BF16:
+                self.x = _view(I.x, (n, I.feat_dim), "<i2", self).view(torch.bfloat16)
+            else:
+                self.x = _view(I.x, (n, I.feat_dim), "<f4", self)
+        else:
+            self.x = None
+        return self
+
+    def factor(self, corr: str) -> float:
+        I = self.info
+        return {"none": 1.0, "uniform": I.c_uniform, "resampling": I.c_resampling,
+                "resampling_hm": I.c_resampling_hm}[corr]
+
+    def destroy(self):
+        if self.h:
+            load().grappa_part_destroy(self.h)
+            self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def grappa_partition(ctx: Context, num_nodes: int, num_chunks: int, seed: int, chunk_of: torch.Tensor,
+                     stream=None):
+    sizes = (ctypes.c_int64 * num_chunks)()
+    _lib.check("grappa_partition", ctx.lib.grappa_partition(
+        ctx.h, num_nodes, num_chunks, ctypes.c_uint64(seed & ((1 << 64) - 1)), _lib.ptr(chunk_of),
+        sizes, _lib.stream_ptr(stream)))
+    return list(sizes)
+
+
+def grappa_repartition(ctx: Context, rowptr: torch.Tensor, col: torch.Tensor, feats, dtype,
+                       chunk_of: torch.Tensor, num_chunks: int, base: int, swept: int,
+                       train_mask: torch.Tensor, labels, part: Part | None = None, stream=None) -> Part:
+    g = _lib.Csr(rowptr.numel() - 1, col.numel(), rowptr.data_ptr(), col.data_ptr())
+    part = part or Part()
+    fdim = 0 if feats is None else feats.shape[1]
+    _lib.check("grappa_repartition", ctx.lib.grappa_repartition(
+        ctx.h, ctypes.byref(g), _lib.ptr(feats), fdim, dtype_code(dtype), _lib.ptr(chunk_of),
+        num_chunks, base, swept, _lib.ptr(train_mask), _lib.ptr(labels), ctypes.byref(part.h),
+        _lib.stream_ptr(stream)))
+    return part.refresh()
+
+
+def layer_saved_bytes(part: Part, arch, f_in, f_out, dtype) -> int:
+    return int(load().grappa_layer_saved_bytes(part.h, arch_code(arch), f_in, f_out, dtype_code(dtype)))
+
+
+def layer_ws_bytes(part: Part, arch, f_in, f_out, dtype) -> int:
+    return int(load().grappa_layer_ws_bytes(part.h, arch_code(arch), f_in, f_out, dtype_code(dtype)))
+
+
+def grappa_layer_fwd(ctx: Context, part: Part, arch, f_in, f_out, relu, h_in, w, h_out, saved, ws,
+                     dtype, stream=None):
+    _lib.check("grappa_layer_fwd", ctx.lib.grappa_layer_fwd(
+        ctx.h, part.h, arch_code(arch), f_in, f_out, int(relu), _lib.ptr(h_in), _lib.ptr(w),
+        _lib.ptr(h_out), _lib.ptr(saved), _lib.ptr(ws), dtype_code(dtype), _lib.stream_ptr(stream)))
+
+
+def grappa_layer_bwd(ctx: Context, part: Part, arch, f_in, f_out, relu_in, dz_out, h_in, w, saved,
+                     dw, dz_in, ws, dtype, stream=None):
+    _lib.check("grappa_layer_bwd", ctx.lib.grappa_layer_bwd(
+        ctx.h, part.h, arch_code(arch), f_in, f_out, int(relu_in), _lib.ptr(dz_out), _lib.ptr(h_in),
+        _lib.ptr(w), _lib.ptr(saved), _lib.ptr(dw), _lib.ptr(dz_in), _lib.ptr(ws), dtype_code(dtype),
+        _lib.stream_ptr(stream)))
+
+
+def grappa_loss(ctx: Context, part: Part, logits, num_classes, k_pad, dlogits, loss_dev, dtype,
+                stream=None):
+    _lib.check("grappa_loss", ctx.lib.grappa_loss(
+        ctx.h, part.h, _lib.ptr(logits), num_classes, k_pad, _lib.ptr(dlogits), _lib.ptr(loss_dev),
+        dtype_code(dtype), _lib.stream_ptr(stream)))
+
+
+def grappa_aggregate_grads(ctx: Context, part: Part | None, corr: str, grad, m_active: int, lr: float,
+                           theta, stream=None):
+    _lib.check("grappa_aggregate_grads", ctx.lib.grappa_aggregate_grads(
+        ctx.h, part.h if part is not None else None, CORR[corr], _lib.ptr(grad), grad.numel(),
+        m_active, ctypes.c_float(lr), _lib.ptr(theta), _lib.stream_ptr(stream)))

@@ -1,0 +1,116 @@
+"""ctypes binding of libgrappa.so -- argument marshalling only, same names as include/grappa.h.
+
+Every function here forwards to the C ABI; no step of the method runs in Python.  Tensors
+are torch CUDA tensors passed as raw device pointers.  A missing or unloadable library is a
+hard error (there is no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgrappa.so")
+
+F32, BF16 = 0, 1
+GCN, SAGE = 0, 1
+CORR = {"none": 0, "uniform": 1, "resampling": 2, "resampling_hm": 3}
+STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_EMPTY", 4: "E_NONFINITE", 5: "E_SUPPORT",
+          6: "E_NOMEM", 7: "E_CUDA", 8: "E_NCCL"}
+
+# every symbol include/grappa.h declares
+SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grappa_ctx_create",
+           "grappa_ctx_destroy", "grappa_partition", "grappa_repartition", "grappa_part_query",
+           "grappa_part_destroy", "grappa_layer_saved_bytes", "grappa_layer_ws_bytes",
+           "grappa_layer_fwd", "grappa_layer_bwd", "grappa_loss", "grappa_aggregate_grads",
+           "grappa_check", "grappa_launch_count", "grappa_profile_enable", "grappa_profile_read"]
+KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5}
+
+
+class GrappaError(RuntimeError):
+    def __init__(self, fn: str, status: int, msg: str):
+        super().__init__(f"{fn} -> {STATUS.get(status, status)}: {msg}")
+        self.status = STATUS.get(status, status)
+
+
+class Csr(ctypes.Structure):
+    _fields_ = [("num_nodes", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("rowptr", ctypes.c_void_p), ("col", ctypes.c_void_p)]
+
+
+class PartInfo(ctypes.Structure):
+    _fields_ = [("n_core", ctypes.c_int64), ("nnz", ctypes.c_int64), ("n_seeds", ctypes.c_int64),
+                ("base", ctypes.c_int32), ("swept", ctypes.c_int32), ("feat_dim", ctypes.c_int32),
+                ("dtype", ctypes.c_int),
+                ("rowptr", ctypes.c_void_p), ("col", ctypes.c_void_p),
+                ("core_global", ctypes.c_void_p), ("d_l", ctypes.c_void_p), ("d_g", ctypes.c_void_p),
+                ("norm_gcn", ctypes.c_void_p), ("norm_sage", ctypes.c_void_p),
+                ("seeds", ctypes.c_void_p), ("labels", ctypes.c_void_p), ("x", ctypes.c_void_p),
+                ("n_heavy", ctypes.c_int64), ("n_slots", ctypes.c_int64),
+                ("c_uniform", ctypes.c_double), ("c_resampling", ctypes.c_double),
+                ("c_resampling_hm", ctypes.c_double), ("D", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libgrappa.so (never builds implicitly; __graft_entry__.build() does that)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} missing: run __graft_entry__.build() (no CPU fallback exists)")
+    lib = ctypes.CDLL(path)
+    vp, i32, i64, u64, f32, dbl, sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64,
+                                        ctypes.c_uint64, ctypes.c_float, ctypes.c_double,
+                                        ctypes.c_size_t)
+    st = ctypes.c_int
+    sig = {
+        "grappa_version": (ctypes.c_char_p, []),
+        "grappa_last_error": (ctypes.c_char_p, []),
+        "grappa_nccl_unique_id": (st, [vp]),
+        "grappa_ctx_create": (st, [ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]),
+        "grappa_ctx_destroy": (None, [vp]),
+        "grappa_partition": (st, [vp, i64, i32, u64, vp, vp, vp]),
+        "grappa_repartition": (st, [vp, ctypes.POINTER(Csr), vp, i32, ctypes.c_int, vp, i32, i32,
+                                    i32, vp, vp, ctypes.POINTER(vp), vp]),
+        "grappa_part_query": (st, [vp, ctypes.POINTER(PartInfo)]),
+        "grappa_part_destroy": (None, [vp]),
+        "grappa_layer_saved_bytes": (sz, [vp, ctypes.c_int, i32, i32, ctypes.c_int]),
+        "grappa_layer_ws_bytes": (sz, [vp, ctypes.c_int, i32, i32, ctypes.c_int]),
+        "grappa_layer_fwd": (st, [vp, vp, ctypes.c_int, i32, i32, ctypes.c_int, vp, vp, vp, vp, vp,
+                                  ctypes.c_int, vp]),
+        "grappa_layer_bwd": (st, [vp, vp, ctypes.c_int, i32, i32, ctypes.c_int, vp, vp, vp, vp, vp,
+                                  vp, vp, ctypes.c_int, vp]),
+        "grappa_loss": (st, [vp, vp, vp, i32, i32, vp, vp, ctypes.c_int, vp]),
+        "grappa_aggregate_grads": (st, [vp, vp, ctypes.c_int, vp, i64, i32, f32, vp, vp]),
+        "grappa_check": (st, [vp, vp]),
+        "grappa_launch_count": (i64, [vp]),
+        "grappa_profile_enable": (st, [vp, ctypes.c_int]),
+        "grappa_profile_read": (st, [vp, ctypes.c_int, ctypes.POINTER(dbl), ctypes.POINTER(i64),
+                                     ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(fn: str, status: int):
+    if status != 0:
+        msg = load().grappa_last_error().decode(errors="replace")
+        raise GrappaError(fn, status, msg)
+
+
+def ptr(t) -> ctypes.c_void_p:
+    """Raw data pointer of a torch tensor (or None)."""
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def stream_ptr(stream) -> ctypes.c_void_p:
+    return ctypes.c_void_p(stream.cuda_stream if stream is not None else 0)

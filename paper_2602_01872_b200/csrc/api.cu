@@ -1,0 +1,378 @@
+// api.cu -- context, error plumbing, layer orchestration (a4/a6) and gradient aggregation
+// (a7/a8) of the grappa C ABI.  See include/grappa.h for the contract of every entry point.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <cmath>
+#include <nccl.h>
+
+#include "gemm.cuh"
+#include "part.cuh"
+#include "spmm.cuh"
+
+namespace grappa {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+grappa_status DevBuf::grow(size_t bytes) {
+    if (bytes <= cap && p) return GRAPPA_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t b = bytes < 256 ? 256 : bytes;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) {
+        p = nullptr;
+        set_error("cudaMalloc(%zu): %s", b, cudaGetErrorString(e));
+        return GRAPPA_E_NOMEM;
+    }
+    cap = b;
+    return GRAPPA_OK;
+}
+
+void DevBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+}
+
+static cudaEvent_t take_event(grappa_ctx* c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+ProfScope::ProfScope(grappa_ctx* c, cudaStream_t st, int cls, double bytes, double flops)
+    : ctx(c), s(st) {
+    if (!ctx || !ctx->profiling) return;
+    ProfRec r{take_event(ctx), take_event(ctx), cls, bytes, flops};
+    cudaEventRecord(r.a, s);
+    idx = (int)ctx->prof.size();
+    ctx->prof.push_back(r);
+}
+
+ProfScope::~ProfScope() {
+    if (idx >= 0) cudaEventRecord(ctx->prof[idx].b, s);
+}
+
+}  // namespace grappa
+
+using namespace grappa;
+
+#define NCCL_OK(expr)                                                                 \
+    do {                                                                              \
+        ncclResult_t _r = (expr);                                                     \
+        if (_r != ncclSuccess) {                                                      \
+            set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr, ncclGetErrorString(_r)); \
+            return GRAPPA_E_NCCL;                                                     \
+        }                                                                             \
+    } while (0)
+
+extern "C" const char* grappa_version(void) { return "grappa-b200 0.1 (sm_100a)"; }
+extern "C" const char* grappa_last_error(void) { return g_err; }
+
+extern "C" grappa_status grappa_nccl_unique_id(void* out128) {
+    GRAPPA_ARG(out128, GRAPPA_E_ARG, "grappa_nccl_unique_id: null");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    NCCL_OK(ncclGetUniqueId(&id));
+    memcpy(out128, &id, 128);
+    return GRAPPA_OK;
+}
+
+extern "C" grappa_status grappa_ctx_create(int device, const void* nccl_uid, int rank, int nranks,
+                                           grappa_ctx** out) {
+    GRAPPA_ARG(out, GRAPPA_E_ARG, "grappa_ctx_create: null out");
+    GRAPPA_ARG(nranks >= 1 && rank >= 0 && rank < nranks, GRAPPA_E_ARG,
+               "grappa_ctx_create: bad rank %d / nranks %d", rank, nranks);
+    GRAPPA_CUDA(cudaSetDevice(device));
+    grappa_ctx* c = new grappa_ctx();
+    c->device = device;
+    c->rank = rank;
+    c->nranks = nranks;
+    cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (cudaMalloc(&c->d_flag, sizeof(int)) != cudaSuccess || cudaMemset(c->d_flag, 0, sizeof(int)) != cudaSuccess) {
+        delete c;
+        set_error("grappa_ctx_create: cannot allocate flag");
+        return GRAPPA_E_NOMEM;
+    }
+    if (nccl_uid && nranks > 1) {
+        ncclUniqueId id;
+        memcpy(&id, nccl_uid, 128);
+        ncclComm_t comm;
+        ncclResult_t r = ncclCommInitRank(&comm, nranks, id, rank);
+        if (r != ncclSuccess) {
+            set_error("ncclCommInitRank: %s", ncclGetErrorString(r));
+            cudaFree(c->d_flag);
+            delete c;
+            return GRAPPA_E_NCCL;
+        }
+        c->comm = comm;
+    }
+    *out = c;
+    return GRAPPA_OK;
+}
+
+extern "C" void grappa_ctx_destroy(grappa_ctx* c) {
+    if (!c) return;
+    if (c->comm) ncclCommDestroy((ncclComm_t)c->comm);
+    c->scan_ws.release();
+    c->red_ws.release();
+    c->small.release();
+    if (c->d_flag) cudaFree(c->d_flag);
+    delete c;
+}
+
+extern "C" int64_t grappa_launch_count(const grappa_ctx* c) { return c ? c->launches : 0; }
+
+extern "C" grappa_status grappa_profile_enable(grappa_ctx* c, int on) {
+    GRAPPA_ARG(c, GRAPPA_E_ARG, "grappa_profile_enable: null ctx");
+    for (auto& r : c->prof) {
+        c->ev_pool.push_back(r.a);
+        c->ev_pool.push_back(r.b);
+    }
+    c->prof.clear();
+    c->profiling = on != 0;
+    return GRAPPA_OK;
+}
+
+extern "C" grappa_status grappa_profile_read(grappa_ctx* c, int cls, double* ms, int64_t* calls,
+                                             double* bytes, double* flops) {
+    GRAPPA_ARG(c && ms && calls && bytes && flops, GRAPPA_E_ARG, "grappa_profile_read: null argument");
+    double t = 0, by = 0, fl = 0;
+    int64_t n = 0;
+    for (auto& r : c->prof) {
+        if (r.cls != cls) continue;
+        GRAPPA_CUDA(cudaEventSynchronize(r.b));
+        float e = 0.f;
+        GRAPPA_CUDA(cudaEventElapsedTime(&e, r.a, r.b));
+        t += e; by += r.bytes; fl += r.flops; n++;
+    }
+    *ms = t; *calls = n; *bytes = by; *flops = fl;
+    return GRAPPA_OK;
+}
+
+// ------------------------------------------------------------------------------ layers
+static inline size_t esz_of(grappa_dtype dt) { return dt == GRAPPA_BF16 ? 2 : 4; }
+
+extern "C" size_t grappa_layer_saved_bytes(const grappa_part* part, grappa_arch arch, int32_t f_in,
+                                           int32_t f_out, grappa_dtype dtype) {
+    (void)f_out;
+    if (!part || arch != GRAPPA_SAGE) return 0;
+    return (size_t)part->info.n_core * f_in * esz_of(dtype);   // M = D^-1 A h_in
+}
+
+extern "C" size_t grappa_layer_ws_bytes(const grappa_part* part, grappa_arch arch, int32_t f_in,
+                                        int32_t f_out, grappa_dtype dtype) {
+    if (!part) return 0;
+    const int64_t n = part->info.n_core, slots = part->info.n_slots;
+    const size_t es = esz_of(dtype);
+    const int wmax = f_in > f_out ? f_in : f_out;
+    size_t node = (size_t)n * (arch == GRAPPA_GCN ? f_out : f_in) * es;       // T / dT / dM
+    size_t partial = (size_t)slots * wmax * 4;
+    int K = arch == GRAPPA_GCN ? f_in : 2 * f_in;
+    size_t splitk = gemm_tn_ws_bytes(n, K, f_out);
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    return al(node) + al(partial) + al(splitk);
+}
+
+struct WsLayout {
+    void* node;
+    float* partial;
+    float* splitk;
+};
+static WsLayout carve(const grappa_part* part, grappa_arch arch, int f_in, int f_out,
+                      grappa_dtype dt, void* ws) {
+    const int64_t n = part->info.n_core, slots = part->info.n_slots;
+    const size_t es = esz_of(dt);
+    const int wmax = f_in > f_out ? f_in : f_out;
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    size_t node = al((size_t)n * (arch == GRAPPA_GCN ? f_out : f_in) * es);
+    size_t partial = al((size_t)slots * wmax * 4);
+    char* b = (char*)ws;
+    return WsLayout{b, (float*)(b + node), (float*)(b + node + partial)};
+}
+
+static grappa_status check_dims(const char* who, int f_in, int f_out) {
+    GRAPPA_ARG(f_in > 0 && f_out > 0 && f_in % 16 == 0 && f_out % 16 == 0, GRAPPA_E_SHAPE,
+               "%s: f_in=%d f_out=%d must be positive multiples of 16", who, f_in, f_out);
+    return GRAPPA_OK;
+}
+
+extern "C" grappa_status grappa_layer_fwd(grappa_ctx* ctx, const grappa_part* part, grappa_arch arch,
+                                          int32_t f_in, int32_t f_out, int relu, const void* h_in,
+                                          const float* w, void* h_out, void* saved, void* ws,
+                                          grappa_dtype dtype, void* stream) {
+    GRAPPA_ARG(ctx && part && h_in && w && h_out && ws, GRAPPA_E_ARG, "grappa_layer_fwd: null argument");
+    GRAPPA_TRY(check_dims("grappa_layer_fwd", f_in, f_out));
+    GRAPPA_ARG(arch != GRAPPA_SAGE || saved, GRAPPA_E_ARG, "grappa_layer_fwd: SAGE needs `saved`");
+    cudaStream_t s = (cudaStream_t)stream;
+    const grappa_part_info& I = part->info;
+    WsLayout L = carve(part, arch, f_in, f_out, dtype, ws);
+    if (arch == GRAPPA_GCN) {
+        // T = h_in W  (transform first: SpMM width = f_out)
+        GemmArgs g;
+        g.M = I.n_core; g.K1 = f_in; g.N = f_out; g.A1 = h_in; g.B = w;
+        g.n_split = f_out; g.C1 = L.node;
+        GRAPPA_TRY(gemm_nn(ctx, g, dtype, s));
+        // h_out = act(n_v (n_v T_v + sum n_u T_u))
+        SpmmArgs a;
+        a.X = L.node; a.width = f_out; a.row_scale = I.norm_gcn; a.col_scale = I.norm_gcn;
+        a.self = 1; a.relu = relu; a.out = h_out; a.partial = L.partial;
+        return spmm(ctx, part, a, dtype, s);
+    }
+    // SAGE: M = D^-1 A h_in ; h_out = act([h_in | M] [Ws; Wn])
+    SpmmArgs a;
+    a.X = h_in; a.width = f_in; a.row_scale = I.norm_sage; a.out = saved; a.partial = L.partial;
+    GRAPPA_TRY(spmm(ctx, part, a, dtype, s));
+    GemmArgs g;
+    g.M = I.n_core; g.K1 = f_in; g.K2 = f_in; g.N = f_out; g.A1 = h_in; g.A2 = saved; g.B = w;
+    g.relu = relu; g.n_split = f_out; g.C1 = h_out;
+    return gemm_nn(ctx, g, dtype, s);
+}
+
+extern "C" grappa_status grappa_layer_bwd(grappa_ctx* ctx, const grappa_part* part, grappa_arch arch,
+                                          int32_t f_in, int32_t f_out, int relu_in, const void* dz_out,
+                                          const void* h_in, const float* w, const void* saved,
+                                          float* dw, void* dz_in, void* ws, grappa_dtype dtype,
+                                          void* stream) {
+    GRAPPA_ARG(ctx && part && dz_out && h_in && w && dw && ws, GRAPPA_E_ARG,
+               "grappa_layer_bwd: null argument");
+    GRAPPA_TRY(check_dims("grappa_layer_bwd", f_in, f_out));
+    GRAPPA_ARG(arch != GRAPPA_SAGE || saved, GRAPPA_E_ARG, "grappa_layer_bwd: SAGE needs `saved`");
+    cudaStream_t s = (cudaStream_t)stream;
+    const grappa_part_info& I = part->info;
+    WsLayout L = carve(part, arch, f_in, f_out, dtype, ws);
+    if (arch == GRAPPA_GCN) {
+        // dT = Ahat dz_out
+        SpmmArgs a;
+        a.X = dz_out; a.width = f_out; a.row_scale = I.norm_gcn; a.col_scale = I.norm_gcn;
+        a.self = 1; a.out = L.node; a.partial = L.partial;
+        GRAPPA_TRY(spmm(ctx, part, a, dtype, s));
+        // dW = h_in^T dT
+        GemmTNArgs t;
+        t.M = I.n_core; t.K1 = f_in; t.N = f_out; t.A1 = h_in; t.B = L.node; t.C = dw; t.ws = L.splitk;
+        GRAPPA_TRY(gemm_tn(ctx, t, dtype, s));
+        if (!dz_in) return GRAPPA_OK;
+        // dz_in = (dT W^T) * relu'(h_in)
+        GemmArgs g;
+        g.M = I.n_core; g.K1 = f_out; g.N = f_in; g.A1 = L.node; g.B = w; g.b_trans = 1;
+        g.mask = relu_in ? h_in : nullptr; g.n_split = f_in; g.C1 = dz_in;
+        return gemm_nn(ctx, g, dtype, s);
+    }
+    // SAGE: [dWs; dWn] = [h_in | M]^T dz_out
+    GemmTNArgs t;
+    t.M = I.n_core; t.K1 = f_in; t.K2 = f_in; t.N = f_out; t.A1 = h_in; t.A2 = saved; t.B = dz_out;
+    t.C = dw; t.ws = L.splitk;
+    GRAPPA_TRY(gemm_tn(ctx, t, dtype, s));
+    if (!dz_in) return GRAPPA_OK;
+    // [dh_s | dM] = dz_out [Ws^T | Wn^T];  dz_in = (dh_s + A D^-1 dM) * relu'(h_in)
+    GemmArgs g;
+    g.M = I.n_core; g.K1 = f_out; g.N = 2 * f_in; g.A1 = dz_out; g.B = w; g.b_trans = 1;
+    g.n_split = f_in; g.C1 = dz_in; g.C2 = L.node;
+    GRAPPA_TRY(gemm_nn(ctx, g, dtype, s));
+    SpmmArgs a;
+    a.X = L.node; a.width = f_in; a.col_scale = I.norm_sage; a.accumulate = 1;
+    a.mask = relu_in ? h_in : nullptr; a.out = dz_in; a.partial = L.partial;
+    return spmm(ctx, part, a, dtype, s);
+}
+
+// ------------------------------------------------------------------------------ aggregate
+namespace grappa {
+
+// grad *= scale; flag non-finite; if fuse_sgd: theta -= lr * grad (single-rank fast path)
+__global__ void k_scale_grad(int64_t n, float* __restrict__ grad, float scale, int* flag,
+                             int fuse_sgd, float lr, float* __restrict__ theta) {
+    int bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float g = grad[i] * scale;
+        bad |= !isfinite(g);
+        grad[i] = g;
+        if (fuse_sgd) theta[i] = theta[i] - lr * g;
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+__global__ void k_sgd(int64_t n, const float* __restrict__ grad, float lr, float* __restrict__ theta,
+                      int* flag) {
+    int bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float g = grad[i];
+        bad |= !isfinite(g);
+        theta[i] = theta[i] - lr * g;
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+}  // namespace grappa
+
+extern "C" grappa_status grappa_aggregate_grads(grappa_ctx* ctx, const grappa_part* part,
+                                                grappa_corr corr, float* grad, int64_t n_params,
+                                                int32_t m_active, float lr, float* theta,
+                                                void* stream) {
+    GRAPPA_ARG(ctx && grad && n_params > 0, GRAPPA_E_ARG, "grappa_aggregate_grads: null argument");
+    GRAPPA_ARG(m_active >= 1, GRAPPA_E_ARG, "grappa_aggregate_grads: m_active must be >= 1");
+    GRAPPA_ARG(lr == 0.f || theta, GRAPPA_E_ARG, "grappa_aggregate_grads: lr != 0 needs theta");
+    cudaStream_t s = (cudaStream_t)stream;
+    double c = 0.0;   // inactive rank: contributes zeros
+    if (part) {
+        const grappa_part_info& I = part->info;
+        switch (corr) {
+            case GRAPPA_CORR_NONE: c = 1.0; break;
+            case GRAPPA_CORR_UNIFORM: c = I.c_uniform; break;
+            case GRAPPA_CORR_RESAMPLING: c = I.c_resampling; break;
+            case GRAPPA_CORR_RESAMPLING_HM: c = I.c_resampling_hm; break;
+            default: set_error("grappa_aggregate_grads: bad corr %d", (int)corr); return GRAPPA_E_ARG;
+        }
+        GRAPPA_ARG(std::isfinite(c), GRAPPA_E_NONFINITE, "grappa_aggregate_grads: non-finite c (S:361)");
+    }
+    const float scale = (float)(c / (double)m_active);
+    const bool multi = ctx->comm && ctx->nranks > 1;
+    ProfScope ps(ctx, s, GRAPPA_K_AGG, (double)n_params * 4.0 * (lr != 0.f ? 4 : 2), 3.0 * n_params);
+    unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n_params, 256), (int64_t)ctx->sm_count * 4);
+    k_scale_grad<<<grid, 256, 0, s>>>(n_params, grad, scale, ctx->d_flag, (!multi && lr != 0.f) ? 1 : 0,
+                                      lr, theta);
+    GRAPPA_LAUNCHED(ctx);
+    if (multi) {
+        NCCL_OK(ncclAllReduce(grad, grad, (size_t)n_params, ncclFloat32, ncclSum,
+                              (ncclComm_t)ctx->comm, s));
+        if (lr != 0.f) {
+            k_sgd<<<grid, 256, 0, s>>>(n_params, grad, lr, theta, ctx->d_flag);
+            GRAPPA_LAUNCHED(ctx);
+        }
+    }
+    return GRAPPA_OK;
+}
+
+extern "C" grappa_status grappa_check(grappa_ctx* ctx, void* stream) {
+    GRAPPA_ARG(ctx, GRAPPA_E_ARG, "grappa_check: null ctx");
+    cudaStream_t s = (cudaStream_t)stream;
+    int flag = 0;
+    GRAPPA_CUDA(cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    GRAPPA_CUDA(cudaStreamSynchronize(s));
+    if (ctx->comm) {
+        ncclResult_t ar;
+        NCCL_OK(ncclCommGetAsyncError((ncclComm_t)ctx->comm, &ar));
+        NCCL_OK(ar);
+    }
+    if (flag) {
+        GRAPPA_CUDA(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), s));
+        set_error("non-finite aggregated gradient (S:424)");
+        return GRAPPA_E_NONFINITE;
+    }
+    return GRAPPA_OK;
+}

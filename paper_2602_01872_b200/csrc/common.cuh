@@ -1,0 +1,119 @@
+// common.cuh -- shared internals of libgrappa.so (status plumbing, ctx, small device helpers).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <string>
+#include "../../include/grappa.h"
+
+namespace grappa {
+
+void set_error(const char* fmt, ...);
+
+#define GRAPPA_ARG(cond, code, ...)              \
+    do {                                         \
+        if (!(cond)) {                           \
+            ::grappa::set_error(__VA_ARGS__);    \
+            return code;                         \
+        }                                        \
+    } while (0)
+
+#define GRAPPA_CUDA(expr)                                                              \
+    do {                                                                               \
+        cudaError_t _e = (expr);                                                       \
+        if (_e != cudaSuccess) {                                                       \
+            ::grappa::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,             \
+                                cudaGetErrorString(_e));                               \
+            return _e == cudaErrorMemoryAllocation ? GRAPPA_E_NOMEM : GRAPPA_E_CUDA;   \
+        }                                                                              \
+    } while (0)
+
+#define GRAPPA_TRY(expr)                          \
+    do {                                          \
+        grappa_status _s = (expr);                \
+        if (_s != GRAPPA_OK) return _s;           \
+    } while (0)
+
+// Launch bookkeeping: every kernel launch goes through LAUNCHED() so the ctx can report
+// how many of its own kernels ran (bench.py's gpu_launches claim).
+#define GRAPPA_LAUNCHED(ctx)                                                             \
+    do {                                                                                 \
+        cudaError_t _e = cudaGetLastError();                                             \
+        if (_e != cudaSuccess) {                                                         \
+            ::grappa::set_error("%s:%d launch: %s", __FILE__, __LINE__,                  \
+                                cudaGetErrorString(_e));                                 \
+            return GRAPPA_E_CUDA;                                                        \
+        }                                                                                \
+        if (ctx) (ctx)->launches++;                                                      \
+    } while (0)
+
+// Growable device scratch buffer owned by the ctx (never used inside graph capture unless
+// already large enough: grow() only allocates when the request exceeds capacity).
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    grappa_status grow(size_t bytes);
+    void release();
+};
+
+// Optional per-kernel-class timing (grappa_profile_*): CUDA events recorded on the launch
+// stream around each class's launches, plus the algorithmic bytes / flops of the call.
+struct ProfRec {
+    cudaEvent_t a, b;
+    int cls;
+    double bytes, flops;
+};
+
+}  // namespace grappa
+
+#include <vector>
+
+struct grappa_ctx {
+    bool profiling = false;
+    std::vector<grappa::ProfRec> prof;
+    std::vector<cudaEvent_t> ev_pool;
+    int device = 0;
+    int rank = 0;
+    int nranks = 1;
+    void* comm = nullptr;        // ncclComm_t
+    int sm_count = 148;
+    int64_t launches = 0;
+    int* d_flag = nullptr;       // non-finite flag (device)
+    grappa::DevBuf scan_ws;      // device-wide scan partials
+    grappa::DevBuf red_ws;       // reductions
+    grappa::DevBuf small;        // small host-visible results staging (device side)
+    void* h_pinned = nullptr;    // pinned host staging (64 KB)
+};
+
+namespace grappa {
+
+constexpr int kWarp = 32;
+// Rows whose local degree exceeds kSegLen are split into kSegLen-edge segments processed
+// by separate warps, combined in segment order by a fix-up kernel (deterministic).
+constexpr int kSegLen = 256;
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// RAII scope: records start/stop events around one class of launches when profiling.
+struct ProfScope {
+    grappa_ctx* ctx;
+    cudaStream_t s;
+    int idx = -1;
+    ProfScope(grappa_ctx* c, cudaStream_t st, int cls, double bytes, double flops);
+    ~ProfScope();
+};
+
+// Device-wide exclusive scan helpers (scan.cu).  `count` elements of int32 `in` (or the
+// flag functor result) -> int64 exclusive prefix in `out` (out[count] = total), total also
+// returned in *d_total (device int64) when non-null.
+grappa_status scan_i32_to_i64(grappa_ctx* ctx, const int32_t* in, int64_t count, int64_t* out,
+                              cudaStream_t s);
+
+}  // namespace grappa

@@ -1,0 +1,44 @@
+// gemm.cuh -- dense feature-transform GEMMs of a4/a6 (the only dense contractions).
+#pragma once
+#include "common.cuh"
+
+namespace grappa {
+
+// C = [A1 | A2] * op(B), fp32 accumulate.
+//   A1 [M x K1], A2 [M x K2] (dtype, row-major; A2 may be null with K2 = 0)
+//   B fp32: b_trans = 0 -> [K x N] row-major;  b_trans = 1 -> [N x K] row-major (i.e. W^T)
+//   columns [0, n_split) -> C1 (row stride n_split), [n_split, N) -> C2 (stride N - n_split)
+//   epilogue on C1 columns: *= 1[mask > 0] (mask [M x n_split], dtype) then ReLU if relu.
+struct GemmArgs {
+    int64_t M = 0;
+    int K1 = 0, K2 = 0, N = 0;
+    const void* A1 = nullptr;
+    const void* A2 = nullptr;
+    const float* B = nullptr;
+    int b_trans = 0;
+    int relu = 0;
+    const void* mask = nullptr;
+    int n_split = 0;
+    void* C1 = nullptr;
+    void* C2 = nullptr;
+};
+
+// dW = [A1 | A2]^T * B  ([K1+K2] x N, fp32), reduction over the M rows split into slabs
+// whose fp32 partials (ws) are summed in slab order (deterministic split-K).
+struct GemmTNArgs {
+    int64_t M = 0;
+    int K1 = 0, K2 = 0, N = 0;
+    const void* A1 = nullptr;
+    const void* A2 = nullptr;
+    const void* B = nullptr;  // [M x N] dtype
+    float* C = nullptr;       // [(K1+K2) x N] fp32
+    float* ws = nullptr;      // split-K partials
+};
+
+constexpr int kMaxSplitK = 128;
+size_t gemm_tn_ws_bytes(int64_t M, int K, int N);
+
+grappa_status gemm_nn(grappa_ctx* ctx, const GemmArgs& g, grappa_dtype dt, cudaStream_t s);
+grappa_status gemm_tn(grappa_ctx* ctx, const GemmTNArgs& g, grappa_dtype dt, cudaStream_t s);
+
+}  // namespace grappa

@@ -1,0 +1,100 @@
+// loss.cu -- a5: mean softmax cross-entropy over the partition's seeds + its gradient.
+//
+// SPEC S:276-285 (loss_and_grad), reading R8 (mean over the partition's seeds):
+//   L = (1/#S) sum_{v in S} [lse(Z_v[0:K]) - Z_v[y_v]],  dZ_v = (softmax(Z_v) - e_{y_v}) / #S
+// on seeds, zero on every other row and on the padded columns (masked to -inf).
+// Warp per seed row; per-block partial losses in f64 combined in block order (deterministic).
+#include "part.cuh"
+#include "spmm.cuh"
+
+namespace grappa {
+
+template <typename T> __device__ __forceinline__ float lf(const T* p);
+template <> __device__ __forceinline__ float lf<float>(const float* p) { return *p; }
+template <> __device__ __forceinline__ float lf<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+template <typename T> __device__ __forceinline__ void sf(T* p, float v);
+template <> __device__ __forceinline__ void sf<float>(float* p, float v) { *p = v; }
+template <> __device__ __forceinline__ void sf<__nv_bfloat16>(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+
+constexpr int kLossThreads = 256;
+constexpr int kMaxKPad = 512;
+
+template <typename T>
+__global__ void __launch_bounds__(kLossThreads) k_loss(int64_t n_seeds, const int32_t* seeds,
+                                                       const int32_t* labels, const T* logits,
+                                                       int K, int kpad, T* dlogits, double* part) {
+    __shared__ double wsum[kLossThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t k = (int64_t)blockIdx.x * (kLossThreads / 32) + wid;
+    double my = 0.0;
+    if (k < n_seeds) {
+        const int32_t v = seeds[k];
+        const T* z = logits + (int64_t)v * kpad;
+        T* dz = dlogits + (int64_t)v * kpad;
+        const int y = labels[v];
+        float m = -INFINITY;
+        for (int c = lane; c < K; c += 32) m = fmaxf(m, lf<T>(z + c));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        float se = 0.f;
+        for (int c = lane; c < K; c += 32) se += expf(lf<T>(z + c) - m);
+        se = warp_sum(se);
+        const float lse = m + logf(se);
+        const float inv = 1.0f / (float)n_seeds;
+        for (int c = lane; c < kpad; c += 32) {
+            float g = 0.f;
+            if (c < K) g = (expf(lf<T>(z + c) - m) / se - (c == y ? 1.f : 0.f)) * inv;
+            sf<T>(dz + c, g);
+        }
+        if (lane == 0) my = (double)lse - (double)lf<T>(z + y);
+    }
+    if (lane == 0) wsum[wid] = my;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kLossThreads / 32; w++) s += wsum[w];
+        part[blockIdx.x] = s;
+    }
+}
+
+__global__ void k_loss_final(int nb, const double* part, double inv_n, double* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int b = 0; b < nb; b++) s += part[b];
+        *out = s * inv_n;
+    }
+}
+
+}  // namespace grappa
+
+using namespace grappa;
+
+extern "C" grappa_status grappa_loss(grappa_ctx* ctx, const grappa_part* part, const void* logits,
+                                     int32_t num_classes, int32_t k_pad, void* dlogits,
+                                     double* loss_dev, grappa_dtype dtype, void* stream) {
+    GRAPPA_ARG(ctx && part && logits && dlogits && loss_dev, GRAPPA_E_ARG, "grappa_loss: null argument");
+    GRAPPA_ARG(num_classes >= 1 && num_classes <= k_pad && k_pad <= kMaxKPad, GRAPPA_E_ARG,
+               "grappa_loss: need 1 <= K <= k_pad <= %d", kMaxKPad);
+    const grappa_part_info& I = part->info;
+    GRAPPA_ARG(I.n_seeds > 0, GRAPPA_E_EMPTY, "grappa_loss: empty seed set (S:213)");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t esz = dtype == GRAPPA_BF16 ? 2 : 4;
+    ProfScope ps(ctx, s, GRAPPA_K_LOSS, (double)I.n_core * k_pad * esz + 2.0 * I.n_seeds * k_pad * esz,
+                 5.0 * I.n_seeds * num_classes);
+    GRAPPA_CUDA(cudaMemsetAsync(dlogits, 0, (size_t)I.n_core * k_pad * esz, s));
+    const int64_t nb = ceil_div(I.n_seeds, kLossThreads / 32);
+    GRAPPA_TRY(ctx->red_ws.grow((size_t)nb * sizeof(double)));
+    double* part_sums = (double*)ctx->red_ws.p;
+    if (dtype == GRAPPA_BF16)
+        k_loss<__nv_bfloat16><<<(unsigned)nb, kLossThreads, 0, s>>>(
+            I.n_seeds, I.seeds, I.labels, (const __nv_bfloat16*)logits, num_classes, k_pad,
+            (__nv_bfloat16*)dlogits, part_sums);
+    else
+        k_loss<float><<<(unsigned)nb, kLossThreads, 0, s>>>(I.n_seeds, I.seeds, I.labels,
+                                                            (const float*)logits, num_classes,
+                                                            k_pad, (float*)dlogits, part_sums);
+    GRAPPA_LAUNCHED(ctx);
+    k_loss_final<<<1, 32, 0, s>>>((int)nb, part_sums, 1.0 / (double)I.n_seeds, loss_dev);
+    GRAPPA_LAUNCHED(ctx);
+    return GRAPPA_OK;
+}

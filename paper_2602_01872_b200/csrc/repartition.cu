@@ -1,0 +1,369 @@
+// repartition.cu -- a3: super-epoch repartition = induced chunk-pair subgraph extraction.
+//
+// PAPER: P:188-198 (§3.3 super-epochs, chunks, partition = base chunk + swept chunk),
+// P:413 (§4 "workers load the new chunk's edges"), SPEC S:135-143 (build_partition,
+// induced-core mode S:116), S:208 (seeds = core train nodes).
+//
+// Integer pipeline, bit-exact with the oracle:
+//   1. rank table   rank[v] = #core nodes < v (exclusive scan of the core flag), -1 if not
+//                   core; core_global[rank[v]] = v  -> local id = ascending global order.
+//   2. row count    warp per core row: d_l = popc(ballot(rank[u] >= 0)) over its neighbours,
+//                   d_g = global degree; norms, labels, seed flag.
+//   3. rowptr       exclusive scan of d_l (int64).  Seeds, split rows, slots: more scans.
+//   4. fill         warp per core row: stable ballot compaction of kept neighbours, written
+//                   as rank[u] (ascending because the global row is sorted and rank is
+//                   monotone).
+//   5. features     core rows gathered into local order (16-byte vector copies).
+//   6. coverage     fixed-order block partials over the seeds: sum d_l/d_g (f64) and the
+//                   exact integers D = sum (d_g - d_l), sum d_l, sum d_g (d_l > 0).
+#include "part.cuh"
+#include "scan.cuh"
+
+#include <cmath>
+
+namespace grappa {
+
+struct FlagCore {
+    const int32_t* chunk_of; int32_t b, s;
+    __device__ int32_t operator()(int64_t v) const {
+        int32_t c = chunk_of[v];
+        return (c == b) | (c == s);
+    }
+};
+struct WriteRank {
+    int32_t* rank; int32_t* core_global; int64_t* stat;
+    __device__ void operator()(int64_t v, int64_t p, int32_t f) const {
+        rank[v] = f ? (int32_t)p : -1;
+        if (f) core_global[p] = (int32_t)v;
+    }
+    __device__ void finish(int64_t, int64_t total) const { stat[0] = total; }
+};
+
+struct ReadI32 {
+    const int32_t* a;
+    __device__ int32_t operator()(int64_t i) const { return a[i]; }
+};
+struct WriteRowptr {
+    int64_t* rowptr; int64_t* stat;
+    __device__ void operator()(int64_t i, int64_t p, int32_t) const { rowptr[i] = p; }
+    __device__ void finish(int64_t n, int64_t total) const { rowptr[n] = total; stat[1] = total; }
+};
+struct FlagSeed {
+    const int32_t* core_global; const uint8_t* train;
+    __device__ int32_t operator()(int64_t i) const { return train[core_global[i]] != 0; }
+};
+struct WriteCompact {
+    int32_t* out; int64_t* stat; int idx;
+    __device__ void operator()(int64_t i, int64_t p, int32_t f) const {
+        if (f) out[p] = (int32_t)i;
+    }
+    __device__ void finish(int64_t, int64_t total) const { stat[idx] = total; }
+};
+struct FlagHeavy {
+    const int32_t* d_l;
+    __device__ int32_t operator()(int64_t i) const { return d_l[i] > kSegLen; }
+};
+struct NumSeg {
+    const int32_t* d_l; const int32_t* heavy_rows;
+    __device__ int32_t operator()(int64_t h) const {
+        return (int32_t)ceil_div(d_l[heavy_rows[h]], kSegLen);
+    }
+};
+struct WriteSlotOff {
+    int32_t* slot_off; int64_t* stat;
+    __device__ void operator()(int64_t h, int64_t p, int32_t) const { slot_off[h] = (int32_t)p; }
+    __device__ void finish(int64_t n, int64_t total) const { slot_off[n] = (int32_t)total; stat[4] = total; }
+};
+
+__global__ void k_row_count(int64_t n_core, const int32_t* __restrict__ core_global,
+                            const int64_t* __restrict__ g_rowptr, const int32_t* __restrict__ g_col,
+                            const int32_t* __restrict__ rank, const int32_t* __restrict__ g_labels,
+                            int32_t* d_l, int32_t* d_g, float* norm_gcn, float* norm_sage,
+                            int32_t* labels) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n_core; i += nwarps) {
+        const int32_t v = core_global[i];
+        const int64_t e0 = g_rowptr[v], e1 = g_rowptr[v + 1];
+        int32_t cnt = 0;
+        for (int64_t e = e0 + lane; e - lane < e1; e += 32) {
+            bool keep = false;
+            if (e < e1) keep = rank[g_col[e]] >= 0;
+            cnt += __popc(__ballot_sync(0xffffffffu, keep));
+        }
+        if (lane == 0) {
+            d_l[i] = cnt;
+            d_g[i] = (int32_t)(e1 - e0);
+            norm_gcn[i] = (float)(1.0 / sqrt((double)cnt + 1.0));
+            norm_sage[i] = cnt > 0 ? (float)(1.0 / (double)cnt) : 0.0f;
+            labels[i] = g_labels ? g_labels[v] : 0;
+        }
+    }
+}
+
+__global__ void k_row_fill(int64_t n_core, const int32_t* __restrict__ core_global,
+                           const int64_t* __restrict__ g_rowptr, const int32_t* __restrict__ g_col,
+                           const int32_t* __restrict__ rank, const int64_t* __restrict__ rowptr,
+                           int32_t* __restrict__ col) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n_core; i += nwarps) {
+        const int32_t v = core_global[i];
+        const int64_t e0 = g_rowptr[v], e1 = g_rowptr[v + 1];
+        int64_t out = rowptr[i];
+        for (int64_t e = e0 + lane; e - lane < e1; e += 32) {
+            int32_t r = -1;
+            if (e < e1) r = rank[g_col[e]];
+            unsigned m = __ballot_sync(0xffffffffu, r >= 0);
+            if (r >= 0) col[out + __popc(m & ((1u << lane) - 1u))] = r;
+            out += __popc(m);
+        }
+    }
+}
+
+__global__ void k_slot_tasks(int64_t n_heavy, const int32_t* heavy_rows, const int32_t* slot_off,
+                             int32_t* slot_row, int32_t* slot_seg) {
+    for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < n_heavy;
+         h += (int64_t)gridDim.x * blockDim.x) {
+        int32_t r = heavy_rows[h];
+        for (int32_t t = slot_off[h], sgi = 0; t < slot_off[h + 1]; t++, sgi++) {
+            slot_row[t] = r;
+            slot_seg[t] = sgi;
+        }
+    }
+}
+
+__global__ void k_gather_rows(int64_t n_core, int64_t row_bytes, const int32_t* __restrict__ core_global,
+                              const uint4* __restrict__ src, uint4* __restrict__ dst) {
+    const int64_t vec = row_bytes / 16;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n_core; i += nwarps) {
+        const uint4* s = src + (int64_t)core_global[i] * vec;
+        uint4* d = dst + i * vec;
+        for (int64_t k = lane; k < vec; k += 32) d[k] = s[k];
+    }
+}
+
+// Coverage statistics over the seeds, fixed-order block partials.
+struct SeedStats {
+    double sum_r;      // sum d_l/d_g (ratio 1 where d_g = 0), R4
+    long long D;       // sum_{d_l>0} (d_g - d_l)
+    long long sum_dl;  // sum_{d_l>0} d_l
+    long long sum_dg;  // sum_{d_l>0} d_g
+};
+
+constexpr int kStatThreads = 256;
+
+__device__ SeedStats block_reduce_stats(SeedStats v) {
+    __shared__ SeedStats sh[kStatThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v.sum_r = warp_sum(v.sum_r);
+    v.D = warp_sum(v.D);
+    v.sum_dl = warp_sum(v.sum_dl);
+    v.sum_dg = warp_sum(v.sum_dg);
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    SeedStats t{0, 0, 0, 0};
+    if (threadIdx.x == 0)
+        for (int w = 0; w < kStatThreads / 32; w++) {
+            t.sum_r += sh[w].sum_r; t.D += sh[w].D; t.sum_dl += sh[w].sum_dl; t.sum_dg += sh[w].sum_dg;
+        }
+    return t;
+}
+
+__global__ void k_seed_stats(int64_t n_seeds, const int32_t* seeds, const int32_t* d_l,
+                             const int32_t* d_g, SeedStats* part) {
+    SeedStats a{0, 0, 0, 0};
+    const int64_t per = ceil_div(n_seeds, gridDim.x);
+    const int64_t s0 = blockIdx.x * per, s1 = min(n_seeds, s0 + per);
+    for (int64_t k = s0 + threadIdx.x; k < s1; k += blockDim.x) {
+        const int32_t i = seeds[k];
+        const int32_t l = d_l[i], g = d_g[i];
+        a.sum_r += g == 0 ? 1.0 : (double)l / (double)g;
+        if (l > 0) { a.D += g - l; a.sum_dl += l; a.sum_dg += g; }
+    }
+    SeedStats t = block_reduce_stats(a);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+__global__ void k_seed_stats_final(int nb, const SeedStats* part, SeedStats* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        SeedStats t{0, 0, 0, 0};
+        for (int b = 0; b < nb; b++) {
+            t.sum_r += part[b].sum_r; t.D += part[b].D; t.sum_dl += part[b].sum_dl; t.sum_dg += part[b].sum_dg;
+        }
+        *out = t;
+    }
+}
+
+}  // namespace grappa
+
+using namespace grappa;
+
+static grappa_status rp_grid(grappa_ctx* ctx, int64_t rows, int threads, unsigned* grid) {
+    int64_t warps_per_block = threads / 32;
+    int64_t b = ceil_div(rows, warps_per_block);
+    int64_t cap = (int64_t)ctx->sm_count * 16;
+    *grid = (unsigned)(b < 1 ? 1 : (b > cap ? cap : b));
+    return GRAPPA_OK;
+}
+
+extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g, const void* feats,
+                                            int32_t feat_dim, grappa_dtype dtype,
+                                            const int32_t* chunk_of, int32_t num_chunks,
+                                            int32_t base, int32_t swept, const uint8_t* train_mask,
+                                            const int32_t* labels, grappa_part** inout,
+                                            void* stream) {
+    GRAPPA_ARG(ctx && g && chunk_of && train_mask && inout, GRAPPA_E_ARG,
+               "grappa_repartition: null argument");
+    GRAPPA_ARG(base != swept, GRAPPA_E_ARG, "grappa_repartition: base == swept (S:139)");
+    GRAPPA_ARG(base >= 0 && swept >= 0 && base < num_chunks && swept < num_chunks, GRAPPA_E_ARG,
+               "grappa_repartition: chunk id out of range");
+    GRAPPA_ARG(feats == nullptr || (feat_dim > 0 && feat_dim % 16 == 0), GRAPPA_E_SHAPE,
+               "grappa_repartition: feat_dim must be a positive multiple of 16");
+    GRAPPA_ARG(g->num_nodes > 0 && g->num_nodes < (1ll << 31), GRAPPA_E_ARG,
+               "grappa_repartition: num_nodes out of int32 range");
+    cudaStream_t s = (cudaStream_t)stream;
+    ProfScope ps(ctx, s, GRAPPA_K_REPART, 0.0, 0.0);
+    grappa_part* p = *inout ? *inout : new grappa_part();
+    const int64_t N = g->num_nodes;
+    auto fail = [&](grappa_status st) {
+        if (!*inout) {
+            grappa_part_destroy(p);
+        }
+        return st;
+    };
+#define RP_TRY(expr)                               \
+    do {                                           \
+        grappa_status _s = (expr);                 \
+        if (_s != GRAPPA_OK) return fail(_s);      \
+    } while (0)
+
+    // stats: [0]=n_core [1]=nnz [2]=n_seeds [3]=n_heavy [4]=n_slots ; then SeedStats
+    RP_TRY(ctx->small.grow(16 * sizeof(int64_t) + sizeof(SeedStats)));
+    int64_t* d_stat = (int64_t*)ctx->small.p;
+    SeedStats* d_seedstats = (SeedStats*)(d_stat + 8);
+    RP_TRY(ctx->red_ws.grow((size_t)N * sizeof(int32_t)));       // rank table
+    int32_t* rank = (int32_t*)ctx->red_ws.p;
+    // 1. rank table.  core_global capacity: N (freed/reused across super-epochs)
+    RP_TRY(p->core_global.grow((size_t)N * sizeof(int32_t)));
+    RP_TRY(device_scan(ctx, FlagCore{chunk_of, base, swept}, N,
+                       WriteRank{rank, (int32_t*)p->core_global.p, d_stat}, s));
+    int64_t n_core = 0;
+    if (cudaMemcpyAsync(&n_core, d_stat, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+        set_error("grappa_repartition: %s", cudaGetErrorString(cudaGetLastError()));
+        return fail(GRAPPA_E_CUDA);
+    }
+    GRAPPA_ARG(n_core > 0, fail(GRAPPA_E_EMPTY), "grappa_repartition: empty partition");
+    // 2. per-row counts
+    RP_TRY(p->d_l.grow(n_core * 4));
+    RP_TRY(p->d_g.grow(n_core * 4));
+    RP_TRY(p->norm_gcn.grow(n_core * 4));
+    RP_TRY(p->norm_sage.grow(n_core * 4));
+    RP_TRY(p->labels.grow(n_core * 4));
+    RP_TRY(p->rowptr.grow((n_core + 1) * 8));
+    RP_TRY(p->seeds.grow(n_core * 4));
+    RP_TRY(p->heavy_rows.grow(n_core * 4));
+    RP_TRY(p->heavy_slot_off.grow((n_core + 1) * 4));
+    unsigned grid;
+    rp_grid(ctx, n_core, 256, &grid);
+    k_row_count<<<grid, 256, 0, s>>>(n_core, (int32_t*)p->core_global.p, g->rowptr, g->col, rank,
+                                      labels, (int32_t*)p->d_l.p, (int32_t*)p->d_g.p,
+                                      (float*)p->norm_gcn.p, (float*)p->norm_sage.p,
+                                      (int32_t*)p->labels.p);
+    GRAPPA_LAUNCHED(ctx);
+    // 3. scans
+    RP_TRY(device_scan(ctx, ReadI32{(int32_t*)p->d_l.p}, n_core,
+                       WriteRowptr{(int64_t*)p->rowptr.p, d_stat}, s));
+    RP_TRY(device_scan(ctx, FlagSeed{(int32_t*)p->core_global.p, train_mask}, n_core,
+                       WriteCompact{(int32_t*)p->seeds.p, d_stat, 2}, s));
+    RP_TRY(device_scan(ctx, FlagHeavy{(int32_t*)p->d_l.p}, n_core,
+                       WriteCompact{(int32_t*)p->heavy_rows.p, d_stat, 3}, s));
+    int64_t st[5];
+    if (cudaMemcpyAsync(st, d_stat, 5 * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+        set_error("grappa_repartition: %s", cudaGetErrorString(cudaGetLastError()));
+        return fail(GRAPPA_E_CUDA);
+    }
+    const int64_t nnz = st[1], n_seeds = st[2], n_heavy = st[3];
+    GRAPPA_ARG(n_seeds > 0, fail(GRAPPA_E_EMPTY),
+               "grappa_repartition: partition (%d,%d) has no seeds (S:213)", base, swept);
+    RP_TRY(device_scan(ctx, NumSeg{(int32_t*)p->d_l.p, (int32_t*)p->heavy_rows.p}, n_heavy,
+                       WriteSlotOff{(int32_t*)p->heavy_slot_off.p, d_stat}, s));
+    // 4. fill
+    RP_TRY(p->col.grow((size_t)(nnz > 0 ? nnz : 1) * 4));
+    k_row_fill<<<grid, 256, 0, s>>>(n_core, (int32_t*)p->core_global.p, g->rowptr, g->col, rank,
+                                     (int64_t*)p->rowptr.p, (int32_t*)p->col.p);
+    GRAPPA_LAUNCHED(ctx);
+    // 5. features
+    const int64_t esz = dtype == GRAPPA_BF16 ? 2 : 4;
+    if (feats) {
+        RP_TRY(p->x.grow((size_t)n_core * feat_dim * esz));
+        k_gather_rows<<<grid, 256, 0, s>>>(n_core, feat_dim * esz, (int32_t*)p->core_global.p,
+                                           (const uint4*)feats, (uint4*)p->x.p);
+        GRAPPA_LAUNCHED(ctx);
+    }
+    // 6. coverage statistics
+    int nb = (int)std::min<int64_t>(ceil_div(n_seeds, 4096), (int64_t)ctx->sm_count * 4);
+    if (nb < 1) nb = 1;
+    RP_TRY(ctx->scan_ws.grow((size_t)nb * sizeof(SeedStats)));
+    k_seed_stats<<<nb, kStatThreads, 0, s>>>(n_seeds, (int32_t*)p->seeds.p, (int32_t*)p->d_l.p,
+                                              (int32_t*)p->d_g.p, (SeedStats*)ctx->scan_ws.p);
+    GRAPPA_LAUNCHED(ctx);
+    k_seed_stats_final<<<1, 32, 0, s>>>(nb, (SeedStats*)ctx->scan_ws.p, d_seedstats);
+    GRAPPA_LAUNCHED(ctx);
+    int64_t n_slots = 0;
+    SeedStats hs;
+    if (cudaMemcpyAsync(&n_slots, d_stat + 4, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(&hs, d_seedstats, sizeof(hs), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+        set_error("grappa_repartition: %s", cudaGetErrorString(cudaGetLastError()));
+        return fail(GRAPPA_E_CUDA);
+    }
+    if (n_heavy == 0) n_slots = 0;
+    RP_TRY(p->slot_row.grow((size_t)(n_slots > 0 ? n_slots : 1) * 4));
+    RP_TRY(p->slot_seg.grow((size_t)(n_slots > 0 ? n_slots : 1) * 4));
+    if (n_heavy > 0) {
+        k_slot_tasks<<<(unsigned)std::min<int64_t>(ceil_div(n_heavy, 256), 1024), 256, 0, s>>>(
+            n_heavy, (int32_t*)p->heavy_rows.p, (int32_t*)p->heavy_slot_off.p,
+            (int32_t*)p->slot_row.p, (int32_t*)p->slot_seg.p);
+        GRAPPA_LAUNCHED(ctx);
+    }
+    // publish
+    grappa_part_info& I = p->info;
+    I.n_core = n_core; I.nnz = nnz; I.n_seeds = n_seeds; I.base = base; I.swept = swept;
+    I.feat_dim = feats ? feat_dim : 0; I.dtype = dtype;
+    I.rowptr = (int64_t*)p->rowptr.p; I.col = (int32_t*)p->col.p;
+    I.core_global = (int32_t*)p->core_global.p; I.d_l = (int32_t*)p->d_l.p; I.d_g = (int32_t*)p->d_g.p;
+    I.norm_gcn = (float*)p->norm_gcn.p; I.norm_sage = (float*)p->norm_sage.p;
+    I.seeds = (int32_t*)p->seeds.p; I.labels = (int32_t*)p->labels.p; I.x = p->x.p;
+    I.n_heavy = n_heavy; I.n_slots = n_slots;
+    I.c_uniform = hs.sum_r / (double)n_seeds;
+    I.D = hs.D;
+    const double D = (double)hs.D;
+    I.c_resampling = D < 1e-9 ? 1.0 : std::min(1.0 / D, 10.0);
+    I.c_resampling_hm = hs.sum_dl > 0 ? (double)hs.sum_dl / (double)hs.sum_dg : 1.0;
+    *inout = p;
+    return GRAPPA_OK;
+#undef RP_TRY
+}
+
+extern "C" grappa_status grappa_part_query(const grappa_part* part, grappa_part_info* out) {
+    GRAPPA_ARG(part && out, GRAPPA_E_ARG, "grappa_part_query: null argument");
+    *out = part->info;
+    return GRAPPA_OK;
+}
+
+extern "C" void grappa_part_destroy(grappa_part* p) {
+    if (!p) return;
+    for (grappa::DevBuf* b : {&p->rowptr, &p->col, &p->core_global, &p->d_l, &p->d_g, &p->norm_gcn,
+                              &p->norm_sage, &p->seeds, &p->labels, &p->x, &p->heavy_rows,
+                              &p->heavy_slot_off, &p->slot_row, &p->slot_seg})
+        b->release();
+    delete p;
+}

@@ -1,0 +1,189 @@
+"""Host-side driver: Algorithm 1 (phase-parallel training) over the grappa C ABI.
+
+PAPER: Alg. 1 P:367-393 (§3.6), super-epochs P:188-190 / P:413, sweep schedule P:207,
+batch-level correction before the all-reduce P:306 / P:407.
+
+One process per GPU.  With P partitions (logical workers, W = P = C) and G ranks, each
+epoch runs ceil(P/G) phases; in phase i rank r trains partition i*G + r (if it exists) and
+all ranks aggregate (NCCL all-reduce inside grappa_aggregate_grads, M = active ranks).
+The only cross-GPU traffic inside an iteration is that all-reduce; partitions are
+re-extracted on every rank's GPU from the replicated global CSR at super-epoch switches
+(no feature exchange needed in replicated mode).
+
+Everything numeric happens in libgrappa.so; this module only schedules calls and owns
+buffers (torch CUDA tensors).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import (BF16, F32, Context, Part, grappa_aggregate_grads, grappa_layer_bwd,
+               grappa_layer_fwd, grappa_loss, grappa_partition, grappa_repartition,
+               layer_saved_bytes, layer_ws_bytes)
+
+
+def sweep_schedule(C: int, W: int):
+    """a2 (reading R2 for W < C): per super-epoch t = 1..cycle, the
+    (base, swept) chunk pair of each worker."""
+    if not (1 <= W <= C and C >= 2):
+        raise ValueError("need 1 <= W <= C, C >= 2")
+    if W == C:
+        return [[(w, (w + t) % C) for w in range(W)] for t in range(1, C)]
+    pairs = [(i, j) for i in range(C) for j in range(i + 1, C)]
+    cycle = -(-len(pairs) // W)
+    return [[pairs[((t - 1) * W + w) % len(pairs)] for w in range(W)] for t in range(1, cycle + 1)]
+
+
+@dataclass
+class ModelSpec:
+    arch: str            # "gcn" | "sage"
+    dims: list           # logical widths [F, hidden..., K]
+    dims_pad: list       # padded widths (multiples of 16)
+
+    @property
+    def depth(self):
+        return len(self.dims) - 1
+
+    def layer_shapes(self):
+        """padded weight block shape per layer: GCN [fin, fout]; SAGE [2 fin, fout]"""
+        m = 1 if self.arch == "gcn" else 2
+        return [(m * self.dims_pad[l], self.dims_pad[l + 1]) for l in range(self.depth)]
+
+    def n_params(self):
+        return sum(a * b for a, b in self.layer_shapes())
+
+
+class Trainer:
+    """Partition-isolated full-graph training (Alg. 1) on this rank's GPU."""
+
+    def __init__(self, ctx: Context, rowptr, col, x, labels, train_mask, spec: ModelSpec, weights,
+                 num_chunks: int, chunk_seed: int, corr: str = "resampling", lr: float = 0.003,
+                 repartition_every: int = 10, dtype: str = "f32", num_workers: int | None = None,
+                 stream=None):
+        self.ctx = ctx
+        self.dev = torch.device("cuda", ctx.device)
+        self.stream = stream or torch.cuda.current_stream(self.dev)
+        self.spec = spec
+        self.C = num_chunks
+        self.W = num_workers or num_chunks                     # P = W logical workers
+        self.G = ctx.nranks
+        self.rank = ctx.rank
+        self.corr = corr
+        self.lr = lr
+        self.rep_every = repartition_every
+        self.dt = BF16 if dtype == "bf16" else F32
+        self.tdt = torch.bfloat16 if self.dt == BF16 else torch.float32
+        self.schedule = sweep_schedule(self.C, self.W)
+        as_t = lambda a, dt: (a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))).to(self.dev, dt)
+        # replicated global graph + node data, resident in HBM for the whole run
+        self.rowptr = as_t(rowptr, torch.int64)
+        self.col = as_t(col, torch.int32)
+        self.N = self.rowptr.numel() - 1
+        self.x = as_t(x, torch.float32).to(self.tdt).contiguous()
+        self.labels = as_t(labels, torch.int32)
+        self.train = as_t(train_mask, torch.uint8)
+        # a1: chunk map, once
+        self.chunk_of = torch.empty(self.N, dtype=torch.int32, device=self.dev)
+        self.chunk_sizes = grappa_partition(ctx, self.N, self.C, chunk_seed, self.chunk_of, self.stream)
+        # theta / grad: one flat fp32 buffer each -> one all-reduce per iteration
+        shapes = spec.layer_shapes()
+        self.theta = torch.zeros(spec.n_params(), dtype=torch.float32, device=self.dev)
+        self.grad = torch.zeros_like(self.theta)
+        self.w_views, self.dw_views, off = [], [], 0
+        for (a, b) in shapes:
+            self.w_views.append(self.theta[off:off + a * b].view(a, b))
+            self.dw_views.append(self.grad[off:off + a * b].view(a, b))
+            off += a * b
+        for l, ws in enumerate(weights):
+            blk = np.concatenate([np.asarray(w, dtype=np.float32) for w in ws], axis=0)
+            self.w_views[l].copy_(torch.from_numpy(blk))
+        self.loss_dev = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.parts: dict = {}            # worker id -> Part (this rank's workers)
+        self.t = None
+        self.epoch = 0
+        self.losses = []
+
+    # ------------------------------------------------------------------ partitions
+    def my_workers(self):
+        """workers this rank runs, one per phase: phase i -> worker i*G + rank"""
+        nphase = -(-self.W // self.G)
+        return [(i, i * self.G + self.rank) for i in range(nphase)]
+
+    def repartition(self, t: int):
+        """a3 for super-epoch t on every worker this rank owns."""
+        pairs = self.schedule[(t - 1) % len(self.schedule)]
+        for _, w in self.my_workers():
+            if w >= self.W:
+                continue
+            b, s = pairs[w]
+            self.parts[w] = grappa_repartition(self.ctx, self.rowptr, self.col, self.x, self.dt,
+                                               self.chunk_of, self.C, b, s, self.train, self.labels,
+                                               self.parts.get(w), self.stream)
+        self.t = t
+        self._alloc()
+
+    def _alloc(self):
+        sp = self.spec
+        n_max = max(p.n_core for p in self.parts.values()) if self.parts else 1
+        self.H = [None] + [torch.zeros(n_max, sp.dims_pad[l], dtype=self.tdt, device=self.dev)
+                           for l in range(1, sp.depth + 1)]
+        wmax = max(sp.dims_pad)
+        self.dz = [torch.zeros(n_max * wmax, dtype=self.tdt, device=self.dev) for _ in range(2)]
+        ws = 1
+        saved = []
+        for l in range(sp.depth):
+            fi, fo = sp.dims_pad[l], sp.dims_pad[l + 1]
+            ws = max([ws] + [layer_ws_bytes(p, sp.arch, fi, fo, self.dt) for p in self.parts.values()])
+            sb = max([0] + [layer_saved_bytes(p, sp.arch, fi, fo, self.dt) for p in self.parts.values()])
+            saved.append(torch.empty(max(sb, 1), dtype=torch.uint8, device=self.dev) if sb else None)
+        self.ws = torch.empty(ws, dtype=torch.uint8, device=self.dev)
+        self.saved = saved
+
+    # ------------------------------------------------------------------ one iteration
+    def forward_backward(self, part: Part):
+        """a4-a6 on one isolated partition: L x layer_fwd, loss, L x layer_bwd -> self.grad"""
+        sp, n, s = self.spec, part.n_core, self.stream
+        L = sp.depth
+        dp = sp.dims_pad
+        H = [part.x] + [h[:n] for h in self.H[1:]]
+        for l in range(L):
+            grappa_layer_fwd(self.ctx, part, sp.arch, dp[l], dp[l + 1], l < L - 1, H[l],
+                             self.w_views[l], H[l + 1], self.saved[l], self.ws, self.dt, s)
+        dz = self.dz[0][: n * dp[L]].view(n, dp[L])
+        grappa_loss(self.ctx, part, H[L], sp.dims[L], dp[L], dz, self.loss_dev, self.dt, s)
+        for l in range(L - 1, -1, -1):
+            dz_in = self.dz[(L - l) % 2][: n * dp[l]].view(n, dp[l]) if l > 0 else None
+            grappa_layer_bwd(self.ctx, part, sp.arch, dp[l], dp[l + 1], l > 0, dz, H[l],
+                             self.w_views[l], self.saved[l], self.dw_views[l], dz_in, self.ws,
+                             self.dt, s)
+            dz = dz_in
+        return H[L]
+
+    def phase_step(self, phase: int, worker: int, m_active: int, lr=None):
+        part = self.parts.get(worker) if worker < self.W else None
+        if part is not None:
+            self.forward_backward(part)
+        else:
+            self.grad.zero_()
+        grappa_aggregate_grads(self.ctx, part, self.corr, self.grad, m_active,
+                               self.lr if lr is None else lr, self.theta, self.stream)
+
+    def run_epoch(self, on_phase=None):
+        """One epoch of Alg. 1: ceil(W/G) phases, one aggregate + SGD step per phase."""
+        t = 1 + self.epoch // self.rep_every
+        if t != self.t:
+            self.repartition(t)
+        for i, w in self.my_workers():
+            m_active = min(self.G, self.W - i * self.G)
+            self.phase_step(i, w, m_active)
+            if on_phase is not None:
+                on_phase()
+        self.epoch += 1
+
+    @property
+    def nnz(self):
+        return int(self.col.numel())
