@@ -221,6 +221,10 @@ typedef enum {
     GRAPPA_K_REPART = 5,
     GRAPPA_K_NCLASS = 6
 } grappa_kclass;
+/* Test hook: on != 0 routes bf16 GEMMs to the CUDA-core kernels instead of tcgen05 (process
+ * wide), so tests can cross-check the two implementations. */
+void grappa_debug_gemm_simt(int on);
+
 grappa_status grappa_profile_enable(grappa_ctx* ctx, int on);
 grappa_status grappa_profile_read(grappa_ctx* ctx, int kclass, double* ms, int64_t* calls,
                                   double* bytes, double* flops);

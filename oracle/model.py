@@ -46,12 +46,16 @@ def sage_operator(rowptr, col, n: int) -> sp.csr_matrix:
     return (sp.diags(inv) @ A).tocsr()
 
 
-def layer_forward(arch: str, op, H, Ws, relu: bool):
+def layer_forward(arch: str, op, H, Ws, relu: bool, mask=None):
     """One layer: P = op H (Ahat H or D^-1 A H); Z = P W (gcn) or H W_self + P W_nbr (sage);
-    returns (P, Z, act(Z))."""
+    returns (P, Z, act(Z)).  `mask` (optional, reading R16b): the ReLU decision 1[Z > 0]
+    taken by the kernel under test in its own precision -- act(Z) = Z * mask -- so that a
+    pre-activation within rounding of 0 does not make the two sides branch differently."""
     P = op @ H
     Z = P @ Ws[0] if arch == "gcn" else H @ Ws[0] + P @ Ws[1]
-    return P, Z, (np.maximum(Z, 0.0) if relu else Z)
+    if not relu:
+        return P, Z, Z
+    return P, Z, (np.maximum(Z, 0.0) if mask is None else Z * mask)
 
 
 def layer_backward(arch: str, op, H, P, Ws, dZ):
@@ -65,16 +69,19 @@ def operator(arch: str, rowptr, col, n: int):
     return gcn_operator(rowptr, col, n) if arch == "gcn" else sage_operator(rowptr, col, n)
 
 
-def forward(arch: str, rowptr, col, X, weights):
-    """Returns (logits, cache).  weights[l] = [W] (gcn) or [W_self, W_nbr] (sage), float64."""
+def forward(arch: str, rowptr, col, X, weights, masks=None):
+    """Returns (logits, cache).  weights[l] = [W] (gcn) or [W_self, W_nbr] (sage), float64.
+    masks (optional): per hidden layer the ReLU decision to use (see layer_forward)."""
     n = X.shape[0]
     op = operator(arch, rowptr, col, n)
     H = np.asarray(X, dtype=np.float64)
-    cache = dict(op=op, H=[], P=[], Z=[])
+    cache = dict(op=op, H=[], P=[], Z=[], M=[])
     L = len(weights)
     for l, Ws in enumerate(weights):
-        P, Z, Hn = layer_forward(arch, op, H, Ws, l < L - 1)
+        mk = None if masks is None or l >= L - 1 else masks[l]
+        P, Z, Hn = layer_forward(arch, op, H, Ws, l < L - 1, mk)
         cache["H"].append(H); cache["P"].append(P); cache["Z"].append(Z)
+        cache["M"].append((Z > 0.0) if mk is None else mk)
         H = Hn
     return H, cache
 
@@ -109,7 +116,7 @@ def backward(arch: str, cache, dlogits, weights):
         grads[l], dH = layer_backward(arch, cache["op"], cache["H"][l], cache["P"][l],
                                       weights[l], dZ)
         if l > 0:
-            dZ = dH * (cache["Z"][l - 1] > 0.0)        # ReLU'(0) = 0 (R16)
+            dZ = dH * cache["M"][l - 1]                # ReLU' = 1[Z > 0], ReLU'(0) = 0 (R16)
     return grads
 
 
@@ -129,10 +136,10 @@ def unflatten(theta, shapes) -> list:
     return out
 
 
-def partition_loss_grad(arch, part, X, y, weights):
+def partition_loss_grad(arch, part, X, y, weights, masks=None):
     """Loss L_p and flat gradient g_p of one isolated partition (full-graph mode).
     X is indexed by the partition's local ids (rows = part['core'])."""
-    logits, cache = forward(arch, part["rowptr"], part["col"], X, weights)
+    logits, cache = forward(arch, part["rowptr"], part["col"], X, weights, masks)
     loss, dZ = loss_and_dlogits(logits, y, part["seeds"])
     grads = backward(arch, cache, dZ, weights)
     return loss, flatten(grads), logits, cache

@@ -23,7 +23,8 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_ctx_destroy", "grappa_partition", "grappa_repartition", "grappa_part_query",
            "grappa_part_destroy", "grappa_layer_saved_bytes", "grappa_layer_ws_bytes",
            "grappa_layer_fwd", "grappa_layer_bwd", "grappa_loss", "grappa_aggregate_grads",
-           "grappa_check", "grappa_launch_count", "grappa_profile_enable", "grappa_profile_read"]
+           "grappa_check", "grappa_launch_count", "grappa_profile_enable", "grappa_profile_read",
+           "grappa_debug_gemm_simt"]
 KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5}
 
 
@@ -88,6 +89,7 @@ def load(path: str = LIB_PATH):
         "grappa_check": (st, [vp, vp]),
         "grappa_launch_count": (i64, [vp]),
         "grappa_profile_enable": (st, [vp, ctypes.c_int]),
+        "grappa_debug_gemm_simt": (None, [ctypes.c_int]),
         "grappa_profile_read": (st, [vp, ctypes.c_int, ctypes.POINTER(dbl), ctypes.POINTER(i64),
                                      ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
     }

@@ -131,11 +131,19 @@ extern "C" void grappa_ctx_destroy(grappa_ctx* c) {
     c->scan_ws.release();
     c->red_ws.release();
     c->small.release();
+    c->rp_ws.release();
+    for (auto& r : c->prof) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->d_flag) cudaFree(c->d_flag);
     delete c;
 }
 
 extern "C" int64_t grappa_launch_count(const grappa_ctx* c) { return c ? c->launches : 0; }
+
+extern "C" void grappa_debug_gemm_simt(int on) { gemm_force_simt(on); }
 
 extern "C" grappa_status grappa_profile_enable(grappa_ctx* c, int on) {
     GRAPPA_ARG(c, GRAPPA_E_ARG, "grappa_profile_enable: null ctx");
@@ -182,8 +190,7 @@ extern "C" size_t grappa_layer_ws_bytes(const grappa_part* part, grappa_arch arc
     const int wmax = f_in > f_out ? f_in : f_out;
     size_t node = (size_t)n * (arch == GRAPPA_GCN ? f_out : f_in) * es;       // T / dT / dM
     size_t partial = (size_t)slots * wmax * 4;
-    int K = arch == GRAPPA_GCN ? f_in : 2 * f_in;
-    size_t splitk = gemm_tn_ws_bytes(n, K, f_out);
+    size_t splitk = gemm_tn_ws_bytes(n, f_in, arch == GRAPPA_GCN ? 0 : f_in, f_out);
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     return al(node) + al(partial) + al(splitk);
 }

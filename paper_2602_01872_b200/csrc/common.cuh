@@ -82,6 +82,7 @@ struct grappa_ctx {
     grappa::DevBuf scan_ws;      // device-wide scan partials
     grappa::DevBuf red_ws;       // reductions
     grappa::DevBuf small;        // small host-visible results staging (device side)
+    grappa::DevBuf rp_ws;        // repartition task tables
     void* h_pinned = nullptr;    // pinned host staging (64 KB)
 };
 

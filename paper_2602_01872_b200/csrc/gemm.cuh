@@ -36,9 +36,20 @@ struct GemmTNArgs {
 };
 
 constexpr int kMaxSplitK = 128;
-size_t gemm_tn_ws_bytes(int64_t M, int K, int N);
+// workspace for gemm_tn (max over the SIMT and tcgen05 plans); K = K1 + K2
+size_t gemm_tn_ws_bytes(int64_t M, int K1, int K2, int N);
 
+// dispatch: bf16 storage -> tcgen05 kernels (gemm_tc.cu) when the shape fits, else SIMT
 grappa_status gemm_nn(grappa_ctx* ctx, const GemmArgs& g, grappa_dtype dt, cudaStream_t s);
 grappa_status gemm_tn(grappa_ctx* ctx, const GemmTNArgs& g, grappa_dtype dt, cudaStream_t s);
+
+// tcgen05 implementations (bf16 operands, fp32 TMEM accumulators)
+bool gemm_tc_nn_supported(const GemmArgs& g);
+bool gemm_tc_tn_supported(const GemmTNArgs& g);
+grappa_status gemm_tc_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s);
+grappa_status gemm_tc_tn(grappa_ctx* ctx, const GemmTNArgs& g, cudaStream_t s);
+size_t gemm_tc_tn_ws_bytes(int64_t M, int K1, int K2, int N);
+// force the SIMT kernels even for bf16 (tests cross-check the two implementations)
+void gemm_force_simt(int on);
 
 }  // namespace grappa

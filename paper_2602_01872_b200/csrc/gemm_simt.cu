@@ -168,9 +168,14 @@ static int slabs_for(int64_t M) {
     return (int)s;
 }
 
-size_t gemm_tn_ws_bytes(int64_t M, int K, int N) {
-    return (size_t)slabs_for(M) * K * N * sizeof(float);
+size_t gemm_tn_ws_bytes(int64_t M, int K1, int K2, int N) {
+    size_t simt = (size_t)slabs_for(M) * (K1 + K2) * N * sizeof(float);
+    size_t tc = gemm_tc_tn_ws_bytes(M, K1, K2, N);
+    return simt > tc ? simt : tc;
 }
+
+static int g_force_simt = 0;
+void gemm_force_simt(int on) { g_force_simt = on; }
 
 grappa_status gemm_nn(grappa_ctx* ctx, const GemmArgs& g, grappa_dtype dt, cudaStream_t s) {
     if (g.M == 0) return GRAPPA_OK;
@@ -178,6 +183,7 @@ grappa_status gemm_nn(grappa_ctx* ctx, const GemmArgs& g, grappa_dtype dt, cudaS
     ProfScope ps(ctx, s, GRAPPA_K_GEMM,
                  (double)g.M * K * es + K * g.N * 4.0 + (double)g.M * g.N * es * (g.mask ? 2 : 1),
                  2.0 * g.M * g.N * K);
+    if (dt == GRAPPA_BF16 && !g_force_simt && gemm_tc_nn_supported(g)) return gemm_tc_nn(ctx, g, s);
     dim3 grid((unsigned)ceil_div(g.M, BM), (unsigned)ceil_div(g.N, BN));
     if (dt == GRAPPA_BF16) k_gemm_nn<__nv_bfloat16><<<grid, 256, 0, s>>>(g);
     else k_gemm_nn<float><<<grid, 256, 0, s>>>(g);
@@ -191,6 +197,7 @@ grappa_status gemm_tn(grappa_ctx* ctx, const GemmTNArgs& g, grappa_dtype dt, cud
     ProfScope ps(ctx, s, GRAPPA_K_GEMM_TN,
                  (double)g.M * K * es + (double)g.M * g.N * es + (double)K * g.N * 4.0,
                  2.0 * g.M * g.N * K);
+    if (dt == GRAPPA_BF16 && !g_force_simt && g.M > 0 && gemm_tc_tn_supported(g)) return gemm_tc_tn(ctx, g, s);
     const int slabs = g.M > 0 ? slabs_for(g.M) : 1;
     const int64_t rps = g.M > 0 ? ceil_div(g.M, slabs) : 0;
     dim3 grid((unsigned)ceil_div(K, 64), (unsigned)ceil_div(g.N, 64), (unsigned)slabs);

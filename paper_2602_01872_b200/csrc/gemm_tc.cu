@@ -1,0 +1,441 @@
+// gemm_tc.cu -- tcgen05 tensor-core GEMMs of a4/a6 for bf16 storage (fp32 accumulate in TMEM).
+//
+//   k_gemm_tc_nn : C[M x N] = [A1 | A2][M x K] * B           (feature transform, dH = dT W^T)
+//   k_gemm_tc_tn : dW[K x N] = [A1 | A2]^T * Bm, split over row slabs (weight gradient)
+//
+// B200 design.  The transform is tall-skinny (M = 10^5..10^8 node rows, K, N <= 256) and
+// HBM-bound (~64 FLOP/B), so the kernels are built to stream rows at full bandwidth:
+//  * persistent CTAs (one per SM), warp-specialised: warp 0 = TMA producer, warp 1 = single-
+//    thread tcgen05.mma issuer (+ TMEM owner), warps 2-5 = epilogue (TMEM -> regs -> HBM);
+//  * A tiles (128 rows x 64 bf16 = one 128-byte SWIZZLE_128B atom row per node) arrive by
+//    TMA into a 6-stage mbarrier ring; OOB rows / columns are zero-filled by TMA;
+//  * the weights (the whole K x N operand, <= 64 KB bf16) are converted fp32 -> bf16 once per
+//    CTA into the K-major SW128 canonical layout and stay resident in shared memory;
+//  * accumulators double-buffered in TMEM (2 x N columns) so the epilogue of tile i overlaps
+//    the MMAs of tile i+1; fused epilogue: ReLU or relu'-mask, column split, bf16 cast.
+//  * The weight gradient reads both operands MN-major straight from the row-major node
+//    tensors (A = h_in^T, B = dZ^T as UMMA operands), accumulates a CTA's row slab in TMEM
+//    and writes an fp32 partial; partials are summed in slab order (deterministic split-K).
+#include <cudaTypedefs.h>
+
+#include "gemm.cuh"
+#include "tc.cuh"
+
+namespace grappa {
+
+constexpr int kTcThreads = 192;
+constexpr int kNNStages = 6;
+constexpr int kNNStageBytes = 128 * 128;    // 128 rows x 128 B
+constexpr int kTNStages = 4;
+constexpr int kMaxSmem = 227 * 1024;
+// weight-gradient split plan: a fixed CTA budget (= B200 SM count) so workspace sizing and
+// the slab partition (hence the summation order) do not depend on the device queried
+constexpr int kTnCtas = 148;
+
+struct TcNN {
+    int64_t M;
+    int K1, K2, N, kb1, kb2;
+    const float* B;
+    int b_trans;
+    int relu;
+    const __nv_bfloat16* mask;
+    int n_split;
+    __nv_bfloat16* C1;
+    __nv_bfloat16* C2;
+    int num_tiles;
+    uint32_t tmem_cols;
+};
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    k_gemm_tc_nn(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2, TcNN p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const int kbt = p.kb1 + p.kb2;
+    uint8_t* sA = smem;
+    uint8_t* sB = sA + kNNStages * kNNStageBytes;
+    uint64_t* full = (uint64_t*)(sB + (size_t)kbt * p.N * 128);
+    uint64_t* empty = full + kNNStages;
+    uint64_t* tfull = empty + kNNStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // weights -> shared memory once: bf16, K-major, SWIZZLE_128B, zero padded
+    const int nchunks = kbt * p.N * 8;
+    const int Kt = p.K1 + p.K2;
+    for (int idx = threadIdx.x; idx < nchunks; idx += blockDim.x) {
+        const int kb = idx / (p.N * 8), rem = idx % (p.N * 8), n = rem >> 3, ch = rem & 7;
+        __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            int kl, kg;
+            bool ok;
+            if (kb < p.kb1) { kl = kb * 64 + ch * 8 + q; kg = kl; ok = kl < p.K1; }
+            else { kl = (kb - p.kb1) * 64 + ch * 8 + q; kg = p.K1 + kl; ok = kl < p.K2; }
+            float f = 0.f;
+            if (ok) f = p.b_trans ? p.B[(int64_t)n * Kt + kg] : p.B[(int64_t)kg * p.N + n];
+            v[q] = __float2bfloat16_rn(f);
+        }
+        *reinterpret_cast<uint4*>(sB + (size_t)kb * p.N * 128 + tc::sw128_off(n, ch)) =
+            *reinterpret_cast<const uint4*>(v);
+    }
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < kNNStages; s++) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; a++) { tc::mbar_init(&tfull[a], 1); tc::mbar_init(&tempty[a], 4); }
+        tc::mbar_fence_init();
+        tc::tma_prefetch(&tmA1);
+        if (p.kb2) tc::tma_prefetch(&tmA2);
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, p.tmem_cols);
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+                for (int kb = 0; kb < kbt; kb++) {
+                    tc::mbar_wait(&empty[stage], phase ^ 1);
+                    tc::mbar_arrive_expect_tx(&full[stage], kNNStageBytes);
+                    const bool first = kb < p.kb1;
+                    tc::tma_load_2d(sA + stage * kNNStageBytes, first ? &tmA1 : &tmA2, &full[stage],
+                                    (first ? kb : kb - p.kb1) * 64, tile * 128);
+                    if (++stage == kNNStages) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        const uint32_t idesc = tc::idesc_bf16(128, p.N, 0, 0);
+        int stage = 0, acc = 0;
+        uint32_t phase = 0, aphase = 0;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            tc::mbar_wait(&tempty[acc], aphase ^ 1);
+            tc::fence_after();
+            const uint32_t d = tmem + (uint32_t)(acc * p.N);
+            for (int kb = 0; kb < kbt; kb++) {
+                tc::mbar_wait(&full[stage], phase);
+                tc::fence_after();
+                if (lane == 0) {
+                    const uint32_t a0 = tc::smem_u32(sA + stage * kNNStageBytes);
+                    const uint32_t b0 = tc::smem_u32(sB + (size_t)kb * p.N * 128);
+#pragma unroll
+                    for (int k = 0; k < 4; k++)
+                        tc::mma_f16(d, tc::smem_desc_sw128(a0 + k * 32, 0, 1024),
+                                    tc::smem_desc_sw128(b0 + k * 32, 0, 1024), idesc, (kb | k) != 0);
+                    tc::mma_commit(&empty[stage]);
+                }
+                __syncwarp();
+                if (++stage == kNNStages) { stage = 0; phase ^= 1; }
+            }
+            if (lane == 0) tc::mma_commit(&tfull[acc]);
+            __syncwarp();
+            acc ^= 1;
+            if (acc == 0) aphase ^= 1;
+        }
+    } else {
+        const int ew = warp & 3;           // TMEM lane quarter this warp may access
+        const int n2 = p.N - p.n_split;
+        int acc = 0;
+        uint32_t aphase = 0;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            tc::mbar_wait(&tfull[acc], aphase);
+            tc::fence_after();
+            const int64_t row = (int64_t)tile * 128 + ew * 32 + lane;
+            const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * p.N);
+            for (int c0 = 0; c0 < p.N; c0 += 16) {
+                float v[16];
+                tc::tmem_ld16(tbase + c0, v);
+                if (row < p.M) {
+                    __nv_bfloat16* dst;
+                    if (c0 < p.n_split) {
+                        if (p.mask) {
+                            __align__(16) __nv_bfloat16 mk[16];
+                            const uint4* ms = reinterpret_cast<const uint4*>(p.mask + row * p.n_split + c0);
+                            *reinterpret_cast<uint4*>(mk) = __ldg(ms);
+                            *reinterpret_cast<uint4*>(mk + 8) = __ldg(ms + 1);
+#pragma unroll
+                            for (int i = 0; i < 16; i++) v[i] = __bfloat162float(mk[i]) > 0.f ? v[i] : 0.f;
+                        }
+                        if (p.relu) {
+#pragma unroll
+                            for (int i = 0; i < 16; i++) v[i] = fmaxf(v[i], 0.f);
+                        }
+                        dst = p.C1 + row * p.n_split + c0;
+                    } else {
+                        dst = p.C2 + row * n2 + (c0 - p.n_split);
+                    }
+                    __align__(16) __nv_bfloat16 o[16];
+#pragma unroll
+                    for (int i = 0; i < 16; i++) o[i] = __float2bfloat16_rn(v[i]);
+                    reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<const uint4*>(o)[0];
+                    reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<const uint4*>(o)[1];
+                }
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) aphase ^= 1;
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc::fence_after();
+        tc::tmem_dealloc(tmem, p.tmem_cols);
+    }
+}
+
+// ------------------------------------------------------------------------------------- TN
+struct TcTN {
+    int64_t M;
+    int K1, K2, N, Nmma, ft1, ft2, nbox_b;
+    int64_t rows_per_slab;
+    int slabs;
+    float* ws;          // [slabs][ftiles][128][N]
+    uint32_t tmem_cols;
+};
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    k_gemm_tc_tn(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
+                 const __grid_constant__ CUtensorMap tmB, TcTN p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const int a_bytes = 2 * 8192, b_bytes = p.nbox_b * 8192, st_bytes = a_bytes + b_bytes;
+    uint64_t* full = (uint64_t*)(smem + (size_t)kTNStages * st_bytes);
+    uint64_t* empty = full + kTNStages;
+    uint64_t* tfull = empty + kTNStages;
+    uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ft = blockIdx.y;
+    const bool src1 = ft < p.ft1;
+    const int fbase = (src1 ? ft : ft - p.ft1) * 128;
+    const int64_t r0 = (int64_t)blockIdx.x * p.rows_per_slab;
+    const int64_t r1 = min(p.M, r0 + p.rows_per_slab);
+    const int nkb = r1 > r0 ? (int)ceil_div(r1 - r0, 64) : 0;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < kTNStages; s++) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+        tc::mbar_init(tfull, 1);
+        tc::mbar_fence_init();
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, p.tmem_cols);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const CUtensorMap* ma = src1 ? &tmA1 : &tmA2;
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int kb = 0; kb < nkb; kb++) {
+                tc::mbar_wait(&empty[stage], phase ^ 1);
+                tc::mbar_arrive_expect_tx(&full[stage], st_bytes);
+                uint8_t* st = smem + (size_t)stage * st_bytes;
+                const int y = (int)(r0 + kb * 64);
+                tc::tma_load_2d(st, ma, &full[stage], fbase, y);
+                tc::tma_load_2d(st + 8192, ma, &full[stage], fbase + 64, y);
+                for (int j = 0; j < p.nbox_b; j++)
+                    tc::tma_load_2d(st + a_bytes + j * 8192, &tmB, &full[stage], j * 64, y);
+                if (++stage == kTNStages) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        const uint32_t idesc = tc::idesc_bf16(128, p.Nmma, 1, 1);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int kb = 0; kb < nkb; kb++) {
+            tc::mbar_wait(&full[stage], phase);
+            tc::fence_after();
+            if (lane == 0) {
+                const uint32_t a0 = tc::smem_u32(smem + (size_t)stage * st_bytes);
+                const uint32_t b0 = a0 + a_bytes;
+#pragma unroll
+                for (int k = 0; k < 4; k++)      // 16 node rows per MMA = two 8-row K groups
+                    tc::mma_f16(tmem, tc::smem_desc_sw128(a0 + k * 2048, 8192, 1024),
+                                tc::smem_desc_sw128(b0 + k * 2048, 8192, 1024), idesc, (kb | k) != 0);
+                tc::mma_commit(&empty[stage]);
+            }
+            __syncwarp();
+            if (++stage == kTNStages) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) tc::mma_commit(tfull);
+        __syncwarp();
+    } else {
+        const int ew = warp & 3;
+        const int frow = ew * 32 + lane;
+        if (nkb > 0) {
+            tc::mbar_wait(tfull, 0);
+            tc::fence_after();
+        }
+        float* out = p.ws + (((int64_t)blockIdx.x * gridDim.y + ft) * 128 + frow) * p.N;
+        const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16);
+        for (int c0 = 0; c0 < p.N; c0 += 16) {
+            float v[16];
+            tc::tmem_ld16(tbase + c0, v);
+            if (nkb == 0) {
+#pragma unroll
+                for (int i = 0; i < 16; i++) v[i] = 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+                *reinterpret_cast<float4*>(out + c0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        }
+        tc::fence_before();
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc::fence_after();
+        tc::tmem_dealloc(tmem, p.tmem_cols);
+    }
+}
+
+// dW[r][n] = sum_slab ws[slab][ft(r)][row(r)][n], slab order fixed
+__global__ void k_tn_reduce(int64_t count, int N, int K1, int K2, int ft1, int ftiles, int slabs,
+                            const float* __restrict__ ws, float* __restrict__ dw) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / N), n = (int)(i % N);
+        int ft, row;
+        if (r < K1) { ft = r / 128; row = r % 128; }
+        else { ft = ft1 + (r - K1) / 128; row = (r - K1) % 128; }
+        float s = 0.f;
+        for (int z = 0; z < slabs; z++) s += ws[(((int64_t)z * ftiles + ft) * 128 + row) * N + n];
+        dw[i] = s;
+    }
+}
+
+// ------------------------------------------------------------------------------------- host
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static grappa_status get_encoder() {
+    if (g_encode) return GRAPPA_OK;
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return GRAPPA_E_CUDA;
+    }
+    g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    return GRAPPA_OK;
+}
+
+// 2-D bf16 row-major [rows x cols] map, box {64 cols, box_rows rows}, SWIZZLE_128B
+static grappa_status make_map(CUtensorMap* m, const void* ptr, int64_t rows, int cols, int box_rows) {
+    GRAPPA_TRY(get_encoder());
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)(rows > 0 ? rows : 1)};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%d", (int)r, (long long)rows, cols);
+        return GRAPPA_E_CUDA;
+    }
+    return GRAPPA_OK;
+}
+
+static size_t nn_smem(int kbt, int N) {
+    return 1024 + (size_t)kNNStages * kNNStageBytes + (size_t)kbt * N * 128 + 256;
+}
+
+bool gemm_tc_nn_supported(const GemmArgs& g) {
+    const int kbt = (int)(ceil_div(g.K1, 64) + ceil_div(g.K2, 64));
+    return g.N % 16 == 0 && g.N <= 256 && g.K1 % 8 == 0 && g.K2 % 8 == 0 &&
+           nn_smem(kbt, g.N) <= (size_t)kMaxSmem && g.M < (1ll << 31);
+}
+
+static uint32_t pow2_cols(int c) {
+    uint32_t n = 32;
+    while ((int)n < c) n <<= 1;
+    return n;
+}
+
+grappa_status gemm_tc_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s) {
+    CUtensorMap m1, m2;
+    GRAPPA_TRY(make_map(&m1, g.A1, g.M, g.K1, 128));
+    if (g.K2 > 0) GRAPPA_TRY(make_map(&m2, g.A2, g.M, g.K2, 128));
+    else m2 = m1;
+    TcNN p;
+    p.M = g.M; p.K1 = g.K1; p.K2 = g.K2; p.N = g.N;
+    p.kb1 = (int)ceil_div(g.K1, 64); p.kb2 = (int)ceil_div(g.K2, 64);
+    p.B = g.B; p.b_trans = g.b_trans; p.relu = g.relu;
+    p.mask = (const __nv_bfloat16*)g.mask; p.n_split = g.n_split;
+    p.C1 = (__nv_bfloat16*)g.C1; p.C2 = (__nv_bfloat16*)g.C2;
+    p.num_tiles = (int)ceil_div(g.M, 128);
+    p.tmem_cols = pow2_cols(2 * g.N);
+    const size_t smem = nn_smem(p.kb1 + p.kb2, g.N);
+    static bool attr = false;
+    if (!attr) {
+        GRAPPA_CUDA(cudaFuncSetAttribute(k_gemm_tc_nn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+        attr = true;
+    }
+    const int grid = (int)std::min<int64_t>(p.num_tiles, ctx->sm_count);
+    k_gemm_tc_nn<<<grid, kTcThreads, smem, s>>>(m1, m2, p);
+    GRAPPA_LAUNCHED(ctx);
+    return GRAPPA_OK;
+}
+
+static int tn_ftiles(int K) { return (int)ceil_div(K, 128); }
+
+static void tn_plan(int64_t M, int ftiles, int sm_count, int* slabs, int64_t* rps) {
+    int s = sm_count / ftiles;
+    if (s < 1) s = 1;
+    int64_t r = ceil_div(ceil_div(M > 0 ? M : 1, s), 64) * 64;
+    *rps = r;
+    *slabs = (int)ceil_div(M > 0 ? M : 1, r);
+}
+
+size_t gemm_tc_tn_ws_bytes(int64_t M, int K1, int K2, int N) {
+    const int ft = tn_ftiles(K1) + (K2 ? tn_ftiles(K2) : 0);
+    int slabs;
+    int64_t rps;
+    tn_plan(M, ft, kTnCtas, &slabs, &rps);
+    return (size_t)slabs * ft * 128 * N * sizeof(float);
+}
+
+bool gemm_tc_tn_supported(const GemmTNArgs& g) {
+    return g.N % 16 == 0 && g.N <= 256 && g.K1 % 8 == 0 && g.K2 % 8 == 0 && g.M < (1ll << 31);
+}
+
+grappa_status gemm_tc_tn(grappa_ctx* ctx, const GemmTNArgs& g, cudaStream_t s) {
+    CUtensorMap m1, m2, mb;
+    GRAPPA_TRY(make_map(&m1, g.A1, g.M, g.K1, 64));
+    if (g.K2 > 0) GRAPPA_TRY(make_map(&m2, g.A2, g.M, g.K2, 64));
+    else m2 = m1;
+    GRAPPA_TRY(make_map(&mb, g.B, g.M, g.N, 64));
+    TcTN p;
+    p.M = g.M; p.K1 = g.K1; p.K2 = g.K2; p.N = g.N;
+    p.Nmma = (int)ceil_div(g.N, 64) * 64;
+    p.nbox_b = p.Nmma / 64;
+    p.ft1 = tn_ftiles(g.K1);
+    p.ft2 = g.K2 ? tn_ftiles(g.K2) : 0;
+    const int ftiles = p.ft1 + p.ft2;
+    tn_plan(g.M, ftiles, kTnCtas, &p.slabs, &p.rows_per_slab);
+    p.ws = g.ws;
+    p.tmem_cols = pow2_cols(p.Nmma);
+    const size_t smem = 1024 + (size_t)kTNStages * (16384 + p.nbox_b * 8192) + 256;
+    static bool attr = false;
+    if (!attr) {
+        GRAPPA_CUDA(cudaFuncSetAttribute(k_gemm_tc_tn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+        attr = true;
+    }
+    dim3 grid(p.slabs, ftiles);
+    k_gemm_tc_tn<<<grid, kTcThreads, smem, s>>>(m1, m2, mb, p);
+    GRAPPA_LAUNCHED(ctx);
+    const int64_t count = (int64_t)(g.K1 + g.K2) * g.N;
+    k_tn_reduce<<<(unsigned)std::min<int64_t>(ceil_div(count, 256), 1024), 256, 0, s>>>(
+        count, g.N, g.K1, g.K2, p.ft1, ftiles, p.slabs, g.ws, g.C);
+    GRAPPA_LAUNCHED(ctx);
+    return GRAPPA_OK;
+}
+
+}  // namespace grappa

@@ -75,48 +75,101 @@ struct WriteSlotOff {
     __device__ void finish(int64_t n, int64_t total) const { slot_off[n] = (int32_t)total; stat[4] = total; }
 };
 
-__global__ void k_row_count(int64_t n_core, const int32_t* __restrict__ core_global,
-                            const int64_t* __restrict__ g_rowptr, const int32_t* __restrict__ g_col,
-                            const int32_t* __restrict__ rank, const int32_t* __restrict__ g_labels,
-                            int32_t* d_l, int32_t* d_g, float* norm_gcn, float* norm_sage,
-                            int32_t* labels) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < n_core; i += nwarps) {
+// Global rows are cut into tasks of at most kTaskLen edges (power-law hubs reach 10^5
+// neighbours; one warp per task keeps every warp's work bounded).  Tasks are numbered in
+// (row, segment) order, so an exclusive scan of the per-task kept counts is directly each
+// task's output offset in the local `col` array -- and the local rowptr.
+constexpr int kTaskLen = 1024;
+
+struct NumTasks {
+    const int32_t* core_global; const int64_t* g_rowptr;
+    __device__ int32_t operator()(int64_t i) const {
         const int32_t v = core_global[i];
-        const int64_t e0 = g_rowptr[v], e1 = g_rowptr[v + 1];
+        const int64_t d = g_rowptr[v + 1] - g_rowptr[v];
+        return d > kTaskLen ? (int32_t)ceil_div(d, kTaskLen) : 1;
+    }
+};
+struct WriteTasks {
+    int32_t* task_off; int32_t* task_row; int64_t* stat;
+    __device__ void operator()(int64_t i, int64_t p, int32_t k) const {
+        task_off[i] = (int32_t)p;
+        for (int32_t j = 0; j < k; j++) task_row[p + j] = (int32_t)i;
+    }
+    __device__ void finish(int64_t n, int64_t total) const { task_off[n] = (int32_t)total; stat[5] = total; }
+};
+struct ReadTcount {
+    const int32_t* tcount; const int64_t* d_T;
+    __device__ int32_t operator()(int64_t t) const { return t < *d_T ? tcount[t] : 0; }
+};
+struct WriteTaskOut {
+    int64_t* task_out; int64_t* stat;
+    __device__ void operator()(int64_t t, int64_t p, int32_t) const { task_out[t] = p; }
+    __device__ void finish(int64_t n, int64_t total) const { task_out[n] = total; stat[1] = total; }
+};
+
+// kept-neighbour count of every task (warp per task, ballot/popc)
+__global__ void k_task_count(const int64_t* __restrict__ d_T, const int32_t* __restrict__ task_row,
+                             const int32_t* __restrict__ task_off, const int32_t* __restrict__ core_global,
+                             const int64_t* __restrict__ g_rowptr, const int32_t* __restrict__ g_col,
+                             const int32_t* __restrict__ rank, int32_t* __restrict__ tcount) {
+    const int lane = threadIdx.x & 31;
+    const int64_t T = *d_T;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T; t += nwarps) {
+        const int32_t i = task_row[t];
+        const int32_t v = core_global[i];
+        const int64_t e0 = g_rowptr[v] + (t - task_off[i]) * (int64_t)kTaskLen;
+        const int64_t e1 = min(g_rowptr[v + 1], e0 + kTaskLen);
         int32_t cnt = 0;
         for (int64_t e = e0 + lane; e - lane < e1; e += 32) {
             bool keep = false;
             if (e < e1) keep = rank[g_col[e]] >= 0;
             cnt += __popc(__ballot_sync(0xffffffffu, keep));
         }
-        if (lane == 0) {
-            d_l[i] = cnt;
-            d_g[i] = (int32_t)(e1 - e0);
-            norm_gcn[i] = (float)(1.0 / sqrt((double)cnt + 1.0));
-            norm_sage[i] = cnt > 0 ? (float)(1.0 / (double)cnt) : 0.0f;
-            labels[i] = g_labels ? g_labels[v] : 0;
-        }
+        if (lane == 0) tcount[t] = cnt;
     }
 }
 
-__global__ void k_row_fill(int64_t n_core, const int32_t* __restrict__ core_global,
-                           const int64_t* __restrict__ g_rowptr, const int32_t* __restrict__ g_col,
-                           const int32_t* __restrict__ rank, const int64_t* __restrict__ rowptr,
-                           int32_t* __restrict__ col) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < n_core; i += nwarps) {
+// per core row: local rowptr / d_l from the task offsets, d_g, norms, labels
+__global__ void k_row_finalize(int64_t n_core, const int32_t* __restrict__ task_off,
+                               const int64_t* __restrict__ task_out, const int32_t* __restrict__ core_global,
+                               const int64_t* __restrict__ g_rowptr, const int32_t* __restrict__ g_labels,
+                               int64_t* rowptr, int32_t* d_l, int32_t* d_g, float* norm_gcn, float* norm_sage,
+                               int32_t* labels) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_core;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = task_out[task_off[i]], b = task_out[task_off[i + 1]];
         const int32_t v = core_global[i];
-        const int64_t e0 = g_rowptr[v], e1 = g_rowptr[v + 1];
-        int64_t out = rowptr[i];
+        const int32_t cnt = (int32_t)(b - a);
+        rowptr[i] = a;
+        if (i == n_core - 1) rowptr[n_core] = b;
+        d_l[i] = cnt;
+        d_g[i] = (int32_t)(g_rowptr[v + 1] - g_rowptr[v]);
+        norm_gcn[i] = (float)(1.0 / sqrt((double)cnt + 1.0));
+        norm_sage[i] = cnt > 0 ? (float)(1.0 / (double)cnt) : 0.0f;
+        labels[i] = g_labels ? g_labels[v] : 0;
+    }
+}
+
+// stable ballot compaction of every task's kept neighbours, relabelled to local ids
+__global__ void k_task_fill(const int64_t* __restrict__ d_T, const int32_t* __restrict__ task_row,
+                            const int32_t* __restrict__ task_off, const int64_t* __restrict__ task_out,
+                            const int32_t* __restrict__ core_global, const int64_t* __restrict__ g_rowptr,
+                            const int32_t* __restrict__ g_col, const int32_t* __restrict__ rank,
+                            int32_t* __restrict__ col) {
+    const int lane = threadIdx.x & 31;
+    const int64_t T = *d_T;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T; t += nwarps) {
+        const int32_t i = task_row[t];
+        const int32_t v = core_global[i];
+        const int64_t e0 = g_rowptr[v] + (t - task_off[i]) * (int64_t)kTaskLen;
+        const int64_t e1 = min(g_rowptr[v + 1], e0 + kTaskLen);
+        int64_t out = task_out[t];
         for (int64_t e = e0 + lane; e - lane < e1; e += 32) {
             int32_t r = -1;
             if (e < e1) r = rank[g_col[e]];
-            unsigned m = __ballot_sync(0xffffffffu, r >= 0);
+            const unsigned m = __ballot_sync(0xffffffffu, r >= 0);
             if (r >= 0) col[out + __popc(m & ((1u << lane) - 1u))] = r;
             out += __popc(m);
         }
@@ -272,14 +325,31 @@ extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g
     RP_TRY(p->heavy_slot_off.grow((n_core + 1) * 4));
     unsigned grid;
     rp_grid(ctx, n_core, 256, &grid);
-    k_row_count<<<grid, 256, 0, s>>>(n_core, (int32_t*)p->core_global.p, g->rowptr, g->col, rank,
-                                      labels, (int32_t*)p->d_l.p, (int32_t*)p->d_g.p,
-                                      (float*)p->norm_gcn.p, (float*)p->norm_sage.p,
-                                      (int32_t*)p->labels.p);
+    // task workspace: T <= n_core + nnz_global / kTaskLen + 1 (upper bound; the exact T stays
+    // on the device and the task kernels grid-stride up to it -- no host sync needed)
+    const int64_t T_max = n_core + g->nnz / kTaskLen + 1;
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t off_b = al((size_t)(n_core + 1) * 4), row_b = al((size_t)T_max * 4),
+                 cnt_b = al((size_t)T_max * 4), out_b = al((size_t)(T_max + 1) * 8);
+    RP_TRY(ctx->rp_ws.grow(off_b + row_b + cnt_b + out_b));
+    int32_t* task_off = (int32_t*)ctx->rp_ws.p;
+    int32_t* task_row = (int32_t*)((char*)ctx->rp_ws.p + off_b);
+    int32_t* tcount = (int32_t*)((char*)ctx->rp_ws.p + off_b + row_b);
+    int64_t* task_out = (int64_t*)((char*)ctx->rp_ws.p + off_b + row_b + cnt_b);
+    const int32_t* core_global = (const int32_t*)p->core_global.p;
+    RP_TRY(device_scan(ctx, NumTasks{core_global, g->rowptr}, n_core,
+                       WriteTasks{task_off, task_row, d_stat}, s));
+    const unsigned tgrid = (unsigned)ctx->sm_count * 16;
+    k_task_count<<<tgrid, 256, 0, s>>>(d_stat + 5, task_row, task_off, core_global, g->rowptr, g->col,
+                                        rank, tcount);
     GRAPPA_LAUNCHED(ctx);
-    // 3. scans
-    RP_TRY(device_scan(ctx, ReadI32{(int32_t*)p->d_l.p}, n_core,
-                       WriteRowptr{(int64_t*)p->rowptr.p, d_stat}, s));
+    // 3. scans: task outputs (= local col offsets, total = nnz), then per-row finalize
+    RP_TRY(device_scan(ctx, ReadTcount{tcount, d_stat + 5}, T_max, WriteTaskOut{task_out, d_stat}, s));
+    k_row_finalize<<<grid, 256, 0, s>>>(n_core, task_off, task_out, core_global, g->rowptr, labels,
+                                         (int64_t*)p->rowptr.p, (int32_t*)p->d_l.p, (int32_t*)p->d_g.p,
+                                         (float*)p->norm_gcn.p, (float*)p->norm_sage.p,
+                                         (int32_t*)p->labels.p);
+    GRAPPA_LAUNCHED(ctx);
     RP_TRY(device_scan(ctx, FlagSeed{(int32_t*)p->core_global.p, train_mask}, n_core,
                        WriteCompact{(int32_t*)p->seeds.p, d_stat, 2}, s));
     RP_TRY(device_scan(ctx, FlagHeavy{(int32_t*)p->d_l.p}, n_core,
@@ -297,8 +367,8 @@ extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g
                        WriteSlotOff{(int32_t*)p->heavy_slot_off.p, d_stat}, s));
     // 4. fill
     RP_TRY(p->col.grow((size_t)(nnz > 0 ? nnz : 1) * 4));
-    k_row_fill<<<grid, 256, 0, s>>>(n_core, (int32_t*)p->core_global.p, g->rowptr, g->col, rank,
-                                     (int64_t*)p->rowptr.p, (int32_t*)p->col.p);
+    k_task_fill<<<tgrid, 256, 0, s>>>(d_stat + 5, task_row, task_off, task_out, core_global, g->rowptr,
+                                       g->col, rank, (int32_t*)p->col.p);
     GRAPPA_LAUNCHED(ctx);
     // 5. features
     const int64_t esz = dtype == GRAPPA_BF16 ? 2 : 4;

@@ -237,11 +237,15 @@ def test_epoch_parity(G, ctx, prod, arxiv, which, corr, epochs, rep):
     lr = 0.05
     tr = Trainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights, wl.chunks,
                  gen.seed_of("chunks"), corr=corr, lr=lr, repartition_every=rep)
-    ghat, thetas = [], [_logical(tr, tr.theta)]
+    ghat, thetas, masks = [], [_logical(tr, tr.theta)], []
 
     def grab():
         ghat.append(_logical(tr, tr.grad))
         thetas.append(_logical(tr, tr.theta))
+        n = tr.parts[len(masks) % wl.chunks].n_core
+        # the kernels' own ReLU decisions (fp32 pre-activation > 0), reading R16b
+        masks.append([(tr.H[l][:n, :wl.dims[l]] > 0).cpu().numpy().astype(np.float64)
+                      for l in range(1, wl.depth)])
 
     for _ in range(epochs):
         tr.run_epoch(on_phase=grab)
@@ -256,15 +260,21 @@ def test_epoch_parity(G, ctx, prod, arxiv, which, corr, epochs, rep):
     shapes = [[w.shape for w in ws] for ws in Wref]
     # step-local parity: the oracle's aggregated update at the GPU's own theta of each phase
     # (ReLU kinks make multi-step trajectories chaotic at the 1e-7 level, so every phase is
-    # checked from the same starting point)
+    # checked from the same starting point), with the ReLU decisions the kernels took
     for k in range(epochs * P):
         e, w = divmod(k, P)
         b, s = sched[(e // rep) % len(sched)][w]
         part = Po.induced_partition(ds.rowptr, ds.col, chunk_of, b, s, ds.train)
-        _, g, _, _ = Mo.partition_loss_grad(wl.arch, part, X[part["core"]], ds.y[part["core"]],
-                                            Mo.unflatten(thetas[k], shapes))
+        Wk = Mo.unflatten(thetas[k], shapes)
+        _, g, _, cache = Mo.partition_loss_grad(wl.arch, part, X[part["core"]], ds.y[part["core"]],
+                                                Wk, masks[k])
         ref = Co.aggregate([Tr.partition_factor(corr, part)], [g], 1)
         assert err(ghat[k], ref) <= 1e-4, k
+        # the decisions themselves: disagreements only where |Z| is at rounding level
+        for l, mk in enumerate(masks[k]):
+            Z = cache["Z"][l]
+            flip = (Z > 0) != (mk > 0)
+            assert np.all(np.abs(Z[flip]) <= 1e-5 * np.max(np.abs(Z))), (k, l)
         step = thetas[k] - thetas[k + 1]
         if corr != "resampling":                       # literal c_resampling ~1e-6: update < ulp
             assert err(step, lr * ghat[k]) <= 1e-3, k
@@ -272,3 +282,31 @@ def test_epoch_parity(G, ctx, prod, arxiv, which, corr, epochs, rep):
     final, recs = Tr.run(wl.arch, ds.rowptr, ds.col, X, ds.y, ds.train, Wref, chunk_of, P, P, 1,
                          corr, lr, 1, rep)
     assert err(thetas[P], Mo.flatten(final)) <= 1e-4
+
+
+@pytest.mark.parametrize("arch", ["gcn", "sage"])
+def test_tcgen05_matches_simt(G, ctx, prod, arch):
+    """The bf16 tcgen05 GEMMs and the CUDA-core GEMMs agree (same layer, same inputs)."""
+    part = _part(G, ctx, prod, 8, 3, 6, "bf16")
+    n, f_in, f_out = part.n_core, 112, 48
+    g = torch.Generator(device="cuda").manual_seed(7)
+    h_in = torch.randn(n, f_in, device="cuda", generator=g).relu().to(torch.bfloat16)
+    m = 1 if arch == "gcn" else 2
+    w = torch.randn(m * f_in, f_out, device="cuda", generator=g) / 10
+    dz = (torch.randn(n, f_out, device="cuda", generator=g) * 1e-2).to(torch.bfloat16)
+    outs = []
+    lib = G.load()
+    for simt in (0, 1):
+        lib.grappa_debug_gemm_simt(simt)
+        h_out = torch.empty(n, f_out, device="cuda", dtype=torch.bfloat16)
+        saved = torch.empty(max(1, G.layer_saved_bytes(part, arch, f_in, f_out, "bf16")), dtype=torch.uint8, device="cuda")
+        ws = torch.empty(G.layer_ws_bytes(part, arch, f_in, f_out, "bf16"), dtype=torch.uint8, device="cuda")
+        G.grappa_layer_fwd(ctx, part, arch, f_in, f_out, True, h_in, w, h_out, saved, ws, "bf16")
+        dw = torch.empty_like(w)
+        dz_in = torch.empty(n, f_in, device="cuda", dtype=torch.bfloat16)
+        G.grappa_layer_bwd(ctx, part, arch, f_in, f_out, True, dz, h_in, w, saved, dw, dz_in, ws, "bf16")
+        torch.cuda.synchronize()
+        outs.append((_np(h_out), _np(dw), _np(dz_in)))
+    lib.grappa_debug_gemm_simt(0)
+    for a, b in zip(*outs):
+        assert err(a, b) <= 1e-2

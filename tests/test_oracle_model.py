@@ -168,6 +168,21 @@ def test_backward_finite_differences(arch, depth):
     assert err <= 1e-5, err
 
 
+@pytest.mark.parametrize("arch", ["gcn", "sage"])
+def test_given_masks_equal_own_decisions(arch):
+    """R16b: passing the oracle's own ReLU decisions reproduces the default path exactly,
+    and a flipped decision changes the gradient only through that unit."""
+    rp, col, X, y, seeds, Ws = _fd_case(arch, 3, 9)
+    logits, cache = Mo.forward(arch, rp, col, X, Ws)
+    own = [(Z > 0).astype(np.float64) for Z in cache["Z"][:-1]]
+    l2, c2 = Mo.forward(arch, rp, col, X, Ws, own)
+    assert np.array_equal(logits, l2)
+    _, dZ = Mo.loss_and_dlogits(logits, y, seeds)
+    g1 = Mo.flatten(Mo.backward(arch, cache, dZ, Ws))
+    g2 = Mo.flatten(Mo.backward(arch, c2, dZ, Ws))
+    assert np.array_equal(g1, g2)
+
+
 def test_empty_seed_and_bad_label():
     with pytest.raises(ValueError):
         Mo.loss_and_dlogits(np.zeros((3, 2)), np.zeros(3, int), [])
