@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--config", default="products")
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--variant", action="append", default=[],
+                    help="kernel A/B knob op=value (grappa_set_kernel_variant), e.g. spmm=2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--out", default=None)
     return ap.parse_args()
@@ -126,78 +128,101 @@ def build_dataset(name: str):
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def oracle_sample_epoch(name: str, max_seconds: float = 30.0, phases=None):
-    """Time the CPU oracle (as it stands, f64 NumPy/SciPy, 1 BLAS thread) on a bounded sample
-    of the workload: the same generator at 1/8 scale, Alg. 1 phases of its P partitions.
-    Returns (edges/s extrapolated to one epoch of the sample, sample description, cores)."""
-    import gen
-    from oracle import partition as Po
-    from oracle import train as Tr
-    try:
-        from threadpoolctl import threadpool_limits
-        limiter = threadpool_limits(1)
-    except Exception:  # pragma: no cover
-        limiter = None
-    wl0 = gen.WORKLOADS[name]
-    n = max(wl0.n // 8, 1000)
-    scale = max(int(np.ceil(np.log2(n))), 4)
-    wl = gen.small_workload(name, n=n, scale=scale, num_samples=max(wl0.num_samples // 8, 1000))
-    ds = gen.make_dataset(wl)
-    X = ds.x[:, :wl.F].astype(np.float64)
-    W0 = [[np.asarray(w, np.float64)[:wl.dims[l], :wl.dims[l + 1]] for w in ws]
-          for l, ws in enumerate(ds.weights)]
-    chunk_of = Po.make_chunks(wl.n, wl.chunks, gen.seed_of("chunks"))
-    P = wl.chunks
-    t0 = time.perf_counter()
-    done = 0
-    budget = phases if phases is not None else P
-    # one phase per call (M = 1): the oracle's Alg. 1 with a fresh repartition each call
-    for i in range(budget):
-        pairs = Po.sweep_schedule(P, P)[0]
-        b, s = pairs[i % P]
-        part = Po.induced_partition(ds.rowptr, ds.col, chunk_of, b, s, ds.train)
-        from oracle import model as Mo
+class OracleSample:
+    """The CPU oracle, as it stands (f64 NumPy/SciPy, BLAS limited to 1 thread), on a bounded
+    sample of the workload: the same generator at 1/`shrink` scale with the same model,
+    P and correction.  One `phase(i)` = the oracle's repartition of partition i + its
+    forward/loss/backward + coverage-corrected aggregation + SGD (Alg. 1 with M = 1)."""
+
+    def __init__(self, name: str, shrink: int = 8):
+        import gen
+        from oracle import partition as Po
+        wl0 = gen.WORKLOADS[name]
+        n = max(wl0.n // shrink, 1000)
+        scale = max(int(np.ceil(np.log2(n))), 4)
+        self.wl = gen.small_workload(name, n=n, scale=scale,
+                                     num_samples=max(wl0.num_samples // shrink, 1000))
+        self.ds = gen.make_dataset(self.wl)
+        self.X = self.ds.x[:, :self.wl.F].astype(np.float64)
+        self.W = [[np.asarray(w, np.float64)[:self.wl.dims[l], :self.wl.dims[l + 1]] for w in ws]
+                  for l, ws in enumerate(self.ds.weights)]
+        self.chunk_of = Po.make_chunks(n, self.wl.chunks, gen.seed_of("chunks"))
+        self.pairs = Po.sweep_schedule(self.wl.chunks, self.wl.chunks)[0]
+        self.shrink = shrink
+
+    def phase(self, i: int) -> float:
         from oracle import correction as Co
-        Xp = X[part["core"]]
-        loss, g, _, _ = Mo.partition_loss_grad(wl.arch, part, Xp, ds.y[part["core"]], W0)
+        from oracle import model as Mo
+        from oracle import partition as Po
+        from oracle import train as Tr
+        try:
+            from threadpoolctl import threadpool_limits
+            lim = threadpool_limits(1)
+        except Exception:  # pragma: no cover
+            lim = None
+        wl, ds = self.wl, self.ds
+        t0 = time.perf_counter()
+        b, s = self.pairs[i % wl.chunks]
+        part = Po.induced_partition(ds.rowptr, ds.col, self.chunk_of, b, s, ds.train)
+        _, g, _, _ = Mo.partition_loss_grad(wl.arch, part, self.X[part["core"]],
+                                            ds.y[part["core"]], self.W)
         c = Tr.partition_factor(wl.correction, part)
-        Co.sgd(Mo.flatten(W0), Co.aggregate([c], [g], 1), 0.003)
-        done += 1
-        if phases is None and time.perf_counter() - t0 > max_seconds:
-            break
-    dt = time.perf_counter() - t0
-    if limiter is not None:
-        limiter.unregister() if hasattr(limiter, "unregister") else None
-    epoch_s = dt / done * P
-    desc = (f"oracle (f64 NumPy/SciPy, 1 thread) on the {name} generator at 1/8 scale "
-            f"(n={wl.n}, nnz={ds.nnz}); {done} of {P} partition-phases timed incl. repartition, "
-            f"epoch extrapolated x{P}/{done}")
-    return ds.nnz / epoch_s, desc, 1, epoch_s
+        Co.sgd(Mo.flatten(self.W), Co.aggregate([c], [g], 1), 0.003)
+        dt = time.perf_counter() - t0
+        if lim is not None and hasattr(lim, "unregister"):
+            lim.unregister()
+        return dt
+
+    def describe(self, phases: int) -> str:
+        return (f"CPU oracle (f64 NumPy/SciPy, 1 thread) on the {self.wl.name.replace('-small', '')} "
+                f"generator at 1/{self.shrink} scale (n={self.wl.n}, nnz={self.ds.nnz}, "
+                f"{self.wl.arch.upper()}-{self.wl.depth}, P={self.wl.chunks}); {phases} partition-phase(s) "
+                f"timed (repartition + fwd/bwd + aggregate + SGD), epoch = x{self.wl.chunks} phases")
+
+
+def oracle_baseline(name: str, budget_s: float = 30.0):
+    """cpu_baseline leg: phases of one epoch of the sample until ~budget_s of CPU work."""
+    o = OracleSample(name)
+    ts = []
+    while len(ts) < o.wl.chunks and sum(ts) < budget_s:
+        ts.append(o.phase(len(ts)))
+    epoch_s = statistics.mean(ts) * o.wl.chunks
+    return {"value": o.ds.nnz / epoch_s, "unit": "edges/s", "cores": 1, "kind": "oracle",
+            "sample": o.describe(len(ts)), "epoch_s": epoch_s}
 
 
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: the oracle as the reference arm (no reference code exists; the
+    paper ships none).  Rank 0 only; each step = one partition-phase of the 1/8 sample."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
+    o = OracleSample(args.config)
     K, W = args.steps, args.warmup
-    for _ in range(W):
-        oracle_sample_epoch(args.config, phases=1)
-    vals = []
-    for _ in range(K):
-        v, desc, cores, ep = oracle_sample_epoch(args.config, phases=1)
-        vals.append(ep)
-    ep = statistics.mean(vals)
-    _, desc, cores, _ = v, desc, cores, ep
-    value = v
+    for i in range(W):
+        o.phase(i)
+    ts = [o.phase(W + i) for i in range(K)]
+    epoch_s = statistics.mean(ts) * o.wl.chunks
+    value = o.ds.nnz / epoch_s
+    desc = o.describe(K)
     line = {"impl": "reference", "metric": "edges_per_sec", "value": value, "unit": "edges/s",
-            "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": ep * 1e3,
+            "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": statistics.mean(ts) * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": f"{args.config} (1/8-scale sample)"},
-            "cpu_baseline": {"value": value, "unit": "edges/s", "cores": cores, "kind": "oracle",
+            "data": "synthetic",
+            "config": {"workload": workload_desc(args.config, args.gpus), "sample": desc},
+            "cpu_baseline": {"value": value, "unit": "edges/s", "cores": 1, "kind": "oracle",
                              "sample": desc},
-            "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def workload_desc(name: str, world: int) -> str:
+    import gen
+    wl = gen.WORKLOADS[name]
+    return (f"{name}-shaped RMAT ({wl.n} nodes), {wl.arch.upper()}-{wl.depth}, P={wl.chunks} "
+            f"partitions, M={world} per phase, full-graph, {wl.correction} correction, "
+            f"repartition every {wl.repartition_every} epochs")
 
 
 # ----------------------------------------------------------------------------- grappa arm
@@ -222,6 +247,9 @@ def run_grappa(args):
         ctx = G.Context(local, rank, world, bytes(t.cpu().tolist()))
     else:
         ctx = G.Context(local)
+    for kv in args.variant:
+        op, val = kv.split("=")
+        G._lib.check("grappa_set_kernel_variant", G.load().grappa_set_kernel_variant(op.encode(), int(val)))
 
     t_gen = time.perf_counter()
     wl, ds = build_dataset(args.config)
@@ -289,17 +317,14 @@ def run_grappa(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, desc, cores, _ = oracle_sample_epoch(args.config)
-        cpu = {"value": v, "unit": "edges/s", "cores": cores, "kind": "oracle", "sample": desc}
+        cpu = oracle_baseline(args.config)
 
     if rank == 0:
         line = {"metric": "edges_per_sec", "value": value, "unit": "edges/s", "n_gpus": world,
                 "steps": K, "warmup": args.warmup, "ms_per_step": ms / K,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32" if args.dtype == "f32" else "bf16", "data": "synthetic",
-                "config": {"workload": f"{args.config}-shaped RMAT ({wl.n} nodes, {nnz} directed edges), "
-                                       f"{wl.arch.upper()}-{wl.depth}, P={wl.chunks} partitions, M={world} per phase, "
-                                       f"full-graph, {wl.correction} correction, repartition every {wl.repartition_every} epochs",
+                "config": {"workload": workload_desc(args.config, world),
                            "nnz_global": nnz, "partitions": wl.chunks, "phases_per_epoch": -(-wl.chunks // world),
                            "repartitions_timed": -(-K // wl.repartition_every),
                            "repartition_ms_total": rep_ms,

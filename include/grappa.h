@@ -221,9 +221,11 @@ typedef enum {
     GRAPPA_K_REPART = 5,
     GRAPPA_K_NCLASS = 6
 } grappa_kclass;
-/* Test hook: on != 0 routes bf16 GEMMs to the CUDA-core kernels instead of tcgen05 (process
- * wide), so tests can cross-check the two implementations. */
-void grappa_debug_gemm_simt(int on);
+/* Test / A-B hook (process wide): select an alternative kernel implementation so tests can
+ * cross-check them.  op "gemm": 0 = auto (tcgen05 for bf16), 1 = CUDA-core kernels.
+ * op "spmm": 0 = auto (row-group kernel for rows of <= 32 vectors), 1 = warp-per-row.
+ * Returns E_ARG for an unknown op. */
+grappa_status grappa_set_kernel_variant(const char* op, int variant);
 
 grappa_status grappa_profile_enable(grappa_ctx* ctx, int on);
 grappa_status grappa_profile_read(grappa_ctx* ctx, int kclass, double* ms, int64_t* calls,

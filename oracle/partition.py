@@ -23,10 +23,11 @@ _M2 = np.uint64(0x94D049BB133111EB)
 
 def mix(x):
     """splitmix64 finalizer on uint64 arrays (wrapping arithmetic)."""
-    z = np.asarray(x, dtype=np.uint64) + _GAMMA
-    z = (z ^ (z >> np.uint64(30))) * _M1
-    z = (z ^ (z >> np.uint64(27))) * _M2
-    return z ^ (z >> np.uint64(31))
+    with np.errstate(over="ignore"):
+        z = np.asarray(x, dtype=np.uint64) + _GAMMA
+        z = (z ^ (z >> np.uint64(30))) * _M1
+        z = (z ^ (z >> np.uint64(27))) * _M2
+        return z ^ (z >> np.uint64(31))
 
 
 def h3(a, b, c):

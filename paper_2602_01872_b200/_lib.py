@@ -24,7 +24,7 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_part_destroy", "grappa_layer_saved_bytes", "grappa_layer_ws_bytes",
            "grappa_layer_fwd", "grappa_layer_bwd", "grappa_loss", "grappa_aggregate_grads",
            "grappa_check", "grappa_launch_count", "grappa_profile_enable", "grappa_profile_read",
-           "grappa_debug_gemm_simt"]
+           "grappa_set_kernel_variant"]
 KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5}
 
 
@@ -89,7 +89,7 @@ def load(path: str = LIB_PATH):
         "grappa_check": (st, [vp, vp]),
         "grappa_launch_count": (i64, [vp]),
         "grappa_profile_enable": (st, [vp, ctypes.c_int]),
-        "grappa_debug_gemm_simt": (None, [ctypes.c_int]),
+        "grappa_set_kernel_variant": (st, [ctypes.c_char_p, ctypes.c_int]),
         "grappa_profile_read": (st, [vp, ctypes.c_int, ctypes.POINTER(dbl), ctypes.POINTER(i64),
                                      ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
     }

@@ -26,7 +26,9 @@ grappa_status DevBuf::grow(size_t bytes) {
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
-    size_t b = bytes < 256 ? 256 : bytes;
+    // 1/8 headroom: partition sizes fluctuate by a few % across super-epochs, and a realloc
+    // (cudaFree synchronises the device) inside a switch is what we want to avoid
+    size_t b = bytes < 256 ? 256 : bytes + bytes / 8;
     cudaError_t e = cudaMalloc(&p, b);
     if (e != cudaSuccess) {
         p = nullptr;
@@ -143,7 +145,15 @@ extern "C" void grappa_ctx_destroy(grappa_ctx* c) {
 
 extern "C" int64_t grappa_launch_count(const grappa_ctx* c) { return c ? c->launches : 0; }
 
-extern "C" void grappa_debug_gemm_simt(int on) { gemm_force_simt(on); }
+namespace grappa { void spmm_force_warp_per_row(int on); }
+
+extern "C" grappa_status grappa_set_kernel_variant(const char* op, int variant) {
+    GRAPPA_ARG(op, GRAPPA_E_ARG, "grappa_set_kernel_variant: null op");
+    if (!strcmp(op, "gemm")) { gemm_force_simt(variant); return GRAPPA_OK; }
+    if (!strcmp(op, "spmm")) { spmm_force_warp_per_row(variant); return GRAPPA_OK; }
+    set_error("grappa_set_kernel_variant: unknown op '%s'", op);
+    return GRAPPA_E_ARG;
+}
 
 extern "C" grappa_status grappa_profile_enable(grappa_ctx* c, int on) {
     GRAPPA_ARG(c, GRAPPA_E_ARG, "grappa_profile_enable: null ctx");

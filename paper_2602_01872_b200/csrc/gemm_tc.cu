@@ -6,13 +6,15 @@
 // B200 design.  The transform is tall-skinny (M = 10^5..10^8 node rows, K, N <= 256) and
 // HBM-bound (~64 FLOP/B), so the kernels are built to stream rows at full bandwidth:
 //  * persistent CTAs (one per SM), warp-specialised: warp 0 = TMA producer, warp 1 = single-
-//    thread tcgen05.mma issuer (+ TMEM owner), warps 2-5 = epilogue (TMEM -> regs -> HBM);
+//    thread tcgen05.mma issuer (+ TMEM owner), warps 2-5 = epilogue (TMEM -> regs -> smem);
 //  * A tiles (128 rows x 64 bf16 = one 128-byte SWIZZLE_128B atom row per node) arrive by
-//    TMA into a 6-stage mbarrier ring; OOB rows / columns are zero-filled by TMA;
+//    TMA into a 4-stage mbarrier ring; OOB rows / columns are zero-filled by TMA;
 //  * the weights (the whole K x N operand, <= 64 KB bf16) are converted fp32 -> bf16 once per
 //    CTA into the K-major SW128 canonical layout and stay resident in shared memory;
 //  * accumulators double-buffered in TMEM (2 x N columns) so the epilogue of tile i overlaps
-//    the MMAs of tile i+1; fused epilogue: ReLU or relu'-mask, column split, bf16 cast.
+//    the MMAs of tile i+1.  Fused epilogue: relu'-mask (mask tile TMA-loaded into smem by the
+//    producer) or ReLU, bf16 cast, column split; the result tile is staged in SW128 smem and
+//    written by TMA bulk-tensor stores (coalesced, asynchronous, clipped at the tensor edge).
 //  * The weight gradient reads both operands MN-major straight from the row-major node
 //    tensors (A = h_in^T, B = dZ^T as UMMA operands), accumulates a CTA's row slab in TMEM
 //    and writes an fp32 partial; partials are summed in slab order (deterministic split-K).
@@ -24,8 +26,9 @@
 namespace grappa {
 
 constexpr int kTcThreads = 192;
-constexpr int kNNStages = 6;
+constexpr int kNNStages = 4;
 constexpr int kNNStageBytes = 128 * 128;    // 128 rows x 128 B
+constexpr int kBoxBytes = 128 * 128;        // one 64-column x 128-row bf16 SW128 box
 constexpr int kTNStages = 4;
 constexpr int kMaxSmem = 227 * 1024;
 // weight-gradient split plan: a fixed CTA budget (= B200 SM count) so workspace sizing and
@@ -38,26 +41,43 @@ struct TcNN {
     const float* B;
     int b_trans;
     int relu;
-    const __nv_bfloat16* mask;
+    int has_mask;
     int n_split;
-    __nv_bfloat16* C1;
-    __nv_bfloat16* C2;
+    int nb1, nb2;          // 64-column output boxes of C1 / C2
     int num_tiles;
     uint32_t tmem_cols;
 };
 
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int x, int y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                 ::"l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(tc::smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
 __global__ void __launch_bounds__(kTcThreads, 1)
-    k_gemm_tc_nn(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2, TcNN p) {
+    k_gemm_tc_nn(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
+                 const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmC2,
+                 const __grid_constant__ CUtensorMap tmMask, TcNN p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const int kbt = p.kb1 + p.kb2;
+    const int nbo = p.nb1 + p.nb2;
     uint8_t* sA = smem;
     uint8_t* sB = sA + kNNStages * kNNStageBytes;
-    uint64_t* full = (uint64_t*)(sB + (size_t)kbt * p.N * 128);
+    uint8_t* sOut = sB + (size_t)kbt * p.N * 128;                  // nbo boxes
+    uint8_t* sMask = sOut + (size_t)nbo * kBoxBytes;               // nb1 boxes if has_mask
+    uint64_t* full = (uint64_t*)(sMask + (p.has_mask ? (size_t)p.nb1 * kBoxBytes : 0));
     uint64_t* empty = full + kNNStages;
     uint64_t* tfull = empty + kNNStages;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    uint64_t* mfull = tempty + 2;
+    uint64_t* mempty = mfull + 1;
+    uint32_t* tmem_slot = (uint32_t*)(mempty + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     // weights -> shared memory once: bf16, K-major, SWIZZLE_128B, zero padded
@@ -82,6 +102,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < kNNStages; s++) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
         for (int a = 0; a < 2; a++) { tc::mbar_init(&tfull[a], 1); tc::mbar_init(&tempty[a], 4); }
+        tc::mbar_init(mfull, 1);
+        tc::mbar_init(mempty, 4);
         tc::mbar_fence_init();
         tc::tma_prefetch(&tmA1);
         if (p.kb2) tc::tma_prefetch(&tmA2);
@@ -96,8 +118,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (warp == 0) {
         if (lane == 0) {
             int stage = 0;
-            uint32_t phase = 0;
+            uint32_t phase = 0, mphase = 0;
             for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+                if (p.has_mask) {           // relu'-mask tile for the epilogue, one buffer
+                    tc::mbar_wait(mempty, mphase ^ 1);
+                    tc::mbar_arrive_expect_tx(mfull, p.nb1 * kBoxBytes);
+                    for (int b = 0; b < p.nb1; b++)
+                        tc::tma_load_2d(sMask + b * kBoxBytes, &tmMask, mfull, b * 64, tile * 128);
+                    mphase ^= 1;
+                }
                 for (int kb = 0; kb < kbt; kb++) {
                     tc::mbar_wait(&empty[stage], phase ^ 1);
                     tc::mbar_arrive_expect_tx(&full[stage], kNNStageBytes);
@@ -138,49 +167,63 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
     } else {
         const int ew = warp & 3;           // TMEM lane quarter this warp may access
-        const int n2 = p.N - p.n_split;
+        const int r = ew * 32 + lane;      // row within the tile
+        const bool leader = (warp == 2 && lane == 0);
         int acc = 0;
-        uint32_t aphase = 0;
+        uint32_t aphase = 0, mphase = 0;
         for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
             tc::mbar_wait(&tfull[acc], aphase);
             tc::fence_after();
-            const int64_t row = (int64_t)tile * 128 + ew * 32 + lane;
+            if (p.has_mask) tc::mbar_wait(mfull, mphase);
+            if (leader) bulk_wait_read();      // previous tile's TMA store has read sOut
+            epi_bar();
             const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * p.N);
             for (int c0 = 0; c0 < p.N; c0 += 16) {
                 float v[16];
                 tc::tmem_ld16(tbase + c0, v);
-                if (row < p.M) {
-                    __nv_bfloat16* dst;
-                    if (c0 < p.n_split) {
-                        if (p.mask) {
-                            __align__(16) __nv_bfloat16 mk[16];
-                            const uint4* ms = reinterpret_cast<const uint4*>(p.mask + row * p.n_split + c0);
-                            *reinterpret_cast<uint4*>(mk) = __ldg(ms);
-                            *reinterpret_cast<uint4*>(mk + 8) = __ldg(ms + 1);
+                const bool first = c0 < p.n_split;
+                const int cc = first ? c0 : c0 - p.n_split;
+                const int box = (first ? 0 : p.nb1) + (cc >> 6);
+                const int ch = (cc & 63) >> 3;     // 16-byte chunk within the 128-byte row
+                if (first && p.has_mask) {
+                    const uint8_t* mrow = sMask + (cc >> 6) * kBoxBytes;
+                    __align__(16) __nv_bfloat16 mk[16];
+                    *reinterpret_cast<uint4*>(mk) = *reinterpret_cast<const uint4*>(mrow + tc::sw128_off(r, ch));
+                    *reinterpret_cast<uint4*>(mk + 8) =
+                        *reinterpret_cast<const uint4*>(mrow + tc::sw128_off(r, ch + 1));
 #pragma unroll
-                            for (int i = 0; i < 16; i++) v[i] = __bfloat162float(mk[i]) > 0.f ? v[i] : 0.f;
-                        }
-                        if (p.relu) {
-#pragma unroll
-                            for (int i = 0; i < 16; i++) v[i] = fmaxf(v[i], 0.f);
-                        }
-                        dst = p.C1 + row * p.n_split + c0;
-                    } else {
-                        dst = p.C2 + row * n2 + (c0 - p.n_split);
-                    }
-                    __align__(16) __nv_bfloat16 o[16];
-#pragma unroll
-                    for (int i = 0; i < 16; i++) o[i] = __float2bfloat16_rn(v[i]);
-                    reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<const uint4*>(o)[0];
-                    reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<const uint4*>(o)[1];
+                    for (int i = 0; i < 16; i++) v[i] = __bfloat162float(mk[i]) > 0.f ? v[i] : 0.f;
                 }
+                if (first && p.relu) {
+#pragma unroll
+                    for (int i = 0; i < 16; i++) v[i] = fmaxf(v[i], 0.f);
+                }
+                __align__(16) __nv_bfloat16 o[16];
+#pragma unroll
+                for (int i = 0; i < 16; i++) o[i] = __float2bfloat16_rn(v[i]);
+                uint8_t* orow = sOut + box * kBoxBytes;
+                *reinterpret_cast<uint4*>(orow + tc::sw128_off(r, ch)) = reinterpret_cast<const uint4*>(o)[0];
+                *reinterpret_cast<uint4*>(orow + tc::sw128_off(r, ch + 1)) = reinterpret_cast<const uint4*>(o)[1];
             }
             tc::fence_before();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                tc::mbar_arrive(&tempty[acc]);
+                if (p.has_mask) tc::mbar_arrive(mempty);
+            }
+            tc::fence_proxy_async();             // staged tile -> visible to the TMA engine
+            epi_bar();
+            if (leader) {
+                for (int b = 0; b < p.nb1; b++) tma_store_2d(&tmC1, sOut + b * kBoxBytes, b * 64, tile * 128);
+                for (int b = 0; b < p.nb2; b++)
+                    tma_store_2d(&tmC2, sOut + (p.nb1 + b) * kBoxBytes, b * 64, tile * 128);
+                bulk_commit();
+            }
             acc ^= 1;
             if (acc == 0) aphase ^= 1;
+            mphase ^= 1;
         }
+        if (leader) bulk_wait_read();
     }
     __syncthreads();
     if (warp == 1) {
@@ -295,18 +338,29 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
 }
 
-// dW[r][n] = sum_slab ws[slab][ft(r)][row(r)][n], slab order fixed
-__global__ void k_tn_reduce(int64_t count, int N, int K1, int K2, int ft1, int ftiles, int slabs,
-                            const float* __restrict__ ws, float* __restrict__ dw) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
-         i += (int64_t)gridDim.x * blockDim.x) {
+// dW[r][n] = sum_slab ws[slab][ft(r)][row(r)][n].  Block = 32 outputs x 8 slab groups: thread
+// (o, g) sums slabs g, g+8, ... in order, then the 8 group sums are added in group order --
+// a fixed summation tree, so the result is bitwise deterministic.
+__global__ void __launch_bounds__(256) k_tn_reduce(int64_t count, int N, int K1, int K2, int ft1, int ftiles,
+                                                   int slabs, const float* __restrict__ ws,
+                                                   float* __restrict__ dw) {
+    __shared__ float part[8][33];
+    const int o = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const int64_t i = (int64_t)blockIdx.x * 32 + o;
+    float s = 0.f;
+    if (i < count) {
         const int r = (int)(i / N), n = (int)(i % N);
         int ft, row;
         if (r < K1) { ft = r / 128; row = r % 128; }
         else { ft = ft1 + (r - K1) / 128; row = (r - K1) % 128; }
-        float s = 0.f;
-        for (int z = 0; z < slabs; z++) s += ws[(((int64_t)z * ftiles + ft) * 128 + row) * N + n];
-        dw[i] = s;
+        for (int z = g; z < slabs; z += 8) s += ws[(((int64_t)z * ftiles + ft) * 128 + row) * N + n];
+    }
+    part[g][o] = s;
+    __syncthreads();
+    if (g == 0 && i < count) {
+        float t = 0.f;
+        for (int k = 0; k < 8; k++) t += part[k][o];
+        dw[i] = t;
     }
 }
 
@@ -343,14 +397,16 @@ static grappa_status make_map(CUtensorMap* m, const void* ptr, int64_t rows, int
     return GRAPPA_OK;
 }
 
-static size_t nn_smem(int kbt, int N) {
-    return 1024 + (size_t)kNNStages * kNNStageBytes + (size_t)kbt * N * 128 + 256;
+static size_t nn_smem(int kbt, int N, int nb1, int nb2, bool mask) {
+    return 1024 + (size_t)kNNStages * kNNStageBytes + (size_t)kbt * N * 128 +
+           (size_t)(nb1 + nb2 + (mask ? nb1 : 0)) * kBoxBytes + 256;
 }
 
 bool gemm_tc_nn_supported(const GemmArgs& g) {
     const int kbt = (int)(ceil_div(g.K1, 64) + ceil_div(g.K2, 64));
-    return g.N % 16 == 0 && g.N <= 256 && g.K1 % 8 == 0 && g.K2 % 8 == 0 &&
-           nn_smem(kbt, g.N) <= (size_t)kMaxSmem && g.M < (1ll << 31);
+    const int nb1 = (int)ceil_div(g.n_split, 64), nb2 = (int)ceil_div(g.N - g.n_split, 64);
+    return g.N % 16 == 0 && g.N <= 256 && g.n_split % 16 == 0 && g.K1 % 8 == 0 && g.K2 % 8 == 0 &&
+           nn_smem(kbt, g.N, nb1, nb2, g.mask != nullptr) <= (size_t)kMaxSmem && g.M < (1ll << 31);
 }
 
 static uint32_t pow2_cols(int c) {
@@ -360,26 +416,31 @@ static uint32_t pow2_cols(int c) {
 }
 
 grappa_status gemm_tc_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s) {
-    CUtensorMap m1, m2;
+    CUtensorMap m1, m2, c1, c2, mk;
     GRAPPA_TRY(make_map(&m1, g.A1, g.M, g.K1, 128));
     if (g.K2 > 0) GRAPPA_TRY(make_map(&m2, g.A2, g.M, g.K2, 128));
     else m2 = m1;
+    GRAPPA_TRY(make_map(&c1, g.C1, g.M, g.n_split, 128));
+    if (g.N > g.n_split) GRAPPA_TRY(make_map(&c2, g.C2, g.M, g.N - g.n_split, 128));
+    else c2 = c1;
+    if (g.mask) GRAPPA_TRY(make_map(&mk, g.mask, g.M, g.n_split, 128));
+    else mk = c1;
     TcNN p;
     p.M = g.M; p.K1 = g.K1; p.K2 = g.K2; p.N = g.N;
     p.kb1 = (int)ceil_div(g.K1, 64); p.kb2 = (int)ceil_div(g.K2, 64);
     p.B = g.B; p.b_trans = g.b_trans; p.relu = g.relu;
-    p.mask = (const __nv_bfloat16*)g.mask; p.n_split = g.n_split;
-    p.C1 = (__nv_bfloat16*)g.C1; p.C2 = (__nv_bfloat16*)g.C2;
+    p.has_mask = g.mask != nullptr; p.n_split = g.n_split;
+    p.nb1 = (int)ceil_div(g.n_split, 64); p.nb2 = (int)ceil_div(g.N - g.n_split, 64);
     p.num_tiles = (int)ceil_div(g.M, 128);
     p.tmem_cols = pow2_cols(2 * g.N);
-    const size_t smem = nn_smem(p.kb1 + p.kb2, g.N);
+    const size_t smem = nn_smem(p.kb1 + p.kb2, g.N, p.nb1, p.nb2, p.has_mask);
     static bool attr = false;
     if (!attr) {
         GRAPPA_CUDA(cudaFuncSetAttribute(k_gemm_tc_nn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
         attr = true;
     }
     const int grid = (int)std::min<int64_t>(p.num_tiles, ctx->sm_count);
-    k_gemm_tc_nn<<<grid, kTcThreads, smem, s>>>(m1, m2, p);
+    k_gemm_tc_nn<<<grid, kTcThreads, smem, s>>>(m1, m2, c1, c2, mk, p);
     GRAPPA_LAUNCHED(ctx);
     return GRAPPA_OK;
 }
@@ -432,7 +493,7 @@ grappa_status gemm_tc_tn(grappa_ctx* ctx, const GemmTNArgs& g, cudaStream_t s) {
     k_gemm_tc_tn<<<grid, kTcThreads, smem, s>>>(m1, m2, mb, p);
     GRAPPA_LAUNCHED(ctx);
     const int64_t count = (int64_t)(g.K1 + g.K2) * g.N;
-    k_tn_reduce<<<(unsigned)std::min<int64_t>(ceil_div(count, 256), 1024), 256, 0, s>>>(
+    k_tn_reduce<<<(unsigned)ceil_div(count, 32), 256, 0, s>>>(
         count, g.N, g.K1, g.K2, p.ft1, ftiles, p.slabs, g.ws, g.C);
     GRAPPA_LAUNCHED(ctx);
     return GRAPPA_OK;

@@ -57,11 +57,19 @@ __global__ void __launch_bounds__(kLossThreads) k_loss(int64_t n_seeds, const in
     }
 }
 
-__global__ void k_loss_final(int nb, const double* part, double inv_n, double* out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double s = 0.0;
-        for (int b = 0; b < nb; b++) s += part[b];
-        *out = s * inv_n;
+// one block: thread t sums a contiguous run of partials, then a fixed-shape tree (deterministic)
+__global__ void __launch_bounds__(256) k_loss_final(int nb, const double* part, double inv_n, double* out) {
+    __shared__ double ws[8];
+    const int per = (nb + 255) / 256;
+    double s = 0.0;
+    for (int b = threadIdx.x * per, e = min(nb, b + per); b < e; b++) s += part[b];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; w++) t += ws[w];
+        *out = t * inv_n;
     }
 }
 
@@ -94,7 +102,7 @@ extern "C" grappa_status grappa_loss(grappa_ctx* ctx, const grappa_part* part, c
                                                             (const float*)logits, num_classes,
                                                             k_pad, (float*)dlogits, part_sums);
     GRAPPA_LAUNCHED(ctx);
-    k_loss_final<<<1, 32, 0, s>>>((int)nb, part_sums, 1.0 / (double)I.n_seeds, loss_dev);
+    k_loss_final<<<1, 256, 0, s>>>((int)nb, part_sums, 1.0 / (double)I.n_seeds, loss_dev);
     GRAPPA_LAUNCHED(ctx);
     return GRAPPA_OK;
 }

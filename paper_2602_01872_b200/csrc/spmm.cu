@@ -61,6 +61,11 @@ template <> struct Vec<__nv_bfloat16> {
 };
 
 constexpr int kUnroll = 4;
+// dispatch knob (tests / A-B timing) for narrow rows: 0 = row-group kernel with 4 feature
+// loads in flight per lane (default; measured best), 1 = warp-per-row kernel, 2 = row-group
+// kernel with 8 loads in flight (more registers, fewer resident warps: slower on B200)
+static int g_spmm_variant = 0;
+void spmm_force_warp_per_row(int v) { g_spmm_variant = v; }
 
 // Gather-sum of edges [e0, e1) of one row into acc (lanes of slot `slot`, sub-lane `sub`).
 template <typename T, int CPL>
@@ -249,6 +254,157 @@ __global__ void __launch_bounds__(256) k_spmm_fixup(SpmmArgs a, int G) {
     epilogue<T, CPL>(a, r, lane, G, WV, acc);
 }
 
+// Narrow rows (W/EPV <= 32 vectors): every group of G = W/EPV lanes owns a different row, so a
+// warp carries P = 32/G independent rows and their dependent load chains (rowptr -> col ->
+// scale / feature row) overlap; no cross-group reduction is needed.  Each lane prefetches
+// R column indices (chunk = G*R edges) and U feature vectors are in flight per lane.
+template <typename T, int R, int U>
+__global__ void __launch_bounds__(256) k_spmm_grp(SpmmArgs a, int G, int P) {
+    constexpr int E = Vec<T>::EPV;
+    const T* X = reinterpret_cast<const T*>(a.X);
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int slot = lane / G, sub = lane - slot * G;
+    const int WV = G;
+    const int64_t vrow = warp * P + slot;
+    int64_t e0 = 0, e1 = 0, orow = -1;
+    bool to_partial = false;
+    if (slot < P) {
+        if (vrow < a.n_slots) {
+            const int32_t r = a.slot_row[vrow], sg = a.slot_seg[vrow];
+            e0 = a.rowptr[r] + (int64_t)sg * kSegLen;
+            e1 = min(a.rowptr[r + 1], e0 + kSegLen);
+            orow = vrow;
+            to_partial = true;
+        } else if (vrow - a.n_slots < a.n) {
+            const int64_t v = vrow - a.n_slots;
+            e0 = a.rowptr[v];
+            e1 = a.rowptr[v + 1];
+            if (e1 - e0 > kSegLen) e1 = e0;          // split row: finished by the fix-up kernel
+            else orow = v;
+        }
+    }
+    const int deg = (int)(e1 - e0);
+    const int maxdeg = __reduce_max_sync(0xffffffffu, deg);
+    float acc[E];
+#pragma unroll
+    for (int q = 0; q < E; q++) acc[q] = 0.f;
+    const int CH = G * R;
+    for (int off = 0; off < maxdeg; off += CH) {
+        int idx[R];
+        float wt[R];
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int p = off + r * G + sub;
+            const bool ok = p < deg;
+            idx[r] = ok ? a.col[e0 + p] : 0;
+            wt[r] = ok ? (a.col_scale ? a.col_scale[idx[r]] : 1.f) : 0.f;
+        }
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int jmax = min(G, maxdeg - off - r * G);
+            for (int j = 0; j < jmax; j += U) {
+                typename Vec<T>::type v[U];
+                float w[U];
+                // issue all U feature-row loads first (they need only the index), then fetch
+                // the edge weights, so the weight gather's latency hides under the loads
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int jj = j + u;
+                    const int srcl = slot * G + (jj < G ? jj : 0);
+                    const int s = __shfl_sync(0xffffffffu, idx[r], srcl);
+                    const bool ok = jj < G && off + r * G + jj < deg;
+                    if (ok) v[u] = Vec<T>::load(X + ((int64_t)s * WV + sub) * E);
+                    else v[u] = {};
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int jj = j + u;
+                    const int srcl = slot * G + (jj < G ? jj : 0);
+                    const float ww = __shfl_sync(0xffffffffu, wt[r], srcl);
+                    w[u] = (jj < G && off + r * G + jj < deg) ? ww : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    float f[E];
+                    Vec<T>::to_f(v[u], f);
+#pragma unroll
+                    for (int q = 0; q < E; q++) acc[q] = fmaf(w[u], f[q], acc[q]);
+                }
+            }
+        }
+    }
+    if (orow < 0) return;
+    if (to_partial) {
+        float* dst = a.partial + ((int64_t)orow * WV + sub) * E;
+#pragma unroll
+        for (int q = 0; q < E; q += 4)
+            *reinterpret_cast<float4*>(dst + q) = make_float4(acc[q], acc[q + 1], acc[q + 2], acc[q + 3]);
+        return;
+    }
+    float acc1[1][E];
+#pragma unroll
+    for (int q = 0; q < E; q++) acc1[0][q] = acc[q];
+    epilogue<T, 1>(a, orow, sub, G, WV, acc1);
+}
+
+// split-row combine, one block per split row: warp w sums slots s0+w, s0+w+8, ... in order,
+// then the 8 warp sums are added in warp order (deterministic) before the epilogue
+template <typename T>
+__global__ void __launch_bounds__(256) k_spmm_fixup_blk(SpmmArgs a, int G) {
+    constexpr int E = Vec<T>::EPV;
+    __shared__ float red[8][32 * E];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t h = blockIdx.x;
+    const int WV = G;
+    const int32_t r = a.heavy_rows[h];
+    const int s0 = a.heavy_slot_off[h], s1 = a.heavy_slot_off[h + 1];
+    float acc[E];
+#pragma unroll
+    for (int q = 0; q < E; q++) acc[q] = 0.f;
+    if (lane < G) {
+        for (int sl = s0 + w; sl < s1; sl += 8) {
+            const float* src = a.partial + ((int64_t)sl * WV + lane) * E;
+#pragma unroll
+            for (int q = 0; q < E; q += 4) {
+                const float4 p = *reinterpret_cast<const float4*>(src + q);
+                acc[q] += p.x; acc[q + 1] += p.y; acc[q + 2] += p.z; acc[q + 3] += p.w;
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < E; q++) red[w][lane * E + q] = acc[q];
+    __syncthreads();
+    if (w == 0 && lane < G) {
+        float tot[1][E];
+#pragma unroll
+        for (int q = 0; q < E; q++) {
+            float t = 0.f;
+            for (int k = 0; k < 8; k++) t += red[k][lane * E + q];
+            tot[0][q] = t;
+        }
+        epilogue<T, 1>(a, r, lane, G, WV, tot);
+    }
+}
+
+template <typename T, int R>
+static grappa_status launch_grp(grappa_ctx* ctx, const SpmmArgs& a, int G, cudaStream_t s) {
+    const int P = 32 / G;
+    const int64_t vrows = a.n + a.n_slots;   // split-row segments first, then the rows
+    if (vrows > 0) {
+        if (g_spmm_variant == 2)
+            k_spmm_grp<T, R, 8><<<(unsigned)ceil_div(ceil_div(vrows, P), 8), 256, 0, s>>>(a, G, P);
+        else
+            k_spmm_grp<T, R, 4><<<(unsigned)ceil_div(ceil_div(vrows, P), 8), 256, 0, s>>>(a, G, P);
+        GRAPPA_LAUNCHED(ctx);
+    }
+    if (a.n_heavy > 0) {
+        k_spmm_fixup_blk<T><<<(unsigned)a.n_heavy, 256, 0, s>>>(a, G);
+        GRAPPA_LAUNCHED(ctx);
+    }
+    return GRAPPA_OK;
+}
+
 template <typename T, int CPL>
 static grappa_status launch_cpl(grappa_ctx* ctx, const SpmmArgs& a, int G, int P, cudaStream_t s) {
     const int64_t vrows = a.n + a.n_slots;
@@ -266,6 +422,13 @@ static grappa_status launch_cpl(grappa_ctx* ctx, const SpmmArgs& a, int G, int P
 template <typename T>
 static grappa_status launch_t(grappa_ctx* ctx, const SpmmArgs& a, cudaStream_t s) {
     const int WV = a.width / Vec<T>::EPV;
+    if (WV <= 32 && g_spmm_variant != 1) {
+        // group-per-row kernel; R index registers per lane so a chunk holds >= 16 edges
+        if (WV >= 16) return launch_grp<T, 1>(ctx, a, WV, s);
+        if (WV >= 8) return launch_grp<T, 2>(ctx, a, WV, s);
+        if (WV >= 4) return launch_grp<T, 4>(ctx, a, WV, s);
+        return launch_grp<T, 8>(ctx, a, WV, s);
+    }
     const int G = WV <= 32 ? WV : 32;
     const int P = 32 / G;
     const int cpl = (WV + G - 1) / G;

@@ -38,6 +38,18 @@ def sweep_schedule(C: int, W: int):
     return [[pairs[((t - 1) * W + w) % len(pairs)] for w in range(W)] for t in range(1, cycle + 1)]
 
 
+def phase_plan(W: int, G: int, rank: int):
+    """Alg. 1 with P = W partitions on G ranks (M = G partitions per phase):
+    phase i -> (worker i*G + rank, or None if this rank idles in a ragged last phase,
+    m_active = number of active partitions in the phase)."""
+    nphase = -(-W // G)
+    plan = []
+    for i in range(nphase):
+        w = i * G + rank
+        plan.append((i, w if w < W else None, min(G, W - i * G)))
+    return plan
+
+
 @dataclass
 class ModelSpec:
     arch: str            # "gcn" | "sage"
@@ -109,9 +121,8 @@ class Trainer:
 
     # ------------------------------------------------------------------ partitions
     def my_workers(self):
-        """workers this rank runs, one per phase: phase i -> worker i*G + rank"""
-        nphase = -(-self.W // self.G)
-        return [(i, i * self.G + self.rank) for i in range(nphase)]
+        """workers this rank runs, one per phase: phase i -> worker i*G + rank (>= W: idle)"""
+        return [(i, i * self.G + self.rank) for i, _, _ in phase_plan(self.W, self.G, self.rank)]
 
     def repartition(self, t: int):
         """a3 for super-epoch t on every worker this rank owns."""
@@ -127,20 +138,28 @@ class Trainer:
         self._alloc()
 
     def _alloc(self):
+        """Activation / workspace buffers sized for the largest partition this rank owns;
+        kept across super-epochs (12.5 % headroom) so a switch does not reallocate."""
         sp = self.spec
         n_max = max(p.n_core for p in self.parts.values()) if self.parts else 1
-        self.H = [None] + [torch.zeros(n_max, sp.dims_pad[l], dtype=self.tdt, device=self.dev)
-                           for l in range(1, sp.depth + 1)]
-        wmax = max(sp.dims_pad)
-        self.dz = [torch.zeros(n_max * wmax, dtype=self.tdt, device=self.dev) for _ in range(2)]
+        if getattr(self, "_n_cap", 0) < n_max:
+            self._n_cap = n_cap = n_max + n_max // 8
+            self.H = [None] + [torch.empty(n_cap, sp.dims_pad[l], dtype=self.tdt, device=self.dev)
+                               for l in range(1, sp.depth + 1)]
+            wmax = max(sp.dims_pad)
+            self.dz = [torch.empty(n_cap * wmax, dtype=self.tdt, device=self.dev) for _ in range(2)]
         ws = 1
         saved = []
         for l in range(sp.depth):
             fi, fo = sp.dims_pad[l], sp.dims_pad[l + 1]
             ws = max([ws] + [layer_ws_bytes(p, sp.arch, fi, fo, self.dt) for p in self.parts.values()])
             sb = max([0] + [layer_saved_bytes(p, sp.arch, fi, fo, self.dt) for p in self.parts.values()])
-            saved.append(torch.empty(max(sb, 1), dtype=torch.uint8, device=self.dev) if sb else None)
-        self.ws = torch.empty(ws, dtype=torch.uint8, device=self.dev)
+            old = self.saved[l] if getattr(self, "saved", None) else None
+            if sb and (old is None or old.numel() < sb):
+                old = torch.empty(sb + sb // 8, dtype=torch.uint8, device=self.dev)
+            saved.append(old if sb else None)
+        if getattr(self, "ws", None) is None or self.ws.numel() < ws:
+            self.ws = torch.empty(ws + ws // 8, dtype=torch.uint8, device=self.dev)
         self.saved = saved
 
     # ------------------------------------------------------------------ one iteration

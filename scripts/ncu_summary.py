@@ -1,0 +1,73 @@
+"""Summarise ncu output for profiles/: per-kernel dram bytes / duration / throughput from a
+`--set full` report, and per-kernel time shares from a `--metrics gpu__time_duration.sum`
+launch list.  Usage:
+  python scripts/ncu_summary.py full  <report.ncu-rep> [<report2> ...] > profiles/ncu_summary.json
+  python scripts/ncu_summary.py launches <launches.csv> > profiles/<round>_launches.txt
+"""
+import collections
+import csv
+import io
+import json
+import subprocess
+import sys
+
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
+        "msecond": 1e-3, "second": 1.0}
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__grid_size",
+        "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"]
+
+
+def full(paths):
+    out = {}
+    for p in paths:
+        raw = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
+        rows = list(csv.reader(io.StringIO(raw)))
+        h, units = rows[0], rows[1]
+        for r in rows[2:]:
+            name = r[h.index("Kernel Name")].split("(")[0].replace("void ", "").replace("grappa::", "")
+            rec = out.setdefault(name, {"launches": 0, "report": p})
+            rec["launches"] += 1
+            for w in WANT:
+                if w in h:
+                    i = h.index(w)
+                    try:
+                        v = float(r[i].replace(",", "")) * UNIT.get(units[i], 1.0)
+                    except ValueError:
+                        continue
+                    rec.setdefault(w, []).append(v)
+    for name, rec in out.items():
+        for w in WANT:
+            if w in rec:
+                rec[w] = sum(rec[w]) / len(rec[w])
+        if "dram__bytes_read.sum" in rec:
+            rec["dram_bytes_per_launch"] = rec["dram__bytes_read.sum"] + rec.get("dram__bytes_write.sum", 0)
+            rec["dram_GBps"] = rec["dram_bytes_per_launch"] / rec["gpu__time_duration.sum"] / 1e9
+    json.dump({"kernels": out}, sys.stdout, indent=1)
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hi]
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in rows[hi + 1:]:
+        if len(r) < len(h):
+            continue
+        v = float(r[h.index("Metric Value")].replace(",", "")) * UNIT.get(r[h.index("Metric Unit")], 1e-9)
+        k = r[h.index("Kernel Name")].split("(")[0].replace("void ", "").replace("grappa::", "")
+        agg[k][0] += 1
+        agg[k][1] += v
+    tot = sum(t for _, t in agg.values())
+    print(f"# {path}: {sum(n for n, _ in agg.values())} launches, {tot*1e3:.3f} ms (cold-cache, serialised)")
+    print(f"{'ms':>9} {'n':>5} {'share':>6}  kernel")
+    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"{t*1e3:9.3f} {n:5d} {100*t/tot:5.1f}%  {k}")
+
+
+if __name__ == "__main__":
+    {"full": lambda: full(sys.argv[2:]), "launches": lambda: launches(sys.argv[2])}[sys.argv[1]]()

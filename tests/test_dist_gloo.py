@@ -1,0 +1,99 @@
+"""N > 1 host logic on CPU: world_size-2 `gloo` process groups run the engine's phase plan
+(phase i -> worker i*G + rank, m_active per phase, idle ranks contribute zeros) with the
+oracle's per-partition gradients and a real all-reduce, and must reproduce the oracle's
+single-process Algorithm 1 with M = G.  The CUDA path's equivalent collective
+is the ncclAllReduce inside grappa_aggregate_grads (exercised on a GPU box)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import gen
+from oracle import correction as Co
+from oracle import model as Mo
+from oracle import partition as Po
+from oracle import train as Tr
+from paper_2602_01872_b200.engine import phase_plan
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _setup(C):
+    wl = gen.small_workload("products", n=1500, scale=11, num_samples=12_000, depth=2, chunks=C,
+                            hidden=16)
+    ds = gen.make_dataset(wl)
+    W0 = [[np.asarray(w, np.float64)[:wl.dims[l], :wl.dims[l + 1]] for w in ws]
+          for l, ws in enumerate(ds.weights)]
+    return wl, ds, W0
+
+
+def _worker(rank, world, port, C, corr, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    wl, ds, W0 = _setup(C)
+    chunk_of = Po.make_chunks(wl.n, C, gen.seed_of("chunks"))
+    pairs = Po.sweep_schedule(C, C)[0]
+    shapes = [[w.shape for w in ws] for ws in W0]
+    theta = Mo.flatten(W0)
+    X = ds.x[:, :wl.F].astype(np.float64)
+    for i, w, m_active in phase_plan(C, world, rank):
+        g = np.zeros_like(theta)
+        c = 0.0
+        if w is not None:
+            part = Po.induced_partition(ds.rowptr, ds.col, chunk_of, *pairs[w], ds.train)
+            _, g, _, _ = Mo.partition_loss_grad(wl.arch, part, X[part["core"]], ds.y[part["core"]],
+                                                Mo.unflatten(theta, shapes))
+            c = Tr.partition_factor(corr, part)
+        t = torch.from_numpy(c / m_active * g)          # fused scale before the all-reduce
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        theta = Co.sgd(theta, t.numpy(), 0.1)
+    th = torch.from_numpy(theta)
+    dist.broadcast(th0 := th.clone(), 0)
+    if rank == 0:
+        out.put(theta)
+    assert np.array_equal(theta, th0.numpy())          # replicas stay identical
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("C,corr", [(4, "uniform"), (3, "none"), (4, "resampling")])
+def test_two_rank_phase_loop_matches_oracle(C, corr):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, C, corr, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    theta = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    wl, ds, W0 = _setup(C)
+    chunk_of = Po.make_chunks(wl.n, C, gen.seed_of("chunks"))
+    final, recs = Tr.run(wl.arch, ds.rowptr, ds.col, ds.x[:, :wl.F].astype(np.float64), ds.y,
+                         ds.train, W0, chunk_of, C, C, 2, corr, 0.1, 1, 10)
+    assert len(recs) == -(-C // 2)
+    ref = Mo.flatten(final)
+    assert np.max(np.abs(theta - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def test_phase_plan():
+    assert phase_plan(8, 1, 0) == [(i, i, 1) for i in range(8)]
+    assert phase_plan(8, 8, 3) == [(0, 3, 8)]
+    assert phase_plan(8, 4, 1) == [(0, 1, 4), (1, 5, 4)]
+    assert phase_plan(3, 2, 1) == [(0, 1, 2), (1, None, 1)]
+    # every worker runs exactly once per epoch across ranks ("every partition
+    # contributes exactly one update per epoch")
+    for W in range(1, 9):
+        for G in range(1, 9):
+            ws = sorted(w for r in range(G) for _, w, _ in phase_plan(W, G, r) if w is not None)
+            assert ws == list(range(W))

@@ -284,29 +284,33 @@ def test_epoch_parity(G, ctx, prod, arxiv, which, corr, epochs, rep):
     assert err(thetas[P], Mo.flatten(final)) <= 1e-4
 
 
-@pytest.mark.parametrize("arch", ["gcn", "sage"])
-def test_tcgen05_matches_simt(G, ctx, prod, arch):
-    """The bf16 tcgen05 GEMMs and the CUDA-core GEMMs agree (same layer, same inputs)."""
-    part = _part(G, ctx, prod, 8, 3, 6, "bf16")
+@pytest.mark.parametrize("arch,op,dtype", [("gcn", "gemm", "bf16"), ("sage", "gemm", "bf16"),
+                                           ("gcn", "spmm", "bf16"), ("sage", "spmm", "f32")])
+def test_kernel_variants_agree(G, ctx, prod, arch, op, dtype):
+    """Alternative implementations agree on the same layer and inputs: bf16 tcgen05 GEMMs vs
+    the CUDA-core GEMMs; the row-group SpMM vs the warp-per-row SpMM."""
+    part = _part(G, ctx, prod, 8, 3, 6, dtype)
     n, f_in, f_out = part.n_core, 112, 48
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     g = torch.Generator(device="cuda").manual_seed(7)
-    h_in = torch.randn(n, f_in, device="cuda", generator=g).relu().to(torch.bfloat16)
+    h_in = torch.randn(n, f_in, device="cuda", generator=g).relu().to(tdt)
     m = 1 if arch == "gcn" else 2
     w = torch.randn(m * f_in, f_out, device="cuda", generator=g) / 10
-    dz = (torch.randn(n, f_out, device="cuda", generator=g) * 1e-2).to(torch.bfloat16)
+    dz = (torch.randn(n, f_out, device="cuda", generator=g) * 1e-2).to(tdt)
     outs = []
     lib = G.load()
-    for simt in (0, 1):
-        lib.grappa_debug_gemm_simt(simt)
-        h_out = torch.empty(n, f_out, device="cuda", dtype=torch.bfloat16)
-        saved = torch.empty(max(1, G.layer_saved_bytes(part, arch, f_in, f_out, "bf16")), dtype=torch.uint8, device="cuda")
-        ws = torch.empty(G.layer_ws_bytes(part, arch, f_in, f_out, "bf16"), dtype=torch.uint8, device="cuda")
-        G.grappa_layer_fwd(ctx, part, arch, f_in, f_out, True, h_in, w, h_out, saved, ws, "bf16")
+    for variant in (0, 1):
+        assert lib.grappa_set_kernel_variant(op.encode(), variant) == 0
+        h_out = torch.empty(n, f_out, device="cuda", dtype=tdt)
+        saved = torch.empty(max(1, G.layer_saved_bytes(part, arch, f_in, f_out, dtype)), dtype=torch.uint8, device="cuda")
+        ws = torch.empty(G.layer_ws_bytes(part, arch, f_in, f_out, dtype), dtype=torch.uint8, device="cuda")
+        G.grappa_layer_fwd(ctx, part, arch, f_in, f_out, True, h_in, w, h_out, saved, ws, dtype)
         dw = torch.empty_like(w)
-        dz_in = torch.empty(n, f_in, device="cuda", dtype=torch.bfloat16)
-        G.grappa_layer_bwd(ctx, part, arch, f_in, f_out, True, dz, h_in, w, saved, dw, dz_in, ws, "bf16")
+        dz_in = torch.empty(n, f_in, device="cuda", dtype=tdt)
+        G.grappa_layer_bwd(ctx, part, arch, f_in, f_out, True, dz, h_in, w, saved, dw, dz_in, ws, dtype)
         torch.cuda.synchronize()
         outs.append((_np(h_out), _np(dw), _np(dz_in)))
-    lib.grappa_debug_gemm_simt(0)
+    lib.grappa_set_kernel_variant(op.encode(), 0)
+    assert lib.grappa_set_kernel_variant(b"nope", 1) == 1
     for a, b in zip(*outs):
-        assert err(a, b) <= 1e-2
+        assert err(a, b) <= (1e-2 if dtype == "bf16" else 1e-5)
