@@ -232,7 +232,7 @@ def run_grappa(args):
 
     import gen
     import paper_2602_01872_b200 as G
-    from paper_2602_01872_b200.engine import ModelSpec, Trainer
+    from paper_2602_01872_b200.engine import MinibatchTrainer, ModelSpec, Trainer
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -256,9 +256,16 @@ def run_grappa(args):
     t_gen = time.perf_counter() - t_gen
     spec = ModelSpec(wl.arch, wl.dims, wl.dims_pad)
     stream = torch.cuda.current_stream(dev)
-    tr = Trainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights, wl.chunks,
-                 gen.seed_of("chunks"), corr=wl.correction, lr=0.003,
-                 repartition_every=wl.repartition_every, dtype=args.dtype, stream=stream)
+    common = dict(corr=wl.correction, lr=0.003, repartition_every=wl.repartition_every,
+                  dtype=args.dtype, stream=stream, num_workers=wl.extra.get("workers"))
+    if wl.extra.get("mode") == "minibatch":
+        tr = MinibatchTrainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights,
+                              wl.chunks, gen.seed_of("chunks"), fanouts=wl.extra["fanouts"],
+                              batch_size=wl.extra["batch_size"], sample_seed=gen.seed_of("sample"),
+                              **common)
+    else:
+        tr = Trainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights, wl.chunks,
+                     gen.seed_of("chunks"), **common)
     nnz = ds.nnz
     del ds
 
@@ -312,7 +319,7 @@ def run_grappa(args):
     # e2e: the same epochs through the public API with host buffers (per phase H2D of the
     # partition's inputs from pinned memory, D2H of the loss), copies inside the timed region
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not isinstance(tr, MinibatchTrainer):
         e2e = measure_e2e(tr, stream, K, barrier, world, dist, nnz)
 
     cpu = None

@@ -215,10 +215,20 @@ WORKLOADS = {
     # configs[2]: ogbn-products-shaped RMAT, GCN-8, 8 partitions, repartition every N epochs
     "products": Workload("products", "rmat", 2_449_029, 100, 47, "gcn", 8, train_frac=0.0803,
                          scale=22, num_samples=65_800_000, chunks=8, repartition_every=10),
-    # configs[4]: R-MAT scaling sweep, GCN-4, min-distance (uniform) correction
+    # configs[3]: ogbn-papers100M-shaped RMAT, SAGE-3 mini-batch (B = 1000, fanouts
+    # {15,10,5} input -> output, R25), 8 partitions
+    "papers": Workload("papers", "rmat", 111_059_956, 128, 172, "sage", 3, train_frac=0.01087,
+                       scale=27, num_samples=1_666_000_000, chunks=8,
+                       extra=dict(mode="minibatch", fanouts=(15, 10, 5), batch_size=1000)),
+    # configs[4]: R-MAT scaling sweep (Graph500, edge factor 16), GCN-4, min-distance
+    # (uniform) correction, W = C partitions
     "rmat22": Workload("rmat22", "rmat", 1 << 22, 128, 16, "gcn", 4, train_frac=0.1, scale=22,
                        num_samples=1 << 26, chunks=8, correction="uniform"),
+    "rmat24": Workload("rmat24", "rmat", 1 << 24, 128, 16, "gcn", 4, train_frac=0.1, scale=24,
+                       num_samples=1 << 28, chunks=8, correction="uniform"),
 }
+WORKLOADS["cora4"] = Workload(**{**WORKLOADS["cora"].__dict__, "name": "cora4", "chunks": 4,
+                                 "extra": dict(workers=2)})
 
 
 def small_workload(name: str, n: int, scale: int, num_samples: int, **kw) -> Workload:

@@ -197,6 +197,66 @@ grappa_status grappa_aggregate_grads(grappa_ctx* ctx, const grappa_part* part, g
                                      float* grad, int64_t n_params, int32_t m_active, float lr,
                                      float* theta, void* stream);
 
+/* a7 with an explicit factor (mini-batch mode: c_p is the batch's factor, grappa_batch_factors).
+ * Same semantics as grappa_aggregate_grads with c_p = c (c = 0 for an idle rank). */
+grappa_status grappa_aggregate_grads_c(grappa_ctx* ctx, double c, float* grad, int64_t n_params,
+                                       int32_t m_active, float lr, float* theta, void* stream);
+
+/* ---------------------------------------------------------------- a10: mini-batch mode
+ * Isolated mini-batch sampling (config 4): P:139/P:177 (§3.2 sampling mode, k-hop subgraphs
+ * from the local partition only), P:382 (Alg. 1 isolated_sampling), P:489 (B = 1000,
+ * fanouts {15,10,5}).  Readings R23-R28:
+ *   epoch order  seeds sorted by (h(seed, epoch, gid), gid)
+ *   hop h        each target v keeps the min(f_h, d_l(v)) local neighbours u with the
+ *                smallest (h(h(seed, epoch, batch, h), gid(v), gid(u)), gid(u))
+ *   sources      targets (prefix, same order) then new nodes in ascending local id
+ *   fanouts      listed input -> output layer: hop 1 (the seeds) uses fanouts[L-1]
+ * GraphSAGE only (config 4 is SAGE-3). */
+typedef struct grappa_batch grappa_batch;   /* library-owned layered blocks of one batch */
+
+typedef struct {
+    int32_t n_dst, n_src;       /* targets (rows) / sources (columns) of the block          */
+    int64_t nnz;
+    const int64_t* rowptr;      /* dev [n_dst+1]  block CSR, col = source positions asc.    */
+    const int32_t* col;         /* dev [nnz]                                                */
+    const int64_t* t_rowptr;    /* dev [n_src+1]  transpose (source -> target positions)    */
+    const int32_t* t_col;       /* dev [nnz]                                                */
+    const float* inv_cnt;       /* dev [n_dst]    1/|S(v)|, 0 for an empty sample           */
+    const int32_t* src;         /* dev [n_src]    partition-local id of each source         */
+} grappa_block_info;
+
+/* Epoch order of the partition's seeds (R23): order dev int32[n_seeds] (out, local ids). */
+grappa_status grappa_epoch_seeds(grappa_ctx* ctx, const grappa_part* part, uint64_t seed,
+                                 int64_t epoch, int32_t* order, void* stream);
+/* Sample the L blocks of one batch.  batch: dev int32[n_batch] local seed ids; fanouts: host
+ * int32[n_layers] (input -> output).  *inout NULL -> created, else reused.  Syncs once.
+ * Errors: E_ARG (n_layers < 1, fanout < 1, n_batch < 1). */
+grappa_status grappa_sample(grappa_ctx* ctx, const grappa_part* part, const int32_t* batch,
+                            int32_t n_batch, const int32_t* fanouts, int32_t n_layers,
+                            uint64_t seed, int64_t epoch, int64_t batch_index,
+                            grappa_batch** inout, void* stream);
+/* layer l = 0 (input) .. n_layers-1 (output: its targets are the batch seeds) */
+grappa_status grappa_batch_query(const grappa_batch* b, int32_t layer, grappa_block_info* out);
+/* Coverage factors of the batch over its seeds with s_v = hop-1 sample size (R28):
+ * eq:correction_uniform, eq:resampling (SPEC guards), and the R13 reading. */
+grappa_status grappa_batch_factors(const grappa_batch* b, double* c_uniform,
+                                   double* c_resampling, double* c_resampling_hm);
+void grappa_batch_destroy(grappa_batch* b);
+
+/* One isolated SAGE mini-batch forward + loss + backward on the sampled blocks:
+ *   h_0 = x[src of layer 0]; layer l: h_{l+1}[v] = act(h_l[v] W_self + mean_{u in S(v)} h_l[u]
+ *   W_nbr); loss = mean softmax-CE over the batch seeds; grad (dev fp32, flat theta layout:
+ *   per layer [W_self; W_nbr] blocks of dims_pad[l] x dims_pad[l+1]) <- dL/dtheta.
+ *   dims_pad: host int32[n_layers+1] (multiples of 16; dims_pad[0] = the partition's
+ *   feat_dim).  ws: grappa_minibatch_ws_bytes.  hidden_out: NULL, or host array of
+ *   n_layers-1 dev pointers receiving h_1..h_{L-1} (rows n_dst of layers 0..L-2) for tests. */
+size_t grappa_minibatch_ws_bytes(const grappa_batch* b, int32_t n_layers, const int32_t* dims_pad,
+                                 grappa_dtype dtype);
+grappa_status grappa_minibatch_step(grappa_ctx* ctx, const grappa_part* part, const grappa_batch* b,
+                                    int32_t n_layers, const int32_t* dims_pad, int32_t num_classes,
+                                    const float* theta, float* grad, void* ws, double* loss_dev,
+                                    void* const* hidden_out, grappa_dtype dtype, void* stream);
+
 /* Sync the stream and report asynchronous faults: E_NONFINITE if any aggregated gradient
  * since the last check was non-finite, E_CUDA / E_NCCL on device or communicator errors. */
 grappa_status grappa_check(grappa_ctx* ctx, void* stream);

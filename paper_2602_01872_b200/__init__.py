@@ -205,3 +205,84 @@ def grappa_aggregate_grads(ctx: Context, part: Part | None, corr: str, grad, m_a
     _lib.check("grappa_aggregate_grads", ctx.lib.grappa_aggregate_grads(
         ctx.h, part.h if part is not None else None, CORR[corr], _lib.ptr(grad), grad.numel(),
         m_active, ctypes.c_float(lr), _lib.ptr(theta), _lib.stream_ptr(stream)))
+
+
+def grappa_aggregate_grads_c(ctx: Context, c: float, grad, m_active: int, lr: float, theta, stream=None):
+    _lib.check("grappa_aggregate_grads_c", ctx.lib.grappa_aggregate_grads_c(
+        ctx.h, ctypes.c_double(c), _lib.ptr(grad), grad.numel(), m_active, ctypes.c_float(lr),
+        _lib.ptr(theta), _lib.stream_ptr(stream)))
+
+
+# ------------------------------------------------------------------ a10: mini-batch mode
+class Batch:
+    """grappa_batch handle (layered blocks of one sampled mini-batch) + tensor views."""
+
+    def __init__(self):
+        self.h = ctypes.c_void_p()
+        self.blocks = []
+
+    def refresh(self, n_layers: int):
+        lib = load()
+        self.blocks = []
+        for l in range(n_layers):
+            bi = _lib.BlockInfo()
+            _lib.check("grappa_batch_query", lib.grappa_batch_query(self.h, l, ctypes.byref(bi)))
+            self.blocks.append(dict(
+                n_dst=bi.n_dst, n_src=bi.n_src, nnz=bi.nnz,
+                rowptr=_view(bi.rowptr, (bi.n_dst + 1,), "<i8", self),
+                col=_view(bi.col, (bi.nnz,), "<i4", self),
+                t_rowptr=_view(bi.t_rowptr, (bi.n_src + 1,), "<i8", self),
+                t_col=_view(bi.t_col, (bi.nnz,), "<i4", self),
+                inv_cnt=_view(bi.inv_cnt, (bi.n_dst,), "<f4", self),
+                src=_view(bi.src, (bi.n_src,), "<i4", self)))
+        cu, cr, ch = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        _lib.check("grappa_batch_factors", lib.grappa_batch_factors(
+            self.h, ctypes.byref(cu), ctypes.byref(cr), ctypes.byref(ch)))
+        self.factors = {"none": 1.0, "uniform": cu.value, "resampling": cr.value,
+                        "resampling_hm": ch.value}
+        return self
+
+    def destroy(self):
+        if self.h:
+            load().grappa_batch_destroy(self.h)
+            self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def grappa_epoch_seeds(ctx: Context, part: Part, seed: int, epoch: int, order, stream=None):
+    _lib.check("grappa_epoch_seeds", ctx.lib.grappa_epoch_seeds(
+        ctx.h, part.h, ctypes.c_uint64(seed & ((1 << 64) - 1)), epoch, _lib.ptr(order),
+        _lib.stream_ptr(stream)))
+
+
+def grappa_sample(ctx: Context, part: Part, batch, fanouts, seed: int, epoch: int, batch_index: int,
+                  out: Batch | None = None, stream=None) -> Batch:
+    out = out or Batch()
+    fan = (ctypes.c_int32 * len(fanouts))(*fanouts)
+    _lib.check("grappa_sample", ctx.lib.grappa_sample(
+        ctx.h, part.h, _lib.ptr(batch), batch.numel(), fan, len(fanouts),
+        ctypes.c_uint64(seed & ((1 << 64) - 1)), epoch, batch_index, ctypes.byref(out.h),
+        _lib.stream_ptr(stream)))
+    return out.refresh(len(fanouts))
+
+
+def minibatch_ws_bytes(batch: Batch, dims_pad, dtype) -> int:
+    dp = (ctypes.c_int32 * len(dims_pad))(*dims_pad)
+    return int(load().grappa_minibatch_ws_bytes(batch.h, len(dims_pad) - 1, dp, dtype_code(dtype)))
+
+
+def grappa_minibatch_step(ctx: Context, part: Part, batch: Batch, dims_pad, num_classes: int, theta,
+                          grad, ws, loss_dev, dtype, hidden_out=None, stream=None):
+    L = len(dims_pad) - 1
+    dp = (ctypes.c_int32 * (L + 1))(*dims_pad)
+    hid = None
+    if hidden_out is not None:
+        hid = (ctypes.c_void_p * max(1, L - 1))(*[t.data_ptr() for t in hidden_out])
+    _lib.check("grappa_minibatch_step", ctx.lib.grappa_minibatch_step(
+        ctx.h, part.h, batch.h, L, dp, num_classes, _lib.ptr(theta), _lib.ptr(grad), _lib.ptr(ws),
+        _lib.ptr(loss_dev), hid, dtype_code(dtype), _lib.stream_ptr(stream)))

@@ -24,7 +24,9 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_part_destroy", "grappa_layer_saved_bytes", "grappa_layer_ws_bytes",
            "grappa_layer_fwd", "grappa_layer_bwd", "grappa_loss", "grappa_aggregate_grads",
            "grappa_check", "grappa_launch_count", "grappa_profile_enable", "grappa_profile_read",
-           "grappa_set_kernel_variant"]
+           "grappa_set_kernel_variant", "grappa_aggregate_grads_c", "grappa_epoch_seeds",
+           "grappa_sample", "grappa_batch_query", "grappa_batch_factors", "grappa_batch_destroy",
+           "grappa_minibatch_ws_bytes", "grappa_minibatch_step"]
 KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5}
 
 
@@ -50,6 +52,13 @@ class PartInfo(ctypes.Structure):
                 ("n_heavy", ctypes.c_int64), ("n_slots", ctypes.c_int64),
                 ("c_uniform", ctypes.c_double), ("c_resampling", ctypes.c_double),
                 ("c_resampling_hm", ctypes.c_double), ("D", ctypes.c_int64)]
+
+
+class BlockInfo(ctypes.Structure):
+    _fields_ = [("n_dst", ctypes.c_int32), ("n_src", ctypes.c_int32), ("nnz", ctypes.c_int64),
+                ("rowptr", ctypes.c_void_p), ("col", ctypes.c_void_p),
+                ("t_rowptr", ctypes.c_void_p), ("t_col", ctypes.c_void_p),
+                ("inv_cnt", ctypes.c_void_p), ("src", ctypes.c_void_p)]
 
 
 _lib = None
@@ -90,6 +99,14 @@ def load(path: str = LIB_PATH):
         "grappa_launch_count": (i64, [vp]),
         "grappa_profile_enable": (st, [vp, ctypes.c_int]),
         "grappa_set_kernel_variant": (st, [ctypes.c_char_p, ctypes.c_int]),
+        "grappa_aggregate_grads_c": (st, [vp, dbl, vp, i64, i32, f32, vp, vp]),
+        "grappa_epoch_seeds": (st, [vp, vp, u64, i64, vp, vp]),
+        "grappa_sample": (st, [vp, vp, vp, i32, vp, i32, u64, i64, i64, ctypes.POINTER(vp), vp]),
+        "grappa_batch_query": (st, [vp, i32, ctypes.POINTER(BlockInfo)]),
+        "grappa_batch_factors": (st, [vp, ctypes.POINTER(dbl), ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
+        "grappa_batch_destroy": (None, [vp]),
+        "grappa_minibatch_ws_bytes": (sz, [vp, i32, vp, ctypes.c_int]),
+        "grappa_minibatch_step": (st, [vp, vp, vp, i32, vp, i32, vp, vp, vp, vp, vp, ctypes.c_int, vp]),
         "grappa_profile_read": (st, [vp, ctypes.c_int, ctypes.POINTER(dbl), ctypes.POINTER(i64),
                                      ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
     }

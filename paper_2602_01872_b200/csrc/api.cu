@@ -344,7 +344,6 @@ extern "C" grappa_status grappa_aggregate_grads(grappa_ctx* ctx, const grappa_pa
     GRAPPA_ARG(ctx && grad && n_params > 0, GRAPPA_E_ARG, "grappa_aggregate_grads: null argument");
     GRAPPA_ARG(m_active >= 1, GRAPPA_E_ARG, "grappa_aggregate_grads: m_active must be >= 1");
     GRAPPA_ARG(lr == 0.f || theta, GRAPPA_E_ARG, "grappa_aggregate_grads: lr != 0 needs theta");
-    cudaStream_t s = (cudaStream_t)stream;
     double c = 0.0;   // inactive rank: contributes zeros
     if (part) {
         const grappa_part_info& I = part->info;
@@ -357,6 +356,16 @@ extern "C" grappa_status grappa_aggregate_grads(grappa_ctx* ctx, const grappa_pa
         }
         GRAPPA_ARG(std::isfinite(c), GRAPPA_E_NONFINITE, "grappa_aggregate_grads: non-finite c (S:361)");
     }
+    return grappa_aggregate_grads_c(ctx, c, grad, n_params, m_active, lr, theta, stream);
+}
+
+extern "C" grappa_status grappa_aggregate_grads_c(grappa_ctx* ctx, double c, float* grad, int64_t n_params,
+                                                  int32_t m_active, float lr, float* theta, void* stream) {
+    GRAPPA_ARG(ctx && grad && n_params > 0, GRAPPA_E_ARG, "grappa_aggregate_grads_c: null argument");
+    GRAPPA_ARG(m_active >= 1, GRAPPA_E_ARG, "grappa_aggregate_grads_c: m_active must be >= 1");
+    GRAPPA_ARG(lr == 0.f || theta, GRAPPA_E_ARG, "grappa_aggregate_grads_c: lr != 0 needs theta");
+    GRAPPA_ARG(std::isfinite(c), GRAPPA_E_NONFINITE, "grappa_aggregate_grads_c: non-finite c (S:361)");
+    cudaStream_t s = (cudaStream_t)stream;
     const float scale = (float)(c / (double)m_active);
     const bool multi = ctx->comm && ctx->nranks > 1;
     ProfScope ps(ctx, s, GRAPPA_K_AGG, (double)n_params * 4.0 * (lr != 0.f ? 4 : 2), 3.0 * n_params);

@@ -19,19 +19,21 @@ template <> __device__ __forceinline__ void sf<__nv_bfloat16>(__nv_bfloat16* p, 
 constexpr int kLossThreads = 256;
 constexpr int kMaxKPad = 512;
 
+// seed k: logits row rows[k] (rows == null: row k), label labels[lidx ? lidx[k] : row]
 template <typename T>
-__global__ void __launch_bounds__(kLossThreads) k_loss(int64_t n_seeds, const int32_t* seeds,
-                                                       const int32_t* labels, const T* logits,
-                                                       int K, int kpad, T* dlogits, double* part) {
+__global__ void __launch_bounds__(kLossThreads) k_loss(int64_t n_seeds, const int32_t* rows,
+                                                       const int32_t* lidx, const int32_t* labels,
+                                                       const T* logits, int K, int kpad, T* dlogits,
+                                                       double* part) {
     __shared__ double wsum[kLossThreads / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t k = (int64_t)blockIdx.x * (kLossThreads / 32) + wid;
     double my = 0.0;
     if (k < n_seeds) {
-        const int32_t v = seeds[k];
-        const T* z = logits + (int64_t)v * kpad;
-        T* dz = dlogits + (int64_t)v * kpad;
-        const int y = labels[v];
+        const int64_t v = rows ? rows[k] : k;
+        const T* z = logits + v * kpad;
+        T* dz = dlogits + v * kpad;
+        const int y = labels[lidx ? lidx[k] : v];
         float m = -INFINITY;
         for (int c = lane; c < K; c += 32) m = fmaxf(m, lf<T>(z + c));
 #pragma unroll
@@ -73,6 +75,31 @@ __global__ void __launch_bounds__(256) k_loss_final(int nb, const double* part, 
     }
 }
 
+// softmax-CE over n_seeds rows of logits [n_rows x k_pad]; dlogits fully written (zeros off
+// the seed rows).  partial sums in the ctx reduction scratch (grown outside graph capture).
+grappa_status loss_rows(grappa_ctx* ctx, int64_t n_seeds, const int32_t* rows, const int32_t* lidx,
+                        const int32_t* labels, int64_t n_rows, const void* logits, int K, int k_pad,
+                        void* dlogits, double* loss_dev, grappa_dtype dtype, cudaStream_t s) {
+    const size_t esz = dtype == GRAPPA_BF16 ? 2 : 4;
+    ProfScope ps(ctx, s, GRAPPA_K_LOSS, (double)n_rows * k_pad * esz + 2.0 * n_seeds * k_pad * esz,
+                 5.0 * n_seeds * K);
+    GRAPPA_CUDA(cudaMemsetAsync(dlogits, 0, (size_t)n_rows * k_pad * esz, s));
+    const int64_t nb = ceil_div(n_seeds, kLossThreads / 32);
+    GRAPPA_TRY(ctx->red_ws.grow((size_t)nb * sizeof(double)));
+    double* part_sums = (double*)ctx->red_ws.p;
+    if (dtype == GRAPPA_BF16)
+        k_loss<__nv_bfloat16><<<(unsigned)nb, kLossThreads, 0, s>>>(
+            n_seeds, rows, lidx, labels, (const __nv_bfloat16*)logits, K, k_pad, (__nv_bfloat16*)dlogits,
+            part_sums);
+    else
+        k_loss<float><<<(unsigned)nb, kLossThreads, 0, s>>>(n_seeds, rows, lidx, labels, (const float*)logits,
+                                                            K, k_pad, (float*)dlogits, part_sums);
+    GRAPPA_LAUNCHED(ctx);
+    k_loss_final<<<1, 256, 0, s>>>((int)nb, part_sums, 1.0 / (double)n_seeds, loss_dev);
+    GRAPPA_LAUNCHED(ctx);
+    return GRAPPA_OK;
+}
+
 }  // namespace grappa
 
 using namespace grappa;
@@ -85,24 +112,6 @@ extern "C" grappa_status grappa_loss(grappa_ctx* ctx, const grappa_part* part, c
                "grappa_loss: need 1 <= K <= k_pad <= %d", kMaxKPad);
     const grappa_part_info& I = part->info;
     GRAPPA_ARG(I.n_seeds > 0, GRAPPA_E_EMPTY, "grappa_loss: empty seed set (S:213)");
-    cudaStream_t s = (cudaStream_t)stream;
-    const size_t esz = dtype == GRAPPA_BF16 ? 2 : 4;
-    ProfScope ps(ctx, s, GRAPPA_K_LOSS, (double)I.n_core * k_pad * esz + 2.0 * I.n_seeds * k_pad * esz,
-                 5.0 * I.n_seeds * num_classes);
-    GRAPPA_CUDA(cudaMemsetAsync(dlogits, 0, (size_t)I.n_core * k_pad * esz, s));
-    const int64_t nb = ceil_div(I.n_seeds, kLossThreads / 32);
-    GRAPPA_TRY(ctx->red_ws.grow((size_t)nb * sizeof(double)));
-    double* part_sums = (double*)ctx->red_ws.p;
-    if (dtype == GRAPPA_BF16)
-        k_loss<__nv_bfloat16><<<(unsigned)nb, kLossThreads, 0, s>>>(
-            I.n_seeds, I.seeds, I.labels, (const __nv_bfloat16*)logits, num_classes, k_pad,
-            (__nv_bfloat16*)dlogits, part_sums);
-    else
-        k_loss<float><<<(unsigned)nb, kLossThreads, 0, s>>>(I.n_seeds, I.seeds, I.labels,
-                                                            (const float*)logits, num_classes,
-                                                            k_pad, (float*)dlogits, part_sums);
-    GRAPPA_LAUNCHED(ctx);
-    k_loss_final<<<1, 256, 0, s>>>((int)nb, part_sums, 1.0 / (double)I.n_seeds, loss_dev);
-    GRAPPA_LAUNCHED(ctx);
-    return GRAPPA_OK;
+    return loss_rows(ctx, I.n_seeds, I.seeds, nullptr, I.labels, I.n_core, logits, num_classes, k_pad,
+                     dlogits, loss_dev, dtype, (cudaStream_t)stream);
 }

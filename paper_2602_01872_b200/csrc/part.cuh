@@ -2,6 +2,16 @@
 #pragma once
 #include "common.cuh"
 
+namespace grappa {
+// dst[i] = src[idx[i]] for i < n (rows of row_bytes, a multiple of 16); warp per row
+__global__ void k_gather_rows(int64_t n, int64_t row_bytes, const int32_t* __restrict__ idx,
+                              const uint4* __restrict__ src, uint4* __restrict__ dst);
+// softmax-CE over explicit seed rows (loss.cu)
+grappa_status loss_rows(grappa_ctx* ctx, int64_t n_seeds, const int32_t* rows, const int32_t* lidx,
+                        const int32_t* labels, int64_t n_rows, const void* logits, int K, int k_pad,
+                        void* dlogits, double* loss_dev, grappa_dtype dtype, cudaStream_t s);
+}  // namespace grappa
+
 struct grappa_part {
     grappa_part_info info{};
     grappa::DevBuf rowptr, col, core_global, d_l, d_g, norm_gcn, norm_sage, seeds, labels, x;

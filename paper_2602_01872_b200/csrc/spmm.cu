@@ -445,6 +445,7 @@ grappa_status spmm(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grappa_
                    cudaStream_t s) {
     const grappa_part_info& I = part->info;
     a.n = I.n_core;
+    a.nnz = I.nnz;
     a.rowptr = I.rowptr;
     a.col = I.col;
     a.n_slots = I.n_slots;
@@ -453,10 +454,15 @@ grappa_status spmm(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grappa_
     a.slot_seg = (const int32_t*)part->slot_seg.p;
     a.heavy_rows = (const int32_t*)part->heavy_rows.p;
     a.heavy_slot_off = (const int32_t*)part->heavy_slot_off.p;
+    return spmm_csr(ctx, a, dt, s);
+}
+
+grappa_status spmm_csr(grappa_ctx* ctx, SpmmArgs a, grappa_dtype dt, cudaStream_t s) {
     if (a.width % 8 != 0) {
         set_error("spmm: width %d not a multiple of 8", a.width);
         return GRAPPA_E_SHAPE;
     }
+    struct { int64_t n_core, nnz; } I{a.n, a.nnz};
     const double es = dt == GRAPPA_BF16 ? 2.0 : 4.0, w = a.width, nnz = (double)I.nnz;
     const double per_edge = 4.0 + (a.col_scale ? 4.0 : 0.0) + w * es;
     const double per_row = 8.0 + (a.row_scale ? 4.0 : 0.0) + (a.col_scale ? 4.0 : 0.0) +

@@ -7,6 +7,7 @@ namespace grappa {
 struct SpmmArgs {
     // filled by spmm() from the partition
     int64_t n = 0;
+    int64_t nnz = 0;
     const int64_t* rowptr = nullptr;
     const int32_t* col = nullptr;
     int64_t n_slots = 0, n_heavy = 0;
@@ -29,5 +30,8 @@ struct SpmmArgs {
 
 grappa_status spmm(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grappa_dtype dt,
                    cudaStream_t s);
+// same kernel on an explicit CSR (a.n rows, a.nnz, a.rowptr, a.col, optional split rows);
+// used for the rectangular mini-batch blocks and their transposes
+grappa_status spmm_csr(grappa_ctx* ctx, SpmmArgs a, grappa_dtype dt, cudaStream_t s);
 
 }  // namespace grappa

@@ -206,3 +206,83 @@ class Trainer:
     @property
     def nnz(self):
         return int(self.col.numel())
+
+
+class MinibatchTrainer(Trainer):
+    """Isolated mini-batch training (sampling mode, config 4).
+
+    Per phase the active workers iterate in lock step over their epoch batches (S:441, S:492:
+    a worker with fewer batches cycles its own); every iteration samples the batch's blocks
+    inside the partition (grappa_sample), runs one SAGE forward/loss/backward on them
+    (grappa_minibatch_step), scales by the batch's coverage factor and all-reduces
+    (grappa_aggregate_grads_c) before the SGD step (Alg. 1)."""
+
+    def __init__(self, *args, fanouts=(15, 10, 5), batch_size=1000, sample_seed=0, **kw):
+        super().__init__(*args, **kw)
+        if self.spec.arch != "sage":
+            raise ValueError("mini-batch mode is implemented for GraphSAGE (config 4)")
+        self.fanouts = list(fanouts)
+        self.B = batch_size
+        self.sample_seed = sample_seed
+        self.batch = None
+        self.mb_ws = None
+        self.order = None
+
+    def iterations(self, part):
+        return 0 if part is None else -(-part.n_seeds // self.B)
+
+    def phase_iterations(self, part):
+        n = self.iterations(part)
+        if self.G > 1:
+            import torch.distributed as dist
+            t = torch.tensor([n], dtype=torch.int64, device=self.dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            n = int(t.item())
+        return n
+
+    def minibatch(self, part, order, it: int, nb: int):
+        """sample + forward/backward of batch (it mod nb) -> self.grad; returns the batch."""
+        from . import grappa_minibatch_step, grappa_sample, minibatch_ws_bytes
+        b = it % nb
+        seeds = order[b * self.B: min((b + 1) * self.B, order.numel())]
+        self.batch = grappa_sample(self.ctx, part, seeds, self.fanouts, self.sample_seed, self.epoch, b,
+                                   self.batch, self.stream)
+        need = minibatch_ws_bytes(self.batch, self.spec.dims_pad, self.dt)
+        if self.mb_ws is None or self.mb_ws.numel() < need:
+            self.mb_ws = torch.empty(need + need // 4, dtype=torch.uint8, device=self.dev)
+        grappa_minibatch_step(self.ctx, part, self.batch, self.spec.dims_pad, self.spec.dims[-1],
+                              self.theta, self.grad, self.mb_ws, self.loss_dev, self.dt,
+                              stream=self.stream)
+        return self.batch
+
+    def run_epoch(self, on_phase=None):
+        from . import grappa_aggregate_grads_c, grappa_epoch_seeds
+        t = 1 + self.epoch // self.rep_every
+        if t != self.t:
+            self.repartition(t)
+        for i, w, m_active in phase_plan(self.W, self.G, self.rank):
+            part = self.parts.get(w) if w is not None else None
+            nb = self.iterations(part)
+            iters = self.phase_iterations(part)
+            if part is not None:
+                if self.order is None or self.order.numel() < part.n_seeds:
+                    self.order = torch.empty(part.n_seeds, dtype=torch.int32, device=self.dev)
+                order = self.order[:part.n_seeds]
+                grappa_epoch_seeds(self.ctx, part, self.sample_seed, self.epoch, order, self.stream)
+            for it in range(iters):
+                if part is not None:
+                    bt = self.minibatch(part, order, it, nb)
+                    c = bt.factors[self.corr]
+                else:
+                    self.grad.zero_()
+                    c = 0.0
+                grappa_aggregate_grads_c(self.ctx, c, self.grad, m_active, self.lr, self.theta,
+                                         self.stream)
+                if on_phase is not None:
+                    on_phase()
+        self.epoch += 1
+
+    def _alloc(self):
+        """mini-batch mode needs no partition-sized activation buffers (per-batch workspace
+        is sized after each sample)."""
+        return None
