@@ -283,7 +283,8 @@ typedef enum {
 } grappa_kclass;
 /* Test / A-B hook (process wide): select an alternative kernel implementation so tests can
  * cross-check them.  op "gemm": 0 = auto (tcgen05 for bf16), 1 = CUDA-core kernels.
- * op "spmm": 0 = auto (row-group kernel for rows of <= 32 vectors), 1 = warp-per-row.
+ * op "spmm": 0 = auto (row-group kernel for rows of <= 32 vectors, degree-bucketed row
+ * order), 1 = warp-per-row, 2 = row-group with 8 loads in flight, 3 = row-group, natural order.
  * Returns E_ARG for an unknown op. */
 grappa_status grappa_set_kernel_variant(const char* op, int variant);
 

@@ -18,4 +18,7 @@ struct grappa_part {
     // SpMM row splitting (rows with d_l > kSegLen): every segment of a split row is one
     // "slot" task (row, segment); slot_off gives each split row's first slot.
     grappa::DevBuf heavy_rows, heavy_slot_off, slot_row, slot_seg;
+    // SpMM processing order: rows bucketed by descending local degree, so the row groups that
+    // share a warp have similar trip counts (results do not depend on the order)
+    grappa::DevBuf row_order;
 };

@@ -201,6 +201,35 @@ __global__ void k_gather_rows(int64_t n_core, int64_t row_bytes, const int32_t* 
     }
 }
 
+// Degree-bucketed SpMM row order (bucket 0 = heaviest); order inside a bucket is arbitrary
+// (it only decides which warp processes a row, never a result).
+constexpr int kDegBuckets = kSegLen + 2;
+__device__ __forceinline__ int deg_bucket(int32_t d) { return kSegLen + 1 - min(d, kSegLen + 1); }
+
+__global__ void k_deg_hist(int64_t n, const int32_t* __restrict__ d_l, unsigned long long* bins) {
+    __shared__ unsigned int sh[kDegBuckets];
+    for (int i = threadIdx.x; i < kDegBuckets; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&sh[deg_bucket(d_l[i])], 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < kDegBuckets; i += blockDim.x)
+        if (sh[i]) atomicAdd(&bins[i], (unsigned long long)sh[i]);
+}
+
+__global__ void k_deg_bins_scan(const unsigned long long* bins, unsigned long long* cursor) {
+    if (threadIdx.x == 0) {
+        unsigned long long run = 0;
+        for (int i = 0; i < kDegBuckets; i++) { cursor[i] = run; run += bins[i]; }
+    }
+}
+
+__global__ void k_deg_scatter(int64_t n, const int32_t* __restrict__ d_l, unsigned long long* cursor,
+                              int32_t* __restrict__ order) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        order[atomicAdd(&cursor[deg_bucket(d_l[i])], 1ull)] = (int32_t)i;
+}
+
 // Coverage statistics over the seeds, fixed-order block partials.
 struct SeedStats {
     double sum_r;      // sum d_l/d_g (ratio 1 where d_g = 0), R4
@@ -404,6 +433,20 @@ extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g
             (int32_t*)p->slot_row.p, (int32_t*)p->slot_seg.p);
         GRAPPA_LAUNCHED(ctx);
     }
+    // SpMM row order: counting sort by descending min(d_l, kSegLen + 1)
+    {
+        RP_TRY(p->row_order.grow((size_t)n_core * 4));
+        RP_TRY(ctx->red_ws.grow((size_t)2 * kDegBuckets * 8));
+        unsigned long long* bins = (unsigned long long*)ctx->red_ws.p;
+        GRAPPA_CUDA(cudaMemsetAsync(bins, 0, (size_t)kDegBuckets * 8, s));
+        const unsigned g2 = (unsigned)std::min<int64_t>(ceil_div(n_core, 256), (int64_t)ctx->sm_count * 8);
+        k_deg_hist<<<g2, 256, 0, s>>>(n_core, (int32_t*)p->d_l.p, bins);
+        GRAPPA_LAUNCHED(ctx);
+        k_deg_bins_scan<<<1, 32, 0, s>>>(bins, bins + kDegBuckets);
+        GRAPPA_LAUNCHED(ctx);
+        k_deg_scatter<<<g2, 256, 0, s>>>(n_core, (int32_t*)p->d_l.p, bins + kDegBuckets, (int32_t*)p->row_order.p);
+        GRAPPA_LAUNCHED(ctx);
+    }
     // publish
     grappa_part_info& I = p->info;
     I.n_core = n_core; I.nnz = nnz; I.n_seeds = n_seeds; I.base = base; I.swept = swept;
@@ -433,7 +476,7 @@ extern "C" void grappa_part_destroy(grappa_part* p) {
     if (!p) return;
     for (grappa::DevBuf* b : {&p->rowptr, &p->col, &p->core_global, &p->d_l, &p->d_g, &p->norm_gcn,
                               &p->norm_sage, &p->seeds, &p->labels, &p->x, &p->heavy_rows,
-                              &p->heavy_slot_off, &p->slot_row, &p->slot_seg})
+                              &p->heavy_slot_off, &p->slot_row, &p->slot_seg, &p->row_order})
         b->release();
     delete p;
 }

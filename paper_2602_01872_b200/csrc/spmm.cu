@@ -63,7 +63,8 @@ template <> struct Vec<__nv_bfloat16> {
 constexpr int kUnroll = 4;
 // dispatch knob (tests / A-B timing) for narrow rows: 0 = row-group kernel with 4 feature
 // loads in flight per lane (default; measured best), 1 = warp-per-row kernel, 2 = row-group
-// kernel with 8 loads in flight (more registers, fewer resident warps: slower on B200)
+// kernel with 8 loads in flight (more registers, fewer resident warps: slower on B200),
+// 3 = row-group kernel over the rows in natural order (no degree bucketing)
 static int g_spmm_variant = 0;
 void spmm_force_warp_per_row(int v) { g_spmm_variant = v; }
 
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(256) k_spmm_grp(SpmmArgs a, int G, int P) {
             orow = vrow;
             to_partial = true;
         } else if (vrow - a.n_slots < a.n) {
-            const int64_t v = vrow - a.n_slots;
+            const int64_t v = a.row_order ? (int64_t)a.row_order[vrow - a.n_slots] : vrow - a.n_slots;
             e0 = a.rowptr[v];
             e1 = a.rowptr[v + 1];
             if (e1 - e0 > kSegLen) e1 = e0;          // split row: finished by the fix-up kernel
@@ -454,6 +455,7 @@ grappa_status spmm(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grappa_
     a.slot_seg = (const int32_t*)part->slot_seg.p;
     a.heavy_rows = (const int32_t*)part->heavy_rows.p;
     a.heavy_slot_off = (const int32_t*)part->heavy_slot_off.p;
+    a.row_order = g_spmm_variant == 3 ? nullptr : (const int32_t*)part->row_order.p;
     return spmm_csr(ctx, a, dt, s);
 }
 

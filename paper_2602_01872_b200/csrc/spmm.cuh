@@ -15,6 +15,7 @@ struct SpmmArgs {
     const int32_t* slot_seg = nullptr;
     const int32_t* heavy_rows = nullptr;
     const int32_t* heavy_slot_off = nullptr;
+    const int32_t* row_order = nullptr;    // optional processing order of the rows
     // caller
     const void* X = nullptr;          // [n x width] dtype
     int width = 0;                    // elements per row (multiple of 4)

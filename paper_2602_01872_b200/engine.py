@@ -95,7 +95,10 @@ class Trainer:
         self.rowptr = as_t(rowptr, torch.int64)
         self.col = as_t(col, torch.int32)
         self.N = self.rowptr.numel() - 1
-        self.x = as_t(x, torch.float32).to(self.tdt).contiguous()
+        # features: cast to the storage dtype on the host first (papers-scale fp32 features
+        # are 57 GB; bf16 halves both the host->device copy and the transient device copy)
+        xt = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+        self.x = xt.to(self.tdt).to(self.dev).contiguous()
         self.labels = as_t(labels, torch.int32)
         self.train = as_t(train_mask, torch.uint8)
         # a1: chunk map, once
@@ -201,6 +204,33 @@ class Trainer:
             self.phase_step(i, w, m_active)
             if on_phase is not None:
                 on_phase()
+        self.epoch += 1
+
+    def run_epoch_graph(self):
+        """Same epoch, replayed from a CUDA graph captured once per super-epoch (the phase
+        loop is launch-bound on small graphs: ~60 kernels per phase).  The first call after a
+        repartition captures (nothing executes during capture) and then replays."""
+        t = 1 + self.epoch // self.rep_every
+        if t != self.t:
+            self.repartition(t)
+            self.graph = None
+        if getattr(self, "graph", None) is None:
+            torch.cuda.synchronize(self.dev)
+            g = torch.cuda.CUDAGraph()
+            main = self.stream
+            cap = torch.cuda.Stream(self.dev)
+            cap.wait_stream(main)
+            l0 = self.ctx.launches()
+            with torch.cuda.graph(g, stream=cap):
+                self.stream = cap
+                try:
+                    for i, w in self.my_workers():
+                        self.phase_step(i, w, min(self.G, self.W - i * self.G))
+                finally:
+                    self.stream = main
+            self.graph = g
+            self.graph_launches = self.ctx.launches() - l0
+        self.graph.replay()
         self.epoch += 1
 
     @property
