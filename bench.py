@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="grappa", choices=["grappa", "reference"])
     ap.add_argument("--config", default="products")
-    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--dtype", default="bf16", choices=["f32", "bf16"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--variant", action="append", default=[],
                     help="kernel A/B knob op=value (grappa_set_kernel_variant), e.g. spmm=2")
@@ -111,16 +111,23 @@ def load_peaks():
     return 6650.0, 1590.0, "fallback"
 
 
-def ncu_traffic(kernel_prefix: str):
-    """dram bytes per launch of the kernel from the committed ncu --set full summary."""
+def ncu_traffic(main_prefix: str, aux_prefix: str | None = None):
+    """DRAM bytes (read + write) per call of an op from the committed ncu --set full summary
+    (profiles/ncu_summary.json): all captured launches of the main kernel(s) plus their
+    companion kernels (e.g. the split-row fix-up), divided by the main launches."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
-    d = json.load(open(p))
-    for k, v in d.get("kernels", {}).items():
-        if k.startswith(kernel_prefix) and v.get("dram_bytes_per_launch"):
-            return v["dram_bytes_per_launch"]
-    return None
+    d = json.load(open(p)).get("kernels", {})
+    main = [v for k, v in d.items() if k.startswith(main_prefix) and v.get("dram_bytes_total")]
+    if not main:
+        return None
+    n = sum(v["launches"] for v in main)
+    tot = sum(v["dram_bytes_total"] for v in main)
+    if aux_prefix:
+        tot += sum(v["dram_bytes_total"] for k, v in d.items()
+                   if k.startswith(aux_prefix) and v.get("dram_bytes_total"))
+    return tot / n
 
 
 def build_dataset(name: str):
@@ -321,7 +328,7 @@ def run_grappa(args):
     hbm, bf16_peak, peak_kind = load_peaks()
     sp_ms, sp_n, sp_b, _ = prof["spmm"]
     achieved = (sp_b / sp_n) / (sp_ms / sp_n / 1e3) / 1e9 if sp_n else None
-    traffic = ncu_traffic("k_spmm")
+    traffic = ncu_traffic("k_spmm_grp", "k_spmm_fixup")
     rep_ms = prof["repart"][0]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": (achieved / hbm) if achieved else None,

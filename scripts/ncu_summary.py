@@ -41,6 +41,9 @@ def full(paths):
                         continue
                     rec.setdefault(w, []).append(v)
     for name, rec in out.items():
+        if "dram__bytes_read.sum" in rec:
+            rec["dram_bytes_total"] = sum(rec["dram__bytes_read.sum"]) + sum(rec.get("dram__bytes_write.sum", [0]))
+            rec["time_total_s"] = sum(rec["gpu__time_duration.sum"])
         for w in WANT:
             if w in rec:
                 rec[w] = sum(rec[w]) / len(rec[w])
