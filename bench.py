@@ -316,7 +316,7 @@ def run_grappa(args):
         launches += tr.graph_launches * args.steps
         ctx.profile(True)              # per-kernel times from one extra eager epoch
         tr.run_epoch()
-    prof = {k: ctx.profile_read(k) for k in ("spmm", "gemm", "gemm_tn", "loss", "agg", "repart")}
+    prof = {k: ctx.profile_read(k) for k in ("spmm", "gemm", "gemm_tn", "loss", "agg", "repart", "sample")}
     ctx.profile(False)
     ctx.check(stream)
     if world > 1:

@@ -279,10 +279,12 @@ typedef enum {
     GRAPPA_K_LOSS = 3,
     GRAPPA_K_AGG = 4,
     GRAPPA_K_REPART = 5,
-    GRAPPA_K_NCLASS = 6
+    GRAPPA_K_SAMPLE = 6,     /* mini-batch sampler (grappa_sample, incl. its one host sync) */
+    GRAPPA_K_NCLASS = 7
 } grappa_kclass;
 /* Test / A-B hook (process wide): select an alternative kernel implementation so tests can
- * cross-check them.  op "gemm": 0 = auto (tcgen05 for bf16), 1 = CUDA-core kernels.
+ * cross-check them.  op "gemm": 0 = auto (tcgen05 for bf16, 128x128 FFMA tiles for fp32),
+ * 1 = CUDA-core kernels for bf16, 2 = the small-tile CUDA-core kernels for both dtypes.
  * op "spmm": 0 = auto (row-group kernel for rows of <= 32 vectors, degree-bucketed row
  * order), 1 = warp-per-row, 2 = row-group with 8 loads in flight, 3 = row-group, natural order.
  * Returns E_ARG for an unknown op. */

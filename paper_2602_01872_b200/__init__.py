@@ -221,10 +221,10 @@ class Batch:
         self.h = ctypes.c_void_p()
         self.blocks = []
 
-    def refresh(self, n_layers: int):
+    def refresh(self, n_layers: int, views: bool = True):
         lib = load()
         self.blocks = []
-        for l in range(n_layers):
+        for l in range(n_layers if views else 0):
             bi = _lib.BlockInfo()
             _lib.check("grappa_batch_query", lib.grappa_batch_query(self.h, l, ctypes.byref(bi)))
             self.blocks.append(dict(
@@ -261,14 +261,14 @@ def grappa_epoch_seeds(ctx: Context, part: Part, seed: int, epoch: int, order, s
 
 
 def grappa_sample(ctx: Context, part: Part, batch, fanouts, seed: int, epoch: int, batch_index: int,
-                  out: Batch | None = None, stream=None) -> Batch:
+                  out: Batch | None = None, stream=None, views: bool = True) -> Batch:
     out = out or Batch()
     fan = (ctypes.c_int32 * len(fanouts))(*fanouts)
     _lib.check("grappa_sample", ctx.lib.grappa_sample(
         ctx.h, part.h, _lib.ptr(batch), batch.numel(), fan, len(fanouts),
         ctypes.c_uint64(seed & ((1 << 64) - 1)), epoch, batch_index, ctypes.byref(out.h),
         _lib.stream_ptr(stream)))
-    return out.refresh(len(fanouts))
+    return out.refresh(len(fanouts), views)
 
 
 def minibatch_ws_bytes(batch: Batch, dims_pad, dtype) -> int:

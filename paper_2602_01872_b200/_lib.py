@@ -27,7 +27,7 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_set_kernel_variant", "grappa_aggregate_grads_c", "grappa_epoch_seeds",
            "grappa_sample", "grappa_batch_query", "grappa_batch_factors", "grappa_batch_destroy",
            "grappa_minibatch_ws_bytes", "grappa_minibatch_step"]
-KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5}
+KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5, "sample": 6}
 
 
 class GrappaError(RuntimeError):

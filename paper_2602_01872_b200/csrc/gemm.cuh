@@ -35,7 +35,11 @@ struct GemmTNArgs {
     float* ws = nullptr;      // split-K partials
 };
 
-constexpr int kMaxSplitK = 128;
+constexpr int kMaxSplitK = 256;
+// fp32 CUDA-core kernels (gemm_f32.cu)
+bool sgemm_supported(int K1, int K2, int N);
+grappa_status sgemm_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s);
+grappa_status sgemm_tn_partials(grappa_ctx* ctx, const GemmTNArgs& g, int slabs, int64_t rps, cudaStream_t s);
 // workspace for gemm_tn (max over the SIMT and tcgen05 plans); K = K1 + K2
 size_t gemm_tn_ws_bytes(int64_t M, int K1, int K2, int N);
 

@@ -151,13 +151,22 @@ __global__ void __launch_bounds__(256) k_gemm_tn(GemmTNArgs g, int64_t rows_per_
     }
 }
 
-__global__ void k_reduce_slabs(int64_t count, int slabs, const float* __restrict__ part,
-                               float* __restrict__ out) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        float s = 0.f;
-        for (int z = 0; z < slabs; z++) s += part[(int64_t)z * count + i];
-        out[i] = s;
+// out[i] = sum over slabs: block = 32 outputs x 8 slab groups, group sums added in group order
+// (fixed summation tree -> bitwise deterministic)
+__global__ void __launch_bounds__(256) k_reduce_slabs(int64_t count, int slabs, const float* __restrict__ part,
+                                                      float* __restrict__ out) {
+    __shared__ float red[8][33];
+    const int o = threadIdx.x & 31, gsl = threadIdx.x >> 5;
+    const int64_t i = (int64_t)blockIdx.x * 32 + o;
+    float s = 0.f;
+    if (i < count)
+        for (int z = gsl; z < slabs; z += 8) s += part[(int64_t)z * count + i];
+    red[gsl][o] = s;
+    __syncthreads();
+    if (gsl == 0 && i < count) {
+        float t = 0.f;
+        for (int k = 0; k < 8; k++) t += red[k][o];
+        out[i] = t;
     }
 }
 
@@ -184,6 +193,7 @@ grappa_status gemm_nn(grappa_ctx* ctx, const GemmArgs& g, grappa_dtype dt, cudaS
                  (double)g.M * K * es + K * g.N * 4.0 + (double)g.M * g.N * es * (g.mask ? 2 : 1),
                  2.0 * g.M * g.N * K);
     if (dt == GRAPPA_BF16 && !g_force_simt && gemm_tc_nn_supported(g)) return gemm_tc_nn(ctx, g, s);
+    if (dt == GRAPPA_F32 && g_force_simt != 2 && sgemm_supported(g.K1, g.K2, g.N)) return sgemm_nn(ctx, g, s);
     dim3 grid((unsigned)ceil_div(g.M, BM), (unsigned)ceil_div(g.N, BN));
     if (dt == GRAPPA_BF16) k_gemm_nn<__nv_bfloat16><<<grid, 256, 0, s>>>(g);
     else k_gemm_nn<float><<<grid, 256, 0, s>>>(g);
@@ -202,15 +212,18 @@ grappa_status gemm_tn(grappa_ctx* ctx, const GemmTNArgs& g, grappa_dtype dt, cud
     const int64_t rps = g.M > 0 ? ceil_div(g.M, slabs) : 0;
     dim3 grid((unsigned)ceil_div(K, 64), (unsigned)ceil_div(g.N, 64), (unsigned)slabs);
     if (g.M > 0) {
-        if (dt == GRAPPA_BF16) k_gemm_tn<__nv_bfloat16><<<grid, 256, 0, s>>>(g, rps, g.ws);
-        else k_gemm_tn<float><<<grid, 256, 0, s>>>(g, rps, g.ws);
-        GRAPPA_LAUNCHED(ctx);
+        if (dt == GRAPPA_F32 && g_force_simt != 2 && sgemm_supported(g.K1, g.K2, g.N)) {
+            GRAPPA_TRY(sgemm_tn_partials(ctx, g, slabs, rps, s));
+        } else {
+            if (dt == GRAPPA_BF16) k_gemm_tn<__nv_bfloat16><<<grid, 256, 0, s>>>(g, rps, g.ws);
+            else k_gemm_tn<float><<<grid, 256, 0, s>>>(g, rps, g.ws);
+            GRAPPA_LAUNCHED(ctx);
+        }
     } else {
         GRAPPA_CUDA(cudaMemsetAsync(g.ws, 0, (size_t)K * g.N * 4, s));
     }
     const int64_t count = (int64_t)K * g.N;
-    k_reduce_slabs<<<(unsigned)std::min<int64_t>(ceil_div(count, 256), 1024), 256, 0, s>>>(
-        count, g.M > 0 ? slabs : 1, g.ws, g.C);
+    k_reduce_slabs<<<(unsigned)ceil_div(count, 32), 256, 0, s>>>(count, g.M > 0 ? slabs : 1, g.ws, g.C);
     GRAPPA_LAUNCHED(ctx);
     return GRAPPA_OK;
 }

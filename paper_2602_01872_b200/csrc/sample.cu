@@ -300,6 +300,7 @@ extern "C" grappa_status grappa_sample(grappa_ctx* ctx, const grappa_part* part,
                    "grappa_sample: fanout must be in [1, %d]", kMaxFanout);
     cudaStream_t s = (cudaStream_t)stream;
     const grappa_part_info& I = part->info;
+    ProfScope ps(ctx, s, GRAPPA_K_SAMPLE, 0.0, 0.0);
     grappa_batch* b = *inout ? *inout : new grappa_batch();
     b->L = n_layers;
     b->n_batch = n_batch;

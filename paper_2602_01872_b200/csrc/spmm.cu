@@ -61,6 +61,19 @@ template <> struct Vec<__nv_bfloat16> {
 };
 
 constexpr int kUnroll = 4;
+
+// (a0, a1) += w * (x0, x1) as one packed FFMA2 (sm_100): halves the FMA issue count of the
+// gather-accumulate loop, whose instruction issue -- not DRAM -- is the limiter (ncu)
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float w, float x0, float x1) {
+    asm("{\n\t.reg .b64 a, x, ww;\n\t"
+        "mov.b64 a, {%0, %1};\n\t"
+        "mov.b64 x, {%2, %3};\n\t"
+        "mov.b64 ww, {%4, %4};\n\t"
+        "fma.rn.f32x2 a, x, ww, a;\n\t"
+        "mov.b64 {%0, %1}, a;\n\t}"
+        : "+f"(a0), "+f"(a1)
+        : "f"(x0), "f"(x1), "f"(w));
+}
 // dispatch knob (tests / A-B timing) for narrow rows: 0 = row-group kernel with 4 feature
 // loads in flight per lane (default; measured best), 1 = warp-per-row kernel, 2 = row-group
 // kernel with 8 loads in flight (more registers, fewer resident warps: slower on B200),
@@ -330,7 +343,7 @@ __global__ void __launch_bounds__(256) k_spmm_grp(SpmmArgs a, int G, int P) {
                     float f[E];
                     Vec<T>::to_f(v[u], f);
 #pragma unroll
-                    for (int q = 0; q < E; q++) acc[q] = fmaf(w[u], f[q], acc[q]);
+                    for (int q = 0; q < E; q += 2) ffma2(acc[q], acc[q + 1], w[u], f[q], f[q + 1]);
                 }
             }
         }

@@ -276,7 +276,7 @@ class MinibatchTrainer(Trainer):
         b = it % nb
         seeds = order[b * self.B: min((b + 1) * self.B, order.numel())]
         self.batch = grappa_sample(self.ctx, part, seeds, self.fanouts, self.sample_seed, self.epoch, b,
-                                   self.batch, self.stream)
+                                   self.batch, self.stream, views=False)
         need = minibatch_ws_bytes(self.batch, self.spec.dims_pad, self.dt)
         if self.mb_ws is None or self.mb_ws.numel() < need:
             self.mb_ws = torch.empty(need + need // 4, dtype=torch.uint8, device=self.dev)

@@ -284,9 +284,11 @@ def test_epoch_parity(G, ctx, prod, arxiv, which, corr, epochs, rep):
     assert err(thetas[P], Mo.flatten(final)) <= 1e-4
 
 
-@pytest.mark.parametrize("arch,op,dtype", [("gcn", "gemm", "bf16"), ("sage", "gemm", "bf16"),
-                                           ("gcn", "spmm", "bf16"), ("sage", "spmm", "f32")])
-def test_kernel_variants_agree(G, ctx, prod, arch, op, dtype):
+@pytest.mark.parametrize("arch,op,dtype,alt", [("gcn", "gemm", "bf16", 1), ("sage", "gemm", "bf16", 1),
+                                               ("gcn", "gemm", "f32", 2), ("sage", "gemm", "f32", 2),
+                                               ("gcn", "spmm", "bf16", 1), ("sage", "spmm", "f32", 1),
+                                               ("gcn", "spmm", "bf16", 3), ("gcn", "spmm", "bf16", 2)])
+def test_kernel_variants_agree(G, ctx, prod, arch, op, dtype, alt):
     """Alternative implementations agree on the same layer and inputs: bf16 tcgen05 GEMMs vs
     the CUDA-core GEMMs; the row-group SpMM vs the warp-per-row SpMM."""
     part = _part(G, ctx, prod, 8, 3, 6, dtype)
@@ -299,7 +301,7 @@ def test_kernel_variants_agree(G, ctx, prod, arch, op, dtype):
     dz = (torch.randn(n, f_out, device="cuda", generator=g) * 1e-2).to(tdt)
     outs = []
     lib = G.load()
-    for variant in (0, 1):
+    for variant in (0, alt):
         assert lib.grappa_set_kernel_variant(op.encode(), variant) == 0
         h_out = torch.empty(n, f_out, device="cuda", dtype=tdt)
         saved = torch.empty(max(1, G.layer_saved_bytes(part, arch, f_in, f_out, dtype)), dtype=torch.uint8, device="cuda")
