@@ -140,6 +140,25 @@ grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g, const voi
 grappa_status grappa_part_query(const grappa_part* part, grappa_part_info* out);
 void grappa_part_destroy(grappa_part* part);
 
+/* Host-memory image of a partition's arrays (sizes as in grappa_part_info; any field may be
+ * NULL = not transferred).  Used when partitions live in host memory between phases -- the
+ * paper keeps partitions in CPU memory and loads them to the GPU; the bench's
+ * end-to-end number streams them per phase.  Host buffers should be pinned for overlap. */
+typedef struct {
+    int64_t* rowptr;        /* [n_core+1] */
+    int32_t* col;           /* [nnz]      */
+    int32_t* d_l;           /* [n_core]   */
+    float* norm_gcn;        /* [n_core]   */
+    float* norm_sage;       /* [n_core]   */
+    int32_t* seeds;         /* [n_seeds]  */
+    int32_t* labels;        /* [n_core]   */
+    void* x;                /* [n_core x feat_dim] */
+} grappa_part_host;
+/* device -> host copy of the selected arrays (enqueued on stream) */
+grappa_status grappa_part_download(const grappa_part* part, const grappa_part_host* dst, void* stream);
+/* host -> device copy into the partition's own buffers (enqueued on stream; same sizes) */
+grappa_status grappa_part_upload(grappa_part* part, const grappa_part_host* src, void* stream);
+
 /* Workspace sizes (bytes) for one layer call on `part`; `saved` persists fwd -> bwd. */
 size_t grappa_layer_saved_bytes(const grappa_part* part, grappa_arch arch, int32_t f_in,
                                 int32_t f_out, grappa_dtype dtype);
@@ -248,14 +267,16 @@ void grappa_batch_destroy(grappa_batch* b);
  *   W_nbr); loss = mean softmax-CE over the batch seeds; grad (dev fp32, flat theta layout:
  *   per layer [W_self; W_nbr] blocks of dims_pad[l] x dims_pad[l+1]) <- dL/dtheta.
  *   dims_pad: host int32[n_layers+1] (multiples of 16; dims_pad[0] = the partition's
- *   feat_dim).  ws: grappa_minibatch_ws_bytes.  hidden_out: NULL, or host array of
- *   n_layers-1 dev pointers receiving h_1..h_{L-1} (rows n_dst of layers 0..L-2) for tests. */
+ *   feat_dim).  ws: ws_bytes >= grappa_minibatch_ws_bytes(b, ...) (E_ARG otherwise: the
+ *   workspace depends on the sampled sizes of THIS batch).  hidden_out: NULL, or host array
+ *   of n_layers-1 dev pointers receiving h_1..h_{L-1} (rows n_dst of layers 0..L-2). */
 size_t grappa_minibatch_ws_bytes(const grappa_batch* b, int32_t n_layers, const int32_t* dims_pad,
                                  grappa_dtype dtype);
 grappa_status grappa_minibatch_step(grappa_ctx* ctx, const grappa_part* part, const grappa_batch* b,
                                     int32_t n_layers, const int32_t* dims_pad, int32_t num_classes,
-                                    const float* theta, float* grad, void* ws, double* loss_dev,
-                                    void* const* hidden_out, grappa_dtype dtype, void* stream);
+                                    const float* theta, float* grad, void* ws, size_t ws_bytes,
+                                    double* loss_dev, void* const* hidden_out, grappa_dtype dtype,
+                                    void* stream);
 
 /* Sync the stream and report asynchronous faults: E_NONFINITE if any aggregated gradient
  * since the last check was non-finite, E_CUDA / E_NCCL on device or communicator errors. */
@@ -287,6 +308,9 @@ typedef enum {
  * 1 = CUDA-core kernels for bf16, 2 = the small-tile CUDA-core kernels for both dtypes.
  * op "spmm": 0 = auto (row-group kernel for rows of <= 32 vectors, degree-bucketed row
  * order), 1 = warp-per-row, 2 = row-group with 8 loads in flight, 3 = row-group, natural order.
+ * op "fuse": 0 = off (default), 1 = bf16 GCN layers run the fused aggregate->transform kernel
+ * (SpMM gather into a shared-memory tile + tcgen05 transform in the same kernel) where the
+ * aggregate is the narrower side.
  * Returns E_ARG for an unknown op. */
 grappa_status grappa_set_kernel_variant(const char* op, int variant);
 

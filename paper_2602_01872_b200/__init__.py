@@ -131,6 +131,26 @@ class Part:
             self.x = None
         return self
 
+    def host_image(self):
+        """Pinned host buffers for this partition's arrays (grappa_part_host) + the struct."""
+        I = self.info
+        tdt = torch.bfloat16 if I.dtype == BF16 else torch.float32
+        pin = lambda n, dt: torch.empty(n, dtype=dt, pin_memory=True)
+        bufs = dict(rowptr=pin(I.n_core + 1, torch.int64), col=pin(I.nnz, torch.int32),
+                    d_l=pin(I.n_core, torch.int32), norm_gcn=pin(I.n_core, torch.float32),
+                    norm_sage=pin(I.n_core, torch.float32), seeds=pin(I.n_seeds, torch.int32),
+                    labels=pin(I.n_core, torch.int32), x=pin(I.n_core * I.feat_dim, tdt))
+        st = _lib.PartHost(**{k: v.data_ptr() for k, v in bufs.items()})
+        return bufs, st
+
+    def download(self, st, stream=None):
+        _lib.check("grappa_part_download", load().grappa_part_download(self.h, ctypes.byref(st),
+                                                                       _lib.stream_ptr(stream)))
+
+    def upload(self, st, stream=None):
+        _lib.check("grappa_part_upload", load().grappa_part_upload(self.h, ctypes.byref(st),
+                                                                   _lib.stream_ptr(stream)))
+
     def factor(self, corr: str) -> float:
         I = self.info
         return {"none": 1.0, "uniform": I.c_uniform, "resampling": I.c_resampling,
@@ -285,4 +305,5 @@ def grappa_minibatch_step(ctx: Context, part: Part, batch: Batch, dims_pad, num_
         hid = (ctypes.c_void_p * max(1, L - 1))(*[t.data_ptr() for t in hidden_out])
     _lib.check("grappa_minibatch_step", ctx.lib.grappa_minibatch_step(
         ctx.h, part.h, batch.h, L, dp, num_classes, _lib.ptr(theta), _lib.ptr(grad), _lib.ptr(ws),
-        _lib.ptr(loss_dev), hid, dtype_code(dtype), _lib.stream_ptr(stream)))
+        ws.numel() * ws.element_size(), _lib.ptr(loss_dev), hid, dtype_code(dtype),
+        _lib.stream_ptr(stream)))

@@ -26,7 +26,8 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_check", "grappa_launch_count", "grappa_profile_enable", "grappa_profile_read",
            "grappa_set_kernel_variant", "grappa_aggregate_grads_c", "grappa_epoch_seeds",
            "grappa_sample", "grappa_batch_query", "grappa_batch_factors", "grappa_batch_destroy",
-           "grappa_minibatch_ws_bytes", "grappa_minibatch_step"]
+           "grappa_minibatch_ws_bytes", "grappa_minibatch_step", "grappa_part_download",
+           "grappa_part_upload"]
 KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5, "sample": 6}
 
 
@@ -52,6 +53,11 @@ class PartInfo(ctypes.Structure):
                 ("n_heavy", ctypes.c_int64), ("n_slots", ctypes.c_int64),
                 ("c_uniform", ctypes.c_double), ("c_resampling", ctypes.c_double),
                 ("c_resampling_hm", ctypes.c_double), ("D", ctypes.c_int64)]
+
+
+class PartHost(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in
+                ("rowptr", "col", "d_l", "norm_gcn", "norm_sage", "seeds", "labels", "x")]
 
 
 class BlockInfo(ctypes.Structure):
@@ -99,6 +105,8 @@ def load(path: str = LIB_PATH):
         "grappa_launch_count": (i64, [vp]),
         "grappa_profile_enable": (st, [vp, ctypes.c_int]),
         "grappa_set_kernel_variant": (st, [ctypes.c_char_p, ctypes.c_int]),
+        "grappa_part_download": (st, [vp, ctypes.POINTER(PartHost), vp]),
+        "grappa_part_upload": (st, [vp, ctypes.POINTER(PartHost), vp]),
         "grappa_aggregate_grads_c": (st, [vp, dbl, vp, i64, i32, f32, vp, vp]),
         "grappa_epoch_seeds": (st, [vp, vp, u64, i64, vp, vp]),
         "grappa_sample": (st, [vp, vp, vp, i32, vp, i32, u64, i64, i64, ctypes.POINTER(vp), vp]),
@@ -106,7 +114,7 @@ def load(path: str = LIB_PATH):
         "grappa_batch_factors": (st, [vp, ctypes.POINTER(dbl), ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
         "grappa_batch_destroy": (None, [vp]),
         "grappa_minibatch_ws_bytes": (sz, [vp, i32, vp, ctypes.c_int]),
-        "grappa_minibatch_step": (st, [vp, vp, vp, i32, vp, i32, vp, vp, vp, vp, vp, ctypes.c_int, vp]),
+        "grappa_minibatch_step": (st, [vp, vp, vp, i32, vp, i32, vp, vp, vp, sz, vp, vp, ctypes.c_int, vp]),
         "grappa_profile_read": (st, [vp, ctypes.c_int, ctypes.POINTER(dbl), ctypes.POINTER(i64),
                                      ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
     }

@@ -151,6 +151,7 @@ extern "C" grappa_status grappa_set_kernel_variant(const char* op, int variant) 
     GRAPPA_ARG(op, GRAPPA_E_ARG, "grappa_set_kernel_variant: null op");
     if (!strcmp(op, "gemm")) { gemm_force_simt(variant); return GRAPPA_OK; }
     if (!strcmp(op, "spmm")) { spmm_force_warp_per_row(variant); return GRAPPA_OK; }
+    if (!strcmp(op, "fuse")) { spmm_set_fuse(variant); return GRAPPA_OK; }
     set_error("grappa_set_kernel_variant: unknown op '%s'", op);
     return GRAPPA_E_ARG;
 }
@@ -201,14 +202,16 @@ extern "C" size_t grappa_layer_ws_bytes(const grappa_part* part, grappa_arch arc
     size_t node = (size_t)n * (arch == GRAPPA_GCN ? f_out : f_in) * es;       // T / dT / dM
     size_t partial = (size_t)slots * wmax * 4;
     size_t splitk = gemm_tn_ws_bytes(n, f_in, arch == GRAPPA_GCN ? 0 : f_in, f_out);
+    size_t hagg = (size_t)part->info.n_heavy * wmax * es;                    // fused path
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
-    return al(node) + al(partial) + al(splitk);
+    return al(node) + al(partial) + al(splitk) + al(hagg);
 }
 
 struct WsLayout {
     void* node;
     float* partial;
     float* splitk;
+    void* hagg;
 };
 static WsLayout carve(const grappa_part* part, grappa_arch arch, int f_in, int f_out,
                       grappa_dtype dt, void* ws) {
@@ -218,8 +221,9 @@ static WsLayout carve(const grappa_part* part, grappa_arch arch, int f_in, int f
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     size_t node = al((size_t)n * (arch == GRAPPA_GCN ? f_out : f_in) * es);
     size_t partial = al((size_t)slots * wmax * 4);
+    size_t splitk = al(gemm_tn_ws_bytes(n, f_in, arch == GRAPPA_GCN ? 0 : f_in, f_out));
     char* b = (char*)ws;
-    return WsLayout{b, (float*)(b + node), (float*)(b + node + partial)};
+    return WsLayout{b, (float*)(b + node), (float*)(b + node + partial), b + node + partial + splitk};
 }
 
 static grappa_status check_dims(const char* who, int f_in, int f_out) {
@@ -238,15 +242,28 @@ extern "C" grappa_status grappa_layer_fwd(grappa_ctx* ctx, const grappa_part* pa
     cudaStream_t s = (cudaStream_t)stream;
     const grappa_part_info& I = part->info;
     WsLayout L = carve(part, arch, f_in, f_out, dtype, ws);
+    if (arch == GRAPPA_GCN && f_in <= f_out && spmm_mm_supported(part, f_in, f_out, dtype)) {
+        // h_out = act((Ahat h_in) W): aggregate at the narrower width, transform fused into
+        // the aggregation kernel (tcgen05 on the smem-resident tile)
+        AggMMArgs m;
+        m.X = h_in; m.K = f_in; m.row_scale = I.norm_gcn; m.col_scale = I.norm_gcn; m.self = 1;
+        m.W = w; m.N = f_out; m.relu = relu; m.out = h_out; m.hagg = L.hagg; m.partial = L.partial;
+        return spmm_mm(ctx, part, m, s);
+    }
     if (arch == GRAPPA_GCN) {
         // T = h_in W  (transform first: SpMM width = f_out)
         GemmArgs g;
         g.M = I.n_core; g.K1 = f_in; g.N = f_out; g.A1 = h_in; g.B = w;
         g.n_split = f_out; g.C1 = L.node;
+        // tcgen05 path: the column normalisation n_u is applied once per row in the GEMM
+        // epilogue (T' = N T), so the SpMM gathers unweighted rows (no per-edge scale load,
+        // mixed-precision adds); otherwise the SpMM weights each gathered row by n_u
+        const bool pre = gemm_nn_row_scale_ok(g, dtype);
+        if (pre) g.row_scale = I.norm_gcn;
         GRAPPA_TRY(gemm_nn(ctx, g, dtype, s));
         // h_out = act(n_v (n_v T_v + sum n_u T_u))
         SpmmArgs a;
-        a.X = L.node; a.width = f_out; a.row_scale = I.norm_gcn; a.col_scale = I.norm_gcn;
+        a.X = L.node; a.width = f_out; a.row_scale = I.norm_gcn; a.col_scale = pre ? nullptr : I.norm_gcn;
         a.self = 1; a.relu = relu; a.out = h_out; a.partial = L.partial;
         return spmm(ctx, part, a, dtype, s);
     }
@@ -272,6 +289,18 @@ extern "C" grappa_status grappa_layer_bwd(grappa_ctx* ctx, const grappa_part* pa
     cudaStream_t s = (cudaStream_t)stream;
     const grappa_part_info& I = part->info;
     WsLayout L = carve(part, arch, f_in, f_out, dtype, ws);
+    if (arch == GRAPPA_GCN && dz_in && spmm_mm_supported(part, f_out, f_in, dtype)) {
+        // dT = Ahat dz_out and dz_in = (dT W^T) * relu'(h_in) in one fused kernel, then
+        // dW = h_in^T dT
+        AggMMArgs m;
+        m.X = dz_out; m.K = f_out; m.row_scale = I.norm_gcn; m.col_scale = I.norm_gcn; m.self = 1;
+        m.W = w; m.N = f_in; m.b_trans = 1; m.mask = relu_in ? h_in : nullptr; m.out = dz_in;
+        m.agg_out = L.node; m.hagg = L.hagg; m.partial = L.partial;
+        GRAPPA_TRY(spmm_mm(ctx, part, m, s));
+        GemmTNArgs t;
+        t.M = I.n_core; t.K1 = f_in; t.N = f_out; t.A1 = h_in; t.B = L.node; t.C = dw; t.ws = L.splitk;
+        return gemm_tn(ctx, t, dtype, s);
+    }
     if (arch == GRAPPA_GCN) {
         // dT = Ahat dz_out
         SpmmArgs a;

@@ -186,11 +186,20 @@ size_t gemm_tn_ws_bytes(int64_t M, int K1, int K2, int N) {
 static int g_force_simt = 0;
 void gemm_force_simt(int on) { g_force_simt = on; }
 
+bool gemm_nn_row_scale_ok(const GemmArgs& g, grappa_dtype dt) {
+    return dt == GRAPPA_BF16 && !g_force_simt && gemm_tc_nn_supported(g);
+}
+
 grappa_status gemm_nn(grappa_ctx* ctx, const GemmArgs& g, grappa_dtype dt, cudaStream_t s) {
     if (g.M == 0) return GRAPPA_OK;
+    if (g.row_scale && !gemm_nn_row_scale_ok(g, dt)) {
+        set_error("gemm_nn: row_scale epilogue needs the tcgen05 path");
+        return GRAPPA_E_SUPPORT;
+    }
     const double es = dt == GRAPPA_BF16 ? 2.0 : 4.0, K = g.K1 + g.K2;
     ProfScope ps(ctx, s, GRAPPA_K_GEMM,
-                 (double)g.M * K * es + K * g.N * 4.0 + (double)g.M * g.N * es * (g.mask ? 2 : 1),
+                 (double)g.M * K * es + K * g.N * 4.0 + (double)g.M * g.N * es * (g.mask ? 2 : 1) +
+                     (g.row_scale ? 4.0 * g.M : 0.0),
                  2.0 * g.M * g.N * K);
     if (dt == GRAPPA_BF16 && !g_force_simt && gemm_tc_nn_supported(g)) return gemm_tc_nn(ctx, g, s);
     if (dt == GRAPPA_F32 && g_force_simt != 2 && sgemm_supported(g.K1, g.K2, g.N)) return sgemm_nn(ctx, g, s);

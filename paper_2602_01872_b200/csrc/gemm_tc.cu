@@ -26,7 +26,8 @@
 namespace grappa {
 
 constexpr int kTcThreads = 192;
-constexpr int kNNStages = 4;
+constexpr int kNNThreads = 320;          // producer, MMA, 2 x 4 epilogue warps
+constexpr int kMaxNNStages = 8;
 constexpr int kNNStageBytes = 128 * 128;    // 128 rows x 128 B
 constexpr int kBoxBytes = 128 * 128;        // one 64-column x 128-row bf16 SW128 box
 constexpr int kTNStages = 4;
@@ -39,12 +40,15 @@ struct TcNN {
     int64_t M;
     int K1, K2, N, kb1, kb2;
     const float* B;
+    const float* rs;
     int b_trans;
     int relu;
     int has_mask;
     int n_split;
     int nb1, nb2;          // 64-column output boxes of C1 / C2
     int num_tiles;
+    int stages;            // A-tile ring depth (<= kMaxNNStages)
+    int nsb;               // staging boxes per epilogue group (1 or 2)
     uint32_t tmem_cols;
 };
 
@@ -59,25 +63,119 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-__global__ void __launch_bounds__(kTcThreads, 1)
+__device__ __forceinline__ void bulk_wait_read1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void grp_bar(int h) { asm volatile("bar.sync %0, 128;" ::"r"(1 + h) : "memory"); }
+
+// Epilogue of one tile for epilogue group H (4 warps = the 4 TMEM lane quarters).  The 64-column
+// output boxes alternate between the two groups, so two groups drain one accumulator in
+// parallel.  Each group stages its boxes in its own `nsb` SW128 buffers (TMA stores).
+template <int H>
+__device__ __forceinline__ void nn_epilogue(const TcNN& p, const CUtensorMap* tmC1, const CUtensorMap* tmC2,
+                                            const __nv_bfloat16* __restrict__ mask, uint8_t* sbuf, int nsb,
+                                            uint32_t tmem_acc, uint64_t* tfull, uint32_t aphase,
+                                            int ew, int lane, int tile, bool leader, int& ob) {
+    const int r = ew * 32 + lane;                 // row within the tile
+    // relu'-mask of this thread's row for this group's C1 chunks (C1 chunk j lies in box j >> 2,
+    // owned by group (j >> 2) & 1), fetched before waiting so the latency hides under the MMAs
+    uint4 mk[8];                                  // this group's first box (C1 box H)
+    const int64_t grow = (int64_t)tile * 128 + r;
+    const bool live = grow < p.M;
+    const float rsv = (p.rs && live) ? __ldg(p.rs + grow) : 1.f;
+    const uint4* msrc = reinterpret_cast<const uint4*>(mask + (live ? grow : 0) * p.n_split);
+    if (mask && live) {
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int j = H * 4 + q;
+            if (j * 16 < p.n_split) {
+                mk[2 * q] = __ldg(msrc + 2 * j);
+                mk[2 * q + 1] = __ldg(msrc + 2 * j + 1);
+            }
+        }
+    }
+    tc::mbar_wait(tfull, aphase);
+    tc::fence_after();
+    const uint32_t tbase = tmem_acc + ((uint32_t)(ew * 32) << 16);
+    const int nbo = p.nb1 + p.nb2;
+#pragma unroll 1
+    for (int bx = H; bx < nbo; bx += 2) {
+        const bool first = bx < p.nb1;
+        const int cbase = first ? bx * 64 : (bx - p.nb1) * 64;              // column inside C1 / C2
+        const int cend = first ? min(cbase + 64, p.n_split) : min(cbase + 64, p.N - p.n_split);
+        const int coff = first ? 0 : p.n_split;                              // accumulator column
+        uint8_t* obox = sbuf + (nsb == 2 ? (ob & 1) : 0) * kBoxBytes;
+        if (leader) {
+            if (nsb == 2) bulk_wait_read1();          // the store that last used this buffer is done
+            else bulk_wait_read0();
+        }
+        grp_bar(H);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int cc = cbase + q * 16;
+            if (cc >= cend) break;
+            float v[16];
+            tc::tmem_ld16(tbase + coff + cc, v);
+            if (first && p.rs) {
+#pragma unroll
+                for (int i = 0; i < 16; i++) v[i] *= rsv;
+            }
+            if (first && mask && live) {
+                uint4 m[2];
+                if (bx == H) {                        // prefetched
+                    m[0] = mk[2 * q];
+                    m[1] = mk[2 * q + 1];
+                } else {                              // later boxes (N > 128): fetched here
+                    m[0] = __ldg(msrc + (cc >> 3));
+                    m[1] = __ldg(msrc + (cc >> 3) + 1);
+                }
+                const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(m);
+#pragma unroll
+                for (int i = 0; i < 16; i++) v[i] = __bfloat162float(mb[i]) > 0.f ? v[i] : 0.f;
+            }
+            if (first && p.relu) {
+#pragma unroll
+                for (int i = 0; i < 16; i++) v[i] = fmaxf(v[i], 0.f);
+            }
+            uint32_t o[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+                o[i] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            const int ch = (cc & 63) >> 3;            // 16-byte chunk within the 128-byte row
+            *reinterpret_cast<uint4*>(obox + tc::sw128_off(r, ch)) = make_uint4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<uint4*>(obox + tc::sw128_off(r, ch + 1)) = make_uint4(o[4], o[5], o[6], o[7]);
+        }
+        tc::fence_proxy_async();                      // staged box -> visible to the TMA engine
+        grp_bar(H);
+        if (leader) {
+            tma_store_2d(first ? tmC1 : tmC2, obox, cbase, tile * 128);
+            bulk_commit();
+        }
+        ob++;
+    }
+}
+
+__global__ void __launch_bounds__(kNNThreads, 1)
     k_gemm_tc_nn(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
                  const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmC2,
-                 const __grid_constant__ CUtensorMap tmMask, TcNN p) {
+                 const __nv_bfloat16* __restrict__ mask, TcNN p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const int kbt = p.kb1 + p.kb2;
-    const int nbo = p.nb1 + p.nb2;
+    const int stages = p.stages;
     uint8_t* sA = smem;
-    uint8_t* sB = sA + kNNStages * kNNStageBytes;
-    uint8_t* sOut = sB + (size_t)kbt * p.N * 128;                  // nbo boxes
-    uint8_t* sMask = sOut + (size_t)nbo * kBoxBytes;               // nb1 boxes if has_mask
-    uint64_t* full = (uint64_t*)(sMask + (p.has_mask ? (size_t)p.nb1 * kBoxBytes : 0));
-    uint64_t* empty = full + kNNStages;
-    uint64_t* tfull = empty + kNNStages;
+    uint8_t* sB = sA + stages * kNNStageBytes;
+    uint8_t* sOut = sB + (size_t)kbt * p.N * 128;                  // 2 groups x nsb boxes
+    uint64_t* full = (uint64_t*)(sOut + 2 * p.nsb * kBoxBytes);
+    uint64_t* empty = full + kMaxNNStages;
+    uint64_t* tfull = empty + kMaxNNStages;
     uint64_t* tempty = tfull + 2;
-    uint64_t* mfull = tempty + 2;
-    uint64_t* mempty = mfull + 1;
-    uint32_t* tmem_slot = (uint32_t*)(mempty + 1);
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     // weights -> shared memory once: bf16, K-major, SWIZZLE_128B, zero padded
@@ -100,10 +198,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             *reinterpret_cast<const uint4*>(v);
     }
     if (warp == 0 && lane == 0) {
-        for (int s = 0; s < kNNStages; s++) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
-        for (int a = 0; a < 2; a++) { tc::mbar_init(&tfull[a], 1); tc::mbar_init(&tempty[a], 4); }
-        tc::mbar_init(mfull, 1);
-        tc::mbar_init(mempty, 4);
+        for (int s = 0; s < stages; s++) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; a++) { tc::mbar_init(&tfull[a], 1); tc::mbar_init(&tempty[a], 8); }
         tc::mbar_fence_init();
         tc::tma_prefetch(&tmA1);
         if (p.kb2) tc::tma_prefetch(&tmA2);
@@ -118,22 +214,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (warp == 0) {
         if (lane == 0) {
             int stage = 0;
-            uint32_t phase = 0, mphase = 0;
+            uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-                if (p.has_mask) {           // relu'-mask tile for the epilogue, one buffer
-                    tc::mbar_wait(mempty, mphase ^ 1);
-                    tc::mbar_arrive_expect_tx(mfull, p.nb1 * kBoxBytes);
-                    for (int b = 0; b < p.nb1; b++)
-                        tc::tma_load_2d(sMask + b * kBoxBytes, &tmMask, mfull, b * 64, tile * 128);
-                    mphase ^= 1;
-                }
                 for (int kb = 0; kb < kbt; kb++) {
                     tc::mbar_wait(&empty[stage], phase ^ 1);
                     tc::mbar_arrive_expect_tx(&full[stage], kNNStageBytes);
                     const bool first = kb < p.kb1;
                     tc::tma_load_2d(sA + stage * kNNStageBytes, first ? &tmA1 : &tmA2, &full[stage],
                                     (first ? kb : kb - p.kb1) * 64, tile * 128);
-                    if (++stage == kNNStages) { stage = 0; phase ^= 1; }
+                    if (++stage == stages) { stage = 0; phase ^= 1; }
                 }
             }
         }
@@ -158,7 +247,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     tc::mma_commit(&empty[stage]);
                 }
                 __syncwarp();
-                if (++stage == kNNStages) { stage = 0; phase ^= 1; }
+                if (++stage == stages) { stage = 0; phase ^= 1; }
             }
             if (lane == 0) tc::mma_commit(&tfull[acc]);
             __syncwarp();
@@ -166,64 +255,28 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (acc == 0) aphase ^= 1;
         }
     } else {
-        const int ew = warp & 3;           // TMEM lane quarter this warp may access
-        const int r = ew * 32 + lane;      // row within the tile
-        const bool leader = (warp == 2 && lane == 0);
-        int acc = 0;
-        uint32_t aphase = 0, mphase = 0;
+        // warps 2-5 = group 0, warps 6-9 = group 1; warp & 3 = the TMEM lane quarter it may read
+        const int grp = (warp - 2) >> 2;
+        const int ew = warp & 3;
+        const bool leader = ((warp - 2) & 3) == 0 && lane == 0;
+        uint8_t* sbuf = sOut + grp * p.nsb * kBoxBytes;
+        int acc = 0, ob = 0;
+        uint32_t aphase = 0;
         for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-            tc::mbar_wait(&tfull[acc], aphase);
-            tc::fence_after();
-            if (p.has_mask) tc::mbar_wait(mfull, mphase);
-            if (leader) bulk_wait_read();      // previous tile's TMA store has read sOut
-            epi_bar();
-            const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * p.N);
-            for (int c0 = 0; c0 < p.N; c0 += 16) {
-                float v[16];
-                tc::tmem_ld16(tbase + c0, v);
-                const bool first = c0 < p.n_split;
-                const int cc = first ? c0 : c0 - p.n_split;
-                const int box = (first ? 0 : p.nb1) + (cc >> 6);
-                const int ch = (cc & 63) >> 3;     // 16-byte chunk within the 128-byte row
-                if (first && p.has_mask) {
-                    const uint8_t* mrow = sMask + (cc >> 6) * kBoxBytes;
-                    __align__(16) __nv_bfloat16 mk[16];
-                    *reinterpret_cast<uint4*>(mk) = *reinterpret_cast<const uint4*>(mrow + tc::sw128_off(r, ch));
-                    *reinterpret_cast<uint4*>(mk + 8) =
-                        *reinterpret_cast<const uint4*>(mrow + tc::sw128_off(r, ch + 1));
-#pragma unroll
-                    for (int i = 0; i < 16; i++) v[i] = __bfloat162float(mk[i]) > 0.f ? v[i] : 0.f;
-                }
-                if (first && p.relu) {
-#pragma unroll
-                    for (int i = 0; i < 16; i++) v[i] = fmaxf(v[i], 0.f);
-                }
-                __align__(16) __nv_bfloat16 o[16];
-#pragma unroll
-                for (int i = 0; i < 16; i++) o[i] = __float2bfloat16_rn(v[i]);
-                uint8_t* orow = sOut + box * kBoxBytes;
-                *reinterpret_cast<uint4*>(orow + tc::sw128_off(r, ch)) = reinterpret_cast<const uint4*>(o)[0];
-                *reinterpret_cast<uint4*>(orow + tc::sw128_off(r, ch + 1)) = reinterpret_cast<const uint4*>(o)[1];
-            }
+            const uint32_t tacc = tmem + (uint32_t)(acc * p.N);
+            if (grp == 0)
+                nn_epilogue<0>(p, &tmC1, &tmC2, mask, sbuf, p.nsb, tacc, &tfull[acc], aphase, ew, lane, tile,
+                               leader, ob);
+            else
+                nn_epilogue<1>(p, &tmC1, &tmC2, mask, sbuf, p.nsb, tacc, &tfull[acc], aphase, ew, lane, tile,
+                               leader, ob);
             tc::fence_before();
             __syncwarp();
-            if (lane == 0) {
-                tc::mbar_arrive(&tempty[acc]);
-                if (p.has_mask) tc::mbar_arrive(mempty);
-            }
-            tc::fence_proxy_async();             // staged tile -> visible to the TMA engine
-            epi_bar();
-            if (leader) {
-                for (int b = 0; b < p.nb1; b++) tma_store_2d(&tmC1, sOut + b * kBoxBytes, b * 64, tile * 128);
-                for (int b = 0; b < p.nb2; b++)
-                    tma_store_2d(&tmC2, sOut + (p.nb1 + b) * kBoxBytes, b * 64, tile * 128);
-                bulk_commit();
-            }
+            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
             acc ^= 1;
             if (acc == 0) aphase ^= 1;
-            mphase ^= 1;
         }
-        if (leader) bulk_wait_read();
+        if (leader) bulk_wait_read0();
     }
     __syncthreads();
     if (warp == 1) {
@@ -397,16 +450,27 @@ static grappa_status make_map(CUtensorMap* m, const void* ptr, int64_t rows, int
     return GRAPPA_OK;
 }
 
-static size_t nn_smem(int kbt, int N, int nb1, int nb2, bool mask) {
-    return 1024 + (size_t)kNNStages * kNNStageBytes + (size_t)kbt * N * 128 +
-           (size_t)(nb1 + nb2 + (mask ? nb1 : 0)) * kBoxBytes + 256;
+// A ring + resident weights + 2 groups x nsb staging boxes + barriers; the deepest ring
+// (<= 8 stages) and double-buffered staging when they fit
+static size_t nn_smem_of(int kbt, int N, int stages, int nsb) {
+    return 1024 + (size_t)stages * kNNStageBytes + (size_t)kbt * N * 128 + (size_t)2 * nsb * kBoxBytes + 256;
+}
+static bool nn_plan(int kbt, int N, int* stages, int* nsb) {
+    for (int b = 2; b >= 1; b--)
+        for (int st = kMaxNNStages; st >= 2; st--)
+            if (nn_smem_of(kbt, N, st, b) <= (size_t)kMaxSmem && (b == 1 || st >= 4)) {
+                *stages = st;
+                *nsb = b;
+                return true;
+            }
+    return false;
 }
 
 bool gemm_tc_nn_supported(const GemmArgs& g) {
     const int kbt = (int)(ceil_div(g.K1, 64) + ceil_div(g.K2, 64));
-    const int nb1 = (int)ceil_div(g.n_split, 64), nb2 = (int)ceil_div(g.N - g.n_split, 64);
+    int st, nsb;
     return g.N % 16 == 0 && g.N <= 256 && g.n_split % 16 == 0 && g.K1 % 8 == 0 && g.K2 % 8 == 0 &&
-           nn_smem(kbt, g.N, nb1, nb2, g.mask != nullptr) <= (size_t)kMaxSmem && g.M < (1ll << 31);
+           nn_plan(kbt, g.N, &st, &nsb) && g.M < (1ll << 31);
 }
 
 static uint32_t pow2_cols(int c) {
@@ -416,31 +480,33 @@ static uint32_t pow2_cols(int c) {
 }
 
 grappa_status gemm_tc_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s) {
-    CUtensorMap m1, m2, c1, c2, mk;
+    CUtensorMap m1, m2, c1, c2;
     GRAPPA_TRY(make_map(&m1, g.A1, g.M, g.K1, 128));
     if (g.K2 > 0) GRAPPA_TRY(make_map(&m2, g.A2, g.M, g.K2, 128));
     else m2 = m1;
     GRAPPA_TRY(make_map(&c1, g.C1, g.M, g.n_split, 128));
     if (g.N > g.n_split) GRAPPA_TRY(make_map(&c2, g.C2, g.M, g.N - g.n_split, 128));
     else c2 = c1;
-    if (g.mask) GRAPPA_TRY(make_map(&mk, g.mask, g.M, g.n_split, 128));
-    else mk = c1;
     TcNN p;
     p.M = g.M; p.K1 = g.K1; p.K2 = g.K2; p.N = g.N;
     p.kb1 = (int)ceil_div(g.K1, 64); p.kb2 = (int)ceil_div(g.K2, 64);
-    p.B = g.B; p.b_trans = g.b_trans; p.relu = g.relu;
+    p.B = g.B; p.rs = g.row_scale; p.b_trans = g.b_trans; p.relu = g.relu;
     p.has_mask = g.mask != nullptr; p.n_split = g.n_split;
     p.nb1 = (int)ceil_div(g.n_split, 64); p.nb2 = (int)ceil_div(g.N - g.n_split, 64);
     p.num_tiles = (int)ceil_div(g.M, 128);
     p.tmem_cols = pow2_cols(2 * g.N);
-    const size_t smem = nn_smem(p.kb1 + p.kb2, g.N, p.nb1, p.nb2, p.has_mask);
+    if (!nn_plan(p.kb1 + p.kb2, g.N, &p.stages, &p.nsb)) {
+        set_error("gemm_tc_nn: shape does not fit shared memory");
+        return GRAPPA_E_SUPPORT;
+    }
+    const size_t smem = nn_smem_of(p.kb1 + p.kb2, g.N, p.stages, p.nsb);
     static bool attr = false;
     if (!attr) {
         GRAPPA_CUDA(cudaFuncSetAttribute(k_gemm_tc_nn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
         attr = true;
     }
     const int grid = (int)std::min<int64_t>(p.num_tiles, ctx->sm_count);
-    k_gemm_tc_nn<<<grid, kTcThreads, smem, s>>>(m1, m2, c1, c2, mk, p);
+    k_gemm_tc_nn<<<grid, kNNThreads, smem, s>>>(m1, m2, c1, c2, (const __nv_bfloat16*)g.mask, p);
     GRAPPA_LAUNCHED(ctx);
     return GRAPPA_OK;
 }

@@ -224,10 +224,26 @@ __global__ void k_deg_bins_scan(const unsigned long long* bins, unsigned long lo
     }
 }
 
-__global__ void k_deg_scatter(int64_t n, const int32_t* __restrict__ d_l, unsigned long long* cursor,
-                              int32_t* __restrict__ order) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        order[atomicAdd(&cursor[deg_bucket(d_l[i])], 1ull)] = (int32_t)i;
+// each block owns a contiguous run of rows: counts its buckets in shared memory, reserves one
+// range per bucket with a single global atomic, then places its rows (no hot global counter)
+__global__ void k_deg_scatter(int64_t n, int64_t per_block, const int32_t* __restrict__ d_l,
+                              unsigned long long* cursor, int32_t* __restrict__ order) {
+    __shared__ unsigned int cnt[kDegBuckets];
+    __shared__ unsigned long long base[kDegBuckets];
+    const int64_t r0 = (int64_t)blockIdx.x * per_block, r1 = min(n, r0 + per_block);
+    for (int i = threadIdx.x; i < kDegBuckets; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) atomicAdd(&cnt[deg_bucket(d_l[i])], 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < kDegBuckets; i += blockDim.x) {
+        base[i] = cnt[i] ? atomicAdd(&cursor[i], (unsigned long long)cnt[i]) : 0ull;
+        cnt[i] = 0;
+    }
+    __syncthreads();
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        const int b = deg_bucket(d_l[i]);
+        order[base[b] + atomicAdd(&cnt[b], 1u)] = (int32_t)i;
+    }
 }
 
 // Coverage statistics over the seeds, fixed-order block partials.
@@ -444,7 +460,9 @@ extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g
         GRAPPA_LAUNCHED(ctx);
         k_deg_bins_scan<<<1, 32, 0, s>>>(bins, bins + kDegBuckets);
         GRAPPA_LAUNCHED(ctx);
-        k_deg_scatter<<<g2, 256, 0, s>>>(n_core, (int32_t*)p->d_l.p, bins + kDegBuckets, (int32_t*)p->row_order.p);
+        const int64_t per = 4096;
+        k_deg_scatter<<<(unsigned)ceil_div(n_core, per), 256, 0, s>>>(n_core, per, (int32_t*)p->d_l.p,
+                                                                      bins + kDegBuckets, (int32_t*)p->row_order.p);
         GRAPPA_LAUNCHED(ctx);
     }
     // publish
@@ -464,6 +482,32 @@ extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g
     *inout = p;
     return GRAPPA_OK;
 #undef RP_TRY
+}
+
+static grappa_status part_copy(const grappa_part* p, const grappa_part_host* h, bool to_host, cudaStream_t s) {
+    const grappa_part_info& I = p->info;
+    const size_t es = I.dtype == GRAPPA_BF16 ? 2 : 4;
+    struct F { void* host; void* dev; size_t bytes; } f[] = {
+        {h->rowptr, p->rowptr.p, (size_t)(I.n_core + 1) * 8}, {h->col, p->col.p, (size_t)I.nnz * 4},
+        {h->d_l, p->d_l.p, (size_t)I.n_core * 4}, {h->norm_gcn, p->norm_gcn.p, (size_t)I.n_core * 4},
+        {h->norm_sage, p->norm_sage.p, (size_t)I.n_core * 4}, {h->seeds, p->seeds.p, (size_t)I.n_seeds * 4},
+        {h->labels, p->labels.p, (size_t)I.n_core * 4}, {h->x, p->x.p, (size_t)I.n_core * I.feat_dim * es}};
+    for (const F& x : f) {
+        if (!x.host || !x.bytes) continue;
+        if (to_host) GRAPPA_CUDA(cudaMemcpyAsync(x.host, x.dev, x.bytes, cudaMemcpyDeviceToHost, s));
+        else GRAPPA_CUDA(cudaMemcpyAsync(x.dev, x.host, x.bytes, cudaMemcpyHostToDevice, s));
+    }
+    return GRAPPA_OK;
+}
+
+extern "C" grappa_status grappa_part_download(const grappa_part* part, const grappa_part_host* dst, void* stream) {
+    GRAPPA_ARG(part && dst, GRAPPA_E_ARG, "grappa_part_download: null argument");
+    return part_copy(part, dst, true, (cudaStream_t)stream);
+}
+
+extern "C" grappa_status grappa_part_upload(grappa_part* part, const grappa_part_host* src, void* stream) {
+    GRAPPA_ARG(part && src, GRAPPA_E_ARG, "grappa_part_upload: null argument");
+    return part_copy(part, src, false, (cudaStream_t)stream);
 }
 
 extern "C" grappa_status grappa_part_query(const grappa_part* part, grappa_part_info* out) {

@@ -46,10 +46,14 @@ __device__ __forceinline__ bool key_lt(uint64_t ak, int32_t ag, uint64_t bk, int
     return ak < bk || (ak == bk && ag < bg);
 }
 
+// targets with more local neighbours than this go to the block-per-target threshold kernel
+constexpr int kHeavyPick = 1024;
+constexpr int kCandCap = 1024;
+
 __global__ void k_pick(const int64_t* __restrict__ d_nt, const int32_t* __restrict__ targets,
                        const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                        const int32_t* __restrict__ gid, int f, uint64_t key0, int32_t* __restrict__ picks,
-                       int32_t* __restrict__ cnt) {
+                       int32_t* __restrict__ cnt, int32_t* __restrict__ heavy_n, int64_t* __restrict__ heavy_q) {
     const int lane = threadIdx.x & 31;
     const int64_t nt = *d_nt;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -61,6 +65,10 @@ __global__ void k_pick(const int64_t* __restrict__ d_nt, const int32_t* __restri
         if (d <= f) {
             for (int i = lane; i < d; i += 32) out[i] = col[e0 + i];
             if (lane == 0) cnt[t] = d;
+            continue;
+        }
+        if (d > kHeavyPick) {                       // hub: handled by k_pick_heavy
+            if (lane == 0) heavy_q[atomicAdd(heavy_n, 1)] = t;
             continue;
         }
         // per-lane sorted list of its f smallest keys (f <= 16), unrolled insertion
@@ -107,6 +115,85 @@ __global__ void k_pick(const int64_t* __restrict__ d_nt, const int32_t* __restri
             if (mine) head++;
         }
         if (lane == 0) cnt[t] = f;
+    }
+}
+
+// Hub targets (d_l > kHeavyPick), one block each.  Keys are uniform 64-bit hashes, so the
+// f smallest lie below T ~ 4f/d * 2^64 with overwhelming probability; the block counts the
+// keys under T (doubling / halving T until f <= count <= kCandCap -- exact either way), gathers
+// those candidates into shared memory and takes the f smallest (key, gid) by f warp arg-min
+// rounds.  The queue order of hubs is irrelevant: each writes only its own output slot.
+__global__ void __launch_bounds__(256) k_pick_heavy(const int32_t* __restrict__ heavy_n,
+                                                    const int64_t* __restrict__ heavy_q,
+                                                    const int32_t* __restrict__ targets,
+                                                    const int64_t* __restrict__ rowptr,
+                                                    const int32_t* __restrict__ col, const int32_t* __restrict__ gid,
+                                                    int f, uint64_t key0, int32_t* __restrict__ picks,
+                                                    int32_t* __restrict__ cnt) {
+    __shared__ uint64_t ck[kCandCap];
+    __shared__ int32_t cg[kCandCap], cu[kCandCap];
+    __shared__ int ncand, wsum[8];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int nq = *heavy_n;
+    for (int q = blockIdx.x; q < nq; q += gridDim.x) {
+        const int64_t t = heavy_q[q];
+        const int32_t v = targets[t];
+        const int64_t e0 = rowptr[v];
+        const int d = (int)(rowptr[v + 1] - e0);
+        const double frac = 4.0 * f / d;
+        uint64_t T = frac >= 1.0 ? ~0ull : (uint64_t)(frac * 18446744073709551616.0);
+        for (;;) {
+            int c = 0;
+            for (int i = tid; i < d; i += 256) {
+                const uint64_t k = smix(key0 ^ smix((uint64_t)gid[v] ^ smix((uint64_t)gid[col[e0 + i]])));
+                c += k < T;
+            }
+            c = warp_sum(c);
+            if (lane == 0) wsum[w] = c;
+            __syncthreads();
+            int tot = 0;
+            for (int k = 0; k < 8; k++) tot += wsum[k];
+            __syncthreads();
+            if (tot >= f && tot <= kCandCap) break;
+            if (tot < f) T = T > (~0ull >> 1) ? ~0ull : T << 1;
+            else T >>= 1;
+        }
+        if (tid == 0) ncand = 0;
+        __syncthreads();
+        for (int i = tid; i < d; i += 256) {
+            const int32_t u = col[e0 + i];
+            const int32_t gu = gid[u];
+            const uint64_t k = smix(key0 ^ smix((uint64_t)gid[v] ^ smix((uint64_t)gu)));
+            if (k < T) {
+                const int p = atomicAdd(&ncand, 1);
+                ck[p] = k; cg[p] = gu; cu[p] = u;
+            }
+        }
+        __syncthreads();
+        if (w == 0) {
+            const int n = ncand;
+            uint64_t lk = 0;
+            int32_t lg = -1;                       // last selected (exclusive lower bound)
+            for (int r = 0; r < f; r++) {
+                uint64_t bk = ~0ull;
+                int32_t bg = 0x7fffffff, bu = -1;
+                for (int j = lane; j < n; j += 32) {
+                    const bool above = r == 0 || key_lt(lk, lg, ck[j], cg[j]);
+                    if (above && key_lt(ck[j], cg[j], bk, bg)) { bk = ck[j]; bg = cg[j]; bu = cu[j]; }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
+                    const int32_t og = __shfl_xor_sync(0xffffffffu, bg, o);
+                    const int32_t ou = __shfl_xor_sync(0xffffffffu, bu, o);
+                    if (key_lt(ok, og, bk, bg)) { bk = ok; bg = og; bu = ou; }
+                }
+                if (lane == 0) picks[t * f + r] = bu;
+                lk = bk; lg = bg;
+            }
+            if (lane == 0) cnt[t] = f;
+        }
+        __syncthreads();
     }
 }
 
@@ -253,7 +340,7 @@ struct grappa_batch {
     int L = 0;
     int32_t n_batch = 0;
     BlockBufs blk[kMaxLayers];
-    DevBuf picks, cnt, bitmap, where, erow, key_pad, skeys, svals, sort_tmp, counts;
+    DevBuf picks, cnt, bitmap, where, erow, key_pad, skeys, svals, sort_tmp, counts, heavy_q;
     double c_uniform = 1, c_resampling = 1, c_hm = 1;
 };
 
@@ -340,8 +427,15 @@ extern "C" grappa_status grappa_sample(grappa_ctx* ctx, const grappa_part* part,
         const uint64_t key0 = hmix(seed ^ hmix((uint64_t)epoch ^ hmix((uint64_t)batch_index ^ hmix((uint64_t)h))));
         const unsigned wgrid = (unsigned)std::min<int64_t>(ceil_div(cap_t, 8), (int64_t)ctx->sm_count * 16);
         const unsigned tgrid = (unsigned)std::min<int64_t>(ceil_div(cap_nnz, 256), (int64_t)ctx->sm_count * 16);
+        GRAPPA_TRY(b->heavy_q.grow((size_t)cap_t * 8));
+        int32_t* heavy_n = (int32_t*)(dstat + 1);
+        GRAPPA_CUDA(cudaMemsetAsync(heavy_n, 0, sizeof(int32_t), s));
         k_pick<<<wgrid, 256, 0, s>>>(d_nt, targets, I.rowptr, I.col, I.core_global, f, key0,
-                                     (int32_t*)b->picks.p, (int32_t*)b->cnt.p);
+                                     (int32_t*)b->picks.p, (int32_t*)b->cnt.p, heavy_n, (int64_t*)b->heavy_q.p);
+        GRAPPA_LAUNCHED(ctx);
+        k_pick_heavy<<<(unsigned)std::min<int64_t>(cap_t, (int64_t)ctx->sm_count * 4), 256, 0, s>>>(
+            heavy_n, (int64_t*)b->heavy_q.p, targets, I.rowptr, I.col, I.core_global, f, key0,
+            (int32_t*)b->picks.p, (int32_t*)b->cnt.p);
         GRAPPA_LAUNCHED(ctx);
         GRAPPA_CUDA(cudaMemsetAsync(b->bitmap.p, 0, (size_t)nwords * 4, s));
         k_mark<<<tgrid, 256, 0, s>>>(d_nt, (int32_t*)b->picks.p, (int32_t*)b->cnt.p, f, (uint32_t*)b->bitmap.p);
@@ -415,7 +509,7 @@ extern "C" void grappa_batch_destroy(grappa_batch* b) {
                           &b->blk[l].inv_cnt, &b->blk[l].src})
             d->release();
     for (DevBuf* d : {&b->picks, &b->cnt, &b->bitmap, &b->where, &b->erow, &b->key_pad, &b->skeys,
-                      &b->svals, &b->sort_tmp, &b->counts})
+                      &b->svals, &b->sort_tmp, &b->counts, &b->heavy_q})
         d->release();
     delete b;
 }
@@ -458,8 +552,9 @@ extern "C" size_t grappa_minibatch_ws_bytes(const grappa_batch* b, int32_t L, co
 
 extern "C" grappa_status grappa_minibatch_step(grappa_ctx* ctx, const grappa_part* part, const grappa_batch* b,
                                                int32_t L, const int32_t* dp, int32_t num_classes,
-                                               const float* theta, float* grad, void* ws, double* loss_dev,
-                                               void* const* hidden_out, grappa_dtype dt, void* stream) {
+                                               const float* theta, float* grad, void* ws, size_t ws_bytes,
+                                               double* loss_dev, void* const* hidden_out, grappa_dtype dt,
+                                               void* stream) {
     GRAPPA_ARG(ctx && part && b && dp && theta && grad && ws && loss_dev, GRAPPA_E_ARG,
                "grappa_minibatch_step: null argument");
     GRAPPA_ARG(L == b->L, GRAPPA_E_ARG, "grappa_minibatch_step: n_layers %d != sampled %d", L, b->L);
@@ -471,6 +566,8 @@ extern "C" grappa_status grappa_minibatch_step(grappa_ctx* ctx, const grappa_par
     cudaStream_t s = (cudaStream_t)stream;
     const size_t es = dt == GRAPPA_BF16 ? 2 : 4;
     const StepLayout lay = step_layout(b, L, dp, dt);
+    GRAPPA_ARG(ws_bytes >= lay.total, GRAPPA_E_ARG,
+               "grappa_minibatch_step: workspace %zu B < %zu B needed by this batch", ws_bytes, lay.total);
     char* w = (char*)ws;
     // h_0 = features of the outermost sources
     const BlockBufs& B0 = b->blk[0];

@@ -33,6 +33,8 @@ ctx.profile(True)
 for it in range(5, 25):
     seeds = order[it*1000:(it+1)*1000]
     b = G.grappa_sample(ctx, p, seeds, [15,10,5], 5, 0, it, tr.batch, views=False); tr.batch = b
+    need = G.minibatch_ws_bytes(b, spec.dims_pad, "bf16")
+    if tr.mb_ws.numel() < need: tr.mb_ws = torch.empty(need, dtype=torch.uint8, device="cuda")
     G.grappa_minibatch_step(ctx, p, b, spec.dims_pad, wl.K, tr.theta, tr.grad, tr.mb_ws, tr.loss_dev, "bf16")
 torch.cuda.synchronize()
 for k in ("sample","spmm","gemm","gemm_tn","loss"):

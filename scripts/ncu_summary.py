@@ -1,7 +1,9 @@
 """Summarise ncu output for profiles/: per-kernel dram bytes / duration / throughput from a
 `--set full` report, and per-kernel time shares from a `--metrics gpu__time_duration.sum`
 launch list.  Usage:
-  python scripts/ncu_summary.py full  <report.ncu-rep> [<report2> ...] > profiles/ncu_summary.json
+  python scripts/ncu_summary.py full  <report.ncu-rep> [<report2> ...] [--calls calls.json] > profiles/ncu_summary.json
+    (--calls: the JSON scripts/ncu_phase.py prints for the captured window; adds "per_call",
+     DRAM bytes per LOGICAL call of each kernel class -- the unit bench.py's roofline uses)
   python scripts/ncu_summary.py launches <launches.csv> > profiles/<round>_launches.txt
 """
 import collections
@@ -21,7 +23,18 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"]
 
 
+# kernel-name prefixes of each profiled class (a logical call = all of its launches)
+CLASS_PREFIX = {"spmm": ("k_spmm",), "gemm": ("k_gemm_tc_nn", "k_sgemm_nn", "k_gemm_nn"),
+                "gemm_tn": ("k_gemm_tc_tn", "k_tn_reduce", "k_sgemm_tn", "k_gemm_tn", "k_reduce_slabs"),
+                "loss": ("k_loss",), "agg": ("k_scale_grad", "k_sgd")}
+
+
 def full(paths):
+    calls = None
+    if "--calls" in paths:
+        i = paths.index("--calls")
+        calls = json.load(open(paths[i + 1]))
+        paths = paths[:i] + paths[i + 2:]
     out = {}
     for p in paths:
         raw = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv"], capture_output=True,
@@ -50,7 +63,21 @@ def full(paths):
         if "dram__bytes_read.sum" in rec:
             rec["dram_bytes_per_launch"] = rec["dram__bytes_read.sum"] + rec.get("dram__bytes_write.sum", 0)
             rec["dram_GBps"] = rec["dram_bytes_per_launch"] / rec["gpu__time_duration.sum"] / 1e9
-    json.dump({"kernels": out}, sys.stdout, indent=1)
+    res = {"kernels": out}
+    if calls:
+        per = {}
+        for cls, pref in CLASS_PREFIX.items():
+            n = calls["logical_calls"].get(cls, 0)
+            ks = [k for k in out if k.startswith(pref) and "dram_bytes_total" in out[k]]
+            if not n or not ks:
+                continue
+            per[cls] = {"logical_calls": n, "kernels": ks,
+                        "dram_bytes_per_call": sum(out[k]["dram_bytes_total"] for k in ks) / n,
+                        "algorithmic_bytes_per_call": calls["algorithmic_bytes"][cls] / n,
+                        "ncu_time_per_call_s": sum(out[k]["time_total_s"] for k in ks) / n}
+        res["window"] = {k: calls[k] for k in ("config", "dtype", "worker")}
+        res["per_call"] = per
+    json.dump(res, sys.stdout, indent=1)
 
 
 def launches(path):

@@ -145,7 +145,8 @@ def _np(t):
 
 
 @pytest.mark.parametrize("arch", ["gcn", "sage"])
-@pytest.mark.parametrize("f_in,f_out", [(112, 128), (128, 48), (128, 16), (16, 128)])
+@pytest.mark.parametrize("f_in,f_out", [(112, 128), (128, 48), (128, 16), (16, 128), (256, 256),
+                                         (112, 256), (256, 48)])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_layer_parity(G, ctx, prod, arch, f_in, f_out, dtype):
     """Layer-local parity: the oracle sees the GPU's own (upcast) layer inputs."""
@@ -287,12 +288,14 @@ def test_epoch_parity(G, ctx, prod, arxiv, which, corr, epochs, rep):
 @pytest.mark.parametrize("arch,op,dtype,alt", [("gcn", "gemm", "bf16", 1), ("sage", "gemm", "bf16", 1),
                                                ("gcn", "gemm", "f32", 2), ("sage", "gemm", "f32", 2),
                                                ("gcn", "spmm", "bf16", 1), ("sage", "spmm", "f32", 1),
-                                               ("gcn", "spmm", "bf16", 3), ("gcn", "spmm", "bf16", 2)])
+                                               ("gcn", "spmm", "bf16", 3), ("gcn", "spmm", "bf16", 2),
+                                               ("gcn", "fuse", "bf16", 1)])
 def test_kernel_variants_agree(G, ctx, prod, arch, op, dtype, alt):
     """Alternative implementations agree on the same layer and inputs: bf16 tcgen05 GEMMs vs
-    the CUDA-core GEMMs; the row-group SpMM vs the warp-per-row SpMM."""
+    the CUDA-core GEMMs; the row-group SpMM vs the warp-per-row SpMM; the fused
+    aggregate->transform kernel vs SpMM + GEMM."""
     part = _part(G, ctx, prod, 8, 3, 6, dtype)
-    n, f_in, f_out = part.n_core, 112, 48
+    n, f_in, f_out = part.n_core, 112, (256 if op == "fuse" else 48)
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     g = torch.Generator(device="cuda").manual_seed(7)
     h_in = torch.randn(n, f_in, device="cuda", generator=g).relu().to(tdt)
