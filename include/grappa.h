@@ -167,9 +167,10 @@ size_t grappa_layer_ws_bytes(const grappa_part* part, grappa_arch arch, int32_t 
 
 /* a4 -- one isolated message-passing layer, forward (§3.2; §5.1):
  *   GCN  (R5):  h_out = act( Ahat h_in W ),  Ahat = Dt^-1/2 (A_loc + I) Dt^-1/2,
- *                      Dt = d_l + 1; computed transform-first: T = h_in W (tensor-core
- *                      GEMM), then h_out_v = act(n_v (n_v T_v + sum_{u in N_loc(v)} n_u T_u))
- *                      (SpMM).  `saved` unused (may be NULL).
+ *                      Dt = d_l + 1; computed transform-first: T' = N h_in W (tensor-core
+ *                      GEMM, row scale n_v = Dt^-1/2 in its epilogue), then
+ *                      h_out_v = act(n_v (T'_v + sum_{u in N_loc(v)} T'_u)) (SpMM).
+ *                      `saved` unused (may be NULL).
  *   SAGE (R6):  M = D_l^-1 A_loc h_in (SpMM, zero rows where d_l = 0, kept in
  *                      `saved`), h_out = act([h_in | M] [W_self; W_nbr]) (one GEMM, K = 2 f_in).
  *   act = ReLU if relu != 0 else identity (output layer).
@@ -194,6 +195,21 @@ grappa_status grappa_layer_bwd(grappa_ctx* ctx, const grappa_part* part, grappa_
                                int32_t f_in, int32_t f_out, int relu_in, const void* dz_out,
                                const void* h_in, const float* w, const void* saved, float* dw,
                                void* dz_in, void* ws, grappa_dtype dtype, void* stream);
+
+/* grappa_layer_bwd with normalised-gradient flags (GCN only; reading R29).  With
+ * N = diag(norm_gcn), Ahat dz = N (A_loc + I) (N dz): a caller that chains GCN layers can pass
+ * gradients pre-multiplied by N, so every backward aggregation gathers unweighted rows.
+ *   GRAPPA_BWD_DZ_OUT_NORMED : dz_out holds N dz_out.
+ *   GRAPPA_BWD_DZ_IN_NORMED  : dz_in receives N dz_in (the relu' gate is applied as usual).
+ * dw is the same in every mode.  flags = 0 is grappa_layer_bwd.  Errors: E_ARG for unknown
+ * flags or flags != 0 with arch SAGE. */
+#define GRAPPA_BWD_DZ_OUT_NORMED 1u
+#define GRAPPA_BWD_DZ_IN_NORMED 2u
+grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part* part, grappa_arch arch,
+                                  int32_t f_in, int32_t f_out, int relu_in, const void* dz_out,
+                                  const void* h_in, const float* w, const void* saved, float* dw,
+                                  void* dz_in, void* ws, grappa_dtype dtype, unsigned flags,
+                                  void* stream);
 
 /* a5 -- mean softmax cross-entropy over the partition's seeds (R8):
  *   L = (1/#S) sum_{v in S} [logsumexp(Z_v[0:K]) - Z_v[y_v]];  dZ_v = (softmax - e_y)/#S on
@@ -311,6 +327,7 @@ typedef enum {
  * op "fuse": 0 = off (default), 1 = bf16 GCN layers run the fused aggregate->transform kernel
  * (SpMM gather into a shared-memory tile + tcgen05 transform in the same kernel) where the
  * aggregate is the narrower side.
+ * op "wide": 0 = unweighted bf16 gathers use 16-byte lanes (default), 1 = 32-byte lanes.
  * Returns E_ARG for an unknown op. */
 grappa_status grappa_set_kernel_variant(const char* op, int variant);
 

@@ -13,10 +13,10 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import BF16, CORR, F32, GCN, SAGE, GrappaError, load
+from ._lib import BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, CORR, F32, GCN, SAGE, GrappaError, load
 
 __all__ = ["Context", "Part", "grappa_partition", "grappa_repartition", "grappa_layer_fwd",
-           "grappa_layer_bwd", "grappa_loss", "grappa_aggregate_grads", "GCN", "SAGE", "F32",
+           "grappa_layer_bwd", "grappa_layer_bwd_ex", "grappa_loss", "grappa_aggregate_grads", "GCN", "SAGE", "F32",
            "BF16", "CORR", "GrappaError", "load"]
 
 _TORCH_DT = {F32: torch.float32, BF16: torch.bfloat16}
@@ -211,6 +211,14 @@ def grappa_layer_bwd(ctx: Context, part: Part, arch, f_in, f_out, relu_in, dz_ou
         ctx.h, part.h, arch_code(arch), f_in, f_out, int(relu_in), _lib.ptr(dz_out), _lib.ptr(h_in),
         _lib.ptr(w), _lib.ptr(saved), _lib.ptr(dw), _lib.ptr(dz_in), _lib.ptr(ws), dtype_code(dtype),
         _lib.stream_ptr(stream)))
+
+
+def grappa_layer_bwd_ex(ctx: Context, part: Part, arch, f_in, f_out, relu_in, dz_out, h_in, w, saved,
+                        dw, dz_in, ws, dtype, flags: int, stream=None):
+    _lib.check("grappa_layer_bwd_ex", ctx.lib.grappa_layer_bwd_ex(
+        ctx.h, part.h, arch_code(arch), f_in, f_out, int(relu_in), _lib.ptr(dz_out), _lib.ptr(h_in),
+        _lib.ptr(w), _lib.ptr(saved), _lib.ptr(dw), _lib.ptr(dz_in), _lib.ptr(ws), dtype_code(dtype),
+        int(flags), _lib.stream_ptr(stream)))
 
 
 def grappa_loss(ctx: Context, part: Part, logits, num_classes, k_pad, dlogits, loss_dev, dtype,

@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libgrappa.so")
 F32, BF16 = 0, 1
 GCN, SAGE = 0, 1
 CORR = {"none": 0, "uniform": 1, "resampling": 2, "resampling_hm": 3}
+BWD_DZ_OUT_NORMED, BWD_DZ_IN_NORMED = 1, 2
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_EMPTY", 4: "E_NONFINITE", 5: "E_SUPPORT",
           6: "E_NOMEM", 7: "E_CUDA", 8: "E_NCCL"}
 
@@ -27,7 +28,7 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_set_kernel_variant", "grappa_aggregate_grads_c", "grappa_epoch_seeds",
            "grappa_sample", "grappa_batch_query", "grappa_batch_factors", "grappa_batch_destroy",
            "grappa_minibatch_ws_bytes", "grappa_minibatch_step", "grappa_part_download",
-           "grappa_part_upload"]
+           "grappa_part_upload", "grappa_layer_bwd_ex"]
 KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5, "sample": 6}
 
 
@@ -99,6 +100,8 @@ def load(path: str = LIB_PATH):
                                   ctypes.c_int, vp]),
         "grappa_layer_bwd": (st, [vp, vp, ctypes.c_int, i32, i32, ctypes.c_int, vp, vp, vp, vp, vp,
                                   vp, vp, ctypes.c_int, vp]),
+        "grappa_layer_bwd_ex": (st, [vp, vp, ctypes.c_int, i32, i32, ctypes.c_int, vp, vp, vp, vp, vp,
+                                     vp, vp, ctypes.c_int, ctypes.c_uint, vp]),
         "grappa_loss": (st, [vp, vp, vp, i32, i32, vp, vp, ctypes.c_int, vp]),
         "grappa_aggregate_grads": (st, [vp, vp, ctypes.c_int, vp, i64, i32, f32, vp, vp]),
         "grappa_check": (st, [vp, vp]),

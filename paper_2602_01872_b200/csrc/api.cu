@@ -152,6 +152,7 @@ extern "C" grappa_status grappa_set_kernel_variant(const char* op, int variant) 
     if (!strcmp(op, "gemm")) { gemm_force_simt(variant); return GRAPPA_OK; }
     if (!strcmp(op, "spmm")) { spmm_force_warp_per_row(variant); return GRAPPA_OK; }
     if (!strcmp(op, "fuse")) { spmm_set_fuse(variant); return GRAPPA_OK; }
+    if (!strcmp(op, "wide")) { spmm_set_wide(variant); return GRAPPA_OK; }
     set_error("grappa_set_kernel_variant: unknown op '%s'", op);
     return GRAPPA_E_ARG;
 }
@@ -255,15 +256,13 @@ extern "C" grappa_status grappa_layer_fwd(grappa_ctx* ctx, const grappa_part* pa
         GemmArgs g;
         g.M = I.n_core; g.K1 = f_in; g.N = f_out; g.A1 = h_in; g.B = w;
         g.n_split = f_out; g.C1 = L.node;
-        // tcgen05 path: the column normalisation n_u is applied once per row in the GEMM
-        // epilogue (T' = N T), so the SpMM gathers unweighted rows (no per-edge scale load,
-        // mixed-precision adds); otherwise the SpMM weights each gathered row by n_u
-        const bool pre = gemm_nn_row_scale_ok(g, dtype);
-        if (pre) g.row_scale = I.norm_gcn;
+        // the column normalisation n_u is applied once per row in the GEMM epilogue
+        // (T' = N T), so the SpMM gathers unweighted rows (no per-edge scale load)
+        g.row_scale = I.norm_gcn;
         GRAPPA_TRY(gemm_nn(ctx, g, dtype, s));
-        // h_out = act(n_v (n_v T_v + sum n_u T_u))
+        // h_out = act(n_v (T'_v + sum T'_u)) = act(n_v (n_v T_v + sum n_u T_u))
         SpmmArgs a;
-        a.X = L.node; a.width = f_out; a.row_scale = I.norm_gcn; a.col_scale = pre ? nullptr : I.norm_gcn;
+        a.X = L.node; a.width = f_out; a.row_scale = I.norm_gcn; a.col_scale = nullptr;
         a.self = 1; a.relu = relu; a.out = h_out; a.partial = L.partial;
         return spmm(ctx, part, a, dtype, s);
     }
@@ -282,6 +281,18 @@ extern "C" grappa_status grappa_layer_bwd(grappa_ctx* ctx, const grappa_part* pa
                                           const void* h_in, const float* w, const void* saved,
                                           float* dw, void* dz_in, void* ws, grappa_dtype dtype,
                                           void* stream) {
+    return grappa_layer_bwd_ex(ctx, part, arch, f_in, f_out, relu_in, dz_out, h_in, w, saved, dw, dz_in,
+                               ws, dtype, 0u, stream);
+}
+
+extern "C" grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part* part, grappa_arch arch,
+                                             int32_t f_in, int32_t f_out, int relu_in, const void* dz_out,
+                                             const void* h_in, const float* w, const void* saved,
+                                             float* dw, void* dz_in, void* ws, grappa_dtype dtype,
+                                             unsigned flags, void* stream) {
+    GRAPPA_ARG((flags & ~3u) == 0 && (flags == 0 || arch == GRAPPA_GCN), GRAPPA_E_ARG,
+               "grappa_layer_bwd_ex: flags 0x%x invalid (normalised gradients are GCN-only)", flags);
+    const bool out_normed = flags & GRAPPA_BWD_DZ_OUT_NORMED, in_normed = flags & GRAPPA_BWD_DZ_IN_NORMED;
     GRAPPA_ARG(ctx && part && dz_out && h_in && w && dw && ws, GRAPPA_E_ARG,
                "grappa_layer_bwd: null argument");
     GRAPPA_TRY(check_dims("grappa_layer_bwd", f_in, f_out));
@@ -289,7 +300,7 @@ extern "C" grappa_status grappa_layer_bwd(grappa_ctx* ctx, const grappa_part* pa
     cudaStream_t s = (cudaStream_t)stream;
     const grappa_part_info& I = part->info;
     WsLayout L = carve(part, arch, f_in, f_out, dtype, ws);
-    if (arch == GRAPPA_GCN && dz_in && spmm_mm_supported(part, f_out, f_in, dtype)) {
+    if (arch == GRAPPA_GCN && dz_in && flags == 0 && spmm_mm_supported(part, f_out, f_in, dtype)) {
         // dT = Ahat dz_out and dz_in = (dT W^T) * relu'(h_in) in one fused kernel, then
         // dW = h_in^T dT
         AggMMArgs m;
@@ -302,9 +313,10 @@ extern "C" grappa_status grappa_layer_bwd(grappa_ctx* ctx, const grappa_part* pa
         return gemm_tn(ctx, t, dtype, s);
     }
     if (arch == GRAPPA_GCN) {
-        // dT = Ahat dz_out
+        // dT = Ahat dz_out = N (A + I) (N dz_out): with a pre-normalised dz_out the SpMM
+        // gathers unweighted rows
         SpmmArgs a;
-        a.X = dz_out; a.width = f_out; a.row_scale = I.norm_gcn; a.col_scale = I.norm_gcn;
+        a.X = dz_out; a.width = f_out; a.row_scale = I.norm_gcn; a.col_scale = out_normed ? nullptr : I.norm_gcn;
         a.self = 1; a.out = L.node; a.partial = L.partial;
         GRAPPA_TRY(spmm(ctx, part, a, dtype, s));
         // dW = h_in^T dT
@@ -316,6 +328,7 @@ extern "C" grappa_status grappa_layer_bwd(grappa_ctx* ctx, const grappa_part* pa
         GemmArgs g;
         g.M = I.n_core; g.K1 = f_out; g.N = f_in; g.A1 = L.node; g.B = w; g.b_trans = 1;
         g.mask = relu_in ? h_in : nullptr; g.n_split = f_in; g.C1 = dz_in;
+        if (in_normed) g.row_scale = I.norm_gcn;          // write N dz_in
         return gemm_nn(ctx, g, dtype, s);
     }
     // SAGE: [dWs; dWn] = [h_in | M]^T dz_out

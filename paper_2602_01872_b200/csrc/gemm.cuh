@@ -8,7 +8,7 @@ namespace grappa {
 //   A1 [M x K1], A2 [M x K2] (dtype, row-major; A2 may be null with K2 = 0)
 //   B fp32: b_trans = 0 -> [K x N] row-major;  b_trans = 1 -> [N x K] row-major (i.e. W^T)
 //   columns [0, n_split) -> C1 (row stride n_split), [n_split, N) -> C2 (stride N - n_split)
-//   epilogue on C1 columns: *= row_scale[m] (tcgen05 path only, see gemm_nn_row_scale_ok),
+//   epilogue on C1 columns: *= row_scale[m] (if set),
 //   *= 1[mask > 0] (mask [M x n_split], dtype), then ReLU if relu.
 struct GemmArgs {
     int64_t M = 0;
@@ -47,8 +47,6 @@ size_t gemm_tn_ws_bytes(int64_t M, int K1, int K2, int N);
 
 // dispatch: bf16 storage -> tcgen05 kernels (gemm_tc.cu) when the shape fits, else SIMT
 grappa_status gemm_nn(grappa_ctx* ctx, const GemmArgs& g, grappa_dtype dt, cudaStream_t s);
-// true when gemm_nn will take the tcgen05 path for g (the only one with the row-scale epilogue)
-bool gemm_nn_row_scale_ok(const GemmArgs& g, grappa_dtype dt);
 grappa_status gemm_tn(grappa_ctx* ctx, const GemmTNArgs& g, grappa_dtype dt, cudaStream_t s);
 
 // tcgen05 implementations (bf16 operands, fp32 TMEM accumulators)

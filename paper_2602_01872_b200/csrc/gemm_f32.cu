@@ -4,7 +4,7 @@
 // 1e-4 bar), so fp32 storage runs on FFMA: 128x128 tiles, 8x8 outputs per thread in two 4x4
 // quadrants (conflict-free float4 smem reads), 8-deep K slices double-buffered through shared
 // memory with the next slice prefetched into registers.
-//   k_sgemm_nn : C = [A1 | A2] * op(B)  (+ relu'-mask / ReLU epilogue, column split)
+//   k_sgemm_nn : C = [A1 | A2] * op(B)  (+ row-scale / relu'-mask / ReLU epilogue, column split)
 //   k_sgemm_tn : fp32 partials of [A1 | A2]^T * Bm over a row slab (weight gradient)
 #include "gemm.cuh"
 
@@ -86,12 +86,15 @@ __global__ void __launch_bounds__(256, 2) k_sgemm_nn(GemmArgs g) {
     for (int i = 0; i < 8; i++) {
         const int64_t r = row0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
         if (r >= g.M) continue;
+        const float rsv = g.row_scale ? g.row_scale[r] : 1.f;
 #pragma unroll
         for (int jh = 0; jh < 2; jh++) {
             const int c = col0 + jh * 64 + tx * 4;       // 4 consecutive columns
             if (c >= g.N) continue;
             float v[4] = {acc[i][jh * 4], acc[i][jh * 4 + 1], acc[i][jh * 4 + 2], acc[i][jh * 4 + 3]};
             if (c < g.n_split) {
+#pragma unroll
+                for (int q = 0; q < 4; q++) v[q] *= rsv;
                 if (mask) {
                     const float4 m = ld4(mask + r * g.n_split + c);
                     v[0] = m.x > 0.f ? v[0] : 0.f; v[1] = m.y > 0.f ? v[1] : 0.f;

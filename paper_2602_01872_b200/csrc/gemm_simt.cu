@@ -77,12 +77,14 @@ __global__ void __launch_bounds__(256) k_gemm_nn(GemmArgs g) {
     for (int i = 0; i < 8; i++) {
         const int64_t r = row0 + ty * 8 + i;
         if (r >= g.M) continue;
+        const float rsv = g.row_scale ? g.row_scale[r] : 1.f;
 #pragma unroll
         for (int j = 0; j < 4; j++) {
             const int c = col0 + tx * 4 + j;
             if (c >= g.N) continue;
             float v = acc[i][j];
             if (c < g.n_split) {
+                v *= rsv;
                 if (mask && !(ld_f<T>(mask + r * g.n_split + c) > 0.f)) v = 0.f;
                 if (g.relu) v = fmaxf(v, 0.f);
                 st_f<T>(C1 + r * g.n_split + c, v);
@@ -186,16 +188,8 @@ size_t gemm_tn_ws_bytes(int64_t M, int K1, int K2, int N) {
 static int g_force_simt = 0;
 void gemm_force_simt(int on) { g_force_simt = on; }
 
-bool gemm_nn_row_scale_ok(const GemmArgs& g, grappa_dtype dt) {
-    return dt == GRAPPA_BF16 && !g_force_simt && gemm_tc_nn_supported(g);
-}
-
 grappa_status gemm_nn(grappa_ctx* ctx, const GemmArgs& g, grappa_dtype dt, cudaStream_t s) {
     if (g.M == 0) return GRAPPA_OK;
-    if (g.row_scale && !gemm_nn_row_scale_ok(g, dt)) {
-        set_error("gemm_nn: row_scale epilogue needs the tcgen05 path");
-        return GRAPPA_E_SUPPORT;
-    }
     const double es = dt == GRAPPA_BF16 ? 2.0 : 4.0, K = g.K1 + g.K2;
     ProfScope ps(ctx, s, GRAPPA_K_GEMM,
                  (double)g.M * K * es + K * g.N * 4.0 + (double)g.M * g.N * es * (g.mask ? 2 : 1) +

@@ -114,11 +114,21 @@ __device__ __forceinline__ void nn_epilogue(const TcNN& p, const CUtensorMap* tm
         }
         grp_bar(H);
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
+        for (int q2 = 0; q2 < 4; q2 += 2) {
+            if (cbase + q2 * 16 >= cend) break;
+            // two 16-column TMEM loads in flight per wait
+            uint32_t raw[2][16];
+            tc::tmem_ld16_nowait(tbase + coff + cbase + q2 * 16, raw[0]);
+            if (cbase + q2 * 16 + 16 < cend) tc::tmem_ld16_nowait(tbase + coff + cbase + q2 * 16 + 16, raw[1]);
+            tc::tmem_wait_ld();
+#pragma unroll
+        for (int qq = 0; qq < 2; qq++) {
+            const int q = q2 + qq;
             const int cc = cbase + q * 16;
             if (cc >= cend) break;
             float v[16];
-            tc::tmem_ld16(tbase + coff + cc, v);
+#pragma unroll
+            for (int i = 0; i < 16; i++) v[i] = __uint_as_float(raw[qq][i]);
             if (first && p.rs) {
 #pragma unroll
                 for (int i = 0; i < 16; i++) v[i] *= rsv;
@@ -149,6 +159,7 @@ __device__ __forceinline__ void nn_epilogue(const TcNN& p, const CUtensorMap* tm
             const int ch = (cc & 63) >> 3;            // 16-byte chunk within the 128-byte row
             *reinterpret_cast<uint4*>(obox + tc::sw128_off(r, ch)) = make_uint4(o[0], o[1], o[2], o[3]);
             *reinterpret_cast<uint4*>(obox + tc::sw128_off(r, ch + 1)) = make_uint4(o[4], o[5], o[6], o[7]);
+        }
         }
         tc::fence_proxy_async();                      // staged box -> visible to the TMA engine
         grp_bar(H);

@@ -71,6 +71,7 @@ template <> struct Vec<__nv_bfloat16> {
 
 constexpr int kUnroll = 4;
 
+
 // (a0, a1) += w * (x0, x1) as one packed FFMA2 (sm_100): halves the FMA issue count of the
 // gather-accumulate loop, whose instruction issue -- not DRAM -- is the limiter (ncu)
 __device__ __forceinline__ void ffma2(float& a0, float& a1, float w, float x0, float x1) {
@@ -89,6 +90,10 @@ __device__ __forceinline__ void ffma2(float& a0, float& a1, float w, float x0, f
 // 3 = row-group kernel over the rows in natural order (no degree bucketing)
 static int g_spmm_variant = 0;
 void spmm_force_warp_per_row(int v) { g_spmm_variant = v; }
+// unweighted bf16 rows: 32-byte lanes (1) or the 16-byte row-group kernel (0, default: measured
+// faster on products -- the 32-byte kernel needs ~2x the registers, halving resident warps)
+static int g_wide_loads = 0;
+void spmm_set_wide(int v) { g_wide_loads = v; }
 
 // Gather-sum of edges [e0, e1) of one row into acc (lanes of slot `slot`, sub-lane `sub`).
 template <typename T, int CPL>
@@ -410,6 +415,113 @@ __global__ void __launch_bounds__(256) k_spmm_grp(SpmmArgs a, int G, int P) {
     epilogue<T, 1>(a, orow, orow, sub, G, WV, acc1);
 }
 
+// 32-byte variant for unweighted bf16 rows (pre-scaled inputs): each lane owns 16 consecutive
+// features and fetches them with one 256-bit load (LDG.E.ENL2.256), so a gathered row costs
+// half the load, shuffle and address instructions of the 16-byte layout; G = width/16 lanes
+// per row, P = 32/G rows per warp.
+__device__ __forceinline__ void ld256(const __nv_bfloat16* p, uint4& a, uint4& b) {
+    asm volatile("ld.global.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                 : "l"(p));
+}
+
+template <int R, int U>
+__device__ __forceinline__ void grp_accumulate16(const __nv_bfloat16* __restrict__ X, const int32_t* __restrict__ col,
+                                                 int64_t e0, int deg, int G, int slot, int P, int sub,
+                                                 float (&lo)[8], float (&hi)[8]) {
+    const int maxdeg = __reduce_max_sync(0xffffffffu, deg);
+    // lanes of idle slots do not constrain the fast path
+    const int mindeg = __reduce_min_sync(0xffffffffu, slot < P ? deg : 0x7fffffff);
+    const int CH = G * R;
+    const __nv_bfloat16* Xs = X + sub * 16;
+    const int64_t rowel = (int64_t)G * 16;                 // elements per row
+    for (int off = 0; off < maxdeg; off += CH) {
+        int idx[R];
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int p = off + r * G + sub;
+            idx[r] = p < deg ? col[e0 + p] : 0;
+        }
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const int base = off + r * G;
+            const int jmax = min(G, maxdeg - base);        // batches any lane needs
+            const int jfull = min(G, mindeg - base);       // batches every lane needs
+            const int lim = deg - base;                    // this lane's valid edges
+            for (int j = 0; j < jmax; j += U) {
+                uint4 va[U], vb[U];
+                if (j + U <= jfull) {
+                    // full batch for the whole warp: no predication
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int s = __shfl_sync(0xffffffffu, idx[r], slot * G + j + u);
+                        ld256(Xs + (int64_t)s * rowel, va[u], vb[u]);
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int jj = j + u;
+                        const int s = __shfl_sync(0xffffffffu, idx[r], (slot * G + jj) & 31);
+                        if (jj < G && jj < lim) ld256(Xs + (int64_t)s * rowel, va[u], vb[u]);
+                        else va[u] = vb[u] = make_uint4(0, 0, 0, 0);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    acc_bf16(lo, va[u]);
+                    acc_bf16(hi, vb[u]);
+                }
+            }
+        }
+    }
+}
+
+template <int R, int U>
+__global__ void __launch_bounds__(256) k_spmm_grp16(SpmmArgs a, int G, int P) {
+    using T = __nv_bfloat16;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int slot = lane / G, sub = lane - slot * G;
+    const int WV = 2 * G;                              // 8-element vectors per row
+    const int64_t vrow = warp * P + slot;
+    int64_t e0 = 0, e1 = 0, orow = -1;
+    bool to_partial = false;
+    if (slot < P) {
+        if (vrow < a.n_slots) {
+            const int32_t r = a.slot_row[vrow], sg = a.slot_seg[vrow];
+            e0 = a.rowptr[r] + (int64_t)sg * kSegLen;
+            e1 = min(a.rowptr[r + 1], e0 + kSegLen);
+            orow = vrow;
+            to_partial = true;
+        } else if (vrow - a.n_slots < a.n) {
+            const int64_t v = a.row_order ? (int64_t)a.row_order[vrow - a.n_slots] : vrow - a.n_slots;
+            e0 = a.rowptr[v];
+            e1 = a.rowptr[v + 1];
+            if (e1 - e0 > kSegLen) e1 = e0;          // split row: finished by the fix-up kernel
+            else orow = v;
+        }
+    }
+    float lo[8], hi[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) lo[q] = hi[q] = 0.f;
+    grp_accumulate16<R, U>(reinterpret_cast<const T*>(a.X), a.col, e0, (int)(e1 - e0), G, slot, P, sub, lo, hi);
+    if (orow < 0) return;
+    if (to_partial) {
+        float* dst = a.partial + ((int64_t)orow * WV + 2 * sub) * 8;
+#pragma unroll
+        for (int q = 0; q < 8; q += 4) {
+            *reinterpret_cast<float4*>(dst + q) = make_float4(lo[q], lo[q + 1], lo[q + 2], lo[q + 3]);
+            *reinterpret_cast<float4*>(dst + 8 + q) = make_float4(hi[q], hi[q + 1], hi[q + 2], hi[q + 3]);
+        }
+        return;
+    }
+    float l1[1][8], h1[1][8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) { l1[0][q] = lo[q]; h1[0][q] = hi[q]; }
+    epilogue<T, 1>(a, orow, orow, 2 * sub, G, WV, l1);
+    epilogue<T, 1>(a, orow, orow, 2 * sub + 1, G, WV, h1);
+}
+
 // split-row combine, one block per split row: warp w sums slots s0+w, s0+w+8, ... in order,
 // then the 8 warp sums are added in warp order (deterministic) before the epilogue
 template <typename T>
@@ -485,9 +597,32 @@ static grappa_status launch_cpl(grappa_ctx* ctx, const SpmmArgs& a, int G, int P
     return GRAPPA_OK;
 }
 
+template <int R>
+static grappa_status launch_grp16(grappa_ctx* ctx, const SpmmArgs& a, int G, cudaStream_t s) {
+    const int P = 32 / G;
+    const int64_t vrows = a.n + a.n_slots;
+    if (vrows > 0) {
+        k_spmm_grp16<R, 4><<<(unsigned)ceil_div(ceil_div(vrows, P), 8), 256, 0, s>>>(a, G, P);
+        GRAPPA_LAUNCHED(ctx);
+    }
+    if (a.n_heavy > 0) {
+        k_spmm_fixup_blk<__nv_bfloat16><<<(unsigned)a.n_heavy, 256, 0, s>>>(a, 2 * G);
+        GRAPPA_LAUNCHED(ctx);
+    }
+    return GRAPPA_OK;
+}
+
 template <typename T>
 static grappa_status launch_t(grappa_ctx* ctx, const SpmmArgs& a, cudaStream_t s) {
     const int WV = a.width / Vec<T>::EPV;
+    if (sizeof(T) == 2 && !a.col_scale && a.width % 16 == 0 && a.width / 16 <= 32 && g_spmm_variant == 0 &&
+        g_wide_loads) {
+        const int G16 = a.width / 16;
+        if (G16 >= 16) return launch_grp16<1>(ctx, a, G16, s);
+        if (G16 >= 8) return launch_grp16<2>(ctx, a, G16, s);
+        if (G16 >= 4) return launch_grp16<4>(ctx, a, G16, s);
+        return launch_grp16<8>(ctx, a, G16, s);
+    }
     if (WV <= 32 && g_spmm_variant != 1) {
         // group-per-row kernel; R index registers per lane so a chunk holds >= 16 edges
         if (WV >= 16) return launch_grp<T, 1>(ctx, a, WV, s);

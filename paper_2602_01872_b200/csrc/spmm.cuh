@@ -55,6 +55,7 @@ struct AggMMArgs {
 bool spmm_mm_supported(const grappa_part* part, int K, int N, grappa_dtype dt);
 grappa_status spmm_mm(grappa_ctx* ctx, const grappa_part* part, const AggMMArgs& m, cudaStream_t s);
 void spmm_set_fuse(int v);
+void spmm_set_wide(int v);
 
 grappa_status spmm(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grappa_dtype dt,
                    cudaStream_t s);

@@ -21,7 +21,8 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import (BF16, F32, Context, Part, grappa_aggregate_grads, grappa_layer_bwd,
+from . import (BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, F32, Context, Part, grappa_aggregate_grads,
+               grappa_layer_bwd, grappa_layer_bwd_ex,
                grappa_layer_fwd, grappa_loss, grappa_partition, grappa_repartition,
                layer_saved_bytes, layer_ws_bytes)
 
@@ -177,11 +178,17 @@ class Trainer:
                              self.w_views[l], H[l + 1], self.saved[l], self.ws, self.dt, s)
         dz = self.dz[0][: n * dp[L]].view(n, dp[L])
         grappa_loss(self.ctx, part, H[L], sp.dims[L], dp[L], dz, self.loss_dev, self.dt, s)
+        gcn = sp.arch == "gcn"
         for l in range(L - 1, -1, -1):
             dz_in = self.dz[(L - l) % 2][: n * dp[l]].view(n, dp[l]) if l > 0 else None
-            grappa_layer_bwd(self.ctx, part, sp.arch, dp[l], dp[l + 1], l > 0, dz, H[l],
-                             self.w_views[l], self.saved[l], self.dw_views[l], dz_in, self.ws,
-                             self.dt, s)
+            # GCN: gradients between layers travel pre-multiplied by N = diag(norm_gcn), so
+            # every backward aggregation gathers unweighted rows (grappa_layer_bwd_ex, R29)
+            flags = 0
+            if gcn:
+                flags = (BWD_DZ_OUT_NORMED if l < L - 1 else 0) | (BWD_DZ_IN_NORMED if l > 0 else 0)
+            grappa_layer_bwd_ex(self.ctx, part, sp.arch, dp[l], dp[l + 1], l > 0, dz, H[l],
+                                self.w_views[l], self.saved[l], self.dw_views[l], dz_in, self.ws,
+                                self.dt, flags, s)
             dz = dz_in
         return H[L]
 

@@ -7,7 +7,7 @@ captures every kernel of that phase once.  The number of LOGICAL calls per kerne
 (one SpMM call = its degree-bucket launches + fix-up) is written next to the report so
 scripts/ncu_summary.py can state DRAM traffic per logical call, the unit bench.py's
 roofline `achieved` uses.
-Usage: python scripts/ncu_phase.py [config] [dtype] > gpurun_out/ncu_phase_calls.json
+Usage: python scripts/ncu_phase.py [config] [dtype] [out.json]   (default gpurun_out/ncu_phase_calls.json)
 """
 import json
 import os
@@ -44,6 +44,8 @@ torch.cuda.cudart().cudaProfilerStop()
 calls = {k: ctx.profile_read(k)[1] for k in _lib.KCLASS}
 alg = {k: ctx.profile_read(k)[2] for k in _lib.KCLASS}
 ctx.profile(False)
-json.dump({"config": cfg, "dtype": dtype, "worker": w, "logical_calls": calls,
-           "algorithmic_bytes": alg}, sys.stdout)
-print()
+out = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "gpurun_out", "ncu_phase_calls.json")
+os.makedirs(os.path.dirname(out), exist_ok=True)
+with open(out, "w") as f:
+    json.dump({"config": cfg, "dtype": dtype, "worker": w, "logical_calls": calls,
+               "algorithmic_bytes": alg}, f)

@@ -181,6 +181,44 @@ def test_layer_parity(G, ctx, prod, arch, f_in, f_out, dtype):
     assert err(_np(dz_in), ref_in) <= tol
 
 
+@pytest.mark.parametrize("f_in,f_out", [(112, 128), (128, 48), (128, 128)])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_layer_bwd_normalised_flags(G, ctx, prod, f_in, f_out, dtype):
+    """grappa_layer_bwd_ex with both GCN normalised-gradient flags (reading R29): the kernel
+    gets dz' = N dz and must return dW and N dz_in of the oracle's backward for dz = dz'/N."""
+    part = _part(G, ctx, prod, 8, 2, 5, dtype)
+    n = part.n_core
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    g = torch.Generator(device="cuda").manual_seed(f_in + 7 * f_out)
+    h_in = torch.randn(n, f_in, device="cuda", generator=g).relu().to(tdt)
+    w = (torch.randn(f_in, f_out, device="cuda", generator=g) / math.sqrt(f_in)).contiguous()
+    nrm = part.norm_gcn
+    dz_s = (torch.randn(n, f_out, device="cuda", generator=g) * 1e-3 * nrm[:, None]).to(tdt)
+    saved = torch.empty(1, dtype=torch.uint8, device="cuda")
+    ws = torch.empty(G.layer_ws_bytes(part, "gcn", f_in, f_out, dtype), dtype=torch.uint8, device="cuda")
+    dw = torch.empty_like(w)
+    dz_in = torch.empty(n, f_in, device="cuda", dtype=tdt)
+    G.grappa_layer_bwd_ex(ctx, part, "gcn", f_in, f_out, True, dz_s, h_in, w, saved, dw, dz_in, ws, dtype,
+                          G.BWD_DZ_OUT_NORMED | G.BWD_DZ_IN_NORMED)
+    torch.cuda.synchronize()
+    N = nrm.cpu().numpy().astype(np.float64)
+    op = Mo.operator("gcn", part.rowptr.cpu().numpy(), part.col.cpu().numpy(), n)
+    H = _np(h_in)
+    Ws = [_np(w)]
+    P, Z, _ = Mo.layer_forward("gcn", op, H, Ws, True)
+    grads, dH = Mo.layer_backward("gcn", op, H, P, Ws, _np(dz_s) / N[:, None])
+    tol = TOL[dtype]
+    assert err(_np(dw), grads[0]) <= tol
+    assert err(_np(dz_in), N[:, None] * dH * (H > 0)) <= tol
+    # flags are GCN-only and must be known
+    with pytest.raises(G.GrappaError, match="E_ARG"):
+        G.grappa_layer_bwd_ex(ctx, part, "gcn", f_in, f_out, True, dz_s, h_in, w, saved, dw, dz_in, ws,
+                              dtype, 4)
+    with pytest.raises(G.GrappaError, match="E_ARG"):
+        G.grappa_layer_bwd_ex(ctx, part, "sage", f_in, f_out, True, dz_s, h_in, w, saved, dw, dz_in, ws,
+                              dtype, 1)
+
+
 @pytest.mark.parametrize("which,K,kpad", [("prod", 47, 48), ("arxiv", 40, 48)])
 def test_loss_parity(G, ctx, prod, arxiv, which, K, kpad):
     ds = prod if which == "prod" else arxiv
@@ -289,7 +327,7 @@ def test_epoch_parity(G, ctx, prod, arxiv, which, corr, epochs, rep):
                                                ("gcn", "gemm", "f32", 2), ("sage", "gemm", "f32", 2),
                                                ("gcn", "spmm", "bf16", 1), ("sage", "spmm", "f32", 1),
                                                ("gcn", "spmm", "bf16", 3), ("gcn", "spmm", "bf16", 2),
-                                               ("gcn", "fuse", "bf16", 1)])
+                                               ("gcn", "fuse", "bf16", 1), ("gcn", "wide", "bf16", 1)])
 def test_kernel_variants_agree(G, ctx, prod, arch, op, dtype, alt):
     """Alternative implementations agree on the same layer and inputs: bf16 tcgen05 GEMMs vs
     the CUDA-core GEMMs; the row-group SpMM vs the warp-per-row SpMM; the fused
@@ -304,7 +342,8 @@ def test_kernel_variants_agree(G, ctx, prod, arch, op, dtype, alt):
     dz = (torch.randn(n, f_out, device="cuda", generator=g) * 1e-2).to(tdt)
     outs = []
     lib = G.load()
-    for variant in (0, alt):
+    default = 0
+    for variant in (default, alt):
         assert lib.grappa_set_kernel_variant(op.encode(), variant) == 0
         h_out = torch.empty(n, f_out, device="cuda", dtype=tdt)
         saved = torch.empty(max(1, G.layer_saved_bytes(part, arch, f_in, f_out, dtype)), dtype=torch.uint8, device="cuda")
@@ -315,7 +354,7 @@ def test_kernel_variants_agree(G, ctx, prod, arch, op, dtype, alt):
         G.grappa_layer_bwd(ctx, part, arch, f_in, f_out, True, dz, h_in, w, saved, dw, dz_in, ws, dtype)
         torch.cuda.synchronize()
         outs.append((_np(h_out), _np(dw), _np(dz_in)))
-    lib.grappa_set_kernel_variant(op.encode(), 0)
+    lib.grappa_set_kernel_variant(op.encode(), default)
     assert lib.grappa_set_kernel_variant(b"nope", 1) == 1
     for a, b in zip(*outs):
         assert err(a, b) <= (1e-2 if dtype == "bf16" else 1e-5)
