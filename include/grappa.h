@@ -156,7 +156,9 @@ typedef struct {
 } grappa_part_host;
 /* device -> host copy of the selected arrays (enqueued on stream) */
 grappa_status grappa_part_download(const grappa_part* part, const grappa_part_host* dst, void* stream);
-/* host -> device copy into the partition's own buffers (enqueued on stream; same sizes) */
+/* host -> device copy into the partition's own buffers (enqueued on stream; same sizes).
+ * The image must be this partition's own (as written by grappa_part_download): the SpMM
+ * metadata derived at repartition time (split rows, degree-bucketed row order) is kept. */
 grappa_status grappa_part_upload(grappa_part* part, const grappa_part_host* src, void* stream);
 
 /* Workspace sizes (bytes) for one layer call on `part`; `saved` persists fwd -> bwd. */

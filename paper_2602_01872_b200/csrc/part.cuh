@@ -21,4 +21,7 @@ struct grappa_part {
     // SpMM processing order: rows bucketed by descending local degree, so the row groups that
     // share a warp have similar trip counts (results do not depend on the order)
     grappa::DevBuf row_order;
+    // per row in that order: {v, d_l, rowptr[v] lo, hi} -- one coalesced 16-byte load replaces
+    // the dependent row_order -> rowptr lookups at the head of every SpMM row
+    grappa::DevBuf row_desc;
 };

@@ -246,6 +246,15 @@ __global__ void k_deg_scatter(int64_t n, int64_t per_block, const int32_t* __res
     }
 }
 
+__global__ void k_row_desc(int64_t n, const int32_t* __restrict__ order, const int64_t* __restrict__ rowptr,
+                           int4* __restrict__ desc) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = order[i];
+        const int64_t e0 = rowptr[v];
+        desc[i] = make_int4(v, (int)(rowptr[v + 1] - e0), (int)(uint32_t)(e0 & 0xffffffffll), (int)(e0 >> 32));
+    }
+}
+
 // Coverage statistics over the seeds, fixed-order block partials.
 struct SeedStats {
     double sum_r;      // sum d_l/d_g (ratio 1 where d_g = 0), R4
@@ -464,6 +473,10 @@ extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g
         k_deg_scatter<<<(unsigned)ceil_div(n_core, per), 256, 0, s>>>(n_core, per, (int32_t*)p->d_l.p,
                                                                       bins + kDegBuckets, (int32_t*)p->row_order.p);
         GRAPPA_LAUNCHED(ctx);
+        RP_TRY(p->row_desc.grow((size_t)n_core * 16));
+        k_row_desc<<<g2, 256, 0, s>>>(n_core, (int32_t*)p->row_order.p, (int64_t*)p->rowptr.p,
+                                      (int4*)p->row_desc.p);
+        GRAPPA_LAUNCHED(ctx);
     }
     // publish
     grappa_part_info& I = p->info;
@@ -520,7 +533,8 @@ extern "C" void grappa_part_destroy(grappa_part* p) {
     if (!p) return;
     for (grappa::DevBuf* b : {&p->rowptr, &p->col, &p->core_global, &p->d_l, &p->d_g, &p->norm_gcn,
                               &p->norm_sage, &p->seeds, &p->labels, &p->x, &p->heavy_rows,
-                              &p->heavy_slot_off, &p->slot_row, &p->slot_seg, &p->row_order})
+                              &p->heavy_slot_off, &p->slot_row, &p->slot_seg, &p->row_order,
+                              &p->row_desc})
         b->release();
     delete p;
 }

@@ -389,9 +389,17 @@ __global__ void __launch_bounds__(256) k_spmm_grp(SpmmArgs a, int G, int P) {
             orow = vrow;
             to_partial = true;
         } else if (vrow - a.n_slots < a.n) {
-            const int64_t v = a.row_order ? (int64_t)a.row_order[vrow - a.n_slots] : vrow - a.n_slots;
-            e0 = a.rowptr[v];
-            e1 = a.rowptr[v + 1];
+            int64_t v;
+            if (a.row_desc) {
+                const int4 d = __ldg(a.row_desc + (vrow - a.n_slots));
+                v = d.x;
+                e0 = (int64_t)(uint32_t)d.z | ((int64_t)d.w << 32);
+                e1 = e0 + d.y;
+            } else {
+                v = a.row_order ? (int64_t)a.row_order[vrow - a.n_slots] : vrow - a.n_slots;
+                e0 = a.rowptr[v];
+                e1 = a.rowptr[v + 1];
+            }
             if (e1 - e0 > kSegLen) e1 = e0;          // split row: finished by the fix-up kernel
             else orow = v;
         }
@@ -929,6 +937,7 @@ grappa_status spmm(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grappa_
     a.heavy_rows = (const int32_t*)part->heavy_rows.p;
     a.heavy_slot_off = (const int32_t*)part->heavy_slot_off.p;
     a.row_order = g_spmm_variant == 3 ? nullptr : (const int32_t*)part->row_order.p;
+    a.row_desc = g_spmm_variant == 3 ? nullptr : (const int4*)part->row_desc.p;
     return spmm_csr(ctx, a, dt, s);
 }
 

@@ -16,6 +16,7 @@ struct SpmmArgs {
     const int32_t* heavy_rows = nullptr;
     const int32_t* heavy_slot_off = nullptr;
     const int32_t* row_order = nullptr;    // optional processing order of the rows
+    const int4* row_desc = nullptr;        // optional {v, deg, e0 lo, e0 hi} in that order
     // caller
     const void* X = nullptr;          // [n x width] dtype
     int width = 0;                    // elements per row (multiple of 4)
