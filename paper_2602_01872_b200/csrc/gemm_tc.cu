@@ -48,6 +48,7 @@ struct TcNN {
     int nb1, nb2;          // 64-column output boxes of C1 / C2
     int num_tiles;
     int stages;            // A-tile ring depth (<= kMaxNNStages)
+    int mask_tma;          // relu'-gate boxes TMA-staged one tile ahead (else register prefetch)
     int nsb;               // staging boxes per epilogue group (1 or 2)
     uint32_t tmem_cols;
 };
@@ -62,6 +63,50 @@ __device__ __forceinline__ void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// Stage the fp32 weights once per CTA as the bf16 B operand: [kb][N rows][64 k] K-major,
+// SWIZZLE_128B, k >= K zero.  Reads are coalesced float4 rows of W (W [Kt x N]) or of W^T
+// (b_trans: W stored [N x Kt]); W1 rows [0, K1) fill k-blocks [0, kb1), rows [K1, Kt) the rest.
+__device__ __forceinline__ void stage_weights(uint8_t* sB, const float* __restrict__ B, int K1, int K2, int N,
+                                              int kb1, int kbt, int b_trans) {
+    const int Kt = K1 + K2;
+    uint4* z = reinterpret_cast<uint4*>(sB);
+    for (int i = threadIdx.x; i < kbt * N * 8; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    auto slot = [&](int kg, int& kb, int& kk) {
+        if (kg < K1) { kb = kg >> 6; kk = kg & 63; }
+        else { const int kl = kg - K1; kb = kb1 + (kl >> 6); kk = kl & 63; }
+    };
+    if (!b_trans) {
+        const int n4 = N >> 2;
+        for (int idx = threadIdx.x; idx < Kt * n4; idx += blockDim.x) {
+            const int kg = idx / n4, c = (idx - kg * n4) * 4;
+            const float4 f = __ldg(reinterpret_cast<const float4*>(B + (int64_t)kg * N + c));
+            int kb, kk;
+            slot(kg, kb, kk);
+            uint8_t* base = sB + (size_t)kb * N * 128 + (kk & 7) * 2;
+            const float v[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+                *reinterpret_cast<__nv_bfloat16*>(base + tc::sw128_off(c + j, kk >> 3)) = __float2bfloat16_rn(v[j]);
+        }
+    } else {
+        const int k8 = Kt >> 3;
+        for (int idx = threadIdx.x; idx < N * k8; idx += blockDim.x) {
+            const int n = idx / k8, kg = (idx - n * k8) * 8;
+            const float4 a = __ldg(reinterpret_cast<const float4*>(B + (int64_t)n * Kt + kg));
+            const float4 b = __ldg(reinterpret_cast<const float4*>(B + (int64_t)n * Kt + kg + 4));
+            int kb, kk;
+            slot(kg, kb, kk);
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x, a.y), h1 = __floats2bfloat162_rn(a.z, a.w);
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(b.x, b.y), h3 = __floats2bfloat162_rn(b.z, b.w);
+            uint4 o;
+            o.x = *reinterpret_cast<uint32_t*>(&h0); o.y = *reinterpret_cast<uint32_t*>(&h1);
+            o.z = *reinterpret_cast<uint32_t*>(&h2); o.w = *reinterpret_cast<uint32_t*>(&h3);
+            *reinterpret_cast<uint4*>(sB + (size_t)kb * N * 128 + tc::sw128_off(n, kk >> 3)) = o;
+        }
+    }
+}
 
 __device__ __forceinline__ void bulk_wait_read1() {
     asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -78,25 +123,14 @@ template <int H>
 __device__ __forceinline__ void nn_epilogue(const TcNN& p, const CUtensorMap* tmC1, const CUtensorMap* tmC2,
                                             const __nv_bfloat16* __restrict__ mask, uint8_t* sbuf, int nsb,
                                             uint32_t tmem_acc, uint64_t* tfull, uint32_t aphase,
-                                            int ew, int lane, int tile, bool leader, int& ob) {
+                                            int ew, int lane, int tile, bool leader, int& ob, float rsv,
+                                            const uint8_t* gsm) {
     const int r = ew * 32 + lane;                 // row within the tile
     // relu'-mask of this thread's row for this group's C1 chunks (C1 chunk j lies in box j >> 2,
     // owned by group (j >> 2) & 1), fetched before waiting so the latency hides under the MMAs
-    uint4 mk[8];                                  // this group's first box (C1 box H)
     const int64_t grow = (int64_t)tile * 128 + r;
     const bool live = grow < p.M;
-    const float rsv = (p.rs && live) ? __ldg(p.rs + grow) : 1.f;
     const uint4* msrc = reinterpret_cast<const uint4*>(mask + (live ? grow : 0) * p.n_split);
-    if (mask && live) {
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-            const int j = H * 4 + q;
-            if (j * 16 < p.n_split) {
-                mk[2 * q] = __ldg(msrc + 2 * j);
-                mk[2 * q + 1] = __ldg(msrc + 2 * j + 1);
-            }
-        }
-    }
     tc::mbar_wait(tfull, aphase);
     tc::fence_after();
     const uint32_t tbase = tmem_acc + ((uint32_t)(ew * 32) << 16);
@@ -135,10 +169,11 @@ __device__ __forceinline__ void nn_epilogue(const TcNN& p, const CUtensorMap* tm
             }
             if (first && mask && live) {
                 uint4 m[2];
-                if (bx == H) {                        // prefetched
-                    m[0] = mk[2 * q];
-                    m[1] = mk[2 * q + 1];
-                } else {                              // later boxes (N > 128): fetched here
+                if (bx == H && gsm) {                 // TMA-staged gate box (SW128 layout)
+                    const int gch = (cc & 63) >> 3;
+                    m[0] = *reinterpret_cast<const uint4*>(gsm + tc::sw128_off(r, gch));
+                    m[1] = *reinterpret_cast<const uint4*>(gsm + tc::sw128_off(r, gch + 1));
+                } else {                              // gate wider than 128 columns: fetched here
                     m[0] = __ldg(msrc + (cc >> 3));
                     m[1] = __ldg(msrc + (cc >> 3) + 1);
                 }
@@ -174,7 +209,7 @@ __device__ __forceinline__ void nn_epilogue(const TcNN& p, const CUtensorMap* tm
 __global__ void __launch_bounds__(kNNThreads, 1)
     k_gemm_tc_nn(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
                  const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmC2,
-                 const __nv_bfloat16* __restrict__ mask, TcNN p) {
+                 const __grid_constant__ CUtensorMap tmMask, const __nv_bfloat16* __restrict__ mask, TcNN p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const int kbt = p.kb1 + p.kb2;
@@ -182,35 +217,21 @@ __global__ void __launch_bounds__(kNNThreads, 1)
     uint8_t* sA = smem;
     uint8_t* sB = sA + stages * kNNStageBytes;
     uint8_t* sOut = sB + (size_t)kbt * p.N * 128;                  // 2 groups x nsb boxes
-    uint64_t* full = (uint64_t*)(sOut + 2 * p.nsb * kBoxBytes);
+    uint8_t* sMask = sOut + 2 * p.nsb * kBoxBytes;                 // [group][buf] gate boxes
+    uint64_t* full = (uint64_t*)(sMask + (p.mask_tma ? 4 * kBoxBytes : 0));
     uint64_t* empty = full + kMaxNNStages;
     uint64_t* tfull = empty + kMaxNNStages;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    uint64_t* mfull = tempty + 2;                                    // [group][buf]
+    uint32_t* tmem_slot = (uint32_t*)(mfull + 4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     // weights -> shared memory once: bf16, K-major, SWIZZLE_128B, zero padded
-    const int nchunks = kbt * p.N * 8;
-    const int Kt = p.K1 + p.K2;
-    for (int idx = threadIdx.x; idx < nchunks; idx += blockDim.x) {
-        const int kb = idx / (p.N * 8), rem = idx % (p.N * 8), n = rem >> 3, ch = rem & 7;
-        __align__(16) __nv_bfloat16 v[8];
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-            int kl, kg;
-            bool ok;
-            if (kb < p.kb1) { kl = kb * 64 + ch * 8 + q; kg = kl; ok = kl < p.K1; }
-            else { kl = (kb - p.kb1) * 64 + ch * 8 + q; kg = p.K1 + kl; ok = kl < p.K2; }
-            float f = 0.f;
-            if (ok) f = p.b_trans ? p.B[(int64_t)n * Kt + kg] : p.B[(int64_t)kg * p.N + n];
-            v[q] = __float2bfloat16_rn(f);
-        }
-        *reinterpret_cast<uint4*>(sB + (size_t)kb * p.N * 128 + tc::sw128_off(n, ch)) =
-            *reinterpret_cast<const uint4*>(v);
-    }
+    stage_weights(sB, p.B, p.K1, p.K2, p.N, p.kb1, kbt, p.b_trans);
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < stages; s++) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
         for (int a = 0; a < 2; a++) { tc::mbar_init(&tfull[a], 1); tc::mbar_init(&tempty[a], 8); }
+        for (int a = 0; a < 4; a++) tc::mbar_init(&mfull[a], 1);
         tc::mbar_fence_init();
         tc::tma_prefetch(&tmA1);
         if (p.kb2) tc::tma_prefetch(&tmA2);
@@ -273,14 +294,41 @@ __global__ void __launch_bounds__(kNNThreads, 1)
         uint8_t* sbuf = sOut + grp * p.nsb * kBoxBytes;
         int acc = 0, ob = 0;
         uint32_t aphase = 0;
-        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        // the row scale is fetched one tile ahead (its latency hides under a whole tile)
+        auto rs_of = [&](int t) {
+            const int64_t g = (int64_t)t * 128 + ew * 32 + lane;
+            return (p.rs && t < p.num_tiles && g < p.M) ? __ldg(p.rs + g) : 1.f;
+        };
+        float rs_next = rs_of(blockIdx.x);
+        // relu'-gate box of this group (C1 box grp), TMA-loaded one tile ahead, double-buffered
+        const bool gated = p.mask_tma && grp < p.nb1;
+        uint8_t* gbox = sMask + grp * 2 * kBoxBytes;
+        uint64_t* gbar = mfull + grp * 2;
+        if (gated && leader && (int)blockIdx.x < p.num_tiles) {
+            tc::mbar_arrive_expect_tx(&gbar[0], kBoxBytes);
+            tc::tma_load_2d(gbox, &tmMask, &gbar[0], grp * 64, blockIdx.x * 128);
+        }
+        int it = 0;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, it++) {
             const uint32_t tacc = tmem + (uint32_t)(acc * p.N);
+            const float rs_cur = rs_next;
+            rs_next = rs_of(tile + gridDim.x);
+            const uint8_t* gcur = nullptr;
+            if (gated) {
+                const int nb = (it + 1) & 1, next = tile + gridDim.x;
+                if (leader && next < p.num_tiles) {   // its buffer was last read by tile it-1
+                    tc::mbar_arrive_expect_tx(&gbar[nb], kBoxBytes);
+                    tc::tma_load_2d(gbox + nb * kBoxBytes, &tmMask, &gbar[nb], grp * 64, next * 128);
+                }
+                tc::mbar_wait(&gbar[it & 1], (uint32_t)((it >> 1) & 1));
+                gcur = gbox + (it & 1) * kBoxBytes;
+            }
             if (grp == 0)
                 nn_epilogue<0>(p, &tmC1, &tmC2, mask, sbuf, p.nsb, tacc, &tfull[acc], aphase, ew, lane, tile,
-                               leader, ob);
+                               leader, ob, rs_cur, gcur);
             else
                 nn_epilogue<1>(p, &tmC1, &tmC2, mask, sbuf, p.nsb, tacc, &tfull[acc], aphase, ew, lane, tile,
-                               leader, ob);
+                               leader, ob, rs_cur, gcur);
             tc::fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[acc]);
@@ -463,13 +511,14 @@ static grappa_status make_map(CUtensorMap* m, const void* ptr, int64_t rows, int
 
 // A ring + resident weights + 2 groups x nsb staging boxes + barriers; the deepest ring
 // (<= 8 stages) and double-buffered staging when they fit
-static size_t nn_smem_of(int kbt, int N, int stages, int nsb) {
-    return 1024 + (size_t)stages * kNNStageBytes + (size_t)kbt * N * 128 + (size_t)2 * nsb * kBoxBytes + 256;
+static size_t nn_smem_of(int kbt, int N, int stages, int nsb, int mask_tma) {
+    return 1024 + (size_t)stages * kNNStageBytes + (size_t)kbt * N * 128 + (size_t)2 * nsb * kBoxBytes +
+           (mask_tma ? (size_t)4 * kBoxBytes : 0) + 256;
 }
-static bool nn_plan(int kbt, int N, int* stages, int* nsb) {
+static bool nn_plan(int kbt, int N, int mask_tma, int* stages, int* nsb) {
     for (int b = 2; b >= 1; b--)
         for (int st = kMaxNNStages; st >= 2; st--)
-            if (nn_smem_of(kbt, N, st, b) <= (size_t)kMaxSmem && (b == 1 || st >= 4)) {
+            if (nn_smem_of(kbt, N, st, b, mask_tma) <= (size_t)kMaxSmem && (b == 1 || st >= 4)) {
                 *stages = st;
                 *nsb = b;
                 return true;
@@ -481,7 +530,7 @@ bool gemm_tc_nn_supported(const GemmArgs& g) {
     const int kbt = (int)(ceil_div(g.K1, 64) + ceil_div(g.K2, 64));
     int st, nsb;
     return g.N % 16 == 0 && g.N <= 256 && g.n_split % 16 == 0 && g.K1 % 8 == 0 && g.K2 % 8 == 0 &&
-           nn_plan(kbt, g.N, &st, &nsb) && g.M < (1ll << 31);
+           nn_plan(kbt, g.N, 0, &st, &nsb) && g.M < (1ll << 31);
 }
 
 static uint32_t pow2_cols(int c) {
@@ -506,18 +555,23 @@ grappa_status gemm_tc_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s) {
     p.nb1 = (int)ceil_div(g.n_split, 64); p.nb2 = (int)ceil_div(g.N - g.n_split, 64);
     p.num_tiles = (int)ceil_div(g.M, 128);
     p.tmem_cols = pow2_cols(2 * g.N);
-    if (!nn_plan(p.kb1 + p.kb2, g.N, &p.stages, &p.nsb)) {
+    // relu'-gate through TMA when each epilogue group owns at most one gated box and it fits
+    p.mask_tma = p.has_mask && p.nb1 <= 2 && nn_plan(p.kb1 + p.kb2, g.N, 1, &p.stages, &p.nsb) ? 1 : 0;
+    if (!p.mask_tma && !nn_plan(p.kb1 + p.kb2, g.N, 0, &p.stages, &p.nsb)) {
         set_error("gemm_tc_nn: shape does not fit shared memory");
         return GRAPPA_E_SUPPORT;
     }
-    const size_t smem = nn_smem_of(p.kb1 + p.kb2, g.N, p.stages, p.nsb);
+    CUtensorMap mk;
+    if (p.mask_tma) GRAPPA_TRY(make_map(&mk, g.mask, g.M, g.n_split, 128));
+    else mk = c1;
+    const size_t smem = nn_smem_of(p.kb1 + p.kb2, g.N, p.stages, p.nsb, p.mask_tma);
     static bool attr = false;
     if (!attr) {
         GRAPPA_CUDA(cudaFuncSetAttribute(k_gemm_tc_nn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
         attr = true;
     }
     const int grid = (int)std::min<int64_t>(p.num_tiles, ctx->sm_count);
-    k_gemm_tc_nn<<<grid, kNNThreads, smem, s>>>(m1, m2, c1, c2, (const __nv_bfloat16*)g.mask, p);
+    k_gemm_tc_nn<<<grid, kNNThreads, smem, s>>>(m1, m2, c1, c2, mk, (const __nv_bfloat16*)g.mask, p);
     GRAPPA_LAUNCHED(ctx);
     return GRAPPA_OK;
 }

@@ -530,12 +530,14 @@ __global__ void __launch_bounds__(256) k_spmm_grp16(SpmmArgs a, int G, int P) {
     epilogue<T, 1>(a, orow, orow, 2 * sub + 1, G, WV, h1);
 }
 
-// split-row combine, one block per split row: warp w sums slots s0+w, s0+w+8, ... in order,
-// then the 8 warp sums are added in warp order (deterministic) before the epilogue
+// split-row combine, one block of kFixWarps warps per split row: warp w sums slots s0+w,
+// s0+w+kFixWarps, ... in order, then the warp sums are added in warp order (deterministic)
+// before the epilogue (most split rows have 2-3 segments, so wider blocks only cost occupancy).
+constexpr int kFixWarps = 8;
 template <typename T>
-__global__ void __launch_bounds__(256) k_spmm_fixup_blk(SpmmArgs a, int G) {
+__global__ void __launch_bounds__(kFixWarps * 32) k_spmm_fixup_blk(SpmmArgs a, int G) {
     constexpr int E = Vec<T>::EPV;
-    __shared__ float red[8][32 * E];
+    __shared__ float red[kFixWarps][32 * E];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t h = blockIdx.x;
     const int WV = G;
@@ -545,7 +547,7 @@ __global__ void __launch_bounds__(256) k_spmm_fixup_blk(SpmmArgs a, int G) {
 #pragma unroll
     for (int q = 0; q < E; q++) acc[q] = 0.f;
     if (lane < G) {
-        for (int sl = s0 + w; sl < s1; sl += 8) {
+        for (int sl = s0 + w; sl < s1; sl += kFixWarps) {
             const float* src = a.partial + ((int64_t)sl * WV + lane) * E;
 #pragma unroll
             for (int q = 0; q < E; q += 4) {
@@ -562,7 +564,7 @@ __global__ void __launch_bounds__(256) k_spmm_fixup_blk(SpmmArgs a, int G) {
 #pragma unroll
         for (int q = 0; q < E; q++) {
             float t = 0.f;
-            for (int k = 0; k < 8; k++) t += red[k][lane * E + q];
+            for (int k = 0; k < kFixWarps; k++) t += red[k][lane * E + q];
             tot[0][q] = t;
         }
         epilogue<T, 1>(a, r, a.out_compact ? h : r, lane, G, WV, tot);
@@ -585,7 +587,7 @@ static grappa_status launch_grp(grappa_ctx* ctx, const SpmmArgs& a, int G, cudaS
         GRAPPA_LAUNCHED(ctx);
     }
     if (a.n_heavy > 0) {
-        k_spmm_fixup_blk<T><<<(unsigned)a.n_heavy, 256, 0, s>>>(a, G);
+        k_spmm_fixup_blk<T><<<(unsigned)a.n_heavy, kFixWarps * 32, 0, s>>>(a, G);
         GRAPPA_LAUNCHED(ctx);
     }
     return GRAPPA_OK;
@@ -614,7 +616,7 @@ static grappa_status launch_grp16(grappa_ctx* ctx, const SpmmArgs& a, int G, cud
         GRAPPA_LAUNCHED(ctx);
     }
     if (a.n_heavy > 0) {
-        k_spmm_fixup_blk<__nv_bfloat16><<<(unsigned)a.n_heavy, 256, 0, s>>>(a, 2 * G);
+        k_spmm_fixup_blk<__nv_bfloat16><<<(unsigned)a.n_heavy, kFixWarps * 32, 0, s>>>(a, 2 * G);
         GRAPPA_LAUNCHED(ctx);
     }
     return GRAPPA_OK;
