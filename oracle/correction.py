@@ -14,6 +14,13 @@ Alg. 1).
   c_resampling_hm (optional reading R13, not the default): sum s_v / sum s_v d_g/d_l over
                v in S with d_l > 0; 1 if that set is empty.
 
+Node-level estimator (eq. (4) and its uniform case eq. (9); SPEC S:321-329,
+S:366-374; reading R30): every target v's neighbour contribution is importance-weighted by
+p_v(u)/q_v^t(u).  Uniform neighbour distributions give p = 1/d_g, q = 1/d_l, i.e. one weight per
+target w_v = d_l(v)/d_g(v) (1 iff d_g = 0, as R4); the weights enter the model as multipliers on
+each target's aggregated neighbour message in every layer (oracle.model operators, node_w) and
+the batch factor is then c_p = 1.
+
 Aggregate (Alg. 1 P:386, S:420-428; R9): g_hat = (1/M) sum_{p active, ascending worker id}
 c_p g_p; non-finite -> error.  SGD (lr = 0.003 P:489): theta - lr g_hat.
 """
@@ -67,7 +74,7 @@ def c_resampling_hm(d_l, d_g, s=None) -> float:
 
 
 def coverage_factor(kind: str, d_l, d_g, s=None) -> float:
-    if kind == "none":
+    if kind in ("none", "node"):      # node-level: the correction is inside the gradient
         return 1.0
     if kind == "uniform":
         return c_uniform(d_l, d_g)
@@ -76,6 +83,31 @@ def coverage_factor(kind: str, d_l, d_g, s=None) -> float:
     if kind == "resampling_hm":
         return c_resampling_hm(d_l, d_g, s)
     raise ValueError(kind)
+
+
+def node_weight(p: float, q: float) -> float:
+    """Importance weight p_v(u)/q_v^t(u) of one locally present neighbour (eq. (4), S:321-327);
+    q = 0 violates Theorem 1's support condition."""
+    if not q > 0.0:
+        raise ValueError("support violation: q_v(u) = 0 (Theorem 1 precondition, S:325)")
+    return p / q
+
+
+def node_weights(d_l, d_g) -> np.ndarray:
+    """Uniform special case (eq. (9) P:283-289): w_v = p/q = (1/d_g)/(1/d_l) = d_l/d_g per target;
+    1 where d_g = 0 (no neighbours at all, nothing to correct; R30)."""
+    d_l = np.asarray(d_l, dtype=np.int64)
+    d_g = np.asarray(d_g, dtype=np.int64)
+    return np.where(d_g == 0, 1.0, d_l / np.where(d_g == 0, 1, d_g))
+
+
+def importance_expectation(p_local, values) -> float:
+    """Left side of the importance identity (eq. (3)) for a target whose local
+    neighbours are drawn uniformly (q = 1/|local|): E_{u~q}[(p(u)/q(u)) g(u)], enumerated."""
+    p_local = np.asarray(p_local, dtype=np.float64)
+    values = np.asarray(values, dtype=np.float64)
+    q = 1.0 / p_local.size
+    return float(sum(q * node_weight(p, q) * g for p, g in zip(p_local, values)))
 
 
 def aggregate(cs, grads, M: int) -> np.ndarray:

@@ -29,20 +29,27 @@ def adjacency(rowptr, col, n: int) -> sp.csr_matrix:
     return sp.csr_matrix((np.ones(col.size, dtype=np.float64), col, rowptr), shape=(n, n))
 
 
-def gcn_operator(rowptr, col, n: int) -> sp.csr_matrix:
-    """Ahat = Dt^-1/2 (A + I) Dt^-1/2 with Dt = d_l + 1 (S:270, S:83)."""
+def gcn_operator(rowptr, col, n: int, node_w=None) -> sp.csr_matrix:
+    """Ahat = Dt^-1/2 (A + I) Dt^-1/2 with Dt = d_l + 1 (S:270, S:83).
+    node_w (node-level estimator, eq. (9), reading R30): target v's neighbour
+    message is multiplied by w_v, the self term is not:  Dt^-1/2 (diag(w) A + I) Dt^-1/2."""
     A = adjacency(rowptr, col, n)
+    if node_w is not None:
+        A = sp.diags(np.asarray(node_w, dtype=np.float64)) @ A
     d_l = np.diff(np.asarray(rowptr, dtype=np.int64)).astype(np.float64)
     nrm = 1.0 / np.sqrt(d_l + 1.0)
     Dn = sp.diags(nrm)
     return (Dn @ (A + sp.identity(n, format="csr")) @ Dn).tocsr()
 
 
-def sage_operator(rowptr, col, n: int) -> sp.csr_matrix:
-    """D_l^-1 A (mean over local neighbours; zero row where d_l = 0)."""
+def sage_operator(rowptr, col, n: int, node_w=None) -> sp.csr_matrix:
+    """D_l^-1 A (mean over local neighbours; zero row where d_l = 0).
+    node_w (R30): the mean message of target v is multiplied by w_v:  diag(w) D_l^-1 A."""
     A = adjacency(rowptr, col, n)
     d_l = np.diff(np.asarray(rowptr, dtype=np.int64)).astype(np.float64)
     inv = np.where(d_l > 0, 1.0 / np.maximum(d_l, 1.0), 0.0)
+    if node_w is not None:
+        inv = inv * np.asarray(node_w, dtype=np.float64)
     return (sp.diags(inv) @ A).tocsr()
 
 
@@ -65,15 +72,17 @@ def layer_backward(arch: str, op, H, P, Ws, dZ):
     return [H.T @ dZ, P.T @ dZ], dZ @ Ws[0].T + op.T @ (dZ @ Ws[1].T)
 
 
-def operator(arch: str, rowptr, col, n: int):
-    return gcn_operator(rowptr, col, n) if arch == "gcn" else sage_operator(rowptr, col, n)
+def operator(arch: str, rowptr, col, n: int, node_w=None):
+    return (gcn_operator(rowptr, col, n, node_w) if arch == "gcn"
+            else sage_operator(rowptr, col, n, node_w))
 
 
-def forward(arch: str, rowptr, col, X, weights, masks=None):
+def forward(arch: str, rowptr, col, X, weights, masks=None, node_w=None):
     """Returns (logits, cache).  weights[l] = [W] (gcn) or [W_self, W_nbr] (sage), float64.
-    masks (optional): per hidden layer the ReLU decision to use (see layer_forward)."""
+    masks (optional): per hidden layer the ReLU decision to use (see layer_forward).
+    node_w (optional): node-level estimator weights, applied in every layer (R30)."""
     n = X.shape[0]
-    op = operator(arch, rowptr, col, n)
+    op = operator(arch, rowptr, col, n, node_w)
     H = np.asarray(X, dtype=np.float64)
     cache = dict(op=op, H=[], P=[], Z=[], M=[])
     L = len(weights)
@@ -136,10 +145,11 @@ def unflatten(theta, shapes) -> list:
     return out
 
 
-def partition_loss_grad(arch, part, X, y, weights, masks=None):
+def partition_loss_grad(arch, part, X, y, weights, masks=None, node_w=None):
     """Loss L_p and flat gradient g_p of one isolated partition (full-graph mode).
-    X is indexed by the partition's local ids (rows = part['core'])."""
-    logits, cache = forward(arch, part["rowptr"], part["col"], X, weights, masks)
+    X is indexed by the partition's local ids (rows = part['core']).  node_w: per local node
+    the node-level estimator weight (correction.node_weights), or None (batch-level kinds)."""
+    logits, cache = forward(arch, part["rowptr"], part["col"], X, weights, masks, node_w)
     loss, dZ = loss_and_dlogits(logits, y, part["seeds"])
     grads = backward(arch, cache, dZ, weights)
     return loss, flatten(grads), logits, cache

@@ -90,22 +90,28 @@ def sample_batch(part, batch_seeds, fanouts, seed_s: int, epoch: int, batch: int
     return hops[::-1]          # blocks[0] = input layer = hop L
 
 
-def block_operator(blk):
-    """D_s^-1 A_block (mean over the sampled set; zero row if none) as a sparse matrix."""
+def block_operator(blk, node_w=None):
+    """D_s^-1 A_block (mean over the sampled set; zero row if none) as a sparse matrix.
+    node_w (node-level estimator, R30): per partition-local node weight d_l/d_g; target v's
+    sampled mean is multiplied by node_w[v] (p/q with q = 1/d_l per draw, p = 1/d_g)."""
     import scipy.sparse as sp
     cnt = np.diff(blk["rowptr"]).astype(np.float64)
-    vals = np.repeat(np.where(cnt > 0, 1.0 / np.maximum(cnt, 1), 0.0), np.diff(blk["rowptr"]))
+    rs = np.where(cnt > 0, 1.0 / np.maximum(cnt, 1), 0.0)
+    if node_w is not None:
+        rs = rs * np.asarray(node_w, dtype=np.float64)[np.asarray(blk["dst"], dtype=np.int64)]
+    vals = np.repeat(rs, np.diff(blk["rowptr"]))
     return sp.csr_matrix((vals, blk["col"], blk["rowptr"]), shape=(blk["n_dst"], blk["n_src"]))
 
 
-def sage_forward(blocks, X_src, weights, masks=None):
+def sage_forward(blocks, X_src, weights, masks=None, node_w=None):
     """R27: SAGE over the blocks; X_src rows = blocks[0]['src'] (features of the outermost
-    sources).  Returns (logits over the seeds, cache)."""
+    sources).  node_w: node-level estimator weights per local node (R30) or None.
+    Returns (logits over the seeds, cache)."""
     H = np.asarray(X_src, dtype=np.float64)
     cache = dict(H=[], P=[], Z=[], M=[], ops=[])
     L = len(blocks)
     for l, (blk, Ws) in enumerate(zip(blocks, weights)):
-        op = block_operator(blk)
+        op = block_operator(blk, node_w)
         P = op @ H
         Z = H[:blk["n_dst"]] @ Ws[0] + P @ Ws[1]
         relu = l < L - 1

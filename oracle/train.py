@@ -8,7 +8,8 @@ partition), scale it by c_p, the scaled gradients are averaged ov
 active workers and one optimizer step is taken; theta is carried to the
 next phase.  Super-epochs: the partition layout is fixed for
 `repartition_every` epochs, then every worker moves to the next swept chunk of the sweep
-schedule (a2).  Reading R11: one iteration per phase in full-graph mode.
+schedule (a2).  kind "node" = the node-level estimator (eq. (9), R30): per-target weights
+d_l/d_g inside every layer's aggregation, c_p = 1.  Reading R11: one iteration per phase in full-graph mode.
 """
 from __future__ import annotations
 
@@ -48,7 +49,8 @@ def run(arch, rowptr, col, X, y, train, weights, chunk_of, C, W, M, kind, lr, ep
                 p = parts[w]
                 Xp = np.asarray(X, dtype=np.float64)[p["core"]]
                 yp = np.asarray(y)[p["core"]]
-                loss, g, _, _ = model.partition_loss_grad(arch, p, Xp, yp, Ws)
+                nw = correction.node_weights(p["d_l"], p["d_g"]) if kind == "node" else None
+                loss, g, _, _ = model.partition_loss_grad(arch, p, Xp, yp, Ws, node_w=nw)
                 cs.append(partition_factor(kind, p)); gs.append(g); losses.append(loss)
             g_hat = correction.aggregate(cs, gs, len(active))
             theta = correction.sgd(theta, g_hat, lr)
