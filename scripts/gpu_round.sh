@@ -1,0 +1,31 @@
+# Round check on one B200: GPU parity tests, smoke(), the default bench line (with e2e and the
+# oracle cpu_baseline), the reference arm, the ncu launch list of the bench command, and one
+# ncu --set full capture of a products phase.  Everything lands in gpurun_out/.
+# Usage (from the repo root, via gpurun): bash scripts/gpu_round.sh [tag]
+TAG=${1:-r01}
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${TAG}_smi.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1
+echo "pytest gpu exit $?"; tail -3 gpurun_out/${TAG}_pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1
+echo "smoke exit $?"; tail -2 gpurun_out/${TAG}_smoke.log
+timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
+echo "bench exit $?"; tail -c 600 gpurun_out/${TAG}_bench.json
+timeout 600 python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/${TAG}_bench_ref.json 2> gpurun_out/${TAG}_bench_ref.err
+echo "ref exit $?"; tail -c 300 gpurun_out/${TAG}_bench_ref.json
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline \
+  > gpurun_out/${TAG}_bench_under_ncu.log 2>&1
+echo "ncu launches exit $?"
+python scripts/ncu_summary.py launches gpurun_out/${TAG}_launches.csv > gpurun_out/${TAG}_launches.txt 2>&1
+head -30 gpurun_out/${TAG}_launches.txt
+if [ "${NCU_FULL:-1}" = "1" ]; then
+  timeout 1200 ncu --profile-from-start off --set full --clock-control none --import-source on \
+    -o /tmp/phase_full python scripts/ncu_phase.py products bf16 gpurun_out/ncu_phase_calls.json \
+    > gpurun_out/${TAG}_ncu_phase.log 2>&1
+  echo "ncu full exit $?"
+  python scripts/ncu_summary.py full /tmp/phase_full.ncu-rep --calls gpurun_out/ncu_phase_calls.json \
+    > gpurun_out/${TAG}_ncu_summary.json
+  ncu -i /tmp/phase_full.ncu-rep --page details --csv > gpurun_out/${TAG}_phase_details.csv 2>/dev/null
+fi
+ls -la gpurun_out | tail -20
