@@ -40,6 +40,9 @@ def parse():
     ap.add_argument("--impl", default="grappa", choices=["grappa", "reference"])
     ap.add_argument("--config", default="products")
     ap.add_argument("--dtype", default="bf16", choices=["f32", "bf16"])
+    ap.add_argument("--corr", default=None,
+                    choices=["none", "uniform", "resampling", "resampling_hm", "node"],
+                    help="override the config's estimator (node = node-level eq. (9), R30)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--variant", action="append", default=[],
                     help="kernel A/B knob op=value (grappa_set_kernel_variant), e.g. spmm=2")
@@ -136,7 +139,7 @@ class OracleSample:
     P and correction.  One `phase(i)` = the oracle's repartition of partition i + its
     forward/loss/backward + coverage-corrected aggregation + SGD (Alg. 1 with M = 1)."""
 
-    def __init__(self, name: str, shrink: int = 8):
+    def __init__(self, name: str, shrink: int = 8, corr: str | None = None):
         import gen
         from oracle import partition as Po
         wl0 = gen.WORKLOADS[name]
@@ -151,6 +154,7 @@ class OracleSample:
         self.chunk_of = Po.make_chunks(n, self.wl.chunks, gen.seed_of("chunks"))
         self.pairs = Po.sweep_schedule(self.wl.chunks, self.wl.chunks)[0]
         self.shrink = shrink
+        self.corr = corr or self.wl.correction
 
     def phase(self, i: int) -> float:
         from oracle import correction as Co
@@ -166,9 +170,10 @@ class OracleSample:
         t0 = time.perf_counter()
         b, s = self.pairs[i % wl.chunks]
         part = Po.induced_partition(ds.rowptr, ds.col, self.chunk_of, b, s, ds.train)
+        nw = Co.node_weights(part["d_l"], part["d_g"]) if self.corr == "node" else None
         _, g, _, _ = Mo.partition_loss_grad(wl.arch, part, self.X[part["core"]],
-                                            ds.y[part["core"]], self.W)
-        c = Tr.partition_factor(wl.correction, part)
+                                            ds.y[part["core"]], self.W, node_w=nw)
+        c = Tr.partition_factor(self.corr, part)
         Co.sgd(Mo.flatten(self.W), Co.aggregate([c], [g], 1), 0.003)
         dt = time.perf_counter() - t0
         if lim is not None and hasattr(lim, "unregister"):
@@ -182,9 +187,9 @@ class OracleSample:
                 f"timed (repartition + fwd/bwd + aggregate + SGD), epoch = x{self.wl.chunks} phases")
 
 
-def oracle_baseline(name: str, budget_s: float = 30.0):
+def oracle_baseline(name: str, budget_s: float = 30.0, corr: str | None = None):
     """cpu_baseline leg: phases of one epoch of the sample until ~budget_s of CPU work."""
-    o = OracleSample(name)
+    o = OracleSample(name, corr=corr)
     ts = []
     while len(ts) < o.wl.chunks and sum(ts) < budget_s:
         ts.append(o.phase(len(ts)))
@@ -199,7 +204,7 @@ def run_reference(args):
     paper ships none).  Rank 0 only; each step = one partition-phase of the 1/8 sample."""
     if int(os.environ.get("RANK", "0")) != 0:
         return
-    o = OracleSample(args.config)
+    o = OracleSample(args.config, corr=args.corr)
     K, W = args.steps, args.warmup
     for i in range(W):
         o.phase(i)
@@ -211,7 +216,7 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": statistics.mean(ts) * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": workload_desc(args.config, args.gpus), "sample": desc},
+            "config": {"workload": workload_desc(args.config, args.gpus, args.corr), "sample": desc},
             "cpu_baseline": {"value": value, "unit": "edges/s", "cores": 1, "kind": "oracle",
                              "sample": desc},
             "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0,
@@ -219,11 +224,11 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def workload_desc(name: str, world: int) -> str:
+def workload_desc(name: str, world: int, corr: str | None = None) -> str:
     import gen
     wl = gen.WORKLOADS[name]
     return (f"{name}-shaped RMAT ({wl.n} nodes), {wl.arch.upper()}-{wl.depth}, P={wl.chunks} "
-            f"partitions, M={world} per phase, full-graph, {wl.correction} correction, "
+            f"partitions, M={world} per phase, full-graph, {corr or wl.correction} correction, "
             f"repartition every {wl.repartition_every} epochs")
 
 
@@ -261,7 +266,7 @@ def run_grappa(args):
     t_gen = time.perf_counter() - t_gen
     spec = ModelSpec(wl.arch, wl.dims, wl.dims_pad)
     stream = torch.cuda.current_stream(dev)
-    common = dict(corr=wl.correction, lr=0.003, repartition_every=wl.repartition_every,
+    common = dict(corr=args.corr or wl.correction, lr=0.003, repartition_every=wl.repartition_every,
                   dtype=args.dtype, stream=stream, num_workers=wl.extra.get("workers"))
     if wl.extra.get("mode") == "minibatch":
         tr = MinibatchTrainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights,
@@ -296,17 +301,18 @@ def run_grappa(args):
         barrier()
     ctx.profile(not use_graph)
     l0 = ctx.launches()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
+    for k in range(args.steps):
         if use_graph:
             tr.run_epoch_graph()
         else:
             tr.run_epoch()
-    ev1.record(stream)
+        evs[k + 1].record(stream)
     barrier()
     clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1)
+    ms = evs[0].elapsed_time(evs[-1])
+    per_epoch = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
     launches = ctx.launches() - l0
     if use_graph:
         launches += tr.graph_launches * args.steps
@@ -354,18 +360,21 @@ def run_grappa(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_baseline(args.config)
+        cpu = oracle_baseline(args.config, corr=args.corr)
 
     if rank == 0:
         line = {"metric": "edges_per_sec", "value": value, "unit": "edges/s", "n_gpus": world,
                 "steps": K, "warmup": args.warmup, "ms_per_step": ms / K,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32" if args.dtype == "f32" else "bf16", "data": "synthetic",
-                "config": {"workload": workload_desc(args.config, world),
+                "config": {"workload": workload_desc(args.config, world, args.corr),
                            "nnz_global": nnz, "partitions": wl.chunks, "phases_per_epoch": -(-wl.chunks // world),
                            "repartitions_timed": -(-K // wl.repartition_every),
                            "repartition_ms_total": rep_ms,
                            "epoch_ms_excl_repartition": (ms - rep_ms) / K,
+                           "epoch_ms": {"median": statistics.median(per_epoch), "min": min(per_epoch),
+                                        "max": max(per_epoch), "note": "rank-local CUDA events; the "
+                                        "epoch holding the repartition is the max"},
                            "l2": "inputs larger than L2 (graph+features ~1.6 GB, activations ~2.8 GB); no flush",
                            "parallelism": f"dp{world} (phase-parallel, gradient-only)",
                            "generate_s": round(t_gen, 1)},

@@ -51,12 +51,16 @@ typedef enum { GRAPPA_GCN = 0, GRAPPA_SAGE = 1 } grappa_arch;
  *  UNIFORM        eq:correction_uniform P:303-305, the minimum-distance factor (Thm 2)
  *  RESAMPLING     eq:resampling P:344-346 literal, with SPEC guards D<eps -> 1, cap c_max
  *                 (S:351); the paper's deployed factor
- *  RESAMPLING_HM  reading R13 (not the default): sum s_v / sum s_v d_g/d_l            */
+ *  RESAMPLING_HM  reading R13 (not the default): sum s_v / sum s_v d_g/d_l
+ *  NODE           node-level estimator (eq. (4)/(9) P:249-289, reading R30): the
+ *                 correction lives inside the gradient (layer calls with
+ *                 GRAPPA_LAYER_NODE_LEVEL, per-target weights d_l/d_g); the batch factor is 1 */
 typedef enum {
     GRAPPA_CORR_NONE = 0,
     GRAPPA_CORR_UNIFORM = 1,
     GRAPPA_CORR_RESAMPLING = 2,
-    GRAPPA_CORR_RESAMPLING_HM = 3
+    GRAPPA_CORR_RESAMPLING_HM = 3,
+    GRAPPA_CORR_NODE = 4
 } grappa_corr;
 
 typedef struct grappa_ctx grappa_ctx;    /* per process + GPU: NCCL comm, workspaces      */
@@ -96,6 +100,11 @@ typedef struct {
     double c_resampling;        /* eq:resampling with guards (eps 1e-9, c_max 10)       */
     double c_resampling_hm;     /* reading R13                                          */
     int64_t D;                  /* sum_{seeds, d_l>0} (d_g - d_l), exact integer        */
+    /* node-level estimator weights (eq. (9), R30), three fp32 rows of n_core:
+     *   [0, n)   w_v = d_l/d_g (1 where d_g = 0)
+     *   [n, 2n)  w_v * norm_gcn[v]        (GCN backward gather scale)
+     *   [2n, 3n) w_v * norm_sage[v] = 1/d_g where d_l > 0, else 0 (SAGE mean scale)      */
+    const float* node_w;
 } grappa_part_info;
 
 /* ----------------------------------------------------------------------------------- */
@@ -153,6 +162,7 @@ typedef struct {
     int32_t* seeds;         /* [n_seeds]  */
     int32_t* labels;        /* [n_core]   */
     void* x;                /* [n_core x feat_dim] */
+    float* node_w;          /* [3 x n_core] (grappa_part_info.node_w) */
 } grappa_part_host;
 /* device -> host copy of the selected arrays (enqueued on stream) */
 grappa_status grappa_part_download(const grappa_part* part, const grappa_part_host* dst, void* stream);
@@ -184,6 +194,20 @@ grappa_status grappa_layer_fwd(grappa_ctx* ctx, const grappa_part* part, grappa_
                                const float* w, void* h_out, void* saved, void* ws,
                                grappa_dtype dtype, void* stream);
 
+/* Layer flags (grappa_layer_fwd_ex / grappa_layer_bwd_ex / grappa_minibatch_step_ex):
+ *   GRAPPA_LAYER_NODE_LEVEL : node-level estimator (eq. (4)/(9) P:249-289; R30) --
+ *     every target's aggregated neighbour message is multiplied by w_v = d_l/d_g:
+ *       GCN  Ahat_w = N (diag(w) A_loc + I) N   (self term unweighted)
+ *       SAGE M = diag(w) D_l^-1 A_loc h_in       (= local sum / d_g)
+ *     and the backward is the exact transpose (Ahat_w^T = N (A_loc diag(w) + I) N).
+ *     Pair it with GRAPPA_CORR_NODE in the aggregation (batch factor 1).               */
+#define GRAPPA_LAYER_NODE_LEVEL 4u
+/* grappa_layer_fwd with flags (0 = grappa_layer_fwd).  Errors: E_ARG for unknown flags. */
+grappa_status grappa_layer_fwd_ex(grappa_ctx* ctx, const grappa_part* part, grappa_arch arch,
+                                  int32_t f_in, int32_t f_out, int relu, const void* h_in,
+                                  const float* w, void* h_out, void* saved, void* ws,
+                                  grappa_dtype dtype, unsigned flags, void* stream);
+
 /* a6 -- the layer's backward (exact reverse mode; ReLU'(0) = 0, R16):
  *   dz_out   dev [n_core x f_out]: dL/dZ of THIS layer's pre-activation output.
  *   dw       dev fp32, same shape as w: dL/dW, combined over row splits in fixed order.
@@ -203,8 +227,9 @@ grappa_status grappa_layer_bwd(grappa_ctx* ctx, const grappa_part* part, grappa_
  * gradients pre-multiplied by N, so every backward aggregation gathers unweighted rows.
  *   GRAPPA_BWD_DZ_OUT_NORMED : dz_out holds N dz_out.
  *   GRAPPA_BWD_DZ_IN_NORMED  : dz_in receives N dz_in (the relu' gate is applied as usual).
- * dw is the same in every mode.  flags = 0 is grappa_layer_bwd.  Errors: E_ARG for unknown
- * flags or flags != 0 with arch SAGE. */
+ * dw is the same in every mode.  flags = 0 is grappa_layer_bwd.  GRAPPA_LAYER_NODE_LEVEL (any
+ * arch) backpropagates through the node-level operator of grappa_layer_fwd_ex.  Errors: E_ARG
+ * for unknown flags or a normalised-gradient flag with arch SAGE. */
 #define GRAPPA_BWD_DZ_OUT_NORMED 1u
 #define GRAPPA_BWD_DZ_IN_NORMED 2u
 grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part* part, grappa_arch arch,
@@ -228,7 +253,8 @@ grappa_status grappa_loss(grappa_ctx* ctx, const grappa_part* part, const void* 
  *   ncclAllReduce(sum) across the context's ranks  =>  grad = (1/M) sum_p c_p g_p (R9),
  *   then, if lr != 0, theta <- theta - lr * grad (SGD, R10).
  *   part == NULL marks a rank with no active partition in this phase (contributes zeros).
- *   c_p is the factor of kind `corr` computed at repartition time (grappa_part_info).
+ *   c_p is the factor of kind `corr` computed at repartition time (grappa_part_info); 1 for
+ *   GRAPPA_CORR_NONE and GRAPPA_CORR_NODE (node-level: the correction is in the gradient).
  *   grad, theta: dev fp32 [n_params].  A COLLECTIVE when the ctx has >1 rank.           */
 grappa_status grappa_aggregate_grads(grappa_ctx* ctx, const grappa_part* part, grappa_corr corr,
                                      float* grad, int64_t n_params, int32_t m_active, float lr,
@@ -260,6 +286,7 @@ typedef struct {
     const int32_t* t_col;       /* dev [nnz]                                                */
     const float* inv_cnt;       /* dev [n_dst]    1/|S(v)|, 0 for an empty sample           */
     const int32_t* src;         /* dev [n_src]    partition-local id of each source         */
+    const float* inv_cnt_node;  /* dev [n_dst]    (d_l/d_g)(v) / |S(v)| (node-level, R30)   */
 } grappa_block_info;
 
 /* Epoch order of the partition's seeds (R23): order dev int32[n_seeds] (out, local ids). */
@@ -295,6 +322,13 @@ grappa_status grappa_minibatch_step(grappa_ctx* ctx, const grappa_part* part, co
                                     const float* theta, float* grad, void* ws, size_t ws_bytes,
                                     double* loss_dev, void* const* hidden_out, grappa_dtype dtype,
                                     void* stream);
+/* with flags: GRAPPA_LAYER_NODE_LEVEL scales every target's sampled mean by d_l/d_g (R30;
+ * inv_cnt_node instead of inv_cnt, forward and backward).  flags = 0 is the call above. */
+grappa_status grappa_minibatch_step_ex(grappa_ctx* ctx, const grappa_part* part, const grappa_batch* b,
+                                       int32_t n_layers, const int32_t* dims_pad, int32_t num_classes,
+                                       const float* theta, float* grad, void* ws, size_t ws_bytes,
+                                       double* loss_dev, void* const* hidden_out, grappa_dtype dtype,
+                                       unsigned flags, void* stream);
 
 /* Sync the stream and report asynchronous faults: E_NONFINITE if any aggregated gradient
  * since the last check was non-finite, E_CUDA / E_NCCL on device or communicator errors. */

@@ -13,7 +13,8 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, CORR, F32, GCN, SAGE, GrappaError, load
+from ._lib import (BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, CORR, F32, GCN, LAYER_NODE_LEVEL, SAGE,
+                   GrappaError, load)
 
 __all__ = ["Context", "Part", "grappa_partition", "grappa_repartition", "grappa_layer_fwd",
            "grappa_layer_bwd", "grappa_layer_bwd_ex", "grappa_loss", "grappa_aggregate_grads", "GCN", "SAGE", "F32",
@@ -122,6 +123,7 @@ class Part:
         self.norm_sage = _view(I.norm_sage, (n,), "<f4", self)
         self.seeds = _view(I.seeds, (s,), "<i4", self)
         self.labels = _view(I.labels, (n,), "<i4", self)
+        self.node_w = _view(I.node_w, (3, n), "<f4", self)
         if I.feat_dim:
             if I.dtype == BF16:
                 self.x = _view(I.x, (n, I.feat_dim), "<i2", self).view(torch.bfloat16)
@@ -139,7 +141,8 @@ class Part:
         bufs = dict(rowptr=pin(I.n_core + 1, torch.int64), col=pin(I.nnz, torch.int32),
                     d_l=pin(I.n_core, torch.int32), norm_gcn=pin(I.n_core, torch.float32),
                     norm_sage=pin(I.n_core, torch.float32), seeds=pin(I.n_seeds, torch.int32),
-                    labels=pin(I.n_core, torch.int32), x=pin(I.n_core * I.feat_dim, tdt))
+                    labels=pin(I.n_core, torch.int32), x=pin(I.n_core * I.feat_dim, tdt),
+                    node_w=pin(3 * I.n_core, torch.float32))
         st = _lib.PartHost(**{k: v.data_ptr() for k, v in bufs.items()})
         return bufs, st
 
@@ -154,7 +157,7 @@ class Part:
     def factor(self, corr: str) -> float:
         I = self.info
         return {"none": 1.0, "uniform": I.c_uniform, "resampling": I.c_resampling,
-                "resampling_hm": I.c_resampling_hm}[corr]
+                "resampling_hm": I.c_resampling_hm, "node": 1.0}[corr]
 
     def destroy(self):
         if self.h:
@@ -203,6 +206,14 @@ def grappa_layer_fwd(ctx: Context, part: Part, arch, f_in, f_out, relu, h_in, w,
     _lib.check("grappa_layer_fwd", ctx.lib.grappa_layer_fwd(
         ctx.h, part.h, arch_code(arch), f_in, f_out, int(relu), _lib.ptr(h_in), _lib.ptr(w),
         _lib.ptr(h_out), _lib.ptr(saved), _lib.ptr(ws), dtype_code(dtype), _lib.stream_ptr(stream)))
+
+
+def grappa_layer_fwd_ex(ctx: Context, part: Part, arch, f_in, f_out, relu, h_in, w, h_out, saved, ws,
+                        dtype, flags: int, stream=None):
+    _lib.check("grappa_layer_fwd_ex", ctx.lib.grappa_layer_fwd_ex(
+        ctx.h, part.h, arch_code(arch), f_in, f_out, int(relu), _lib.ptr(h_in), _lib.ptr(w),
+        _lib.ptr(h_out), _lib.ptr(saved), _lib.ptr(ws), dtype_code(dtype), int(flags),
+        _lib.stream_ptr(stream)))
 
 
 def grappa_layer_bwd(ctx: Context, part: Part, arch, f_in, f_out, relu_in, dz_out, h_in, w, saved,
@@ -262,12 +273,13 @@ class Batch:
                 t_rowptr=_view(bi.t_rowptr, (bi.n_src + 1,), "<i8", self),
                 t_col=_view(bi.t_col, (bi.nnz,), "<i4", self),
                 inv_cnt=_view(bi.inv_cnt, (bi.n_dst,), "<f4", self),
+                inv_cnt_node=_view(bi.inv_cnt_node, (bi.n_dst,), "<f4", self),
                 src=_view(bi.src, (bi.n_src,), "<i4", self)))
         cu, cr, ch = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
         _lib.check("grappa_batch_factors", lib.grappa_batch_factors(
             self.h, ctypes.byref(cu), ctypes.byref(cr), ctypes.byref(ch)))
         self.factors = {"none": 1.0, "uniform": cu.value, "resampling": cr.value,
-                        "resampling_hm": ch.value}
+                        "resampling_hm": ch.value, "node": 1.0}
         return self
 
     def destroy(self):
@@ -305,13 +317,13 @@ def minibatch_ws_bytes(batch: Batch, dims_pad, dtype) -> int:
 
 
 def grappa_minibatch_step(ctx: Context, part: Part, batch: Batch, dims_pad, num_classes: int, theta,
-                          grad, ws, loss_dev, dtype, hidden_out=None, stream=None):
+                          grad, ws, loss_dev, dtype, hidden_out=None, stream=None, flags: int = 0):
     L = len(dims_pad) - 1
     dp = (ctypes.c_int32 * (L + 1))(*dims_pad)
     hid = None
     if hidden_out is not None:
         hid = (ctypes.c_void_p * max(1, L - 1))(*[t.data_ptr() for t in hidden_out])
-    _lib.check("grappa_minibatch_step", ctx.lib.grappa_minibatch_step(
+    _lib.check("grappa_minibatch_step_ex", ctx.lib.grappa_minibatch_step_ex(
         ctx.h, part.h, batch.h, L, dp, num_classes, _lib.ptr(theta), _lib.ptr(grad), _lib.ptr(ws),
-        ws.numel() * ws.element_size(), _lib.ptr(loss_dev), hid, dtype_code(dtype),
+        ws.numel() * ws.element_size(), _lib.ptr(loss_dev), hid, dtype_code(dtype), int(flags),
         _lib.stream_ptr(stream)))

@@ -14,8 +14,9 @@ LIB_PATH = os.path.join(_HERE, "libgrappa.so")
 
 F32, BF16 = 0, 1
 GCN, SAGE = 0, 1
-CORR = {"none": 0, "uniform": 1, "resampling": 2, "resampling_hm": 3}
+CORR = {"none": 0, "uniform": 1, "resampling": 2, "resampling_hm": 3, "node": 4}
 BWD_DZ_OUT_NORMED, BWD_DZ_IN_NORMED = 1, 2
+LAYER_NODE_LEVEL = 4
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_EMPTY", 4: "E_NONFINITE", 5: "E_SUPPORT",
           6: "E_NOMEM", 7: "E_CUDA", 8: "E_NCCL"}
 
@@ -28,7 +29,8 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_set_kernel_variant", "grappa_aggregate_grads_c", "grappa_epoch_seeds",
            "grappa_sample", "grappa_batch_query", "grappa_batch_factors", "grappa_batch_destroy",
            "grappa_minibatch_ws_bytes", "grappa_minibatch_step", "grappa_part_download",
-           "grappa_part_upload", "grappa_layer_bwd_ex"]
+           "grappa_part_upload", "grappa_layer_bwd_ex", "grappa_layer_fwd_ex",
+           "grappa_minibatch_step_ex"]
 KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5, "sample": 6}
 
 
@@ -53,19 +55,21 @@ class PartInfo(ctypes.Structure):
                 ("seeds", ctypes.c_void_p), ("labels", ctypes.c_void_p), ("x", ctypes.c_void_p),
                 ("n_heavy", ctypes.c_int64), ("n_slots", ctypes.c_int64),
                 ("c_uniform", ctypes.c_double), ("c_resampling", ctypes.c_double),
-                ("c_resampling_hm", ctypes.c_double), ("D", ctypes.c_int64)]
+                ("c_resampling_hm", ctypes.c_double), ("D", ctypes.c_int64),
+                ("node_w", ctypes.c_void_p)]
 
 
 class PartHost(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in
-                ("rowptr", "col", "d_l", "norm_gcn", "norm_sage", "seeds", "labels", "x")]
+                ("rowptr", "col", "d_l", "norm_gcn", "norm_sage", "seeds", "labels", "x", "node_w")]
 
 
 class BlockInfo(ctypes.Structure):
     _fields_ = [("n_dst", ctypes.c_int32), ("n_src", ctypes.c_int32), ("nnz", ctypes.c_int64),
                 ("rowptr", ctypes.c_void_p), ("col", ctypes.c_void_p),
                 ("t_rowptr", ctypes.c_void_p), ("t_col", ctypes.c_void_p),
-                ("inv_cnt", ctypes.c_void_p), ("src", ctypes.c_void_p)]
+                ("inv_cnt", ctypes.c_void_p), ("src", ctypes.c_void_p),
+                ("inv_cnt_node", ctypes.c_void_p)]
 
 
 _lib = None
@@ -102,6 +106,8 @@ def load(path: str = LIB_PATH):
                                   vp, vp, ctypes.c_int, vp]),
         "grappa_layer_bwd_ex": (st, [vp, vp, ctypes.c_int, i32, i32, ctypes.c_int, vp, vp, vp, vp, vp,
                                      vp, vp, ctypes.c_int, ctypes.c_uint, vp]),
+        "grappa_layer_fwd_ex": (st, [vp, vp, ctypes.c_int, i32, i32, ctypes.c_int, vp, vp, vp, vp, vp,
+                                     ctypes.c_int, ctypes.c_uint, vp]),
         "grappa_loss": (st, [vp, vp, vp, i32, i32, vp, vp, ctypes.c_int, vp]),
         "grappa_aggregate_grads": (st, [vp, vp, ctypes.c_int, vp, i64, i32, f32, vp, vp]),
         "grappa_check": (st, [vp, vp]),
@@ -118,6 +124,8 @@ def load(path: str = LIB_PATH):
         "grappa_batch_destroy": (None, [vp]),
         "grappa_minibatch_ws_bytes": (sz, [vp, i32, vp, ctypes.c_int]),
         "grappa_minibatch_step": (st, [vp, vp, vp, i32, vp, i32, vp, vp, vp, sz, vp, vp, ctypes.c_int, vp]),
+        "grappa_minibatch_step_ex": (st, [vp, vp, vp, i32, vp, i32, vp, vp, vp, sz, vp, vp, ctypes.c_int,
+                                          ctypes.c_uint, vp]),
         "grappa_profile_read": (st, [vp, ctypes.c_int, ctypes.POINTER(dbl), ctypes.POINTER(i64),
                                      ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
     }

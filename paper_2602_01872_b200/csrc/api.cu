@@ -237,13 +237,26 @@ extern "C" grappa_status grappa_layer_fwd(grappa_ctx* ctx, const grappa_part* pa
                                           int32_t f_in, int32_t f_out, int relu, const void* h_in,
                                           const float* w, void* h_out, void* saved, void* ws,
                                           grappa_dtype dtype, void* stream) {
+    return grappa_layer_fwd_ex(ctx, part, arch, f_in, f_out, relu, h_in, w, h_out, saved, ws, dtype, 0u,
+                               stream);
+}
+
+extern "C" grappa_status grappa_layer_fwd_ex(grappa_ctx* ctx, const grappa_part* part, grappa_arch arch,
+                                             int32_t f_in, int32_t f_out, int relu, const void* h_in,
+                                             const float* w, void* h_out, void* saved, void* ws,
+                                             grappa_dtype dtype, unsigned flags, void* stream) {
+    GRAPPA_ARG((flags & ~GRAPPA_LAYER_NODE_LEVEL) == 0, GRAPPA_E_ARG, "grappa_layer_fwd_ex: flags 0x%x invalid",
+               flags);
     GRAPPA_ARG(ctx && part && h_in && w && h_out && ws, GRAPPA_E_ARG, "grappa_layer_fwd: null argument");
     GRAPPA_TRY(check_dims("grappa_layer_fwd", f_in, f_out));
     GRAPPA_ARG(arch != GRAPPA_SAGE || saved, GRAPPA_E_ARG, "grappa_layer_fwd: SAGE needs `saved`");
     cudaStream_t s = (cudaStream_t)stream;
     const grappa_part_info& I = part->info;
+    const bool node = flags & GRAPPA_LAYER_NODE_LEVEL;
+    const float* w_node = node ? I.node_w : nullptr;                       // w_v
+    const float* sage_scale = node ? I.node_w + 2 * I.n_core : I.norm_sage;  // w_v / d_l
     WsLayout L = carve(part, arch, f_in, f_out, dtype, ws);
-    if (arch == GRAPPA_GCN && f_in <= f_out && spmm_mm_supported(part, f_in, f_out, dtype)) {
+    if (arch == GRAPPA_GCN && !node && f_in <= f_out && spmm_mm_supported(part, f_in, f_out, dtype)) {
         // h_out = act((Ahat h_in) W): aggregate at the narrower width, transform fused into
         // the aggregation kernel (tcgen05 on the smem-resident tile)
         AggMMArgs m;
@@ -261,14 +274,16 @@ extern "C" grappa_status grappa_layer_fwd(grappa_ctx* ctx, const grappa_part* pa
         g.row_scale = I.norm_gcn;
         GRAPPA_TRY(gemm_nn(ctx, g, dtype, s));
         // h_out = act(n_v (T'_v + sum T'_u)) = act(n_v (n_v T_v + sum n_u T_u))
+        // node-level: act(n_v (T'_v + w_v sum T'_u))
         SpmmArgs a;
         a.X = L.node; a.width = f_out; a.row_scale = I.norm_gcn; a.col_scale = nullptr;
+        a.nbr_scale = w_node;
         a.self = 1; a.relu = relu; a.out = h_out; a.partial = L.partial;
         return spmm(ctx, part, a, dtype, s);
     }
-    // SAGE: M = D^-1 A h_in ; h_out = act([h_in | M] [Ws; Wn])
+    // SAGE: M = D^-1 A h_in (node-level: diag(w) D^-1 A h_in) ; h_out = act([h_in | M] [Ws; Wn])
     SpmmArgs a;
-    a.X = h_in; a.width = f_in; a.row_scale = I.norm_sage; a.out = saved; a.partial = L.partial;
+    a.X = h_in; a.width = f_in; a.row_scale = sage_scale; a.out = saved; a.partial = L.partial;
     GRAPPA_TRY(spmm(ctx, part, a, dtype, s));
     GemmArgs g;
     g.M = I.n_core; g.K1 = f_in; g.K2 = f_in; g.N = f_out; g.A1 = h_in; g.A2 = saved; g.B = w;
@@ -290,9 +305,10 @@ extern "C" grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part*
                                              const void* h_in, const float* w, const void* saved,
                                              float* dw, void* dz_in, void* ws, grappa_dtype dtype,
                                              unsigned flags, void* stream) {
-    GRAPPA_ARG((flags & ~3u) == 0 && (flags == 0 || arch == GRAPPA_GCN), GRAPPA_E_ARG,
-               "grappa_layer_bwd_ex: flags 0x%x invalid (normalised gradients are GCN-only)", flags);
+    GRAPPA_ARG((flags & ~(3u | GRAPPA_LAYER_NODE_LEVEL)) == 0 && ((flags & 3u) == 0 || arch == GRAPPA_GCN),
+               GRAPPA_E_ARG, "grappa_layer_bwd_ex: flags 0x%x invalid (normalised gradients are GCN-only)", flags);
     const bool out_normed = flags & GRAPPA_BWD_DZ_OUT_NORMED, in_normed = flags & GRAPPA_BWD_DZ_IN_NORMED;
+    const bool node = flags & GRAPPA_LAYER_NODE_LEVEL;
     GRAPPA_ARG(ctx && part && dz_out && h_in && w && dw && ws, GRAPPA_E_ARG,
                "grappa_layer_bwd: null argument");
     GRAPPA_TRY(check_dims("grappa_layer_bwd", f_in, f_out));
@@ -314,9 +330,15 @@ extern "C" grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part*
     }
     if (arch == GRAPPA_GCN) {
         // dT = Ahat dz_out = N (A + I) (N dz_out): with a pre-normalised dz_out the SpMM
-        // gathers unweighted rows
+        // gathers unweighted rows.  Node-level (R30): Ahat_w^T dz = N (A diag(w) + I) (N dz) --
+        // neighbours gathered with scale w_u (w_u n_u unnormalised), self term unweighted
         SpmmArgs a;
         a.X = dz_out; a.width = f_out; a.row_scale = I.norm_gcn; a.col_scale = out_normed ? nullptr : I.norm_gcn;
+        if (node) {
+            a.col_scale = out_normed ? I.node_w : I.node_w + I.n_core;
+            a.self_sep = 1;
+            a.self_scale = out_normed ? nullptr : I.norm_gcn;
+        }
         a.self = 1; a.out = L.node; a.partial = L.partial;
         GRAPPA_TRY(spmm(ctx, part, a, dtype, s));
         // dW = h_in^T dT
@@ -343,7 +365,7 @@ extern "C" grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part*
     g.n_split = f_in; g.C1 = dz_in; g.C2 = L.node;
     GRAPPA_TRY(gemm_nn(ctx, g, dtype, s));
     SpmmArgs a;
-    a.X = L.node; a.width = f_in; a.col_scale = I.norm_sage; a.accumulate = 1;
+    a.X = L.node; a.width = f_in; a.col_scale = node ? I.node_w + 2 * I.n_core : I.norm_sage; a.accumulate = 1;
     a.mask = relu_in ? h_in : nullptr; a.out = dz_in; a.partial = L.partial;
     return spmm(ctx, part, a, dtype, s);
 }
@@ -391,6 +413,7 @@ extern "C" grappa_status grappa_aggregate_grads(grappa_ctx* ctx, const grappa_pa
         const grappa_part_info& I = part->info;
         switch (corr) {
             case GRAPPA_CORR_NONE: c = 1.0; break;
+            case GRAPPA_CORR_NODE: c = 1.0; break;      // correction inside the gradient (R30)
             case GRAPPA_CORR_UNIFORM: c = I.c_uniform; break;
             case GRAPPA_CORR_RESAMPLING: c = I.c_resampling; break;
             case GRAPPA_CORR_RESAMPLING_HM: c = I.c_resampling_hm; break;

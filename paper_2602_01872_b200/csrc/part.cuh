@@ -15,6 +15,8 @@ grappa_status loss_rows(grappa_ctx* ctx, int64_t n_seeds, const int32_t* rows, c
 struct grappa_part {
     grappa_part_info info{};
     grappa::DevBuf rowptr, col, core_global, d_l, d_g, norm_gcn, norm_sage, seeds, labels, x;
+    // node-level estimator weights (R30): [w | w*norm_gcn | w*norm_sage], 3 x n_core fp32
+    grappa::DevBuf node_w;
     // SpMM row splitting (rows with d_l > kSegLen): every segment of a split row is one
     // "slot" task (row, segment); slot_off gives each split row's first slot.
     grappa::DevBuf heavy_rows, heavy_slot_off, slot_row, slot_seg;

@@ -135,7 +135,7 @@ __global__ void k_row_finalize(int64_t n_core, const int32_t* __restrict__ task_
                                const int64_t* __restrict__ task_out, const int32_t* __restrict__ core_global,
                                const int64_t* __restrict__ g_rowptr, const int32_t* __restrict__ g_labels,
                                int64_t* rowptr, int32_t* d_l, int32_t* d_g, float* norm_gcn, float* norm_sage,
-                               int32_t* labels) {
+                               float* node_w, int32_t* labels) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_core;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t a = task_out[task_off[i]], b = task_out[task_off[i + 1]];
@@ -144,9 +144,16 @@ __global__ void k_row_finalize(int64_t n_core, const int32_t* __restrict__ task_
         rowptr[i] = a;
         if (i == n_core - 1) rowptr[n_core] = b;
         d_l[i] = cnt;
-        d_g[i] = (int32_t)(g_rowptr[v + 1] - g_rowptr[v]);
-        norm_gcn[i] = (float)(1.0 / sqrt((double)cnt + 1.0));
-        norm_sage[i] = cnt > 0 ? (float)(1.0 / (double)cnt) : 0.0f;
+        const int32_t dg = (int32_t)(g_rowptr[v + 1] - g_rowptr[v]);
+        d_g[i] = dg;
+        const double ng = 1.0 / sqrt((double)cnt + 1.0), ns = cnt > 0 ? 1.0 / (double)cnt : 0.0;
+        norm_gcn[i] = (float)ng;
+        norm_sage[i] = (float)ns;
+        // node-level estimator (eq. (9), R30): w = d_l/d_g, 1 iff d_g = 0
+        const double w = dg == 0 ? 1.0 : (double)cnt / (double)dg;
+        node_w[i] = (float)w;
+        node_w[n_core + i] = (float)(w * ng);
+        node_w[2 * n_core + i] = (float)(w * ns);
         labels[i] = g_labels ? g_labels[v] : 0;
     }
 }
@@ -372,6 +379,7 @@ extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g
     RP_TRY(p->d_g.grow(n_core * 4));
     RP_TRY(p->norm_gcn.grow(n_core * 4));
     RP_TRY(p->norm_sage.grow(n_core * 4));
+    RP_TRY(p->node_w.grow(n_core * 12));
     RP_TRY(p->labels.grow(n_core * 4));
     RP_TRY(p->rowptr.grow((n_core + 1) * 8));
     RP_TRY(p->seeds.grow(n_core * 4));
@@ -402,7 +410,7 @@ extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g
     k_row_finalize<<<grid, 256, 0, s>>>(n_core, task_off, task_out, core_global, g->rowptr, labels,
                                          (int64_t*)p->rowptr.p, (int32_t*)p->d_l.p, (int32_t*)p->d_g.p,
                                          (float*)p->norm_gcn.p, (float*)p->norm_sage.p,
-                                         (int32_t*)p->labels.p);
+                                         (float*)p->node_w.p, (int32_t*)p->labels.p);
     GRAPPA_LAUNCHED(ctx);
     RP_TRY(device_scan(ctx, FlagSeed{(int32_t*)p->core_global.p, train_mask}, n_core,
                        WriteCompact{(int32_t*)p->seeds.p, d_stat, 2}, s));
@@ -485,6 +493,7 @@ extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g
     I.rowptr = (int64_t*)p->rowptr.p; I.col = (int32_t*)p->col.p;
     I.core_global = (int32_t*)p->core_global.p; I.d_l = (int32_t*)p->d_l.p; I.d_g = (int32_t*)p->d_g.p;
     I.norm_gcn = (float*)p->norm_gcn.p; I.norm_sage = (float*)p->norm_sage.p;
+    I.node_w = (float*)p->node_w.p;
     I.seeds = (int32_t*)p->seeds.p; I.labels = (int32_t*)p->labels.p; I.x = p->x.p;
     I.n_heavy = n_heavy; I.n_slots = n_slots;
     I.c_uniform = hs.sum_r / (double)n_seeds;
@@ -504,7 +513,8 @@ static grappa_status part_copy(const grappa_part* p, const grappa_part_host* h, 
         {h->rowptr, p->rowptr.p, (size_t)(I.n_core + 1) * 8}, {h->col, p->col.p, (size_t)I.nnz * 4},
         {h->d_l, p->d_l.p, (size_t)I.n_core * 4}, {h->norm_gcn, p->norm_gcn.p, (size_t)I.n_core * 4},
         {h->norm_sage, p->norm_sage.p, (size_t)I.n_core * 4}, {h->seeds, p->seeds.p, (size_t)I.n_seeds * 4},
-        {h->labels, p->labels.p, (size_t)I.n_core * 4}, {h->x, p->x.p, (size_t)I.n_core * I.feat_dim * es}};
+        {h->labels, p->labels.p, (size_t)I.n_core * 4}, {h->x, p->x.p, (size_t)I.n_core * I.feat_dim * es},
+        {h->node_w, p->node_w.p, (size_t)I.n_core * 12}};
     for (const F& x : f) {
         if (!x.host || !x.bytes) continue;
         if (to_host) GRAPPA_CUDA(cudaMemcpyAsync(x.host, x.dev, x.bytes, cudaMemcpyDeviceToHost, s));
@@ -532,7 +542,7 @@ extern "C" grappa_status grappa_part_query(const grappa_part* part, grappa_part_
 extern "C" void grappa_part_destroy(grappa_part* p) {
     if (!p) return;
     for (grappa::DevBuf* b : {&p->rowptr, &p->col, &p->core_global, &p->d_l, &p->d_g, &p->norm_gcn,
-                              &p->norm_sage, &p->seeds, &p->labels, &p->x, &p->heavy_rows,
+                              &p->norm_sage, &p->node_w, &p->seeds, &p->labels, &p->x, &p->heavy_rows,
                               &p->heavy_slot_off, &p->slot_row, &p->slot_seg, &p->row_order,
                               &p->row_desc})
         b->release();

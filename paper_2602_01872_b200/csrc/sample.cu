@@ -255,7 +255,9 @@ __global__ void k_fill_block(const int64_t* __restrict__ d_nt, const int64_t* __
                              int64_t cap_nnz, const int32_t* __restrict__ picks, const int32_t* __restrict__ cnt,
                              int f, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ where,
                              int32_t* __restrict__ col, int32_t* __restrict__ erow, int32_t* __restrict__ key_pad,
-                             float* __restrict__ inv_cnt) {
+                             float* __restrict__ inv_cnt, const int32_t* __restrict__ targets,
+                             const int32_t* __restrict__ d_l, const int32_t* __restrict__ d_g,
+                             float* __restrict__ inv_cnt_node) {
     const int64_t nt = *d_nt, nnz = *d_nnz;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
         const int c = cnt[t];
@@ -270,6 +272,10 @@ __global__ void k_fill_block(const int64_t* __restrict__ d_nt, const int64_t* __
         const int64_t o = rowptr[t];
         for (int j = 0; j < c; j++) { col[o + j] = p[j]; erow[o + j] = (int32_t)t; key_pad[o + j] = p[j]; }
         inv_cnt[t] = c > 0 ? 1.0f / (float)c : 0.0f;
+        // node-level estimator (R30): the sampled mean times w_v = d_l/d_g (1 iff d_g = 0)
+        const int32_t v = targets[t], dg = d_g[v];
+        const double wv = dg == 0 ? 1.0 : (double)d_l[v] / (double)dg;
+        inv_cnt_node[t] = c > 0 ? (float)(wv / (double)c) : 0.0f;
     }
     // pad the sort keys past nnz so they sort last
     for (int64_t e = nnz + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < cap_nnz;
@@ -331,7 +337,7 @@ __global__ void k_seed_keys(int64_t n, const int32_t* seeds, const int32_t* gid,
 using namespace grappa;
 
 struct BlockBufs {
-    DevBuf rowptr, col, trowptr, tcol, inv_cnt, src;
+    DevBuf rowptr, col, trowptr, tcol, inv_cnt, src, inv_cnt_node;
     int32_t n_dst = 0, n_src = 0;
     int64_t nnz = 0;
 };
@@ -418,6 +424,7 @@ extern "C" grappa_status grappa_sample(grappa_ctx* ctx, const grappa_part* part,
         GRAPPA_TRY(B.rowptr.grow((size_t)(cap_t + 1) * 8));
         GRAPPA_TRY(B.col.grow((size_t)cap_nnz * 4));
         GRAPPA_TRY(B.inv_cnt.grow((size_t)cap_t * 4));
+        GRAPPA_TRY(B.inv_cnt_node.grow((size_t)cap_t * 4));
         GRAPPA_TRY(B.trowptr.grow((size_t)(cap_s + 1) * 8));
         GRAPPA_TRY(B.tcol.grow((size_t)cap_nnz * 4));
         GRAPPA_TRY(b->erow.grow((size_t)cap_nnz * 4));
@@ -449,7 +456,8 @@ extern "C" grappa_status grappa_sample(grappa_ctx* ctx, const grappa_part* part,
                                WriteBRow{(int64_t*)B.rowptr.p, d_nnz}, s));
         k_fill_block<<<tgrid, 256, 0, s>>>(d_nt, d_nnz, cap_nnz, (int32_t*)b->picks.p, (int32_t*)b->cnt.p, f,
                                            (int64_t*)B.rowptr.p, (int32_t*)b->where.p, (int32_t*)B.col.p,
-                                           (int32_t*)b->erow.p, (int32_t*)b->key_pad.p, (float*)B.inv_cnt.p);
+                                           (int32_t*)b->erow.p, (int32_t*)b->key_pad.p, (float*)B.inv_cnt.p,
+                                           targets, I.d_l, I.d_g, (float*)B.inv_cnt_node.p);
         GRAPPA_LAUNCHED(ctx);
         int end_bit = 1;
         while (((int64_t)1 << end_bit) - 1 <= cap_s) end_bit++;
@@ -493,6 +501,7 @@ extern "C" grappa_status grappa_batch_query(const grappa_batch* b, int32_t layer
     out->rowptr = (const int64_t*)B.rowptr.p; out->col = (const int32_t*)B.col.p;
     out->t_rowptr = (const int64_t*)B.trowptr.p; out->t_col = (const int32_t*)B.tcol.p;
     out->inv_cnt = (const float*)B.inv_cnt.p; out->src = (const int32_t*)B.src.p;
+    out->inv_cnt_node = (const float*)B.inv_cnt_node.p;
     return GRAPPA_OK;
 }
 
@@ -506,7 +515,7 @@ extern "C" void grappa_batch_destroy(grappa_batch* b) {
     if (!b) return;
     for (int l = 0; l < kMaxLayers; l++)
         for (DevBuf* d : {&b->blk[l].rowptr, &b->blk[l].col, &b->blk[l].trowptr, &b->blk[l].tcol,
-                          &b->blk[l].inv_cnt, &b->blk[l].src})
+                          &b->blk[l].inv_cnt, &b->blk[l].src, &b->blk[l].inv_cnt_node})
             d->release();
     for (DevBuf* d : {&b->picks, &b->cnt, &b->bitmap, &b->where, &b->erow, &b->key_pad, &b->skeys,
                       &b->svals, &b->sort_tmp, &b->counts, &b->heavy_q})
@@ -555,6 +564,18 @@ extern "C" grappa_status grappa_minibatch_step(grappa_ctx* ctx, const grappa_par
                                                const float* theta, float* grad, void* ws, size_t ws_bytes,
                                                double* loss_dev, void* const* hidden_out, grappa_dtype dt,
                                                void* stream) {
+    return grappa_minibatch_step_ex(ctx, part, b, L, dp, num_classes, theta, grad, ws, ws_bytes, loss_dev,
+                                    hidden_out, dt, 0u, stream);
+}
+
+extern "C" grappa_status grappa_minibatch_step_ex(grappa_ctx* ctx, const grappa_part* part, const grappa_batch* b,
+                                                  int32_t L, const int32_t* dp, int32_t num_classes,
+                                                  const float* theta, float* grad, void* ws, size_t ws_bytes,
+                                                  double* loss_dev, void* const* hidden_out, grappa_dtype dt,
+                                                  unsigned flags, void* stream) {
+    GRAPPA_ARG((flags & ~GRAPPA_LAYER_NODE_LEVEL) == 0, GRAPPA_E_ARG,
+               "grappa_minibatch_step_ex: flags 0x%x invalid", flags);
+    const bool node = flags & GRAPPA_LAYER_NODE_LEVEL;
     GRAPPA_ARG(ctx && part && b && dp && theta && grad && ws && loss_dev, GRAPPA_E_ARG,
                "grappa_minibatch_step: null argument");
     GRAPPA_ARG(L == b->L, GRAPPA_E_ARG, "grappa_minibatch_step: n_layers %d != sampled %d", L, b->L);
@@ -580,7 +601,8 @@ extern "C" grappa_status grappa_minibatch_step(grappa_ctx* ctx, const grappa_par
         const BlockBufs& B = b->blk[l];
         SpmmArgs a;
         a.n = B.n_dst; a.nnz = B.nnz; a.rowptr = (const int64_t*)B.rowptr.p; a.col = (const int32_t*)B.col.p;
-        a.X = w + lay.H[l]; a.width = dp[l]; a.row_scale = (const float*)B.inv_cnt.p; a.out = w + lay.M[l];
+        a.X = w + lay.H[l]; a.width = dp[l];
+        a.row_scale = (const float*)(node ? B.inv_cnt_node.p : B.inv_cnt.p); a.out = w + lay.M[l];
         GRAPPA_TRY(spmm_csr(ctx, a, dt, s));
         GemmArgs g;
         g.M = B.n_dst; g.K1 = dp[l]; g.K2 = dp[l]; g.N = dp[l + 1];
@@ -614,7 +636,8 @@ extern "C" grappa_status grappa_minibatch_step(grappa_ctx* ctx, const grappa_par
                                         (size_t)(B.n_src - B.n_dst) * dp[l] * es, s));
         SpmmArgs a;
         a.n = B.n_src; a.nnz = B.nnz; a.rowptr = (const int64_t*)B.trowptr.p; a.col = (const int32_t*)B.tcol.p;
-        a.X = w + lay.dM; a.width = dp[l]; a.col_scale = (const float*)B.inv_cnt.p; a.accumulate = 1;
+        a.X = w + lay.dM; a.width = dp[l];
+        a.col_scale = (const float*)(node ? B.inv_cnt_node.p : B.inv_cnt.p); a.accumulate = 1;
         a.mask = w + lay.H[l]; a.out = dz_in;
         GRAPPA_TRY(spmm_csr(ctx, a, dt, s));
         dz = dz_in;

@@ -3,7 +3,8 @@
 // PAPER: P:141/P:177 (§3.2 isolated message passing over local nodes and edges only),
 // P:435-437 (§5.1 GCN / GraphSAGE aggregation).
 //
-//   out[v] = epi( rs[v] * ( self * cs[v] * X[v] + sum_{u in N_loc(v)} cs[u] * X[u] ) )
+//   out[v] = epi( rs[v] * ( self * ss[v] * X[v] + ns[v] * sum_{u in N_loc(v)} cs[u] * X[u] ) )
+//   ss = cs unless self_sep (then self_scale, or 1); ns = nbr_scale or 1 (node-level, R30)
 //   epi(a) = relu?( (accumulate ? out_old[v] + a : a) * (mask ? 1[mask[v] > 0] : 1) )
 //
 //   GCN  fwd/bwd : rs = cs = (d_l+1)^-1/2, self = 1   (Dt^-1/2 (A+I) Dt^-1/2, symmetric)
@@ -170,7 +171,8 @@ __device__ __forceinline__ void epilogue(const SpmmArgs& a, int64_t v, int64_t o
     T* out = reinterpret_cast<T*>(a.out);
     const T* mask = reinterpret_cast<const T*>(a.mask);
     const float rs = a.row_scale ? a.row_scale[v] : 1.f;
-    const float cs = a.col_scale ? a.col_scale[v] : 1.f;
+    const float cs = a.self_sep ? (a.self_scale ? a.self_scale[v] : 1.f) : (a.col_scale ? a.col_scale[v] : 1.f);
+    const float ns = a.nbr_scale ? a.nbr_scale[v] : 1.f;
 #pragma unroll
     for (int c = 0; c < CPL; c++) {
         const int cv = sub + c * G;
@@ -180,6 +182,10 @@ __device__ __forceinline__ void epilogue(const SpmmArgs& a, int64_t v, int64_t o
         float r[E];
 #pragma unroll
         for (int q = 0; q < E; q++) r[q] = acc[c][q];
+        if (a.nbr_scale) {
+#pragma unroll
+            for (int q = 0; q < E; q++) r[q] *= ns;
+        }
         if (a.self) {
             float f[E];
             Vec<T>::to_f(Vec<T>::load(X + off), f);
@@ -951,9 +957,10 @@ grappa_status spmm_csr(grappa_ctx* ctx, SpmmArgs a, grappa_dtype dt, cudaStream_
     struct { int64_t n_core, nnz; } I{a.n, a.nnz};
     const double es = dt == GRAPPA_BF16 ? 2.0 : 4.0, w = a.width, nnz = (double)I.nnz;
     const double per_edge = 4.0 + (a.col_scale ? 4.0 : 0.0) + w * es;
-    const double per_row = 8.0 + (a.row_scale ? 4.0 : 0.0) + (a.col_scale ? 4.0 : 0.0) +
-                           (a.self ? w * es : 0.0) + w * es + (a.accumulate ? w * es : 0.0) +
-                           (a.mask ? w * es : 0.0);
+    const bool self_coef = a.self && (a.self_sep ? a.self_scale != nullptr : a.col_scale != nullptr);
+    const double per_row = 8.0 + (a.row_scale ? 4.0 : 0.0) + (self_coef ? 4.0 : 0.0) +
+                           (a.nbr_scale ? 4.0 : 0.0) + (a.self ? w * es : 0.0) + w * es +
+                           (a.accumulate ? w * es : 0.0) + (a.mask ? w * es : 0.0);
     ProfScope ps(ctx, s, GRAPPA_K_SPMM, nnz * per_edge + (double)I.n_core * per_row, 2.0 * nnz * w);
     return dt == GRAPPA_BF16 ? launch_t<__nv_bfloat16>(ctx, a, s) : launch_t<float>(ctx, a, s);
 }

@@ -22,7 +22,10 @@ struct SpmmArgs {
     int width = 0;                    // elements per row (multiple of 4)
     const float* row_scale = nullptr; // rs[v] or null (1)
     const float* col_scale = nullptr; // cs[u] or null (1); also weights the self term
+    const float* nbr_scale = nullptr; // ns[v] or null (1): multiplies the neighbour sum only
     int self = 0;
+    int self_sep = 0;                 // self term weighted by self_scale[v] (null: 1), not cs[v]
+    const float* self_scale = nullptr;
     int relu = 0;
     int accumulate = 0;
     const void* mask = nullptr;       // [n x width] dtype or null

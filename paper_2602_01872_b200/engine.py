@@ -21,10 +21,9 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import (BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, F32, Context, Part, grappa_aggregate_grads,
-               grappa_layer_bwd, grappa_layer_bwd_ex,
-               grappa_layer_fwd, grappa_loss, grappa_partition, grappa_repartition,
-               layer_saved_bytes, layer_ws_bytes)
+from . import (BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, F32, LAYER_NODE_LEVEL, Context, Part,
+               grappa_aggregate_grads, grappa_layer_bwd, grappa_layer_bwd_ex, grappa_layer_fwd_ex,
+               grappa_loss, grappa_partition, grappa_repartition, layer_saved_bytes, layer_ws_bytes)
 
 
 def sweep_schedule(C: int, W: int):
@@ -173,9 +172,11 @@ class Trainer:
         L = sp.depth
         dp = sp.dims_pad
         H = [part.x] + [h[:n] for h in self.H[1:]]
+        # node-level estimator (corr "node", eq. (9), R30): weighted aggregation in every layer
+        nl = LAYER_NODE_LEVEL if self.corr == "node" else 0
         for l in range(L):
-            grappa_layer_fwd(self.ctx, part, sp.arch, dp[l], dp[l + 1], l < L - 1, H[l],
-                             self.w_views[l], H[l + 1], self.saved[l], self.ws, self.dt, s)
+            grappa_layer_fwd_ex(self.ctx, part, sp.arch, dp[l], dp[l + 1], l < L - 1, H[l],
+                                self.w_views[l], H[l + 1], self.saved[l], self.ws, self.dt, nl, s)
         dz = self.dz[0][: n * dp[L]].view(n, dp[L])
         grappa_loss(self.ctx, part, H[L], sp.dims[L], dp[L], dz, self.loss_dev, self.dt, s)
         gcn = sp.arch == "gcn"
@@ -183,9 +184,9 @@ class Trainer:
             dz_in = self.dz[(L - l) % 2][: n * dp[l]].view(n, dp[l]) if l > 0 else None
             # GCN: gradients between layers travel pre-multiplied by N = diag(norm_gcn), so
             # every backward aggregation gathers unweighted rows (grappa_layer_bwd_ex, R29)
-            flags = 0
+            flags = nl
             if gcn:
-                flags = (BWD_DZ_OUT_NORMED if l < L - 1 else 0) | (BWD_DZ_IN_NORMED if l > 0 else 0)
+                flags |= (BWD_DZ_OUT_NORMED if l < L - 1 else 0) | (BWD_DZ_IN_NORMED if l > 0 else 0)
             grappa_layer_bwd_ex(self.ctx, part, sp.arch, dp[l], dp[l + 1], l > 0, dz, H[l],
                                 self.w_views[l], self.saved[l], self.dw_views[l], dz_in, self.ws,
                                 self.dt, flags, s)
@@ -289,7 +290,7 @@ class MinibatchTrainer(Trainer):
             self.mb_ws = torch.empty(need + need // 4, dtype=torch.uint8, device=self.dev)
         grappa_minibatch_step(self.ctx, part, self.batch, self.spec.dims_pad, self.spec.dims[-1],
                               self.theta, self.grad, self.mb_ws, self.loss_dev, self.dt,
-                              stream=self.stream)
+                              stream=self.stream, flags=LAYER_NODE_LEVEL if self.corr == "node" else 0)
         return self.batch
 
     def run_epoch(self, on_phase=None):

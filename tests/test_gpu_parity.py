@@ -213,7 +213,7 @@ def test_layer_bwd_normalised_flags(G, ctx, prod, f_in, f_out, dtype):
     # flags are GCN-only and must be known
     with pytest.raises(G.GrappaError, match="E_ARG"):
         G.grappa_layer_bwd_ex(ctx, part, "gcn", f_in, f_out, True, dz_s, h_in, w, saved, dw, dz_in, ws,
-                              dtype, 4)
+                              dtype, 8)
     with pytest.raises(G.GrappaError, match="E_ARG"):
         G.grappa_layer_bwd_ex(ctx, part, "sage", f_in, f_out, True, dz_s, h_in, w, saved, dw, dz_in, ws,
                               dtype, 1)
