@@ -226,6 +226,8 @@ WORKLOADS = {
                        num_samples=1 << 26, chunks=8, correction="uniform"),
     "rmat24": Workload("rmat24", "rmat", 1 << 24, 128, 16, "gcn", 4, train_frac=0.1, scale=24,
                        num_samples=1 << 28, chunks=8, correction="uniform"),
+    "rmat26": Workload("rmat26", "rmat", 1 << 26, 128, 16, "gcn", 4, train_frac=0.1, scale=26,
+                       num_samples=1 << 30, chunks=8, correction="uniform"),
 }
 WORKLOADS["cora4"] = Workload(**{**WORKLOADS["cora"].__dict__, "name": "cora4", "chunks": 4,
                                  "extra": dict(workers=2)})

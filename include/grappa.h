@@ -299,6 +299,21 @@ grappa_status grappa_sample(grappa_ctx* ctx, const grappa_part* part, const int3
                             int32_t n_batch, const int32_t* fanouts, int32_t n_layers,
                             uint64_t seed, int64_t epoch, int64_t batch_index,
                             grappa_batch** inout, void* stream);
+/* The same call split in two, so a caller can sample batch i+1 on a side stream while batch i
+ * trains: grappa_sample_async enqueues every kernel and a D2H copy of the block sizes into
+ * pinned memory owned by the batch (no host sync); grappa_sample_wait blocks until that copy
+ * has landed and publishes the sizes and coverage factors.  Until then grappa_batch_query /
+ * grappa_batch_factors / grappa_minibatch_step return E_ARG and grappa_minibatch_ws_bytes 0.
+ * grappa_sample_event returns the cudaEvent_t (as void*) recorded after the sample's last
+ * kernel, for a consumer stream to wait on.  Reusing a batch object for a new sample is the
+ * caller's to order after every consumer of its previous blocks (stream/event order).
+ * grappa_sample = grappa_sample_async + grappa_sample_wait. */
+grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part* part, const int32_t* batch,
+                                  int32_t n_batch, const int32_t* fanouts, int32_t n_layers,
+                                  uint64_t seed, int64_t epoch, int64_t batch_index,
+                                  grappa_batch** inout, void* stream);
+grappa_status grappa_sample_wait(grappa_batch* b);
+grappa_status grappa_sample_event(const grappa_batch* b, void** event_out);
 /* layer l = 0 (input) .. n_layers-1 (output: its targets are the batch seeds) */
 grappa_status grappa_batch_query(const grappa_batch* b, int32_t layer, grappa_block_info* out);
 /* Coverage factors of the batch over its seeds with s_v = hop-1 sample size (R28):
@@ -322,7 +337,9 @@ grappa_status grappa_minibatch_step(grappa_ctx* ctx, const grappa_part* part, co
                                     const float* theta, float* grad, void* ws, size_t ws_bytes,
                                     double* loss_dev, void* const* hidden_out, grappa_dtype dtype,
                                     void* stream);
-/* with flags: GRAPPA_LAYER_NODE_LEVEL scales every target's sampled mean by d_l/d_g (R30;
+/* The step enqueues a wait on the batch's sample-completion event first, so the batch may have
+ * been sampled on another stream (grappa_sample_async).
+ * with flags: GRAPPA_LAYER_NODE_LEVEL scales every target's sampled mean by d_l/d_g (R30;
  * inv_cnt_node instead of inv_cnt, forward and backward).  flags = 0 is the call above. */
 grappa_status grappa_minibatch_step_ex(grappa_ctx* ctx, const grappa_part* part, const grappa_batch* b,
                                        int32_t n_layers, const int32_t* dims_pad, int32_t num_classes,

@@ -311,6 +311,30 @@ def grappa_sample(ctx: Context, part: Part, batch, fanouts, seed: int, epoch: in
     return out.refresh(len(fanouts), views)
 
 
+def grappa_sample_async(ctx: Context, part: Part, batch, fanouts, seed: int, epoch: int, batch_index: int,
+                        out: Batch | None = None, stream=None) -> Batch:
+    """enqueue only (no host sync); call grappa_sample_wait(out) before using its blocks"""
+    out = out or Batch()
+    fan = (ctypes.c_int32 * len(fanouts))(*fanouts)
+    _lib.check("grappa_sample_async", ctx.lib.grappa_sample_async(
+        ctx.h, part.h, _lib.ptr(batch), batch.numel(), fan, len(fanouts),
+        ctypes.c_uint64(seed & ((1 << 64) - 1)), epoch, batch_index, ctypes.byref(out.h),
+        _lib.stream_ptr(stream)))
+    out.n_layers = len(fanouts)
+    return out
+
+
+def grappa_sample_wait(batch: Batch, views: bool = True) -> Batch:
+    _lib.check("grappa_sample_wait", load().grappa_sample_wait(batch.h))
+    return batch.refresh(batch.n_layers, views)
+
+
+def grappa_sample_event(batch: Batch) -> int:
+    ev = ctypes.c_void_p()
+    _lib.check("grappa_sample_event", load().grappa_sample_event(batch.h, ctypes.byref(ev)))
+    return ev.value
+
+
 def minibatch_ws_bytes(batch: Batch, dims_pad, dtype) -> int:
     dp = (ctypes.c_int32 * len(dims_pad))(*dims_pad)
     return int(load().grappa_minibatch_ws_bytes(batch.h, len(dims_pad) - 1, dp, dtype_code(dtype)))

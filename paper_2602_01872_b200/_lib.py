@@ -30,7 +30,8 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_sample", "grappa_batch_query", "grappa_batch_factors", "grappa_batch_destroy",
            "grappa_minibatch_ws_bytes", "grappa_minibatch_step", "grappa_part_download",
            "grappa_part_upload", "grappa_layer_bwd_ex", "grappa_layer_fwd_ex",
-           "grappa_minibatch_step_ex"]
+           "grappa_minibatch_step_ex", "grappa_sample_async", "grappa_sample_wait",
+           "grappa_sample_event"]
 KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5, "sample": 6}
 
 
@@ -119,6 +120,9 @@ def load(path: str = LIB_PATH):
         "grappa_aggregate_grads_c": (st, [vp, dbl, vp, i64, i32, f32, vp, vp]),
         "grappa_epoch_seeds": (st, [vp, vp, u64, i64, vp, vp]),
         "grappa_sample": (st, [vp, vp, vp, i32, vp, i32, u64, i64, i64, ctypes.POINTER(vp), vp]),
+        "grappa_sample_async": (st, [vp, vp, vp, i32, vp, i32, u64, i64, i64, ctypes.POINTER(vp), vp]),
+        "grappa_sample_wait": (st, [vp]),
+        "grappa_sample_event": (st, [vp, ctypes.POINTER(vp)]),
         "grappa_batch_query": (st, [vp, i32, ctypes.POINTER(BlockInfo)]),
         "grappa_batch_factors": (st, [vp, ctypes.POINTER(dbl), ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
         "grappa_batch_destroy": (None, [vp]),

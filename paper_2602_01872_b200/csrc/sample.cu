@@ -14,6 +14,8 @@
 //   transpose     stable radix sort of (source position, target) pairs -> CSC for backward
 #include <cub/device/device_radix_sort.cuh>
 
+#include <cstring>
+
 #include "gemm.cuh"
 #include "part.cuh"
 #include "scan.cuh"
@@ -197,6 +199,117 @@ __global__ void __launch_bounds__(256) k_pick_heavy(const int32_t* __restrict__ 
     }
 }
 
+// Hub targets, grid-parallel (the per-hub block loop of k_pick_heavy serialises ~d/256 dependent
+// random gid loads per thread: 0.76 ms per hop on papers-shaped hubs).  The f smallest of d
+// uniform 64-bit keys lie below T = min(1, 6f/d) 2^64 except with negligible probability
+// (count ~ Binomial(d, 6f/d), mean 6f <= 96 for f <= 16: P[count < f] ~ 2.5e-3 at f = 1 (exp(-6)),
+// < 1e-8 for f >= 5; P[count > kCand = 512] is negligible); every (hub, 2048-edge segment) task appends its keys below T to the hub's
+// candidate list, then one block per hub takes the f smallest (key, gid) -- a total order, so
+// the append order (atomics) does not matter.  A hub whose count falls outside [f, kCand] is
+// redone exactly by k_pick_heavy (flag in cand_n).
+constexpr int kCand = 512;
+constexpr int kHubSeg = 2048;
+__host__ __device__ __forceinline__ uint64_t hub_threshold(int f, int64_t d) {
+    const double frac = 6.0 * f / (double)d;
+    return frac >= 1.0 ? ~0ull : (uint64_t)(frac * 18446744073709551616.0);
+}
+struct HubSegs {
+    const int32_t* heavy_n; const int64_t* heavy_q; const int32_t* targets; const int64_t* rowptr;
+    __device__ int32_t operator()(int64_t q) const {
+        if (q >= *heavy_n) return 0;
+        const int32_t v = targets[heavy_q[q]];
+        return (int32_t)ceil_div(rowptr[v + 1] - rowptr[v], kHubSeg);
+    }
+};
+struct WriteHubSegs {
+    int32_t* seg_off; int64_t* d_tasks;
+    __device__ void operator()(int64_t q, int64_t p, int32_t) const { seg_off[q] = (int32_t)p; }
+    __device__ void finish(int64_t n, int64_t total) const { seg_off[n] = (int32_t)total; *d_tasks = total; }
+};
+
+__global__ void __launch_bounds__(256) k_hub_cand(const int32_t* __restrict__ heavy_n, const int64_t* __restrict__ d_tasks,
+                                                  const int32_t* __restrict__ seg_off, const int64_t* __restrict__ heavy_q,
+                                                  const int32_t* __restrict__ targets, const int64_t* __restrict__ rowptr,
+                                                  const int32_t* __restrict__ col, const int32_t* __restrict__ gid, int f,
+                                                  uint64_t key0, int32_t* __restrict__ cand_n,
+                                                  uint4* __restrict__ cand) {
+    const int nq = *heavy_n;
+    const int64_t ntask = *d_tasks;
+    for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
+        // hub of this task: last q with seg_off[q] <= task (binary search, block-uniform)
+        int lo = 0, hi = nq - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (seg_off[mid] <= task) lo = mid; else hi = mid - 1;
+        }
+        const int q = lo;
+        const int32_t v = targets[heavy_q[q]];
+        const int64_t e0 = rowptr[v], d = rowptr[v + 1] - e0;
+        const uint64_t T = hub_threshold(f, d);
+        const int64_t s0 = (task - seg_off[q]) * (int64_t)kHubSeg;
+        const int64_t s1 = min(d, s0 + kHubSeg);
+        for (int64_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+            const int32_t u = col[e0 + i];
+            const int32_t gu = gid[u];
+            const uint64_t k = smix(key0 ^ smix((uint64_t)gid[v] ^ smix((uint64_t)gu)));
+            if (k < T) {
+                const int p = atomicAdd(&cand_n[q], 1);
+                if (p < kCand) cand[(int64_t)q * kCand + p] = make_uint4((uint32_t)k, (uint32_t)(k >> 32), (uint32_t)gu, (uint32_t)u);
+            }
+        }
+    }
+}
+
+// one block per hub: f smallest (key, gid) among its candidates; hubs whose candidate count is
+// outside [f, kCand] are left to the exact k_pick_heavy (their queue entry is kept in redo_q)
+__global__ void __launch_bounds__(256) k_hub_select(const int32_t* __restrict__ heavy_n, const int64_t* __restrict__ heavy_q,
+                                                    const int32_t* __restrict__ cand_n, const uint4* __restrict__ cand, int f,
+                                                    int32_t* __restrict__ picks, int32_t* __restrict__ cnt,
+                                                    int32_t* __restrict__ redo_n, int64_t* __restrict__ redo_q) {
+    __shared__ uint64_t ck[kCand];
+    __shared__ int32_t cg[kCand], cu[kCand];
+    const int nq = *heavy_n;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    for (int q = blockIdx.x; q < nq; q += gridDim.x) {
+        const int n = cand_n[q];
+        const int64_t t = heavy_q[q];
+        if (n < f || n > kCand) {
+            if (tid == 0) redo_q[atomicAdd(redo_n, 1)] = t;
+            continue;
+        }
+        for (int j = tid; j < n; j += blockDim.x) {
+            const uint4 c = cand[(int64_t)q * kCand + j];
+            ck[j] = (uint64_t)c.x | ((uint64_t)c.y << 32);
+            cg[j] = (int32_t)c.z;
+            cu[j] = (int32_t)c.w;
+        }
+        __syncthreads();
+        if (w == 0) {
+            uint64_t lk = 0;
+            int32_t lg = -1;                       // last selected (exclusive lower bound)
+            for (int r = 0; r < f; r++) {
+                uint64_t bk = ~0ull;
+                int32_t bg = 0x7fffffff, bu = -1;
+                for (int j = lane; j < n; j += 32) {
+                    const bool above = r == 0 || key_lt(lk, lg, ck[j], cg[j]);
+                    if (above && key_lt(ck[j], cg[j], bk, bg)) { bk = ck[j]; bg = cg[j]; bu = cu[j]; }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
+                    const int32_t og = __shfl_xor_sync(0xffffffffu, bg, o);
+                    const int32_t ou = __shfl_xor_sync(0xffffffffu, bu, o);
+                    if (key_lt(ok, og, bk, bg)) { bk = ok; bg = og; bu = ou; }
+                }
+                if (lane == 0) picks[t * f + r] = bu;
+                lk = bk; lg = bg;
+            }
+            if (lane == 0) cnt[t] = f;
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void k_mark(const int64_t* __restrict__ d_nt, const int32_t* __restrict__ picks,
                        const int32_t* __restrict__ cnt, int f, uint32_t* __restrict__ bitmap) {
     const int64_t n = *d_nt * f;
@@ -347,7 +460,13 @@ struct grappa_batch {
     int32_t n_batch = 0;
     BlockBufs blk[kMaxLayers];
     DevBuf picks, cnt, bitmap, where, erow, key_pad, skeys, svals, sort_tmp, counts, heavy_q;
+    DevBuf hub_seg, hub_cand_n, hub_cand;   // grid-parallel hub pick (k_hub_cand / k_hub_select)
+    DevBuf scan_ws;                         // own scan partials (the sampler may run on a side stream)
     double c_uniform = 1, c_resampling = 1, c_hm = 1;
+    // grappa_sample_async -> grappa_sample_wait: counts + stats land in pinned host memory
+    void* host = nullptr;                   // int64 [3 kMaxLayers] + BatchStats
+    cudaEvent_t done = nullptr;
+    bool pending = false;
 };
 
 static grappa_status sort_pairs(DevBuf& tmp, const int32_t* kin, int32_t* kout, const int32_t* vin,
@@ -385,6 +504,15 @@ extern "C" grappa_status grappa_sample(grappa_ctx* ctx, const grappa_part* part,
                                        int32_t n_batch, const int32_t* fanouts, int32_t n_layers,
                                        uint64_t seed, int64_t epoch, int64_t batch_index,
                                        grappa_batch** inout, void* stream) {
+    GRAPPA_TRY(grappa_sample_async(ctx, part, batch, n_batch, fanouts, n_layers, seed, epoch, batch_index,
+                                   inout, stream));
+    return grappa_sample_wait(*inout);
+}
+
+extern "C" grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part* part, const int32_t* batch,
+                                             int32_t n_batch, const int32_t* fanouts, int32_t n_layers,
+                                             uint64_t seed, int64_t epoch, int64_t batch_index,
+                                             grappa_batch** inout, void* stream) {
     GRAPPA_ARG(ctx && part && batch && fanouts && inout, GRAPPA_E_ARG, "grappa_sample: null argument");
     GRAPPA_ARG(n_layers >= 1 && n_layers <= kMaxLayers, GRAPPA_E_ARG, "grappa_sample: 1 <= n_layers <= %d", kMaxLayers);
     GRAPPA_ARG(n_batch >= 1, GRAPPA_E_ARG, "grappa_sample: empty batch (S:213)");
@@ -434,14 +562,35 @@ extern "C" grappa_status grappa_sample(grappa_ctx* ctx, const grappa_part* part,
         const uint64_t key0 = hmix(seed ^ hmix((uint64_t)epoch ^ hmix((uint64_t)batch_index ^ hmix((uint64_t)h))));
         const unsigned wgrid = (unsigned)std::min<int64_t>(ceil_div(cap_t, 8), (int64_t)ctx->sm_count * 16);
         const unsigned tgrid = (unsigned)std::min<int64_t>(ceil_div(cap_nnz, 256), (int64_t)ctx->sm_count * 16);
-        GRAPPA_TRY(b->heavy_q.grow((size_t)cap_t * 8));
+        // hubs: at most the partition's rows with d_l > kHeavyPick (<= n_heavy, d_l > kSegLen)
+        const int64_t cap_h = std::max<int64_t>(1, std::min<int64_t>(cap_t, I.n_heavy));
+        GRAPPA_TRY(b->heavy_q.grow((size_t)cap_h * 8 * 2));
+        GRAPPA_TRY(b->hub_seg.grow((size_t)(cap_h + 1) * 4));
+        GRAPPA_TRY(b->hub_cand_n.grow((size_t)cap_h * 4));
+        GRAPPA_TRY(b->hub_cand.grow((size_t)cap_h * kCand * 16));
         int32_t* heavy_n = (int32_t*)(dstat + 1);
-        GRAPPA_CUDA(cudaMemsetAsync(heavy_n, 0, sizeof(int32_t), s));
+        int32_t* redo_n = heavy_n + 1;
+        int64_t* d_tasks = (int64_t*)(heavy_n + 2);
+        int64_t* heavy_q = (int64_t*)b->heavy_q.p;
+        int64_t* redo_q = heavy_q + cap_h;
+        GRAPPA_CUDA(cudaMemsetAsync(heavy_n, 0, 2 * sizeof(int32_t), s));
+        GRAPPA_CUDA(cudaMemsetAsync(b->hub_cand_n.p, 0, (size_t)cap_h * 4, s));
         k_pick<<<wgrid, 256, 0, s>>>(d_nt, targets, I.rowptr, I.col, I.core_global, f, key0,
-                                     (int32_t*)b->picks.p, (int32_t*)b->cnt.p, heavy_n, (int64_t*)b->heavy_q.p);
+                                     (int32_t*)b->picks.p, (int32_t*)b->cnt.p, heavy_n, heavy_q);
         GRAPPA_LAUNCHED(ctx);
-        k_pick_heavy<<<(unsigned)std::min<int64_t>(cap_t, (int64_t)ctx->sm_count * 4), 256, 0, s>>>(
-            heavy_n, (int64_t*)b->heavy_q.p, targets, I.rowptr, I.col, I.core_global, f, key0,
+        GRAPPA_TRY(device_scan(ctx, HubSegs{heavy_n, heavy_q, targets, I.rowptr}, cap_h,
+                               WriteHubSegs{(int32_t*)b->hub_seg.p, d_tasks}, s, nullptr, &b->scan_ws));
+        k_hub_cand<<<(unsigned)ctx->sm_count * 8, 256, 0, s>>>(
+            heavy_n, d_tasks, (const int32_t*)b->hub_seg.p, heavy_q, targets, I.rowptr, I.col, I.core_global, f,
+            key0, (int32_t*)b->hub_cand_n.p, (uint4*)b->hub_cand.p);
+        GRAPPA_LAUNCHED(ctx);
+        k_hub_select<<<(unsigned)std::min<int64_t>(cap_h, (int64_t)ctx->sm_count * 4), 256, 0, s>>>(
+            heavy_n, heavy_q, (const int32_t*)b->hub_cand_n.p, (const uint4*)b->hub_cand.p, f,
+            (int32_t*)b->picks.p, (int32_t*)b->cnt.p, redo_n, redo_q);
+        GRAPPA_LAUNCHED(ctx);
+        // exact fallback for the (vanishingly rare) hubs outside [f, kCand] candidates
+        k_pick_heavy<<<(unsigned)std::min<int64_t>(cap_h, (int64_t)ctx->sm_count), 256, 0, s>>>(
+            redo_n, redo_q, targets, I.rowptr, I.col, I.core_global, f, key0,
             (int32_t*)b->picks.p, (int32_t*)b->cnt.p);
         GRAPPA_LAUNCHED(ctx);
         GRAPPA_CUDA(cudaMemsetAsync(b->bitmap.p, 0, (size_t)nwords * 4, s));
@@ -451,9 +600,10 @@ extern "C" grappa_status grappa_sample(grappa_ctx* ctx, const grappa_part* part,
             d_nt, targets, (uint32_t*)b->bitmap.p, (int32_t*)b->where.p, (int32_t*)B.src.p);
         GRAPPA_LAUNCHED(ctx);
         GRAPPA_TRY(device_scan(ctx, PopWord{(uint32_t*)b->bitmap.p}, nwords,
-                               WriteNew{(uint32_t*)b->bitmap.p, d_nt, (int32_t*)B.src.p, (int32_t*)b->where.p, d_ns}, s));
+                               WriteNew{(uint32_t*)b->bitmap.p, d_nt, (int32_t*)B.src.p, (int32_t*)b->where.p, d_ns}, s,
+                               nullptr, &b->scan_ws));
         GRAPPA_TRY(device_scan(ctx, CntUpTo{(int32_t*)b->cnt.p, d_nt}, cap_t,
-                               WriteBRow{(int64_t*)B.rowptr.p, d_nnz}, s));
+                               WriteBRow{(int64_t*)B.rowptr.p, d_nnz}, s, nullptr, &b->scan_ws));
         k_fill_block<<<tgrid, 256, 0, s>>>(d_nt, d_nnz, cap_nnz, (int32_t*)b->picks.p, (int32_t*)b->cnt.p, f,
                                            (int64_t*)B.rowptr.p, (int32_t*)b->where.p, (int32_t*)B.col.p,
                                            (int32_t*)b->erow.p, (int32_t*)b->key_pad.p, (float*)B.inv_cnt.p,
@@ -475,11 +625,33 @@ extern "C" grappa_status grappa_sample(grappa_ctx* ctx, const grappa_part* part,
     // batch coverage statistics over the seeds (hop 1 = output layer block)
     k_batch_stats<<<1, 256, 0, s>>>(n_batch, batch, I.d_l, I.d_g, (int64_t*)b->blk[n_layers - 1].rowptr.p, dstat);
     GRAPPA_LAUNCHED(ctx);
-    int64_t hc[3 * kMaxLayers];
+    if (!b->host) {
+        GRAPPA_CUDA(cudaMallocHost(&b->host, sizeof(int64_t) * 3 * kMaxLayers + sizeof(BatchStats)));
+        GRAPPA_CUDA(cudaEventCreateWithFlags(&b->done, cudaEventDisableTiming));
+    }
+    GRAPPA_CUDA(cudaMemcpyAsync(b->host, dc, sizeof(int64_t) * 3 * kMaxLayers + sizeof(BatchStats),
+                                cudaMemcpyDeviceToHost, s));
+    GRAPPA_CUDA(cudaEventRecord(b->done, s));
+    b->pending = true;
+    *inout = b;
+    return GRAPPA_OK;
+}
+
+extern "C" grappa_status grappa_sample_event(const grappa_batch* b, void** event_out) {
+    GRAPPA_ARG(b && event_out, GRAPPA_E_ARG, "grappa_sample_event: null argument");
+    *event_out = (void*)b->done;
+    return GRAPPA_OK;
+}
+
+extern "C" grappa_status grappa_sample_wait(grappa_batch* b) {
+    GRAPPA_ARG(b, GRAPPA_E_ARG, "grappa_sample_wait: null argument");
+    if (!b->pending) return GRAPPA_OK;
+    GRAPPA_CUDA(cudaEventSynchronize(b->done));
+    b->pending = false;
+    const int n_layers = b->L, n_batch = b->n_batch;
+    const int64_t* hc = (const int64_t*)b->host;
     BatchStats hs;
-    GRAPPA_CUDA(cudaMemcpyAsync(hc, dc, sizeof(int64_t) * 3 * n_layers, cudaMemcpyDeviceToHost, s));
-    GRAPPA_CUDA(cudaMemcpyAsync(&hs, dstat, sizeof(hs), cudaMemcpyDeviceToHost, s));
-    GRAPPA_CUDA(cudaStreamSynchronize(s));
+    memcpy(&hs, hc + 3 * kMaxLayers, sizeof(hs));
     for (int h = 1; h <= n_layers; h++) {
         BlockBufs& B = b->blk[n_layers - h];
         B.n_dst = (int32_t)hc[3 * (h - 1)];
@@ -489,13 +661,13 @@ extern "C" grappa_status grappa_sample(grappa_ctx* ctx, const grappa_part* part,
     b->c_uniform = hs.sum_r / (double)n_batch;
     b->c_resampling = hs.D < 1e-9 ? 1.0 : std::min(1.0 / hs.D, 10.0);
     b->c_hm = hs.num > 0 ? hs.num / hs.den : 1.0;
-    *inout = b;
     return GRAPPA_OK;
 }
 
 extern "C" grappa_status grappa_batch_query(const grappa_batch* b, int32_t layer, grappa_block_info* out) {
     GRAPPA_ARG(b && out, GRAPPA_E_ARG, "grappa_batch_query: null argument");
     GRAPPA_ARG(layer >= 0 && layer < b->L, GRAPPA_E_ARG, "grappa_batch_query: layer out of range");
+    GRAPPA_ARG(!b->pending, GRAPPA_E_ARG, "grappa_batch_query: batch not published (grappa_sample_wait)");
     const BlockBufs& B = b->blk[layer];
     out->n_dst = B.n_dst; out->n_src = B.n_src; out->nnz = B.nnz;
     out->rowptr = (const int64_t*)B.rowptr.p; out->col = (const int32_t*)B.col.p;
@@ -507,18 +679,22 @@ extern "C" grappa_status grappa_batch_query(const grappa_batch* b, int32_t layer
 
 extern "C" grappa_status grappa_batch_factors(const grappa_batch* b, double* cu, double* cr, double* ch) {
     GRAPPA_ARG(b && cu && cr && ch, GRAPPA_E_ARG, "grappa_batch_factors: null argument");
+    GRAPPA_ARG(!b->pending, GRAPPA_E_ARG, "grappa_batch_factors: batch not published (grappa_sample_wait)");
     *cu = b->c_uniform; *cr = b->c_resampling; *ch = b->c_hm;
     return GRAPPA_OK;
 }
 
 extern "C" void grappa_batch_destroy(grappa_batch* b) {
     if (!b) return;
+    if (b->done) { cudaEventSynchronize(b->done); cudaEventDestroy(b->done); }
+    if (b->host) cudaFreeHost(b->host);
     for (int l = 0; l < kMaxLayers; l++)
         for (DevBuf* d : {&b->blk[l].rowptr, &b->blk[l].col, &b->blk[l].trowptr, &b->blk[l].tcol,
                           &b->blk[l].inv_cnt, &b->blk[l].src, &b->blk[l].inv_cnt_node})
             d->release();
     for (DevBuf* d : {&b->picks, &b->cnt, &b->bitmap, &b->where, &b->erow, &b->key_pad, &b->skeys,
-                      &b->svals, &b->sort_tmp, &b->counts, &b->heavy_q})
+                      &b->svals, &b->sort_tmp, &b->counts, &b->heavy_q, &b->hub_seg, &b->hub_cand_n,
+                      &b->hub_cand, &b->scan_ws})
         d->release();
     delete b;
 }
@@ -555,7 +731,7 @@ StepLayout step_layout(const grappa_batch* b, int L, const int32_t* dp, grappa_d
 
 extern "C" size_t grappa_minibatch_ws_bytes(const grappa_batch* b, int32_t L, const int32_t* dims_pad,
                                             grappa_dtype dtype) {
-    if (!b || !dims_pad || L != b->L) return 0;
+    if (!b || !dims_pad || L != b->L || b->pending) return 0;
     return step_layout(b, L, dims_pad, dtype).total;
 }
 
@@ -579,6 +755,9 @@ extern "C" grappa_status grappa_minibatch_step_ex(grappa_ctx* ctx, const grappa_
     GRAPPA_ARG(ctx && part && b && dp && theta && grad && ws && loss_dev, GRAPPA_E_ARG,
                "grappa_minibatch_step: null argument");
     GRAPPA_ARG(L == b->L, GRAPPA_E_ARG, "grappa_minibatch_step: n_layers %d != sampled %d", L, b->L);
+    GRAPPA_ARG(!b->pending, GRAPPA_E_ARG, "grappa_minibatch_step: batch not published (grappa_sample_wait)");
+    // the blocks may have been sampled on another stream (grappa_sample_async): order after them
+    if (b->done) GRAPPA_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, b->done, 0));
     for (int l = 0; l <= L; l++)
         GRAPPA_ARG(dp[l] > 0 && dp[l] % 16 == 0, GRAPPA_E_SHAPE, "grappa_minibatch_step: dims must be multiples of 16");
     GRAPPA_ARG(dp[0] == part->info.feat_dim && dt == part->info.dtype, GRAPPA_E_SHAPE,

@@ -80,12 +80,14 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(F f, int64_t n, cons
 
 // Exclusive scan of f(0..n) with per-element writer w(i, prefix, value) and w.finish(n, total).
 // Grand total left in device memory at *d_total_out (pointer into ctx scratch) if requested.
+// ws: partials buffer (default ctx->scan_ws; a caller on its own stream passes its own).
 template <class F, class W>
 grappa_status device_scan(grappa_ctx* ctx, F f, int64_t n, W w, cudaStream_t s,
-                          const int64_t** d_total_out = nullptr) {
+                          const int64_t** d_total_out = nullptr, DevBuf* ws = nullptr) {
     int64_t nb = n > 0 ? ceil_div(n, kScanTile) : 1;
-    GRAPPA_TRY(ctx->scan_ws.grow((size_t)(nb + 1) * sizeof(int64_t)));
-    int64_t* part = (int64_t*)ctx->scan_ws.p;
+    DevBuf& buf = ws ? *ws : ctx->scan_ws;
+    GRAPPA_TRY(buf.grow((size_t)(nb + 1) * sizeof(int64_t)));
+    int64_t* part = (int64_t*)buf.p;
     k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, s>>>(f, n, part);
     GRAPPA_LAUNCHED(ctx);
     k_scan_partials<<<1, kScanThreads, 0, s>>>(part, nb);

@@ -171,7 +171,10 @@ __device__ __forceinline__ void epilogue(const SpmmArgs& a, int64_t v, int64_t o
     T* out = reinterpret_cast<T*>(a.out);
     const T* mask = reinterpret_cast<const T*>(a.mask);
     const float rs = a.row_scale ? a.row_scale[v] : 1.f;
-    const float cs = a.self_sep ? (a.self_scale ? a.self_scale[v] : 1.f) : (a.col_scale ? a.col_scale[v] : 1.f);
+    // self coefficient: read only when there is a self term (on a rectangular block, e.g. the
+    // mini-batch transpose, col_scale is indexed by the other side and v may be out of its range)
+    const float cs = !a.self ? 0.f
+                     : a.self_sep ? (a.self_scale ? a.self_scale[v] : 1.f) : (a.col_scale ? a.col_scale[v] : 1.f);
     const float ns = a.nbr_scale ? a.nbr_scale[v] : 1.f;
 #pragma unroll
     for (int c = 0; c < CPL; c++) {

@@ -38,6 +38,17 @@ def sweep_schedule(C: int, W: int):
     return [[pairs[((t - 1) * W + w) % len(pairs)] for w in range(W)] for t in range(1, cycle + 1)]
 
 
+def merge_step_factors(per_rank) -> list:
+    """per_rank[r] = [(c, active), ...] for the same lock-step sequence of optimizer steps;
+    returns per step the mean c over the ranks that were active (steps with none are dropped)"""
+    out = []
+    for k in range(len(per_rank[0]) if per_rank else 0):
+        cs = [r[k][0] for r in per_rank if r[k][1] > 0]
+        if cs:
+            out.append(sum(cs) / len(cs))
+    return out
+
+
 def phase_plan(W: int, G: int, rank: int):
     """Alg. 1 with P = W partitions on G ranks (M = G partitions per phase):
     phase i -> (worker i*G + rank, or None if this rank idles in a ragged last phase,
@@ -75,7 +86,7 @@ class Trainer:
     def __init__(self, ctx: Context, rowptr, col, x, labels, train_mask, spec: ModelSpec, weights,
                  num_chunks: int, chunk_seed: int, corr: str = "resampling", lr: float = 0.003,
                  repartition_every: int = 10, dtype: str = "f32", num_workers: int | None = None,
-                 stream=None):
+                 stream=None, controller=None):
         self.ctx = ctx
         self.dev = torch.device("cuda", ctx.device)
         self.stream = stream or torch.cuda.current_stream(self.dev)
@@ -87,6 +98,11 @@ class Trainer:
         self.corr = corr
         self.lr = lr
         self.rep_every = repartition_every
+        # optional §3.5 controller (paper_2602_01872_b200.controller.Controller): decides the
+        # super-epoch switches instead of the fixed `repartition_every`
+        self.controller = controller
+        self.t_ctrl = 1
+        self._steps = []
         self.dt = BF16 if dtype == "bf16" else F32
         self.tdt = torch.bfloat16 if self.dt == BF16 else torch.float32
         self.schedule = sweep_schedule(self.C, self.W)
@@ -201,10 +217,37 @@ class Trainer:
             self.grad.zero_()
         grappa_aggregate_grads(self.ctx, part, self.corr, self.grad, m_active,
                                self.lr if lr is None else lr, self.theta, self.stream)
+        self._steps.append((part.factor(self.corr), 1.0) if part is not None else (0.0, 0.0))
+
+    # ------------------------------------------------------------------ super-epochs
+    def super_epoch(self) -> int:
+        """super-epoch index of the next epoch: fixed length, or the controller's count"""
+        return self.t_ctrl if self.controller is not None else 1 + self.epoch // self.rep_every
+
+    def end_epoch(self):
+        """epoch boundary: feed the controller this epoch's per-step coverage factors (mean over
+        the active ranks of each step, identical on every rank) and advance the super-epoch if it
+        says so (§3.5, R32)"""
+        self.epoch += 1
+        steps, self._steps = self._steps, []
+        if self.controller is None:
+            return
+        if self.G > 1:
+            import torch.distributed as dist
+            mine = torch.tensor(steps, dtype=torch.float64, device=self.dev).reshape(-1, 2)
+            every = [torch.empty_like(mine) for _ in range(self.G)]
+            dist.all_gather(every, mine)
+            seq = merge_step_factors([e.cpu().tolist() for e in every])
+        else:
+            seq = merge_step_factors([steps])
+        for c in seq:
+            self.controller.observe(c)
+        if self.controller.end_epoch():
+            self.t_ctrl += 1
 
     def run_epoch(self, on_phase=None):
         """One epoch of Alg. 1: ceil(W/G) phases, one aggregate + SGD step per phase."""
-        t = 1 + self.epoch // self.rep_every
+        t = self.super_epoch()
         if t != self.t:
             self.repartition(t)
         for i, w in self.my_workers():
@@ -212,13 +255,13 @@ class Trainer:
             self.phase_step(i, w, m_active)
             if on_phase is not None:
                 on_phase()
-        self.epoch += 1
+        self.end_epoch()
 
     def run_epoch_graph(self):
         """Same epoch, replayed from a CUDA graph captured once per super-epoch (the phase
         loop is launch-bound on small graphs: ~60 kernels per phase).  The first call after a
         repartition captures (nothing executes during capture) and then replays."""
-        t = 1 + self.epoch // self.rep_every
+        t = self.super_epoch()
         if t != self.t:
             self.repartition(t)
             self.graph = None
@@ -238,8 +281,11 @@ class Trainer:
                     self.stream = main
             self.graph = g
             self.graph_launches = self.ctx.launches() - l0
+            self.graph_steps, self._steps = list(self._steps), []
         self.graph.replay()
-        self.epoch += 1
+        if self.controller is not None:        # the captured steps' factors (fixed per super-epoch)
+            self._steps = list(self.graph_steps)
+        self.end_epoch()
 
     @property
     def nnz(self):
@@ -279,46 +325,81 @@ class MinibatchTrainer(Trainer):
         return n
 
     def minibatch(self, part, order, it: int, nb: int):
-        """sample + forward/backward of batch (it mod nb) -> self.grad; returns the batch."""
-        from . import grappa_minibatch_step, grappa_sample, minibatch_ws_bytes
+        """sample + forward/backward of batch (it mod nb) -> self.grad; returns the batch
+        (unpipelined single-batch path, used by tests and diagnostics)."""
+        from . import grappa_sample
         b = it % nb
         seeds = order[b * self.B: min((b + 1) * self.B, order.numel())]
         self.batch = grappa_sample(self.ctx, part, seeds, self.fanouts, self.sample_seed, self.epoch, b,
                                    self.batch, self.stream, views=False)
-        need = minibatch_ws_bytes(self.batch, self.spec.dims_pad, self.dt)
-        if self.mb_ws is None or self.mb_ws.numel() < need:
-            self.mb_ws = torch.empty(need + need // 4, dtype=torch.uint8, device=self.dev)
-        grappa_minibatch_step(self.ctx, part, self.batch, self.spec.dims_pad, self.spec.dims[-1],
-                              self.theta, self.grad, self.mb_ws, self.loss_dev, self.dt,
-                              stream=self.stream, flags=LAYER_NODE_LEVEL if self.corr == "node" else 0)
+        self._step(part, self.batch)
         return self.batch
 
+    def _step(self, part, batch):
+        from . import grappa_minibatch_step, minibatch_ws_bytes
+        need = minibatch_ws_bytes(batch, self.spec.dims_pad, self.dt)
+        if self.mb_ws is None or self.mb_ws.numel() < need:
+            self.mb_ws = torch.empty(need + need // 4, dtype=torch.uint8, device=self.dev)
+        grappa_minibatch_step(self.ctx, part, batch, self.spec.dims_pad, self.spec.dims[-1],
+                              self.theta, self.grad, self.mb_ws, self.loss_dev, self.dt,
+                              stream=self.stream, flags=LAYER_NODE_LEVEL if self.corr == "node" else 0)
+
+    def _sample_async(self, part, order, it: int, nb: int, slot: int):
+        from . import Batch, grappa_sample_async
+        b = it % nb
+        seeds = order[b * self.B: min((b + 1) * self.B, order.numel())]
+        self.slots[slot] = grappa_sample_async(self.ctx, part, seeds, self.fanouts, self.sample_seed,
+                                               self.epoch, b, self.slots[slot] or Batch(), self.sstream)
+
     def run_epoch(self, on_phase=None):
-        from . import grappa_aggregate_grads_c, grappa_epoch_seeds
-        t = 1 + self.epoch // self.rep_every
+        """Alg. 1 in mini-batch mode.  Sampling runs one batch ahead on a side stream into the
+        other of two batch slots (grappa_sample_async), so the sampler kernels of batch i+1
+        overlap the SAGE step of batch i; the host waits only for batch i's block sizes
+        (grappa_sample_wait) before launching its step."""
+        from . import grappa_aggregate_grads_c, grappa_epoch_seeds, grappa_sample_wait
+        t = self.super_epoch()
         if t != self.t:
             self.repartition(t)
+        if getattr(self, "sstream", None) is None:
+            self.sstream = torch.cuda.Stream(self.dev)
+            self.slots = [None, None]
         for i, w, m_active in phase_plan(self.W, self.G, self.rank):
             part = self.parts.get(w) if w is not None else None
             nb = self.iterations(part)
             iters = self.phase_iterations(part)
+            done = [None, None]
             if part is not None:
                 if self.order is None or self.order.numel() < part.n_seeds:
                     self.order = torch.empty(part.n_seeds, dtype=torch.int32, device=self.dev)
                 order = self.order[:part.n_seeds]
                 grappa_epoch_seeds(self.ctx, part, self.sample_seed, self.epoch, order, self.stream)
+                if iters:
+                    ev = torch.cuda.Event()
+                    ev.record(self.stream)               # seeds (and every earlier step) first
+                    self.sstream.wait_event(ev)
+                    self._sample_async(part, order, 0, nb, 0)
             for it in range(iters):
+                slot = it & 1
                 if part is not None:
-                    bt = self.minibatch(part, order, it, nb)
+                    bt = grappa_sample_wait(self.slots[slot], views=False)
+                    if it + 1 < iters:
+                        if done[slot ^ 1] is not None:  # the other slot's blocks are consumed
+                            self.sstream.wait_event(done[slot ^ 1])
+                        self._sample_async(part, order, it + 1, nb, slot ^ 1)
+                    self.batch = bt
+                    self._step(part, bt)                 # waits on bt's sample event itself
+                    done[slot] = torch.cuda.Event()
+                    done[slot].record(self.stream)
                     c = bt.factors[self.corr]
                 else:
                     self.grad.zero_()
                     c = 0.0
                 grappa_aggregate_grads_c(self.ctx, c, self.grad, m_active, self.lr, self.theta,
                                          self.stream)
+                self._steps.append((c, 1.0) if part is not None else (0.0, 0.0))
                 if on_phase is not None:
                     on_phase()
-        self.epoch += 1
+        self.end_epoch()
 
     def _alloc(self):
         """mini-batch mode needs no partition-sized activation buffers (per-batch workspace

@@ -97,3 +97,61 @@ def test_phase_plan():
         for G in range(1, 9):
             ws = sorted(w for r in range(G) for _, w, _ in phase_plan(W, G, r) if w is not None)
             assert ws == list(range(W))
+
+
+def _ctrl_worker(rank, world, port, out):
+    """each rank sees different coverage factors (its own partitions); after gathering the
+    per-step (c, active) lists once per epoch (Trainer.end_epoch) every rank must take the same
+    switch decisions, equal to the oracle controller fed the per-step mean over active ranks"""
+    from paper_2602_01872_b200.controller import Controller
+    from paper_2602_01872_b200.engine import merge_step_factors
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(100 + rank)
+    ctrl = Controller(30, 4, streak_threshold=5)
+    decisions = []
+    for epoch in range(25):
+        steps = []
+        for i, w, m in phase_plan(3, world, rank):     # W = 3: rank 1 idle in phase 1
+            steps.append((float(rng.uniform(0.0, 1.0)), 1.0) if w is not None else (0.0, 0.0))
+        mine = torch.tensor(steps, dtype=torch.float64).reshape(-1, 2)
+        every = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(every, mine)
+        lists = [e.tolist() for e in every]
+        for c in merge_step_factors(lists):
+            ctrl.observe(c)
+        decisions.append(ctrl.end_epoch())
+        out.put((rank, epoch, lists))
+    out.put((rank, "decisions", decisions))
+    dist.destroy_process_group()
+
+
+def test_two_rank_controller_agrees():
+    from oracle.controller import Controller as OC
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_ctrl_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    lists = {}
+    for _ in range(2 * 26):
+        r, k, v = q.get(timeout=300)
+        if k == "decisions":
+            got[r] = v
+        elif r == 0:
+            lists[k] = v
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    assert got[0] == got[1]
+    oc = OC(30, 4, streak_threshold=5)
+    ref = []
+    for epoch in range(25):
+        per_rank = lists[epoch]
+        for k in range(len(per_rank[0])):
+            cs = [r[k][0] for r in per_rank if r[k][1] > 0]
+            oc.observe(sum(cs) / len(cs))
+        ref.append(oc.end_epoch())
+    assert got[0] == ref and any(ref)

@@ -144,3 +144,33 @@ def test_minibatch_epoch_runs_and_reduces_loss(G, setup):
         ref = 0.05 * g.double()
         # theta is fp32 (~0.1): each update is exact up to theta's rounding (~1e-8)
         assert (d - ref).abs().max().item() <= 1e-3 * ref.abs().max().item() + 2e-8
+
+
+@pytest.mark.parametrize("fan", [[15, 10, 5], [1, 1, 2]])
+def test_sampled_blocks_bitexact_hubs(G, fan):
+    """Power-law partition with hub targets (d_l > 1024, the grid-parallel hub pick and, at
+    fanout 1, its exact fallback for hubs with fewer than f candidates): blocks bit-exact."""
+    ctx = G.Context(0)
+    wl = gen.small_workload("products", n=20011, scale=15, num_samples=540_000, train_frac=0.2)
+    ds = gen.make_dataset(wl)
+    d = "cuda"
+    rp, col = torch.from_numpy(ds.rowptr).to(d), torch.from_numpy(ds.col).to(d)
+    ch = torch.empty(wl.n, dtype=torch.int32, device=d)
+    G.grappa_partition(ctx, wl.n, 2, gen.seed_of("chunks"), ch)
+    chunk_of = Po.make_chunks(wl.n, 2, gen.seed_of("chunks"))
+    ref = Po.induced_partition(ds.rowptr, ds.col, chunk_of, 0, 1, ds.train)
+    assert np.max(ref["d_l"]) > 1024
+    p = G.grappa_repartition(ctx, rp, col, torch.from_numpy(ds.x).to(d), "f32", ch, 2, 0, 1,
+                             torch.from_numpy(ds.train).to(d), torch.from_numpy(ds.y).to(d))
+    hubs_seen = 0
+    for bi in range(3):
+        seeds = Sa.epoch_batches(ref, 11, 0, 1000)[bi]
+        b = G.grappa_sample(ctx, p, torch.from_numpy(seeds.astype(np.int32)).cuda(), fan, 11, 0, bi)
+        blocks = Sa.sample_batch(ref, seeds, fan, 11, 0, bi)
+        for l, (gb, ob) in enumerate(zip(b.blocks, blocks)):
+            hubs_seen += int(np.sum(np.asarray(ref["d_l"])[ob["dst"]] > 1024))
+            assert np.array_equal(gb["src"].cpu().numpy(), ob["src"]), (bi, l)
+            assert np.array_equal(gb["rowptr"].cpu().numpy(), ob["rowptr"]), (bi, l)
+            assert np.array_equal(gb["col"].cpu().numpy(), ob["col"]), (bi, l)
+    assert hubs_seen > 10
+    ctx.close()
