@@ -94,30 +94,49 @@ def pair_coverage(schedule: list, C: int) -> set:
     return {frozenset((i, j)) for i in range(C) for j in range(i + 1, C)} - covered
 
 
-def induced_partition(rowptr, col, chunk_of, base: int, swept: int, train=None):
-    """a3: induced-core partition of chunks {base, swept}.
+def induced_partition(rowptr, col, chunk_of, base: int, swept: int, train=None, halo: bool = False):
+    """a3: partition of chunks {base, swept}.
 
-    Returns dict: core (global ids, ascending), rowptr/col (local CSR, local ids, ascending),
-    d_l, d_g, seeds (local ids of core train nodes, ascending)."""
+    induced-core (default): core = nodes of both chunks, each core row keeps the
+    neighbours inside the core (cut edges dropped).
+    halo-1 ("halo nodes ... cache boundary neighbors", "Should an endpoint not be
+    part of the initial partition, it is incorporated as a halo node"; readings
+    R33/R34): halo = {u not in core : u in N(v) for some core v}; every core row keeps ALL its
+    neighbours (d_l = d_g), halo rows are empty (truncated adjacency, d_l = 0); local ids =
+    core in ascending global id, then halo in ascending global id.
+
+    Returns dict: core (global ids of ALL local nodes, core then halo), n_core, rowptr/col
+    (local CSR over all local nodes, local ids listed in ascending GLOBAL id per row -- the
+    same as ascending local id in induced-core mode), d_l, d_g (per local node),
+    seeds (local ids of core train nodes, ascending)."""
     if base == swept:
         raise ValueError("base == swept (S:139)")
     rowptr = np.asarray(rowptr, dtype=np.int64)
     col = np.asarray(col, dtype=np.int64)
     in_core = (chunk_of == base) | (chunk_of == swept)
     core = np.nonzero(in_core)[0]                       # ascending global id
+    nodes = core
+    if halo:
+        reach = np.zeros(chunk_of.size, dtype=bool)
+        for v in core:
+            reach[col[rowptr[v]:rowptr[v + 1]]] = True
+        nodes = np.concatenate([core, np.nonzero(reach & ~in_core)[0]])
+    visible = np.zeros(chunk_of.size, dtype=bool)
+    visible[nodes] = True
     local_of = np.full(chunk_of.size, -1, dtype=np.int64)
-    local_of[core] = np.arange(core.size)
-    d_g = (rowptr[core + 1] - rowptr[core]).astype(np.int64)
-    lrow = [np.zeros(0, dtype=np.int64)] * core.size
-    d_l = np.zeros(core.size, dtype=np.int64)
-    for i, v in enumerate(core):
+    local_of[nodes] = np.arange(nodes.size)
+    d_g = (rowptr[nodes + 1] - rowptr[nodes]).astype(np.int64)
+    lrow = [np.zeros(0, dtype=np.int64)] * nodes.size
+    d_l = np.zeros(nodes.size, dtype=np.int64)
+    for i, v in enumerate(core):                        # halo rows stay empty
         nb = col[rowptr[v]:rowptr[v + 1]]
-        kept = nb[in_core[nb]]                          # keeps ascending order
+        kept = nb[visible[nb]]                          # keeps ascending global order
         lrow[i] = local_of[kept]
         d_l[i] = kept.size
-    lrowptr = np.zeros(core.size + 1, dtype=np.int64)
+    lrowptr = np.zeros(nodes.size + 1, dtype=np.int64)
     np.cumsum(d_l, out=lrowptr[1:])
-    lcol = np.concatenate(lrow) if core.size else np.zeros(0, dtype=np.int64)
+    lcol = np.concatenate(lrow) if nodes.size else np.zeros(0, dtype=np.int64)
     seeds = np.zeros(0, dtype=np.int64) if train is None else \
         np.nonzero(np.asarray(train)[core] != 0)[0]
-    return dict(core=core, rowptr=lrowptr, col=lcol, d_l=d_l, d_g=d_g, seeds=seeds)
+    return dict(core=nodes, n_core=core.size, rowptr=lrowptr, col=lcol, d_l=d_l, d_g=d_g,
+                seeds=seeds)

@@ -188,3 +188,38 @@ def test_empty_seed_and_bad_label():
         Mo.loss_and_dlogits(np.zeros((3, 2)), np.zeros(3, int), [])
     with pytest.raises(ValueError):
         Mo.loss_and_dlogits(np.zeros((3, 2)), np.array([0, 2, 1]), [0, 1])
+
+
+@pytest.mark.parametrize("arch", ["gcn", "sage"])
+def test_halo1_partition_finite_differences(arch):
+    """halo-1 partitions make the local operator non-symmetric (core rows see halo nodes, halo
+    rows are empty): the backward must use the transpose.  Central differences of the loss over
+    the core seeds vs the reverse-mode gradient, depth 2."""
+    from oracle import partition as P
+    n = 40
+    rng = np.random.default_rng(3)
+    edges = [(a, b) for a in range(n) for b in range(a + 1, n) if rng.random() < 0.1]
+    rp, col = gen.csr_from_edges(n, edges)
+    ch = P.make_chunks(n, 5, 17)
+    part = P.induced_partition(rp, col, ch, 1, 3, np.ones(n, np.uint8), halo=True)
+    assert part["core"].size > part["n_core"]                 # there is a halo
+    m = part["core"].size
+    X = rng.standard_normal((m, 3))
+    y = rng.integers(0, 3, m)
+    nm = 1 if arch == "gcn" else 2
+    Ws = [[rng.standard_normal((3, 4)) for _ in range(nm)], [rng.standard_normal((4, 3)) for _ in range(nm)]]
+    L0, g, _, cache = Mo.partition_loss_grad(arch, part, X, y, Ws)
+    if np.min(np.abs(cache["Z"][0])) < 1e-4:
+        pytest.skip("pre-activation near a ReLU kink")
+    op = cache["op"].toarray()
+    assert not np.allclose(op, op.T)
+    theta = Mo.flatten(Ws)
+    shapes = [[w.shape for w in ws] for ws in Ws]
+    num = np.zeros_like(theta)
+    for i in range(theta.size):
+        tp, tm = theta.copy(), theta.copy()
+        tp[i] += 1e-6
+        tm[i] -= 1e-6
+        num[i] = (Mo.partition_loss_grad(arch, part, X, y, Mo.unflatten(tp, shapes))[0] -
+                  Mo.partition_loss_grad(arch, part, X, y, Mo.unflatten(tm, shapes))[0]) / 2e-6
+    assert np.max(np.abs(num - g)) / np.max(np.abs(g)) <= 1e-5

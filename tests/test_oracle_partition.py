@@ -153,3 +153,51 @@ def test_base_equals_swept_rejected():
     rp, col = gen.csr_from_edges(3, [(0, 1)])
     with pytest.raises(ValueError):
         P.induced_partition(rp, col, np.array([0, 1, 1]), 1, 1)
+
+
+def test_triangle_halo1_hand_example():
+    g = GOLD["triangle_partition_halo1"]
+    rp, col = gen.csr_from_edges(g["n"], g["edges"])
+    part = P.induced_partition(rp, col, np.array(g["chunk_of"]), g["base"], g["swept"], halo=True)
+    nc = part["n_core"]
+    assert part["core"][:nc].tolist() == g["core"] and part["core"][nc:].tolist() == g["halo"]
+    assert part["d_l"][:nc].tolist() == g["d_l_core"] and part["d_l"][nc:].tolist() == g["d_l_halo"]
+    # node 0's row: global neighbours 1 (core, local 1) and 2 (halo, local 2), ascending gid
+    assert part["col"][part["rowptr"][0]:part["rowptr"][1]].tolist() == [1, 2]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_halo1_partition_brute_force(seed):
+    """halo = {u not in core : some core v has u in N(v)}, by enumeration over the dense
+    adjacency; core rows keep every neighbour (d_l = d_g), halo rows are empty, every local edge
+    has a core endpoint, core and halo are disjoint, local ids core-then-halo ascending."""
+    n = 29
+    edges = _random_graph(n, 0.12, seed)
+    rp, col = gen.csr_from_edges(n, edges)
+    C = 5
+    ch = P.make_chunks(n, C, seed + 7)
+    train = (np.arange(n) % 2 == 0).astype(np.uint8)
+    Adense = np.zeros((n, n), dtype=int)
+    for u, v in edges:
+        Adense[u, v] = Adense[v, u] = 1
+    for b, s in itertools.permutations(range(C), 2):
+        part = P.induced_partition(rp, col, ch, b, s, train, halo=True)
+        core = [v for v in range(n) if ch[v] in (b, s)]
+        halo = [u for u in range(n) if u not in core and any(Adense[v, u] for v in core)]
+        nodes = core + halo
+        assert part["n_core"] == len(core) and part["core"].tolist() == nodes
+        for i, v in enumerate(nodes):
+            nb = part["col"][part["rowptr"][i]:part["rowptr"][i + 1]].tolist()
+            if i < len(core):
+                assert [nodes[j] for j in nb] == np.nonzero(Adense[v])[0].tolist()
+            else:
+                assert nb == []
+        assert part["d_l"][:len(core)].tolist() == part["d_g"][:len(core)].tolist()
+        assert part["d_g"].tolist() == Adense[nodes].sum(1).tolist()
+        assert part["seeds"].tolist() == [i for i, v in enumerate(core) if train[v]]
+    # C = 2: one pair holds every node, no halo, identical to induced-core
+    ch2 = P.make_chunks(n, 2, seed)
+    a = P.induced_partition(rp, col, ch2, 0, 1, train, halo=True)
+    b = P.induced_partition(rp, col, ch2, 0, 1, train)
+    for k in ("core", "rowptr", "col", "d_l", "d_g", "seeds"):
+        assert np.array_equal(a[k], b[k])
