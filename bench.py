@@ -44,6 +44,8 @@ def parse():
                     choices=["none", "uniform", "resampling", "resampling_hm", "node"],
                     help="override the config's estimator (node = node-level eq. (9), R30)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--halo", action="store_true",
+                    help="halo-1 partitions (R33) instead of induced-core")
     ap.add_argument("--variant", action="append", default=[],
                     help="kernel A/B knob op=value (grappa_set_kernel_variant), e.g. spmm=2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -139,7 +141,7 @@ class OracleSample:
     P and correction.  One `phase(i)` = the oracle's repartition of partition i + its
     forward/loss/backward + coverage-corrected aggregation + SGD (Alg. 1 with M = 1)."""
 
-    def __init__(self, name: str, shrink: int = 8, corr: str | None = None):
+    def __init__(self, name: str, shrink: int = 8, corr: str | None = None, halo: bool = False):
         import gen
         from oracle import partition as Po
         wl0 = gen.WORKLOADS[name]
@@ -155,6 +157,7 @@ class OracleSample:
         self.pairs = Po.sweep_schedule(self.wl.chunks, self.wl.chunks)[0]
         self.shrink = shrink
         self.corr = corr or self.wl.correction
+        self.halo = halo
 
     def phase(self, i: int) -> float:
         from oracle import correction as Co
@@ -169,7 +172,7 @@ class OracleSample:
         wl, ds = self.wl, self.ds
         t0 = time.perf_counter()
         b, s = self.pairs[i % wl.chunks]
-        part = Po.induced_partition(ds.rowptr, ds.col, self.chunk_of, b, s, ds.train)
+        part = Po.induced_partition(ds.rowptr, ds.col, self.chunk_of, b, s, ds.train, halo=self.halo)
         nw = Co.node_weights(part["d_l"], part["d_g"]) if self.corr == "node" else None
         _, g, _, _ = Mo.partition_loss_grad(wl.arch, part, self.X[part["core"]],
                                             ds.y[part["core"]], self.W, node_w=nw)
@@ -187,9 +190,9 @@ class OracleSample:
                 f"timed (repartition + fwd/bwd + aggregate + SGD), epoch = x{self.wl.chunks} phases")
 
 
-def oracle_baseline(name: str, budget_s: float = 30.0, corr: str | None = None):
+def oracle_baseline(name: str, budget_s: float = 30.0, corr: str | None = None, halo: bool = False):
     """cpu_baseline leg: phases of one epoch of the sample until ~budget_s of CPU work."""
-    o = OracleSample(name, corr=corr)
+    o = OracleSample(name, corr=corr, halo=halo)
     ts = []
     while len(ts) < o.wl.chunks and sum(ts) < budget_s:
         ts.append(o.phase(len(ts)))
@@ -204,7 +207,7 @@ def run_reference(args):
     paper ships none).  Rank 0 only; each step = one partition-phase of the 1/8 sample."""
     if int(os.environ.get("RANK", "0")) != 0:
         return
-    o = OracleSample(args.config, corr=args.corr)
+    o = OracleSample(args.config, corr=args.corr, halo=args.halo)
     K, W = args.steps, args.warmup
     for i in range(W):
         o.phase(i)
@@ -216,7 +219,7 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": statistics.mean(ts) * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": workload_desc(args.config, args.gpus, args.corr), "sample": desc},
+            "config": {"workload": workload_desc(args.config, args.gpus, args.corr, args.halo), "sample": desc},
             "cpu_baseline": {"value": value, "unit": "edges/s", "cores": 1, "kind": "oracle",
                              "sample": desc},
             "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0,
@@ -224,11 +227,12 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def workload_desc(name: str, world: int, corr: str | None = None) -> str:
+def workload_desc(name: str, world: int, corr: str | None = None, halo: bool = False) -> str:
     import gen
     wl = gen.WORKLOADS[name]
     return (f"{name}-shaped RMAT ({wl.n} nodes), {wl.arch.upper()}-{wl.depth}, P={wl.chunks} "
-            f"partitions, M={world} per phase, full-graph, {corr or wl.correction} correction, "
+            f"{'halo-1' if halo else 'induced-core'} partitions, M={world} per phase, full-graph, "
+            f"{corr or wl.correction} correction, "
             f"repartition every {wl.repartition_every} epochs")
 
 
@@ -267,7 +271,7 @@ def run_grappa(args):
     spec = ModelSpec(wl.arch, wl.dims, wl.dims_pad)
     stream = torch.cuda.current_stream(dev)
     common = dict(corr=args.corr or wl.correction, lr=0.003, repartition_every=wl.repartition_every,
-                  dtype=args.dtype, stream=stream, num_workers=wl.extra.get("workers"))
+                  dtype=args.dtype, stream=stream, num_workers=wl.extra.get("workers"), halo=args.halo)
     if wl.extra.get("mode") == "minibatch":
         tr = MinibatchTrainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights,
                               wl.chunks, gen.seed_of("chunks"), fanouts=wl.extra["fanouts"],
@@ -360,14 +364,14 @@ def run_grappa(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_baseline(args.config, corr=args.corr)
+        cpu = oracle_baseline(args.config, corr=args.corr, halo=args.halo)
 
     if rank == 0:
         line = {"metric": "edges_per_sec", "value": value, "unit": "edges/s", "n_gpus": world,
                 "steps": K, "warmup": args.warmup, "ms_per_step": ms / K,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32" if args.dtype == "f32" else "bf16", "data": "synthetic",
-                "config": {"workload": workload_desc(args.config, world, args.corr),
+                "config": {"workload": workload_desc(args.config, world, args.corr, args.halo),
                            "nnz_global": nnz, "partitions": wl.chunks, "phases_per_epoch": -(-wl.chunks // world),
                            "repartitions_timed": -(-K // wl.repartition_every),
                            "repartition_ms_total": rep_ms,

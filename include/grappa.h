@@ -77,7 +77,8 @@ typedef struct {
 
 /* Read-only view of a partition (all pointers dev, owned by the grappa_part). */
 typedef struct {
-    int64_t n_core;             /* |base chunk| + |swept chunk|                         */
+    int64_t n_core;             /* local nodes = rows of the local CSR: |base| + |swept|
+                                   core nodes, then n_halo halo nodes (halo-1 mode)     */
     int64_t nnz;                /* local directed edges (cut edges dropped)             */
     int64_t n_seeds;            /* core train nodes (reading R3)                 */
     int32_t base, swept;        /* chunk ids                                            */
@@ -105,6 +106,12 @@ typedef struct {
      *   [n, 2n)  w_v * norm_gcn[v]        (GCN backward gather scale)
      *   [2n, 3n) w_v * norm_sage[v] = 1/d_g where d_l > 0, else 0 (SAGE mean scale)      */
     const float* node_w;
+    /* halo-1 mode (GRAPPA_PART_HALO1, R33): local ids n_core - n_halo .. n_core - 1 are halo
+     * nodes (empty rows); the local operator is not symmetric, so the library also keeps its
+     * transpose (the backward aggregations run on it).  n_halo = 0 and t_* = NULL otherwise. */
+    int64_t n_halo;
+    const int64_t* t_rowptr;    /* [n_core+1] transpose CSR (sources of every column)   */
+    const int32_t* t_col;       /* [nnz] source local ids, ascending per row            */
 } grappa_part_info;
 
 /* ----------------------------------------------------------------------------------- */
@@ -146,6 +153,20 @@ grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g, const voi
                                  int32_t num_chunks, int32_t base, int32_t swept,
                                  const uint8_t* train_mask, const int32_t* labels,
                                  grappa_part** inout, void* stream);
+/* grappa_repartition with flags:
+ *   GRAPPA_PART_HALO1 : halo-1 partition ("halo nodes ... cache boundary neighbors", P:196
+ *     "incorporated as a halo node"; readings R33/R34): halo = non-core neighbours
+ *     of core nodes; core rows keep ALL their neighbours (d_l = d_g), halo rows are empty; local
+ *     ids = core (ascending global id) then halo (ascending global id); each row lists its
+ *     neighbours in ascending global id; features gathered for core and halo rows; seeds = core
+ *     train nodes.  One more host sync (halo count) and a transpose (radix sort) are built.
+ * flags = 0 is grappa_repartition.  Errors as grappa_repartition; E_ARG for unknown flags. */
+#define GRAPPA_PART_HALO1 1u
+grappa_status grappa_repartition_ex(grappa_ctx* ctx, const grappa_csr* g, const void* feats,
+                                    int32_t feat_dim, grappa_dtype dtype, const int32_t* chunk_of,
+                                    int32_t num_chunks, int32_t base, int32_t swept,
+                                    const uint8_t* train_mask, const int32_t* labels, unsigned flags,
+                                    grappa_part** inout, void* stream);
 grappa_status grappa_part_query(const grappa_part* part, grappa_part_info* out);
 void grappa_part_destroy(grappa_part* part);
 

@@ -124,6 +124,9 @@ class Part:
         self.seeds = _view(I.seeds, (s,), "<i4", self)
         self.labels = _view(I.labels, (n,), "<i4", self)
         self.node_w = _view(I.node_w, (3, n), "<f4", self)
+        self.n_halo = I.n_halo
+        self.t_rowptr = _view(I.t_rowptr, (n + 1,), "<i8", self) if I.t_rowptr else None
+        self.t_col = _view(I.t_col, (m,), "<i4", self) if I.t_col else None
         if I.feat_dim:
             if I.dtype == BF16:
                 self.x = _view(I.x, (n, I.feat_dim), "<i2", self).view(torch.bfloat16)
@@ -182,14 +185,15 @@ def grappa_partition(ctx: Context, num_nodes: int, num_chunks: int, seed: int, c
 
 def grappa_repartition(ctx: Context, rowptr: torch.Tensor, col: torch.Tensor, feats, dtype,
                        chunk_of: torch.Tensor, num_chunks: int, base: int, swept: int,
-                       train_mask: torch.Tensor, labels, part: Part | None = None, stream=None) -> Part:
+                       train_mask: torch.Tensor, labels, part: Part | None = None, stream=None,
+                       halo: bool = False) -> Part:
     g = _lib.Csr(rowptr.numel() - 1, col.numel(), rowptr.data_ptr(), col.data_ptr())
     part = part or Part()
     fdim = 0 if feats is None else feats.shape[1]
-    _lib.check("grappa_repartition", ctx.lib.grappa_repartition(
+    _lib.check("grappa_repartition_ex", ctx.lib.grappa_repartition_ex(
         ctx.h, ctypes.byref(g), _lib.ptr(feats), fdim, dtype_code(dtype), _lib.ptr(chunk_of),
-        num_chunks, base, swept, _lib.ptr(train_mask), _lib.ptr(labels), ctypes.byref(part.h),
-        _lib.stream_ptr(stream)))
+        num_chunks, base, swept, _lib.ptr(train_mask), _lib.ptr(labels),
+        _lib.PART_HALO1 if halo else 0, ctypes.byref(part.h), _lib.stream_ptr(stream)))
     return part.refresh()
 
 

@@ -17,6 +17,7 @@ GCN, SAGE = 0, 1
 CORR = {"none": 0, "uniform": 1, "resampling": 2, "resampling_hm": 3, "node": 4}
 BWD_DZ_OUT_NORMED, BWD_DZ_IN_NORMED = 1, 2
 LAYER_NODE_LEVEL = 4
+PART_HALO1 = 1
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_EMPTY", 4: "E_NONFINITE", 5: "E_SUPPORT",
           6: "E_NOMEM", 7: "E_CUDA", 8: "E_NCCL"}
 
@@ -31,7 +32,7 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_minibatch_ws_bytes", "grappa_minibatch_step", "grappa_part_download",
            "grappa_part_upload", "grappa_layer_bwd_ex", "grappa_layer_fwd_ex",
            "grappa_minibatch_step_ex", "grappa_sample_async", "grappa_sample_wait",
-           "grappa_sample_event"]
+           "grappa_sample_event", "grappa_repartition_ex"]
 KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5, "sample": 6}
 
 
@@ -57,7 +58,8 @@ class PartInfo(ctypes.Structure):
                 ("n_heavy", ctypes.c_int64), ("n_slots", ctypes.c_int64),
                 ("c_uniform", ctypes.c_double), ("c_resampling", ctypes.c_double),
                 ("c_resampling_hm", ctypes.c_double), ("D", ctypes.c_int64),
-                ("node_w", ctypes.c_void_p)]
+                ("node_w", ctypes.c_void_p), ("n_halo", ctypes.c_int64),
+                ("t_rowptr", ctypes.c_void_p), ("t_col", ctypes.c_void_p)]
 
 
 class PartHost(ctypes.Structure):
@@ -97,6 +99,8 @@ def load(path: str = LIB_PATH):
         "grappa_partition": (st, [vp, i64, i32, u64, vp, vp, vp]),
         "grappa_repartition": (st, [vp, ctypes.POINTER(Csr), vp, i32, ctypes.c_int, vp, i32, i32,
                                     i32, vp, vp, ctypes.POINTER(vp), vp]),
+        "grappa_repartition_ex": (st, [vp, ctypes.POINTER(Csr), vp, i32, ctypes.c_int, vp, i32, i32,
+                                       i32, vp, vp, ctypes.c_uint, ctypes.POINTER(vp), vp]),
         "grappa_part_query": (st, [vp, ctypes.POINTER(PartInfo)]),
         "grappa_part_destroy": (None, [vp]),
         "grappa_layer_saved_bytes": (sz, [vp, ctypes.c_int, i32, i32, ctypes.c_int]),

@@ -197,7 +197,7 @@ extern "C" size_t grappa_layer_saved_bytes(const grappa_part* part, grappa_arch 
 extern "C" size_t grappa_layer_ws_bytes(const grappa_part* part, grappa_arch arch, int32_t f_in,
                                         int32_t f_out, grappa_dtype dtype) {
     if (!part) return 0;
-    const int64_t n = part->info.n_core, slots = part->info.n_slots;
+    const int64_t n = part->info.n_core, slots = std::max<int64_t>(part->info.n_slots, part->t_n_slots);
     const size_t es = esz_of(dtype);
     const int wmax = f_in > f_out ? f_in : f_out;
     size_t node = (size_t)n * (arch == GRAPPA_GCN ? f_out : f_in) * es;       // T / dT / dM
@@ -216,7 +216,7 @@ struct WsLayout {
 };
 static WsLayout carve(const grappa_part* part, grappa_arch arch, int f_in, int f_out,
                       grappa_dtype dt, void* ws) {
-    const int64_t n = part->info.n_core, slots = part->info.n_slots;
+    const int64_t n = part->info.n_core, slots = std::max<int64_t>(part->info.n_slots, part->t_n_slots);
     const size_t es = esz_of(dt);
     const int wmax = f_in > f_out ? f_in : f_out;
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
@@ -316,7 +316,7 @@ extern "C" grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part*
     cudaStream_t s = (cudaStream_t)stream;
     const grappa_part_info& I = part->info;
     WsLayout L = carve(part, arch, f_in, f_out, dtype, ws);
-    if (arch == GRAPPA_GCN && dz_in && flags == 0 && spmm_mm_supported(part, f_out, f_in, dtype)) {
+    if (arch == GRAPPA_GCN && dz_in && flags == 0 && !part->halo && spmm_mm_supported(part, f_out, f_in, dtype)) {
         // dT = Ahat dz_out and dz_in = (dT W^T) * relu'(h_in) in one fused kernel, then
         // dW = h_in^T dT
         AggMMArgs m;
@@ -340,7 +340,7 @@ extern "C" grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part*
             a.self_scale = out_normed ? nullptr : I.norm_gcn;
         }
         a.self = 1; a.out = L.node; a.partial = L.partial;
-        GRAPPA_TRY(spmm(ctx, part, a, dtype, s));
+        GRAPPA_TRY(spmm_t(ctx, part, a, dtype, s));          // transpose operator (halo-1, R33)
         // dW = h_in^T dT
         GemmTNArgs t;
         t.M = I.n_core; t.K1 = f_in; t.N = f_out; t.A1 = h_in; t.B = L.node; t.C = dw; t.ws = L.splitk;
@@ -367,7 +367,7 @@ extern "C" grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part*
     SpmmArgs a;
     a.X = L.node; a.width = f_in; a.col_scale = node ? I.node_w + 2 * I.n_core : I.norm_sage; a.accumulate = 1;
     a.mask = relu_in ? h_in : nullptr; a.out = dz_in; a.partial = L.partial;
-    return spmm(ctx, part, a, dtype, s);
+    return spmm_t(ctx, part, a, dtype, s);
 }
 
 // ------------------------------------------------------------------------------ aggregate

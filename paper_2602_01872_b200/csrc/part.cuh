@@ -26,4 +26,11 @@ struct grappa_part {
     // per row in that order: {v, d_l, rowptr[v] lo, hi} -- one coalesced 16-byte load replaces
     // the dependent row_order -> rowptr lookups at the head of every SpMM row
     grappa::DevBuf row_desc;
+    // halo-1 mode (R33): the local operator is not symmetric, so the backward aggregations run
+    // on its transpose, with the same SpMM plan structures (split rows, order, descriptors)
+    bool halo = false;
+    int64_t n_halo = 0;
+    grappa::DevBuf t_rowptr, t_col, t_deg, t_heavy_rows, t_heavy_slot_off, t_slot_row, t_slot_seg,
+        t_row_order, t_row_desc, t_tmp;
+    int64_t t_n_heavy = 0, t_n_slots = 0;
 };

@@ -16,6 +16,8 @@
 //   5. features     core rows gathered into local order (16-byte vector copies).
 //   6. coverage     fixed-order block partials over the seeds: sum d_l/d_g (f64) and the
 //                   exact integers D = sum (d_g - d_l), sum d_l, sum d_g (d_l > 0).
+#include <cub/device/device_radix_sort.cuh>
+
 #include "part.cuh"
 #include "scan.cuh"
 
@@ -70,10 +72,82 @@ struct NumSeg {
     }
 };
 struct WriteSlotOff {
-    int32_t* slot_off; int64_t* stat;
+    int32_t* slot_off; int64_t* stat; int idx;
     __device__ void operator()(int64_t h, int64_t p, int32_t) const { slot_off[h] = (int32_t)p; }
-    __device__ void finish(int64_t n, int64_t total) const { slot_off[n] = (int32_t)total; stat[4] = total; }
+    __device__ void finish(int64_t n, int64_t total) const { slot_off[n] = (int32_t)total; stat[idx] = total; }
 };
+
+// halo-1 (R33): halo = non-core neighbours of core rows; local ids n_core + rank among them
+__global__ void k_mark_halo(const int64_t* __restrict__ d_ncore, const int32_t* __restrict__ core_global,
+                            const int64_t* __restrict__ g_rowptr, const int32_t* __restrict__ g_col,
+                            const int32_t* __restrict__ rank, uint8_t* __restrict__ flag) {
+    const int lane = threadIdx.x & 31;
+    const int64_t n = *d_ncore;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps) {
+        const int32_t v = core_global[i];
+        for (int64_t e = g_rowptr[v] + lane; e < g_rowptr[v + 1]; e += 32) {
+            const int32_t u = g_col[e];
+            if (rank[u] < 0) flag[u] = 1;          // idempotent store
+        }
+    }
+}
+struct FlagHalo {
+    const uint8_t* flag;
+    __device__ int32_t operator()(int64_t v) const { return flag[v]; }
+};
+struct WriteHaloRank {
+    int32_t* rank; int32_t* core_global; int64_t* stat;
+    __device__ void operator()(int64_t v, int64_t p, int32_t f) const {
+        if (f) {
+            const int64_t id = stat[0] + p;          // after the n_core core nodes
+            rank[v] = (int32_t)id;
+            core_global[id] = (int32_t)v;
+        }
+    }
+    __device__ void finish(int64_t, int64_t total) const { stat[6] = total; }
+};
+// halo rows: empty (d_l = 0), GCN norm 1, SAGE norm 0, node weight w = [d_g == 0]
+__global__ void k_halo_rows(int64_t n_core, int64_t n_local, const int64_t* __restrict__ d_nnz,
+                            const int32_t* __restrict__ core_global, const int64_t* __restrict__ g_rowptr,
+                            const int32_t* __restrict__ g_labels, int64_t* rowptr, int32_t* d_l, int32_t* d_g,
+                            float* norm_gcn, float* norm_sage, float* node_w, int32_t* labels) {
+    const int64_t nnz = *d_nnz;
+    for (int64_t i = n_core + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_local;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = core_global[i];
+        const int32_t dg = (int32_t)(g_rowptr[v + 1] - g_rowptr[v]);
+        rowptr[i + 1] = nnz;
+        d_l[i] = 0;
+        d_g[i] = dg;
+        norm_gcn[i] = 1.0f;
+        norm_sage[i] = 0.0f;
+        const float w = dg == 0 ? 1.0f : 0.0f;
+        node_w[i] = w;
+        node_w[n_local + i] = w;
+        node_w[2 * n_local + i] = 0.0f;
+        labels[i] = g_labels ? g_labels[v] : 0;
+    }
+}
+// transpose support: source row of every local edge
+__global__ void k_edge_rows(int64_t n_rows, const int64_t* __restrict__ rowptr, int32_t* __restrict__ erow) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_rows; i += nwarps)
+        for (int64_t e = rowptr[i] + lane; e < rowptr[i + 1]; e += 32) erow[e] = (int32_t)i;
+}
+// transpose rowptr from the sorted column keys; degree of every transposed row
+__global__ void k_t_rowptr(int64_t n, int64_t nnz, const int32_t* __restrict__ skeys, int64_t* __restrict__ trowptr) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t cur = e < nnz ? skeys[e] : n;
+        const int64_t prev = e > 0 ? skeys[e - 1] : -1;
+        for (int64_t r = prev + 1; r <= cur && r <= n; r++) trowptr[r] = e;
+    }
+}
+__global__ void k_row_deg(int64_t n, const int64_t* __restrict__ rowptr, int32_t* __restrict__ deg) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        deg[i] = (int32_t)(rowptr[i + 1] - rowptr[i]);
+}
 
 // Global rows are cut into tasks of at most kTaskLen edges (power-law hubs reach 10^5
 // neighbours; one warp per task keeps every warp's work bounded).  Tasks are numbered in
@@ -135,7 +209,7 @@ __global__ void k_row_finalize(int64_t n_core, const int32_t* __restrict__ task_
                                const int64_t* __restrict__ task_out, const int32_t* __restrict__ core_global,
                                const int64_t* __restrict__ g_rowptr, const int32_t* __restrict__ g_labels,
                                int64_t* rowptr, int32_t* d_l, int32_t* d_g, float* norm_gcn, float* norm_sage,
-                               float* node_w, int32_t* labels) {
+                               float* node_w, int64_t w_stride, int32_t* labels) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_core;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t a = task_out[task_off[i]], b = task_out[task_off[i + 1]];
@@ -152,8 +226,8 @@ __global__ void k_row_finalize(int64_t n_core, const int32_t* __restrict__ task_
         // node-level estimator (eq. (9), R30): w = d_l/d_g, 1 iff d_g = 0
         const double w = dg == 0 ? 1.0 : (double)cnt / (double)dg;
         node_w[i] = (float)w;
-        node_w[n_core + i] = (float)(w * ng);
-        node_w[2 * n_core + i] = (float)(w * ns);
+        node_w[w_stride + i] = (float)(w * ng);
+        node_w[2 * w_stride + i] = (float)(w * ns);
         labels[i] = g_labels ? g_labels[v] : 0;
     }
 }
@@ -326,14 +400,80 @@ static grappa_status rp_grid(grappa_ctx* ctx, int64_t rows, int threads, unsigne
     return GRAPPA_OK;
 }
 
+// SpMM plan of one CSR: rows with deg > kSegLen split into kSegLen-edge slots (fixed-order
+// fix-up combine), degree-bucketed row order, 16-byte row descriptors.  Two host syncs (the
+// split-row and slot counts size the slot tables).
+struct PlanBufs {
+    DevBuf *heavy_rows, *heavy_slot_off, *slot_row, *slot_seg, *row_order, *row_desc;
+};
+static grappa_status build_plan(grappa_ctx* ctx, cudaStream_t s, int64_t n, const int64_t* rowptr,
+                                const int32_t* deg, PlanBufs b, int64_t* d_st, int64_t* n_heavy_out,
+                                int64_t* n_slots_out) {
+    GRAPPA_TRY(b.heavy_rows->grow((size_t)(n > 0 ? n : 1) * 4));
+    GRAPPA_TRY(b.heavy_slot_off->grow((size_t)(n + 1) * 4));
+    GRAPPA_TRY(device_scan(ctx, FlagHeavy{deg}, n, WriteCompact{(int32_t*)b.heavy_rows->p, d_st, 0}, s));
+    int64_t n_heavy = 0;
+    GRAPPA_CUDA(cudaMemcpyAsync(&n_heavy, d_st, 8, cudaMemcpyDeviceToHost, s));
+    GRAPPA_CUDA(cudaStreamSynchronize(s));
+    int64_t n_slots = 0;
+    if (n_heavy > 0) {
+        GRAPPA_TRY(device_scan(ctx, NumSeg{deg, (int32_t*)b.heavy_rows->p}, n_heavy,
+                               WriteSlotOff{(int32_t*)b.heavy_slot_off->p, d_st, 1}, s));
+        GRAPPA_CUDA(cudaMemcpyAsync(&n_slots, d_st + 1, 8, cudaMemcpyDeviceToHost, s));
+        GRAPPA_CUDA(cudaStreamSynchronize(s));
+    }
+    GRAPPA_TRY(b.slot_row->grow((size_t)(n_slots > 0 ? n_slots : 1) * 4));
+    GRAPPA_TRY(b.slot_seg->grow((size_t)(n_slots > 0 ? n_slots : 1) * 4));
+    if (n_heavy > 0) {
+        k_slot_tasks<<<(unsigned)std::min<int64_t>(ceil_div(n_heavy, 256), 1024), 256, 0, s>>>(
+            n_heavy, (int32_t*)b.heavy_rows->p, (int32_t*)b.heavy_slot_off->p, (int32_t*)b.slot_row->p,
+            (int32_t*)b.slot_seg->p);
+        GRAPPA_LAUNCHED(ctx);
+    }
+    // row order: counting sort by descending min(deg, kSegLen + 1)
+    GRAPPA_TRY(b.row_order->grow((size_t)(n > 0 ? n : 1) * 4));
+    GRAPPA_TRY(ctx->red_ws.grow((size_t)2 * kDegBuckets * 8));
+    unsigned long long* bins = (unsigned long long*)ctx->red_ws.p;
+    GRAPPA_CUDA(cudaMemsetAsync(bins, 0, (size_t)kDegBuckets * 8, s));
+    const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 8));
+    k_deg_hist<<<g2, 256, 0, s>>>(n, deg, bins);
+    GRAPPA_LAUNCHED(ctx);
+    k_deg_bins_scan<<<1, 32, 0, s>>>(bins, bins + kDegBuckets);
+    GRAPPA_LAUNCHED(ctx);
+    const int64_t per = 4096;
+    if (n > 0) {
+        k_deg_scatter<<<(unsigned)ceil_div(n, per), 256, 0, s>>>(n, per, deg, bins + kDegBuckets,
+                                                                 (int32_t*)b.row_order->p);
+        GRAPPA_LAUNCHED(ctx);
+    }
+    GRAPPA_TRY(b.row_desc->grow((size_t)(n > 0 ? n : 1) * 16));
+    k_row_desc<<<g2, 256, 0, s>>>(n, (int32_t*)b.row_order->p, rowptr, (int4*)b.row_desc->p);
+    GRAPPA_LAUNCHED(ctx);
+    *n_heavy_out = n_heavy;
+    *n_slots_out = n_slots;
+    return GRAPPA_OK;
+}
+
 extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g, const void* feats,
                                             int32_t feat_dim, grappa_dtype dtype,
                                             const int32_t* chunk_of, int32_t num_chunks,
                                             int32_t base, int32_t swept, const uint8_t* train_mask,
                                             const int32_t* labels, grappa_part** inout,
                                             void* stream) {
+    return grappa_repartition_ex(ctx, g, feats, feat_dim, dtype, chunk_of, num_chunks, base, swept,
+                                 train_mask, labels, 0u, inout, stream);
+}
+
+extern "C" grappa_status grappa_repartition_ex(grappa_ctx* ctx, const grappa_csr* g, const void* feats,
+                                               int32_t feat_dim, grappa_dtype dtype,
+                                               const int32_t* chunk_of, int32_t num_chunks,
+                                               int32_t base, int32_t swept, const uint8_t* train_mask,
+                                               const int32_t* labels, unsigned flags,
+                                               grappa_part** inout, void* stream) {
     GRAPPA_ARG(ctx && g && chunk_of && train_mask && inout, GRAPPA_E_ARG,
                "grappa_repartition: null argument");
+    GRAPPA_ARG((flags & ~GRAPPA_PART_HALO1) == 0, GRAPPA_E_ARG, "grappa_repartition_ex: flags 0x%x invalid",
+               flags);
     GRAPPA_ARG(base != swept, GRAPPA_E_ARG, "grappa_repartition: base == swept (S:139)");
     GRAPPA_ARG(base >= 0 && swept >= 0 && base < num_chunks && swept < num_chunks, GRAPPA_E_ARG,
                "grappa_repartition: chunk id out of range");
@@ -341,6 +481,7 @@ extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g
                "grappa_repartition: feat_dim must be a positive multiple of 16");
     GRAPPA_ARG(g->num_nodes > 0 && g->num_nodes < (1ll << 31), GRAPPA_E_ARG,
                "grappa_repartition: num_nodes out of int32 range");
+    const bool halo = flags & GRAPPA_PART_HALO1;
     cudaStream_t s = (cudaStream_t)stream;
     ProfScope ps(ctx, s, GRAPPA_K_REPART, 0.0, 0.0);
     grappa_part* p = *inout ? *inout : new grappa_part();
@@ -357,36 +498,47 @@ extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g
         if (_s != GRAPPA_OK) return fail(_s);      \
     } while (0)
 
-    // stats: [0]=n_core [1]=nnz [2]=n_seeds [3]=n_heavy [4]=n_slots ; then SeedStats
+    // stats: [0]=n_core [1]=nnz [2]=n_seeds [3]=n_heavy [4]=n_slots [5]=T [6]=n_halo ; then SeedStats
     RP_TRY(ctx->small.grow(16 * sizeof(int64_t) + sizeof(SeedStats)));
     int64_t* d_stat = (int64_t*)ctx->small.p;
     SeedStats* d_seedstats = (SeedStats*)(d_stat + 8);
-    RP_TRY(ctx->red_ws.grow((size_t)N * sizeof(int32_t)));       // rank table
+    // rank table (int32 [N]) + halo flags (uint8 [N], halo-1 only)
+    RP_TRY(ctx->red_ws.grow((size_t)N * sizeof(int32_t) + (halo ? (size_t)N : 0)));
     int32_t* rank = (int32_t*)ctx->red_ws.p;
+    uint8_t* hflag = (uint8_t*)(rank + N);
     // 1. rank table.  core_global capacity: N (freed/reused across super-epochs)
     RP_TRY(p->core_global.grow((size_t)N * sizeof(int32_t)));
     RP_TRY(device_scan(ctx, FlagCore{chunk_of, base, swept}, N,
                        WriteRank{rank, (int32_t*)p->core_global.p, d_stat}, s));
-    int64_t n_core = 0;
-    if (cudaMemcpyAsync(&n_core, d_stat, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+    if (halo) {
+        // 1b. halo = non-core neighbours of core rows; they extend the rank table after the core
+        GRAPPA_CUDA(cudaMemsetAsync(hflag, 0, (size_t)N, s));
+        k_mark_halo<<<(unsigned)ctx->sm_count * 16, 256, 0, s>>>(d_stat, (int32_t*)p->core_global.p,
+                                                                  g->rowptr, g->col, rank, hflag);
+        GRAPPA_LAUNCHED(ctx);
+        RP_TRY(device_scan(ctx, FlagHalo{hflag}, N, WriteHaloRank{rank, (int32_t*)p->core_global.p, d_stat}, s));
+    } else {
+        GRAPPA_CUDA(cudaMemsetAsync(d_stat + 6, 0, 8, s));
+    }
+    int64_t cnt2[7];
+    if (cudaMemcpyAsync(cnt2, d_stat, 7 * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess) {
         set_error("grappa_repartition: %s", cudaGetErrorString(cudaGetLastError()));
         return fail(GRAPPA_E_CUDA);
     }
+    const int64_t n_core = cnt2[0], n_halo = cnt2[6], n_local = n_core + n_halo;
     GRAPPA_ARG(n_core > 0, fail(GRAPPA_E_EMPTY), "grappa_repartition: empty partition");
-    // 2. per-row counts
-    RP_TRY(p->d_l.grow(n_core * 4));
-    RP_TRY(p->d_g.grow(n_core * 4));
-    RP_TRY(p->norm_gcn.grow(n_core * 4));
-    RP_TRY(p->norm_sage.grow(n_core * 4));
-    RP_TRY(p->node_w.grow(n_core * 12));
-    RP_TRY(p->labels.grow(n_core * 4));
-    RP_TRY(p->rowptr.grow((n_core + 1) * 8));
+    // 2. per-row counts (core rows from their global rows; halo rows are empty)
+    RP_TRY(p->d_l.grow(n_local * 4));
+    RP_TRY(p->d_g.grow(n_local * 4));
+    RP_TRY(p->norm_gcn.grow(n_local * 4));
+    RP_TRY(p->norm_sage.grow(n_local * 4));
+    RP_TRY(p->node_w.grow(n_local * 12));
+    RP_TRY(p->labels.grow(n_local * 4));
+    RP_TRY(p->rowptr.grow((n_local + 1) * 8));
     RP_TRY(p->seeds.grow(n_core * 4));
-    RP_TRY(p->heavy_rows.grow(n_core * 4));
-    RP_TRY(p->heavy_slot_off.grow((n_core + 1) * 4));
     unsigned grid;
-    rp_grid(ctx, n_core, 256, &grid);
+    rp_grid(ctx, n_local, 256, &grid);
     // task workspace: T <= n_core + nnz_global / kTaskLen + 1 (upper bound; the exact T stays
     // on the device and the task kernels grid-stride up to it -- no host sync needed)
     const int64_t T_max = n_core + g->nnz / kTaskLen + 1;
@@ -410,37 +562,40 @@ extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g
     k_row_finalize<<<grid, 256, 0, s>>>(n_core, task_off, task_out, core_global, g->rowptr, labels,
                                          (int64_t*)p->rowptr.p, (int32_t*)p->d_l.p, (int32_t*)p->d_g.p,
                                          (float*)p->norm_gcn.p, (float*)p->norm_sage.p,
-                                         (float*)p->node_w.p, (int32_t*)p->labels.p);
+                                         (float*)p->node_w.p, n_local, (int32_t*)p->labels.p);
     GRAPPA_LAUNCHED(ctx);
+    if (halo && n_halo > 0) {
+        k_halo_rows<<<grid, 256, 0, s>>>(n_core, n_local, d_stat + 1, core_global, g->rowptr, labels,
+                                          (int64_t*)p->rowptr.p, (int32_t*)p->d_l.p, (int32_t*)p->d_g.p,
+                                          (float*)p->norm_gcn.p, (float*)p->norm_sage.p,
+                                          (float*)p->node_w.p, (int32_t*)p->labels.p);
+        GRAPPA_LAUNCHED(ctx);
+    }
     RP_TRY(device_scan(ctx, FlagSeed{(int32_t*)p->core_global.p, train_mask}, n_core,
                        WriteCompact{(int32_t*)p->seeds.p, d_stat, 2}, s));
-    RP_TRY(device_scan(ctx, FlagHeavy{(int32_t*)p->d_l.p}, n_core,
-                       WriteCompact{(int32_t*)p->heavy_rows.p, d_stat, 3}, s));
-    int64_t st[5];
-    if (cudaMemcpyAsync(st, d_stat, 5 * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+    int64_t st[3];
+    if (cudaMemcpyAsync(st, d_stat, 3 * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess) {
         set_error("grappa_repartition: %s", cudaGetErrorString(cudaGetLastError()));
         return fail(GRAPPA_E_CUDA);
     }
-    const int64_t nnz = st[1], n_seeds = st[2], n_heavy = st[3];
+    const int64_t nnz = st[1], n_seeds = st[2];
     GRAPPA_ARG(n_seeds > 0, fail(GRAPPA_E_EMPTY),
                "grappa_repartition: partition (%d,%d) has no seeds (S:213)", base, swept);
-    RP_TRY(device_scan(ctx, NumSeg{(int32_t*)p->d_l.p, (int32_t*)p->heavy_rows.p}, n_heavy,
-                       WriteSlotOff{(int32_t*)p->heavy_slot_off.p, d_stat}, s));
     // 4. fill
     RP_TRY(p->col.grow((size_t)(nnz > 0 ? nnz : 1) * 4));
     k_task_fill<<<tgrid, 256, 0, s>>>(d_stat + 5, task_row, task_off, task_out, core_global, g->rowptr,
                                        g->col, rank, (int32_t*)p->col.p);
     GRAPPA_LAUNCHED(ctx);
-    // 5. features
+    // 5. features (core and halo rows)
     const int64_t esz = dtype == GRAPPA_BF16 ? 2 : 4;
     if (feats) {
-        RP_TRY(p->x.grow((size_t)n_core * feat_dim * esz));
-        k_gather_rows<<<grid, 256, 0, s>>>(n_core, feat_dim * esz, (int32_t*)p->core_global.p,
+        RP_TRY(p->x.grow((size_t)n_local * feat_dim * esz));
+        k_gather_rows<<<grid, 256, 0, s>>>(n_local, feat_dim * esz, (int32_t*)p->core_global.p,
                                            (const uint4*)feats, (uint4*)p->x.p);
         GRAPPA_LAUNCHED(ctx);
     }
-    // 6. coverage statistics
+    // 6. coverage statistics over the seeds (R3; in halo-1 mode every seed has d_l = d_g, R33)
     int nb = (int)std::min<int64_t>(ceil_div(n_seeds, 4096), (int64_t)ctx->sm_count * 4);
     if (nb < 1) nb = 1;
     RP_TRY(ctx->scan_ws.grow((size_t)nb * sizeof(SeedStats)));
@@ -449,46 +604,60 @@ extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g
     GRAPPA_LAUNCHED(ctx);
     k_seed_stats_final<<<1, 32, 0, s>>>(nb, (SeedStats*)ctx->scan_ws.p, d_seedstats);
     GRAPPA_LAUNCHED(ctx);
-    int64_t n_slots = 0;
     SeedStats hs;
-    if (cudaMemcpyAsync(&n_slots, d_stat + 4, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaMemcpyAsync(&hs, d_seedstats, sizeof(hs), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess) {
+    if (cudaMemcpyAsync(&hs, d_seedstats, sizeof(hs), cudaMemcpyDeviceToHost, s) != cudaSuccess) {
         set_error("grappa_repartition: %s", cudaGetErrorString(cudaGetLastError()));
         return fail(GRAPPA_E_CUDA);
     }
-    if (n_heavy == 0) n_slots = 0;
-    RP_TRY(p->slot_row.grow((size_t)(n_slots > 0 ? n_slots : 1) * 4));
-    RP_TRY(p->slot_seg.grow((size_t)(n_slots > 0 ? n_slots : 1) * 4));
-    if (n_heavy > 0) {
-        k_slot_tasks<<<(unsigned)std::min<int64_t>(ceil_div(n_heavy, 256), 1024), 256, 0, s>>>(
-            n_heavy, (int32_t*)p->heavy_rows.p, (int32_t*)p->heavy_slot_off.p,
-            (int32_t*)p->slot_row.p, (int32_t*)p->slot_seg.p);
+    // 7. SpMM plan of the local CSR (split rows, row order, descriptors)
+    int64_t n_heavy = 0, n_slots = 0;
+    RP_TRY(build_plan(ctx, s, n_local, (int64_t*)p->rowptr.p, (int32_t*)p->d_l.p,
+                      PlanBufs{&p->heavy_rows, &p->heavy_slot_off, &p->slot_row, &p->slot_seg, &p->row_order,
+                               &p->row_desc},
+                      d_stat + 3, &n_heavy, &n_slots));
+    // 8. halo-1: transpose CSR + its plan (the backward aggregations, R33).  Stable radix sort
+    // of (column, source row) over edges listed row by row -> each transposed row lists its
+    // sources in ascending local id (deterministic).
+    p->halo = halo;
+    p->n_halo = n_halo;
+    p->t_n_heavy = p->t_n_slots = 0;
+    if (halo) {
+        RP_TRY(p->t_rowptr.grow((size_t)(n_local + 1) * 8));
+        RP_TRY(p->t_col.grow((size_t)(nnz > 0 ? nnz : 1) * 4));
+        RP_TRY(p->t_deg.grow((size_t)n_local * 4));
+        int end_bit = 1;
+        while (((int64_t)1 << end_bit) <= n_local) end_bit++;
+        size_t sort_bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                        (const int32_t*)nullptr, (int32_t*)nullptr, (int)nnz, 0, end_bit, s);
+        const size_t e4 = al((size_t)(nnz > 0 ? nnz : 1) * 4);
+        RP_TRY(p->t_tmp.grow(2 * e4 + sort_bytes));
+        int32_t* erow = (int32_t*)p->t_tmp.p;
+        int32_t* skeys = (int32_t*)((char*)p->t_tmp.p + e4);
+        void* stmp = (char*)p->t_tmp.p + 2 * e4;
+        if (nnz > 0) {
+            k_edge_rows<<<tgrid, 256, 0, s>>>(n_core, (int64_t*)p->rowptr.p, erow);
+            GRAPPA_LAUNCHED(ctx);
+            GRAPPA_CUDA(cub::DeviceRadixSort::SortPairs(stmp, sort_bytes, (const int32_t*)p->col.p, skeys,
+                                                        (const int32_t*)erow, (int32_t*)p->t_col.p, (int)nnz, 0,
+                                                        end_bit, s));
+            ctx->launches++;
+        }
+        k_t_rowptr<<<(unsigned)std::min<int64_t>(ceil_div(nnz + 1, 256), 4096), 256, 0, s>>>(
+            n_local, nnz, skeys, (int64_t*)p->t_rowptr.p);
         GRAPPA_LAUNCHED(ctx);
+        k_row_deg<<<grid, 256, 0, s>>>(n_local, (int64_t*)p->t_rowptr.p, (int32_t*)p->t_deg.p);
+        GRAPPA_LAUNCHED(ctx);
+        RP_TRY(build_plan(ctx, s, n_local, (int64_t*)p->t_rowptr.p, (int32_t*)p->t_deg.p,
+                          PlanBufs{&p->t_heavy_rows, &p->t_heavy_slot_off, &p->t_slot_row, &p->t_slot_seg,
+                                   &p->t_row_order, &p->t_row_desc},
+                          d_stat + 3, &p->t_n_heavy, &p->t_n_slots));
     }
-    // SpMM row order: counting sort by descending min(d_l, kSegLen + 1)
-    {
-        RP_TRY(p->row_order.grow((size_t)n_core * 4));
-        RP_TRY(ctx->red_ws.grow((size_t)2 * kDegBuckets * 8));
-        unsigned long long* bins = (unsigned long long*)ctx->red_ws.p;
-        GRAPPA_CUDA(cudaMemsetAsync(bins, 0, (size_t)kDegBuckets * 8, s));
-        const unsigned g2 = (unsigned)std::min<int64_t>(ceil_div(n_core, 256), (int64_t)ctx->sm_count * 8);
-        k_deg_hist<<<g2, 256, 0, s>>>(n_core, (int32_t*)p->d_l.p, bins);
-        GRAPPA_LAUNCHED(ctx);
-        k_deg_bins_scan<<<1, 32, 0, s>>>(bins, bins + kDegBuckets);
-        GRAPPA_LAUNCHED(ctx);
-        const int64_t per = 4096;
-        k_deg_scatter<<<(unsigned)ceil_div(n_core, per), 256, 0, s>>>(n_core, per, (int32_t*)p->d_l.p,
-                                                                      bins + kDegBuckets, (int32_t*)p->row_order.p);
-        GRAPPA_LAUNCHED(ctx);
-        RP_TRY(p->row_desc.grow((size_t)n_core * 16));
-        k_row_desc<<<g2, 256, 0, s>>>(n_core, (int32_t*)p->row_order.p, (int64_t*)p->rowptr.p,
-                                      (int4*)p->row_desc.p);
-        GRAPPA_LAUNCHED(ctx);
-    }
+    GRAPPA_CUDA(cudaStreamSynchronize(s));
     // publish
     grappa_part_info& I = p->info;
-    I.n_core = n_core; I.nnz = nnz; I.n_seeds = n_seeds; I.base = base; I.swept = swept;
+    I.n_core = n_local; I.nnz = nnz; I.n_seeds = n_seeds; I.base = base; I.swept = swept;
+    I.n_halo = n_halo;
     I.feat_dim = feats ? feat_dim : 0; I.dtype = dtype;
     I.rowptr = (int64_t*)p->rowptr.p; I.col = (int32_t*)p->col.p;
     I.core_global = (int32_t*)p->core_global.p; I.d_l = (int32_t*)p->d_l.p; I.d_g = (int32_t*)p->d_g.p;
@@ -496,6 +665,8 @@ extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g
     I.node_w = (float*)p->node_w.p;
     I.seeds = (int32_t*)p->seeds.p; I.labels = (int32_t*)p->labels.p; I.x = p->x.p;
     I.n_heavy = n_heavy; I.n_slots = n_slots;
+    I.t_rowptr = halo ? (int64_t*)p->t_rowptr.p : nullptr;
+    I.t_col = halo ? (int32_t*)p->t_col.p : nullptr;
     I.c_uniform = hs.sum_r / (double)n_seeds;
     I.D = hs.D;
     const double D = (double)hs.D;
@@ -544,7 +715,9 @@ extern "C" void grappa_part_destroy(grappa_part* p) {
     for (grappa::DevBuf* b : {&p->rowptr, &p->col, &p->core_global, &p->d_l, &p->d_g, &p->norm_gcn,
                               &p->norm_sage, &p->node_w, &p->seeds, &p->labels, &p->x, &p->heavy_rows,
                               &p->heavy_slot_off, &p->slot_row, &p->slot_seg, &p->row_order,
-                              &p->row_desc})
+                              &p->row_desc, &p->t_rowptr, &p->t_col, &p->t_deg, &p->t_heavy_rows,
+                              &p->t_heavy_slot_off, &p->t_slot_row, &p->t_slot_seg, &p->t_row_order,
+                              &p->t_row_desc, &p->t_tmp})
         b->release();
     delete p;
 }

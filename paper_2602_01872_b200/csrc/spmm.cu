@@ -952,6 +952,25 @@ grappa_status spmm(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grappa_
     return spmm_csr(ctx, a, dt, s);
 }
 
+grappa_status spmm_t(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grappa_dtype dt,
+                     cudaStream_t s) {
+    if (!part->halo) return spmm(ctx, part, a, dt, s);     // induced-core: A^T = A
+    const grappa_part_info& I = part->info;
+    a.n = I.n_core;
+    a.nnz = I.nnz;
+    a.rowptr = (const int64_t*)part->t_rowptr.p;
+    a.col = (const int32_t*)part->t_col.p;
+    a.n_slots = part->t_n_slots;
+    a.n_heavy = part->t_n_heavy;
+    a.slot_row = (const int32_t*)part->t_slot_row.p;
+    a.slot_seg = (const int32_t*)part->t_slot_seg.p;
+    a.heavy_rows = (const int32_t*)part->t_heavy_rows.p;
+    a.heavy_slot_off = (const int32_t*)part->t_heavy_slot_off.p;
+    a.row_order = g_spmm_variant == 3 ? nullptr : (const int32_t*)part->t_row_order.p;
+    a.row_desc = g_spmm_variant == 3 ? nullptr : (const int4*)part->t_row_desc.p;
+    return spmm_csr(ctx, a, dt, s);
+}
+
 grappa_status spmm_csr(grappa_ctx* ctx, SpmmArgs a, grappa_dtype dt, cudaStream_t s) {
     if (a.width % 8 != 0) {
         set_error("spmm: width %d not a multiple of 8", a.width);

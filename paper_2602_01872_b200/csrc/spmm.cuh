@@ -63,6 +63,10 @@ void spmm_set_wide(int v);
 
 grappa_status spmm(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grappa_dtype dt,
                    cudaStream_t s);
+// the transpose operator A_loc^T (backward aggregations): A_loc itself for induced-core
+// partitions (symmetric), the stored transpose for halo-1 partitions
+grappa_status spmm_t(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grappa_dtype dt,
+                     cudaStream_t s);
 // same kernel on an explicit CSR (a.n rows, a.nnz, a.rowptr, a.col, optional split rows);
 // used for the rectangular mini-batch blocks and their transposes
 grappa_status spmm_csr(grappa_ctx* ctx, SpmmArgs a, grappa_dtype dt, cudaStream_t s);

@@ -86,7 +86,7 @@ class Trainer:
     def __init__(self, ctx: Context, rowptr, col, x, labels, train_mask, spec: ModelSpec, weights,
                  num_chunks: int, chunk_seed: int, corr: str = "resampling", lr: float = 0.003,
                  repartition_every: int = 10, dtype: str = "f32", num_workers: int | None = None,
-                 stream=None, controller=None):
+                 stream=None, controller=None, halo: bool = False):
         self.ctx = ctx
         self.dev = torch.device("cuda", ctx.device)
         self.stream = stream or torch.cuda.current_stream(self.dev)
@@ -101,6 +101,7 @@ class Trainer:
         # optional §3.5 controller (paper_2602_01872_b200.controller.Controller): decides the
         # super-epoch switches instead of the fixed `repartition_every`
         self.controller = controller
+        self.halo = halo                 # halo-1 partitions (R33) instead of induced-core
         self.t_ctrl = 1
         self._steps = []
         self.dt = BF16 if dtype == "bf16" else F32
@@ -152,7 +153,7 @@ class Trainer:
             b, s = pairs[w]
             self.parts[w] = grappa_repartition(self.ctx, self.rowptr, self.col, self.x, self.dt,
                                                self.chunk_of, self.C, b, s, self.train, self.labels,
-                                               self.parts.get(w), self.stream)
+                                               self.parts.get(w), self.stream, halo=self.halo)
         self.t = t
         self._alloc()
 
