@@ -192,6 +192,24 @@ grappa_status grappa_part_download(const grappa_part* part, const grappa_part_ho
  * metadata derived at repartition time (split rows, degree-bucketed row order) is kept. */
 grappa_status grappa_part_upload(grappa_part* part, const grappa_part_host* src, void* stream);
 
+/* Partition images: the whole partition (arrays, SpMM plans, transpose) serialised into ONE
+ * host buffer, for phase-parallel capacity mode -- partitions parked in host memory and streamed
+ * to a GPU slot per phase (Alg. 1 with M < P; "trades training time for memory
+ * capacity" P:395; partitions in CPU memory, loaded to the GPU).
+ *   grappa_part_image_bytes  size of the image of `part` (0 if part is NULL)
+ *   grappa_part_save         enqueue D2H copies of every array into host (pinned for overlap)
+ *                            and write the header at once; the image is complete when the
+ *                            stream reaches this point.  E_ARG if host_bytes is too small.
+ *   grappa_part_image_info   the image's grappa_part_info (pointers NULL), read on the host
+ *   grappa_part_load         (re)allocate *inout's buffers (growing only) and enqueue H2D copies
+ *                            of an image; *inout NULL -> a new part.  No host sync: the header is
+ *                            read from host memory.  The image must stay valid until the copies
+ *                            are done (stream order).  E_ARG if host is not an image. */
+size_t grappa_part_image_bytes(const grappa_part* part);
+grappa_status grappa_part_save(const grappa_part* part, void* host, size_t host_bytes, void* stream);
+grappa_status grappa_part_image_info(const void* host, grappa_part_info* out);
+grappa_status grappa_part_load(grappa_part** inout, const void* host, void* stream);
+
 /* Workspace sizes (bytes) for one layer call on `part`; `saved` persists fwd -> bwd. */
 size_t grappa_layer_saved_bytes(const grappa_part* part, grappa_arch arch, int32_t f_in,
                                 int32_t f_out, grappa_dtype dtype);

@@ -157,6 +157,28 @@ class Part:
         _lib.check("grappa_part_upload", load().grappa_part_upload(self.h, ctypes.byref(st),
                                                                    _lib.stream_ptr(stream)))
 
+    # ---------------------------------------------------------- images (capacity mode)
+    def image_bytes(self) -> int:
+        return int(load().grappa_part_image_bytes(self.h))
+
+    def save(self, host: torch.Tensor, stream=None):
+        """enqueue D2H of the whole partition into `host` (a pinned uint8 tensor)"""
+        _lib.check("grappa_part_save", load().grappa_part_save(
+            self.h, ctypes.c_void_p(host.data_ptr()), host.numel(), _lib.stream_ptr(stream)))
+
+    def load_image(self, host: torch.Tensor, stream=None):
+        """enqueue H2D of an image into this part's buffers (no host sync)"""
+        _lib.check("grappa_part_load", load().grappa_part_load(
+            ctypes.byref(self.h), ctypes.c_void_p(host.data_ptr()), _lib.stream_ptr(stream)))
+        return self.refresh()
+
+    @staticmethod
+    def image_info(host: torch.Tensor):
+        info = _lib.PartInfo()
+        _lib.check("grappa_part_image_info", load().grappa_part_image_info(
+            ctypes.c_void_p(host.data_ptr()), ctypes.byref(info)))
+        return info
+
     def factor(self, corr: str) -> float:
         I = self.info
         return {"none": 1.0, "uniform": I.c_uniform, "resampling": I.c_resampling,

@@ -32,7 +32,8 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_minibatch_ws_bytes", "grappa_minibatch_step", "grappa_part_download",
            "grappa_part_upload", "grappa_layer_bwd_ex", "grappa_layer_fwd_ex",
            "grappa_minibatch_step_ex", "grappa_sample_async", "grappa_sample_wait",
-           "grappa_sample_event", "grappa_repartition_ex"]
+           "grappa_sample_event", "grappa_repartition_ex", "grappa_part_image_bytes",
+           "grappa_part_save", "grappa_part_image_info", "grappa_part_load"]
 KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5, "sample": 6}
 
 
@@ -102,6 +103,10 @@ def load(path: str = LIB_PATH):
         "grappa_repartition_ex": (st, [vp, ctypes.POINTER(Csr), vp, i32, ctypes.c_int, vp, i32, i32,
                                        i32, vp, vp, ctypes.c_uint, ctypes.POINTER(vp), vp]),
         "grappa_part_query": (st, [vp, ctypes.POINTER(PartInfo)]),
+        "grappa_part_image_bytes": (sz, [vp]),
+        "grappa_part_save": (st, [vp, vp, sz, vp]),
+        "grappa_part_image_info": (st, [vp, ctypes.POINTER(PartInfo)]),
+        "grappa_part_load": (st, [ctypes.POINTER(vp), vp, vp]),
         "grappa_part_destroy": (None, [vp]),
         "grappa_layer_saved_bytes": (sz, [vp, ctypes.c_int, i32, i32, ctypes.c_int]),
         "grappa_layer_ws_bytes": (sz, [vp, ctypes.c_int, i32, i32, ctypes.c_int]),

@@ -22,6 +22,7 @@
 #include "scan.cuh"
 
 #include <cmath>
+#include <cstring>
 
 namespace grappa {
 
@@ -720,4 +721,120 @@ extern "C" void grappa_part_destroy(grappa_part* p) {
                               &p->t_row_desc, &p->t_tmp})
         b->release();
     delete p;
+}
+
+// ------------------------------------------------------------------ partition images
+// A partition serialised into one host buffer (capacity mode: partitions parked in host memory
+// between phases and streamed to the GPU per phase).  Layout: header, then
+// every array at a 256-byte aligned offset, in the fixed order of part_arrays().
+namespace {
+constexpr uint64_t kImageMagic = 0x4752415050414931ull;   // "GRAPPAI1"
+constexpr int kImageArrays = 26;
+struct ImageHeader {
+    uint64_t magic;
+    grappa_part_info info;      // pointers are meaningless in the image
+    int32_t halo;
+    int64_t n_halo, t_n_heavy, t_n_slots;
+    uint64_t off[kImageArrays], bytes[kImageArrays];
+};
+struct ArrRef { grappa::DevBuf* buf; size_t bytes; };
+
+// (buffer, bytes) of every array of a partition with the given counts
+static int part_arrays(grappa_part* p, const grappa_part_info& I, bool halo, int64_t t_n_heavy,
+                       int64_t t_n_slots, ArrRef* out) {
+    const size_t n = (size_t)I.n_core, nnz = (size_t)I.nnz, es = I.dtype == GRAPPA_BF16 ? 2 : 4;
+    const size_t nh = (size_t)I.n_heavy, ns = (size_t)I.n_slots;
+    int k = 0;
+    auto add = [&](grappa::DevBuf& b, size_t bytes) { out[k++] = ArrRef{&b, bytes}; };
+    add(p->rowptr, (n + 1) * 8); add(p->col, nnz * 4); add(p->core_global, n * 4); add(p->d_l, n * 4);
+    add(p->d_g, n * 4); add(p->norm_gcn, n * 4); add(p->norm_sage, n * 4); add(p->node_w, n * 12);
+    add(p->seeds, (size_t)I.n_seeds * 4); add(p->labels, n * 4); add(p->x, n * (size_t)I.feat_dim * es);
+    add(p->heavy_rows, nh * 4); add(p->heavy_slot_off, (nh + 1) * 4); add(p->slot_row, ns * 4);
+    add(p->slot_seg, ns * 4); add(p->row_order, n * 4); add(p->row_desc, n * 16);
+    const size_t th = halo ? (size_t)t_n_heavy : 0, ts = halo ? (size_t)t_n_slots : 0;
+    add(p->t_rowptr, halo ? (n + 1) * 8 : 0); add(p->t_col, halo ? nnz * 4 : 0); add(p->t_deg, halo ? n * 4 : 0);
+    add(p->t_heavy_rows, th * 4); add(p->t_heavy_slot_off, halo ? (th + 1) * 4 : 0);
+    add(p->t_slot_row, ts * 4); add(p->t_slot_seg, ts * 4); add(p->t_row_order, halo ? n * 4 : 0);
+    add(p->t_row_desc, halo ? n * 16 : 0);
+    return k;
+}
+static size_t al256(size_t b) { return (b + 255) / 256 * 256; }
+}  // namespace
+
+extern "C" size_t grappa_part_image_bytes(const grappa_part* part) {
+    if (!part) return 0;
+    grappa_part* p = const_cast<grappa_part*>(part);
+    ArrRef a[kImageArrays];
+    const int k = part_arrays(p, p->info, p->halo, p->t_n_heavy, p->t_n_slots, a);
+    size_t off = al256(sizeof(ImageHeader));
+    for (int i = 0; i < k; i++) off += al256(a[i].bytes);
+    return off;
+}
+
+extern "C" grappa_status grappa_part_save(const grappa_part* part, void* host, size_t host_bytes, void* stream) {
+    GRAPPA_ARG(part && host, GRAPPA_E_ARG, "grappa_part_save: null argument");
+    const size_t need = grappa_part_image_bytes(part);
+    GRAPPA_ARG(host_bytes >= need, GRAPPA_E_ARG, "grappa_part_save: %zu B < %zu B needed", host_bytes, need);
+    grappa_part* p = const_cast<grappa_part*>(part);
+    ArrRef a[kImageArrays];
+    const int k = part_arrays(p, p->info, p->halo, p->t_n_heavy, p->t_n_slots, a);
+    ImageHeader h{};
+    h.magic = kImageMagic;
+    h.info = p->info;
+    h.halo = p->halo;
+    h.n_halo = p->n_halo; h.t_n_heavy = p->t_n_heavy; h.t_n_slots = p->t_n_slots;
+    size_t off = al256(sizeof(ImageHeader));
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int i = 0; i < k; i++) {
+        h.off[i] = off; h.bytes[i] = a[i].bytes;
+        if (a[i].bytes)
+            GRAPPA_CUDA(cudaMemcpyAsync((char*)host + off, a[i].buf->p, a[i].bytes, cudaMemcpyDeviceToHost, s));
+        off += al256(a[i].bytes);
+    }
+    memcpy(host, &h, sizeof(h));
+    return GRAPPA_OK;
+}
+
+extern "C" grappa_status grappa_part_image_info(const void* host, grappa_part_info* out) {
+    GRAPPA_ARG(host && out, GRAPPA_E_ARG, "grappa_part_image_info: null argument");
+    ImageHeader h;
+    memcpy(&h, host, sizeof(h));
+    GRAPPA_ARG(h.magic == kImageMagic, GRAPPA_E_ARG, "grappa_part_image_info: not a partition image");
+    *out = h.info;
+    out->rowptr = nullptr; out->col = nullptr; out->core_global = nullptr; out->d_l = nullptr;
+    out->d_g = nullptr; out->norm_gcn = nullptr; out->norm_sage = nullptr; out->seeds = nullptr;
+    out->labels = nullptr; out->x = nullptr; out->node_w = nullptr; out->t_rowptr = nullptr; out->t_col = nullptr;
+    return GRAPPA_OK;
+}
+
+extern "C" grappa_status grappa_part_load(grappa_part** inout, const void* host, void* stream) {
+    GRAPPA_ARG(inout && host, GRAPPA_E_ARG, "grappa_part_load: null argument");
+    ImageHeader h;
+    memcpy(&h, host, sizeof(h));
+    GRAPPA_ARG(h.magic == kImageMagic, GRAPPA_E_ARG, "grappa_part_load: not a partition image");
+    grappa_part* p = *inout ? *inout : new grappa_part();
+    ArrRef a[kImageArrays];
+    const int k = part_arrays(p, h.info, h.halo != 0, h.t_n_heavy, h.t_n_slots, a);
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int i = 0; i < k; i++) {
+        if (!a[i].bytes) continue;
+        grappa_status st = a[i].buf->grow(a[i].bytes);
+        if (st != GRAPPA_OK) {
+            if (!*inout) grappa_part_destroy(p);
+            return st;
+        }
+        GRAPPA_CUDA(cudaMemcpyAsync(a[i].buf->p, (const char*)host + h.off[i], a[i].bytes, cudaMemcpyHostToDevice, s));
+    }
+    p->halo = h.halo != 0;
+    p->n_halo = h.n_halo; p->t_n_heavy = h.t_n_heavy; p->t_n_slots = h.t_n_slots;
+    grappa_part_info& I = p->info;
+    I = h.info;
+    I.rowptr = (int64_t*)p->rowptr.p; I.col = (int32_t*)p->col.p;
+    I.core_global = (int32_t*)p->core_global.p; I.d_l = (int32_t*)p->d_l.p; I.d_g = (int32_t*)p->d_g.p;
+    I.norm_gcn = (float*)p->norm_gcn.p; I.norm_sage = (float*)p->norm_sage.p; I.node_w = (float*)p->node_w.p;
+    I.seeds = (int32_t*)p->seeds.p; I.labels = (int32_t*)p->labels.p; I.x = p->x.p;
+    I.t_rowptr = p->halo ? (int64_t*)p->t_rowptr.p : nullptr;
+    I.t_col = p->halo ? (int32_t*)p->t_col.p : nullptr;
+    *inout = p;
+    return GRAPPA_OK;
 }

@@ -48,6 +48,13 @@ __device__ __forceinline__ bool key_lt(uint64_t ak, int32_t ag, uint64_t bk, int
     return ak < bk || (ak == bk && ag < bg);
 }
 
+// keys of uniform 64-bit hashes below T = min(1, frac) 2^64 with frac = 6f/d: the f smallest
+// of d keys lie below it except with small probability (count ~ Binomial(d, 6f/d))
+__host__ __device__ __forceinline__ uint64_t hub_threshold(int f, int64_t d) {
+    const double frac = 6.0 * f / (double)d;
+    return frac >= 1.0 ? ~0ull : (uint64_t)(frac * 18446744073709551616.0);
+}
+
 // targets with more local neighbours than this go to the block-per-target threshold kernel
 constexpr int kHeavyPick = 1024;
 constexpr int kCandCap = 1024;
@@ -73,25 +80,45 @@ __global__ void k_pick(const int64_t* __restrict__ d_nt, const int32_t* __restri
             if (lane == 0) heavy_q[atomicAdd(heavy_n, 1)] = t;
             continue;
         }
-        // per-lane sorted list of its f smallest keys (f <= 16), unrolled insertion
+        // per-lane sorted list of its f smallest keys (f <= 16), unrolled insertion.  Only keys
+        // below T = min(1, 8f/d) 2^64 are inserted (expected 8f of them, so the insertion chain
+        // runs ~8f/32 times per lane instead of d/32); the warp's f smallest keys are all below T
+        // whenever at least f keys are, which the ballot count checks -- otherwise the row is
+        // redone with T = 2^64 (exact either way).
         uint64_t lk[kMaxFanout];
         int32_t lg[kMaxFanout], lu[kMaxFanout];
+        const uint64_t gv = (uint64_t)gid[v];
+        uint64_t T = hub_threshold(f + f / 3, d);              // ~8f/d (6f/d at 4f/3)
+        for (int pass = 0; pass < 2; pass++) {
 #pragma unroll
-        for (int j = 0; j < kMaxFanout; j++) { lk[j] = ~0ull; lg[j] = 0x7fffffff; lu[j] = -1; }
-        for (int i = lane; i < d; i += 32) {
-            const int32_t u = col[e0 + i];
-            const int32_t gu = gid[u];
-            // h(h(seed, epoch, batch, hop), gid(v), gid(u)) = mix(key0 ^ mix(gid(v) ^ mix(gid(u))))
-            uint64_t k = smix(key0 ^ smix((uint64_t)gid[v] ^ smix((uint64_t)gu)));
-            int32_t g = gu, uu = u;
+            for (int j = 0; j < kMaxFanout; j++) { lk[j] = ~0ull; lg[j] = 0x7fffffff; lu[j] = -1; }
+            int below = 0;
+            for (int i0 = 0; i0 < d; i0 += 32) {
+                const int i = i0 + lane;
+                bool take = false;
+                uint64_t k = 0;
+                int32_t g = 0, uu = 0;
+                if (i < d) {
+                    uu = col[e0 + i];
+                    g = gid[uu];
+                    // h(h(seed, epoch, batch, hop), gid(v), gid(u)) = mix(key0 ^ mix(gid(v) ^ mix(gid(u))))
+                    k = smix(key0 ^ smix(gv ^ smix((uint64_t)g)));
+                    take = k < T;
+                }
+                below += __popc(__ballot_sync(0xffffffffu, take));
+                if (take) {
 #pragma unroll
-            for (int j = 0; j < kMaxFanout; j++) {       // bubble the new key into place
-                if (j < f && key_lt(k, g, lk[j], lg[j])) {
-                    uint64_t tk = lk[j]; int32_t tg = lg[j], tu = lu[j];
-                    lk[j] = k; lg[j] = g; lu[j] = uu;
-                    k = tk; g = tg; uu = tu;
+                    for (int j = 0; j < kMaxFanout; j++) {   // bubble the new key into place
+                        if (j < f && key_lt(k, g, lk[j], lg[j])) {
+                            uint64_t tk = lk[j]; int32_t tg = lg[j], tu = lu[j];
+                            lk[j] = k; lg[j] = g; lu[j] = uu;
+                            k = tk; g = tg; uu = tu;
+                        }
+                    }
                 }
             }
+            if (below >= f || T == ~0ull) break;
+            T = ~0ull;                                         // too few below T: exact redo
         }
         // f rounds of warp arg-min over the lanes' list heads
         int head = 0;
@@ -209,10 +236,6 @@ __global__ void __launch_bounds__(256) k_pick_heavy(const int32_t* __restrict__ 
 // redone exactly by k_pick_heavy (flag in cand_n).
 constexpr int kCand = 512;
 constexpr int kHubSeg = 2048;
-__host__ __device__ __forceinline__ uint64_t hub_threshold(int f, int64_t d) {
-    const double frac = 6.0 * f / (double)d;
-    return frac >= 1.0 ? ~0ull : (uint64_t)(frac * 18446744073709551616.0);
-}
 struct HubSegs {
     const int32_t* heavy_n; const int64_t* heavy_q; const int32_t* targets; const int64_t* rowptr;
     __device__ int32_t operator()(int64_t q) const {

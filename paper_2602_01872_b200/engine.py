@@ -86,7 +86,7 @@ class Trainer:
     def __init__(self, ctx: Context, rowptr, col, x, labels, train_mask, spec: ModelSpec, weights,
                  num_chunks: int, chunk_seed: int, corr: str = "resampling", lr: float = 0.003,
                  repartition_every: int = 10, dtype: str = "f32", num_workers: int | None = None,
-                 stream=None, controller=None, halo: bool = False):
+                 stream=None, controller=None, halo: bool = False, capacity: bool = False):
         self.ctx = ctx
         self.dev = torch.device("cuda", ctx.device)
         self.stream = stream or torch.cuda.current_stream(self.dev)
@@ -102,6 +102,11 @@ class Trainer:
         # super-epoch switches instead of the fixed `repartition_every`
         self.controller = controller
         self.halo = halo                 # halo-1 partitions (R33) instead of induced-core
+        # capacity mode (Alg. 1 with M < P beyond HBM): partitions live as images in
+        # pinned host memory and are streamed into one of two device slots per phase
+        self.capacity = capacity
+        self.host_imgs: dict = {}
+        self.cap_slots = None
         self.t_ctrl = 1
         self._steps = []
         self.dt = BF16 if dtype == "bf16" else F32
@@ -147,6 +152,8 @@ class Trainer:
     def repartition(self, t: int):
         """a3 for super-epoch t on every worker this rank owns."""
         pairs = self.schedule[(t - 1) % len(self.schedule)]
+        if self.capacity:
+            return self._repartition_to_host(t, pairs)
         for _, w in self.my_workers():
             if w >= self.W:
                 continue
@@ -157,11 +164,46 @@ class Trainer:
         self.t = t
         self._alloc()
 
-    def _alloc(self):
-        """Activation / workspace buffers sized for the largest partition this rank owns;
-        kept across super-epochs (12.5 % headroom) so a switch does not reallocate."""
+    def _repartition_to_host(self, t, pairs):
+        """capacity mode: extract each partition into device slot 0, save its image to pinned
+        host memory (grappa_part_save), keep only the images"""
+        if self.cap_slots is None:
+            self.cap_slots = [Part(), Part()]
+            self.cap_stream = torch.cuda.Stream(self.dev)
+        self.parts = {}
+        sizes = []
+        for _, w in self.my_workers():
+            if w >= self.W:
+                continue
+            b, s = pairs[w]
+            p = grappa_repartition(self.ctx, self.rowptr, self.col, self.x, self.dt, self.chunk_of, self.C,
+                                   b, s, self.train, self.labels, self.cap_slots[0], self.stream,
+                                   halo=self.halo)
+            nb = p.image_bytes()
+            host = self.host_imgs.get(w)
+            if host is None or host.numel() < nb:
+                host = torch.empty(nb + nb // 8, dtype=torch.uint8, pin_memory=True)
+                self.host_imgs[w] = host
+            p.save(host, self.stream)
+            sizes.append(self._sizes(p))
+            self.stream.synchronize()              # the image is complete before slot 0 is reused
+        self.t = t
+        self._alloc(sizes)
+
+    def _sizes(self, p):
         sp = self.spec
-        n_max = max(p.n_core for p in self.parts.values()) if self.parts else 1
+        ws = [layer_ws_bytes(p, sp.arch, sp.dims_pad[l], sp.dims_pad[l + 1], self.dt) for l in range(sp.depth)]
+        sv = [layer_saved_bytes(p, sp.arch, sp.dims_pad[l], sp.dims_pad[l + 1], self.dt) for l in range(sp.depth)]
+        return p.n_core, ws, sv
+
+    def _alloc(self, sizes=None):
+        """Activation / workspace buffers sized for the largest partition this rank owns;
+        kept across super-epochs (12.5 % headroom) so a switch does not reallocate.
+        sizes: [(n_core, ws per layer, saved per layer)] (default: from the resident parts)."""
+        sp = self.spec
+        if sizes is None:
+            sizes = [self._sizes(p) for p in self.parts.values()]
+        n_max = max([1] + [z[0] for z in sizes])
         if getattr(self, "_n_cap", 0) < n_max:
             self._n_cap = n_cap = n_max + n_max // 8
             self.H = [None] + [torch.empty(n_cap, sp.dims_pad[l], dtype=self.tdt, device=self.dev)
@@ -171,9 +213,8 @@ class Trainer:
         ws = 1
         saved = []
         for l in range(sp.depth):
-            fi, fo = sp.dims_pad[l], sp.dims_pad[l + 1]
-            ws = max([ws] + [layer_ws_bytes(p, sp.arch, fi, fo, self.dt) for p in self.parts.values()])
-            sb = max([0] + [layer_saved_bytes(p, sp.arch, fi, fo, self.dt) for p in self.parts.values()])
+            ws = max([ws] + [z[1][l] for z in sizes])
+            sb = max([0] + [z[2][l] for z in sizes])
             old = self.saved[l] if getattr(self, "saved", None) else None
             if sb and (old is None or old.numel() < sb):
                 old = torch.empty(sb + sb // 8, dtype=torch.uint8, device=self.dev)
@@ -251,11 +292,48 @@ class Trainer:
         t = self.super_epoch()
         if t != self.t:
             self.repartition(t)
+        if self.capacity:
+            return self._run_epoch_capacity(on_phase)
         for i, w in self.my_workers():
             m_active = min(self.G, self.W - i * self.G)
             self.phase_step(i, w, m_active)
             if on_phase is not None:
                 on_phase()
+        self.end_epoch()
+
+    def _run_epoch_capacity(self, on_phase=None):
+        """capacity mode: phase k's partition image is copied H2D into slot k % 2 on a copy
+        stream while phase k-1 computes on the other slot (grappa_part_load)"""
+        plan = self.my_workers()
+        free = [None, None]                       # compute done with the slot's previous image
+
+        def load(k):
+            _, w = plan[k]
+            if w >= self.W:
+                return None
+            if free[k % 2] is not None:
+                self.cap_stream.wait_event(free[k % 2])
+            self.cap_slots[k % 2].load_image(self.host_imgs[w], self.cap_stream)
+            ev = torch.cuda.Event()
+            ev.record(self.cap_stream)
+            return ev
+
+        self.cap_stream.wait_stream(self.stream)  # e.g. the repartition's use of slot 0
+        ready = load(0) if plan else None
+        for k, (i, w) in enumerate(plan):
+            nxt = load(k + 1) if k + 1 < len(plan) else None
+            if ready is not None:
+                self.stream.wait_event(ready)
+                self.parts = {w: self.cap_slots[k % 2]}
+            else:
+                self.parts = {}
+            m_active = min(self.G, self.W - i * self.G)
+            self.phase_step(i, w, m_active)
+            free[k % 2] = torch.cuda.Event()
+            free[k % 2].record(self.stream)
+            if on_phase is not None:
+                on_phase()
+            ready = nxt
         self.end_epoch()
 
     def run_epoch_graph(self):
@@ -302,8 +380,11 @@ class MinibatchTrainer(Trainer):
     (grappa_minibatch_step), scales by the batch's coverage factor and all-reduces
     (grappa_aggregate_grads_c) before the SGD step (Alg. 1)."""
 
-    def __init__(self, *args, fanouts=(15, 10, 5), batch_size=1000, sample_seed=0, **kw):
+    def __init__(self, *args, fanouts=(15, 10, 5), batch_size=1000, sample_seed=0, depth: int = 2, **kw):
         super().__init__(*args, **kw)
+        if self.capacity:
+            raise ValueError("capacity mode is implemented for full-graph training")
+        self.depth = max(1, depth)         # batches sampled ahead (side streams)
         if self.spec.arch != "sage":
             raise ValueError("mini-batch mode is implemented for GraphSAGE (config 4)")
         self.fanouts = list(fanouts)
@@ -345,48 +426,54 @@ class MinibatchTrainer(Trainer):
                               self.theta, self.grad, self.mb_ws, self.loss_dev, self.dt,
                               stream=self.stream, flags=LAYER_NODE_LEVEL if self.corr == "node" else 0)
 
-    def _sample_async(self, part, order, it: int, nb: int, slot: int):
+    def _sample_async(self, part, order, it: int, nb: int):
         from . import Batch, grappa_sample_async
         b = it % nb
+        slot = it % len(self.slots)
         seeds = order[b * self.B: min((b + 1) * self.B, order.numel())]
         self.slots[slot] = grappa_sample_async(self.ctx, part, seeds, self.fanouts, self.sample_seed,
-                                               self.epoch, b, self.slots[slot] or Batch(), self.sstream)
+                                               self.epoch, b, self.slots[slot] or Batch(),
+                                               self.sstreams[it % self.depth])
 
     def run_epoch(self, on_phase=None):
-        """Alg. 1 in mini-batch mode.  Sampling runs one batch ahead on a side stream into the
-        other of two batch slots (grappa_sample_async), so the sampler kernels of batch i+1
-        overlap the SAGE step of batch i; the host waits only for batch i's block sizes
+        """Alg. 1 in mini-batch mode.  Sampling runs `depth` batches ahead on `depth` side streams
+        (grappa_sample_async into depth + 1 batch slots), so the samplers of batches i+1 .. i+depth
+        run concurrently with each other and with the SAGE step of batch i (the sampler is a chain
+        of small latency-bound kernels); the host waits only for batch i's block sizes
         (grappa_sample_wait) before launching its step."""
         from . import grappa_aggregate_grads_c, grappa_epoch_seeds, grappa_sample_wait
         t = self.super_epoch()
         if t != self.t:
             self.repartition(t)
-        if getattr(self, "sstream", None) is None:
-            self.sstream = torch.cuda.Stream(self.dev)
-            self.slots = [None, None]
+        D = self.depth
+        if getattr(self, "sstreams", None) is None:
+            self.sstreams = [torch.cuda.Stream(self.dev) for _ in range(D)]
+            self.slots = [None] * (D + 1)
+        S = len(self.slots)
         for i, w, m_active in phase_plan(self.W, self.G, self.rank):
             part = self.parts.get(w) if w is not None else None
             nb = self.iterations(part)
             iters = self.phase_iterations(part)
-            done = [None, None]
+            done = [None] * S
             if part is not None:
                 if self.order is None or self.order.numel() < part.n_seeds:
                     self.order = torch.empty(part.n_seeds, dtype=torch.int32, device=self.dev)
                 order = self.order[:part.n_seeds]
                 grappa_epoch_seeds(self.ctx, part, self.sample_seed, self.epoch, order, self.stream)
-                if iters:
-                    ev = torch.cuda.Event()
-                    ev.record(self.stream)               # seeds (and every earlier step) first
-                    self.sstream.wait_event(ev)
-                    self._sample_async(part, order, 0, nb, 0)
+                ev = torch.cuda.Event()
+                ev.record(self.stream)                   # seeds (and every earlier step) first
+                for k in range(min(D, iters)):
+                    self.sstreams[k % D].wait_event(ev)
+                    self._sample_async(part, order, k, nb)
             for it in range(iters):
-                slot = it & 1
+                slot = it % S
                 if part is not None:
                     bt = grappa_sample_wait(self.slots[slot], views=False)
-                    if it + 1 < iters:
-                        if done[slot ^ 1] is not None:  # the other slot's blocks are consumed
-                            self.sstream.wait_event(done[slot ^ 1])
-                        self._sample_async(part, order, it + 1, nb, slot ^ 1)
+                    nxt = it + D
+                    if nxt < iters:
+                        if done[nxt % S] is not None:    # that slot's previous blocks are consumed
+                            self.sstreams[nxt % D].wait_event(done[nxt % S])
+                        self._sample_async(part, order, nxt, nb)
                     self.batch = bt
                     self._step(part, bt)                 # waits on bt's sample event itself
                     done[slot] = torch.cuda.Event()

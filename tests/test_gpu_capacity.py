@@ -1,0 +1,74 @@
+"""Capacity mode (Alg. 1 with partitions streamed from host memory, P:395,
+P:139): partition images round-trip bit-exactly (grappa_part_save / grappa_part_load),
+and an epoch that streams every phase's partition from pinned host memory into two device slots
+reproduces the resident-partition epoch bit for bit (same kernels, same inputs, same order)."""
+import pytest
+import torch
+
+import gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    import paper_2602_01872_b200 as G
+    G.load()
+    return G
+
+
+@pytest.fixture(scope="module")
+def prod():
+    wl = gen.small_workload("products", n=20011, scale=15, num_samples=540_000, depth=3)
+    return gen.make_dataset(wl)
+
+
+@pytest.mark.parametrize("halo", [False, True])
+def test_image_roundtrip(G, prod, halo):
+    ctx = G.Context(0)
+    ds = prod
+    d = "cuda"
+    rp, col = torch.from_numpy(ds.rowptr).to(d), torch.from_numpy(ds.col).to(d)
+    ch = torch.empty(ds.wl.n, dtype=torch.int32, device=d)
+    G.grappa_partition(ctx, ds.wl.n, 8, gen.seed_of("chunks"), ch)
+    p = G.grappa_repartition(ctx, rp, col, torch.from_numpy(ds.x).to(d).to(torch.bfloat16), "bf16", ch, 8, 1, 6,
+                             torch.from_numpy(ds.train).to(d), torch.from_numpy(ds.y).to(d), halo=halo)
+    host = torch.empty(p.image_bytes(), dtype=torch.uint8, pin_memory=True)
+    p.save(host)
+    torch.cuda.synchronize()
+    info = G.Part.image_info(host)
+    assert info.n_core == p.n_core and info.nnz == p.nnz and info.n_halo == p.n_halo
+    q = G.Part().load_image(host)
+    torch.cuda.synchronize()
+    for k in ("rowptr", "col", "core_global", "d_l", "d_g", "norm_gcn", "norm_sage", "seeds", "labels",
+              "node_w"):
+        assert torch.equal(getattr(p, k), getattr(q, k)), k
+    assert torch.equal(p.x.view(torch.int16), q.x.view(torch.int16))
+    if halo:
+        assert torch.equal(p.t_rowptr, q.t_rowptr) and torch.equal(p.t_col, q.t_col)
+    assert q.info.c_resampling == p.info.c_resampling and q.info.n_slots == p.info.n_slots
+    with pytest.raises(G.GrappaError, match="E_ARG"):
+        G.Part().load_image(torch.zeros(4096, dtype=torch.uint8, pin_memory=True))
+    ctx.close()
+
+
+@pytest.mark.parametrize("halo,dtype", [(False, "bf16"), (True, "f32")])
+def test_capacity_epoch_equals_resident(G, prod, halo, dtype):
+    from paper_2602_01872_b200.engine import ModelSpec, Trainer
+    ctx = G.Context(0)
+    ds = prod
+    wl = ds.wl
+    spec = ModelSpec(wl.arch, wl.dims, wl.dims_pad)
+    mk = lambda cap: Trainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights, wl.chunks,
+                             gen.seed_of("chunks"), corr="uniform", lr=0.05, repartition_every=1,
+                             dtype=dtype, halo=halo, capacity=cap)
+    a, b = mk(False), mk(True)
+    for _ in range(2):                       # two super-epochs (repartition every epoch)
+        a.run_epoch()
+        b.run_epoch()
+    torch.cuda.synchronize()
+    ctx.check()
+    assert not b.parts or len(b.parts) == 1
+    assert torch.equal(a.theta, b.theta)
+    assert not torch.equal(a.theta, mk(False).theta)       # the epochs did move theta
+    ctx.close()
