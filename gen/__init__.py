@@ -181,7 +181,7 @@ class Workload:
     n: int
     F: int
     K: int
-    arch: str                    # "gcn" | "sage"
+    arch: str                    # "gcn" | "sage" | "gat"
     depth: int
     hidden: int = 128
     train_frac: float = 0.1
@@ -287,6 +287,10 @@ def init_weights(wl: Workload, seed: int) -> list:
     dims, dp = wl.dims, wl.dims_pad
     out = []
     for l in range(wl.depth):
+        if wl.arch == "gat":     # [W, [a_src; a_dst]] (2 x f_out attention vectors, glorot)
+            out.append([glorot(dims[l], dims[l + 1], dp[l], dp[l + 1], seed, l, 0),
+                        glorot(2, dims[l + 1], 2, dp[l + 1], seed, l, 1)])
+            continue
         mats = 1 if wl.arch == "gcn" else 2
         out.append([glorot(dims[l], dims[l + 1], dp[l], dp[l + 1], seed, l, m)
                     for m in range(mats)])

@@ -10,6 +10,11 @@ GCN layer ("averages neighbors with degree-based weights"; readings
 SAGE layer ("aggregated (for example, by averaging) ... combined and multiplied by a
 matrix"; reading R6):
     M = D_l^-1 A H  (row of zeros where d_l = 0),  Z = H W_self + M W_nbr
+GAT layer ("assigns weights to different neighborhood nodes using attention ... modified
+by a matrix (a linear layer) ... averaging its neighbors' hidden states using learned weights";
+reading R35: one head, self loop, LeakyReLU 0.2, no bias):
+    z = H W,  alpha_vu = softmax_{u in N(v)+v} LeakyReLU(z_u a_src + z_v a_dst),  Z = alpha z
+    parameters per layer [W, [a_src; a_dst]]
 Activation: ReLU on hidden layers, identity on the output layer; ReLU'(0) = 0 (R16).
 No biases (R7).  Loss: mean softmax cross-entropy over the partition's seeds with a
 max-subtracted log-sum-exp (R8).  Backward: exact reverse mode.
@@ -58,8 +63,16 @@ def layer_forward(arch: str, op, H, Ws, relu: bool, mask=None):
     returns (P, Z, act(Z)).  `mask` (optional, reading R16b): the ReLU decision 1[Z > 0]
     taken by the kernel under test in its own precision -- act(Z) = Z * mask -- so that a
     pre-activation within rounding of 0 does not make the two sides branch differently."""
-    P = op @ H
-    Z = P @ Ws[0] if arch == "gcn" else H @ Ws[0] + P @ Ws[1]
+    if arch == "gat":
+        # GAT (P:438, R35): z = H W; alpha from (z a_src, z a_dst); Z = alpha z.  P carries the
+        # cache (z, alpha, LeakyReLU') for the backward.
+        z = H @ Ws[0]
+        alpha, slope = gat_attention(op, z, Ws[1][0], Ws[1][1])
+        Z = alpha @ z
+        P = (z, alpha, slope)
+    else:
+        P = op @ H
+        Z = P @ Ws[0] if arch == "gcn" else H @ Ws[0] + P @ Ws[1]
     if not relu:
         return P, Z, Z
     return P, Z, (np.maximum(Z, 0.0) if mask is None else Z * mask)
@@ -67,12 +80,66 @@ def layer_forward(arch: str, op, H, Ws, relu: bool, mask=None):
 
 def layer_backward(arch: str, op, H, P, Ws, dZ):
     """Reverse mode of layer_forward given dL/dZ: returns (weight grads, dL/dH)."""
+    if arch == "gat":
+        z, alpha, slope = P
+        a_src, a_dst = Ws[1][0], Ws[1][1]
+        dz = alpha.T @ dZ                                  # through Z = alpha z
+        rows = np.repeat(np.arange(alpha.shape[0]), np.diff(alpha.indptr))
+        cols = alpha.indices
+        dalpha = np.einsum("ij,ij->i", dZ[rows], z[cols])  # dL/dalpha_vu = dZ_v . z_u
+        c = np.zeros(alpha.shape[0])
+        np.add.at(c, rows, alpha.data * dalpha)            # softmax backward
+        dpre = alpha.data * (dalpha - c[rows]) * slope     # through LeakyReLU
+        ds = np.zeros(alpha.shape[0])
+        dt = np.zeros(alpha.shape[0])
+        np.add.at(ds, cols, dpre)                          # s_u enters every edge (v, u)
+        np.add.at(dt, rows, dpre)                          # t_v enters every edge of row v
+        dz = dz + np.outer(ds, a_src) + np.outer(dt, a_dst)
+        return [H.T @ dz, np.stack([z.T @ ds, z.T @ dt])], dz @ Ws[0].T
     if arch == "gcn":
         return [P.T @ dZ], op.T @ (dZ @ Ws[0].T)
     return [H.T @ dZ, P.T @ dZ], dZ @ Ws[0].T + op.T @ (dZ @ Ws[1].T)
 
 
+def gat_pattern(rowptr, col, n: int) -> sp.csr_matrix:
+    """GAT's attention support A_loc + I (each target attends to its local neighbours and to
+    itself, reading R35) as a 0/1 matrix with sorted indices."""
+    A = adjacency(rowptr, col, n)
+    M = (A + sp.identity(n, format="csr")).tocsr()
+    M.sort_indices()
+    M.data[:] = 1.0
+    return M
+
+
+LRELU_SLOPE = 0.2     # GAT's LeakyReLU negative slope (Velickovic et al., reading R35)
+
+
+def gat_attention(pattern, z, a_src, a_dst):
+    """alpha_vu = softmax_{u in N(v) + v} LeakyReLU(s_u + t_v), s = z a_src, t = z a_dst
+    (P:438 "assigns weights to different neighborhood nodes using attention"; R35).  Returns
+    (alpha as a sparse matrix on the pattern, LeakyReLU' per stored entry)."""
+    s = z @ a_src
+    t = z @ a_dst
+    rows = np.repeat(np.arange(pattern.shape[0]), np.diff(pattern.indptr))
+    cols = pattern.indices
+    pre = s[cols] + t[rows]
+    e = np.where(pre > 0, pre, LRELU_SLOPE * pre)
+    slope = np.where(pre > 0, 1.0, LRELU_SLOPE)          # LeakyReLU'(0) = slope (R35)
+    alpha = np.zeros_like(e)
+    for v in range(pattern.shape[0]):                      # row-wise max-shifted softmax
+        k0, k1 = pattern.indptr[v], pattern.indptr[v + 1]
+        ev = e[k0:k1]
+        w = np.exp(ev - ev.max())
+        alpha[k0:k1] = w / w.sum()
+    A = sp.csr_matrix((alpha, cols.copy(), pattern.indptr.copy()), shape=pattern.shape)
+    return A, slope
+
+
 def operator(arch: str, rowptr, col, n: int, node_w=None):
+    if arch == "gat":
+        if node_w is not None:
+            raise ValueError("node-level weights are defined for mean/sum aggregators (R30), not GAT")
+        return gat_pattern(rowptr, col, n)
     return (gcn_operator(rowptr, col, n, node_w) if arch == "gcn"
             else sage_operator(rowptr, col, n, node_w))
 
