@@ -229,6 +229,9 @@ WORKLOADS = {
     "rmat26": Workload("rmat26", "rmat", 1 << 26, 128, 16, "gcn", 4, train_frac=0.1, scale=26,
                        num_samples=1 << 30, chunks=8, correction="uniform"),
 }
+# §8f row 4: the products graph under GAT-3 (R35), full-graph, P = 8 (not a BASELINE config)
+WORKLOADS["products_gat"] = Workload(**{**WORKLOADS["products"].__dict__, "name": "products_gat",
+                                        "arch": "gat", "depth": 3})
 WORKLOADS["cora4"] = Workload(**{**WORKLOADS["cora"].__dict__, "name": "cora4", "chunks": 4,
                                  "extra": dict(workers=2)})
 

@@ -44,7 +44,10 @@ typedef enum {
 } grappa_status;
 
 typedef enum { GRAPPA_F32 = 0, GRAPPA_BF16 = 1 } grappa_dtype;
-typedef enum { GRAPPA_GCN = 0, GRAPPA_SAGE = 1 } grappa_arch;
+/* GRAPPA_GAT (reading R35): one attention head over N_loc(v) + v,
+ * e_vu = LeakyReLU_0.2(z_u . a_src + z_v . a_dst), alpha = row softmax, out_v = sum alpha_vu z_u,
+ * z = h W; weights per layer [W; a_src; a_dst] = fp32 [(f_in + 2) x f_out] (W rows first). */
+typedef enum { GRAPPA_GCN = 0, GRAPPA_SAGE = 1, GRAPPA_GAT = 2 } grappa_arch;
 
 /* Coverage-correction factor kinds (§3.4):
  *  NONE           c = 1                         (ablation "UW")
@@ -224,6 +227,10 @@ size_t grappa_layer_ws_bytes(const grappa_part* part, grappa_arch arch, int32_t 
  *                      `saved` unused (may be NULL).
  *   SAGE (R6):  M = D_l^-1 A_loc h_in (SpMM, zero rows where d_l = 0, kept in
  *                      `saved`), h_out = act([h_in | M] [W_self; W_nbr]) (one GEMM, K = 2 f_in).
+ *   GAT  (R35):        [z | s t] = h_in [W | W a_src | W a_dst] (one GEMM; z, s, t kept in
+ *                      `saved` with the attention coefficients), alpha per edge and self loop
+ *                      (row log-sum-exp), h_out = act(sum_u alpha_vu z_u) (the SpMM with
+ *                      per-edge weights).  f_out <= 256 (bf16) / 128 (fp32), else E_SHAPE.
  *   act = ReLU if relu != 0 else identity (output layer).
  *   h_in dev [n_core x f_in], h_out dev [n_core x f_out] (dtype); w dev fp32: GCN
  *   [f_in x f_out], SAGE [2 f_in x f_out] (W_self rows first).  ws: grappa_layer_ws_bytes.

@@ -13,7 +13,7 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import (BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, CORR, F32, GCN, LAYER_NODE_LEVEL, SAGE,
+from ._lib import (BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, CORR, F32, GAT, GCN, LAYER_NODE_LEVEL, SAGE,
                    GrappaError, load)
 
 __all__ = ["Context", "Part", "grappa_partition", "grappa_repartition", "grappa_layer_fwd",
@@ -31,7 +31,7 @@ def dtype_code(dt) -> int:
 
 
 def arch_code(a) -> int:
-    return {"gcn": GCN, "sage": SAGE, GCN: GCN, SAGE: SAGE}[a]
+    return {"gcn": GCN, "sage": SAGE, "gat": GAT, GCN: GCN, SAGE: SAGE, GAT: GAT}[a]
 
 
 class _DevView:

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgrappa.so")
 
 F32, BF16 = 0, 1
-GCN, SAGE = 0, 1
+GCN, SAGE, GAT = 0, 1, 2
 CORR = {"none": 0, "uniform": 1, "resampling": 2, "resampling_hm": 3, "node": 4}
 BWD_DZ_OUT_NORMED, BWD_DZ_IN_NORMED = 1, 2
 LAYER_NODE_LEVEL = 4

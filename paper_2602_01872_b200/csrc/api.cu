@@ -187,9 +187,19 @@ extern "C" grappa_status grappa_profile_read(grappa_ctx* c, int cls, double* ms,
 // ------------------------------------------------------------------------------ layers
 static inline size_t esz_of(grappa_dtype dt) { return dt == GRAPPA_BF16 ? 2 : 4; }
 
+namespace grappa {
+size_t gat_saved_bytes(const grappa_part* part, int f_out, grappa_dtype dt);
+size_t gat_ws_bytes(const grappa_part* part, int f_in, int f_out, grappa_dtype dt);
+grappa_status gat_fwd(grappa_ctx* ctx, const grappa_part* part, int f_in, int f_out, int relu, const void* h_in,
+                      const float* w, void* h_out, void* saved, void* ws, grappa_dtype dt, cudaStream_t s);
+grappa_status gat_bwd(grappa_ctx* ctx, const grappa_part* part, int f_in, int f_out, int relu_in,
+                      const void* dz_out, const void* h_in, const float* w, const void* saved, float* dw,
+                      void* dz_in, void* ws, grappa_dtype dt, cudaStream_t s);
+}  // namespace grappa
+
 extern "C" size_t grappa_layer_saved_bytes(const grappa_part* part, grappa_arch arch, int32_t f_in,
                                            int32_t f_out, grappa_dtype dtype) {
-    (void)f_out;
+    if (part && arch == GRAPPA_GAT) return gat_saved_bytes(part, f_out, dtype);
     if (!part || arch != GRAPPA_SAGE) return 0;
     return (size_t)part->info.n_core * f_in * esz_of(dtype);   // M = D^-1 A h_in
 }
@@ -197,6 +207,7 @@ extern "C" size_t grappa_layer_saved_bytes(const grappa_part* part, grappa_arch 
 extern "C" size_t grappa_layer_ws_bytes(const grappa_part* part, grappa_arch arch, int32_t f_in,
                                         int32_t f_out, grappa_dtype dtype) {
     if (!part) return 0;
+    if (arch == GRAPPA_GAT) return gat_ws_bytes(part, f_in, f_out, dtype);
     const int64_t n = part->info.n_core, slots = std::max<int64_t>(part->info.n_slots, part->t_n_slots);
     const size_t es = esz_of(dtype);
     const int wmax = f_in > f_out ? f_in : f_out;
@@ -249,10 +260,16 @@ extern "C" grappa_status grappa_layer_fwd_ex(grappa_ctx* ctx, const grappa_part*
                flags);
     GRAPPA_ARG(ctx && part && h_in && w && h_out && ws, GRAPPA_E_ARG, "grappa_layer_fwd: null argument");
     GRAPPA_TRY(check_dims("grappa_layer_fwd", f_in, f_out));
-    GRAPPA_ARG(arch != GRAPPA_SAGE || saved, GRAPPA_E_ARG, "grappa_layer_fwd: SAGE needs `saved`");
+    GRAPPA_ARG(arch == GRAPPA_GCN || saved, GRAPPA_E_ARG, "grappa_layer_fwd: SAGE / GAT need `saved`");
+    GRAPPA_ARG(arch == GRAPPA_GCN || arch == GRAPPA_SAGE || arch == GRAPPA_GAT, GRAPPA_E_ARG,
+               "grappa_layer_fwd: unknown arch %d", (int)arch);
     cudaStream_t s = (cudaStream_t)stream;
     const grappa_part_info& I = part->info;
     const bool node = flags & GRAPPA_LAYER_NODE_LEVEL;
+    if (arch == GRAPPA_GAT) {
+        GRAPPA_ARG(!node, GRAPPA_E_ARG, "grappa_layer_fwd_ex: node-level weights are not defined for GAT (R35)");
+        return gat_fwd(ctx, part, f_in, f_out, relu, h_in, w, h_out, saved, ws, dtype, s);
+    }
     const float* w_node = node ? I.node_w : nullptr;                       // w_v
     const float* sage_scale = node ? I.node_w + 2 * I.n_core : I.norm_sage;  // w_v / d_l
     WsLayout L = carve(part, arch, f_in, f_out, dtype, ws);
@@ -312,9 +329,15 @@ extern "C" grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part*
     GRAPPA_ARG(ctx && part && dz_out && h_in && w && dw && ws, GRAPPA_E_ARG,
                "grappa_layer_bwd: null argument");
     GRAPPA_TRY(check_dims("grappa_layer_bwd", f_in, f_out));
-    GRAPPA_ARG(arch != GRAPPA_SAGE || saved, GRAPPA_E_ARG, "grappa_layer_bwd: SAGE needs `saved`");
+    GRAPPA_ARG(arch == GRAPPA_GCN || saved, GRAPPA_E_ARG, "grappa_layer_bwd: SAGE / GAT need `saved`");
+    GRAPPA_ARG(arch == GRAPPA_GCN || arch == GRAPPA_SAGE || arch == GRAPPA_GAT, GRAPPA_E_ARG,
+               "grappa_layer_bwd: unknown arch %d", (int)arch);
     cudaStream_t s = (cudaStream_t)stream;
     const grappa_part_info& I = part->info;
+    if (arch == GRAPPA_GAT) {
+        GRAPPA_ARG(!node, GRAPPA_E_ARG, "grappa_layer_bwd_ex: node-level weights are not defined for GAT (R35)");
+        return gat_bwd(ctx, part, f_in, f_out, relu_in, dz_out, h_in, w, saved, dw, dz_in, ws, dtype, s);
+    }
     WsLayout L = carve(part, arch, f_in, f_out, dtype, ws);
     if (arch == GRAPPA_GCN && dz_in && flags == 0 && !part->halo && spmm_mm_supported(part, f_out, f_in, dtype)) {
         // dT = Ahat dz_out and dz_in = (dT W^T) * relu'(h_in) in one fused kernel, then

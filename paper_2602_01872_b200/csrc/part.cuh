@@ -33,4 +33,9 @@ struct grappa_part {
     grappa::DevBuf t_rowptr, t_col, t_deg, t_heavy_rows, t_heavy_slot_off, t_slot_row, t_slot_seg,
         t_row_order, t_row_desc, t_tmp;
     int64_t t_n_heavy = 0, t_n_slots = 0;
+    // forward edge id of every transposed entry (GAT backward needs the attention coefficient of
+    // (v -> u) while walking u's transposed row): built at repartition in halo-1 mode, lazily
+    // (k_gat_rev) on the first GAT backward in induced-core mode
+    grappa::DevBuf t_eid;
+    bool t_eid_ready = false;
 };

@@ -145,6 +145,15 @@ __global__ void k_t_rowptr(int64_t n, int64_t nnz, const int32_t* __restrict__ s
         for (int64_t r = prev + 1; r <= cur && r <= n; r++) trowptr[r] = e;
     }
 }
+__global__ void k_iota(int64_t n, int32_t* __restrict__ a) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = (int32_t)i;
+}
+__global__ void k_take(int64_t n, const int32_t* __restrict__ idx, const int32_t* __restrict__ src,
+                       int32_t* __restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
 __global__ void k_row_deg(int64_t n, const int64_t* __restrict__ rowptr, int32_t* __restrict__ deg) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         deg[i] = (int32_t)(rowptr[i + 1] - rowptr[i]);
@@ -622,6 +631,7 @@ extern "C" grappa_status grappa_repartition_ex(grappa_ctx* ctx, const grappa_csr
     p->halo = halo;
     p->n_halo = n_halo;
     p->t_n_heavy = p->t_n_slots = 0;
+    p->t_eid_ready = halo;            // induced-core: built lazily by the first GAT backward
     if (halo) {
         RP_TRY(p->t_rowptr.grow((size_t)(n_local + 1) * 8));
         RP_TRY(p->t_col.grow((size_t)(nnz > 0 ? nnz : 1) * 4));
@@ -632,17 +642,25 @@ extern "C" grappa_status grappa_repartition_ex(grappa_ctx* ctx, const grappa_csr
         cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
                                         (const int32_t*)nullptr, (int32_t*)nullptr, (int)nnz, 0, end_bit, s);
         const size_t e4 = al((size_t)(nnz > 0 ? nnz : 1) * 4);
-        RP_TRY(p->t_tmp.grow(2 * e4 + sort_bytes));
+        RP_TRY(p->t_tmp.grow(3 * e4 + sort_bytes));
+        RP_TRY(p->t_eid.grow((size_t)(nnz > 0 ? nnz : 1) * 4));
         int32_t* erow = (int32_t*)p->t_tmp.p;
         int32_t* skeys = (int32_t*)((char*)p->t_tmp.p + e4);
-        void* stmp = (char*)p->t_tmp.p + 2 * e4;
+        int32_t* iota = (int32_t*)((char*)p->t_tmp.p + 2 * e4);
+        void* stmp = (char*)p->t_tmp.p + 3 * e4;
         if (nnz > 0) {
             k_edge_rows<<<tgrid, 256, 0, s>>>(n_core, (int64_t*)p->rowptr.p, erow);
             GRAPPA_LAUNCHED(ctx);
+            k_iota<<<(unsigned)std::min<int64_t>(ceil_div(nnz, 256), 4096), 256, 0, s>>>(nnz, iota);
+            GRAPPA_LAUNCHED(ctx);
+            // stable sort of edge ids by column: t_eid = forward edge of each transposed entry
             GRAPPA_CUDA(cub::DeviceRadixSort::SortPairs(stmp, sort_bytes, (const int32_t*)p->col.p, skeys,
-                                                        (const int32_t*)erow, (int32_t*)p->t_col.p, (int)nnz, 0,
+                                                        (const int32_t*)iota, (int32_t*)p->t_eid.p, (int)nnz, 0,
                                                         end_bit, s));
             ctx->launches++;
+            k_take<<<(unsigned)std::min<int64_t>(ceil_div(nnz, 256), 4096), 256, 0, s>>>(
+                nnz, (const int32_t*)p->t_eid.p, erow, (int32_t*)p->t_col.p);
+            GRAPPA_LAUNCHED(ctx);
         }
         k_t_rowptr<<<(unsigned)std::min<int64_t>(ceil_div(nnz + 1, 256), 4096), 256, 0, s>>>(
             n_local, nnz, skeys, (int64_t*)p->t_rowptr.p);
@@ -718,7 +736,7 @@ extern "C" void grappa_part_destroy(grappa_part* p) {
                               &p->heavy_slot_off, &p->slot_row, &p->slot_seg, &p->row_order,
                               &p->row_desc, &p->t_rowptr, &p->t_col, &p->t_deg, &p->t_heavy_rows,
                               &p->t_heavy_slot_off, &p->t_slot_row, &p->t_slot_seg, &p->t_row_order,
-                              &p->t_row_desc, &p->t_tmp})
+                              &p->t_row_desc, &p->t_tmp, &p->t_eid})
         b->release();
     delete p;
 }
@@ -729,7 +747,7 @@ extern "C" void grappa_part_destroy(grappa_part* p) {
 // every array at a 256-byte aligned offset, in the fixed order of part_arrays().
 namespace {
 constexpr uint64_t kImageMagic = 0x4752415050414931ull;   // "GRAPPAI1"
-constexpr int kImageArrays = 26;
+constexpr int kImageArrays = 27;
 struct ImageHeader {
     uint64_t magic;
     grappa_part_info info;      // pointers are meaningless in the image
@@ -756,6 +774,7 @@ static int part_arrays(grappa_part* p, const grappa_part_info& I, bool halo, int
     add(p->t_heavy_rows, th * 4); add(p->t_heavy_slot_off, halo ? (th + 1) * 4 : 0);
     add(p->t_slot_row, ts * 4); add(p->t_slot_seg, ts * 4); add(p->t_row_order, halo ? n * 4 : 0);
     add(p->t_row_desc, halo ? n * 16 : 0);
+    add(p->t_eid, halo ? nnz * 4 : 0);
     return k;
 }
 static size_t al256(size_t b) { return (b + 255) / 256 * 256; }
@@ -827,6 +846,7 @@ extern "C" grappa_status grappa_part_load(grappa_part** inout, const void* host,
     }
     p->halo = h.halo != 0;
     p->n_halo = h.n_halo; p->t_n_heavy = h.t_n_heavy; p->t_n_slots = h.t_n_slots;
+    p->t_eid_ready = p->halo;
     grappa_part_info& I = p->info;
     I = h.info;
     I.rowptr = (int64_t*)p->rowptr.p; I.col = (int32_t*)p->col.p;

@@ -109,7 +109,8 @@ __device__ __forceinline__ void gather_edges(const SpmmArgs& a, int64_t e0, int6
         float my_w = 1.f;
         if (lane < cnt) {
             my_idx = a.col[base + lane];
-            if (a.col_scale) my_w = a.col_scale[my_idx];
+            if (a.edge_w) my_w = a.edge_w[base + lane];
+            else if (a.col_scale) my_w = a.col_scale[my_idx];
         }
         for (int j = 0; j < cnt; j += P * kUnroll) {
             typename Vec<T>::type v[kUnroll][CPL];
@@ -319,7 +320,8 @@ template <typename T, int R, int U, bool WT>
 __device__ __forceinline__ void grp_accumulate(const T* __restrict__ X, const int32_t* __restrict__ col,
                                                const float* __restrict__ col_scale, int64_t e0,
                                                int deg, int G, int slot, int sub,
-                                               float (&acc)[Vec<T>::EPV]) {
+                                               float (&acc)[Vec<T>::EPV],
+                                               const float* __restrict__ edge_w = nullptr) {
     constexpr int E = Vec<T>::EPV;
     const int WV = G;
     const int maxdeg = __reduce_max_sync(0xffffffffu, deg);
@@ -332,7 +334,7 @@ __device__ __forceinline__ void grp_accumulate(const T* __restrict__ X, const in
             const int p = off + r * G + sub;
             const bool ok = p < deg;
             idx[r] = ok ? col[e0 + p] : 0;
-            if (WT) wt[r] = ok ? col_scale[idx[r]] : 0.f;
+            if (WT) wt[r] = ok ? (edge_w ? edge_w[e0 + p] : col_scale[idx[r]]) : 0.f;
         }
 #pragma unroll
         for (int r = 0; r < R; r++) {
@@ -417,7 +419,7 @@ __global__ void __launch_bounds__(256) k_spmm_grp(SpmmArgs a, int G, int P) {
 #pragma unroll
     for (int q = 0; q < E; q++) acc[q] = 0.f;
     grp_accumulate<T, R, U, WT>(reinterpret_cast<const T*>(a.X), a.col, a.col_scale, e0, (int)(e1 - e0),
-                                G, slot, sub, acc);
+                                G, slot, sub, acc, a.edge_w);
     if (orow < 0) return;
     if (to_partial) {
         float* dst = a.partial + ((int64_t)orow * WV + sub) * E;
@@ -587,10 +589,10 @@ static grappa_status launch_grp(grappa_ctx* ctx, const SpmmArgs& a, int G, cudaS
     if (vrows > 0) {
         const unsigned grid = (unsigned)ceil_div(ceil_div(vrows, P), 8);
         if (g_spmm_variant == 2) {
-            if (a.col_scale) k_spmm_grp<T, R, 8, true><<<grid, 256, 0, s>>>(a, G, P);
+            if (a.col_scale || a.edge_w) k_spmm_grp<T, R, 8, true><<<grid, 256, 0, s>>>(a, G, P);
             else k_spmm_grp<T, R, 8, false><<<grid, 256, 0, s>>>(a, G, P);
         } else {
-            if (a.col_scale) k_spmm_grp<T, R, 4, true><<<grid, 256, 0, s>>>(a, G, P);
+            if (a.col_scale || a.edge_w) k_spmm_grp<T, R, 4, true><<<grid, 256, 0, s>>>(a, G, P);
             else k_spmm_grp<T, R, 4, false><<<grid, 256, 0, s>>>(a, G, P);
         }
         GRAPPA_LAUNCHED(ctx);
@@ -634,7 +636,7 @@ static grappa_status launch_grp16(grappa_ctx* ctx, const SpmmArgs& a, int G, cud
 template <typename T>
 static grappa_status launch_t(grappa_ctx* ctx, const SpmmArgs& a, cudaStream_t s) {
     const int WV = a.width / Vec<T>::EPV;
-    if (sizeof(T) == 2 && !a.col_scale && a.width % 16 == 0 && a.width / 16 <= 32 && g_spmm_variant == 0 &&
+    if (sizeof(T) == 2 && !a.col_scale && !a.edge_w && a.width % 16 == 0 && a.width / 16 <= 32 && g_spmm_variant == 0 &&
         g_wide_loads) {
         const int G16 = a.width / 16;
         if (G16 >= 16) return launch_grp16<1>(ctx, a, G16, s);
@@ -978,7 +980,7 @@ grappa_status spmm_csr(grappa_ctx* ctx, SpmmArgs a, grappa_dtype dt, cudaStream_
     }
     struct { int64_t n_core, nnz; } I{a.n, a.nnz};
     const double es = dt == GRAPPA_BF16 ? 2.0 : 4.0, w = a.width, nnz = (double)I.nnz;
-    const double per_edge = 4.0 + (a.col_scale ? 4.0 : 0.0) + w * es;
+    const double per_edge = 4.0 + (a.col_scale || a.edge_w ? 4.0 : 0.0) + w * es;
     const bool self_coef = a.self && (a.self_sep ? a.self_scale != nullptr : a.col_scale != nullptr);
     const double per_row = 8.0 + (a.row_scale ? 4.0 : 0.0) + (self_coef ? 4.0 : 0.0) +
                            (a.nbr_scale ? 4.0 : 0.0) + (a.self ? w * es : 0.0) + w * es +

@@ -23,6 +23,7 @@ struct SpmmArgs {
     const float* row_scale = nullptr; // rs[v] or null (1)
     const float* col_scale = nullptr; // cs[u] or null (1); also weights the self term
     const float* nbr_scale = nullptr; // ns[v] or null (1): multiplies the neighbour sum only
+    const float* edge_w = nullptr;    // per-edge weight w[e] (CSR order) instead of cs[u] (GAT)
     int self = 0;
     int self_sep = 0;                 // self term weighted by self_scale[v] (null: 1), not cs[v]
     const float* self_scale = nullptr;

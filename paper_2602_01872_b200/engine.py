@@ -72,7 +72,10 @@ class ModelSpec:
         return len(self.dims) - 1
 
     def layer_shapes(self):
-        """padded weight block shape per layer: GCN [fin, fout]; SAGE [2 fin, fout]"""
+        """padded weight block shape per layer: GCN [fin, fout]; SAGE [2 fin, fout];
+        GAT [fin + 2, fout] (W, then the a_src and a_dst rows)"""
+        if self.arch == "gat":
+            return [(self.dims_pad[l] + 2, self.dims_pad[l + 1]) for l in range(self.depth)]
         m = 1 if self.arch == "gcn" else 2
         return [(m * self.dims_pad[l], self.dims_pad[l + 1]) for l in range(self.depth)]
 
