@@ -18,6 +18,7 @@
 namespace grappa {
 
 constexpr float kSlope = 0.2f;     // LeakyReLU negative slope (R35)
+constexpr int kHW = 32;            // warps per block of the block-per-hub-row kernels
 
 template <typename T> struct GV;
 template <> struct GV<float> {
@@ -107,9 +108,10 @@ __global__ void k_gat_alpha(int64_t n, const int64_t* __restrict__ rowptr, const
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += nwarps) {
+        const int64_t e0 = rowptr[v], e1 = rowptr[v + 1];
+        if (e1 - e0 > kSegLen) continue;                 // hub rows: k_gat_alpha_heavy
         const float4 av = att[v];
         const float sv = av.x, tv = av.y;
-        const int64_t e0 = rowptr[v], e1 = rowptr[v + 1];
         const float eself = lrelu(sv + tv);
         // online max / sum per lane, then a fixed-order warp combine
         float m = lane == 0 ? eself : -INFINITY, sum = lane == 0 ? 1.f : 0.f;
@@ -132,6 +134,51 @@ __global__ void k_gat_alpha(int64_t n, const int64_t* __restrict__ rowptr, const
             att[v].z = lse;
         }
     }
+}
+
+// hub rows (deg > kSegLen), one kHW-warp block each: per-thread online (max, sum), combined
+// across lanes then warps in a fixed order; then every thread writes its edges' coefficients
+__global__ void __launch_bounds__(kHW * 32) k_gat_alpha_heavy(const int32_t* __restrict__ heavy_rows,
+                                                               const int64_t* __restrict__ rowptr,
+                                                               const int32_t* __restrict__ col,
+                                                               float* __restrict__ alpha, float* __restrict__ alpha_self,
+                                                               float4* __restrict__ att) {
+    __shared__ float sm[kHW], ss[kHW];
+    __shared__ float s_lse;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t v = heavy_rows[blockIdx.x];
+    const int64_t e0 = rowptr[v], e1 = rowptr[v + 1];
+    const float4 av = att[v];
+    const float tv = av.y, eself = lrelu(av.x + av.y);
+    float m = threadIdx.x == 0 ? eself : -INFINITY, sum = threadIdx.x == 0 ? 1.f : 0.f;
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        const float x = lrelu(att[col[e]].x + tv);
+        if (x > m) { sum = sum * __expf(m - x) + 1.f; m = x; }
+        else sum += __expf(x - m);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+        const float mm = fmaxf(m, m2);
+        sum = (m == -INFINITY ? 0.f : sum * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+        m = mm;
+    }
+    if (lane == 0) { sm[w] = m; ss[w] = sum; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float M = -INFINITY, S = 0.f;
+        for (int k = 0; k < kHW; k++) {
+            const float mm = fmaxf(M, sm[k]);
+            S = (M == -INFINITY ? 0.f : S * __expf(M - mm)) + (sm[k] == -INFINITY ? 0.f : ss[k] * __expf(sm[k] - mm));
+            M = mm;
+        }
+        s_lse = M + __logf(S);
+        alpha_self[v] = __expf(eself - s_lse);
+        att[v].z = s_lse;
+    }
+    __syncthreads();
+    const float lse = s_lse;
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) alpha[e] = __expf(lrelu(att[col[e]].x + tv) - lse);
 }
 
 // induced-core: the CSR is symmetric with ascending rows, so the transpose is the CSR itself and
@@ -236,23 +283,23 @@ __global__ void __launch_bounds__(256) k_gat_rows(int64_t n, const int4* __restr
     }
 }
 
-// heavy rows (deg > kSegLen): one 256-thread block per row; warp w takes the contiguous edge range
-// [w L/8, (w+1) L/8), its P lane groups every P-th edge of it; group sums are combined in slot
+// heavy rows (deg > kSegLen): one kHW-warp block per row; warp w takes the contiguous edge range
+// [w L/kHW, (w+1) L/kHW), its P lane groups every P-th edge of it; group sums are combined in slot
 // order, warp sums in warp order, the self loop last (deterministic).
 template <typename T>
-__global__ void __launch_bounds__(256) k_gat_rows_heavy(const int32_t* __restrict__ heavy_rows,
+__global__ void __launch_bounds__(kHW * 32) k_gat_rows_heavy(const int32_t* __restrict__ heavy_rows,
                                                         const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                                                         const T* __restrict__ z, const T* __restrict__ g,
                                                         const float* __restrict__ alpha, const float* __restrict__ alpha_self,
                                                         float4* __restrict__ att, float* __restrict__ dt, int W, int G, int G2) {
     constexpr int E = GV<T>::E;
-    __shared__ RowAcc part[8];
+    __shared__ RowAcc part[kHW];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t v = heavy_rows[blockIdx.x];
     const int64_t r0 = rowptr[v], r1 = rowptr[v + 1], L = r1 - r0;
     // the warp's lanes: P = 32/G2 groups, each takes every P-th edge of the warp's range
     const int P = 32 / G2, slot = lane / G2, sub = lane % G2;
-    const int64_t w0 = r0 + L * w / 8, w1 = r0 + L * (w + 1) / 8;
+    const int64_t w0 = r0 + L * w / kHW, w1 = r0 + L * (w + 1) / kHW;
     float gv[E];
     const float tv = att[v].y;
     if (sub < G) GV<T>::load(g + v * W + sub * E, gv);
@@ -302,7 +349,7 @@ __global__ void __launch_bounds__(256) k_gat_rows_heavy(const int32_t* __restric
         const float dd = group_sum<T>(p, G2);
         if (lane == 0) {
             RowAcc s{0.f, 0.f, 0.f};
-            for (int k = 0; k < 8; k++) { s.A += part[k].A; s.B += part[k].B; s.C += part[k].C; }
+            for (int k = 0; k < kHW; k++) { s.A += part[k].A; s.B += part[k].B; s.C += part[k].C; }
             const float4 av = att[v];
             const float a = alpha_self[v], lam = lrelu_d(av.x + av.y);
             s.A = fmaf(a, dd, s.A);
@@ -401,7 +448,7 @@ __global__ void __launch_bounds__(256) k_gat_cols(int64_t n, const int4* __restr
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_gat_cols_heavy(const int32_t* __restrict__ heavy_rows,
+__global__ void __launch_bounds__(kHW * 32) k_gat_cols_heavy(const int32_t* __restrict__ heavy_rows,
                                                         const int64_t* __restrict__ trowptr, const int32_t* __restrict__ tcol,
                                                         const int32_t* __restrict__ eid, const T* __restrict__ z,
                                                         const T* __restrict__ g, const float* __restrict__ alpha,
@@ -410,13 +457,13 @@ __global__ void __launch_bounds__(256) k_gat_cols_heavy(const int32_t* __restric
                                                         const float* __restrict__ adst, T* __restrict__ dz, T* __restrict__ DS,
                                                         int W, int G, int G2) {
     constexpr int E = GV<T>::E;
-    __shared__ float red[8][32 * 8 + 1];
-    __shared__ float dsw[8];
+    __shared__ float red[kHW][32 * 8 + 1];
+    __shared__ float dsw[kHW];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t u = heavy_rows[blockIdx.x];
     const int64_t r0 = trowptr[u], r1 = trowptr[u + 1], L = r1 - r0;
     const int P = 32 / G2, slot = lane / G2, sub = lane % G2;
-    const int64_t w0 = r0 + L * w / 8, w1 = r0 + L * (w + 1) / 8;
+    const int64_t w0 = r0 + L * w / kHW, w1 = r0 + L * (w + 1) / kHW;
     float zu[E], acc[E];
 #pragma unroll
     for (int q = 0; q < E; q++) { zu[q] = 0.f; acc[q] = 0.f; }
@@ -467,7 +514,7 @@ __global__ void __launch_bounds__(256) k_gat_cols_heavy(const int32_t* __restric
 #pragma unroll
         for (int q = 0; q < E; q++) s[q] = 0.f;
         float sds = 0.f;
-        for (int k = 0; k < 8; k++) {
+        for (int k = 0; k < kHW; k++) {
             if (sub < G) {
 #pragma unroll
                 for (int q = 0; q < E; q++) s[q] += red[k][sub * E + q];
@@ -579,6 +626,11 @@ grappa_status gat_fwd(grappa_ctx* ctx, const grappa_part* part, int f_in, int f_
     // attention coefficients
     k_gat_alpha<<<grid, 256, 0, s>>>(n, I.rowptr, I.col, S.alpha, S.alpha_self, S.att);
     GRAPPA_LAUNCHED(ctx);
+    if (I.n_heavy > 0) {
+        k_gat_alpha_heavy<<<(unsigned)I.n_heavy, kHW * 32, 0, s>>>((const int32_t*)part->heavy_rows.p, I.rowptr,
+                                                                   I.col, S.alpha, S.alpha_self, S.att);
+        GRAPPA_LAUNCHED(ctx);
+    }
     // h_out = act(alpha_self z_v + sum alpha_e z_u): the SpMM with per-edge weights
     SpmmArgs a;
     a.X = S.Z; a.width = f_out; a.edge_w = S.alpha; a.self = 1; a.self_sep = 1; a.self_scale = S.alpha_self;
@@ -624,7 +676,7 @@ grappa_status gat_bwd(grappa_ctx* ctx, const grappa_part* part, int f_in, int f_
                 GRAPPA_LAUNCHED(ctx);
             }
             if (I.n_heavy > 0) {
-                k_gat_rows_heavy<T><<<(unsigned)I.n_heavy, 256, 0, s>>>((const int32_t*)part->heavy_rows.p, I.rowptr,
+                k_gat_rows_heavy<T><<<(unsigned)I.n_heavy, kHW * 32, 0, s>>>((const int32_t*)part->heavy_rows.p, I.rowptr,
                                                                         I.col, (const T*)S.Z, (const T*)dz_out, S.alpha,
                                                                         S.alpha_self, S.att, Wk.dtv, f_out, G, G2);
                 GRAPPA_LAUNCHED(ctx);
@@ -636,7 +688,7 @@ grappa_status gat_bwd(grappa_ctx* ctx, const grappa_part* part, int f_in, int f_
                 GRAPPA_LAUNCHED(ctx);
             }
             if (tn_heavy > 0) {
-                k_gat_cols_heavy<T><<<(unsigned)tn_heavy, 256, 0, s>>>(theavy, trow, tcol, eid, (const T*)S.Z,
+                k_gat_cols_heavy<T><<<(unsigned)tn_heavy, kHW * 32, 0, s>>>(theavy, trow, tcol, eid, (const T*)S.Z,
                                                                        (const T*)dz_out, S.alpha, S.alpha_self, S.att,
                                                                        Wk.dtv, asrc, adst, (T*)Wk.dZ, (T*)Wk.DS,
                                                                        f_out, G, G2);
@@ -650,7 +702,7 @@ grappa_status gat_bwd(grappa_ctx* ctx, const grappa_part* part, int f_in, int f_
                 GRAPPA_LAUNCHED(ctx);
             }
             if (I.n_heavy > 0) {
-                k_gat_rows_heavy<T><<<(unsigned)I.n_heavy, 256, 0, s>>>((const int32_t*)part->heavy_rows.p, I.rowptr,
+                k_gat_rows_heavy<T><<<(unsigned)I.n_heavy, kHW * 32, 0, s>>>((const int32_t*)part->heavy_rows.p, I.rowptr,
                                                                         I.col, (const T*)S.Z, (const T*)dz_out, S.alpha,
                                                                         S.alpha_self, S.att, Wk.dtv, f_out, G, G2);
                 GRAPPA_LAUNCHED(ctx);
@@ -662,7 +714,7 @@ grappa_status gat_bwd(grappa_ctx* ctx, const grappa_part* part, int f_in, int f_
                 GRAPPA_LAUNCHED(ctx);
             }
             if (tn_heavy > 0) {
-                k_gat_cols_heavy<T><<<(unsigned)tn_heavy, 256, 0, s>>>(theavy, trow, tcol, eid, (const T*)S.Z,
+                k_gat_cols_heavy<T><<<(unsigned)tn_heavy, kHW * 32, 0, s>>>(theavy, trow, tcol, eid, (const T*)S.Z,
                                                                        (const T*)dz_out, S.alpha, S.alpha_self, S.att,
                                                                        Wk.dtv, asrc, adst, (T*)Wk.dZ, (T*)Wk.DS,
                                                                        f_out, G, G2);
