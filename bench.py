@@ -44,6 +44,8 @@ def parse():
                     choices=["none", "uniform", "resampling", "resampling_hm", "node"],
                     help="override the config's estimator (node = node-level eq. (9), R30)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--capacity", action="store_true",
+                    help="capacity mode: partitions streamed per phase from pinned host images")
     ap.add_argument("--halo", action="store_true",
                     help="halo-1 partitions (R33) instead of induced-core")
     ap.add_argument("--variant", action="append", default=[],
@@ -145,6 +147,8 @@ class OracleSample:
         import gen
         from oracle import partition as Po
         wl0 = gen.WORKLOADS[name]
+        if wl0.n <= 200_000 or wl0.kind == "sbm":
+            shrink = 1                      # small graphs (and fixed-size SBMs): the full workload
         n = max(wl0.n // shrink, 1000)
         scale = max(int(np.ceil(np.log2(n))), 4)
         self.wl = gen.small_workload(name, n=n, scale=scale,
@@ -271,7 +275,8 @@ def run_grappa(args):
     spec = ModelSpec(wl.arch, wl.dims, wl.dims_pad)
     stream = torch.cuda.current_stream(dev)
     common = dict(corr=args.corr or wl.correction, lr=0.003, repartition_every=wl.repartition_every,
-                  dtype=args.dtype, stream=stream, num_workers=wl.extra.get("workers"), halo=args.halo)
+                  dtype=args.dtype, stream=stream, num_workers=wl.extra.get("workers"), halo=args.halo,
+                  capacity=args.capacity)
     if wl.extra.get("mode") == "minibatch":
         tr = MinibatchTrainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights,
                               wl.chunks, gen.seed_of("chunks"), fanouts=wl.extra["fanouts"],
@@ -359,7 +364,7 @@ def run_grappa(args):
     # e2e: the same epochs through the public API with host buffers (per phase H2D of the
     # partition's inputs from pinned memory, D2H of the loss), copies inside the timed region
     e2e = None
-    if not args.no_e2e and not isinstance(tr, MinibatchTrainer):
+    if not args.no_e2e and not isinstance(tr, MinibatchTrainer) and not args.capacity:
         e2e = measure_e2e(tr, stream, K, barrier, world, dist, nnz)
 
     cpu = None
@@ -380,6 +385,8 @@ def run_grappa(args):
                                         "max": max(per_epoch), "note": "rank-local CUDA events; the "
                                         "epoch holding the repartition is the max"},
                            "l2": "inputs larger than L2 (graph+features ~1.6 GB, activations ~2.8 GB); no flush",
+                           "capacity_mode": bool(args.capacity),
+                           "capacity_h2d_bytes_per_epoch": int(sum(tr.img_bytes.values())) if args.capacity else 0,
                            "parallelism": f"dp{world} (phase-parallel, gradient-only)",
                            "generate_s": round(t_gen, 1)},
                 "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu,

@@ -109,6 +109,7 @@ class Trainer:
         # pinned host memory and are streamed into one of two device slots per phase
         self.capacity = capacity
         self.host_imgs: dict = {}
+        self.img_bytes: dict = {}
         self.cap_slots = None
         self.t_ctrl = 1
         self._steps = []
@@ -188,6 +189,7 @@ class Trainer:
                 host = torch.empty(nb + nb // 8, dtype=torch.uint8, pin_memory=True)
                 self.host_imgs[w] = host
             p.save(host, self.stream)
+            self.img_bytes[w] = nb
             sizes.append(self._sizes(p))
             self.stream.synchronize()              # the image is complete before slot 0 is reused
         self.t = t
