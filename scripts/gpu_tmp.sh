@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-free -g | head -2
-timeout 1500 python -m pytest tests/test_gpu_fullsize.py -x -q > gpurun_out/r01r_full.log 2>&1; echo "full $?"; tail -30 gpurun_out/r01r_full.log
+timeout 900 python -m pytest tests/test_gpu_edge_cases.py -x -q > gpurun_out/r01s_edge.log 2>&1; echo "edge $?"; tail -30 gpurun_out/r01s_edge.log
