@@ -248,6 +248,15 @@ grappa_status grappa_layer_fwd(grappa_ctx* ctx, const grappa_part* part, grappa_
  *     and the backward is the exact transpose (Ahat_w^T = N (A_loc diag(w) + I) N).
  *     Pair it with GRAPPA_CORR_NODE in the aggregation (batch factor 1).               */
 #define GRAPPA_LAYER_NODE_LEVEL 4u
+/*   GRAPPA_LAYER_INPUT : the model's first layer (its backward is called with dz_in = NULL).
+ *     GCN then evaluates aggregate-first, Z = (Ahat h_in) W: the forward keeps P = Ahat h_in in
+ *     `saved` (size: grappa_layer_saved_bytes_ex with this flag), and the backward is dW = P^T dz
+ *     alone -- no aggregation (a re-association of the same products, reading R29; one bf16
+ *     rounding of P instead of one of h_in W).  The backward takes no normalised-gradient flags.
+ *     No effect for SAGE / GAT (SAGE is aggregate-first already). */
+#define GRAPPA_LAYER_INPUT 8u
+size_t grappa_layer_saved_bytes_ex(const grappa_part* part, grappa_arch arch, int32_t f_in,
+                                   int32_t f_out, grappa_dtype dtype, unsigned flags);
 /* grappa_layer_fwd with flags (0 = grappa_layer_fwd).  Errors: E_ARG for unknown flags. */
 grappa_status grappa_layer_fwd_ex(grappa_ctx* ctx, const grappa_part* part, grappa_arch arch,
                                   int32_t f_in, int32_t f_out, int relu, const void* h_in,

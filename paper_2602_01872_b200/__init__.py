@@ -13,7 +13,7 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import (BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, CORR, F32, GAT, GCN, LAYER_NODE_LEVEL, SAGE,
+from ._lib import (BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, CORR, F32, GAT, GCN, LAYER_INPUT, LAYER_NODE_LEVEL, SAGE,
                    GrappaError, load)
 
 __all__ = ["Context", "Part", "grappa_partition", "grappa_repartition", "grappa_layer_fwd",
@@ -219,8 +219,9 @@ def grappa_repartition(ctx: Context, rowptr: torch.Tensor, col: torch.Tensor, fe
     return part.refresh()
 
 
-def layer_saved_bytes(part: Part, arch, f_in, f_out, dtype) -> int:
-    return int(load().grappa_layer_saved_bytes(part.h, arch_code(arch), f_in, f_out, dtype_code(dtype)))
+def layer_saved_bytes(part: Part, arch, f_in, f_out, dtype, flags: int = 0) -> int:
+    return int(load().grappa_layer_saved_bytes_ex(part.h, arch_code(arch), f_in, f_out, dtype_code(dtype),
+                                                  int(flags)))
 
 
 def layer_ws_bytes(part: Part, arch, f_in, f_out, dtype) -> int:

@@ -17,6 +17,7 @@ GCN, SAGE, GAT = 0, 1, 2
 CORR = {"none": 0, "uniform": 1, "resampling": 2, "resampling_hm": 3, "node": 4}
 BWD_DZ_OUT_NORMED, BWD_DZ_IN_NORMED = 1, 2
 LAYER_NODE_LEVEL = 4
+LAYER_INPUT = 8
 PART_HALO1 = 1
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_EMPTY", 4: "E_NONFINITE", 5: "E_SUPPORT",
           6: "E_NOMEM", 7: "E_CUDA", 8: "E_NCCL"}
@@ -33,7 +34,7 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_part_upload", "grappa_layer_bwd_ex", "grappa_layer_fwd_ex",
            "grappa_minibatch_step_ex", "grappa_sample_async", "grappa_sample_wait",
            "grappa_sample_event", "grappa_repartition_ex", "grappa_part_image_bytes",
-           "grappa_part_save", "grappa_part_image_info", "grappa_part_load"]
+           "grappa_part_save", "grappa_part_image_info", "grappa_part_load", "grappa_layer_saved_bytes_ex"]
 KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5, "sample": 6}
 
 
@@ -110,6 +111,7 @@ def load(path: str = LIB_PATH):
         "grappa_part_destroy": (None, [vp]),
         "grappa_layer_saved_bytes": (sz, [vp, ctypes.c_int, i32, i32, ctypes.c_int]),
         "grappa_layer_ws_bytes": (sz, [vp, ctypes.c_int, i32, i32, ctypes.c_int]),
+        "grappa_layer_saved_bytes_ex": (sz, [vp, ctypes.c_int, i32, i32, ctypes.c_int, ctypes.c_uint]),
         "grappa_layer_fwd": (st, [vp, vp, ctypes.c_int, i32, i32, ctypes.c_int, vp, vp, vp, vp, vp,
                                   ctypes.c_int, vp]),
         "grappa_layer_bwd": (st, [vp, vp, ctypes.c_int, i32, i32, ctypes.c_int, vp, vp, vp, vp, vp,

@@ -197,6 +197,13 @@ grappa_status gat_bwd(grappa_ctx* ctx, const grappa_part* part, int f_in, int f_
                       void* dz_in, void* ws, grappa_dtype dt, cudaStream_t s);
 }  // namespace grappa
 
+extern "C" size_t grappa_layer_saved_bytes_ex(const grappa_part* part, grappa_arch arch, int32_t f_in,
+                                              int32_t f_out, grappa_dtype dtype, unsigned flags) {
+    if (part && arch == GRAPPA_GCN && (flags & GRAPPA_LAYER_INPUT))
+        return (size_t)part->info.n_core * f_in * esz_of(dtype);   // P = Ahat h_in (aggregate-first)
+    return grappa_layer_saved_bytes(part, arch, f_in, f_out, dtype);
+}
+
 extern "C" size_t grappa_layer_saved_bytes(const grappa_part* part, grappa_arch arch, int32_t f_in,
                                            int32_t f_out, grappa_dtype dtype) {
     if (part && arch == GRAPPA_GAT) return gat_saved_bytes(part, f_out, dtype);
@@ -256,8 +263,10 @@ extern "C" grappa_status grappa_layer_fwd_ex(grappa_ctx* ctx, const grappa_part*
                                              int32_t f_in, int32_t f_out, int relu, const void* h_in,
                                              const float* w, void* h_out, void* saved, void* ws,
                                              grappa_dtype dtype, unsigned flags, void* stream) {
-    GRAPPA_ARG((flags & ~GRAPPA_LAYER_NODE_LEVEL) == 0, GRAPPA_E_ARG, "grappa_layer_fwd_ex: flags 0x%x invalid",
-               flags);
+    GRAPPA_ARG((flags & ~(GRAPPA_LAYER_NODE_LEVEL | GRAPPA_LAYER_INPUT)) == 0, GRAPPA_E_ARG,
+               "grappa_layer_fwd_ex: flags 0x%x invalid", flags);
+    GRAPPA_ARG(arch != GRAPPA_GCN || !(flags & GRAPPA_LAYER_INPUT) || saved, GRAPPA_E_ARG,
+               "grappa_layer_fwd_ex: GRAPPA_LAYER_INPUT (GCN) needs `saved` (grappa_layer_saved_bytes_ex)");
     GRAPPA_ARG(ctx && part && h_in && w && h_out && ws, GRAPPA_E_ARG, "grappa_layer_fwd: null argument");
     GRAPPA_TRY(check_dims("grappa_layer_fwd", f_in, f_out));
     GRAPPA_ARG(arch == GRAPPA_GCN || saved, GRAPPA_E_ARG, "grappa_layer_fwd: SAGE / GAT need `saved`");
@@ -273,6 +282,18 @@ extern "C" grappa_status grappa_layer_fwd_ex(grappa_ctx* ctx, const grappa_part*
     const float* w_node = node ? I.node_w : nullptr;                       // w_v
     const float* sage_scale = node ? I.node_w + 2 * I.n_core : I.norm_sage;  // w_v / d_l
     WsLayout L = carve(part, arch, f_in, f_out, dtype, ws);
+    if (arch == GRAPPA_GCN && (flags & GRAPPA_LAYER_INPUT)) {
+        // input layer, aggregate-first: P = Ahat h_in (kept in `saved`), h_out = act(P W); its
+        // backward is then dW = P^T dz with no aggregation at all (no dh_in for the input)
+        SpmmArgs a;
+        a.X = h_in; a.width = f_in; a.row_scale = I.norm_gcn; a.col_scale = I.norm_gcn; a.nbr_scale = w_node;
+        a.self = 1; a.out = saved; a.partial = L.partial;
+        GRAPPA_TRY(spmm(ctx, part, a, dtype, s));
+        GemmArgs g;
+        g.M = I.n_core; g.K1 = f_in; g.N = f_out; g.A1 = saved; g.B = w; g.relu = relu; g.n_split = f_out;
+        g.C1 = h_out;
+        return gemm_nn(ctx, g, dtype, s);
+    }
     if (arch == GRAPPA_GCN && !node && f_in <= f_out && spmm_mm_supported(part, f_in, f_out, dtype)) {
         // h_out = act((Ahat h_in) W): aggregate at the narrower width, transform fused into
         // the aggregation kernel (tcgen05 on the smem-resident tile)
@@ -322,7 +343,8 @@ extern "C" grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part*
                                              const void* h_in, const float* w, const void* saved,
                                              float* dw, void* dz_in, void* ws, grappa_dtype dtype,
                                              unsigned flags, void* stream) {
-    GRAPPA_ARG((flags & ~(3u | GRAPPA_LAYER_NODE_LEVEL)) == 0 && ((flags & 3u) == 0 || arch == GRAPPA_GCN),
+    GRAPPA_ARG((flags & ~(3u | GRAPPA_LAYER_NODE_LEVEL | GRAPPA_LAYER_INPUT)) == 0 &&
+                   ((flags & 3u) == 0 || arch == GRAPPA_GCN),
                GRAPPA_E_ARG, "grappa_layer_bwd_ex: flags 0x%x invalid (normalised gradients are GCN-only)", flags);
     const bool out_normed = flags & GRAPPA_BWD_DZ_OUT_NORMED, in_normed = flags & GRAPPA_BWD_DZ_IN_NORMED;
     const bool node = flags & GRAPPA_LAYER_NODE_LEVEL;
@@ -337,6 +359,15 @@ extern "C" grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part*
     if (arch == GRAPPA_GAT) {
         GRAPPA_ARG(!node, GRAPPA_E_ARG, "grappa_layer_bwd_ex: node-level weights are not defined for GAT (R35)");
         return gat_bwd(ctx, part, f_in, f_out, relu_in, dz_out, h_in, w, saved, dw, dz_in, ws, dtype, s);
+    }
+    if (arch == GRAPPA_GCN && (flags & GRAPPA_LAYER_INPUT)) {
+        GRAPPA_ARG(!dz_in && !(flags & 3u) && saved, GRAPPA_E_ARG,
+                   "grappa_layer_bwd_ex: GRAPPA_LAYER_INPUT takes no dz_in, no normalised flags, and the "
+                   "forward's `saved`");
+        GemmTNArgs t;
+        t.M = I.n_core; t.K1 = f_in; t.N = f_out; t.A1 = saved; t.B = dz_out; t.C = dw;
+        t.ws = carve(part, arch, f_in, f_out, dtype, ws).splitk;
+        return gemm_tn(ctx, t, dtype, s);
     }
     WsLayout L = carve(part, arch, f_in, f_out, dtype, ws);
     if (arch == GRAPPA_GCN && dz_in && flags == 0 && !part->halo && spmm_mm_supported(part, f_out, f_in, dtype)) {

@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import (BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, F32, LAYER_NODE_LEVEL, Context, Part,
+from . import (BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, F32, LAYER_INPUT, LAYER_NODE_LEVEL, Context, Part,
                grappa_aggregate_grads, grappa_layer_bwd, grappa_layer_bwd_ex, grappa_layer_fwd_ex,
                grappa_loss, grappa_partition, grappa_repartition, layer_saved_bytes, layer_ws_bytes)
 
@@ -198,8 +198,14 @@ class Trainer:
     def _sizes(self, p):
         sp = self.spec
         ws = [layer_ws_bytes(p, sp.arch, sp.dims_pad[l], sp.dims_pad[l + 1], self.dt) for l in range(sp.depth)]
-        sv = [layer_saved_bytes(p, sp.arch, sp.dims_pad[l], sp.dims_pad[l + 1], self.dt) for l in range(sp.depth)]
+        sv = [layer_saved_bytes(p, sp.arch, sp.dims_pad[l], sp.dims_pad[l + 1], self.dt, self._input_flag(l))
+              for l in range(sp.depth)]
         return p.n_core, ws, sv
+
+    def _input_flag(self, l: int) -> int:
+        """GCN input layer: aggregate-first (GRAPPA_LAYER_INPUT), so its backward needs no
+        aggregation (R29 re-association)"""
+        return LAYER_INPUT if (l == 0 and self.spec.arch == "gcn") else 0
 
     def _alloc(self, sizes=None):
         """Activation / workspace buffers sized for the largest partition this rank owns;
@@ -239,7 +245,8 @@ class Trainer:
         nl = LAYER_NODE_LEVEL if self.corr == "node" else 0
         for l in range(L):
             grappa_layer_fwd_ex(self.ctx, part, sp.arch, dp[l], dp[l + 1], l < L - 1, H[l],
-                                self.w_views[l], H[l + 1], self.saved[l], self.ws, self.dt, nl, s)
+                                self.w_views[l], H[l + 1], self.saved[l], self.ws, self.dt,
+                                nl | self._input_flag(l), s)
         dz = self.dz[0][: n * dp[L]].view(n, dp[L])
         grappa_loss(self.ctx, part, H[L], sp.dims[L], dp[L], dz, self.loss_dev, self.dt, s)
         gcn = sp.arch == "gcn"
@@ -247,9 +254,10 @@ class Trainer:
             dz_in = self.dz[(L - l) % 2][: n * dp[l]].view(n, dp[l]) if l > 0 else None
             # GCN: gradients between layers travel pre-multiplied by N = diag(norm_gcn), so
             # every backward aggregation gathers unweighted rows (grappa_layer_bwd_ex, R29)
-            flags = nl
+            # (the aggregate-first input layer takes its dz un-normalised: no IN_NORMED into l = 0)
+            flags = nl | self._input_flag(l)
             if gcn:
-                flags |= (BWD_DZ_OUT_NORMED if l < L - 1 else 0) | (BWD_DZ_IN_NORMED if l > 0 else 0)
+                flags |= (BWD_DZ_OUT_NORMED if 0 < l < L - 1 else 0) | (BWD_DZ_IN_NORMED if l > 1 else 0)
             grappa_layer_bwd_ex(self.ctx, part, sp.arch, dp[l], dp[l + 1], l > 0, dz, H[l],
                                 self.w_views[l], self.saved[l], self.dw_views[l], dz_in, self.ws,
                                 self.dt, flags, s)

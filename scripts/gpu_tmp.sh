@@ -1,2 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_edge_cases.py -x -q > gpurun_out/r01s_edge.log 2>&1; echo "edge $?"; tail -30 gpurun_out/r01s_edge.log
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r01t_gpu.log 2>&1; echo "gpu suite $?"; tail -15 gpurun_out/r01t_gpu.log
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/r01t_bench.json 2> gpurun_out/r01t_bench.err; echo "bench $?"; tail -2 gpurun_out/r01t_bench.err
+python -c "
+import json; d=json.load(open('gpurun_out/r01t_bench.json')); print('products', d['ms_per_step'], d['value']/1e9, d['e2e']['ms_per_step'], {k:(round(v['ms'],1),v['calls']) for k,v in d['kernels'].items()})"

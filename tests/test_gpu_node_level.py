@@ -253,3 +253,38 @@ def test_minibatch_node_level(G, ctx, dtype):
     assert err(g, g_ref) <= TOL[dtype]
     assert math.isclose(loss.item(), L_ref, rel_tol=TOL[dtype])
     assert b.factors["node"] == 1.0
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("node", [False, True])
+@pytest.mark.parametrize("f_in,f_out", [(112, 128), (16, 48)])
+def test_gcn_input_layer_aggregate_first(G, ctx, prod, dtype, node, f_in, f_out):
+    """GRAPPA_LAYER_INPUT (GCN): Z = (Ahat h_in) W with P kept in `saved`; backward dW = P^T dz
+    only (no dh_in).  Same operator as the transform-first layer (R29 re-association)."""
+    part = _part(G, ctx, prod, 8, 2, 5, dtype)
+    n = part.n_core
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    g = torch.Generator(device="cuda").manual_seed(f_in + f_out)
+    h_in = torch.randn(n, f_in, device="cuda", generator=g).to(tdt)
+    w = (torch.randn(f_in, f_out, device="cuda", generator=g) / math.sqrt(f_in)).contiguous()
+    fl = G.LAYER_INPUT | (G.LAYER_NODE_LEVEL if node else 0)
+    saved = torch.empty(G.layer_saved_bytes(part, "gcn", f_in, f_out, dtype, fl), dtype=torch.uint8, device="cuda")
+    assert saved.numel() == n * f_in * (2 if dtype == "bf16" else 4)
+    ws = torch.empty(G.layer_ws_bytes(part, "gcn", f_in, f_out, dtype), dtype=torch.uint8, device="cuda")
+    h_out = torch.empty(n, f_out, device="cuda", dtype=tdt)
+    G.grappa_layer_fwd_ex(ctx, part, "gcn", f_in, f_out, True, h_in, w, h_out, saved, ws, dtype, fl)
+    dz = (torch.randn(n, f_out, device="cuda", generator=g) * 1e-3).to(tdt)
+    dw = torch.empty_like(w)
+    G.grappa_layer_bwd_ex(ctx, part, "gcn", f_in, f_out, False, dz, h_in, w, saved, dw, None, ws, dtype, fl)
+    torch.cuda.synchronize()
+    node_w = Co.node_weights(part.d_l.cpu().numpy(), part.d_g.cpu().numpy()) if node else None
+    op = Mo.operator("gcn", part.rowptr.cpu().numpy(), part.col.cpu().numpy(), n, node_w)
+    H, W = _np(h_in), _np(w)
+    P, Z, Hn = Mo.layer_forward("gcn", op, H, [W], True, mask=(_np(h_out) > 0).astype(np.float64))
+    tol = TOL[dtype]
+    assert err(_np(h_out), Hn) <= tol
+    grads, _ = Mo.layer_backward("gcn", op, H, P, [W], _np(dz))
+    assert err(_np(dw), grads[0]) <= tol
+    with pytest.raises(G.GrappaError, match="E_ARG"):
+        G.grappa_layer_bwd_ex(ctx, part, "gcn", f_in, f_out, False, dz, h_in, w, saved, dw,
+                              torch.empty(n, f_in, device="cuda", dtype=tdt), ws, dtype, fl)
