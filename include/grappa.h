@@ -436,6 +436,8 @@ typedef enum {
  * (SpMM gather into a shared-memory tile + tcgen05 transform in the same kernel) where the
  * aggregate is the narrower side.
  * op "wide": 0 = unweighted bf16 gathers use 16-byte lanes (default), 1 = 32-byte lanes.
+ * op "tnstages": ring depth of the tcgen05 weight-gradient GEMM (default 4; 0 = fill shared memory).
+ * op "tnred": slab groups of its fixed-order split-K reduction (8 default, or 32).
  * Returns E_ARG for an unknown op. */
 grappa_status grappa_set_kernel_variant(const char* op, int variant);
 

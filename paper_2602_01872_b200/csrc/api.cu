@@ -153,6 +153,8 @@ extern "C" grappa_status grappa_set_kernel_variant(const char* op, int variant) 
     if (!strcmp(op, "spmm")) { spmm_force_warp_per_row(variant); return GRAPPA_OK; }
     if (!strcmp(op, "fuse")) { spmm_set_fuse(variant); return GRAPPA_OK; }
     if (!strcmp(op, "wide")) { spmm_set_wide(variant); return GRAPPA_OK; }
+    if (!strcmp(op, "tnstages")) { gemm_tn_set_stages(variant); return GRAPPA_OK; }
+    if (!strcmp(op, "tnred")) { gemm_tn_set_red(variant); return GRAPPA_OK; }
     set_error("grappa_set_kernel_variant: unknown op '%s'", op);
     return GRAPPA_E_ARG;
 }

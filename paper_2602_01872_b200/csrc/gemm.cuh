@@ -57,5 +57,7 @@ grappa_status gemm_tc_tn(grappa_ctx* ctx, const GemmTNArgs& g, cudaStream_t s);
 size_t gemm_tc_tn_ws_bytes(int64_t M, int K1, int K2, int N);
 // force the SIMT kernels even for bf16 (tests cross-check the two implementations)
 void gemm_force_simt(int on);
+void gemm_tn_set_stages(int v);
+void gemm_tn_set_red(int v);
 
 }  // namespace grappa

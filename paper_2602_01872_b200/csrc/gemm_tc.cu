@@ -30,7 +30,7 @@ constexpr int kNNThreads = 320;          // producer, MMA, 2 x 4 epilogue warps
 constexpr int kMaxNNStages = 8;
 constexpr int kNNStageBytes = 128 * 128;    // 128 rows x 128 B
 constexpr int kBoxBytes = 128 * 128;        // one 64-column x 128-row bf16 SW128 box
-constexpr int kTNStages = 4;
+constexpr int kTNMaxStages = 8;
 constexpr int kMaxSmem = 227 * 1024;
 // weight-gradient split plan: a fixed CTA budget (= B200 SM count) so workspace sizing and
 // the slab partition (hence the summation order) do not depend on the device queried
@@ -350,6 +350,7 @@ struct TcTN {
     int K1, K2, N, Nmma, ft1, ft2, nbox_b;
     int64_t rows_per_slab;
     int slabs;
+    int stages;         // ring depth (fills shared memory, <= kTNMaxStages)
     float* ws;          // [slabs][ftiles][128][N]
     uint32_t tmem_cols;
 };
@@ -360,8 +361,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const int a_bytes = 2 * 8192, b_bytes = p.nbox_b * 8192, st_bytes = a_bytes + b_bytes;
+    const int kTNStages = p.stages;
     uint64_t* full = (uint64_t*)(smem + (size_t)kTNStages * st_bytes);
-    uint64_t* empty = full + kTNStages;
+    uint64_t* empty = full + kTNMaxStages;
     uint64_t* tfull = empty + kTNStages;
     uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -450,13 +452,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
 }
 
-// dW[r][n] = sum_slab ws[slab][ft(r)][row(r)][n].  Block = 32 outputs x 8 slab groups: thread
-// (o, g) sums slabs g, g+8, ... in order, then the 8 group sums are added in group order --
-// a fixed summation tree, so the result is bitwise deterministic.
-__global__ void __launch_bounds__(256) k_tn_reduce(int64_t count, int N, int K1, int K2, int ft1, int ftiles,
-                                                   int slabs, const float* __restrict__ ws,
-                                                   float* __restrict__ dw) {
-    __shared__ float part[8][33];
+// dW[r][n] = sum_slab ws[slab][ft(r)][row(r)][n].  Block = 32 outputs x kRedGroups slab groups:
+// thread (o, g) sums slabs g, g + kRedGroups, ... in order (a few independent loads in flight),
+// then the group sums are added in group order -- a fixed summation tree, so the result is
+// bitwise deterministic.
+constexpr int kRedGroupsMax = 32;
+// A/B knobs (grappa_set_kernel_variant "tnstages" / "tnred"): ring depth (0 = fill shared
+// memory) and slab groups of the reduction (8 or 32)
+static int g_tn_stages = 4, g_tn_red = 8;   // 4 stages measured best (6-7 slower)
+void gemm_tn_set_stages(int v) { g_tn_stages = v; }
+void gemm_tn_set_red(int v) { g_tn_red = v == 32 ? 32 : 8; }
+template <int kRedGroups>
+__global__ void __launch_bounds__(32 * kRedGroups) k_tn_reduce(int64_t count, int N, int K1, int K2, int ft1,
+                                                               int ftiles, int slabs, const float* __restrict__ ws,
+                                                               float* __restrict__ dw) {
+    __shared__ float part[kRedGroups][33];   // kRedGroups <= kRedGroupsMax
     const int o = threadIdx.x & 31, g = threadIdx.x >> 5;
     const int64_t i = (int64_t)blockIdx.x * 32 + o;
     float s = 0.f;
@@ -465,13 +475,16 @@ __global__ void __launch_bounds__(256) k_tn_reduce(int64_t count, int N, int K1,
         int ft, row;
         if (r < K1) { ft = r / 128; row = r % 128; }
         else { ft = ft1 + (r - K1) / 128; row = (r - K1) % 128; }
-        for (int z = g; z < slabs; z += 8) s += ws[(((int64_t)z * ftiles + ft) * 128 + row) * N + n];
+        const float* src = ws + ((int64_t)ft * 128 + row) * N + n;
+        const int64_t zstride = (int64_t)ftiles * 128 * N;
+#pragma unroll 4
+        for (int z = g; z < slabs; z += kRedGroups) s += src[(int64_t)z * zstride];
     }
     part[g][o] = s;
     __syncthreads();
     if (g == 0 && i < count) {
         float t = 0.f;
-        for (int k = 0; k < 8; k++) t += part[k][o];
+        for (int k = 0; k < kRedGroups; k++) t += part[k][o];
         dw[i] = t;
     }
 }
@@ -614,7 +627,10 @@ grappa_status gemm_tc_tn(grappa_ctx* ctx, const GemmTNArgs& g, cudaStream_t s) {
     tn_plan(g.M, ftiles, kTnCtas, &p.slabs, &p.rows_per_slab);
     p.ws = g.ws;
     p.tmem_cols = pow2_cols(p.Nmma);
-    const size_t smem = 1024 + (size_t)kTNStages * (16384 + p.nbox_b * 8192) + 256;
+    const size_t st_bytes = 16384 + (size_t)p.nbox_b * 8192;
+    p.stages = (int)std::min<size_t>(kTNMaxStages, (kMaxSmem - 1024 - 512) / st_bytes);
+    if (g_tn_stages > 0) p.stages = std::min(p.stages, g_tn_stages);
+    const size_t smem = 1024 + (size_t)p.stages * st_bytes + 512;
     static bool attr = false;
     if (!attr) {
         GRAPPA_CUDA(cudaFuncSetAttribute(k_gemm_tc_tn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
@@ -624,8 +640,12 @@ grappa_status gemm_tc_tn(grappa_ctx* ctx, const GemmTNArgs& g, cudaStream_t s) {
     k_gemm_tc_tn<<<grid, kTcThreads, smem, s>>>(m1, m2, mb, p);
     GRAPPA_LAUNCHED(ctx);
     const int64_t count = (int64_t)(g.K1 + g.K2) * g.N;
-    k_tn_reduce<<<(unsigned)ceil_div(count, 32), 256, 0, s>>>(
-        count, g.N, g.K1, g.K2, p.ft1, ftiles, p.slabs, g.ws, g.C);
+    if (g_tn_red == 32)
+        k_tn_reduce<32><<<(unsigned)ceil_div(count, 32), 32 * 32, 0, s>>>(count, g.N, g.K1, g.K2, p.ft1, ftiles,
+                                                                         p.slabs, g.ws, g.C);
+    else
+        k_tn_reduce<8><<<(unsigned)ceil_div(count, 32), 32 * 8, 0, s>>>(count, g.N, g.K1, g.K2, p.ft1, ftiles,
+                                                                       p.slabs, g.ws, g.C);
     GRAPPA_LAUNCHED(ctx);
     return GRAPPA_OK;
 }
