@@ -301,6 +301,13 @@ grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part* part, grap
 grappa_status grappa_loss(grappa_ctx* ctx, const grappa_part* part, const void* logits,
                           int32_t num_classes, int32_t k_pad, void* dlogits, double* loss_dev,
                           grappa_dtype dtype, void* stream);
+/* with flags: GRAPPA_LOSS_DZ_NORMED writes N dZ (rows times norm_gcn, the GCN
+ * normalised-gradient chain of reading R29), for a last GCN layer's backward called with
+ * GRAPPA_BWD_DZ_OUT_NORMED.  The loss value is unchanged.  flags = 0 is grappa_loss. */
+#define GRAPPA_LOSS_DZ_NORMED 1u
+grappa_status grappa_loss_ex(grappa_ctx* ctx, const grappa_part* part, const void* logits,
+                             int32_t num_classes, int32_t k_pad, void* dlogits, double* loss_dev,
+                             grappa_dtype dtype, unsigned flags, void* stream);
 
 /* a7 + a8 -- coverage-corrected aggregation and optimizer step (P:291-306 eq:batch-estimator,
  * Alg. 1, "applied immediately before the all-reduce"):

@@ -260,10 +260,10 @@ def grappa_layer_bwd_ex(ctx: Context, part: Part, arch, f_in, f_out, relu_in, dz
 
 
 def grappa_loss(ctx: Context, part: Part, logits, num_classes, k_pad, dlogits, loss_dev, dtype,
-                stream=None):
-    _lib.check("grappa_loss", ctx.lib.grappa_loss(
+                stream=None, flags: int = 0):
+    _lib.check("grappa_loss_ex", ctx.lib.grappa_loss_ex(
         ctx.h, part.h, _lib.ptr(logits), num_classes, k_pad, _lib.ptr(dlogits), _lib.ptr(loss_dev),
-        dtype_code(dtype), _lib.stream_ptr(stream)))
+        dtype_code(dtype), int(flags), _lib.stream_ptr(stream)))
 
 
 def grappa_aggregate_grads(ctx: Context, part: Part | None, corr: str, grad, m_active: int, lr: float,

@@ -34,7 +34,8 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_part_upload", "grappa_layer_bwd_ex", "grappa_layer_fwd_ex",
            "grappa_minibatch_step_ex", "grappa_sample_async", "grappa_sample_wait",
            "grappa_sample_event", "grappa_repartition_ex", "grappa_part_image_bytes",
-           "grappa_part_save", "grappa_part_image_info", "grappa_part_load", "grappa_layer_saved_bytes_ex"]
+           "grappa_part_save", "grappa_part_image_info", "grappa_part_load", "grappa_layer_saved_bytes_ex",
+           "grappa_loss_ex"]
 KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5, "sample": 6}
 
 
@@ -121,6 +122,7 @@ def load(path: str = LIB_PATH):
         "grappa_layer_fwd_ex": (st, [vp, vp, ctypes.c_int, i32, i32, ctypes.c_int, vp, vp, vp, vp, vp,
                                      ctypes.c_int, ctypes.c_uint, vp]),
         "grappa_loss": (st, [vp, vp, vp, i32, i32, vp, vp, ctypes.c_int, vp]),
+        "grappa_loss_ex": (st, [vp, vp, vp, i32, i32, vp, vp, ctypes.c_int, ctypes.c_uint, vp]),
         "grappa_aggregate_grads": (st, [vp, vp, ctypes.c_int, vp, i64, i32, f32, vp, vp]),
         "grappa_check": (st, [vp, vp]),
         "grappa_launch_count": (i64, [vp]),

@@ -24,7 +24,7 @@ template <typename T>
 __global__ void __launch_bounds__(kLossThreads) k_loss(int64_t n_seeds, const int32_t* rows,
                                                        const int32_t* lidx, const int32_t* labels,
                                                        const T* logits, int K, int kpad, T* dlogits,
-                                                       double* part) {
+                                                       double* part, const float* __restrict__ rscale) {
     __shared__ double wsum[kLossThreads / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t k = (int64_t)blockIdx.x * (kLossThreads / 32) + wid;
@@ -42,7 +42,8 @@ __global__ void __launch_bounds__(kLossThreads) k_loss(int64_t n_seeds, const in
         for (int c = lane; c < K; c += 32) se += expf(lf<T>(z + c) - m);
         se = warp_sum(se);
         const float lse = m + logf(se);
-        const float inv = 1.0f / (float)n_seeds;
+        // optional row scale (GCN normalised-gradient chain, R29): dz_v * n_v
+        const float inv = (1.0f / (float)n_seeds) * (rscale ? rscale[v] : 1.f);
         for (int c = lane; c < kpad; c += 32) {
             float g = 0.f;
             if (c < K) g = (expf(lf<T>(z + c) - m) / se - (c == y ? 1.f : 0.f)) * inv;
@@ -79,7 +80,8 @@ __global__ void __launch_bounds__(256) k_loss_final(int nb, const double* part, 
 // the seed rows).  partial sums in the ctx reduction scratch (grown outside graph capture).
 grappa_status loss_rows(grappa_ctx* ctx, int64_t n_seeds, const int32_t* rows, const int32_t* lidx,
                         const int32_t* labels, int64_t n_rows, const void* logits, int K, int k_pad,
-                        void* dlogits, double* loss_dev, grappa_dtype dtype, cudaStream_t s) {
+                        void* dlogits, double* loss_dev, grappa_dtype dtype, cudaStream_t s,
+                        const float* rscale) {
     const size_t esz = dtype == GRAPPA_BF16 ? 2 : 4;
     ProfScope ps(ctx, s, GRAPPA_K_LOSS, (double)n_rows * k_pad * esz + 2.0 * n_seeds * k_pad * esz,
                  5.0 * n_seeds * K);
@@ -90,10 +92,10 @@ grappa_status loss_rows(grappa_ctx* ctx, int64_t n_seeds, const int32_t* rows, c
     if (dtype == GRAPPA_BF16)
         k_loss<__nv_bfloat16><<<(unsigned)nb, kLossThreads, 0, s>>>(
             n_seeds, rows, lidx, labels, (const __nv_bfloat16*)logits, K, k_pad, (__nv_bfloat16*)dlogits,
-            part_sums);
+            part_sums, rscale);
     else
         k_loss<float><<<(unsigned)nb, kLossThreads, 0, s>>>(n_seeds, rows, lidx, labels, (const float*)logits,
-                                                            K, k_pad, (float*)dlogits, part_sums);
+                                                            K, k_pad, (float*)dlogits, part_sums, rscale);
     GRAPPA_LAUNCHED(ctx);
     k_loss_final<<<1, 256, 0, s>>>((int)nb, part_sums, 1.0 / (double)n_seeds, loss_dev);
     GRAPPA_LAUNCHED(ctx);
@@ -107,11 +109,19 @@ using namespace grappa;
 extern "C" grappa_status grappa_loss(grappa_ctx* ctx, const grappa_part* part, const void* logits,
                                      int32_t num_classes, int32_t k_pad, void* dlogits,
                                      double* loss_dev, grappa_dtype dtype, void* stream) {
+    return grappa_loss_ex(ctx, part, logits, num_classes, k_pad, dlogits, loss_dev, dtype, 0u, stream);
+}
+
+extern "C" grappa_status grappa_loss_ex(grappa_ctx* ctx, const grappa_part* part, const void* logits,
+                                        int32_t num_classes, int32_t k_pad, void* dlogits,
+                                        double* loss_dev, grappa_dtype dtype, unsigned flags, void* stream) {
+    GRAPPA_ARG((flags & ~GRAPPA_LOSS_DZ_NORMED) == 0, GRAPPA_E_ARG, "grappa_loss_ex: flags 0x%x invalid", flags);
     GRAPPA_ARG(ctx && part && logits && dlogits && loss_dev, GRAPPA_E_ARG, "grappa_loss: null argument");
     GRAPPA_ARG(num_classes >= 1 && num_classes <= k_pad && k_pad <= kMaxKPad, GRAPPA_E_ARG,
                "grappa_loss: need 1 <= K <= k_pad <= %d", kMaxKPad);
     const grappa_part_info& I = part->info;
     GRAPPA_ARG(I.n_seeds > 0, GRAPPA_E_EMPTY, "grappa_loss: empty seed set (S:213)");
     return loss_rows(ctx, I.n_seeds, I.seeds, nullptr, I.labels, I.n_core, logits, num_classes, k_pad,
-                     dlogits, loss_dev, dtype, (cudaStream_t)stream);
+                     dlogits, loss_dev, dtype, (cudaStream_t)stream,
+                     (flags & GRAPPA_LOSS_DZ_NORMED) ? I.norm_gcn : nullptr);
 }

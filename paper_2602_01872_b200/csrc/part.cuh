@@ -9,7 +9,8 @@ __global__ void k_gather_rows(int64_t n, int64_t row_bytes, const int32_t* __res
 // softmax-CE over explicit seed rows (loss.cu)
 grappa_status loss_rows(grappa_ctx* ctx, int64_t n_seeds, const int32_t* rows, const int32_t* lidx,
                         const int32_t* labels, int64_t n_rows, const void* logits, int K, int k_pad,
-                        void* dlogits, double* loss_dev, grappa_dtype dtype, cudaStream_t s);
+                        void* dlogits, double* loss_dev, grappa_dtype dtype, cudaStream_t s,
+                        const float* rscale = nullptr);
 }  // namespace grappa
 
 struct grappa_part {

@@ -248,8 +248,12 @@ class Trainer:
                                 self.w_views[l], H[l + 1], self.saved[l], self.ws, self.dt,
                                 nl | self._input_flag(l), s)
         dz = self.dz[0][: n * dp[L]].view(n, dp[L])
-        grappa_loss(self.ctx, part, H[L], sp.dims[L], dp[L], dz, self.loss_dev, self.dt, s)
         gcn = sp.arch == "gcn"
+        # GCN: the loss writes N dZ directly when the last layer is not the (aggregate-first)
+        # input layer, so its backward gathers unweighted rows too (R29)
+        last_normed = gcn and L > 1
+        grappa_loss(self.ctx, part, H[L], sp.dims[L], dp[L], dz, self.loss_dev, self.dt, s,
+                    flags=1 if last_normed else 0)
         for l in range(L - 1, -1, -1):
             dz_in = self.dz[(L - l) % 2][: n * dp[l]].view(n, dp[l]) if l > 0 else None
             # GCN: gradients between layers travel pre-multiplied by N = diag(norm_gcn), so
@@ -257,7 +261,7 @@ class Trainer:
             # (the aggregate-first input layer takes its dz un-normalised: no IN_NORMED into l = 0)
             flags = nl | self._input_flag(l)
             if gcn:
-                flags |= (BWD_DZ_OUT_NORMED if 0 < l < L - 1 else 0) | (BWD_DZ_IN_NORMED if l > 1 else 0)
+                flags |= (BWD_DZ_OUT_NORMED if l > 0 else 0) | (BWD_DZ_IN_NORMED if l > 1 else 0)
             grappa_layer_bwd_ex(self.ctx, part, sp.arch, dp[l], dp[l + 1], l > 0, dz, H[l],
                                 self.w_views[l], self.saved[l], self.dw_views[l], dz_in, self.ws,
                                 self.dt, flags, s)

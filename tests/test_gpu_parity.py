@@ -358,3 +358,24 @@ def test_kernel_variants_agree(G, ctx, prod, arch, op, dtype, alt):
     assert lib.grappa_set_kernel_variant(b"nope", 1) == 1
     for a, b in zip(*outs):
         assert err(a, b) <= (1e-2 if dtype == "bf16" else 1e-5)
+
+
+def test_loss_dz_normed_flag(G, ctx, prod):
+    """grappa_loss_ex(GRAPPA_LOSS_DZ_NORMED): dZ rows scaled by norm_gcn (R29 chain), same loss."""
+    part = _part(G, ctx, prod, 8, 1, 4)
+    n = part.n_core
+    g = torch.Generator(device="cuda").manual_seed(3)
+    logits = torch.randn(n, 48, device="cuda", generator=g) * 3
+    logits[:, 47:] = 0
+    dl0, dl1 = torch.empty_like(logits), torch.empty_like(logits)
+    l0 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    l1 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    G.grappa_loss(ctx, part, logits, 47, 48, dl0, l0, "f32")
+    G.grappa_loss(ctx, part, logits, 47, 48, dl1, l1, "f32", flags=1)
+    torch.cuda.synchronize()
+    assert l0.item() == l1.item()
+    ref_loss, ref_dz = Mo.loss_and_dlogits(_np(logits)[:, :47], part.labels.cpu().numpy(), part.seeds.cpu().numpy())
+    nrm = part.norm_gcn.cpu().numpy().astype(np.float64)
+    assert err(_np(dl1)[:, :47], nrm[:, None] * ref_dz) <= 1e-4
+    with pytest.raises(G.GrappaError, match="E_ARG"):
+        G.grappa_loss(ctx, part, logits, 47, 48, dl1, l1, "f32", flags=2)
