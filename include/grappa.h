@@ -8,13 +8,15 @@
  * Conventions (all entry points)
  *  - Plain C types only.  "dev" pointers are CUDA device pointers, "host" pointers are
  *    host memory.  Streams are cudaStream_t passed as void* (NULL = legacy default stream).
- *  - Tensors passed in are CALLER-OWNED; the library never frees them.  grappa_ctx and
- *    grappa_part are LIBRARY-OWNED and released by their *_destroy call.
+ *  - Tensors passed in are CALLER-OWNED; the library never frees them.  grappa_ctx,
+ *    grappa_part, grappa_shard and grappa_batch are LIBRARY-OWNED and released by their
+ *    *_destroy call.
  *  - Dense node tensors are row-major [rows x cols] with cols = the padded width given in
  *    the call (every width is a multiple of 16; padded columns must be zero on input and
  *    are kept zero on output).  Weights are fp32 row-major [f_in x f_out].
  *  - Every call enqueues on the given stream and returns without a device sync, except
- *    grappa_partition, grappa_repartition, grappa_part_query and grappa_check (documented).
+ *    grappa_partition, grappa_repartition(_ex/_shards), grappa_shard_extract,
+ *    grappa_shard_exchange, grappa_part_query and grappa_check (documented).
  *  - Argument errors are detected synchronously before anything is enqueued and return a
  *    status != GRAPPA_OK; grappa_last_error() then returns a thread-local message.  After
  *    an error the outputs are unspecified and nothing leaks.  One host thread per ctx.
@@ -172,6 +174,61 @@ grappa_status grappa_repartition_ex(grappa_ctx* ctx, const grappa_csr* g, const 
                                     grappa_part** inout, void* stream);
 grappa_status grappa_part_query(const grappa_part* part, grappa_part_info* out);
 void grappa_part_destroy(grappa_part* part);
+
+/* ---- sharded mode (a3 (i); "each chunk stored ... loaded" , §4 "at a switch,
+ * workers load the new chunk's edges", "the only data moved ... at super-epoch switches";
+ * SURVEY §8e per-super-epoch shift permutation).  Instead of replicating the global graph on
+ * every GPU, each rank keeps only the CHUNK SHARDS it owns -- the rows of one chunk: its nodes
+ * in ascending global id, their full adjacency lists (global neighbour ids, sorted), features,
+ * labels and train flags -- and at a super-epoch switch receives the swept chunk's shard from
+ * its owner (NCCL point-to-point over NVLink).  The partition is then built from the two shards
+ * (grappa_repartition_shards); it is bitwise the partition grappa_repartition builds from the
+ * replicated graph.  Only induced-core partitions (halo-1 needs non-core features). */
+typedef struct grappa_shard grappa_shard;   /* library-owned; grappa_shard_destroy */
+typedef struct {
+    int32_t chunk;              /* chunk id c                                           */
+    int32_t feat_dim;           /* padded feature width (0 = no features)               */
+    grappa_dtype dtype;         /* storage dtype of x                                   */
+    int64_t n_rows;             /* |chunk c|                                            */
+    int64_t nnz;                /* sum of the rows' global degrees                      */
+    const int32_t* ids;         /* dev [n_rows] global ids, ascending                  */
+    const int64_t* rowptr;      /* dev [n_rows+1], rowptr[0] = 0                        */
+    const int32_t* col;         /* dev [nnz] global neighbour ids, ascending per row    */
+    const void* x;              /* dev [n_rows x feat_dim]                              */
+    const int32_t* labels;      /* dev [n_rows]                                         */
+    const uint8_t* train;       /* dev [n_rows]                                         */
+} grappa_shard_info;
+/* Cut chunk `chunk`'s shard out of a global CSR (the loader step a rank runs once for every
+ * chunk it owns; the global graph may be dropped afterwards).  Inputs as grappa_repartition.
+ * *inout NULL -> new shard, else its buffers are reused.  Syncs the stream once (row count).
+ * Errors: E_ARG chunk out of range / null; E_EMPTY if the chunk has no nodes. */
+grappa_status grappa_shard_extract(grappa_ctx* ctx, const grappa_csr* g, const void* feats,
+                                   int32_t feat_dim, grappa_dtype dtype, const int32_t* chunk_of,
+                                   int32_t num_chunks, int32_t chunk, const uint8_t* train_mask,
+                                   const int32_t* labels, grappa_shard** inout, void* stream);
+grappa_status grappa_shard_query(const grappa_shard* shard, grappa_shard_info* out);
+void grappa_shard_destroy(grappa_shard* shard);
+/* One point-to-point transfer of a shard: exactly one of send / recv is non-NULL. */
+typedef struct {
+    int32_t peer;               /* the other rank (may be this rank: a self copy through NCCL) */
+    const grappa_shard* send;   /* send this shard to peer                              */
+    grappa_shard** recv;        /* receive a shard from peer into *recv (NULL -> created) */
+} grappa_shard_xfer;
+/* Collective over the ctx's NCCL communicator (ctx created with a uid, any nranks >= 1):
+ * every transfer listed on one rank must be matched by the opposite transfer on its peer, and
+ * transfers between the same two ranks must be listed in the same order on both.  Two grouped
+ * NCCL rounds: a 32-byte header per transfer (then one host sync to size the receive buffers),
+ * then the arrays (ids, rowptr, col, x, labels, train).  Errors: E_ARG no communicator / bad
+ * peer / both or neither of send, recv; E_NCCL. */
+grappa_status grappa_shard_exchange(grappa_ctx* ctx, int32_t n_xfers, const grappa_shard_xfer* xfers,
+                                    void* stream);
+/* a3 from two shards: the partition of chunk pair {base->chunk, swept->chunk} (rank table from
+ * the replicated chunk map, 4 bytes per node; rows, features, labels and train flags from the
+ * shards).  Output, syncs and errors as grappa_repartition (E_ARG if the shards hold the same
+ * chunk, their feature widths or dtypes differ, or a chunk id is out of range). */
+grappa_status grappa_repartition_shards(grappa_ctx* ctx, const grappa_shard* base, const grappa_shard* swept,
+                                        const int32_t* chunk_of, int64_t num_nodes, int32_t num_chunks,
+                                        grappa_part** inout, void* stream);
 
 /* Host-memory image of a partition's arrays (sizes as in grappa_part_info; any field may be
  * NULL = not transferred).  Used when partitions live in host memory between phases -- the

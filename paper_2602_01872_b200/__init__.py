@@ -16,7 +16,8 @@ from . import _lib
 from ._lib import (BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, CORR, F32, GAT, GCN, LAYER_INPUT, LAYER_NODE_LEVEL, SAGE,
                    GrappaError, load)
 
-__all__ = ["Context", "Part", "grappa_partition", "grappa_repartition", "grappa_layer_fwd",
+__all__ = ["Context", "Part", "Shard", "grappa_shard_extract", "grappa_shard_exchange",
+           "grappa_repartition_shards", "grappa_partition", "grappa_repartition", "grappa_layer_fwd",
            "grappa_layer_bwd", "grappa_layer_bwd_ex", "grappa_loss", "grappa_aggregate_grads", "GCN", "SAGE", "F32",
            "BF16", "CORR", "GrappaError", "load"]
 
@@ -216,6 +217,83 @@ def grappa_repartition(ctx: Context, rowptr: torch.Tensor, col: torch.Tensor, fe
         ctx.h, ctypes.byref(g), _lib.ptr(feats), fdim, dtype_code(dtype), _lib.ptr(chunk_of),
         num_chunks, base, swept, _lib.ptr(train_mask), _lib.ptr(labels),
         _lib.PART_HALO1 if halo else 0, ctypes.byref(part.h), _lib.stream_ptr(stream)))
+    return part.refresh()
+
+
+class Shard:
+    """grappa_shard handle (one chunk's rows, sharded mode) + views of its device arrays."""
+
+    def __init__(self):
+        self.h = ctypes.c_void_p()
+        self.info = _lib.ShardInfo()
+
+    def refresh(self):
+        _lib.check("grappa_shard_query", load().grappa_shard_query(self.h, ctypes.byref(self.info)))
+        I = self.info
+        n, m = I.n_rows, I.nnz
+        self.chunk, self.n_rows, self.nnz = I.chunk, n, m
+        self.ids = _view(I.ids, (n,), "<i4", self)
+        self.rowptr = _view(I.rowptr, (n + 1,), "<i8", self)
+        self.col = _view(I.col, (m,), "<i4", self)
+        self.labels = _view(I.labels, (n,), "<i4", self)
+        self.train = _view(I.train, (n,), "|u1", self)
+        if I.feat_dim:
+            if I.dtype == BF16:
+                self.x = _view(I.x, (n, I.feat_dim), "<i2", self).view(torch.bfloat16)
+            else:
+                self.x = _view(I.x, (n, I.feat_dim), "<f4", self)
+        else:
+            self.x = None
+        return self
+
+    def destroy(self):
+        if self.h:
+            load().grappa_shard_destroy(self.h)
+            self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def grappa_shard_extract(ctx: Context, rowptr: torch.Tensor, col: torch.Tensor, feats, dtype,
+                         chunk_of: torch.Tensor, num_chunks: int, chunk: int, train_mask: torch.Tensor,
+                         labels, shard: Shard | None = None, stream=None) -> Shard:
+    g = _lib.Csr(rowptr.numel() - 1, col.numel(), rowptr.data_ptr(), col.data_ptr())
+    shard = shard or Shard()
+    fdim = 0 if feats is None else feats.shape[1]
+    _lib.check("grappa_shard_extract", ctx.lib.grappa_shard_extract(
+        ctx.h, ctypes.byref(g), _lib.ptr(feats), fdim, dtype_code(dtype), _lib.ptr(chunk_of), num_chunks,
+        chunk, _lib.ptr(train_mask), _lib.ptr(labels), ctypes.byref(shard.h), _lib.stream_ptr(stream)))
+    return shard.refresh()
+
+
+def grappa_shard_exchange(ctx: Context, sends, recvs, stream=None):
+    """sends: [(peer, Shard)], recvs: [(peer, Shard)] (the receiving Shard objects are filled);
+    listed in the order both sides agree on (engine.shard_plan)."""
+    n = len(sends) + len(recvs)
+    arr = (_lib.ShardXfer * max(n, 1))()
+    k = 0
+    for peer, sh in sends:
+        arr[k] = _lib.ShardXfer(peer, sh.h.value, None)
+        k += 1
+    for peer, sh in recvs:
+        arr[k] = _lib.ShardXfer(peer, None, ctypes.addressof(sh.h))
+        k += 1
+    _lib.check("grappa_shard_exchange", ctx.lib.grappa_shard_exchange(
+        ctx.h, n, ctypes.cast(arr, ctypes.c_void_p), _lib.stream_ptr(stream)))
+    for _, sh in recvs:
+        sh.refresh()
+
+
+def grappa_repartition_shards(ctx: Context, base: Shard, swept: Shard, chunk_of: torch.Tensor, num_chunks: int,
+                              part: Part | None = None, stream=None) -> Part:
+    part = part or Part()
+    _lib.check("grappa_repartition_shards", ctx.lib.grappa_repartition_shards(
+        ctx.h, base.h, swept.h, _lib.ptr(chunk_of), chunk_of.numel(), num_chunks, ctypes.byref(part.h),
+        _lib.stream_ptr(stream)))
     return part.refresh()
 
 

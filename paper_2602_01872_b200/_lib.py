@@ -35,7 +35,8 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_minibatch_step_ex", "grappa_sample_async", "grappa_sample_wait",
            "grappa_sample_event", "grappa_repartition_ex", "grappa_part_image_bytes",
            "grappa_part_save", "grappa_part_image_info", "grappa_part_load", "grappa_layer_saved_bytes_ex",
-           "grappa_loss_ex"]
+           "grappa_loss_ex", "grappa_shard_extract", "grappa_shard_query", "grappa_shard_destroy",
+           "grappa_shard_exchange", "grappa_repartition_shards"]
 KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5, "sample": 6}
 
 
@@ -63,6 +64,17 @@ class PartInfo(ctypes.Structure):
                 ("c_resampling_hm", ctypes.c_double), ("D", ctypes.c_int64),
                 ("node_w", ctypes.c_void_p), ("n_halo", ctypes.c_int64),
                 ("t_rowptr", ctypes.c_void_p), ("t_col", ctypes.c_void_p)]
+
+
+class ShardInfo(ctypes.Structure):
+    _fields_ = [("chunk", ctypes.c_int32), ("feat_dim", ctypes.c_int32), ("dtype", ctypes.c_int),
+                ("n_rows", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("ids", ctypes.c_void_p), ("rowptr", ctypes.c_void_p), ("col", ctypes.c_void_p),
+                ("x", ctypes.c_void_p), ("labels", ctypes.c_void_p), ("train", ctypes.c_void_p)]
+
+
+class ShardXfer(ctypes.Structure):
+    _fields_ = [("peer", ctypes.c_int32), ("send", ctypes.c_void_p), ("recv", ctypes.c_void_p)]
 
 
 class PartHost(ctypes.Structure):
@@ -105,6 +117,12 @@ def load(path: str = LIB_PATH):
         "grappa_repartition_ex": (st, [vp, ctypes.POINTER(Csr), vp, i32, ctypes.c_int, vp, i32, i32,
                                        i32, vp, vp, ctypes.c_uint, ctypes.POINTER(vp), vp]),
         "grappa_part_query": (st, [vp, ctypes.POINTER(PartInfo)]),
+        "grappa_shard_extract": (st, [vp, ctypes.POINTER(Csr), vp, i32, ctypes.c_int, vp, i32, i32, vp, vp,
+                                      ctypes.POINTER(vp), vp]),
+        "grappa_shard_query": (st, [vp, ctypes.POINTER(ShardInfo)]),
+        "grappa_shard_destroy": (None, [vp]),
+        "grappa_shard_exchange": (st, [vp, i32, vp, vp]),
+        "grappa_repartition_shards": (st, [vp, vp, vp, vp, i64, i32, ctypes.POINTER(vp), vp]),
         "grappa_part_image_bytes": (sz, [vp]),
         "grappa_part_save": (st, [vp, vp, sz, vp]),
         "grappa_part_image_info": (st, [vp, ctypes.POINTER(PartInfo)]),

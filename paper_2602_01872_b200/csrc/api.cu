@@ -110,7 +110,7 @@ extern "C" grappa_status grappa_ctx_create(int device, const void* nccl_uid, int
         set_error("grappa_ctx_create: cannot allocate flag");
         return GRAPPA_E_NOMEM;
     }
-    if (nccl_uid && nranks > 1) {
+    if (nccl_uid) {   // a 1-rank communicator serves the shard exchange's self transfers
         ncclUniqueId id;
         memcpy(&id, nccl_uid, 128);
         ncclComm_t comm;
@@ -134,6 +134,8 @@ extern "C" void grappa_ctx_destroy(grappa_ctx* c) {
     c->red_ws.release();
     c->small.release();
     c->rp_ws.release();
+    c->sh_ws.release();
+    c->xf_hdr.release();
     for (auto& r : c->prof) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);

@@ -83,6 +83,8 @@ struct grappa_ctx {
     grappa::DevBuf red_ws;       // reductions
     grappa::DevBuf small;        // small host-visible results staging (device side)
     grappa::DevBuf rp_ws;        // repartition task tables
+    grappa::DevBuf sh_ws;        // sharded repartition: merged two-shard CSR
+    grappa::DevBuf xf_hdr;       // shard exchange headers
     void* h_pinned = nullptr;    // pinned host staging (64 KB)
 };
 

@@ -11,7 +11,19 @@ grappa_status loss_rows(grappa_ctx* ctx, int64_t n_seeds, const int32_t* rows, c
                         const int32_t* labels, int64_t n_rows, const void* logits, int K, int k_pad,
                         void* dlogits, double* loss_dev, grappa_dtype dtype, cudaStream_t s,
                         const float* rscale = nullptr);
+// sharded repartition (shard.cu): merge two chunk shards into one CSR in local order (row i =
+// core row i, rank[] = the chunk-pair rank table); features / labels / train flags follow
+grappa_status shard_merge(grappa_ctx* ctx, const grappa_shard* sa, const grappa_shard* sb, const int32_t* rank,
+                          int64_t n_core, int64_t* m_src, int32_t* m_deg, int64_t* m_rowptr, int32_t* m_col,
+                          int32_t* m_lab, uint8_t* m_tr, void* x_out, int64_t row_bytes, int64_t* d_stat,
+                          cudaStream_t s);
 }  // namespace grappa
+
+// one chunk's rows (sharded mode): ids ascending, local rowptr from 0, global neighbour ids
+struct grappa_shard {
+    grappa_shard_info info{};
+    grappa::DevBuf ids, rowptr, col, x, labels, train;
+};
 
 struct grappa_part {
     grappa_part_info info{};

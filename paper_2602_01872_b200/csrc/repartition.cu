@@ -26,6 +26,8 @@
 
 namespace grappa {
 
+static size_t al256(size_t b) { return (b + 255) / 256 * 256; }
+
 struct FlagCore {
     const int32_t* chunk_of; int32_t b, s;
     __device__ int32_t operator()(int64_t v) const {
@@ -53,7 +55,7 @@ struct WriteRowptr {
 };
 struct FlagSeed {
     const int32_t* core_global; const uint8_t* train;
-    __device__ int32_t operator()(int64_t i) const { return train[core_global[i]] != 0; }
+    __device__ int32_t operator()(int64_t i) const { return train[core_global ? core_global[i] : i] != 0; }
 };
 struct WriteCompact {
     int32_t* out; int64_t* stat; int idx;
@@ -86,7 +88,7 @@ __global__ void k_mark_halo(const int64_t* __restrict__ d_ncore, const int32_t* 
     const int64_t n = *d_ncore;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps) {
-        const int32_t v = core_global[i];
+        const int32_t v = core_global ? core_global[i] : (int32_t)i;
         for (int64_t e = g_rowptr[v] + lane; e < g_rowptr[v + 1]; e += 32) {
             const int32_t u = g_col[e];
             if (rank[u] < 0) flag[u] = 1;          // idempotent store
@@ -116,7 +118,7 @@ __global__ void k_halo_rows(int64_t n_core, int64_t n_local, const int64_t* __re
     const int64_t nnz = *d_nnz;
     for (int64_t i = n_core + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_local;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t v = core_global[i];
+        const int32_t v = core_global ? core_global[i] : (int32_t)i;
         const int32_t dg = (int32_t)(g_rowptr[v + 1] - g_rowptr[v]);
         rowptr[i + 1] = nnz;
         d_l[i] = 0;
@@ -168,7 +170,7 @@ constexpr int kTaskLen = 1024;
 struct NumTasks {
     const int32_t* core_global; const int64_t* g_rowptr;
     __device__ int32_t operator()(int64_t i) const {
-        const int32_t v = core_global[i];
+        const int32_t v = core_global ? core_global[i] : (int32_t)i;
         const int64_t d = g_rowptr[v + 1] - g_rowptr[v];
         return d > kTaskLen ? (int32_t)ceil_div(d, kTaskLen) : 1;
     }
@@ -201,7 +203,7 @@ __global__ void k_task_count(const int64_t* __restrict__ d_T, const int32_t* __r
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T; t += nwarps) {
         const int32_t i = task_row[t];
-        const int32_t v = core_global[i];
+        const int32_t v = core_global ? core_global[i] : (int32_t)i;
         const int64_t e0 = g_rowptr[v] + (t - task_off[i]) * (int64_t)kTaskLen;
         const int64_t e1 = min(g_rowptr[v + 1], e0 + kTaskLen);
         int32_t cnt = 0;
@@ -223,7 +225,7 @@ __global__ void k_row_finalize(int64_t n_core, const int32_t* __restrict__ task_
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_core;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t a = task_out[task_off[i]], b = task_out[task_off[i + 1]];
-        const int32_t v = core_global[i];
+        const int32_t v = core_global ? core_global[i] : (int32_t)i;
         const int32_t cnt = (int32_t)(b - a);
         rowptr[i] = a;
         if (i == n_core - 1) rowptr[n_core] = b;
@@ -253,7 +255,7 @@ __global__ void k_task_fill(const int64_t* __restrict__ d_T, const int32_t* __re
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T; t += nwarps) {
         const int32_t i = task_row[t];
-        const int32_t v = core_global[i];
+        const int32_t v = core_global ? core_global[i] : (int32_t)i;
         const int64_t e0 = g_rowptr[v] + (t - task_off[i]) * (int64_t)kTaskLen;
         const int64_t e1 = min(g_rowptr[v + 1], e0 + kTaskLen);
         int64_t out = task_out[t];
@@ -474,14 +476,11 @@ extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g
                                  train_mask, labels, 0u, inout, stream);
 }
 
-extern "C" grappa_status grappa_repartition_ex(grappa_ctx* ctx, const grappa_csr* g, const void* feats,
-                                               int32_t feat_dim, grappa_dtype dtype,
-                                               const int32_t* chunk_of, int32_t num_chunks,
-                                               int32_t base, int32_t swept, const uint8_t* train_mask,
-                                               const int32_t* labels, unsigned flags,
-                                               grappa_part** inout, void* stream) {
-    GRAPPA_ARG(ctx && g && chunk_of && train_mask && inout, GRAPPA_E_ARG,
-               "grappa_repartition: null argument");
+static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const void* feats,
+                                 int32_t feat_dim, grappa_dtype dtype, const int32_t* chunk_of,
+                                 int32_t num_chunks, int32_t base, int32_t swept, const uint8_t* train_mask,
+                                 const int32_t* labels, unsigned flags, const grappa_shard* sa,
+                                 const grappa_shard* sb, grappa_part** inout, cudaStream_t s) {
     GRAPPA_ARG((flags & ~GRAPPA_PART_HALO1) == 0, GRAPPA_E_ARG, "grappa_repartition_ex: flags 0x%x invalid",
                flags);
     GRAPPA_ARG(base != swept, GRAPPA_E_ARG, "grappa_repartition: base == swept (S:139)");
@@ -492,7 +491,6 @@ extern "C" grappa_status grappa_repartition_ex(grappa_ctx* ctx, const grappa_csr
     GRAPPA_ARG(g->num_nodes > 0 && g->num_nodes < (1ll << 31), GRAPPA_E_ARG,
                "grappa_repartition: num_nodes out of int32 range");
     const bool halo = flags & GRAPPA_PART_HALO1;
-    cudaStream_t s = (cudaStream_t)stream;
     ProfScope ps(ctx, s, GRAPPA_K_REPART, 0.0, 0.0);
     grappa_part* p = *inout ? *inout : new grappa_part();
     const int64_t N = g->num_nodes;
@@ -538,6 +536,34 @@ extern "C" grappa_status grappa_repartition_ex(grappa_ctx* ctx, const grappa_csr
     }
     const int64_t n_core = cnt2[0], n_halo = cnt2[6], n_local = n_core + n_halo;
     GRAPPA_ARG(n_core > 0, fail(GRAPPA_E_EMPTY), "grappa_repartition: empty partition");
+    // Source rows.  Replicated: row v of the global CSR for core row i (v = core_global[i]);
+    // sharded: the two shards merged into one CSR in local order (row i = core row i).
+    const int32_t* srow = (const int32_t*)p->core_global.p;
+    const int64_t* G_rowptr = g->rowptr;
+    const int32_t* G_col = g->col;
+    int64_t G_nnz = g->nnz;
+    const int32_t* G_labels = labels;
+    const uint8_t* G_train = train_mask;
+    const int64_t esz = dtype == GRAPPA_BF16 ? 2 : 4;
+    if (sa) {
+        G_nnz = sa->info.nnz + sb->info.nnz;
+        const size_t a_src = al256((size_t)n_core * 8), a_deg = al256((size_t)n_core * 4),
+                     a_rp = al256((size_t)(n_core + 1) * 8), a_col = al256((size_t)(G_nnz > 0 ? G_nnz : 1) * 4),
+                     a_lab = al256((size_t)n_core * 4), a_tr = al256((size_t)n_core);
+        RP_TRY(ctx->sh_ws.grow(a_src + a_deg + a_rp + a_col + a_lab + a_tr));
+        char* w = (char*)ctx->sh_ws.p;
+        int64_t* m_src = (int64_t*)w; w += a_src;
+        int32_t* m_deg = (int32_t*)w; w += a_deg;
+        int64_t* m_rowptr = (int64_t*)w; w += a_rp;
+        int32_t* m_col = (int32_t*)w; w += a_col;
+        int32_t* m_lab = (int32_t*)w; w += a_lab;
+        uint8_t* m_tr = (uint8_t*)w;
+        if (feats) RP_TRY(p->x.grow((size_t)n_core * feat_dim * esz));
+        RP_TRY(shard_merge(ctx, sa, sb, rank, n_core, m_src, m_deg, m_rowptr, m_col, m_lab, m_tr,
+                           feats ? p->x.p : nullptr, feat_dim * esz, d_stat, s));
+        srow = nullptr;
+        G_rowptr = m_rowptr; G_col = m_col; G_labels = m_lab; G_train = m_tr;
+    }
     // 2. per-row counts (core rows from their global rows; halo rows are empty)
     RP_TRY(p->d_l.grow(n_local * 4));
     RP_TRY(p->d_g.grow(n_local * 4));
@@ -551,7 +577,7 @@ extern "C" grappa_status grappa_repartition_ex(grappa_ctx* ctx, const grappa_csr
     rp_grid(ctx, n_local, 256, &grid);
     // task workspace: T <= n_core + nnz_global / kTaskLen + 1 (upper bound; the exact T stays
     // on the device and the task kernels grid-stride up to it -- no host sync needed)
-    const int64_t T_max = n_core + g->nnz / kTaskLen + 1;
+    const int64_t T_max = n_core + G_nnz / kTaskLen + 1;
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     const size_t off_b = al((size_t)(n_core + 1) * 4), row_b = al((size_t)T_max * 4),
                  cnt_b = al((size_t)T_max * 4), out_b = al((size_t)(T_max + 1) * 8);
@@ -561,15 +587,15 @@ extern "C" grappa_status grappa_repartition_ex(grappa_ctx* ctx, const grappa_csr
     int32_t* tcount = (int32_t*)((char*)ctx->rp_ws.p + off_b + row_b);
     int64_t* task_out = (int64_t*)((char*)ctx->rp_ws.p + off_b + row_b + cnt_b);
     const int32_t* core_global = (const int32_t*)p->core_global.p;
-    RP_TRY(device_scan(ctx, NumTasks{core_global, g->rowptr}, n_core,
+    RP_TRY(device_scan(ctx, NumTasks{srow, G_rowptr}, n_core,
                        WriteTasks{task_off, task_row, d_stat}, s));
     const unsigned tgrid = (unsigned)ctx->sm_count * 16;
-    k_task_count<<<tgrid, 256, 0, s>>>(d_stat + 5, task_row, task_off, core_global, g->rowptr, g->col,
+    k_task_count<<<tgrid, 256, 0, s>>>(d_stat + 5, task_row, task_off, srow, G_rowptr, G_col,
                                         rank, tcount);
     GRAPPA_LAUNCHED(ctx);
     // 3. scans: task outputs (= local col offsets, total = nnz), then per-row finalize
     RP_TRY(device_scan(ctx, ReadTcount{tcount, d_stat + 5}, T_max, WriteTaskOut{task_out, d_stat}, s));
-    k_row_finalize<<<grid, 256, 0, s>>>(n_core, task_off, task_out, core_global, g->rowptr, labels,
+    k_row_finalize<<<grid, 256, 0, s>>>(n_core, task_off, task_out, srow, G_rowptr, G_labels,
                                          (int64_t*)p->rowptr.p, (int32_t*)p->d_l.p, (int32_t*)p->d_g.p,
                                          (float*)p->norm_gcn.p, (float*)p->norm_sage.p,
                                          (float*)p->node_w.p, n_local, (int32_t*)p->labels.p);
@@ -581,7 +607,7 @@ extern "C" grappa_status grappa_repartition_ex(grappa_ctx* ctx, const grappa_csr
                                           (float*)p->node_w.p, (int32_t*)p->labels.p);
         GRAPPA_LAUNCHED(ctx);
     }
-    RP_TRY(device_scan(ctx, FlagSeed{(int32_t*)p->core_global.p, train_mask}, n_core,
+    RP_TRY(device_scan(ctx, FlagSeed{srow, G_train}, n_core,
                        WriteCompact{(int32_t*)p->seeds.p, d_stat, 2}, s));
     int64_t st[3];
     if (cudaMemcpyAsync(st, d_stat, 3 * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
@@ -594,12 +620,11 @@ extern "C" grappa_status grappa_repartition_ex(grappa_ctx* ctx, const grappa_csr
                "grappa_repartition: partition (%d,%d) has no seeds (S:213)", base, swept);
     // 4. fill
     RP_TRY(p->col.grow((size_t)(nnz > 0 ? nnz : 1) * 4));
-    k_task_fill<<<tgrid, 256, 0, s>>>(d_stat + 5, task_row, task_off, task_out, core_global, g->rowptr,
-                                       g->col, rank, (int32_t*)p->col.p);
+    k_task_fill<<<tgrid, 256, 0, s>>>(d_stat + 5, task_row, task_off, task_out, srow, G_rowptr,
+                                       G_col, rank, (int32_t*)p->col.p);
     GRAPPA_LAUNCHED(ctx);
     // 5. features (core and halo rows)
-    const int64_t esz = dtype == GRAPPA_BF16 ? 2 : 4;
-    if (feats) {
+    if (feats && !sa) {
         RP_TRY(p->x.grow((size_t)n_local * feat_dim * esz));
         k_gather_rows<<<grid, 256, 0, s>>>(n_local, feat_dim * esz, (int32_t*)p->core_global.p,
                                            (const uint4*)feats, (uint4*)p->x.p);
@@ -696,6 +721,36 @@ extern "C" grappa_status grappa_repartition_ex(grappa_ctx* ctx, const grappa_csr
 #undef RP_TRY
 }
 
+extern "C" grappa_status grappa_repartition_ex(grappa_ctx* ctx, const grappa_csr* g, const void* feats,
+                                               int32_t feat_dim, grappa_dtype dtype,
+                                               const int32_t* chunk_of, int32_t num_chunks,
+                                               int32_t base, int32_t swept, const uint8_t* train_mask,
+                                               const int32_t* labels, unsigned flags,
+                                               grappa_part** inout, void* stream) {
+    GRAPPA_ARG(ctx && g && chunk_of && train_mask && inout, GRAPPA_E_ARG,
+               "grappa_repartition: null argument");
+    return repart_impl(ctx, g, feats, feat_dim, dtype, chunk_of, num_chunks, base, swept, train_mask, labels,
+                       flags, nullptr, nullptr, inout, (cudaStream_t)stream);
+}
+
+extern "C" grappa_status grappa_repartition_shards(grappa_ctx* ctx, const grappa_shard* base,
+                                                   const grappa_shard* swept, const int32_t* chunk_of,
+                                                   int64_t num_nodes, int32_t num_chunks, grappa_part** inout,
+                                                   void* stream) {
+    GRAPPA_ARG(ctx && base && swept && chunk_of && inout, GRAPPA_E_ARG,
+               "grappa_repartition_shards: null argument");
+    const grappa_shard_info &A = base->info, &B = swept->info;
+    GRAPPA_ARG(A.feat_dim == B.feat_dim && (A.feat_dim == 0 || A.dtype == B.dtype), GRAPPA_E_ARG,
+               "grappa_repartition_shards: shards differ in feature width or dtype");
+    GRAPPA_ARG(A.n_rows + B.n_rows <= num_nodes, GRAPPA_E_ARG,
+               "grappa_repartition_shards: shards larger than the graph");
+    // only num_nodes is read from the CSR descriptor in sharded mode (rank table over N)
+    grappa_csr gn{num_nodes, 0, nullptr, nullptr};
+    return repart_impl(ctx, &gn, A.feat_dim ? (const void*)A.x : nullptr, A.feat_dim, A.dtype, chunk_of,
+                       num_chunks, A.chunk, B.chunk, A.train, A.labels, 0u, base, swept, inout,
+                       (cudaStream_t)stream);
+}
+
 static grappa_status part_copy(const grappa_part* p, const grappa_part_host* h, bool to_host, cudaStream_t s) {
     const grappa_part_info& I = p->info;
     const size_t es = I.dtype == GRAPPA_BF16 ? 2 : 4;
@@ -777,7 +832,6 @@ static int part_arrays(grappa_part* p, const grappa_part_info& I, bool halo, int
     add(p->t_eid, halo ? nnz * 4 : 0);
     return k;
 }
-static size_t al256(size_t b) { return (b + 255) / 256 * 256; }
 }  // namespace
 
 extern "C" size_t grappa_part_image_bytes(const grappa_part* part) {

@@ -22,8 +22,9 @@ import numpy as np
 import torch
 
 from . import (BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, F32, LAYER_INPUT, LAYER_NODE_LEVEL, Context, Part,
-               grappa_aggregate_grads, grappa_layer_bwd, grappa_layer_bwd_ex, grappa_layer_fwd_ex,
-               grappa_loss, grappa_partition, grappa_repartition, layer_saved_bytes, layer_ws_bytes)
+               Shard, grappa_aggregate_grads, grappa_layer_bwd, grappa_layer_bwd_ex, grappa_layer_fwd_ex,
+               grappa_loss, grappa_partition, grappa_repartition, grappa_repartition_shards,
+               grappa_shard_exchange, grappa_shard_extract, layer_saved_bytes, layer_ws_bytes)
 
 
 def sweep_schedule(C: int, W: int):
@@ -61,6 +62,41 @@ def phase_plan(W: int, G: int, rank: int):
     return plan
 
 
+def shard_owner(c: int, G: int) -> int:
+    """sharded mode: chunk c's shard lives on rank c mod G (with W = C: worker w's base chunk w
+    sits on the rank that trains w, phase_plan)"""
+    return c % G
+
+
+def shard_plan(pairs, W: int, G: int):
+    """a3 (i) in sharded mode ("workers load the new chunk's edges"): per phase
+    i, the point-to-point shard transfers (chunk, src rank, dst rank) that give the worker
+    i*G + r on rank r both chunks of its pair.  One global order (phase, dst, chunk) that every
+    rank derives identically, so transfers between two ranks are listed in the same order on
+    both.  With W = C = G this is the shift permutation: rank r receives chunk (r + t) mod C
+    from rank (r + t) mod C and sends its own chunk to rank (r - t) mod C."""
+    plan = []
+    for i in range(-(-W // G)):
+        xs = []
+        for r in range(G):
+            w = i * G + r
+            if w >= W:
+                continue
+            for c in sorted(set(pairs[w])):
+                o = shard_owner(c, G)
+                if o != r:
+                    xs.append((c, o, r))
+        plan.append(xs)
+    return plan
+
+
+def shard_xfers(xs, rank: int):
+    """this rank's side of one phase of shard_plan: sends [(dst, chunk)], receives [(src, chunk)],
+    each in the plan's global order"""
+    return ([(dst, c) for (c, src, dst) in xs if src == rank],
+            [(src, c) for (c, src, dst) in xs if dst == rank])
+
+
 @dataclass
 class ModelSpec:
     arch: str            # "gcn" | "sage"
@@ -89,7 +125,8 @@ class Trainer:
     def __init__(self, ctx: Context, rowptr, col, x, labels, train_mask, spec: ModelSpec, weights,
                  num_chunks: int, chunk_seed: int, corr: str = "resampling", lr: float = 0.003,
                  repartition_every: int = 10, dtype: str = "f32", num_workers: int | None = None,
-                 stream=None, controller=None, halo: bool = False, capacity: bool = False):
+                 stream=None, controller=None, halo: bool = False, capacity: bool = False,
+                 sharded: bool = False):
         self.ctx = ctx
         self.dev = torch.device("cuda", ctx.device)
         self.stream = stream or torch.cuda.current_stream(self.dev)
@@ -108,6 +145,10 @@ class Trainer:
         # capacity mode (Alg. 1 with M < P beyond HBM): partitions live as images in
         # pinned host memory and are streamed into one of two device slots per phase
         self.capacity = capacity
+        # sharded mode (a3 (i)): keep only the owned chunk shards, exchange swept shards at switches
+        self.sharded = sharded
+        if sharded and (halo or capacity):
+            raise ValueError("sharded mode builds induced-core partitions held in HBM (no halo / capacity)")
         self.host_imgs: dict = {}
         self.img_bytes: dict = {}
         self.cap_slots = None
@@ -130,6 +171,15 @@ class Trainer:
         # a1: chunk map, once
         self.chunk_of = torch.empty(self.N, dtype=torch.int32, device=self.dev)
         self.chunk_sizes = grappa_partition(ctx, self.N, self.C, chunk_seed, self.chunk_of, self.stream)
+        self.nnz_global = int(self.col.numel())
+        if sharded:
+            # cut this rank's chunk shards out, then drop the replicated graph: from here on the
+            # rank holds its shards, the chunk map and the partitions it trains
+            self.shards = {c: grappa_shard_extract(ctx, self.rowptr, self.col, self.x, self.dt, self.chunk_of,
+                                                   self.C, c, self.train, self.labels, None, self.stream)
+                           for c in range(self.C) if shard_owner(c, self.G) == self.rank}
+            self.recv_slots = [Shard(), Shard()]
+            self.rowptr = self.col = self.x = self.labels = self.train = None
         # theta / grad: one flat fp32 buffer each -> one all-reduce per iteration
         shapes = spec.layer_shapes()
         self.theta = torch.zeros(spec.n_params(), dtype=torch.float32, device=self.dev)
@@ -158,6 +208,8 @@ class Trainer:
         pairs = self.schedule[(t - 1) % len(self.schedule)]
         if self.capacity:
             return self._repartition_to_host(t, pairs)
+        if self.sharded:
+            return self._repartition_sharded(t, pairs)
         for _, w in self.my_workers():
             if w >= self.W:
                 continue
@@ -165,6 +217,29 @@ class Trainer:
             self.parts[w] = grappa_repartition(self.ctx, self.rowptr, self.col, self.x, self.dt,
                                                self.chunk_of, self.C, b, s, self.train, self.labels,
                                                self.parts.get(w), self.stream, halo=self.halo)
+        self.t = t
+        self._alloc()
+
+    def _repartition_sharded(self, t, pairs):
+        """sharded mode: per phase, the NCCL shard transfers of shard_plan (collective over the
+        ranks that take part), then the partition from the two shards; the receive slots are
+        reused phase to phase (stream order: a phase's partition is built before the next
+        phase's transfers overwrite them)"""
+        plan = shard_plan(pairs, self.W, self.G)
+        for i, w in self.my_workers():
+            snd, rcv = shard_xfers(plan[i], self.rank)
+            sends = [(dst, self.shards[c]) for dst, c in snd]
+            recvs = [(src, self.recv_slots[k]) for k, (src, c) in enumerate(rcv)]
+            got = {c: self.recv_slots[k] for k, (src, c) in enumerate(rcv)}
+            if sends or recvs:
+                grappa_shard_exchange(self.ctx, sends, recvs, self.stream)
+            if w >= self.W:
+                continue
+            b, s = pairs[w]
+            sb = self.shards.get(b) or got[b]
+            ss = self.shards.get(s) or got[s]
+            self.parts[w] = grappa_repartition_shards(self.ctx, sb, ss, self.chunk_of, self.C, self.parts.get(w),
+                                                      self.stream)
         self.t = t
         self._alloc()
 
@@ -385,7 +460,7 @@ class Trainer:
 
     @property
     def nnz(self):
-        return int(self.col.numel())
+        return self.nnz_global
 
 
 class MinibatchTrainer(Trainer):

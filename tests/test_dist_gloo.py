@@ -155,3 +155,90 @@ def test_two_rank_controller_agrees():
             oc.observe(sum(cs) / len(cs))
         ref.append(oc.end_epoch())
     assert got[0] == ref and any(ref)
+
+
+def test_shard_plan():
+    """sharded mode (a3 (i)): every worker ends each phase holding both chunks of its pair; with
+    W = C = G the plan is the shift permutation (rank r receives chunk (r+t) mod C from its owner)"""
+    from paper_2602_01872_b200.engine import shard_owner, shard_plan, sweep_schedule
+    for C in range(2, 9):
+        for G in range(1, C + 1):
+            for W in sorted({C, max(1, C - 1)}):
+                for pairs in sweep_schedule(C, W):
+                    plan = shard_plan(pairs, W, G)
+                    assert len(plan) == -(-W // G)
+                    for i, xs in enumerate(plan):
+                        for r in range(G):
+                            w = i * G + r
+                            if w >= W:
+                                continue
+                            held = {c for c in range(C) if shard_owner(c, G) == r}
+                            held |= {c for (c, src, dst) in xs if dst == r}
+                            assert set(pairs[w]) <= held
+                        assert all(src != dst and shard_owner(c, G) == src for c, src, dst in xs)
+    for C in (2, 4, 8):
+        for t, pairs in enumerate(sweep_schedule(C, C), start=1):
+            (xs,) = shard_plan(pairs, C, C)
+            assert sorted(xs) == sorted(((r + t) % C, (r + t) % C, r) for r in range(C))
+
+
+def _shard_worker(rank, world, port, C, out):
+    """the engine's per-phase transfer lists (shard_plan / shard_xfers) driven through real gloo
+    point-to-point sends: every rank receives exactly the chunk rows its worker's pair needs"""
+    from paper_2602_01872_b200.engine import shard_owner, shard_plan, shard_xfers, sweep_schedule
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    wl, ds, _ = _setup(C)
+    chunk_of = Po.make_chunks(wl.n, C, gen.seed_of("chunks"))
+
+    def rows(c):        # a shard's ids and concatenated adjacency (host stand-in)
+        ids = np.flatnonzero(chunk_of == c)
+        return ids, np.concatenate([ds.col[ds.rowptr[v]:ds.rowptr[v + 1]] for v in ids])
+
+    owned = {c: rows(c) for c in range(C) if shard_owner(c, world) == rank}
+    ok = True
+    for pairs in sweep_schedule(C, C):
+        for i, xs in enumerate(shard_plan(pairs, C, world)):
+            snd, rcv = shard_xfers(xs, rank)
+            reqs = []
+            for dst, c in snd:
+                ids, col = owned[c]
+                bufs = [torch.tensor([c, ids.size, col.size], dtype=torch.int64),
+                        torch.from_numpy(ids.astype(np.int64)), torch.from_numpy(col.astype(np.int64))]
+                reqs += [dist.isend(b, dst) for b in bufs]
+            got = {}
+            for src, c in rcv:
+                hdr = torch.empty(3, dtype=torch.int64)
+                dist.recv(hdr, src)
+                ids = torch.empty(int(hdr[1]), dtype=torch.int64)
+                col = torch.empty(int(hdr[2]), dtype=torch.int64)
+                dist.recv(ids, src)
+                dist.recv(col, src)
+                got[int(hdr[0])] = (ids.numpy(), col.numpy())
+                ok &= int(hdr[0]) == c
+            for r in reqs:
+                r.wait()
+            w = i * world + rank
+            if w < C:
+                for c in pairs[w]:
+                    have = owned.get(c) or got.get(c)
+                    ref = rows(c)
+                    ok &= have is not None and np.array_equal(have[0], ref[0]) and np.array_equal(have[1], ref[1])
+            dist.barrier()
+    out.put((rank, bool(ok)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("C", [2, 4])
+def test_two_rank_shard_exchange(C):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, C, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    assert res == {0: True, 1: True}
