@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--capacity", action="store_true",
                     help="capacity mode: partitions streamed per phase from pinned host images")
+    ap.add_argument("--sharded", action="store_true",
+                    help="sharded mode (a3 (i)): each rank keeps its chunk shards only; swept shards "
+                         "arrive by NCCL point-to-point at super-epoch switches")
     ap.add_argument("--halo", action="store_true",
                     help="halo-1 partitions (R33) instead of induced-core")
     ap.add_argument("--variant", action="append", default=[],
@@ -276,7 +279,7 @@ def run_grappa(args):
     stream = torch.cuda.current_stream(dev)
     common = dict(corr=args.corr or wl.correction, lr=0.003, repartition_every=wl.repartition_every,
                   dtype=args.dtype, stream=stream, num_workers=wl.extra.get("workers"), halo=args.halo,
-                  capacity=args.capacity)
+                  capacity=args.capacity, sharded=args.sharded)
     if wl.extra.get("mode") == "minibatch":
         tr = MinibatchTrainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights,
                               wl.chunks, gen.seed_of("chunks"), fanouts=wl.extra["fanouts"],
@@ -386,6 +389,7 @@ def run_grappa(args):
                                         "epoch holding the repartition is the max"},
                            "l2": "inputs larger than L2 (graph+features ~1.6 GB, activations ~2.8 GB); no flush",
                            "capacity_mode": bool(args.capacity),
+                           "sharded_mode": bool(args.sharded),
                            "capacity_h2d_bytes_per_epoch": int(sum(tr.img_bytes.values())) if args.capacity else 0,
                            "parallelism": f"dp{world} (phase-parallel, gradient-only)",
                            "generate_s": round(t_gen, 1)},

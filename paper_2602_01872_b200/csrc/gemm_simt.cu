@@ -196,6 +196,7 @@ grappa_status gemm_nn(grappa_ctx* ctx, const GemmArgs& g, grappa_dtype dt, cudaS
                      (g.row_scale ? 4.0 * g.M : 0.0),
                  2.0 * g.M * g.N * K);
     if (dt == GRAPPA_BF16 && !g_force_simt && gemm_tc_nn_supported(g)) return gemm_tc_nn(ctx, g, s);
+    if (dt == GRAPPA_F32 && !g_force_simt && gemm_x3_nn_supported(g)) return gemm_x3_nn(ctx, g, s);
     if (dt == GRAPPA_F32 && g_force_simt != 2 && sgemm_supported(g.K1, g.K2, g.N)) return sgemm_nn(ctx, g, s);
     dim3 grid((unsigned)ceil_div(g.M, BM), (unsigned)ceil_div(g.N, BN));
     if (dt == GRAPPA_BF16) k_gemm_nn<__nv_bfloat16><<<grid, 256, 0, s>>>(g);

@@ -67,8 +67,12 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: 
 // Stage the fp32 weights once per CTA as the bf16 B operand: [kb][N rows][64 k] K-major,
 // SWIZZLE_128B, k >= K zero.  Reads are coalesced float4 rows of W (W [Kt x N]) or of W^T
 // (b_trans: W stored [N x Kt]); W1 rows [0, K1) fill k-blocks [0, kb1), rows [K1, Kt) the rest.
+// part = 1 stages the bf16 residual lo = bf16(w - bf16(w)) instead (split-fp32 GEMM below).
+__device__ __forceinline__ float wpart(float v, int part) {
+    return part ? v - __bfloat162float(__float2bfloat16_rn(v)) : v;
+}
 __device__ __forceinline__ void stage_weights(uint8_t* sB, const float* __restrict__ B, int K1, int K2, int N,
-                                              int kb1, int kbt, int b_trans) {
+                                              int kb1, int kbt, int b_trans, int part = 0) {
     const int Kt = K1 + K2;
     uint4* z = reinterpret_cast<uint4*>(sB);
     for (int i = threadIdx.x; i < kbt * N * 8; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
@@ -85,7 +89,7 @@ __device__ __forceinline__ void stage_weights(uint8_t* sB, const float* __restri
             int kb, kk;
             slot(kg, kb, kk);
             uint8_t* base = sB + (size_t)kb * N * 128 + (kk & 7) * 2;
-            const float v[4] = {f.x, f.y, f.z, f.w};
+            const float v[4] = {wpart(f.x, part), wpart(f.y, part), wpart(f.z, part), wpart(f.w, part)};
 #pragma unroll
             for (int j = 0; j < 4; j++)
                 *reinterpret_cast<__nv_bfloat16*>(base + tc::sw128_off(c + j, kk >> 3)) = __float2bfloat16_rn(v[j]);
@@ -98,8 +102,10 @@ __device__ __forceinline__ void stage_weights(uint8_t* sB, const float* __restri
             const float4 b = __ldg(reinterpret_cast<const float4*>(B + (int64_t)n * Kt + kg + 4));
             int kb, kk;
             slot(kg, kb, kk);
-            __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x, a.y), h1 = __floats2bfloat162_rn(a.z, a.w);
-            __nv_bfloat162 h2 = __floats2bfloat162_rn(b.x, b.y), h3 = __floats2bfloat162_rn(b.z, b.w);
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(wpart(a.x, part), wpart(a.y, part)),
+                           h1 = __floats2bfloat162_rn(wpart(a.z, part), wpart(a.w, part));
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(wpart(b.x, part), wpart(b.y, part)),
+                           h3 = __floats2bfloat162_rn(wpart(b.z, part), wpart(b.w, part));
             uint4 o;
             o.x = *reinterpret_cast<uint32_t*>(&h0); o.y = *reinterpret_cast<uint32_t*>(&h1);
             o.z = *reinterpret_cast<uint32_t*>(&h2); o.w = *reinterpret_cast<uint32_t*>(&h3);
@@ -339,6 +345,208 @@ __global__ void __launch_bounds__(kNNThreads, 1)
     }
     __syncthreads();
     if (warp == 1) {
+        tc::fence_after();
+        tc::tmem_dealloc(tmem, p.tmem_cols);
+    }
+}
+
+
+// ------------------------------------------------------------------------------ NN, fp32 storage
+// Split-fp32 transform for the fp32-storage path (1e-4 parity): every fp32 operand x is split
+// into x_hi = bf16(x) and x_lo = bf16(x - x_hi) (together 16 significant bits; the residual is
+// below 2^-16 |x|) and C = A_hi B_hi + A_hi B_lo + A_lo B_hi on the bf16 tensor cores (the lo*lo
+// term, ~2^-18 relative, is dropped), fp32 accumulators in TMEM.  The A split cannot be done by
+// TMA, so eight converter warps stream the fp32 rows with coalesced float4 loads (the next
+// k-block's loads in flight while the current one is converted), write hi and lo straight into
+// the K-major SWIZZLE_128B stage and arrive on the stage's mbarrier; one thread issues 3 MMAs per
+// 16-wide K step; four epilogue warps apply row scale / relu'-gate / ReLU and store fp32 rows.
+constexpr int kX3Conv = 8;                            // converter warps
+constexpr int kX3Threads = 32 * (kX3Conv + 1 + 4);    // + MMA warp + 4 epilogue warps
+constexpr int kX3StageBytes = 2 * 16384;              // hi + lo, 128 rows x 64 bf16 each
+constexpr int kX3MaxStages = 4;
+
+struct TcX3 {
+    int64_t M;
+    int K1, K2, N, kb1, kb2, n_split, stages, num_tiles, relu, b_trans;
+    const float* A1;
+    const float* A2;
+    const float* B;
+    const float* rs;
+    const float* mask;
+    float* C1;
+    float* C2;
+    uint32_t tmem_cols;
+};
+
+__global__ void __launch_bounds__(kX3Threads, 1) k_gemm_x3_nn(TcX3 p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const int kbt = p.kb1 + p.kb2;
+    uint8_t* sA = smem;
+    uint8_t* sBh = sA + (size_t)p.stages * kX3StageBytes;
+    uint8_t* sBl = sBh + (size_t)kbt * p.N * 128;
+    uint64_t* full = (uint64_t*)(sBl + (size_t)kbt * p.N * 128);
+    uint64_t* empty = full + kX3MaxStages;
+    uint64_t* tfull = empty + kX3MaxStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    stage_weights(sBh, p.B, p.K1, p.K2, p.N, p.kb1, kbt, p.b_trans, 0);
+    stage_weights(sBl, p.B, p.K1, p.K2, p.N, p.kb1, kbt, p.b_trans, 1);
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < p.stages; st++) { tc::mbar_init(&full[st], kX3Conv); tc::mbar_init(&empty[st], 1); }
+        for (int a = 0; a < 2; a++) { tc::mbar_init(&tfull[a], 1); tc::mbar_init(&tempty[a], 4); }
+        tc::mbar_fence_init();
+    }
+    if (warp == kX3Conv) tc::tmem_alloc(tmem_slot, p.tmem_cols);
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < kX3Conv) {
+        // thread t: float4 column c4 = t & 15 of the k-block, rows (t >> 4) + 16 i
+        const int t = threadIdx.x, c4 = t & 15, rsub = t >> 4;
+        const int items = ((p.num_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * kbt;
+        auto load = [&](int it, float4 (&v)[8]) {
+            const int tile = (int)blockIdx.x + (it / kbt) * (int)gridDim.x, kb = it % kbt;
+            const bool first = kb < p.kb1;
+            const float* A = first ? p.A1 : p.A2;
+            const int Ks = first ? p.K1 : p.K2;
+            const int k = (first ? kb : kb - p.kb1) * 64 + c4 * 4;
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const int64_t row = (int64_t)tile * 128 + rsub + 16 * i;
+                v[i] = (row < p.M && k < Ks) ? __ldg(reinterpret_cast<const float4*>(A + row * Ks + k))
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        };
+        float4 cur[8], nxt[8];
+        int stage = 0;
+        uint32_t phase = 0;
+        if (items > 0) load(0, cur);
+        for (int it = 0; it < items; it++) {
+            if (it + 1 < items) load(it + 1, nxt);
+            tc::mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* hi = sA + (size_t)stage * kX3StageBytes;
+            uint8_t* lo = hi + 16384;
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const int r = rsub + 16 * i;
+                const float f[4] = {cur[i].x, cur[i].y, cur[i].z, cur[i].w};
+                uint32_t h[2], l[2];
+#pragma unroll
+                for (int j = 0; j < 2; j++) {
+                    const __nv_bfloat162 bh = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+                    const float2 fh = __bfloat1622float2(bh);
+                    const __nv_bfloat162 bl = __floats2bfloat162_rn(f[2 * j] - fh.x, f[2 * j + 1] - fh.y);
+                    h[j] = *reinterpret_cast<const uint32_t*>(&bh);
+                    l[j] = *reinterpret_cast<const uint32_t*>(&bl);
+                }
+                const uint32_t off = tc::sw128_off(r, c4 >> 1) + (c4 & 1) * 8;
+                *reinterpret_cast<uint2*>(hi + off) = make_uint2(h[0], h[1]);
+                *reinterpret_cast<uint2*>(lo + off) = make_uint2(l[0], l[1]);
+            }
+            tc::fence_proxy_async();                  // generic-proxy stores -> tensor core
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&full[stage]);
+            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+#pragma unroll
+            for (int i = 0; i < 8; i++) cur[i] = nxt[i];
+        }
+    } else if (warp == kX3Conv) {
+        const uint32_t idesc = tc::idesc_bf16(128, p.N, 0, 0);
+        int stage = 0, acc = 0;
+        uint32_t phase = 0, aphase = 0;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            tc::mbar_wait(&tempty[acc], aphase ^ 1);
+            tc::fence_after();
+            const uint32_t d = tmem + (uint32_t)(acc * p.N);
+            for (int kb = 0; kb < kbt; kb++) {
+                tc::mbar_wait(&full[stage], phase);
+                tc::fence_after();
+                if (lane == 0) {
+                    const uint32_t ah = tc::smem_u32(sA + (size_t)stage * kX3StageBytes), al = ah + 16384;
+                    const uint32_t bh = tc::smem_u32(sBh + (size_t)kb * p.N * 128);
+                    const uint32_t bl = tc::smem_u32(sBl + (size_t)kb * p.N * 128);
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        tc::mma_f16(d, tc::smem_desc_sw128(al + k * 32, 0, 1024),
+                                    tc::smem_desc_sw128(bh + k * 32, 0, 1024), idesc, (kb | k) != 0);
+                        tc::mma_f16(d, tc::smem_desc_sw128(ah + k * 32, 0, 1024),
+                                    tc::smem_desc_sw128(bl + k * 32, 0, 1024), idesc, 1);
+                        tc::mma_f16(d, tc::smem_desc_sw128(ah + k * 32, 0, 1024),
+                                    tc::smem_desc_sw128(bh + k * 32, 0, 1024), idesc, 1);
+                    }
+                    tc::mma_commit(&empty[stage]);
+                }
+                __syncwarp();
+                if (++stage == p.stages) { stage = 0; phase ^= 1; }
+            }
+            if (lane == 0) tc::mma_commit(&tfull[acc]);
+            __syncwarp();
+            acc ^= 1;
+            if (acc == 0) aphase ^= 1;
+        }
+    } else {
+        const int ew = warp & 3;
+        const int r = ew * 32 + lane;
+        const uint32_t tq = (uint32_t)(ew * 32) << 16;
+        const int n2 = p.N - p.n_split;
+        int acc = 0;
+        uint32_t aphase = 0;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            const int64_t grow = (int64_t)tile * 128 + r;
+            const bool live = grow < p.M;
+            const float rsv = (p.rs && live) ? __ldg(p.rs + grow) : 1.f;
+            tc::mbar_wait(&tfull[acc], aphase);
+            tc::fence_after();
+            const uint32_t tb = tmem + (uint32_t)(acc * p.N) + tq;
+            for (int c0 = 0; c0 < p.N; c0 += 16) {
+                float v[16];
+                __syncwarp();
+                tc::tmem_ld16(tb + c0, v);
+                if (!live) continue;        // (the next iteration's __syncwarp reconverges the warp)
+                float* dst;
+                if (c0 < p.n_split) {
+                    if (p.rs) {
+#pragma unroll
+                        for (int i = 0; i < 16; i++) v[i] *= rsv;
+                    }
+                    if (p.mask) {
+                        const float4* mk = reinterpret_cast<const float4*>(p.mask + grow * p.n_split + c0);
+#pragma unroll
+                        for (int q = 0; q < 4; q++) {
+                            const float4 m = __ldg(mk + q);
+                            v[4 * q] = m.x > 0.f ? v[4 * q] : 0.f;
+                            v[4 * q + 1] = m.y > 0.f ? v[4 * q + 1] : 0.f;
+                            v[4 * q + 2] = m.z > 0.f ? v[4 * q + 2] : 0.f;
+                            v[4 * q + 3] = m.w > 0.f ? v[4 * q + 3] : 0.f;
+                        }
+                    }
+                    if (p.relu) {
+#pragma unroll
+                        for (int i = 0; i < 16; i++) v[i] = fmaxf(v[i], 0.f);
+                    }
+                    dst = p.C1 + grow * p.n_split + c0;
+                } else {
+                    dst = p.C2 + grow * n2 + (c0 - p.n_split);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) aphase ^= 1;
+        }
+    }
+    __syncthreads();
+    if (warp == kX3Conv) {
         tc::fence_after();
         tc::tmem_dealloc(tmem, p.tmem_cols);
     }
@@ -585,6 +793,42 @@ grappa_status gemm_tc_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s) {
     }
     const int grid = (int)std::min<int64_t>(p.num_tiles, ctx->sm_count);
     k_gemm_tc_nn<<<grid, kNNThreads, smem, s>>>(m1, m2, c1, c2, mk, (const __nv_bfloat16*)g.mask, p);
+    GRAPPA_LAUNCHED(ctx);
+    return GRAPPA_OK;
+}
+
+
+// split-fp32 NN (fp32 storage): resident hi + lo weights, 2..4 A stages
+static size_t x3_smem_of(int kbt, int N, int stages) {
+    return 1024 + (size_t)stages * kX3StageBytes + (size_t)2 * kbt * N * 128 + 256;
+}
+static int x3_stages(int kbt, int N) {
+    for (int st = kX3MaxStages; st >= 2; st--)
+        if (x3_smem_of(kbt, N, st) <= (size_t)kMaxSmem) return st;
+    return 0;
+}
+bool gemm_x3_nn_supported(const GemmArgs& g) {
+    const int kbt = (int)(ceil_div(g.K1, 64) + ceil_div(g.K2, 64));
+    return g.N % 16 == 0 && g.N <= 256 && g.n_split % 16 == 0 && g.K1 % 4 == 0 && g.K2 % 4 == 0 &&
+           x3_stages(kbt, g.N) >= 2 && g.M < (1ll << 31);
+}
+grappa_status gemm_x3_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s) {
+    TcX3 p;
+    p.M = g.M; p.K1 = g.K1; p.K2 = g.K2; p.N = g.N;
+    p.kb1 = (int)ceil_div(g.K1, 64); p.kb2 = (int)ceil_div(g.K2, 64);
+    p.n_split = g.n_split; p.relu = g.relu; p.b_trans = g.b_trans;
+    p.stages = x3_stages(p.kb1 + p.kb2, g.N);
+    p.num_tiles = (int)ceil_div(g.M, 128);
+    p.A1 = (const float*)g.A1; p.A2 = (const float*)g.A2; p.B = g.B; p.rs = g.row_scale;
+    p.mask = (const float*)g.mask; p.C1 = (float*)g.C1; p.C2 = (float*)g.C2;
+    p.tmem_cols = pow2_cols(2 * g.N);
+    static bool attr = false;
+    if (!attr) {
+        GRAPPA_CUDA(cudaFuncSetAttribute(k_gemm_x3_nn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+        attr = true;
+    }
+    const int grid = (int)std::min<int64_t>(p.num_tiles, ctx->sm_count);
+    k_gemm_x3_nn<<<grid, kX3Threads, x3_smem_of(p.kb1 + p.kb2, g.N, p.stages), s>>>(p);
     GRAPPA_LAUNCHED(ctx);
     return GRAPPA_OK;
 }
