@@ -212,6 +212,7 @@ grappa_status gemm_tn(grappa_ctx* ctx, const GemmTNArgs& g, grappa_dtype dt, cud
                  (double)g.M * K * es + (double)g.M * g.N * es + (double)K * g.N * 4.0,
                  2.0 * g.M * g.N * K);
     if (dt == GRAPPA_BF16 && !g_force_simt && g.M > 0 && gemm_tc_tn_supported(g)) return gemm_tc_tn(ctx, g, s);
+    if (dt == GRAPPA_F32 && !g_force_simt && g.M > 0 && gemm_x3_tn_supported(g)) return gemm_x3_tn(ctx, g, s);
     const int slabs = g.M > 0 ? slabs_for(g.M) : 1;
     const int64_t rps = g.M > 0 ? ceil_div(g.M, slabs) : 0;
     dim3 grid((unsigned)ceil_div(K, 64), (unsigned)ceil_div(g.N, 64), (unsigned)slabs);

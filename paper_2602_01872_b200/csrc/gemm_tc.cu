@@ -552,6 +552,172 @@ __global__ void __launch_bounds__(kX3Threads, 1) k_gemm_x3_nn(TcX3 p) {
     }
 }
 
+
+// Split-fp32 weight gradient (fp32 storage): dW partial of one (row slab, 128-feature tile) =
+// A_hi^T B_hi + A_hi^T B_lo + A_lo^T B_hi over the slab, both operands MN-major (node rows are
+// the reduction dimension), split by the converter warps into the SW128 boxes TMA would write
+// for bf16 (64 node rows x 64 columns per box).  Same slab plan, workspace and fixed-order
+// reduction (k_tn_reduce) as the bf16 kernel.
+struct TcX3TN {
+    int64_t M;
+    int K1, K2, N, Nmma, ft1, nbox_b, slabs, stages;
+    int64_t rows_per_slab;
+    const float* A1;
+    const float* A2;
+    const float* B;
+    float* ws;
+    uint32_t tmem_cols;
+};
+
+__device__ __forceinline__ void x3_split_store(uint8_t* hi, uint8_t* lo, int r, int c4, const float4& v) {
+    const float f[4] = {v.x, v.y, v.z, v.w};
+    uint32_t h[2], l[2];
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+        const __nv_bfloat162 bh = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+        const float2 fh = __bfloat1622float2(bh);
+        const __nv_bfloat162 bl = __floats2bfloat162_rn(f[2 * j] - fh.x, f[2 * j + 1] - fh.y);
+        h[j] = *reinterpret_cast<const uint32_t*>(&bh);
+        l[j] = *reinterpret_cast<const uint32_t*>(&bl);
+    }
+    const uint32_t off = tc::sw128_off(r, c4 >> 1) + (c4 & 1) * 8;
+    *reinterpret_cast<uint2*>(hi + off) = make_uint2(h[0], h[1]);
+    *reinterpret_cast<uint2*>(lo + off) = make_uint2(l[0], l[1]);
+}
+
+__global__ void __launch_bounds__(kX3Threads, 1) k_gemm_x3_tn(TcX3TN p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const int a_bytes = 2 * 8192, b_bytes = p.nbox_b * 8192;
+    const int st_bytes = 2 * (a_bytes + b_bytes);        // [A hi | A lo | B hi | B lo]
+    uint64_t* full = (uint64_t*)(smem + (size_t)p.stages * st_bytes);
+    uint64_t* empty = full + kX3MaxStages;
+    uint64_t* tfull = empty + kX3MaxStages;
+    uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ft = blockIdx.y;
+    const bool src1 = ft < p.ft1;
+    const float* A = src1 ? p.A1 : p.A2;
+    const int Ks = src1 ? p.K1 : p.K2;
+    const int fbase = (src1 ? ft : ft - p.ft1) * 128;
+    const int64_t r0 = (int64_t)blockIdx.x * p.rows_per_slab;
+    const int64_t r1 = min(p.M, r0 + p.rows_per_slab);
+    const int nkb = r1 > r0 ? (int)ceil_div(r1 - r0, 64) : 0;
+
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < p.stages; st++) { tc::mbar_init(&full[st], kX3Conv); tc::mbar_init(&empty[st], 1); }
+        tc::mbar_init(tfull, 1);
+        tc::mbar_fence_init();
+    }
+    if (warp == kX3Conv) tc::tmem_alloc(tmem_slot, p.tmem_cols);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < kX3Conv) {
+        const int t = threadIdx.x, c4 = t & 15, rr = t >> 4;     // rows rr + 16 i, i < 4
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int kb = 0; kb < nkb; kb++) {
+            const int64_t rowb = r0 + (int64_t)kb * 64;
+            float4 va[2][4], vb[4][4];
+#pragma unroll
+            for (int bx = 0; bx < 2; bx++) {
+                const int f = fbase + bx * 64 + c4 * 4;
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const int64_t row = rowb + rr + 16 * i;
+                    va[bx][i] = (row < r1 && f < Ks) ? __ldg(reinterpret_cast<const float4*>(A + row * Ks + f))
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+#pragma unroll
+            for (int bx = 0; bx < 4; bx++) {
+                const int n = bx * 64 + c4 * 4;
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const int64_t row = rowb + rr + 16 * i;
+                    vb[bx][i] = (bx < p.nbox_b && row < r1 && n < p.N)
+                                    ? __ldg(reinterpret_cast<const float4*>(p.B + row * p.N + n))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+            tc::mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* st = smem + (size_t)stage * st_bytes;
+#pragma unroll
+            for (int bx = 0; bx < 2; bx++)
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+                    x3_split_store(st + bx * 8192, st + a_bytes + bx * 8192, rr + 16 * i, c4, va[bx][i]);
+#pragma unroll
+            for (int bx = 0; bx < 4; bx++) {
+                if (bx >= p.nbox_b) break;
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+                    x3_split_store(st + 2 * a_bytes + bx * 8192, st + 2 * a_bytes + b_bytes + bx * 8192, rr + 16 * i,
+                                   c4, vb[bx][i]);
+            }
+            tc::fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&full[stage]);
+            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+        }
+    } else if (warp == kX3Conv) {
+        const uint32_t idesc = tc::idesc_bf16(128, p.Nmma, 1, 1);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int kb = 0; kb < nkb; kb++) {
+            tc::mbar_wait(&full[stage], phase);
+            tc::fence_after();
+            if (lane == 0) {
+                const uint32_t ah = tc::smem_u32(smem + (size_t)stage * st_bytes), al = ah + a_bytes;
+                const uint32_t bh = ah + 2 * a_bytes, bl = bh + b_bytes;
+#pragma unroll
+                for (int k = 0; k < 4; k++) {      // 16 node rows per MMA = two 8-row K groups
+                    tc::mma_f16(tmem, tc::smem_desc_sw128(al + k * 2048, 8192, 1024),
+                                tc::smem_desc_sw128(bh + k * 2048, 8192, 1024), idesc, (kb | k) != 0);
+                    tc::mma_f16(tmem, tc::smem_desc_sw128(ah + k * 2048, 8192, 1024),
+                                tc::smem_desc_sw128(bl + k * 2048, 8192, 1024), idesc, 1);
+                    tc::mma_f16(tmem, tc::smem_desc_sw128(ah + k * 2048, 8192, 1024),
+                                tc::smem_desc_sw128(bh + k * 2048, 8192, 1024), idesc, 1);
+                }
+                tc::mma_commit(&empty[stage]);
+            }
+            __syncwarp();
+            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) tc::mma_commit(tfull);
+        __syncwarp();
+    } else {
+        const int ew = warp & 3;
+        const int frow = ew * 32 + lane;
+        if (nkb > 0) {
+            tc::mbar_wait(tfull, 0);
+            tc::fence_after();
+        }
+        float* out = p.ws + (((int64_t)blockIdx.x * gridDim.y + ft) * 128 + frow) * p.N;
+        const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16);
+        for (int c0 = 0; c0 < p.N; c0 += 16) {
+            float v[16];
+            tc::tmem_ld16(tbase + c0, v);
+            if (nkb == 0) {
+#pragma unroll
+                for (int i = 0; i < 16; i++) v[i] = 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+                *reinterpret_cast<float4*>(out + c0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        }
+        tc::fence_before();
+    }
+    __syncthreads();
+    if (warp == kX3Conv) {
+        tc::fence_after();
+        tc::tmem_dealloc(tmem, p.tmem_cols);
+    }
+}
+
 // ------------------------------------------------------------------------------------- TN
 struct TcTN {
     int64_t M;
@@ -890,6 +1056,38 @@ grappa_status gemm_tc_tn(grappa_ctx* ctx, const GemmTNArgs& g, cudaStream_t s) {
     else
         k_tn_reduce<8><<<(unsigned)ceil_div(count, 32), 32 * 8, 0, s>>>(count, g.N, g.K1, g.K2, p.ft1, ftiles,
                                                                        p.slabs, g.ws, g.C);
+    GRAPPA_LAUNCHED(ctx);
+    return GRAPPA_OK;
+}
+
+
+bool gemm_x3_tn_supported(const GemmTNArgs& g) {
+    return g.N % 16 == 0 && g.N <= 256 && g.K1 % 4 == 0 && g.K2 % 4 == 0 && g.M < (1ll << 31);
+}
+grappa_status gemm_x3_tn(grappa_ctx* ctx, const GemmTNArgs& g, cudaStream_t s) {
+    TcX3TN p;
+    p.M = g.M; p.K1 = g.K1; p.K2 = g.K2; p.N = g.N;
+    p.Nmma = (int)ceil_div(g.N, 64) * 64;
+    p.nbox_b = p.Nmma / 64;
+    p.ft1 = tn_ftiles(g.K1);
+    const int ftiles = p.ft1 + (g.K2 ? tn_ftiles(g.K2) : 0);
+    tn_plan(g.M, ftiles, kTnCtas, &p.slabs, &p.rows_per_slab);
+    p.A1 = (const float*)g.A1; p.A2 = (const float*)g.A2; p.B = (const float*)g.B; p.ws = g.ws;
+    p.tmem_cols = pow2_cols(p.Nmma);
+    const size_t st_bytes = 2 * (16384 + (size_t)p.nbox_b * 8192);
+    p.stages = (int)std::min<size_t>(kX3MaxStages, (kMaxSmem - 1024 - 512) / st_bytes);
+    const size_t smem = 1024 + (size_t)p.stages * st_bytes + 512;
+    static bool attr = false;
+    if (!attr) {
+        GRAPPA_CUDA(cudaFuncSetAttribute(k_gemm_x3_tn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+        attr = true;
+    }
+    dim3 grid(p.slabs, ftiles);
+    k_gemm_x3_tn<<<grid, kX3Threads, smem, s>>>(p);
+    GRAPPA_LAUNCHED(ctx);
+    const int64_t count = (int64_t)(g.K1 + g.K2) * g.N;
+    k_tn_reduce<8><<<(unsigned)ceil_div(count, 32), 32 * 8, 0, s>>>(count, g.N, g.K1, g.K2, p.ft1, ftiles, p.slabs,
+                                                                   g.ws, g.C);
     GRAPPA_LAUNCHED(ctx);
     return GRAPPA_OK;
 }
