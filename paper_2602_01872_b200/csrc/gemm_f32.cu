@@ -1,7 +1,9 @@
 // gemm_f32.cu -- fp32 CUDA-core GEMMs for the fp32-storage (1e-4 parity) path.
 //
-// tcgen05 has no fp32-exact kind (TF32 rounds operands to 10 mantissa bits, which misses the
-// 1e-4 bar), so fp32 storage runs on FFMA: 128x128 tiles, 8x8 outputs per thread in two 4x4
+// fp32 storage normally runs on the split-fp32 tcgen05 kernels (gemm_tc.cu: bf16 hi + lo
+// operands, 3 MMAs per K step; plain TF32 rounds operands to 10 mantissa bits and misses the
+// 1e-4 bar).  These FFMA kernels serve the shapes those do not take and the cross-check
+// variant (grappa_set_kernel_variant("gemm", 1)): 128x128 tiles, 8x8 outputs per thread in two 4x4
 // quadrants (conflict-free float4 smem reads), 8-deep K slices double-buffered through shared
 // memory with the next slice prefetched into registers.
 //   k_sgemm_nn : C = [A1 | A2] * op(B)  (+ row-scale / relu'-mask / ReLU epilogue, column split)

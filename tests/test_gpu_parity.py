@@ -325,12 +325,13 @@ def test_epoch_parity(G, ctx, prod, arxiv, which, corr, epochs, rep):
 
 @pytest.mark.parametrize("arch,op,dtype,alt", [("gcn", "gemm", "bf16", 1), ("sage", "gemm", "bf16", 1),
                                                ("gcn", "gemm", "f32", 2), ("sage", "gemm", "f32", 2),
+                                               ("gcn", "gemm", "f32", 1), ("sage", "gemm", "f32", 1),
                                                ("gcn", "spmm", "bf16", 1), ("sage", "spmm", "f32", 1),
                                                ("gcn", "spmm", "bf16", 3), ("gcn", "spmm", "bf16", 2),
                                                ("gcn", "fuse", "bf16", 1), ("gcn", "wide", "bf16", 1)])
 def test_kernel_variants_agree(G, ctx, prod, arch, op, dtype, alt):
     """Alternative implementations agree on the same layer and inputs: bf16 tcgen05 GEMMs vs
-    the CUDA-core GEMMs; the row-group SpMM vs the warp-per-row SpMM; the fused
+    the CUDA-core GEMMs; the split-fp32 tcgen05 GEMMs (fp32 storage) vs the FFMA ones (1e-5); the row-group SpMM vs the warp-per-row SpMM; the fused
     aggregate->transform kernel vs SpMM + GEMM."""
     part = _part(G, ctx, prod, 8, 3, 6, dtype)
     n, f_in, f_out = part.n_core, 112, (256 if op == "fuse" else 48)
