@@ -156,6 +156,7 @@ extern "C" grappa_status grappa_set_kernel_variant(const char* op, int variant) 
     if (!strcmp(op, "fuse")) { spmm_set_fuse(variant); return GRAPPA_OK; }
     if (!strcmp(op, "wide")) { spmm_set_wide(variant); return GRAPPA_OK; }
     if (!strcmp(op, "tnstages")) { gemm_tn_set_stages(variant); return GRAPPA_OK; }
+    if (!strcmp(op, "x3dbg")) { gemm_x3_set_dbg(variant); return GRAPPA_OK; }
     if (!strcmp(op, "tnred")) { gemm_tn_set_red(variant); return GRAPPA_OK; }
     set_error("grappa_set_kernel_variant: unknown op '%s'", op);
     return GRAPPA_E_ARG;

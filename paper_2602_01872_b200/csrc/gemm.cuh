@@ -59,6 +59,7 @@ size_t gemm_tc_tn_ws_bytes(int64_t M, int K1, int K2, int N);
 bool gemm_x3_nn_supported(const GemmArgs& g);
 grappa_status gemm_x3_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s);
 bool gemm_x3_tn_supported(const GemmTNArgs& g);
+void gemm_x3_set_dbg(int v);   // timing probes only (results invalid when != 0)
 grappa_status gemm_x3_tn(grappa_ctx* ctx, const GemmTNArgs& g, cudaStream_t s);
 // force the SIMT kernels even for bf16 (tests cross-check the two implementations)
 void gemm_force_simt(int on);

@@ -65,52 +65,41 @@ __device__ __forceinline__ void bulk_wait_read() {
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 // Stage the fp32 weights once per CTA as the bf16 B operand: [kb][N rows][64 k] K-major,
-// SWIZZLE_128B, k >= K zero.  Reads are coalesced float4 rows of W (W [Kt x N]) or of W^T
-// (b_trans: W stored [N x Kt]); W1 rows [0, K1) fill k-blocks [0, kb1), rows [K1, Kt) the rest.
-// part = 1 stages the bf16 residual lo = bf16(w - bf16(w)) instead (split-fp32 GEMM below).
-__device__ __forceinline__ float wpart(float v, int part) {
-    return part ? v - __bfloat162float(__float2bfloat16_rn(v)) : v;
-}
-__device__ __forceinline__ void stage_weights(uint8_t* sB, const float* __restrict__ B, int K1, int K2, int N,
-                                              int kb1, int kbt, int b_trans, int part = 0) {
+// SWIZZLE_128B, k >= K zero; W1 rows [0, K1) fill k-blocks [0, kb1), rows [K1, Kt) the rest.
+// One thread per 16-byte chunk (operand row n, 8 consecutive k): consecutive threads take
+// consecutive n, so the reads of W [Kt x N] are coalesced (b_trans: W stored [N x Kt], 32
+// contiguous bytes per thread); 8 independent loads per chunk and 4 chunks unrolled keep the
+// prologue short (it was a serial chain of dependent loads and 2-byte scattered stores).
+// sBlo != nullptr also stages the residual lo = bf16(w - bf16(w)) (split-fp32 GEMMs).
+__device__ __forceinline__ void stage_weights(uint8_t* sB, uint8_t* sBlo, const float* __restrict__ B, int K1,
+                                              int K2, int N, int kb1, int kbt, int b_trans) {
     const int Kt = K1 + K2;
-    uint4* z = reinterpret_cast<uint4*>(sB);
-    for (int i = threadIdx.x; i < kbt * N * 8; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
-    auto slot = [&](int kg, int& kb, int& kk) {
-        if (kg < K1) { kb = kg >> 6; kk = kg & 63; }
-        else { const int kl = kg - K1; kb = kb1 + (kl >> 6); kk = kl & 63; }
-    };
-    if (!b_trans) {
-        const int n4 = N >> 2;
-        for (int idx = threadIdx.x; idx < Kt * n4; idx += blockDim.x) {
-            const int kg = idx / n4, c = (idx - kg * n4) * 4;
-            const float4 f = __ldg(reinterpret_cast<const float4*>(B + (int64_t)kg * N + c));
-            int kb, kk;
-            slot(kg, kb, kk);
-            uint8_t* base = sB + (size_t)kb * N * 128 + (kk & 7) * 2;
-            const float v[4] = {wpart(f.x, part), wpart(f.y, part), wpart(f.z, part), wpart(f.w, part)};
+    const int total = kbt * 8 * N;
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+        const int n = idx % N, kc = idx / N;
+        const int kb = kc >> 3, c8 = kc & 7;
+        int k0, kend;
+        if (kb < kb1) { k0 = kb * 64 + c8 * 8; kend = K1; }
+        else { k0 = K1 + (kb - kb1) * 64 + c8 * 8; kend = Kt; }
+        float v[8];
 #pragma unroll
-            for (int j = 0; j < 4; j++)
-                *reinterpret_cast<__nv_bfloat16*>(base + tc::sw128_off(c + j, kk >> 3)) = __float2bfloat16_rn(v[j]);
+        for (int j = 0; j < 8; j++) {
+            const int k = k0 + j;
+            v[j] = k < kend ? __ldg(b_trans ? B + (int64_t)n * Kt + k : B + (int64_t)k * N + n) : 0.f;
         }
-    } else {
-        const int k8 = Kt >> 3;
-        for (int idx = threadIdx.x; idx < N * k8; idx += blockDim.x) {
-            const int n = idx / k8, kg = (idx - n * k8) * 8;
-            const float4 a = __ldg(reinterpret_cast<const float4*>(B + (int64_t)n * Kt + kg));
-            const float4 b = __ldg(reinterpret_cast<const float4*>(B + (int64_t)n * Kt + kg + 4));
-            int kb, kk;
-            slot(kg, kb, kk);
-            __nv_bfloat162 h0 = __floats2bfloat162_rn(wpart(a.x, part), wpart(a.y, part)),
-                           h1 = __floats2bfloat162_rn(wpart(a.z, part), wpart(a.w, part));
-            __nv_bfloat162 h2 = __floats2bfloat162_rn(wpart(b.x, part), wpart(b.y, part)),
-                           h3 = __floats2bfloat162_rn(wpart(b.z, part), wpart(b.w, part));
-            uint4 o;
-            o.x = *reinterpret_cast<uint32_t*>(&h0); o.y = *reinterpret_cast<uint32_t*>(&h1);
-            o.z = *reinterpret_cast<uint32_t*>(&h2); o.w = *reinterpret_cast<uint32_t*>(&h3);
-            *reinterpret_cast<uint4*>(sB + (size_t)kb * N * 128 + tc::sw128_off(n, kk >> 3)) = o;
+        uint32_t h[4], l[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const __nv_bfloat162 bh = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+            const float2 fh = __bfloat1622float2(bh);
+            const __nv_bfloat162 bl = __floats2bfloat162_rn(v[2 * j] - fh.x, v[2 * j + 1] - fh.y);
+            h[j] = *reinterpret_cast<const uint32_t*>(&bh);
+            l[j] = *reinterpret_cast<const uint32_t*>(&bl);
         }
+        const uint32_t off = (uint32_t)kb * N * 128 + tc::sw128_off(n, c8);
+        *reinterpret_cast<uint4*>(sB + off) = make_uint4(h[0], h[1], h[2], h[3]);
+        if (sBlo) *reinterpret_cast<uint4*>(sBlo + off) = make_uint4(l[0], l[1], l[2], l[3]);
     }
 }
 
@@ -233,7 +222,7 @@ __global__ void __launch_bounds__(kNNThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     // weights -> shared memory once: bf16, K-major, SWIZZLE_128B, zero padded
-    stage_weights(sB, p.B, p.K1, p.K2, p.N, p.kb1, kbt, p.b_trans);
+    stage_weights(sB, nullptr, p.B, p.K1, p.K2, p.N, p.kb1, kbt, p.b_trans);
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < stages; s++) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
         for (int a = 0; a < 2; a++) { tc::mbar_init(&tfull[a], 1); tc::mbar_init(&tempty[a], 8); }
@@ -368,6 +357,7 @@ constexpr int kX3MaxStages = 4;
 struct TcX3 {
     int64_t M;
     int K1, K2, N, kb1, kb2, n_split, stages, num_tiles, relu, b_trans;
+    int dbg;               // diagnostic knob (timing probes only): 1 no A loads, 2 no stores, 4 no weights
     const float* A1;
     const float* A2;
     const float* B;
@@ -378,22 +368,43 @@ struct TcX3 {
     uint32_t tmem_cols;
 };
 
-__global__ void __launch_bounds__(kX3Threads, 1) k_gemm_x3_nn(TcX3 p) {
+__device__ __forceinline__ void x3_split_store(uint8_t* hi_p, uint8_t* lo_p, int r, int c4, const float4& v) {
+    const uint32_t hi = tc::smem_u32(hi_p), lo = tc::smem_u32(lo_p);
+    const float f[4] = {v.x, v.y, v.z, v.w};
+    uint32_t h[2], l[2];
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+        const __nv_bfloat162 bh = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+        const float2 fh = __bfloat1622float2(bh);
+        const __nv_bfloat162 bl = __floats2bfloat162_rn(f[2 * j] - fh.x, f[2 * j + 1] - fh.y);
+        h[j] = *reinterpret_cast<const uint32_t*>(&bh);
+        l[j] = *reinterpret_cast<const uint32_t*>(&bl);
+    }
+    const uint32_t off = tc::sw128_off(r, c4 >> 1) + (c4 & 1) * 8;
+    tc::sts_v2(hi + off, h[0], h[1]);
+    tc::sts_v2(lo + off, l[0], l[1]);
+}
+
+template <int IPR>
+__global__ void __launch_bounds__(kX3Threads, 1)
+    k_gemm_x3_nn(const __grid_constant__ CUtensorMap tmC1, const __grid_constant__ CUtensorMap tmC2, TcX3 p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const int kbt = p.kb1 + p.kb2;
     uint8_t* sA = smem;
     uint8_t* sBh = sA + (size_t)p.stages * kX3StageBytes;
     uint8_t* sBl = sBh + (size_t)kbt * p.N * 128;
-    uint64_t* full = (uint64_t*)(sBl + (size_t)kbt * p.N * 128);
+    uint8_t* sOut = sBl + (size_t)kbt * p.N * 128;              // 2 fp32 SW128 staging boxes
+    uint64_t* full = (uint64_t*)(sOut + 2 * 16384);
     uint64_t* empty = full + kX3MaxStages;
     uint64_t* tfull = empty + kX3MaxStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    stage_weights(sBh, p.B, p.K1, p.K2, p.N, p.kb1, kbt, p.b_trans, 0);
-    stage_weights(sBl, p.B, p.K1, p.K2, p.N, p.kb1, kbt, p.b_trans, 1);
+    if (!(p.dbg & 4)) {
+        stage_weights(sBh, sBl, p.B, p.K1, p.K2, p.N, p.kb1, kbt, p.b_trans);
+    }
     if (threadIdx.x == 0) {
         for (int st = 0; st < p.stages; st++) { tc::mbar_init(&full[st], kX3Conv); tc::mbar_init(&empty[st], 1); }
         for (int a = 0; a < 2; a++) { tc::mbar_init(&tfull[a], 1); tc::mbar_init(&tempty[a], 4); }
@@ -419,42 +430,41 @@ __global__ void __launch_bounds__(kX3Threads, 1) k_gemm_x3_nn(TcX3 p) {
 #pragma unroll
             for (int i = 0; i < 8; i++) {
                 const int64_t row = (int64_t)tile * 128 + rsub + 16 * i;
-                v[i] = (row < p.M && k < Ks) ? __ldg(reinterpret_cast<const float4*>(A + row * Ks + k))
-                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+                v[i] = (row < p.M && k < Ks && !(p.dbg & 1)) ? __ldg(reinterpret_cast<const float4*>(A + row * Ks + k))
+                                                             : make_float4(0.f, 0.f, 0.f, 0.f);
             }
         };
-        float4 cur[8], nxt[8];
+        // IPR k-blocks per round: all their loads are issued together (8 IPR float4 per thread,
+        // 32 IPR KB per SM in flight), converted, and published with ONE proxy fence.  The fence
+        // compiles to MEMBAR.ALL.CTA + FENCE.VIEW.ASYNC, and the MEMBAR waits for every global
+        // load still in flight -- so no load is left pending across it, and the bytes in flight
+        // per round set the bandwidth (measured: 2 per round 3.3 TB/s).
+        float4 v[IPR][8];
         int stage = 0;
         uint32_t phase = 0;
-        if (items > 0) load(0, cur);
-        for (int it = 0; it < items; it++) {
-            if (it + 1 < items) load(it + 1, nxt);
-            tc::mbar_wait(&empty[stage], phase ^ 1);
-            uint8_t* hi = sA + (size_t)stage * kX3StageBytes;
-            uint8_t* lo = hi + 16384;
+        for (int it = 0; it < items; it += IPR) {
+            const int n = min(IPR, items - it);
 #pragma unroll
-            for (int i = 0; i < 8; i++) {
-                const int r = rsub + 16 * i;
-                const float f[4] = {cur[i].x, cur[i].y, cur[i].z, cur[i].w};
-                uint32_t h[2], l[2];
+            for (int j = 0; j < IPR; j++)
+                if (j < n) load(it + j, v[j]);
+            int st[IPR];
 #pragma unroll
-                for (int j = 0; j < 2; j++) {
-                    const __nv_bfloat162 bh = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
-                    const float2 fh = __bfloat1622float2(bh);
-                    const __nv_bfloat162 bl = __floats2bfloat162_rn(f[2 * j] - fh.x, f[2 * j + 1] - fh.y);
-                    h[j] = *reinterpret_cast<const uint32_t*>(&bh);
-                    l[j] = *reinterpret_cast<const uint32_t*>(&bl);
-                }
-                const uint32_t off = tc::sw128_off(r, c4 >> 1) + (c4 & 1) * 8;
-                *reinterpret_cast<uint2*>(hi + off) = make_uint2(h[0], h[1]);
-                *reinterpret_cast<uint2*>(lo + off) = make_uint2(l[0], l[1]);
+            for (int j = 0; j < IPR; j++) {
+                if (j >= n) break;
+                st[j] = stage;
+                tc::mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* hi = sA + (size_t)stage * kX3StageBytes;
+#pragma unroll
+                for (int i = 0; i < 8; i++) x3_split_store(hi, hi + 16384, rsub + 16 * i, c4, v[j][i]);
+                if (++stage == p.stages) { stage = 0; phase ^= 1; }
             }
             tc::fence_proxy_async();                  // generic-proxy stores -> tensor core
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&full[stage]);
-            if (++stage == p.stages) { stage = 0; phase ^= 1; }
+            if (lane == 0) {
 #pragma unroll
-            for (int i = 0; i < 8; i++) cur[i] = nxt[i];
+                for (int j = 0; j < IPR; j++)
+                    if (j < n) tc::mbar_arrive(&full[st[j]]);
+            }
         }
     } else if (warp == kX3Conv) {
         const uint32_t idesc = tc::idesc_bf16(128, p.N, 0, 0);
@@ -473,10 +483,12 @@ __global__ void __launch_bounds__(kX3Threads, 1) k_gemm_x3_nn(TcX3 p) {
                     const uint32_t bl = tc::smem_u32(sBl + (size_t)kb * p.N * 128);
 #pragma unroll
                     for (int k = 0; k < 4; k++) {
+                        if (!(p.dbg & 8)) {
                         tc::mma_f16(d, tc::smem_desc_sw128(al + k * 32, 0, 1024),
                                     tc::smem_desc_sw128(bh + k * 32, 0, 1024), idesc, (kb | k) != 0);
                         tc::mma_f16(d, tc::smem_desc_sw128(ah + k * 32, 0, 1024),
                                     tc::smem_desc_sw128(bl + k * 32, 0, 1024), idesc, 1);
+                        }
                         tc::mma_f16(d, tc::smem_desc_sw128(ah + k * 32, 0, 1024),
                                     tc::smem_desc_sw128(bh + k * 32, 0, 1024), idesc, 1);
                     }
@@ -491,11 +503,15 @@ __global__ void __launch_bounds__(kX3Threads, 1) k_gemm_x3_nn(TcX3 p) {
             if (acc == 0) aphase ^= 1;
         }
     } else {
+        // epilogue: per 32-column output box, TMEM -> registers -> row scale / relu'-gate /
+        // ReLU -> SW128 fp32 staging box (double-buffered) -> TMA bulk-tensor store (coalesced;
+        // rows past M and columns past the tensor edge are clipped by the TMA unit)
         const int ew = warp & 3;
         const int r = ew * 32 + lane;
         const uint32_t tq = (uint32_t)(ew * 32) << 16;
-        const int n2 = p.N - p.n_split;
-        int acc = 0;
+        const bool leader = warp == kX3Conv + 1 && lane == 0;
+        const int nb1 = (p.n_split + 31) >> 5, nb2 = (p.N - p.n_split + 31) >> 5;
+        int acc = 0, ob = 0;
         uint32_t aphase = 0;
         for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
             const int64_t grow = (int64_t)tile * 128 + r;
@@ -504,39 +520,52 @@ __global__ void __launch_bounds__(kX3Threads, 1) k_gemm_x3_nn(TcX3 p) {
             tc::mbar_wait(&tfull[acc], aphase);
             tc::fence_after();
             const uint32_t tb = tmem + (uint32_t)(acc * p.N) + tq;
-            for (int c0 = 0; c0 < p.N; c0 += 16) {
-                float v[16];
-                __syncwarp();
-                tc::tmem_ld16(tb + c0, v);
-                if (!live) continue;        // (the next iteration's __syncwarp reconverges the warp)
-                float* dst;
-                if (c0 < p.n_split) {
-                    if (p.rs) {
+            for (int bx = 0; bx < ((p.dbg & 16) ? 0 : nb1 + nb2); bx++) {
+                const bool first = bx < nb1;
+                const int cbase = first ? bx * 32 : (bx - nb1) * 32;          // column in C1 / C2
+                const int cend = first ? min(cbase + 32, p.n_split) : min(cbase + 32, p.N - p.n_split);
+                const int coff = first ? 0 : p.n_split;                        // accumulator column
+                uint8_t* obox = sOut + (ob & 1) * 16384;
+                if (leader) bulk_wait_read1();        // the store that last used this buffer is done
+                epi_bar();
+                for (int h = 0; h < 2; h++) {
+                    const int cc = cbase + h * 16;
+                    if (cc >= cend) break;
+                    float v[16];
+                    tc::tmem_ld16(tb + coff + cc, v);
+                    if (first) {
+                        if (p.rs) {
 #pragma unroll
-                        for (int i = 0; i < 16; i++) v[i] *= rsv;
-                    }
-                    if (p.mask) {
-                        const float4* mk = reinterpret_cast<const float4*>(p.mask + grow * p.n_split + c0);
+                            for (int i = 0; i < 16; i++) v[i] *= rsv;
+                        }
+                        if (p.mask && live) {
+                            const float4* mk = reinterpret_cast<const float4*>(p.mask + grow * p.n_split + cc);
 #pragma unroll
-                        for (int q = 0; q < 4; q++) {
-                            const float4 m = __ldg(mk + q);
-                            v[4 * q] = m.x > 0.f ? v[4 * q] : 0.f;
-                            v[4 * q + 1] = m.y > 0.f ? v[4 * q + 1] : 0.f;
-                            v[4 * q + 2] = m.z > 0.f ? v[4 * q + 2] : 0.f;
-                            v[4 * q + 3] = m.w > 0.f ? v[4 * q + 3] : 0.f;
+                            for (int q = 0; q < 4; q++) {
+                                const float4 m = __ldg(mk + q);
+                                v[4 * q] = m.x > 0.f ? v[4 * q] : 0.f;
+                                v[4 * q + 1] = m.y > 0.f ? v[4 * q + 1] : 0.f;
+                                v[4 * q + 2] = m.z > 0.f ? v[4 * q + 2] : 0.f;
+                                v[4 * q + 3] = m.w > 0.f ? v[4 * q + 3] : 0.f;
+                            }
+                        }
+                        if (p.relu) {
+#pragma unroll
+                            for (int i = 0; i < 16; i++) v[i] = fmaxf(v[i], 0.f);
                         }
                     }
-                    if (p.relu) {
 #pragma unroll
-                        for (int i = 0; i < 16; i++) v[i] = fmaxf(v[i], 0.f);
-                    }
-                    dst = p.C1 + grow * p.n_split + c0;
-                } else {
-                    dst = p.C2 + grow * n2 + (c0 - p.n_split);
+                    for (int q = 0; q < 4; q++)
+                        tc::sts_v4(tc::smem_u32(obox) + tc::sw128_off(r, h * 4 + q), v[4 * q], v[4 * q + 1],
+                                   v[4 * q + 2], v[4 * q + 3]);
                 }
-#pragma unroll
-                for (int q = 0; q < 4; q++)
-                    reinterpret_cast<float4*>(dst)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                tc::fence_proxy_async();              // staged box -> visible to the TMA engine
+                epi_bar();
+                if (leader && !(p.dbg & 2)) {
+                    tma_store_2d(first ? &tmC1 : &tmC2, obox, cbase, tile * 128);
+                    bulk_commit();
+                }
+                ob++;
             }
             tc::fence_before();
             __syncwarp();
@@ -544,6 +573,7 @@ __global__ void __launch_bounds__(kX3Threads, 1) k_gemm_x3_nn(TcX3 p) {
             acc ^= 1;
             if (acc == 0) aphase ^= 1;
         }
+        if (leader) bulk_wait_read0();
     }
     __syncthreads();
     if (warp == kX3Conv) {
@@ -568,22 +598,6 @@ struct TcX3TN {
     float* ws;
     uint32_t tmem_cols;
 };
-
-__device__ __forceinline__ void x3_split_store(uint8_t* hi, uint8_t* lo, int r, int c4, const float4& v) {
-    const float f[4] = {v.x, v.y, v.z, v.w};
-    uint32_t h[2], l[2];
-#pragma unroll
-    for (int j = 0; j < 2; j++) {
-        const __nv_bfloat162 bh = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
-        const float2 fh = __bfloat1622float2(bh);
-        const __nv_bfloat162 bl = __floats2bfloat162_rn(f[2 * j] - fh.x, f[2 * j + 1] - fh.y);
-        h[j] = *reinterpret_cast<const uint32_t*>(&bh);
-        l[j] = *reinterpret_cast<const uint32_t*>(&bl);
-    }
-    const uint32_t off = tc::sw128_off(r, c4 >> 1) + (c4 & 1) * 8;
-    *reinterpret_cast<uint2*>(hi + off) = make_uint2(h[0], h[1]);
-    *reinterpret_cast<uint2*>(lo + off) = make_uint2(l[0], l[1]);
-}
 
 __global__ void __launch_bounds__(kX3Threads, 1) k_gemm_x3_tn(TcX3TN p) {
     extern __shared__ uint8_t smem_raw[];
@@ -880,13 +894,15 @@ static grappa_status get_encoder() {
 }
 
 // 2-D bf16 row-major [rows x cols] map, box {64 cols, box_rows rows}, SWIZZLE_128B
-static grappa_status make_map(CUtensorMap* m, const void* ptr, int64_t rows, int cols, int box_rows) {
+static grappa_status make_map(CUtensorMap* m, const void* ptr, int64_t rows, int cols, int box_rows,
+                              bool f32 = false) {
     GRAPPA_TRY(get_encoder());
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)(rows > 0 ? rows : 1)};
-    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * (f32 ? 4 : 2)};
+    cuuint32_t box[2] = {f32 ? 32u : 64u, (cuuint32_t)box_rows};     // 128-byte box rows
     cuuint32_t es[2] = {1, 1};
-    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+    CUresult r = g_encode(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                          const_cast<void*>(ptr), dims, strides, box, es,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
@@ -966,7 +982,7 @@ grappa_status gemm_tc_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s) {
 
 // split-fp32 NN (fp32 storage): resident hi + lo weights, 2..4 A stages
 static size_t x3_smem_of(int kbt, int N, int stages) {
-    return 1024 + (size_t)stages * kX3StageBytes + (size_t)2 * kbt * N * 128 + 256;
+    return 1024 + (size_t)stages * kX3StageBytes + (size_t)2 * kbt * N * 128 + 2 * 16384 + 256;
 }
 static int x3_stages(int kbt, int N) {
     for (int st = kX3MaxStages; st >= 2; st--)
@@ -978,8 +994,11 @@ bool gemm_x3_nn_supported(const GemmArgs& g) {
     return g.N % 16 == 0 && g.N <= 256 && g.n_split % 16 == 0 && g.K1 % 4 == 0 && g.K2 % 4 == 0 &&
            x3_stages(kbt, g.N) >= 2 && g.M < (1ll << 31);
 }
+static int g_x3_dbg = 0;
+void gemm_x3_set_dbg(int v) { g_x3_dbg = v; }
 grappa_status gemm_x3_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s) {
     TcX3 p;
+    p.dbg = g_x3_dbg;
     p.M = g.M; p.K1 = g.K1; p.K2 = g.K2; p.N = g.N;
     p.kb1 = (int)ceil_div(g.K1, 64); p.kb2 = (int)ceil_div(g.K2, 64);
     p.n_split = g.n_split; p.relu = g.relu; p.b_trans = g.b_trans;
@@ -990,11 +1009,18 @@ grappa_status gemm_x3_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s) {
     p.tmem_cols = pow2_cols(2 * g.N);
     static bool attr = false;
     if (!attr) {
-        GRAPPA_CUDA(cudaFuncSetAttribute(k_gemm_x3_nn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+        GRAPPA_CUDA(cudaFuncSetAttribute(k_gemm_x3_nn<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+        GRAPPA_CUDA(cudaFuncSetAttribute(k_gemm_x3_nn<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
         attr = true;
     }
+    CUtensorMap c1, c2;
+    GRAPPA_TRY(make_map(&c1, g.C1, g.M, g.n_split, 128, true));
+    if (g.N > g.n_split) GRAPPA_TRY(make_map(&c2, g.C2, g.M, g.N - g.n_split, 128, true));
+    else c2 = c1;
     const int grid = (int)std::min<int64_t>(p.num_tiles, ctx->sm_count);
-    k_gemm_x3_nn<<<grid, kX3Threads, x3_smem_of(p.kb1 + p.kb2, g.N, p.stages), s>>>(p);
+    const size_t smem = x3_smem_of(p.kb1 + p.kb2, g.N, p.stages);
+    if (p.stages >= 3) k_gemm_x3_nn<3><<<grid, kX3Threads, smem, s>>>(c1, c2, p);
+    else k_gemm_x3_nn<2><<<grid, kX3Threads, smem, s>>>(c1, c2, p);
     GRAPPA_LAUNCHED(ctx);
     return GRAPPA_OK;
 }
