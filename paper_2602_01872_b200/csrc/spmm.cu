@@ -541,35 +541,12 @@ __global__ void __launch_bounds__(256) k_spmm_grp16(SpmmArgs a, int G, int P) {
     epilogue<T, 1>(a, orow, orow, 2 * sub + 1, G, WV, h1);
 }
 
-// split-row combine.  Rows of <= kFixWarps segments (almost all: 2-3 segments) take one warp
-// each (k_spmm_fixup_warp, slots summed in order); longer rows (hubs) one block of kFixWarps
-// warps (k_spmm_fixup_blk): warp w sums slots s0+w, s0+w+kFixWarps, ... in order, then the
-// warp sums are added in warp order.  For <= kFixWarps segments both orders are the same sum.
+// split-row combine, one launch per SpMM call, one block per split row.  Rows of <= kFixWarps
+// segments (almost all: 2-3 segments): warp 0 sums the slots in order; longer rows (hubs): warp
+// w sums slots s0+w, s0+w+kFixWarps, ... in order, then the warp sums are added in warp order.
+// For <= kFixWarps segments both orders are the same sum.  (A separate warp-per-row launch for
+// the short rows cost one more kernel boundary per SpMM call.)
 constexpr int kFixWarps = 8;
-template <typename T>
-__global__ void __launch_bounds__(256) k_spmm_fixup_warp(SpmmArgs a, int G) {
-    constexpr int E = Vec<T>::EPV;
-    const int lane = threadIdx.x & 31;
-    const int64_t h = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (h >= a.n_heavy) return;
-    const int s0 = a.heavy_slot_off[h], s1 = a.heavy_slot_off[h + 1];
-    if (s1 - s0 > kFixWarps || lane >= G) return;
-    const int WV = G;
-    const int32_t r = a.heavy_rows[h];
-    float tot[1][E];
-#pragma unroll
-    for (int q = 0; q < E; q++) tot[0][q] = 0.f;
-    for (int sl = s0; sl < s1; sl++) {
-        const float* src = a.partial + ((int64_t)sl * WV + lane) * E;
-#pragma unroll
-        for (int q = 0; q < E; q += 4) {
-            const float4 p = *reinterpret_cast<const float4*>(src + q);
-            tot[0][q] += p.x; tot[0][q + 1] += p.y; tot[0][q + 2] += p.z; tot[0][q + 3] += p.w;
-        }
-    }
-    epilogue<T, 1>(a, r, a.out_compact ? h : r, lane, G, WV, tot);
-}
-
 template <typename T>
 __global__ void __launch_bounds__(kFixWarps * 32) k_spmm_fixup_blk(SpmmArgs a, int G) {
     constexpr int E = Vec<T>::EPV;
@@ -579,7 +556,24 @@ __global__ void __launch_bounds__(kFixWarps * 32) k_spmm_fixup_blk(SpmmArgs a, i
     const int WV = G;
     const int32_t r = a.heavy_rows[h];
     const int s0 = a.heavy_slot_off[h], s1 = a.heavy_slot_off[h + 1];
-    if (s1 - s0 <= kFixWarps) return;                  // k_spmm_fixup_warp's row
+    if (s1 - s0 <= kFixWarps) {
+        // short split row: warp 0 sums its slots in order (k_spmm_fixup_warp's sum, so one
+        // launch serves both kinds of split rows)
+        if (w != 0 || lane >= G) return;
+        float tot[1][E];
+#pragma unroll
+        for (int q = 0; q < E; q++) tot[0][q] = 0.f;
+        for (int sl = s0; sl < s1; sl++) {
+            const float* src = a.partial + ((int64_t)sl * WV + lane) * E;
+#pragma unroll
+            for (int q = 0; q < E; q += 4) {
+                const float4 p = *reinterpret_cast<const float4*>(src + q);
+                tot[0][q] += p.x; tot[0][q + 1] += p.y; tot[0][q + 2] += p.z; tot[0][q + 3] += p.w;
+            }
+        }
+        epilogue<T, 1>(a, r, a.out_compact ? h : r, lane, G, WV, tot);
+        return;
+    }
     float acc[E];
 #pragma unroll
     for (int q = 0; q < E; q++) acc[q] = 0.f;
@@ -624,8 +618,6 @@ static grappa_status launch_grp(grappa_ctx* ctx, const SpmmArgs& a, int G, cudaS
         GRAPPA_LAUNCHED(ctx);
     }
     if (a.n_heavy > 0) {
-        k_spmm_fixup_warp<T><<<(unsigned)ceil_div(a.n_heavy, 8), 256, 0, s>>>(a, G);
-        GRAPPA_LAUNCHED(ctx);
         k_spmm_fixup_blk<T><<<(unsigned)a.n_heavy, kFixWarps * 32, 0, s>>>(a, G);
         GRAPPA_LAUNCHED(ctx);
     }
@@ -655,8 +647,6 @@ static grappa_status launch_grp16(grappa_ctx* ctx, const SpmmArgs& a, int G, cud
         GRAPPA_LAUNCHED(ctx);
     }
     if (a.n_heavy > 0) {
-        k_spmm_fixup_warp<__nv_bfloat16><<<(unsigned)ceil_div(a.n_heavy, 8), 256, 0, s>>>(a, 2 * G);
-        GRAPPA_LAUNCHED(ctx);
         k_spmm_fixup_blk<__nv_bfloat16><<<(unsigned)a.n_heavy, kFixWarps * 32, 0, s>>>(a, 2 * G);
         GRAPPA_LAUNCHED(ctx);
     }
