@@ -148,6 +148,8 @@ extern "C" void grappa_ctx_destroy(grappa_ctx* c) {
 extern "C" int64_t grappa_launch_count(const grappa_ctx* c) { return c ? c->launches : 0; }
 
 namespace grappa { void spmm_force_warp_per_row(int on); }
+// 1: GCN backward runs the two separate GEMMs instead of the one-pass pair (A/B, tests)
+static int g_pair_off = 0;
 
 extern "C" grappa_status grappa_set_kernel_variant(const char* op, int variant) {
     GRAPPA_ARG(op, GRAPPA_E_ARG, "grappa_set_kernel_variant: null op");
@@ -157,6 +159,7 @@ extern "C" grappa_status grappa_set_kernel_variant(const char* op, int variant) 
     if (!strcmp(op, "wide")) { spmm_set_wide(variant); return GRAPPA_OK; }
     if (!strcmp(op, "tnstages")) { gemm_tn_set_stages(variant); return GRAPPA_OK; }
     if (!strcmp(op, "x3dbg")) { gemm_x3_set_dbg(variant); return GRAPPA_OK; }
+    if (!strcmp(op, "pair")) { g_pair_off = variant; return GRAPPA_OK; }
     if (!strcmp(op, "tnred")) { gemm_tn_set_red(variant); return GRAPPA_OK; }
     set_error("grappa_set_kernel_variant: unknown op '%s'", op);
     return GRAPPA_E_ARG;
@@ -400,6 +403,15 @@ extern "C" grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part*
         }
         a.self = 1; a.out = L.node; a.partial = L.partial;
         GRAPPA_TRY(spmm_t(ctx, part, a, dtype, s));          // transpose operator (halo-1, R33)
+        if (dz_in && dtype == GRAPPA_BF16 && !g_pair_off && gemm_tc_pair_supported(I.n_core, f_in, f_out)) {
+            // both backward GEMMs from one read of dT and h_in (dz_in with the relu' gate, dW)
+            const double M = (double)I.n_core;
+            ProfScope ps(ctx, s, GRAPPA_K_GEMM, M * (f_out + 2.0 * f_in) * 2.0 + 4.0 * f_in * f_out * 2.0 +
+                                                    (in_normed ? 4.0 * M : 0.0),
+                         4.0 * M * f_in * f_out);
+            return gemm_tc_pair(ctx, I.n_core, f_in, f_out, L.node, h_in, w, in_normed ? I.norm_gcn : nullptr,
+                                relu_in, dz_in, L.splitk, dw, s);
+        }
         // dW = h_in^T dT
         GemmTNArgs t;
         t.M = I.n_core; t.K1 = f_in; t.N = f_out; t.A1 = h_in; t.B = L.node; t.C = dw; t.ws = L.splitk;

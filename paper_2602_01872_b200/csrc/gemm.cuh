@@ -55,6 +55,12 @@ bool gemm_tc_tn_supported(const GemmTNArgs& g);
 grappa_status gemm_tc_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s);
 grappa_status gemm_tc_tn(grappa_ctx* ctx, const GemmTNArgs& g, cudaStream_t s);
 size_t gemm_tc_tn_ws_bytes(int64_t M, int K1, int K2, int N);
+// GCN backward pair in one pass over dT and h_in (bf16, tcgen05): dz_in = (dT W^T) * relu'(h_in)
+// [* rs] and dW = h_in^T dT (partials in ws, summed in CTA order).  f_in in (64, 128], f_out <= 128.
+bool gemm_tc_pair_supported(int64_t M, int f_in, int f_out);
+grappa_status gemm_tc_pair(grappa_ctx* ctx, int64_t M, int f_in, int f_out, const void* dT, const void* h,
+                           const float* W, const float* rs, int gate, void* dz_in, float* ws, float* dw,
+                           cudaStream_t s);
 // split-fp32 tcgen05 NN for fp32 storage (3 bf16 MMAs per K step; gemm_tc.cu)
 bool gemm_x3_nn_supported(const GemmArgs& g);
 grappa_status gemm_x3_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s);

@@ -340,6 +340,170 @@ __global__ void __launch_bounds__(kNNThreads, 1)
 }
 
 
+// ------------------------------------------------------------------------- backward pair (GCN)
+// One pass over a 128-row tile of dT (= Ahat dz_out) and h_in gives both backward GEMMs of a GCN
+// layer: dH = (dT W^T) * relu'(h_in) [* N] (K-major operands, accumulator double-buffered in TMEM)
+// and this CTA's partial of dW = h_in^T dT (MN-major operands read from the SAME shared-memory
+// tiles, accumulated in TMEM over all the CTA's tiles).  The separate kernels read dT twice and
+// h_in twice (once as the dW operand, once as the relu' gate); here each is read once and the
+// gate comes from the staged h tile.  Partials are summed in CTA order by k_tn_reduce.
+struct TcPair {
+    int64_t M;
+    int f_in, f_out, kbo, kbi, stages, num_tiles, nmma_w;
+    const float* W;        // [f_in x f_out] fp32 (dH = dT W^T: B operand staged K-major)
+    const float* rs;       // row scale of dH (N) or null
+    int gate;              // relu'(h_in) gate
+    float* ws;             // [grid][128][f_out] dW partials
+    uint32_t tmem_cols;
+};
+
+__global__ void __launch_bounds__(kNNThreads, 1)
+    k_gemm_tc_pair(const __grid_constant__ CUtensorMap tmT, const __grid_constant__ CUtensorMap tmH,
+                   const __grid_constant__ CUtensorMap tmC, TcPair q) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const int st_bytes = (q.kbo + q.kbi) * kBoxBytes;              // [dT boxes | h boxes]
+    uint8_t* sW = smem + (size_t)q.stages * st_bytes;
+    uint8_t* sOut = sW + (size_t)q.kbo * q.f_in * 128;             // 2 groups x 2 boxes
+    uint64_t* full = (uint64_t*)(sOut + 4 * kBoxBytes);
+    uint64_t* empty = full + kMaxNNStages;
+    uint64_t* tfull = empty + kMaxNNStages;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* wfull = tempty + 2;
+    uint32_t* tmem_slot = (uint32_t*)(wfull + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // W^T as the dH B operand: n = input feature (f_in rows), k = output feature, K-major
+    stage_weights(sW, nullptr, q.W, q.f_out, 0, q.f_in, q.kbo, q.kbo, 1);
+    if (warp == 0 && lane == 0) {
+        for (int st = 0; st < q.stages; st++) { tc::mbar_init(&full[st], 1); tc::mbar_init(&empty[st], 3); }
+        for (int a = 0; a < 2; a++) { tc::mbar_init(&tfull[a], 1); tc::mbar_init(&tempty[a], 8); }
+        tc::mbar_init(wfull, 1);
+        tc::mbar_fence_init();
+        tc::tma_prefetch(&tmT);
+        tc::tma_prefetch(&tmH);
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, q.tmem_cols);
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tw = tmem + 2u * (uint32_t)q.f_in;              // dW accumulator columns
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < q.num_tiles; tile += gridDim.x) {
+                tc::mbar_wait(&empty[stage], phase ^ 1);
+                tc::mbar_arrive_expect_tx(&full[stage], st_bytes);
+                uint8_t* st = smem + (size_t)stage * st_bytes;
+                for (int b = 0; b < q.kbo; b++) tc::tma_load_2d(st + b * kBoxBytes, &tmT, &full[stage], b * 64, tile * 128);
+                for (int b = 0; b < q.kbi; b++)
+                    tc::tma_load_2d(st + (q.kbo + b) * kBoxBytes, &tmH, &full[stage], b * 64, tile * 128);
+                if (++stage == q.stages) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        const uint32_t id_h = tc::idesc_bf16(128, q.f_in, 0, 0);
+        const uint32_t id_w = tc::idesc_bf16(128, q.nmma_w, 1, 1);
+        int stage = 0, acc = 0, it = 0;
+        uint32_t phase = 0, aphase = 0;
+        for (int tile = blockIdx.x; tile < q.num_tiles; tile += gridDim.x, it++) {
+            tc::mbar_wait(&full[stage], phase);
+            tc::mbar_wait(&tempty[acc], aphase ^ 1);
+            tc::fence_after();
+            if (lane == 0) {
+                const uint32_t sT = tc::smem_u32(smem + (size_t)stage * st_bytes);
+                const uint32_t sH = sT + q.kbo * kBoxBytes;
+                const uint32_t d = tmem + (uint32_t)(acc * q.f_in);
+                // dH tile = dT W^T (K = output features)
+                for (int kb = 0; kb < q.kbo; kb++) {
+                    const uint32_t b0 = tc::smem_u32(sW + (size_t)kb * q.f_in * 128);
+#pragma unroll
+                    for (int k = 0; k < 4; k++)
+                        tc::mma_f16(d, tc::smem_desc_sw128(sT + kb * kBoxBytes + k * 32, 0, 1024),
+                                    tc::smem_desc_sw128(b0 + k * 32, 0, 1024), id_h, (kb | k) != 0);
+                }
+                tc::mma_commit(&tfull[acc]);
+                // dW += h^T dT over this tile's 128 rows (16 rows per MMA, MN-major operands)
+#pragma unroll
+                for (int k = 0; k < 8; k++)
+                    tc::mma_f16(tw, tc::smem_desc_sw128(sH + k * 2048, kBoxBytes, 1024),
+                                tc::smem_desc_sw128(sT + k * 2048, kBoxBytes, 1024), id_w, (it | k) != 0);
+                tc::mma_commit(&empty[stage]);
+            }
+            __syncwarp();
+            if (++stage == q.stages) { stage = 0; phase ^= 1; }
+            acc ^= 1;
+            if (acc == 0) aphase ^= 1;
+        }
+        if (lane == 0) tc::mma_commit(wfull);
+        __syncwarp();
+    } else {
+        const int grp = (warp - 2) >> 2;
+        const int ew = warp & 3;
+        const bool leader = ((warp - 2) & 3) == 0 && lane == 0;
+        uint8_t* sbuf = sOut + grp * 2 * kBoxBytes;
+        TcNN p;
+        p.M = q.M; p.N = q.f_in; p.n_split = q.f_in; p.nb1 = (q.f_in + 63) / 64; p.nb2 = 0;
+        p.rs = q.rs; p.relu = 0;
+        int acc = 0, ob = 0, stage = 0;
+        uint32_t aphase = 0, sphase = 0;
+        auto rs_of = [&](int t) {
+            const int64_t g = (int64_t)t * 128 + ew * 32 + lane;
+            return (q.rs && t < q.num_tiles && g < q.M) ? __ldg(q.rs + g) : 1.f;
+        };
+        float rs_next = rs_of(blockIdx.x);
+        int it = 0;
+        for (int tile = blockIdx.x; tile < q.num_tiles; tile += gridDim.x, it++) {
+            const uint32_t tacc = tmem + (uint32_t)(acc * q.f_in);
+            const float rs_cur = rs_next;
+            rs_next = rs_of(tile + gridDim.x);
+            // the relu' gate: this group's h box of the tile's stage (full[stage] completed before
+            // the MMA issued, and the accumulator wait below orders after that)
+            const uint8_t* gcur = q.gate ? smem + (size_t)stage * st_bytes + (q.kbo + grp) * kBoxBytes : nullptr;
+            if (q.gate) tc::mbar_wait(&full[stage], sphase);     // TMA-written gate visible here
+            const __nv_bfloat16* gmask = q.gate ? reinterpret_cast<const __nv_bfloat16*>(gcur) : nullptr;
+            if (grp == 0)
+                nn_epilogue<0>(p, &tmC, &tmC, gmask, sbuf, 2, tacc, &tfull[acc], aphase, ew, lane, tile, leader,
+                               ob, rs_cur, gcur);
+            else
+                nn_epilogue<1>(p, &tmC, &tmC, gmask, sbuf, 2, tacc, &tfull[acc], aphase, ew, lane, tile, leader,
+                               ob, rs_cur, gcur);
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+            grp_bar(grp);                               // the group is done with the gate box
+            if (leader) tc::mbar_arrive(&empty[stage]);
+            if (++stage == q.stages) { stage = 0; sphase ^= 1; }
+            acc ^= 1;
+            if (acc == 0) aphase ^= 1;
+        }
+        if (leader) bulk_wait_read0();
+        // this CTA's dW partial: TMEM lane = input feature, columns = output features
+        tc::mbar_wait(wfull, 0);
+        tc::fence_after();
+        const int frow = ew * 32 + lane;
+        float* out = q.ws + ((int64_t)blockIdx.x * 128 + frow) * q.f_out;
+        const uint32_t tb = tw + ((uint32_t)(ew * 32) << 16);
+        for (int c0 = grp * 16; c0 < q.f_out; c0 += 32) {
+            float v[16];
+            tc::tmem_ld16(tb + c0, v);
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+                *reinterpret_cast<float4*>(out + c0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        }
+        tc::fence_before();
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc::fence_after();
+        tc::tmem_dealloc(tmem, q.tmem_cols);
+    }
+}
+
 // ------------------------------------------------------------------------------ NN, fp32 storage
 // Split-fp32 transform for the fp32-storage path (1e-4 parity): every fp32 operand x is split
 // into x_hi = bf16(x) and x_lo = bf16(x - x_hi) (together 16 significant bits; the residual is
@@ -1025,6 +1189,7 @@ grappa_status gemm_x3_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s) {
     return GRAPPA_OK;
 }
 
+
 static int tn_ftiles(int K) { return (int)ceil_div(K, 128); }
 
 static void tn_plan(int64_t M, int ftiles, int sm_count, int* slabs, int64_t* rps) {
@@ -1034,6 +1199,50 @@ static void tn_plan(int64_t M, int ftiles, int sm_count, int* slabs, int64_t* rp
     *rps = r;
     *slabs = (int)ceil_div(M > 0 ? M : 1, r);
 }
+
+// backward pair (GCN, bf16): dz_in = (dT W^T) * relu'(h_in) [* rs] and dW = h_in^T dT
+static size_t pair_smem_of(int kbo, int kbi, int f_in, int stages) {
+    return 1024 + (size_t)stages * (kbo + kbi) * kBoxBytes + (size_t)kbo * f_in * 128 + 4 * kBoxBytes + 256;
+}
+bool gemm_tc_pair_supported(int64_t M, int f_in, int f_out) {
+    if (f_in <= 64 || f_in > 128 || f_in % 16 || f_out > 128 || f_out % 16 || M >= (1ll << 31)) return false;
+    const int kbo = (f_out + 63) / 64;
+    return pair_smem_of(kbo, 2, f_in, 2) <= (size_t)kMaxSmem;
+}
+grappa_status gemm_tc_pair(grappa_ctx* ctx, int64_t M, int f_in, int f_out, const void* dT, const void* h,
+                           const float* W, const float* rs, int gate, void* dz_in, float* ws, float* dw,
+                           cudaStream_t s) {
+    CUtensorMap mt, mh, mc;
+    GRAPPA_TRY(make_map(&mt, dT, M, f_out, 128));
+    GRAPPA_TRY(make_map(&mh, h, M, f_in, 128));
+    GRAPPA_TRY(make_map(&mc, dz_in, M, f_in, 128));
+    TcPair q;
+    q.M = M; q.f_in = f_in; q.f_out = f_out;
+    q.kbo = (f_out + 63) / 64; q.kbi = 2;
+    q.nmma_w = q.kbo * 64;
+    q.W = W; q.rs = rs; q.gate = gate; q.ws = ws;
+    q.num_tiles = (int)ceil_div(M, 128);
+    q.tmem_cols = 512;
+    q.stages = 2;
+    while (q.stages < 4 && pair_smem_of(q.kbo, q.kbi, f_in, q.stages + 1) <= (size_t)kMaxSmem) q.stages++;
+    // the dW split: CTA b owns tiles b, b + grid, ... (grid fixed by M: deterministic sums)
+    int slabs;
+    int64_t rps;
+    tn_plan(M, 1, kTnCtas, &slabs, &rps);
+    const int grid = (int)std::min<int64_t>(q.num_tiles, slabs);
+    static bool attr = false;
+    if (!attr) {
+        GRAPPA_CUDA(cudaFuncSetAttribute(k_gemm_tc_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+        attr = true;
+    }
+    k_gemm_tc_pair<<<grid, kNNThreads, pair_smem_of(q.kbo, q.kbi, f_in, q.stages), s>>>(mt, mh, mc, q);
+    GRAPPA_LAUNCHED(ctx);
+    const int64_t count = (int64_t)f_in * f_out;
+    k_tn_reduce<8><<<(unsigned)ceil_div(count, 32), 32 * 8, 0, s>>>(count, f_out, f_in, 0, 1, 1, grid, ws, dw);
+    GRAPPA_LAUNCHED(ctx);
+    return GRAPPA_OK;
+}
+
 
 size_t gemm_tc_tn_ws_bytes(int64_t M, int K1, int K2, int N) {
     const int ft = tn_ftiles(K1) + (K2 ? tn_ftiles(K2) : 0);

@@ -29,3 +29,8 @@ if [ "${NCU_FULL:-1}" = "1" ]; then
   ncu -i /tmp/phase_full.ncu-rep --page details --csv > gpurun_out/${TAG}_phase_details.csv 2>/dev/null
 fi
 ls -la gpurun_out | tail -20
+# side lines: fp32 storage (split-fp32 GEMMs) and sharded mode
+timeout 500 python bench.py --dtype f32 --no-cpu-baseline > gpurun_out/${TAG}_bench_f32.json 2> gpurun_out/${TAG}_bench_f32.err
+echo "bench f32 exit $?"; tail -c 300 gpurun_out/${TAG}_bench_f32.json
+timeout 500 python bench.py --sharded --no-cpu-baseline > gpurun_out/${TAG}_bench_sharded.json 2> gpurun_out/${TAG}_bench_sharded.err
+echo "bench sharded exit $?"; tail -c 300 gpurun_out/${TAG}_bench_sharded.json

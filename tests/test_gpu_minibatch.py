@@ -174,3 +174,21 @@ def test_sampled_blocks_bitexact_hubs(G, fan):
             assert np.array_equal(gb["col"].cpu().numpy(), ob["col"]), (bi, l)
     assert hubs_seen > 10
     ctx.close()
+
+
+def test_sharded_minibatch_equals_replicated(G, setup):
+    """sharded mode (a3 (i)) under the mini-batch trainer: partitions built from chunk shards
+    feed the sampler exactly like replicated ones -- one epoch, theta bit for bit"""
+    from paper_2602_01872_b200.engine import MinibatchTrainer, ModelSpec
+    ctx, wl, ds, ref, parts = setup
+    spec = ModelSpec(wl.arch, wl.dims, wl.dims_pad)
+    mk = lambda sh: MinibatchTrainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights, 4,
+                                     gen.seed_of("chunks"), corr="uniform", lr=0.05, repartition_every=10,
+                                     fanouts=FAN, batch_size=500, sample_seed=3, dtype="bf16", sharded=sh)
+    a, b = mk(False), mk(True)
+    assert b.rowptr is None
+    a.run_epoch()
+    b.run_epoch()
+    torch.cuda.synchronize()
+    ctx.check()
+    assert torch.equal(a.theta, b.theta)

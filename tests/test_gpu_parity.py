@@ -380,3 +380,35 @@ def test_loss_dz_normed_flag(G, ctx, prod):
     assert err(_np(dl1)[:, :47], nrm[:, None] * ref_dz) <= 1e-4
     with pytest.raises(G.GrappaError, match="E_ARG"):
         G.grappa_loss(ctx, part, logits, 47, 48, dl1, l1, "f32", flags=2)
+
+
+@pytest.mark.parametrize("f_in,f_out,normed,relu", [(128, 128, True, True), (128, 48, False, True),
+                                                    (112, 128, True, False), (80, 16, False, True)])
+def test_backward_pair_matches_separate_gemms(G, ctx, prod, f_in, f_out, normed, relu):
+    """GCN backward: the one-pass pair kernel (dz_in and dW from one read of dT and h_in) gives
+    the separate NN/TN kernels' dz_in bit for bit (same MMAs, same epilogue) and dW up to the
+    fp32 summation order of the split (1e-5); the oracle parity of the layer is covered by
+    test_layer_parity, which runs the pair by default"""
+    part = _part(G, ctx, prod, 8, 3, 6, "bf16")
+    n = part.n_core
+    g = torch.Generator(device="cuda").manual_seed(f_in + 7 * f_out)
+    h_in = torch.randn(n, f_in, device="cuda", generator=g).to(torch.bfloat16)
+    w = torch.randn(f_in, f_out, device="cuda", generator=g) / 10
+    dz = (torch.randn(n, f_out, device="cuda", generator=g) * 1e-2).to(torch.bfloat16)
+    lib = G.load()
+    outs = []
+    flags = 3 if normed else 0
+    for off in (0, 1):
+        assert lib.grappa_set_kernel_variant(b"pair", off) == 0
+        ws = torch.empty(G.layer_ws_bytes(part, "gcn", f_in, f_out, "bf16"), dtype=torch.uint8, device="cuda")
+        dw = torch.full_like(w, float("nan"))
+        dz_in = torch.empty(n, f_in, device="cuda", dtype=torch.bfloat16)
+        G.grappa_layer_bwd_ex(ctx, part, "gcn", f_in, f_out, relu, dz, h_in, w, None, dw, dz_in, ws, "bf16",
+                              flags=flags)
+        torch.cuda.synchronize()
+        outs.append((dz_in.clone(), dw.clone()))
+    lib.grappa_set_kernel_variant(b"pair", 0)
+    (a_dz, a_dw), (b_dz, b_dw) = outs
+    assert torch.equal(a_dz.view(torch.int16), b_dz.view(torch.int16))
+    assert torch.isfinite(a_dw).all()
+    assert err(_np(a_dw), _np(b_dw)) <= 1e-5
