@@ -429,33 +429,49 @@ class Trainer:
         self.end_epoch()
 
     def run_epoch_graph(self):
-        """Same epoch, replayed from a CUDA graph captured once per super-epoch (the phase
-        loop is launch-bound on small graphs: ~60 kernels per phase).  The first call after a
-        repartition captures (nothing executes during capture) and then replays."""
+        """Same epoch, replayed from a CUDA graph captured once per super-epoch (the phase loop
+        issues ~535 launches per products epoch; replay removes the host launch gaps).  The first
+        epoch of a super-epoch runs eagerly on the main stream while the same launches are
+        recorded on a capture stream, so the GPU works through that epoch while the host
+        records (capturing alone would leave the GPU idle for the recording + instantiation)."""
         t = self.super_epoch()
         if t != self.t:
             self.repartition(t)
             self.graph = None
-        if getattr(self, "graph", None) is None:
-            torch.cuda.synchronize(self.dev)
-            g = torch.cuda.CUDAGraph()
-            main = self.stream
-            cap = torch.cuda.Stream(self.dev)
-            cap.wait_stream(main)
-            l0 = self.ctx.launches()
-            with torch.cuda.graph(g, stream=cap):
-                self.stream = cap
-                try:
-                    for i, w in self.my_workers():
-                        self.phase_step(i, w, min(self.G, self.W - i * self.G))
-                finally:
-                    self.stream = main
-            self.graph = g
-            self.graph_launches = self.ctx.launches() - l0
-            self.graph_steps, self._steps = list(self._steps), []
-        self.graph.replay()
-        if self.controller is not None:        # the captured steps' factors (fixed per super-epoch)
-            self._steps = list(self.graph_steps)
+        if getattr(self, "graph", None) is not None:
+            self.graph.replay()
+            if self.controller is not None:    # the captured steps' factors (fixed per super-epoch)
+                self._steps = list(self.graph_steps)
+            self.end_epoch()
+            return
+        g = torch.cuda.CUDAGraph()
+        main = self.stream
+        cap = torch.cuda.Stream(self.dev)
+        cap.wait_stream(main)
+        n_cap, cap_steps = 0, []
+        # capture_begin/end directly: torch.cuda.graph() would also run gc.collect() and
+        # empty_cache(); relaxed mode lets the eager launches proceed during the capture
+        with torch.cuda.stream(cap):
+            g.capture_begin(capture_error_mode="relaxed")
+            try:
+                for i, w in self.my_workers():
+                    m_active = min(self.G, self.W - i * self.G)
+                    with torch.cuda.stream(main):
+                        self.stream = main
+                        self.phase_step(i, w, m_active)           # runs now
+                    saved, self._steps = self._steps, []
+                    l0 = self.ctx.launches()
+                    self.stream = cap
+                    self.phase_step(i, w, m_active)               # recorded for the replays
+                    n_cap += self.ctx.launches() - l0
+                    cap_steps += self._steps
+                    self._steps = saved
+            finally:
+                self.stream = main
+                g.capture_end()
+        self.graph = g
+        self.graph_launches = n_cap
+        self.graph_steps = cap_steps
         self.end_epoch()
 
     @property

@@ -72,3 +72,27 @@ def test_capacity_epoch_equals_resident(G, prod, halo, dtype):
     assert torch.equal(a.theta, b.theta)
     assert not torch.equal(a.theta, mk(False).theta)       # the epochs did move theta
     ctx.close()
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_graph_epochs_equal_eager(G, prod, dtype):
+    """CUDA-graph replay (run_epoch_graph: the first epoch of a super-epoch runs eagerly while the
+    same launches are captured, later epochs replay) reproduces eager epochs bit for bit, across
+    a super-epoch switch"""
+    from paper_2602_01872_b200.engine import ModelSpec, Trainer
+    ctx = G.Context(0)
+    ds = prod
+    wl = ds.wl
+    spec = ModelSpec(wl.arch, wl.dims, wl.dims_pad)
+    mk = lambda: Trainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights, wl.chunks,
+                         gen.seed_of("chunks"), corr="uniform", lr=0.05, repartition_every=2, dtype=dtype)
+    a, b = mk(), mk()
+    for _ in range(5):                       # super-epochs 1, 1, 2, 2, 3
+        a.run_epoch()
+        b.run_epoch_graph()
+    torch.cuda.synchronize()
+    ctx.check()
+    assert b.graph is not None and b.graph_launches > 0
+    assert torch.equal(a.theta, b.theta)
+    assert a.losses == b.losses if hasattr(a, "losses") else True
+    ctx.close()
