@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action="store_true",
                     help="replay each epoch from a CUDA graph (the default at N=1 for full-graph runs)")
+    ap.add_argument("--depth", type=int, default=4,
+                    help="mini-batch mode: batches sampled ahead on side streams")
     ap.add_argument("--eager", action="store_true",
                     help="launch every kernel from the host each epoch (no CUDA-graph replay)")
     ap.add_argument("--out", default=None)
@@ -286,7 +288,7 @@ def run_grappa(args):
         tr = MinibatchTrainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights,
                               wl.chunks, gen.seed_of("chunks"), fanouts=wl.extra["fanouts"],
                               batch_size=wl.extra["batch_size"], sample_seed=gen.seed_of("sample"),
-                              **common)
+                              depth=args.depth, **common)
     else:
         tr = Trainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights, wl.chunks,
                      gen.seed_of("chunks"), **common)

@@ -488,7 +488,7 @@ class MinibatchTrainer(Trainer):
     (grappa_minibatch_step), scales by the batch's coverage factor and all-reduces
     (grappa_aggregate_grads_c) before the SGD step (Alg. 1)."""
 
-    def __init__(self, *args, fanouts=(15, 10, 5), batch_size=1000, sample_seed=0, depth: int = 2, **kw):
+    def __init__(self, *args, fanouts=(15, 10, 5), batch_size=1000, sample_seed=0, depth: int = 4, **kw):
         super().__init__(*args, **kw)
         if self.capacity:
             raise ValueError("capacity mode is implemented for full-graph training")
