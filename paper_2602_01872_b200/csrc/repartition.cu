@@ -206,11 +206,21 @@ __global__ void k_task_count(const int64_t* __restrict__ d_T, const int32_t* __r
         const int32_t v = core_global ? core_global[i] : (int32_t)i;
         const int64_t e0 = g_rowptr[v] + (t - task_off[i]) * (int64_t)kTaskLen;
         const int64_t e1 = min(g_rowptr[v + 1], e0 + kTaskLen);
+        // 4 x 32 edges per round: the column loads, then the (dependent, L2-resident) rank
+        // probes, are issued together -- 4 probes in flight per lane instead of 1
         int32_t cnt = 0;
-        for (int64_t e = e0 + lane; e - lane < e1; e += 32) {
-            bool keep = false;
-            if (e < e1) keep = rank[g_col[e]] >= 0;
-            cnt += __popc(__ballot_sync(0xffffffffu, keep));
+        for (int64_t b = e0; b < e1; b += 128) {
+            int32_t u[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int64_t e = b + k * 32 + lane;
+                u[k] = e < e1 ? g_col[e] : -1;
+            }
+            int32_t r[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) r[k] = u[k] >= 0 ? rank[u[k]] : -1;
+#pragma unroll
+            for (int k = 0; k < 4; k++) cnt += __popc(__ballot_sync(0xffffffffu, r[k] >= 0));
         }
         if (lane == 0) tcount[t] = cnt;
     }
@@ -259,12 +269,22 @@ __global__ void k_task_fill(const int64_t* __restrict__ d_T, const int32_t* __re
         const int64_t e0 = g_rowptr[v] + (t - task_off[i]) * (int64_t)kTaskLen;
         const int64_t e1 = min(g_rowptr[v + 1], e0 + kTaskLen);
         int64_t out = task_out[t];
-        for (int64_t e = e0 + lane; e - lane < e1; e += 32) {
-            int32_t r = -1;
-            if (e < e1) r = rank[g_col[e]];
-            const unsigned m = __ballot_sync(0xffffffffu, r >= 0);
-            if (r >= 0) col[out + __popc(m & ((1u << lane) - 1u))] = r;
-            out += __popc(m);
+        for (int64_t b = e0; b < e1; b += 128) {          // 4 probes in flight per lane (as above)
+            int32_t u[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int64_t e = b + k * 32 + lane;
+                u[k] = e < e1 ? g_col[e] : -1;
+            }
+            int32_t r[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) r[k] = u[k] >= 0 ? rank[u[k]] : -1;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {                  // stable: edge order kept
+                const unsigned m = __ballot_sync(0xffffffffu, r[k] >= 0);
+                if (r[k] >= 0) col[out + __popc(m & ((1u << lane) - 1u))] = r[k];
+                out += __popc(m);
+            }
         }
     }
 }
