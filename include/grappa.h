@@ -492,8 +492,9 @@ typedef enum {
     GRAPPA_K_NCLASS = 7
 } grappa_kclass;
 /* Test / A-B hook (process wide): select an alternative kernel implementation so tests can
- * cross-check them.  op "gemm": 0 = auto (tcgen05 for bf16, 128x128 FFMA tiles for fp32),
- * 1 = CUDA-core kernels for bf16, 2 = the small-tile CUDA-core kernels for both dtypes.
+ * cross-check them.  op "gemm": 0 = auto (tcgen05 for bf16, split-fp32 tcgen05 for fp32),
+ * 1 = CUDA-core kernels (bf16; 128x128 FFMA tiles for fp32), 2 = the small-tile CUDA-core
+ * kernels for both dtypes.
  * op "spmm": 0 = auto (row-group kernel for rows of <= 32 vectors, degree-bucketed row
  * order), 1 = warp-per-row, 2 = row-group with 8 loads in flight, 3 = row-group, natural order.
  * op "fuse": 0 = off (default), 1 = bf16 GCN layers run the fused aggregate->transform kernel
@@ -502,6 +503,10 @@ typedef enum {
  * op "wide": 0 = unweighted bf16 gathers use 16-byte lanes (default), 1 = 32-byte lanes.
  * op "tnstages": ring depth of the tcgen05 weight-gradient GEMM (default 4; 0 = fill shared memory).
  * op "tnred": slab groups of its fixed-order split-K reduction (8 default, or 32).
+ * op "pair": 0 = GCN backward runs dz_in and dW as one pass over dT and h_in (default, bf16),
+ * 1 = the two separate GEMMs.
+ * op "x3dbg": timing probes of the split-fp32 transform only (results invalid when != 0):
+ * bit 1 no A loads, 2 no output stores, 4 no weight staging, 8 one MMA per K step, 16 no epilogue.
  * Returns E_ARG for an unknown op. */
 grappa_status grappa_set_kernel_variant(const char* op, int variant);
 

@@ -29,8 +29,14 @@ if [ "${NCU_FULL:-1}" = "1" ]; then
   ncu -i /tmp/phase_full.ncu-rep --page details --csv > gpurun_out/${TAG}_phase_details.csv 2>/dev/null
 fi
 ls -la gpurun_out | tail -20
-# side lines: fp32 storage (split-fp32 GEMMs) and sharded mode
-timeout 500 python bench.py --dtype f32 --no-cpu-baseline > gpurun_out/${TAG}_bench_f32.json 2> gpurun_out/${TAG}_bench_f32.err
-echo "bench f32 exit $?"; tail -c 300 gpurun_out/${TAG}_bench_f32.json
-timeout 500 python bench.py --sharded --no-cpu-baseline > gpurun_out/${TAG}_bench_sharded.json 2> gpurun_out/${TAG}_bench_sharded.err
-echo "bench sharded exit $?"; tail -c 300 gpurun_out/${TAG}_bench_sharded.json
+# side lines (profiles/r01_bench_*.json): every BASELINE config and option the bench offers
+if [ "${SIDE:-1}" = "1" ]; then
+  nb=--no-cpu-baseline
+  for spec in "f32:--dtype f32 $nb" "sharded:--sharded $nb" "halo:--halo $nb" "node:--corr node $nb" \
+              "rmat24:--config rmat24 $nb" "rmat26:--config rmat26 $nb" "arxiv:--config arxiv" "cora:--config cora" \
+              "gat:--config products_gat $nb" "capacity:--capacity $nb" "papers:--config papers --steps 2 --warmup 1 $nb"; do
+    name=${spec%%:*}; a=${spec#*:}
+    timeout 1200 python bench.py $a > gpurun_out/${TAG}_bench_${name}.json 2> gpurun_out/${TAG}_bench_${name}.err
+    echo "bench $name exit $?"; python -c "import json,sys; d=json.load(open(sys.argv[1])); print(d['ms_per_step'], d['config']['epoch_ms']['median'], (d.get('e2e') or {}).get('ms_per_step'))" gpurun_out/${TAG}_bench_${name}.json
+  done
+fi

@@ -28,8 +28,8 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 
 
 # kernel-name prefixes of each profiled class (a logical call = all of its launches)
-CLASS_PREFIX = {"spmm": ("k_spmm",), "gemm": ("k_gemm_tc_nn", "k_sgemm_nn", "k_gemm_nn"),
-                "gemm_tn": ("k_gemm_tc_tn", "k_tn_reduce", "k_sgemm_tn", "k_gemm_tn", "k_reduce_slabs"),
+CLASS_PREFIX = {"spmm": ("k_spmm",), "gemm": ("k_gemm_tc_nn", "k_gemm_tc_pair", "k_gemm_x3_nn", "k_sgemm_nn", "k_gemm_nn"),
+                "gemm_tn": ("k_gemm_tc_tn", "k_gemm_x3_tn", "k_tn_reduce", "k_sgemm_tn", "k_gemm_tn", "k_reduce_slabs"),
                 "loss": ("k_loss",), "agg": ("k_scale_grad", "k_sgd")}
 
 
