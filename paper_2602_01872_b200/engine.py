@@ -430,10 +430,11 @@ class Trainer:
 
     def run_epoch_graph(self):
         """Same epoch, replayed from a CUDA graph captured once per super-epoch (the phase loop
-        issues ~535 launches per products epoch; replay removes the host launch gaps).  The first
-        epoch of a super-epoch runs eagerly on the main stream while the same launches are
-        recorded on a capture stream, so the GPU works through that epoch while the host
-        records (capturing alone would leave the GPU idle for the recording + instantiation)."""
+        issues ~535 launches per products epoch; replay removes the host launch gaps).  On large
+        partitions the first epoch of a super-epoch runs eagerly on the main stream while the same
+        launches are recorded on a capture stream, so the GPU works through that epoch while the
+        host records (capturing alone would leave the GPU idle for the recording +
+        instantiation); on small ones (host-bound epochs) it is recorded only, then replayed."""
         t = self.super_epoch()
         if t != self.t:
             self.repartition(t)
@@ -449,6 +450,9 @@ class Trainer:
         cap = torch.cuda.Stream(self.dev)
         cap.wait_stream(main)
         n_cap, cap_steps = 0, []
+        # small partitions (host-bound epochs): record only, then replay -- running the epoch
+        # eagerly as well would double the host work that bounds them
+        eager = sum(p.nnz for p in self.parts.values()) >= getattr(self, "graph_eager_min_nnz", 4_000_000)
         # capture_begin/end directly: torch.cuda.graph() would also run gc.collect() and
         # empty_cache(); relaxed mode lets the eager launches proceed during the capture
         with torch.cuda.stream(cap):
@@ -456,9 +460,10 @@ class Trainer:
             try:
                 for i, w in self.my_workers():
                     m_active = min(self.G, self.W - i * self.G)
-                    with torch.cuda.stream(main):
-                        self.stream = main
-                        self.phase_step(i, w, m_active)           # runs now
+                    if eager:
+                        with torch.cuda.stream(main):
+                            self.stream = main
+                            self.phase_step(i, w, m_active)       # runs now
                     saved, self._steps = self._steps, []
                     l0 = self.ctx.launches()
                     self.stream = cap
@@ -472,6 +477,9 @@ class Trainer:
         self.graph = g
         self.graph_launches = n_cap
         self.graph_steps = cap_steps
+        if not eager:
+            g.replay()
+            self._steps += cap_steps
         self.end_epoch()
 
     @property

@@ -74,8 +74,8 @@ def test_capacity_epoch_equals_resident(G, prod, halo, dtype):
     ctx.close()
 
 
-@pytest.mark.parametrize("dtype", ["bf16", "f32"])
-def test_graph_epochs_equal_eager(G, prod, dtype):
+@pytest.mark.parametrize("dtype,eager_min", [("bf16", None), ("f32", None), ("bf16", 0)])
+def test_graph_epochs_equal_eager(G, prod, dtype, eager_min):
     """CUDA-graph replay (run_epoch_graph: the first epoch of a super-epoch runs eagerly while the
     same launches are captured, later epochs replay) reproduces eager epochs bit for bit, across
     a super-epoch switch"""
@@ -87,6 +87,8 @@ def test_graph_epochs_equal_eager(G, prod, dtype):
     mk = lambda: Trainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights, wl.chunks,
                          gen.seed_of("chunks"), corr="uniform", lr=0.05, repartition_every=2, dtype=dtype)
     a, b = mk(), mk()
+    if eager_min is not None:                # the eager-while-capturing path of large partitions
+        b.graph_eager_min_nnz = eager_min
     for _ in range(5):                       # super-epochs 1, 1, 2, 2, 3
         a.run_epoch()
         b.run_epoch_graph()
