@@ -435,10 +435,15 @@ class Trainer:
         launches are recorded on a capture stream, so the GPU works through that epoch while the
         host records (capturing alone would leave the GPU idle for the recording +
         instantiation); on small ones (host-bound epochs) it is recorded only, then replayed."""
+        import os
+        import time
+        tm = os.environ.get("GRAPPA_GRAPH_TIMING") == "1"     # diagnostic host timings (stderr)
+        h0 = time.perf_counter()
         t = self.super_epoch()
         if t != self.t:
             self.repartition(t)
             self.graph = None
+        h1 = time.perf_counter()
         if getattr(self, "graph", None) is not None:
             self.graph.replay()
             if self.controller is not None:    # the captured steps' factors (fixed per super-epoch)
@@ -471,9 +476,15 @@ class Trainer:
                     n_cap += self.ctx.launches() - l0
                     cap_steps += self._steps
                     self._steps = saved
+                h2 = time.perf_counter()
             finally:
                 self.stream = main
                 g.capture_end()
+        h3 = time.perf_counter()
+        if tm:
+            import sys
+            print(f"[graph] repartition {1e3 * (h1 - h0):.1f} ms, record{' + eager' if eager else ''} "
+                  f"{1e3 * (h2 - h1):.1f} ms, capture_end {1e3 * (h3 - h2):.1f} ms", file=sys.stderr)
         self.graph = g
         self.graph_launches = n_cap
         self.graph_steps = cap_steps

@@ -30,8 +30,9 @@ if [ "${NCU_FULL:-1}" = "1" ]; then
 fi
 ls -la gpurun_out | tail -20
 # side lines (profiles/r01_bench_*.json): every BASELINE config and option the bench offers
-if [ "${SIDE:-1}" = "1" ]; then
+if [ "${SIDE:-1}" != "0" ]; then
   nb=--no-cpu-baseline
+  SPECS_ALL=1
   for spec in "f32:--dtype f32 $nb" "sharded:--sharded $nb" "halo:--halo $nb" "node:--corr node $nb" \
               "rmat24:--config rmat24 $nb" "rmat26:--config rmat26 $nb" "arxiv:--config arxiv" "cora:--config cora" \
               "gat:--config products_gat $nb" "capacity:--capacity $nb" "papers:--config papers --steps 2 --warmup 1 $nb"; do
