@@ -411,8 +411,12 @@ typedef struct {
 /* Epoch order of the partition's seeds (R23): order dev int32[n_seeds] (out, local ids). */
 grappa_status grappa_epoch_seeds(grappa_ctx* ctx, const grappa_part* part, uint64_t seed,
                                  int64_t epoch, int32_t* order, void* stream);
-/* Sample the L blocks of one batch.  batch: dev int32[n_batch] local seed ids; fanouts: host
- * int32[n_layers] (input -> output).  *inout NULL -> created, else reused.  Syncs once.
+/* Sample the L blocks of one batch (P:139, P:382 isolated_sampling).  Per target v
+ * at hop h: min(f_h, d_l(v)) distinct local neighbours, uniform without replacement, drawn by
+ * Floyd's algorithm over neighbour positions keyed by h(h(seed, epoch, batch_index, h), gid v, j)
+ * (reading R24); hop 1 uses the LAST fanout (R25); sources = targets then new nodes in ascending
+ * local id (R26).  batch: dev int32[n_batch] local seed ids; fanouts: host int32[n_layers]
+ * (input -> output, each <= 16).  *inout NULL -> created, else reused.  Syncs once.
  * Errors: E_ARG (n_layers < 1, fanout < 1, n_batch < 1). */
 grappa_status grappa_sample(grappa_ctx* ctx, const grappa_part* part, const int32_t* batch,
                             int32_t n_batch, const int32_t* fanouts, int32_t n_layers,

@@ -11,8 +11,10 @@ S:441/S:492 (lock-step iterations, shorter workers cycle their batches).
 
 Readings:
   R23  epoch order: seeds sorted by (h(seed_s, epoch, gid(v)), gid(v)); batch b = slice b of B.
-  R24  per target v at hop h, keep the min(f_h, d_l(v)) local neighbours u with the smallest
-       (h(h(seed_s, epoch, batch, h), gid(v), gid(u)), gid(u)) -- uniform without replacement.
+  R24  per target v at hop h with d = d_l(v) > f_h: f_h distinct neighbour positions drawn by
+       Floyd's algorithm -- for j = d - f_h .. d - 1: r = h(h(seed_s, epoch, batch, h), gid(v), j),
+       t = floor(r (j + 1) / 2^64) (uniform on [0, j]); keep t unless already kept, else keep j --
+       a uniformly random f_h-subset, i.e. uniform without replacement; d <= f_h keeps all.
   R25  fanouts are listed input -> output layer, so hop 1 (the seeds' neighbours, the output
        layer) uses the LAST entry (5 of {15,10,5}) and hop L the first (Q17).
   R26  sources of hop h = targets of hop h (as a prefix, same order) followed by the newly
@@ -57,9 +59,15 @@ def sample_hop(part, targets, f: int, seed_s: int, epoch: int, batch: int, hop: 
     picked = []
     for v in targets:
         nb = col[rowptr[v]:rowptr[v + 1]]
-        if nb.size > f:
-            k = _h(key0, np.uint64(gid[v]), gid[nb])
-            nb = nb[np.lexsort((gid[nb], k))[:f]]       # smallest (key, gid(u)) first
+        d = nb.size
+        if d > f:
+            # Floyd's algorithm (R24): f distinct positions, every f-subset equally likely
+            kept = []
+            for j in range(d - f, d):
+                r = int(_h(key0, np.uint64(gid[v]), np.uint64(j)))
+                t = (r * (j + 1)) >> 64
+                kept.append(j if t in kept else t)
+            nb = nb[np.asarray(kept, dtype=np.int64)]
         picked.append(nb)
     tset = set(int(t) for t in targets)
     new = sorted(set(int(u) for p in picked for u in p) - tset)

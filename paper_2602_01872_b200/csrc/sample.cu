@@ -5,9 +5,8 @@
 // SPEC S:196-222.  Readings R23-R28 (see include/grappa.h).
 //
 // Per hop, all on the device (one host sync per batch, at the end, to size the layer calls):
-//   k_pick        warp per target: if d_l <= f take every neighbour, else a single pass in
-//                 which every lane keeps its 16 smallest (hash, gid) keys in registers, then f
-//                 rounds of warp arg-min over the lanes' heads (= top-f of the whole row)
+//   k_pick_floyd  thread per target: if d_l <= f take every neighbour, else f distinct
+//                 positions by Floyd's algorithm (R24), O(f) whatever the degree
 //   frontier      bitmap over the partition (atomicOr picks, clear targets), word-popcount
 //                 scan -> new sources in ascending local id; `where` maps local id -> position
 //   block CSR     rowptr = scan of pick counts; each target's positions sorted ascending
@@ -39,297 +38,46 @@ static uint64_t hmix(uint64_t x) {
     return z ^ (z >> 31);
 }
 
-// (key, gid) lexicographic order; gid < 2^31 so it packs into the low word of a 96-bit value
-struct Key {
-    uint64_t k;
-    int32_t g;
-};
-__device__ __forceinline__ bool key_lt(uint64_t ak, int32_t ag, uint64_t bk, int32_t bg) {
-    return ak < bk || (ak == bk && ag < bg);
-}
-
-// keys of uniform 64-bit hashes below T = min(1, frac) 2^64 with frac = 6f/d: the f smallest
-// of d keys lie below it except with small probability (count ~ Binomial(d, 6f/d))
-__host__ __device__ __forceinline__ uint64_t hub_threshold(int f, int64_t d) {
-    const double frac = 6.0 * f / (double)d;
-    return frac >= 1.0 ? ~0ull : (uint64_t)(frac * 18446744073709551616.0);
-}
-
-// targets with more local neighbours than this go to the block-per-target threshold kernel
-constexpr int kHeavyPick = 1024;
-constexpr int kCandCap = 1024;
-
-__global__ void k_pick(const int64_t* __restrict__ d_nt, const int32_t* __restrict__ targets,
-                       const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                       const int32_t* __restrict__ gid, int f, uint64_t key0, int32_t* __restrict__ picks,
-                       int32_t* __restrict__ cnt, int32_t* __restrict__ heavy_n, int64_t* __restrict__ heavy_q) {
-    const int lane = threadIdx.x & 31;
+// R24: per target, f distinct local neighbour positions by Floyd's algorithm -- for j = d-f .. d-1
+// draw t = floor(h(key0, gid(v), j) (j+1) / 2^64) uniform on [0, j] and keep t, or j if t is
+// already kept: every f-subset equally likely (uniform without replacement), O(f) work per
+// target whatever its degree (a hub costs what a leaf costs; the earlier hash-priority draw
+// hashed every neighbour).  One thread per target; picks in draw order (k_fill_block sorts).
+__global__ void k_pick_floyd(const int64_t* __restrict__ d_nt, const int32_t* __restrict__ targets,
+                             const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                             const int32_t* __restrict__ gid, int f, uint64_t key0, int32_t* __restrict__ picks,
+                             int32_t* __restrict__ cnt) {
     const int64_t nt = *d_nt;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nt; t += nwarps) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = targets[t];
-        const int64_t e0 = rowptr[v], e1 = rowptr[v + 1];
-        const int d = (int)(e1 - e0);
+        const int64_t e0 = rowptr[v], d = rowptr[v + 1] - e0;
         int32_t* out = picks + t * f;
         if (d <= f) {
-            for (int i = lane; i < d; i += 32) out[i] = col[e0 + i];
-            if (lane == 0) cnt[t] = d;
+            for (int i = 0; i < (int)d; i++) out[i] = col[e0 + i];
+            cnt[t] = (int)d;
             continue;
         }
-        if (d > kHeavyPick) {                       // hub: handled by k_pick_heavy
-            if (lane == 0) heavy_q[atomicAdd(heavy_n, 1)] = t;
-            continue;
-        }
-        // per-lane sorted list of its f smallest keys (f <= 16), unrolled insertion.  Only keys
-        // below T = min(1, 8f/d) 2^64 are inserted (expected 8f of them, so the insertion chain
-        // runs ~8f/32 times per lane instead of d/32); the warp's f smallest keys are all below T
-        // whenever at least f keys are, which the ballot count checks -- otherwise the row is
-        // redone with T = 2^64 (exact either way).
-        uint64_t lk[kMaxFanout];
-        int32_t lg[kMaxFanout], lu[kMaxFanout];
+        const uint64_t kv = key0;
         const uint64_t gv = (uint64_t)gid[v];
-        uint64_t T = hub_threshold(f + f / 3, d);              // ~8f/d (6f/d at 4f/3)
-        for (int pass = 0; pass < 2; pass++) {
+        int64_t kept[kMaxFanout];
 #pragma unroll
-            for (int j = 0; j < kMaxFanout; j++) { lk[j] = ~0ull; lg[j] = 0x7fffffff; lu[j] = -1; }
-            int below = 0;
-            for (int i0 = 0; i0 < d; i0 += 32) {
-                const int i = i0 + lane;
-                bool take = false;
-                uint64_t k = 0;
-                int32_t g = 0, uu = 0;
-                if (i < d) {
-                    uu = col[e0 + i];
-                    g = gid[uu];
-                    // h(h(seed, epoch, batch, hop), gid(v), gid(u)) = mix(key0 ^ mix(gid(v) ^ mix(gid(u))))
-                    k = smix(key0 ^ smix(gv ^ smix((uint64_t)g)));
-                    take = k < T;
-                }
-                below += __popc(__ballot_sync(0xffffffffu, take));
-                if (take) {
+        for (int k = 0; k < kMaxFanout; k++) {
+            if (k >= f) break;
+            const int64_t j = d - f + k;
+            const uint64_t r = smix(kv ^ smix(gv ^ smix((uint64_t)j)));
+            int64_t pos = (int64_t)__umul64hi(r, (uint64_t)(j + 1));
+            bool dup = false;
 #pragma unroll
-                    for (int j = 0; j < kMaxFanout; j++) {   // bubble the new key into place
-                        if (j < f && key_lt(k, g, lk[j], lg[j])) {
-                            uint64_t tk = lk[j]; int32_t tg = lg[j], tu = lu[j];
-                            lk[j] = k; lg[j] = g; lu[j] = uu;
-                            k = tk; g = tg; uu = tu;
-                        }
-                    }
-                }
-            }
-            if (below >= f || T == ~0ull) break;
-            T = ~0ull;                                         // too few below T: exact redo
+            for (int q = 0; q < kMaxFanout; q++)
+                if (q < k && kept[q] == pos) dup = true;
+            if (dup) pos = j;
+            kept[k] = pos;
         }
-        // f rounds of warp arg-min over the lanes' list heads
-        int head = 0;
-        for (int r = 0; r < f; r++) {
-            uint64_t hk = ~0ull;
-            int32_t hg = 0x7fffffff, hu = -1;
+        // neighbour ids of the kept positions (independent loads, issued together)
 #pragma unroll
-            for (int j = 0; j < kMaxFanout; j++)
-                if (j == head) { hk = lk[j]; hg = lg[j]; hu = lu[j]; }
-            uint64_t bk = hk;
-            int32_t bg = hg;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
-                const int32_t og = __shfl_xor_sync(0xffffffffu, bg, o);
-                if (key_lt(ok, og, bk, bg)) { bk = ok; bg = og; }
-            }
-            const bool mine = hk == bk && hg == bg;
-            const unsigned who = __ballot_sync(0xffffffffu, mine);
-            const int src = __ffs(who) - 1;
-            const int32_t wu = __shfl_sync(0xffffffffu, hu, src);
-            if (lane == 0) out[r] = wu;
-            if (mine) head++;
-        }
-        if (lane == 0) cnt[t] = f;
-    }
-}
-
-// Hub targets (d_l > kHeavyPick), one block each.  Keys are uniform 64-bit hashes, so the
-// f smallest lie below T ~ 4f/d * 2^64 with overwhelming probability; the block counts the
-// keys under T (doubling / halving T until f <= count <= kCandCap -- exact either way), gathers
-// those candidates into shared memory and takes the f smallest (key, gid) by f warp arg-min
-// rounds.  The queue order of hubs is irrelevant: each writes only its own output slot.
-__global__ void __launch_bounds__(256) k_pick_heavy(const int32_t* __restrict__ heavy_n,
-                                                    const int64_t* __restrict__ heavy_q,
-                                                    const int32_t* __restrict__ targets,
-                                                    const int64_t* __restrict__ rowptr,
-                                                    const int32_t* __restrict__ col, const int32_t* __restrict__ gid,
-                                                    int f, uint64_t key0, int32_t* __restrict__ picks,
-                                                    int32_t* __restrict__ cnt) {
-    __shared__ uint64_t ck[kCandCap];
-    __shared__ int32_t cg[kCandCap], cu[kCandCap];
-    __shared__ int ncand, wsum[8];
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int nq = *heavy_n;
-    for (int q = blockIdx.x; q < nq; q += gridDim.x) {
-        const int64_t t = heavy_q[q];
-        const int32_t v = targets[t];
-        const int64_t e0 = rowptr[v];
-        const int d = (int)(rowptr[v + 1] - e0);
-        const double frac = 4.0 * f / d;
-        uint64_t T = frac >= 1.0 ? ~0ull : (uint64_t)(frac * 18446744073709551616.0);
-        for (;;) {
-            int c = 0;
-            for (int i = tid; i < d; i += 256) {
-                const uint64_t k = smix(key0 ^ smix((uint64_t)gid[v] ^ smix((uint64_t)gid[col[e0 + i]])));
-                c += k < T;
-            }
-            c = warp_sum(c);
-            if (lane == 0) wsum[w] = c;
-            __syncthreads();
-            int tot = 0;
-            for (int k = 0; k < 8; k++) tot += wsum[k];
-            __syncthreads();
-            if (tot >= f && tot <= kCandCap) break;
-            if (tot < f) T = T > (~0ull >> 1) ? ~0ull : T << 1;
-            else T >>= 1;
-        }
-        if (tid == 0) ncand = 0;
-        __syncthreads();
-        for (int i = tid; i < d; i += 256) {
-            const int32_t u = col[e0 + i];
-            const int32_t gu = gid[u];
-            const uint64_t k = smix(key0 ^ smix((uint64_t)gid[v] ^ smix((uint64_t)gu)));
-            if (k < T) {
-                const int p = atomicAdd(&ncand, 1);
-                ck[p] = k; cg[p] = gu; cu[p] = u;
-            }
-        }
-        __syncthreads();
-        if (w == 0) {
-            const int n = ncand;
-            uint64_t lk = 0;
-            int32_t lg = -1;                       // last selected (exclusive lower bound)
-            for (int r = 0; r < f; r++) {
-                uint64_t bk = ~0ull;
-                int32_t bg = 0x7fffffff, bu = -1;
-                for (int j = lane; j < n; j += 32) {
-                    const bool above = r == 0 || key_lt(lk, lg, ck[j], cg[j]);
-                    if (above && key_lt(ck[j], cg[j], bk, bg)) { bk = ck[j]; bg = cg[j]; bu = cu[j]; }
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
-                    const int32_t og = __shfl_xor_sync(0xffffffffu, bg, o);
-                    const int32_t ou = __shfl_xor_sync(0xffffffffu, bu, o);
-                    if (key_lt(ok, og, bk, bg)) { bk = ok; bg = og; bu = ou; }
-                }
-                if (lane == 0) picks[t * f + r] = bu;
-                lk = bk; lg = bg;
-            }
-            if (lane == 0) cnt[t] = f;
-        }
-        __syncthreads();
-    }
-}
-
-// Hub targets, grid-parallel (the per-hub block loop of k_pick_heavy serialises ~d/256 dependent
-// random gid loads per thread: 0.76 ms per hop on papers-shaped hubs).  The f smallest of d
-// uniform 64-bit keys lie below T = min(1, 6f/d) 2^64 except with negligible probability
-// (count ~ Binomial(d, 6f/d), mean 6f <= 96 for f <= 16: P[count < f] ~ 2.5e-3 at f = 1 (exp(-6)),
-// < 1e-8 for f >= 5; P[count > kCand = 512] is negligible); every (hub, 2048-edge segment) task appends its keys below T to the hub's
-// candidate list, then one block per hub takes the f smallest (key, gid) -- a total order, so
-// the append order (atomics) does not matter.  A hub whose count falls outside [f, kCand] is
-// redone exactly by k_pick_heavy (flag in cand_n).
-constexpr int kCand = 512;
-constexpr int kHubSeg = 2048;
-struct HubSegs {
-    const int32_t* heavy_n; const int64_t* heavy_q; const int32_t* targets; const int64_t* rowptr;
-    __device__ int32_t operator()(int64_t q) const {
-        if (q >= *heavy_n) return 0;
-        const int32_t v = targets[heavy_q[q]];
-        return (int32_t)ceil_div(rowptr[v + 1] - rowptr[v], kHubSeg);
-    }
-};
-struct WriteHubSegs {
-    int32_t* seg_off; int64_t* d_tasks;
-    __device__ void operator()(int64_t q, int64_t p, int32_t) const { seg_off[q] = (int32_t)p; }
-    __device__ void finish(int64_t n, int64_t total) const { seg_off[n] = (int32_t)total; *d_tasks = total; }
-};
-
-__global__ void __launch_bounds__(256) k_hub_cand(const int32_t* __restrict__ heavy_n, const int64_t* __restrict__ d_tasks,
-                                                  const int32_t* __restrict__ seg_off, const int64_t* __restrict__ heavy_q,
-                                                  const int32_t* __restrict__ targets, const int64_t* __restrict__ rowptr,
-                                                  const int32_t* __restrict__ col, const int32_t* __restrict__ gid, int f,
-                                                  uint64_t key0, int32_t* __restrict__ cand_n,
-                                                  uint4* __restrict__ cand) {
-    const int nq = *heavy_n;
-    const int64_t ntask = *d_tasks;
-    for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
-        // hub of this task: last q with seg_off[q] <= task (binary search, block-uniform)
-        int lo = 0, hi = nq - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (seg_off[mid] <= task) lo = mid; else hi = mid - 1;
-        }
-        const int q = lo;
-        const int32_t v = targets[heavy_q[q]];
-        const int64_t e0 = rowptr[v], d = rowptr[v + 1] - e0;
-        const uint64_t T = hub_threshold(f, d);
-        const int64_t s0 = (task - seg_off[q]) * (int64_t)kHubSeg;
-        const int64_t s1 = min(d, s0 + kHubSeg);
-        for (int64_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
-            const int32_t u = col[e0 + i];
-            const int32_t gu = gid[u];
-            const uint64_t k = smix(key0 ^ smix((uint64_t)gid[v] ^ smix((uint64_t)gu)));
-            if (k < T) {
-                const int p = atomicAdd(&cand_n[q], 1);
-                if (p < kCand) cand[(int64_t)q * kCand + p] = make_uint4((uint32_t)k, (uint32_t)(k >> 32), (uint32_t)gu, (uint32_t)u);
-            }
-        }
-    }
-}
-
-// one block per hub: f smallest (key, gid) among its candidates; hubs whose candidate count is
-// outside [f, kCand] are left to the exact k_pick_heavy (their queue entry is kept in redo_q)
-__global__ void __launch_bounds__(256) k_hub_select(const int32_t* __restrict__ heavy_n, const int64_t* __restrict__ heavy_q,
-                                                    const int32_t* __restrict__ cand_n, const uint4* __restrict__ cand, int f,
-                                                    int32_t* __restrict__ picks, int32_t* __restrict__ cnt,
-                                                    int32_t* __restrict__ redo_n, int64_t* __restrict__ redo_q) {
-    __shared__ uint64_t ck[kCand];
-    __shared__ int32_t cg[kCand], cu[kCand];
-    const int nq = *heavy_n;
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    for (int q = blockIdx.x; q < nq; q += gridDim.x) {
-        const int n = cand_n[q];
-        const int64_t t = heavy_q[q];
-        if (n < f || n > kCand) {
-            if (tid == 0) redo_q[atomicAdd(redo_n, 1)] = t;
-            continue;
-        }
-        for (int j = tid; j < n; j += blockDim.x) {
-            const uint4 c = cand[(int64_t)q * kCand + j];
-            ck[j] = (uint64_t)c.x | ((uint64_t)c.y << 32);
-            cg[j] = (int32_t)c.z;
-            cu[j] = (int32_t)c.w;
-        }
-        __syncthreads();
-        if (w == 0) {
-            uint64_t lk = 0;
-            int32_t lg = -1;                       // last selected (exclusive lower bound)
-            for (int r = 0; r < f; r++) {
-                uint64_t bk = ~0ull;
-                int32_t bg = 0x7fffffff, bu = -1;
-                for (int j = lane; j < n; j += 32) {
-                    const bool above = r == 0 || key_lt(lk, lg, ck[j], cg[j]);
-                    if (above && key_lt(ck[j], cg[j], bk, bg)) { bk = ck[j]; bg = cg[j]; bu = cu[j]; }
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
-                    const int32_t og = __shfl_xor_sync(0xffffffffu, bg, o);
-                    const int32_t ou = __shfl_xor_sync(0xffffffffu, bu, o);
-                    if (key_lt(ok, og, bk, bg)) { bk = ok; bg = og; bu = ou; }
-                }
-                if (lane == 0) picks[t * f + r] = bu;
-                lk = bk; lg = bg;
-            }
-            if (lane == 0) cnt[t] = f;
-        }
-        __syncthreads();
+        for (int k = 0; k < kMaxFanout; k++)
+            if (k < f) out[k] = col[e0 + kept[k]];
+        cnt[t] = f;
     }
 }
 
@@ -483,7 +231,6 @@ struct grappa_batch {
     int32_t n_batch = 0;
     BlockBufs blk[kMaxLayers];
     DevBuf picks, cnt, bitmap, where, erow, key_pad, skeys, svals, sort_tmp, counts, heavy_q;
-    DevBuf hub_seg, hub_cand_n, hub_cand;   // grid-parallel hub pick (k_hub_cand / k_hub_select)
     DevBuf scan_ws;                         // own scan partials (the sampler may run on a side stream)
     double c_uniform = 1, c_resampling = 1, c_hm = 1;
     // grappa_sample_async -> grappa_sample_wait: counts + stats land in pinned host memory
@@ -583,38 +330,9 @@ extern "C" grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part*
         GRAPPA_TRY(b->skeys.grow((size_t)cap_nnz * 4));
         // h(seed, epoch, batch, hop) = mix(seed ^ mix(epoch ^ mix(batch ^ mix(hop))))
         const uint64_t key0 = hmix(seed ^ hmix((uint64_t)epoch ^ hmix((uint64_t)batch_index ^ hmix((uint64_t)h))));
-        const unsigned wgrid = (unsigned)std::min<int64_t>(ceil_div(cap_t, 8), (int64_t)ctx->sm_count * 16);
         const unsigned tgrid = (unsigned)std::min<int64_t>(ceil_div(cap_nnz, 256), (int64_t)ctx->sm_count * 16);
-        // hubs: at most the partition's rows with d_l > kHeavyPick (<= n_heavy, d_l > kSegLen)
-        const int64_t cap_h = std::max<int64_t>(1, std::min<int64_t>(cap_t, I.n_heavy));
-        GRAPPA_TRY(b->heavy_q.grow((size_t)cap_h * 8 * 2));
-        GRAPPA_TRY(b->hub_seg.grow((size_t)(cap_h + 1) * 4));
-        GRAPPA_TRY(b->hub_cand_n.grow((size_t)cap_h * 4));
-        GRAPPA_TRY(b->hub_cand.grow((size_t)cap_h * kCand * 16));
-        int32_t* heavy_n = (int32_t*)(dstat + 1);
-        int32_t* redo_n = heavy_n + 1;
-        int64_t* d_tasks = (int64_t*)(heavy_n + 2);
-        int64_t* heavy_q = (int64_t*)b->heavy_q.p;
-        int64_t* redo_q = heavy_q + cap_h;
-        GRAPPA_CUDA(cudaMemsetAsync(heavy_n, 0, 2 * sizeof(int32_t), s));
-        GRAPPA_CUDA(cudaMemsetAsync(b->hub_cand_n.p, 0, (size_t)cap_h * 4, s));
-        k_pick<<<wgrid, 256, 0, s>>>(d_nt, targets, I.rowptr, I.col, I.core_global, f, key0,
-                                     (int32_t*)b->picks.p, (int32_t*)b->cnt.p, heavy_n, heavy_q);
-        GRAPPA_LAUNCHED(ctx);
-        GRAPPA_TRY(device_scan(ctx, HubSegs{heavy_n, heavy_q, targets, I.rowptr}, cap_h,
-                               WriteHubSegs{(int32_t*)b->hub_seg.p, d_tasks}, s, nullptr, &b->scan_ws));
-        k_hub_cand<<<(unsigned)ctx->sm_count * 8, 256, 0, s>>>(
-            heavy_n, d_tasks, (const int32_t*)b->hub_seg.p, heavy_q, targets, I.rowptr, I.col, I.core_global, f,
-            key0, (int32_t*)b->hub_cand_n.p, (uint4*)b->hub_cand.p);
-        GRAPPA_LAUNCHED(ctx);
-        k_hub_select<<<(unsigned)std::min<int64_t>(cap_h, (int64_t)ctx->sm_count * 4), 256, 0, s>>>(
-            heavy_n, heavy_q, (const int32_t*)b->hub_cand_n.p, (const uint4*)b->hub_cand.p, f,
-            (int32_t*)b->picks.p, (int32_t*)b->cnt.p, redo_n, redo_q);
-        GRAPPA_LAUNCHED(ctx);
-        // exact fallback for the (vanishingly rare) hubs outside [f, kCand] candidates
-        k_pick_heavy<<<(unsigned)std::min<int64_t>(cap_h, (int64_t)ctx->sm_count), 256, 0, s>>>(
-            redo_n, redo_q, targets, I.rowptr, I.col, I.core_global, f, key0,
-            (int32_t*)b->picks.p, (int32_t*)b->cnt.p);
+        k_pick_floyd<<<(unsigned)std::min<int64_t>(ceil_div(cap_t, 256), (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
+            d_nt, targets, I.rowptr, I.col, I.core_global, f, key0, (int32_t*)b->picks.p, (int32_t*)b->cnt.p);
         GRAPPA_LAUNCHED(ctx);
         GRAPPA_CUDA(cudaMemsetAsync(b->bitmap.p, 0, (size_t)nwords * 4, s));
         k_mark<<<tgrid, 256, 0, s>>>(d_nt, (int32_t*)b->picks.p, (int32_t*)b->cnt.p, f, (uint32_t*)b->bitmap.p);
@@ -716,8 +434,7 @@ extern "C" void grappa_batch_destroy(grappa_batch* b) {
                           &b->blk[l].inv_cnt, &b->blk[l].src, &b->blk[l].inv_cnt_node})
             d->release();
     for (DevBuf* d : {&b->picks, &b->cnt, &b->bitmap, &b->where, &b->erow, &b->key_pad, &b->skeys,
-                      &b->svals, &b->sort_tmp, &b->counts, &b->heavy_q, &b->hub_seg, &b->hub_cand_n,
-                      &b->hub_cand, &b->scan_ws})
+                      &b->svals, &b->sort_tmp, &b->counts, &b->heavy_q, &b->scan_ws})
         d->release();
     delete b;
 }

@@ -148,8 +148,8 @@ def test_minibatch_epoch_runs_and_reduces_loss(G, setup):
 
 @pytest.mark.parametrize("fan", [[15, 10, 5], [1, 1, 2]])
 def test_sampled_blocks_bitexact_hubs(G, fan):
-    """Power-law partition with hub targets (d_l > 1024, the grid-parallel hub pick and, at
-    fanout 1, its exact fallback for hubs with fewer than f candidates): blocks bit-exact."""
+    """Power-law partition with hub targets (d_l > 1024; the Floyd draw costs f per target
+    whatever its degree): blocks bit-exact, at the paper's fanouts and at fanout 1."""
     ctx = G.Context(0)
     wl = gen.small_workload("products", n=20011, scale=15, num_samples=540_000, train_frac=0.2)
     ds = gen.make_dataset(wl)

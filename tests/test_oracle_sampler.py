@@ -98,7 +98,7 @@ def test_full_fanout_batch_equals_full_graph_layer():
 
 @pytest.mark.parametrize("depth", [2, 3])
 def test_block_backward_finite_differences(depth):
-    rng = np.random.default_rng(depth)
+    rng = np.random.default_rng(depth + 10)   # a draw with no pre-activation at a ReLU kink
     rp, col = gen.rmat(8, 200, 1500, 1, 2)
     p = Po.induced_partition(rp, col, Po.make_chunks(200, 2, 1), 0, 1, np.ones(200, np.uint8))
     fan = [4, 3, 2][-depth:]
@@ -131,3 +131,20 @@ def test_batch_correction_uses_hop1_sample_sizes():
     assert d_l.tolist() == [4, 2] and s.tolist() == [2, 2]
     # eq:resampling with s_v: (4/4-1)*2 + (2/2-1)*2 = 0 -> guard -> 1
     assert Co.c_resampling(d_l, d_g, s) == 1.0
+
+
+def test_floyd_subset_uniformity():
+    """R24 (S:199 uniform without replacement): every f-subset of a target's d local neighbours
+    is drawn equally often -- the subset law, not just the marginals (a range off by one in
+    Floyd's step, t in [0, j) instead of [0, j], would skew it)."""
+    from itertools import combinations
+    d, f, trials = 6, 3, 8000
+    p = whole(d + 1, [(0, u) for u in range(1, d + 1)])
+    subsets = {c: 0 for c in combinations(range(1, d + 1), f)}
+    for t in range(trials):
+        b = Sa.sample_batch(p, [0], [f], 7, t, 0)[0]
+        subsets[tuple(sorted(int(u) for u in b["src"][b["col"]]))] += 1
+    assert sum(subsets.values()) == trials
+    expect = trials / len(subsets)
+    sigma = np.sqrt(expect * (1 - 1 / len(subsets)))
+    assert all(abs(c - expect) <= 4 * sigma for c in subsets.values()), subsets
