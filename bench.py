@@ -320,7 +320,9 @@ def run_grappa(args):
         # timed region repartitions + re-captures in place, amortised like the eager path
         tr.run_epoch_graph()
         barrier()
-    ctx.profile(not use_graph)
+    # the timed epochs run without the per-kernel-class event probes (their cudaEventRecord
+    # calls would add host work to host-bound loops); one extra profiled epoch follows
+    ctx.profile(False)
     l0 = ctx.launches()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     evs[0].record(stream)
@@ -337,12 +339,12 @@ def run_grappa(args):
     launches = ctx.launches() - l0
     if use_graph:
         launches += tr.graph_launches * args.steps
-        ctx.profile(True)              # per-kernel times from one extra eager epoch
-        tr.run_epoch()
-        # the switch inside the timed region ran outside any profile window: time one more
-        # (idempotent) extraction of the current super-epoch's partitions for the report
-        tr.repartition(tr.super_epoch())
-        tr.graph = None
+    ctx.profile(True)                  # per-kernel times from one extra eager epoch
+    tr.run_epoch()
+    # the switch inside the timed region ran outside any profile window: time one more
+    # (idempotent) extraction of the current super-epoch's partitions for the report
+    tr.repartition(tr.super_epoch())
+    tr.graph = None
     prof = {k: ctx.profile_read(k) for k in ("spmm", "gemm", "gemm_tn", "loss", "agg", "repart", "sample")}
     ctx.profile(False)
     ctx.check(stream)
@@ -367,7 +369,7 @@ def run_grappa(args):
                        "window_dram_bytes_per_call": rec["dram_bytes_per_call"],
                        "window_algorithmic_bytes_per_call": rec["algorithmic_bytes_per_call"]}
     rep_ms = prof["repart"][0]
-    if use_graph and prof["repart"][1]:
+    if prof["repart"][1]:
         # per switch = the profiled extractions / switches they make up, times the switches timed
         n_parts = sum(1 for _, w in tr.my_workers() if w < tr.W)
         rep_ms = prof["repart"][0] / (prof["repart"][1] / n_parts) * (-(-K // wl.repartition_every))
@@ -375,10 +377,10 @@ def run_grappa(args):
                 "frac": (achieved / hbm) if achieved else None,
                 "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": "k_spmm (+k_spmm_fixup)", "peak_kind": peak_kind,
-                "spmm_share_of_step": sp_ms / (ms / K if use_graph else ms), "spmm_launches": sp_n,
+                "spmm_share_of_step": sp_ms / (ms / K), "spmm_launches": sp_n,
                 "algorithmic_bytes_per_launch": sp_b / sp_n if sp_n else None}
-    # per-kernel-class totals: over the K timed epochs (eager), or over one extra eager epoch
-    # (graph replay: the replayed kernels are not individually timed) -- see "kernels_window"
+    # per-kernel-class totals over one extra eager epoch after the timed region (the timed
+    # epochs run without per-class event probes; replayed graphs are not timed per kernel)
     kernels = {k: {"ms": v[0], "calls": v[1], "GB/s": (v[2] / (v[0] / 1e3) / 1e9) if v[0] else None,
                    "TFLOP/s": (v[3] / (v[0] / 1e3) / 1e12) if v[0] and v[3] else None}
                for k, v in prof.items()}
@@ -414,7 +416,7 @@ def run_grappa(args):
                            "parallelism": f"dp{world} (phase-parallel, gradient-only)",
                            "generate_s": round(t_gen, 1)},
                 "roofline": roofline, "kernels": kernels,
-                "kernels_window": "1 eager epoch after the timed region" if use_graph else f"{K} timed epochs",
+                "kernels_window": "1 eager epoch after the timed region",
                 "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk}
         s = json.dumps(line)

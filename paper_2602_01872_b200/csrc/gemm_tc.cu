@@ -1008,7 +1008,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 // thread (o, g) sums slabs g, g + kRedGroups, ... in order (a few independent loads in flight),
 // then the group sums are added in group order -- a fixed summation tree, so the result is
 // bitwise deterministic.
-constexpr int kRedGroupsMax = 32;
 // A/B knobs (grappa_set_kernel_variant "tnstages" / "tnred"): ring depth (0 = fill shared
 // memory) and slab groups of the reduction (8 or 32)
 static int g_tn_stages = 4, g_tn_red = 8;   // 4 stages measured best (6-7 slower)
@@ -1018,7 +1017,7 @@ template <int kRedGroups>
 __global__ void __launch_bounds__(32 * kRedGroups) k_tn_reduce(int64_t count, int N, int K1, int K2, int ft1,
                                                                int ftiles, int slabs, const float* __restrict__ ws,
                                                                float* __restrict__ dw) {
-    __shared__ float part[kRedGroups][33];   // kRedGroups <= kRedGroupsMax
+    __shared__ float part[kRedGroups][33];
     const int o = threadIdx.x & 31, g = threadIdx.x >> 5;
     const int64_t i = (int64_t)blockIdx.x * 32 + o;
     float s = 0.f;

@@ -7,7 +7,7 @@
 // Per hop, all on the device (one host sync per batch, at the end, to size the layer calls):
 //   k_pick_floyd  thread per target: if d_l <= f take every neighbour, else f distinct
 //                 positions by Floyd's algorithm (R24), O(f) whatever the degree
-//   frontier      bitmap over the partition (atomicOr picks, clear targets), word-popcount
+//   frontier      bitmap over the partition (picks marked by k_pick_floyd, targets cleared), word-popcount
 //                 scan -> new sources in ascending local id; `where` maps local id -> position
 //   block CSR     rowptr = scan of pick counts; each target's positions sorted ascending
 //   transpose     stable radix sort of (source position, target) pairs -> CSC for backward
@@ -43,17 +43,23 @@ static uint64_t hmix(uint64_t x) {
 // already kept: every f-subset equally likely (uniform without replacement), O(f) work per
 // target whatever its degree (a hub costs what a leaf costs; the earlier hash-priority draw
 // hashed every neighbour).  One thread per target; picks in draw order (k_fill_block sorts).
+// The picked neighbours are also marked in the frontier bitmap here (cleared beforehand), which
+// saves the separate marking pass over the picks.
 __global__ void k_pick_floyd(const int64_t* __restrict__ d_nt, const int32_t* __restrict__ targets,
                              const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                              const int32_t* __restrict__ gid, int f, uint64_t key0, int32_t* __restrict__ picks,
-                             int32_t* __restrict__ cnt) {
+                             int32_t* __restrict__ cnt, uint32_t* __restrict__ bitmap) {
     const int64_t nt = *d_nt;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = targets[t];
         const int64_t e0 = rowptr[v], d = rowptr[v + 1] - e0;
         int32_t* out = picks + t * f;
         if (d <= f) {
-            for (int i = 0; i < (int)d; i++) out[i] = col[e0 + i];
+            for (int i = 0; i < (int)d; i++) {
+                const int32_t u = col[e0 + i];
+                out[i] = u;
+                atomicOr(&bitmap[u >> 5], 1u << (u & 31));
+            }
             cnt[t] = (int)d;
             continue;
         }
@@ -74,22 +80,17 @@ __global__ void k_pick_floyd(const int64_t* __restrict__ d_nt, const int32_t* __
             kept[k] = pos;
         }
         // neighbour ids of the kept positions (independent loads, issued together)
+        int32_t u[kMaxFanout];
 #pragma unroll
         for (int k = 0; k < kMaxFanout; k++)
-            if (k < f) out[k] = col[e0 + kept[k]];
+            if (k < f) u[k] = col[e0 + kept[k]];
+#pragma unroll
+        for (int k = 0; k < kMaxFanout; k++)
+            if (k < f) {
+                out[k] = u[k];
+                atomicOr(&bitmap[u[k] >> 5], 1u << (u[k] & 31));
+            }
         cnt[t] = f;
-    }
-}
-
-__global__ void k_mark(const int64_t* __restrict__ d_nt, const int32_t* __restrict__ picks,
-                       const int32_t* __restrict__ cnt, int f, uint32_t* __restrict__ bitmap) {
-    const int64_t n = *d_nt * f;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t t = i / f;
-        if (i - t * f < cnt[t]) {
-            const int32_t u = picks[i];
-            atomicOr(&bitmap[u >> 5], 1u << (u & 31));
-        }
     }
 }
 
@@ -331,11 +332,10 @@ extern "C" grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part*
         // h(seed, epoch, batch, hop) = mix(seed ^ mix(epoch ^ mix(batch ^ mix(hop))))
         const uint64_t key0 = hmix(seed ^ hmix((uint64_t)epoch ^ hmix((uint64_t)batch_index ^ hmix((uint64_t)h))));
         const unsigned tgrid = (unsigned)std::min<int64_t>(ceil_div(cap_nnz, 256), (int64_t)ctx->sm_count * 16);
-        k_pick_floyd<<<(unsigned)std::min<int64_t>(ceil_div(cap_t, 256), (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
-            d_nt, targets, I.rowptr, I.col, I.core_global, f, key0, (int32_t*)b->picks.p, (int32_t*)b->cnt.p);
-        GRAPPA_LAUNCHED(ctx);
         GRAPPA_CUDA(cudaMemsetAsync(b->bitmap.p, 0, (size_t)nwords * 4, s));
-        k_mark<<<tgrid, 256, 0, s>>>(d_nt, (int32_t*)b->picks.p, (int32_t*)b->cnt.p, f, (uint32_t*)b->bitmap.p);
+        k_pick_floyd<<<(unsigned)std::min<int64_t>(ceil_div(cap_t, 256), (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
+            d_nt, targets, I.rowptr, I.col, I.core_global, f, key0, (int32_t*)b->picks.p, (int32_t*)b->cnt.p,
+            (uint32_t*)b->bitmap.p);
         GRAPPA_LAUNCHED(ctx);
         k_unmark<<<(unsigned)std::min<int64_t>(ceil_div(cap_t, 256), 4096), 256, 0, s>>>(
             d_nt, targets, (uint32_t*)b->bitmap.p, (int32_t*)b->where.p, (int32_t*)B.src.p);
