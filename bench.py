@@ -274,7 +274,7 @@ def run_grappa(args):
         ctx = G.Context(local)
     for kv in args.variant:
         op, val = kv.split("=")
-        G._lib.check("grappa_set_kernel_variant", G.load().grappa_set_kernel_variant(op.encode(), int(val)))
+        ctx.set_variant(op, int(val))
 
     t_gen = time.perf_counter()
     wl, ds = build_dataset(args.config)

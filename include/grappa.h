@@ -129,9 +129,24 @@ const char* grappa_last_error(void);
 grappa_status grappa_nccl_unique_id(void* out128 /* host, 128 bytes */);
 
 /* Create a context on `device`.  nccl_uid == NULL or nranks == 1 -> single GPU, no NCCL.
- * Otherwise a collective: every rank must call it with the same uid (ncclCommInitRank). */
+ * Otherwise a collective: every rank must call it with the same uid (ncclCommInitRank).
+ * Library-owned device memory is cudaMalloc'd (grappa_ctx_create_ex to supply an allocator). */
 grappa_status grappa_ctx_create(int device, const void* nccl_uid, int rank, int nranks,
                                 grappa_ctx** out);
+/* Caller allocator for the device memory of library-owned objects (partitions, shards, batches,
+ * ctx workspaces): alloc(bytes, stream, user) returns a device pointer usable on `stream` (the
+ * stream of the API call that grows the buffer; NULL = legacy default) or NULL on failure
+ * (-> GRAPPA_E_NOMEM); free(ptr, bytes, stream, user) returns it (stream = the one it was
+ * allocated for; the library frees only after its own work on that stream is enqueued, so a
+ * stream-ordered pool such as PyTorch's caching allocator may reuse it in stream order).  Buffers
+ * grown while the call's stream is being captured into a CUDA graph are cudaMalloc'd instead.
+ * Objects keep the allocator they were grown with, so the callbacks must stay valid until every
+ * object created through this ctx is destroyed.  alloc == NULL or free == NULL -> cudaMalloc. */
+typedef void* (*grappa_alloc_fn)(size_t bytes, void* stream, void* user);
+typedef void (*grappa_free_fn)(void* ptr, size_t bytes, void* stream, void* user);
+grappa_status grappa_ctx_create_ex(int device, const void* nccl_uid, int rank, int nranks,
+                                   grappa_alloc_fn alloc, grappa_free_fn free_fn, void* alloc_user,
+                                   grappa_ctx** out);
 void grappa_ctx_destroy(grappa_ctx* ctx);
 
 /* a1 -- random chunking, performed once (§3.3; reading R1):
@@ -216,10 +231,14 @@ typedef struct {
 } grappa_shard_xfer;
 /* Collective over the ctx's NCCL communicator (ctx created with a uid, any nranks >= 1):
  * every transfer listed on one rank must be matched by the opposite transfer on its peer, and
- * transfers between the same two ranks must be listed in the same order on both.  Two grouped
+ * transfers between the same two ranks must be listed in the same order on both.  Three grouped
  * NCCL rounds: a 32-byte header per transfer (then one host sync to size the receive buffers),
- * then the arrays (ids, rowptr, col, x, labels, train).  Errors: E_ARG no communicator / bad
- * peer / both or neither of send, recv; E_NCCL. */
+ * an 8-byte status from every receiver to its sender (one more host sync: both sides of every
+ * transfer agree that the receiver could allocate before any array moves, so a failure on one
+ * rank is reported on its peers instead of leaving them in an unmatched send), then the arrays
+ * (ids, rowptr, col, x, labels, train; counted in grappa_comm_bytes' `other`).  Errors: E_ARG
+ * no communicator / bad peer / both or neither of send, recv / malformed header; E_NOMEM;
+ * E_NCCL (also on a sender whose receiver failed). */
 grappa_status grappa_shard_exchange(grappa_ctx* ctx, int32_t n_xfers, const grappa_shard_xfer* xfers,
                                     void* stream);
 /* a3 from two shards: the partition of chunk pair {base->chunk, swept->chunk} (rank table from
@@ -368,21 +387,40 @@ grappa_status grappa_loss_ex(grappa_ctx* ctx, const grappa_part* part, const voi
 
 /* a7 + a8 -- coverage-corrected aggregation and optimizer step (P:291-306 eq:batch-estimator,
  * Alg. 1, "applied immediately before the all-reduce"):
- *   grad <- c_p / m_active * grad (fused scale + non-finite check, device flag), then
- *   ncclAllReduce(sum) across the context's ranks  =>  grad = (1/M) sum_p c_p g_p (R9),
- *   then, if lr != 0, theta <- theta - lr * grad (SGD, R10).
+ *   comm <- (c_p / m_active) * grad, cast to comm_dtype (one fused scale/cast pass that also
+ *   flags non-finite values), then ncclAllReduce(sum) of comm across the context's ranks
+ *   =>  grad = (1/M) sum_p c_p g_p (R9; fp32, or rounded to bf16 once and summed in bf16 by
+ *   NCCL when comm_dtype = GRAPPA_BF16), then, if lr != 0, theta <- theta - lr * grad (SGD,
+ *   S:429-437, R10).  The update is skipped on the device when the aggregated gradient -- or any
+ *   aggregated since the last grappa_check -- is non-finite ("non-finite grad -> error"):
+ *   theta is never written with a non-finite step, and grappa_check reports E_NONFINITE.
  *   part == NULL marks a rank with no active partition in this phase (contributes zeros).
- *   c_p is the factor of kind `corr` computed at repartition time (grappa_part_info); 1 for
- *   GRAPPA_CORR_NONE and GRAPPA_CORR_NODE (node-level: the correction is in the gradient).
- *   grad, theta: dev fp32 [n_params].  A COLLECTIVE when the ctx has >1 rank.           */
+ *   c_p is the factor of kind `corr` from the partition's coverage statistics
+ *   (grappa_part_info): UNIFORM c_uniform; RESAMPLING from the exact integer D:
+ *   1 if D < eps, else min(1/D, c_max) (SPEC CorrectionConfig S:311-314 --
+ *   eps > 0, c_max >= 1; the oracle's defaults are 1e-9 and 10); RESAMPLING_HM c_resampling_hm;
+ *   1 for NONE and NODE (node-level: the correction is in the gradient).
+ *   grad, theta: dev fp32 [n_params].  A COLLECTIVE when the ctx has >1 rank.
+ *   Errors: E_ARG (null, m_active < 1, eps <= 0, c_max < 1, unknown corr / comm_dtype, lr != 0
+ *   without theta); E_NONFINITE if c_p is not finite; E_NOMEM (bf16 comm buffer);
+ *   E_NCCL. */
 grappa_status grappa_aggregate_grads(grappa_ctx* ctx, const grappa_part* part, grappa_corr corr,
-                                     float* grad, int64_t n_params, int32_t m_active, float lr,
-                                     float* theta, void* stream);
+                                     double eps, double c_max, float* grad, int64_t n_params,
+                                     int32_t m_active, grappa_dtype comm_dtype, float lr, float* theta,
+                                     void* stream);
 
 /* a7 with an explicit factor (mini-batch mode: c_p is the batch's factor, grappa_batch_factors).
  * Same semantics as grappa_aggregate_grads with c_p = c (c = 0 for an idle rank). */
 grappa_status grappa_aggregate_grads_c(grappa_ctx* ctx, double c, float* grad, int64_t n_params,
-                                       int32_t m_active, float lr, float* theta, void* stream);
+                                       int32_t m_active, grappa_dtype comm_dtype, float lr, float* theta,
+                                       void* stream);
+
+/* Bytes this ctx has moved between GPUs since creation, by purpose (host counters, updated when
+ * a call enqueues the transfer): grad = gradient all-reduce payloads (per rank, the buffer
+ * size of every ncclAllReduce), other = everything else (shard / halo exchange at super-epoch
+ * switches).  The paper's invariant "cross-server traffic consists only of gradient all-reduce"
+ * is that `other` does not grow inside training iterations. */
+grappa_status grappa_comm_bytes(const grappa_ctx* ctx, int64_t* grad_bytes, int64_t* other_bytes);
 
 /* ---------------------------------------------------------------- a10: mini-batch mode
  * Isolated mini-batch sampling (config 4): P:139/P:177 (§3.2 sampling mode, k-hop subgraphs
@@ -495,24 +533,35 @@ typedef enum {
     GRAPPA_K_SAMPLE = 6,     /* mini-batch sampler (grappa_sample, incl. its one host sync) */
     GRAPPA_K_NCLASS = 7
 } grappa_kclass;
-/* Test / A-B hook (process wide): select an alternative kernel implementation so tests can
- * cross-check them.  op "gemm": 0 = auto (tcgen05 for bf16, split-fp32 tcgen05 for fp32),
- * 1 = CUDA-core kernels (bf16; 128x128 FFMA tiles for fp32), 2 = the small-tile CUDA-core
- * kernels for both dtypes.
- * op "spmm": 0 = auto (row-group kernel for rows of <= 32 vectors, degree-bucketed row
- * order), 1 = warp-per-row, 2 = row-group with 8 loads in flight, 3 = row-group, natural order.
- * op "fuse": 0 = off (default), 1 = bf16 GCN layers run the fused aggregate->transform kernel
- * (SpMM gather into a shared-memory tile + tcgen05 transform in the same kernel) where the
- * aggregate is the narrower side.
- * op "wide": 0 = unweighted bf16 gathers use 16-byte lanes (default), 1 = 32-byte lanes.
- * op "tnstages": ring depth of the tcgen05 weight-gradient GEMM (default 4; 0 = fill shared memory).
- * op "tnred": slab groups of its fixed-order split-K reduction (8 default, or 32).
- * op "pair": 0 = GCN backward runs dz_in and dW as one pass over dT and h_in (default, bf16),
- * 1 = the two separate GEMMs.
- * op "x3dbg": timing probes of the split-fp32 transform only (results invalid when != 0):
- * bit 1 no A loads, 2 no output stores, 4 no weight staging, 8 one MMA per K step, 16 no epilogue.
- * Returns E_ARG for an unknown op. */
-grappa_status grappa_set_kernel_variant(const char* op, int variant);
+/* Test hook (per ctx): select an alternative implementation of the same arithmetic so tests can
+ * cross-check kernels against each other.  Every variant computes the documented result.
+ *   op "gemm": 0 = tensor cores (tcgen05 for bf16, split-fp32 tcgen05 for fp32; default),
+ *              1 = CUDA-core kernels (bf16; 128x128 FFMA tiles for fp32), 2 = small-tile CUDA-core.
+ *   op "spmm": 0 = row-group kernel (rows of <= 32 vectors) over the degree-bucketed row order
+ *              (default), 1 = warp per row, 2 = row-group with 8 loads in flight, 3 = row-group
+ *              over the natural row order.
+ *   op "pair": 0 = GCN backward computes dz_in and dW in one pass over dT and h_in (bf16,
+ *              default), 1 = the two separate GEMMs.
+ * Returns E_ARG for a null ctx, an unknown op or an out-of-range variant. */
+grappa_status grappa_set_kernel_variant(grappa_ctx* ctx, const char* op, int variant);
+
+/* Roofline probes (diagnostics; bench.py's live ceilings).  Allocates its own
+ * buffers (cudaMalloc / cudaFree: synchronises the device; never call inside graph capture),
+ * runs one warm-up launch and `iters` timed launches on `stream` (CUDA events) and returns the
+ * achieved bandwidth in *gbps (1e9 bytes/s):
+ *   GRAPPA_PROBE_HBM_COPY    dst = src over `bytes` each (use bytes >> L2): (read + write) / time
+ *   GRAPPA_PROBE_L2_READ     8 passes of coalesced 16-byte reads over `bytes` (L2-resident if
+ *                            bytes < L2): bytes read / time
+ *   GRAPPA_PROBE_L2_GATHER   whole-row gathers of a `bytes`-sized table of row_bytes rows (16 *
+ *                            a divisor of 32) at random row ids read from an index array, the
+ *                            SpMM's access pattern with no arithmetic: row bytes / time
+ * Errors: E_ARG (bytes < 1 MiB or not a multiple of 16, iters < 1, bad row_bytes or kind),
+ * E_NOMEM. */
+#define GRAPPA_PROBE_HBM_COPY 0
+#define GRAPPA_PROBE_L2_READ 1
+#define GRAPPA_PROBE_L2_GATHER 2
+grappa_status grappa_roofline_probe(grappa_ctx* ctx, int kind, int64_t bytes, int32_t row_bytes, int32_t iters,
+                                    double* gbps, void* stream);
 
 grappa_status grappa_profile_enable(grappa_ctx* ctx, int on);
 grappa_status grappa_profile_read(grappa_ctx* ctx, int kclass, double* ms, int64_t* calls,

@@ -53,19 +53,55 @@ def _view(ptr, shape, typestr, owner):
     return torch.as_tensor(_DevView(ptr, shape, typestr, owner), device="cuda")
 
 
-class Context:
-    """grappa_ctx: one per process + GPU (holds the NCCL communicator when world > 1)."""
+def _torch_alloc(nbytes, stream, user):
+    """grappa_alloc_fn over PyTorch's caching allocator (stream-ordered; no cudaFree sync)."""
+    try:
+        dev = torch.cuda.current_device()
+        return torch.cuda.caching_allocator_alloc(int(nbytes), dev, int(stream or 0)) or None
+    except Exception:          # out of memory -> NULL -> GRAPPA_E_NOMEM
+        return None
 
-    def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1, nccl_uid: bytes | None = None):
+
+def _torch_free(ptr, nbytes, stream, user):
+    if ptr:
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+
+# module-level: library objects may outlive any one Context and free through these
+_ALLOC_CB = _lib.ALLOC_FN(_torch_alloc)
+_FREE_CB = _lib.FREE_FN(_torch_free)
+
+
+class Context:
+    """grappa_ctx: one per process + GPU (holds the NCCL communicator when world > 1).  Library-owned
+    device memory comes from PyTorch's caching allocator (grappa_ctx_create_ex) unless
+    torch_alloc=False (cudaMalloc)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1, nccl_uid: bytes | None = None,
+                 torch_alloc: bool = True):
         lib = load()
         self.lib = lib
         h = ctypes.c_void_p()
         uid = None
         if nccl_uid is not None:
             uid = ctypes.create_string_buffer(bytes(nccl_uid), 128)
-        _lib.check("grappa_ctx_create", lib.grappa_ctx_create(device, uid, rank, nranks, ctypes.byref(h)))
+        if torch_alloc:
+            _lib.check("grappa_ctx_create_ex", lib.grappa_ctx_create_ex(device, uid, rank, nranks, _ALLOC_CB,
+                                                                        _FREE_CB, None, ctypes.byref(h)))
+        else:
+            _lib.check("grappa_ctx_create", lib.grappa_ctx_create(device, uid, rank, nranks, ctypes.byref(h)))
         self.h = h
         self.device, self.rank, self.nranks = device, rank, nranks
+
+    def set_variant(self, op: str, variant: int):
+        """grappa_set_kernel_variant (tests: cross-check alternative kernels on this ctx)."""
+        _lib.check("grappa_set_kernel_variant", self.lib.grappa_set_kernel_variant(self.h, op.encode(), int(variant)))
+
+    def comm_bytes(self):
+        """(gradient all-reduce bytes, every other cross-GPU byte) moved by this ctx so far."""
+        g, o = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check("grappa_comm_bytes", self.lib.grappa_comm_bytes(self.h, ctypes.byref(g), ctypes.byref(o)))
+        return g.value, o.value
 
     @staticmethod
     def nccl_unique_id() -> bytes:
@@ -87,6 +123,15 @@ class Context:
             self.h, _lib.KCLASS[kclass], ctypes.byref(ms), ctypes.byref(n), ctypes.byref(by),
             ctypes.byref(fl)))
         return ms.value, n.value, by.value, fl.value
+
+    def roofline_probe(self, kind: str, nbytes: int, row_bytes: int = 256, iters: int = 5, stream=None) -> float:
+        """grappa_roofline_probe: measured GB/s of an HBM copy, an L2-resident read or an
+        L2-resident whole-row gather (the SpMM's access pattern without arithmetic)."""
+        g = ctypes.c_double()
+        _lib.check("grappa_roofline_probe", self.lib.grappa_roofline_probe(
+            self.h, _lib.PROBE[kind], int(nbytes), int(row_bytes), int(iters), ctypes.byref(g),
+            _lib.stream_ptr(stream)))
+        return g.value
 
     def check(self, stream=None):
         _lib.check("grappa_check", self.lib.grappa_check(self.h, _lib.stream_ptr(stream)))
@@ -345,16 +390,18 @@ def grappa_loss(ctx: Context, part: Part, logits, num_classes, k_pad, dlogits, l
 
 
 def grappa_aggregate_grads(ctx: Context, part: Part | None, corr: str, grad, m_active: int, lr: float,
-                           theta, stream=None):
+                           theta, stream=None, eps: float = 1e-9, c_max: float = 10.0, comm_dtype="f32"):
     _lib.check("grappa_aggregate_grads", ctx.lib.grappa_aggregate_grads(
-        ctx.h, part.h if part is not None else None, CORR[corr], _lib.ptr(grad), grad.numel(),
-        m_active, ctypes.c_float(lr), _lib.ptr(theta), _lib.stream_ptr(stream)))
+        ctx.h, part.h if part is not None else None, CORR[corr], ctypes.c_double(eps), ctypes.c_double(c_max),
+        _lib.ptr(grad), grad.numel(), m_active, dtype_code(comm_dtype), ctypes.c_float(lr), _lib.ptr(theta),
+        _lib.stream_ptr(stream)))
 
 
-def grappa_aggregate_grads_c(ctx: Context, c: float, grad, m_active: int, lr: float, theta, stream=None):
+def grappa_aggregate_grads_c(ctx: Context, c: float, grad, m_active: int, lr: float, theta, stream=None,
+                             comm_dtype="f32"):
     _lib.check("grappa_aggregate_grads_c", ctx.lib.grappa_aggregate_grads_c(
-        ctx.h, ctypes.c_double(c), _lib.ptr(grad), grad.numel(), m_active, ctypes.c_float(lr),
-        _lib.ptr(theta), _lib.stream_ptr(stream)))
+        ctx.h, ctypes.c_double(c), _lib.ptr(grad), grad.numel(), m_active, dtype_code(comm_dtype),
+        ctypes.c_float(lr), _lib.ptr(theta), _lib.stream_ptr(stream)))
 
 
 # ------------------------------------------------------------------ a10: mini-batch mode

@@ -19,6 +19,7 @@ BWD_DZ_OUT_NORMED, BWD_DZ_IN_NORMED = 1, 2
 LAYER_NODE_LEVEL = 4
 LAYER_INPUT = 8
 PART_HALO1 = 1
+PROBE = {"hbm_copy": 0, "l2_read": 1, "l2_gather": 2}
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_SHAPE", 3: "E_EMPTY", 4: "E_NONFINITE", 5: "E_SUPPORT",
           6: "E_NOMEM", 7: "E_CUDA", 8: "E_NCCL"}
 
@@ -36,8 +37,15 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_sample_event", "grappa_repartition_ex", "grappa_part_image_bytes",
            "grappa_part_save", "grappa_part_image_info", "grappa_part_load", "grappa_layer_saved_bytes_ex",
            "grappa_loss_ex", "grappa_shard_extract", "grappa_shard_query", "grappa_shard_destroy",
-           "grappa_shard_exchange", "grappa_repartition_shards"]
+           "grappa_shard_exchange", "grappa_repartition_shards", "grappa_roofline_probe",
+           "grappa_ctx_create_ex", "grappa_comm_bytes"]
 KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5, "sample": 6}
+
+
+# caller allocator callbacks (grappa_ctx_create_ex): void* alloc(size_t, void* stream, void* user),
+# void free(void* ptr, size_t, void* stream, void* user)
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
 
 
 class GrappaError(RuntimeError):
@@ -141,14 +149,17 @@ def load(path: str = LIB_PATH):
                                      ctypes.c_int, ctypes.c_uint, vp]),
         "grappa_loss": (st, [vp, vp, vp, i32, i32, vp, vp, ctypes.c_int, vp]),
         "grappa_loss_ex": (st, [vp, vp, vp, i32, i32, vp, vp, ctypes.c_int, ctypes.c_uint, vp]),
-        "grappa_aggregate_grads": (st, [vp, vp, ctypes.c_int, vp, i64, i32, f32, vp, vp]),
+        "grappa_aggregate_grads": (st, [vp, vp, ctypes.c_int, dbl, dbl, vp, i64, i32, ctypes.c_int, f32, vp, vp]),
+        "grappa_comm_bytes": (st, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+        "grappa_ctx_create_ex": (st, [ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ALLOC_FN, FREE_FN, vp,
+                                      ctypes.POINTER(vp)]),
         "grappa_check": (st, [vp, vp]),
         "grappa_launch_count": (i64, [vp]),
         "grappa_profile_enable": (st, [vp, ctypes.c_int]),
-        "grappa_set_kernel_variant": (st, [ctypes.c_char_p, ctypes.c_int]),
+        "grappa_set_kernel_variant": (st, [vp, ctypes.c_char_p, ctypes.c_int]),
         "grappa_part_download": (st, [vp, ctypes.POINTER(PartHost), vp]),
         "grappa_part_upload": (st, [vp, ctypes.POINTER(PartHost), vp]),
-        "grappa_aggregate_grads_c": (st, [vp, dbl, vp, i64, i32, f32, vp, vp]),
+        "grappa_aggregate_grads_c": (st, [vp, dbl, vp, i64, i32, ctypes.c_int, f32, vp, vp]),
         "grappa_epoch_seeds": (st, [vp, vp, u64, i64, vp, vp]),
         "grappa_sample": (st, [vp, vp, vp, i32, vp, i32, u64, i64, i64, ctypes.POINTER(vp), vp]),
         "grappa_sample_async": (st, [vp, vp, vp, i32, vp, i32, u64, i64, i64, ctypes.POINTER(vp), vp]),
@@ -161,6 +172,7 @@ def load(path: str = LIB_PATH):
         "grappa_minibatch_step": (st, [vp, vp, vp, i32, vp, i32, vp, vp, vp, sz, vp, vp, ctypes.c_int, vp]),
         "grappa_minibatch_step_ex": (st, [vp, vp, vp, i32, vp, i32, vp, vp, vp, sz, vp, vp, ctypes.c_int,
                                           ctypes.c_uint, vp]),
+        "grappa_roofline_probe": (st, [vp, ctypes.c_int, i64, i32, i32, ctypes.POINTER(dbl), vp]),
         "grappa_profile_read": (st, [vp, ctypes.c_int, ctypes.POINTER(dbl), ctypes.POINTER(i64),
                                      ctypes.POINTER(dbl), ctypes.POINTER(dbl)]),
     }

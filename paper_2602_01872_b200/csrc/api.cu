@@ -21,28 +21,60 @@ void set_error(const char* fmt, ...) {
     va_end(ap);
 }
 
+static thread_local std::shared_ptr<const Allocator> tl_alloc;
+static thread_local void* tl_stream = nullptr;
+
+CallScope::CallScope(const grappa_ctx* ctx, void* stream) : prev_al(tl_alloc), prev_stream(tl_stream) {
+    tl_alloc = ctx ? ctx->alloc : nullptr;
+    tl_stream = stream;
+}
+CallScope::~CallScope() {
+    tl_alloc = prev_al;
+    tl_stream = prev_stream;
+}
+
 grappa_status DevBuf::grow(size_t bytes) {
     if (bytes <= cap && p) return GRAPPA_OK;
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
+    release();
     // 1/8 headroom: partition sizes fluctuate by a few % across super-epochs, and a realloc
-    // (cudaFree synchronises the device) inside a switch is what we want to avoid
+    // inside a switch is what we want to avoid
     size_t b = bytes < 256 ? 256 : bytes + bytes / 8;
-    cudaError_t e = cudaMalloc(&p, b);
-    if (e != cudaSuccess) {
-        p = nullptr;
-        set_error("cudaMalloc(%zu): %s", b, cudaGetErrorString(e));
-        return GRAPPA_E_NOMEM;
+    std::shared_ptr<const Allocator> a = tl_alloc;
+    if (a) {
+        // a caller pool bound to a stream under graph capture would tie the block to the graph
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing((cudaStream_t)tl_stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+            a = nullptr;
+    }
+    if (a) {
+        p = a->alloc(b, tl_stream, a->user);
+        if (!p) {
+            set_error("caller allocator failed for %zu bytes", b);
+            return GRAPPA_E_NOMEM;
+        }
+        al = a;
+        al_stream = tl_stream;
+    } else {
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            set_error("cudaMalloc(%zu): %s", b, cudaGetErrorString(e));
+            return GRAPPA_E_NOMEM;
+        }
+        al = nullptr;
     }
     cap = b;
     return GRAPPA_OK;
 }
 
 void DevBuf::release() {
-    if (p) cudaFree(p);
+    if (p) {
+        if (al) al->free(p, cap, al_stream, al->user);
+        else cudaFree(p);
+    }
     p = nullptr;
     cap = 0;
+    al = nullptr;
 }
 
 static cudaEvent_t take_event(grappa_ctx* c) {
@@ -96,6 +128,12 @@ extern "C" grappa_status grappa_nccl_unique_id(void* out128) {
 
 extern "C" grappa_status grappa_ctx_create(int device, const void* nccl_uid, int rank, int nranks,
                                            grappa_ctx** out) {
+    return grappa_ctx_create_ex(device, nccl_uid, rank, nranks, nullptr, nullptr, nullptr, out);
+}
+
+extern "C" grappa_status grappa_ctx_create_ex(int device, const void* nccl_uid, int rank, int nranks,
+                                              grappa_alloc_fn alloc, grappa_free_fn free_fn, void* alloc_user,
+                                              grappa_ctx** out) {
     GRAPPA_ARG(out, GRAPPA_E_ARG, "grappa_ctx_create: null out");
     GRAPPA_ARG(nranks >= 1 && rank >= 0 && rank < nranks, GRAPPA_E_ARG,
                "grappa_ctx_create: bad rank %d / nranks %d", rank, nranks);
@@ -104,6 +142,13 @@ extern "C" grappa_status grappa_ctx_create(int device, const void* nccl_uid, int
     c->device = device;
     c->rank = rank;
     c->nranks = nranks;
+    if (alloc && free_fn) {
+        auto a = std::make_shared<Allocator>();
+        a->alloc = alloc;
+        a->free = free_fn;
+        a->user = alloc_user;
+        c->alloc = a;
+    }
     cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
     if (cudaMalloc(&c->d_flag, sizeof(int)) != cudaSuccess || cudaMemset(c->d_flag, 0, sizeof(int)) != cudaSuccess) {
         delete c;
@@ -127,6 +172,13 @@ extern "C" grappa_status grappa_ctx_create(int device, const void* nccl_uid, int
     return GRAPPA_OK;
 }
 
+extern "C" grappa_status grappa_comm_bytes(const grappa_ctx* ctx, int64_t* grad_bytes, int64_t* other_bytes) {
+    GRAPPA_ARG(ctx && grad_bytes && other_bytes, GRAPPA_E_ARG, "grappa_comm_bytes: null argument");
+    *grad_bytes = ctx->comm_grad_bytes;
+    *other_bytes = ctx->comm_other_bytes;
+    return GRAPPA_OK;
+}
+
 extern "C" void grappa_ctx_destroy(grappa_ctx* c) {
     if (!c) return;
     if (c->comm) ncclCommDestroy((ncclComm_t)c->comm);
@@ -136,6 +188,7 @@ extern "C" void grappa_ctx_destroy(grappa_ctx* c) {
     c->rp_ws.release();
     c->sh_ws.release();
     c->xf_hdr.release();
+    c->comm_buf.release();
     for (auto& r : c->prof) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -147,21 +200,12 @@ extern "C" void grappa_ctx_destroy(grappa_ctx* c) {
 
 extern "C" int64_t grappa_launch_count(const grappa_ctx* c) { return c ? c->launches : 0; }
 
-namespace grappa { void spmm_force_warp_per_row(int on); }
-// 1: GCN backward runs the two separate GEMMs instead of the one-pass pair (A/B, tests)
-static int g_pair_off = 0;
-
-extern "C" grappa_status grappa_set_kernel_variant(const char* op, int variant) {
-    GRAPPA_ARG(op, GRAPPA_E_ARG, "grappa_set_kernel_variant: null op");
-    if (!strcmp(op, "gemm")) { gemm_force_simt(variant); return GRAPPA_OK; }
-    if (!strcmp(op, "spmm")) { spmm_force_warp_per_row(variant); return GRAPPA_OK; }
-    if (!strcmp(op, "fuse")) { spmm_set_fuse(variant); return GRAPPA_OK; }
-    if (!strcmp(op, "wide")) { spmm_set_wide(variant); return GRAPPA_OK; }
-    if (!strcmp(op, "tnstages")) { gemm_tn_set_stages(variant); return GRAPPA_OK; }
-    if (!strcmp(op, "x3dbg")) { gemm_x3_set_dbg(variant); return GRAPPA_OK; }
-    if (!strcmp(op, "pair")) { g_pair_off = variant; return GRAPPA_OK; }
-    if (!strcmp(op, "tnred")) { gemm_tn_set_red(variant); return GRAPPA_OK; }
-    set_error("grappa_set_kernel_variant: unknown op '%s'", op);
+extern "C" grappa_status grappa_set_kernel_variant(grappa_ctx* ctx, const char* op, int variant) {
+    GRAPPA_ARG(ctx && op, GRAPPA_E_ARG, "grappa_set_kernel_variant: null argument");
+    if (!strcmp(op, "gemm") && variant >= 0 && variant <= 2) { ctx->var_gemm = variant; return GRAPPA_OK; }
+    if (!strcmp(op, "spmm") && variant >= 0 && variant <= 3) { ctx->var_spmm = variant; return GRAPPA_OK; }
+    if (!strcmp(op, "pair") && variant >= 0 && variant <= 1) { ctx->var_pair = variant; return GRAPPA_OK; }
+    set_error("grappa_set_kernel_variant: unknown op '%s' or variant %d", op, variant);
     return GRAPPA_E_ARG;
 }
 
@@ -229,16 +273,14 @@ extern "C" size_t grappa_layer_ws_bytes(const grappa_part* part, grappa_arch arc
     size_t node = (size_t)n * (arch == GRAPPA_GCN ? f_out : f_in) * es;       // T / dT / dM
     size_t partial = (size_t)slots * wmax * 4;
     size_t splitk = gemm_tn_ws_bytes(n, f_in, arch == GRAPPA_GCN ? 0 : f_in, f_out);
-    size_t hagg = (size_t)part->info.n_heavy * wmax * es;                    // fused path
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
-    return al(node) + al(partial) + al(splitk) + al(hagg);
+    return al(node) + al(partial) + al(splitk);
 }
 
 struct WsLayout {
     void* node;
     float* partial;
     float* splitk;
-    void* hagg;
 };
 static WsLayout carve(const grappa_part* part, grappa_arch arch, int f_in, int f_out,
                       grappa_dtype dt, void* ws) {
@@ -248,9 +290,8 @@ static WsLayout carve(const grappa_part* part, grappa_arch arch, int f_in, int f
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     size_t node = al((size_t)n * (arch == GRAPPA_GCN ? f_out : f_in) * es);
     size_t partial = al((size_t)slots * wmax * 4);
-    size_t splitk = al(gemm_tn_ws_bytes(n, f_in, arch == GRAPPA_GCN ? 0 : f_in, f_out));
     char* b = (char*)ws;
-    return WsLayout{b, (float*)(b + node), (float*)(b + node + partial), b + node + partial + splitk};
+    return WsLayout{b, (float*)(b + node), (float*)(b + node + partial)};
 }
 
 static grappa_status check_dims(const char* who, int f_in, int f_out) {
@@ -263,6 +304,7 @@ extern "C" grappa_status grappa_layer_fwd(grappa_ctx* ctx, const grappa_part* pa
                                           int32_t f_in, int32_t f_out, int relu, const void* h_in,
                                           const float* w, void* h_out, void* saved, void* ws,
                                           grappa_dtype dtype, void* stream) {
+    CallScope call_scope(ctx, stream);
     return grappa_layer_fwd_ex(ctx, part, arch, f_in, f_out, relu, h_in, w, h_out, saved, ws, dtype, 0u,
                                stream);
 }
@@ -271,6 +313,7 @@ extern "C" grappa_status grappa_layer_fwd_ex(grappa_ctx* ctx, const grappa_part*
                                              int32_t f_in, int32_t f_out, int relu, const void* h_in,
                                              const float* w, void* h_out, void* saved, void* ws,
                                              grappa_dtype dtype, unsigned flags, void* stream) {
+    CallScope call_scope(ctx, stream);
     GRAPPA_ARG((flags & ~(GRAPPA_LAYER_NODE_LEVEL | GRAPPA_LAYER_INPUT)) == 0, GRAPPA_E_ARG,
                "grappa_layer_fwd_ex: flags 0x%x invalid", flags);
     GRAPPA_ARG(arch != GRAPPA_GCN || !(flags & GRAPPA_LAYER_INPUT) || saved, GRAPPA_E_ARG,
@@ -301,14 +344,6 @@ extern "C" grappa_status grappa_layer_fwd_ex(grappa_ctx* ctx, const grappa_part*
         g.M = I.n_core; g.K1 = f_in; g.N = f_out; g.A1 = saved; g.B = w; g.relu = relu; g.n_split = f_out;
         g.C1 = h_out;
         return gemm_nn(ctx, g, dtype, s);
-    }
-    if (arch == GRAPPA_GCN && !node && f_in <= f_out && spmm_mm_supported(part, f_in, f_out, dtype)) {
-        // h_out = act((Ahat h_in) W): aggregate at the narrower width, transform fused into
-        // the aggregation kernel (tcgen05 on the smem-resident tile)
-        AggMMArgs m;
-        m.X = h_in; m.K = f_in; m.row_scale = I.norm_gcn; m.col_scale = I.norm_gcn; m.self = 1;
-        m.W = w; m.N = f_out; m.relu = relu; m.out = h_out; m.hagg = L.hagg; m.partial = L.partial;
-        return spmm_mm(ctx, part, m, s);
     }
     if (arch == GRAPPA_GCN) {
         // T = h_in W  (transform first: SpMM width = f_out)
@@ -342,6 +377,7 @@ extern "C" grappa_status grappa_layer_bwd(grappa_ctx* ctx, const grappa_part* pa
                                           const void* h_in, const float* w, const void* saved,
                                           float* dw, void* dz_in, void* ws, grappa_dtype dtype,
                                           void* stream) {
+    CallScope call_scope(ctx, stream);
     return grappa_layer_bwd_ex(ctx, part, arch, f_in, f_out, relu_in, dz_out, h_in, w, saved, dw, dz_in,
                                ws, dtype, 0u, stream);
 }
@@ -351,6 +387,7 @@ extern "C" grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part*
                                              const void* h_in, const float* w, const void* saved,
                                              float* dw, void* dz_in, void* ws, grappa_dtype dtype,
                                              unsigned flags, void* stream) {
+    CallScope call_scope(ctx, stream);
     GRAPPA_ARG((flags & ~(3u | GRAPPA_LAYER_NODE_LEVEL | GRAPPA_LAYER_INPUT)) == 0 &&
                    ((flags & 3u) == 0 || arch == GRAPPA_GCN),
                GRAPPA_E_ARG, "grappa_layer_bwd_ex: flags 0x%x invalid (normalised gradients are GCN-only)", flags);
@@ -378,18 +415,6 @@ extern "C" grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part*
         return gemm_tn(ctx, t, dtype, s);
     }
     WsLayout L = carve(part, arch, f_in, f_out, dtype, ws);
-    if (arch == GRAPPA_GCN && dz_in && flags == 0 && !part->halo && spmm_mm_supported(part, f_out, f_in, dtype)) {
-        // dT = Ahat dz_out and dz_in = (dT W^T) * relu'(h_in) in one fused kernel, then
-        // dW = h_in^T dT
-        AggMMArgs m;
-        m.X = dz_out; m.K = f_out; m.row_scale = I.norm_gcn; m.col_scale = I.norm_gcn; m.self = 1;
-        m.W = w; m.N = f_in; m.b_trans = 1; m.mask = relu_in ? h_in : nullptr; m.out = dz_in;
-        m.agg_out = L.node; m.hagg = L.hagg; m.partial = L.partial;
-        GRAPPA_TRY(spmm_mm(ctx, part, m, s));
-        GemmTNArgs t;
-        t.M = I.n_core; t.K1 = f_in; t.N = f_out; t.A1 = h_in; t.B = L.node; t.C = dw; t.ws = L.splitk;
-        return gemm_tn(ctx, t, dtype, s);
-    }
     if (arch == GRAPPA_GCN) {
         // dT = Ahat dz_out = N (A + I) (N dz_out): with a pre-normalised dz_out the SpMM
         // gathers unweighted rows.  Node-level (R30): Ahat_w^T dz = N (A diag(w) + I) (N dz) --
@@ -403,7 +428,7 @@ extern "C" grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part*
         }
         a.self = 1; a.out = L.node; a.partial = L.partial;
         GRAPPA_TRY(spmm_t(ctx, part, a, dtype, s));          // transpose operator (halo-1, R33)
-        if (dz_in && dtype == GRAPPA_BF16 && !g_pair_off && gemm_tc_pair_supported(I.n_core, f_in, f_out)) {
+        if (dz_in && dtype == GRAPPA_BF16 && !ctx->var_pair && gemm_tc_pair_supported(I.n_core, f_in, f_out)) {
             // both backward GEMMs from one read of dT and h_in (dz_in with the relu' gate, dW)
             const double M = (double)I.n_core;
             ProfScope ps(ctx, s, GRAPPA_K_GEMM, M * (f_out + 2.0 * f_in) * 2.0 + 4.0 * f_in * f_out * 2.0 +
@@ -444,83 +469,132 @@ extern "C" grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part*
 // ------------------------------------------------------------------------------ aggregate
 namespace grappa {
 
-// grad *= scale; flag non-finite; if fuse_sgd: theta -= lr * grad (single-rank fast path)
-__global__ void k_scale_grad(int64_t n, float* __restrict__ grad, float scale, int* flag,
-                             int fuse_sgd, float lr, float* __restrict__ theta) {
+// one fused pass before the all-reduce: comm = scale * grad (fp32 in place, or bf16 into
+// the comm buffer); flags a non-finite scaled value
+template <typename C>
+__global__ void k_scale_grad(int64_t n, float* __restrict__ grad, float scale, C* __restrict__ comm, int* flag) {
     int bad = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        float g = grad[i] * scale;
+        const float g = grad[i] * scale;
         bad |= !isfinite(g);
-        grad[i] = g;
-        if (fuse_sgd) theta[i] = theta[i] - lr * g;
+        if constexpr (sizeof(C) == 4) grad[i] = g;
+        else comm[i] = __float2bfloat16_rn(g);
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
-__global__ void k_sgd(int64_t n, const float* __restrict__ grad, float lr, float* __restrict__ theta,
-                      int* flag) {
+// after the all-reduce: non-finite values that arrived from other ranks (or overflowed in the sum)
+template <typename C>
+__global__ void k_flag_nonfinite(int64_t n, const C* __restrict__ v, int* flag) {
     int bad = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        float g = grad[i];
+        float g;
+        if constexpr (sizeof(C) == 4) g = v[i];
+        else g = __bfloat162float(v[i]);
         bad |= !isfinite(g);
-        theta[i] = theta[i] - lr * g;
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// grad <- the aggregated value (bf16 comm buffer upcast; nothing for fp32) and, unless the flag is
+// set (a non-finite aggregate in this or an earlier unchecked step), theta -= lr * grad
+template <typename C>
+__global__ void k_finish_sgd(int64_t n, const C* __restrict__ comm, float* __restrict__ grad, float lr,
+                             float* __restrict__ theta, const int* __restrict__ flag) {
+    const bool skip = *(volatile const int*)flag != 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float g;
+        if constexpr (sizeof(C) == 4) {
+            g = grad[i];
+        } else {
+            g = __bfloat162float(comm[i]);
+            grad[i] = g;
+        }
+        if (theta && !skip) theta[i] = theta[i] - lr * g;
+    }
+}
+
+static double factor_of(const grappa_part_info& I, grappa_corr corr, double eps, double c_max, bool* ok) {
+    *ok = true;
+    switch (corr) {
+        case GRAPPA_CORR_NONE: return 1.0;
+        case GRAPPA_CORR_NODE: return 1.0;          // correction inside the gradient (R30)
+        case GRAPPA_CORR_UNIFORM: return I.c_uniform;
+        case GRAPPA_CORR_RESAMPLING: {
+            // full-graph: D = sum_{seeds, d_l>0} (d_g - d_l) exactly (s_v = d_l); R12 guards
+            const double D = (double)I.D;
+            return D < eps ? 1.0 : std::min(1.0 / D, c_max);
+        }
+        case GRAPPA_CORR_RESAMPLING_HM: return I.c_resampling_hm;
+        default: *ok = false; return 0.0;
+    }
 }
 
 }  // namespace grappa
 
-extern "C" grappa_status grappa_aggregate_grads(grappa_ctx* ctx, const grappa_part* part,
-                                                grappa_corr corr, float* grad, int64_t n_params,
-                                                int32_t m_active, float lr, float* theta,
+extern "C" grappa_status grappa_aggregate_grads(grappa_ctx* ctx, const grappa_part* part, grappa_corr corr,
+                                                double eps, double c_max, float* grad, int64_t n_params,
+                                                int32_t m_active, grappa_dtype comm_dtype, float lr, float* theta,
                                                 void* stream) {
+    CallScope call_scope(ctx, stream);
     GRAPPA_ARG(ctx && grad && n_params > 0, GRAPPA_E_ARG, "grappa_aggregate_grads: null argument");
-    GRAPPA_ARG(m_active >= 1, GRAPPA_E_ARG, "grappa_aggregate_grads: m_active must be >= 1");
-    GRAPPA_ARG(lr == 0.f || theta, GRAPPA_E_ARG, "grappa_aggregate_grads: lr != 0 needs theta");
+    GRAPPA_ARG(eps > 0.0 && c_max >= 1.0, GRAPPA_E_ARG,
+               "grappa_aggregate_grads: need eps > 0 and c_max >= 1 (S:311-314), got %g / %g", eps, c_max);
     double c = 0.0;   // inactive rank: contributes zeros
     if (part) {
-        const grappa_part_info& I = part->info;
-        switch (corr) {
-            case GRAPPA_CORR_NONE: c = 1.0; break;
-            case GRAPPA_CORR_NODE: c = 1.0; break;      // correction inside the gradient (R30)
-            case GRAPPA_CORR_UNIFORM: c = I.c_uniform; break;
-            case GRAPPA_CORR_RESAMPLING: c = I.c_resampling; break;
-            case GRAPPA_CORR_RESAMPLING_HM: c = I.c_resampling_hm; break;
-            default: set_error("grappa_aggregate_grads: bad corr %d", (int)corr); return GRAPPA_E_ARG;
-        }
+        bool ok;
+        c = factor_of(part->info, corr, eps, c_max, &ok);
+        GRAPPA_ARG(ok, GRAPPA_E_ARG, "grappa_aggregate_grads: bad corr %d", (int)corr);
         GRAPPA_ARG(std::isfinite(c), GRAPPA_E_NONFINITE, "grappa_aggregate_grads: non-finite c (S:361)");
     }
-    return grappa_aggregate_grads_c(ctx, c, grad, n_params, m_active, lr, theta, stream);
+    return grappa_aggregate_grads_c(ctx, c, grad, n_params, m_active, comm_dtype, lr, theta, stream);
 }
 
 extern "C" grappa_status grappa_aggregate_grads_c(grappa_ctx* ctx, double c, float* grad, int64_t n_params,
-                                                  int32_t m_active, float lr, float* theta, void* stream) {
+                                                  int32_t m_active, grappa_dtype comm_dtype, float lr, float* theta,
+                                                  void* stream) {
+    CallScope scope(ctx, stream);
     GRAPPA_ARG(ctx && grad && n_params > 0, GRAPPA_E_ARG, "grappa_aggregate_grads_c: null argument");
     GRAPPA_ARG(m_active >= 1, GRAPPA_E_ARG, "grappa_aggregate_grads_c: m_active must be >= 1");
     GRAPPA_ARG(lr == 0.f || theta, GRAPPA_E_ARG, "grappa_aggregate_grads_c: lr != 0 needs theta");
+    GRAPPA_ARG(comm_dtype == GRAPPA_F32 || comm_dtype == GRAPPA_BF16, GRAPPA_E_ARG,
+               "grappa_aggregate_grads_c: bad comm_dtype %d", (int)comm_dtype);
     GRAPPA_ARG(std::isfinite(c), GRAPPA_E_NONFINITE, "grappa_aggregate_grads_c: non-finite c (S:361)");
     cudaStream_t s = (cudaStream_t)stream;
     const float scale = (float)(c / (double)m_active);
     const bool multi = ctx->comm && ctx->nranks > 1;
-    ProfScope ps(ctx, s, GRAPPA_K_AGG, (double)n_params * 4.0 * (lr != 0.f ? 4 : 2), 3.0 * n_params);
-    unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n_params, 256), (int64_t)ctx->sm_count * 4);
-    k_scale_grad<<<grid, 256, 0, s>>>(n_params, grad, scale, ctx->d_flag, (!multi && lr != 0.f) ? 1 : 0,
-                                      lr, theta);
+    const bool bf = comm_dtype == GRAPPA_BF16;
+    const size_t cbytes = (size_t)n_params * (bf ? 2 : 4);
+    if (bf) GRAPPA_TRY(ctx->comm_buf.grow(cbytes));
+    __nv_bfloat16* cb = bf ? (__nv_bfloat16*)ctx->comm_buf.p : nullptr;
+    ProfScope ps(ctx, s, GRAPPA_K_AGG, (double)n_params * (4.0 + (bf ? 2.0 : 4.0) + (lr != 0.f ? 12.0 : 0.0)),
+                 3.0 * n_params);
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n_params, 256), (int64_t)ctx->sm_count * 4);
+    if (bf) k_scale_grad<__nv_bfloat16><<<grid, 256, 0, s>>>(n_params, grad, scale, cb, ctx->d_flag);
+    else k_scale_grad<float><<<grid, 256, 0, s>>>(n_params, grad, scale, nullptr, ctx->d_flag);
     GRAPPA_LAUNCHED(ctx);
     if (multi) {
-        NCCL_OK(ncclAllReduce(grad, grad, (size_t)n_params, ncclFloat32, ncclSum,
-                              (ncclComm_t)ctx->comm, s));
-        if (lr != 0.f) {
-            k_sgd<<<grid, 256, 0, s>>>(n_params, grad, lr, theta, ctx->d_flag);
-            GRAPPA_LAUNCHED(ctx);
-        }
+        NCCL_OK(ncclAllReduce(bf ? (void*)cb : (void*)grad, bf ? (void*)cb : (void*)grad, (size_t)n_params,
+                              bf ? ncclBfloat16 : ncclFloat32, ncclSum, (ncclComm_t)ctx->comm, s));
+        ctx->comm_grad_bytes += (int64_t)cbytes;
+        if (bf) k_flag_nonfinite<__nv_bfloat16><<<grid, 256, 0, s>>>(n_params, cb, ctx->d_flag);
+        else k_flag_nonfinite<float><<<grid, 256, 0, s>>>(n_params, grad, ctx->d_flag);
+        GRAPPA_LAUNCHED(ctx);
+    }
+    if (bf || lr != 0.f) {
+        if (bf) k_finish_sgd<__nv_bfloat16><<<grid, 256, 0, s>>>(n_params, cb, grad, lr, lr != 0.f ? theta : nullptr,
+                                                                 ctx->d_flag);
+        else k_finish_sgd<float><<<grid, 256, 0, s>>>(n_params, nullptr, grad, lr, theta, ctx->d_flag);
+        GRAPPA_LAUNCHED(ctx);
     }
     return GRAPPA_OK;
 }
 
 extern "C" grappa_status grappa_check(grappa_ctx* ctx, void* stream) {
+    CallScope call_scope(ctx, stream);
     GRAPPA_ARG(ctx, GRAPPA_E_ARG, "grappa_check: null ctx");
     cudaStream_t s = (cudaStream_t)stream;
     int flag = 0;

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <memory>
 #include <string>
 #include "../../include/grappa.h"
 
@@ -47,13 +48,36 @@ void set_error(const char* fmt, ...);
         if (ctx) (ctx)->launches++;                                                      \
     } while (0)
 
-// Growable device scratch buffer owned by the ctx (never used inside graph capture unless
-// already large enough: grow() only allocates when the request exceeds capacity).
+// Caller allocator (grappa_ctx_create_ex): device memory of library-owned objects comes from
+// the caller's allocator (the PyTorch caching allocator in the binding), so a regrow does not
+// cudaFree (which synchronises the device).  Shared by the ctx and every buffer it allocated,
+// so buffers of objects that outlive the ctx are still freed through the allocator that made them.
+struct Allocator {
+    grappa_alloc_fn alloc = nullptr;
+    grappa_free_fn free = nullptr;
+    void* user = nullptr;
+};
+
+// Growable device buffer of a library-owned object.  grow() allocates through the allocator of
+// the API call in progress (CallScope) on that call's stream -- or cudaMalloc when the ctx has
+// none or the stream is being captured into a CUDA graph -- and release() frees through the
+// allocator that made the block.  grow() only allocates when the request exceeds capacity.
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
+    std::shared_ptr<const Allocator> al;   // null: cudaMalloc'd
+    void* al_stream = nullptr;
     grappa_status grow(size_t bytes);
     void release();
+};
+
+// Per API call: the ctx's allocator and the call's stream, seen by DevBuf::grow (thread-local;
+// nested calls restore the outer scope).
+struct CallScope {
+    std::shared_ptr<const Allocator> prev_al;
+    void* prev_stream;
+    CallScope(const grappa_ctx* ctx, void* stream);
+    ~CallScope();
 };
 
 // Optional per-kernel-class timing (grappa_profile_*): CUDA events recorded on the launch
@@ -86,6 +110,14 @@ struct grappa_ctx {
     grappa::DevBuf sh_ws;        // sharded repartition: merged two-shard CSR
     grappa::DevBuf xf_hdr;       // shard exchange headers
     void* h_pinned = nullptr;    // pinned host staging (64 KB)
+    std::shared_ptr<const grappa::Allocator> alloc;   // caller allocator (null: cudaMalloc)
+    grappa::DevBuf comm_buf;     // bf16 communication buffer of grappa_aggregate_grads
+    // test / A-B kernel selection (grappa_set_kernel_variant): gemm 0 = tensor cores, 1/2 = CUDA
+    // cores; spmm 0 = row-group, 1 = warp per row, 2 = 8 loads in flight, 3 = natural row order;
+    // pair 1 = separate GCN backward GEMMs
+    int var_gemm = 0, var_spmm = 0, var_pair = 0;
+    int64_t comm_grad_bytes = 0;   // gradient all-reduce payload bytes (grappa_comm_bytes)
+    int64_t comm_other_bytes = 0;  // every other cross-GPU byte (shard / halo exchange)
 };
 
 namespace grappa {

@@ -65,11 +65,7 @@ grappa_status gemm_tc_pair(grappa_ctx* ctx, int64_t M, int f_in, int f_out, cons
 bool gemm_x3_nn_supported(const GemmArgs& g);
 grappa_status gemm_x3_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s);
 bool gemm_x3_tn_supported(const GemmTNArgs& g);
-void gemm_x3_set_dbg(int v);   // timing probes only (results invalid when != 0)
 grappa_status gemm_x3_tn(grappa_ctx* ctx, const GemmTNArgs& g, cudaStream_t s);
 // force the SIMT kernels even for bf16 (tests cross-check the two implementations)
-void gemm_force_simt(int on);
-void gemm_tn_set_stages(int v);
-void gemm_tn_set_red(int v);
 
 }  // namespace grappa

@@ -185,8 +185,8 @@ size_t gemm_tn_ws_bytes(int64_t M, int K1, int K2, int N) {
     return simt > tc ? simt : tc;
 }
 
-static int g_force_simt = 0;
-void gemm_force_simt(int on) { g_force_simt = on; }
+// ctx->var_gemm (grappa_set_kernel_variant "gemm"): 0 = tensor cores, 1 / 2 = CUDA-core kernels
+static inline int gemm_var(const grappa_ctx* c) { return c ? c->var_gemm : 0; }
 
 grappa_status gemm_nn(grappa_ctx* ctx, const GemmArgs& g, grappa_dtype dt, cudaStream_t s) {
     if (g.M == 0) return GRAPPA_OK;
@@ -195,9 +195,9 @@ grappa_status gemm_nn(grappa_ctx* ctx, const GemmArgs& g, grappa_dtype dt, cudaS
                  (double)g.M * K * es + K * g.N * 4.0 + (double)g.M * g.N * es * (g.mask ? 2 : 1) +
                      (g.row_scale ? 4.0 * g.M : 0.0),
                  2.0 * g.M * g.N * K);
-    if (dt == GRAPPA_BF16 && !g_force_simt && gemm_tc_nn_supported(g)) return gemm_tc_nn(ctx, g, s);
-    if (dt == GRAPPA_F32 && !g_force_simt && gemm_x3_nn_supported(g)) return gemm_x3_nn(ctx, g, s);
-    if (dt == GRAPPA_F32 && g_force_simt != 2 && sgemm_supported(g.K1, g.K2, g.N)) return sgemm_nn(ctx, g, s);
+    if (dt == GRAPPA_BF16 && !gemm_var(ctx) && gemm_tc_nn_supported(g)) return gemm_tc_nn(ctx, g, s);
+    if (dt == GRAPPA_F32 && !gemm_var(ctx) && gemm_x3_nn_supported(g)) return gemm_x3_nn(ctx, g, s);
+    if (dt == GRAPPA_F32 && gemm_var(ctx) != 2 && sgemm_supported(g.K1, g.K2, g.N)) return sgemm_nn(ctx, g, s);
     dim3 grid((unsigned)ceil_div(g.M, BM), (unsigned)ceil_div(g.N, BN));
     if (dt == GRAPPA_BF16) k_gemm_nn<__nv_bfloat16><<<grid, 256, 0, s>>>(g);
     else k_gemm_nn<float><<<grid, 256, 0, s>>>(g);
@@ -211,13 +211,13 @@ grappa_status gemm_tn(grappa_ctx* ctx, const GemmTNArgs& g, grappa_dtype dt, cud
     ProfScope ps(ctx, s, GRAPPA_K_GEMM_TN,
                  (double)g.M * K * es + (double)g.M * g.N * es + (double)K * g.N * 4.0,
                  2.0 * g.M * g.N * K);
-    if (dt == GRAPPA_BF16 && !g_force_simt && g.M > 0 && gemm_tc_tn_supported(g)) return gemm_tc_tn(ctx, g, s);
-    if (dt == GRAPPA_F32 && !g_force_simt && g.M > 0 && gemm_x3_tn_supported(g)) return gemm_x3_tn(ctx, g, s);
+    if (dt == GRAPPA_BF16 && !gemm_var(ctx) && g.M > 0 && gemm_tc_tn_supported(g)) return gemm_tc_tn(ctx, g, s);
+    if (dt == GRAPPA_F32 && !gemm_var(ctx) && g.M > 0 && gemm_x3_tn_supported(g)) return gemm_x3_tn(ctx, g, s);
     const int slabs = g.M > 0 ? slabs_for(g.M) : 1;
     const int64_t rps = g.M > 0 ? ceil_div(g.M, slabs) : 0;
     dim3 grid((unsigned)ceil_div(K, 64), (unsigned)ceil_div(g.N, 64), (unsigned)slabs);
     if (g.M > 0) {
-        if (dt == GRAPPA_F32 && g_force_simt != 2 && sgemm_supported(g.K1, g.K2, g.N)) {
+        if (dt == GRAPPA_F32 && gemm_var(ctx) != 2 && sgemm_supported(g.K1, g.K2, g.N)) {
             GRAPPA_TRY(sgemm_tn_partials(ctx, g, slabs, rps, s));
         } else {
             if (dt == GRAPPA_BF16) k_gemm_tn<__nv_bfloat16><<<grid, 256, 0, s>>>(g, rps, g.ws);

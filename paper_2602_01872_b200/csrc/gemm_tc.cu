@@ -521,7 +521,6 @@ constexpr int kX3MaxStages = 4;
 struct TcX3 {
     int64_t M;
     int K1, K2, N, kb1, kb2, n_split, stages, num_tiles, relu, b_trans;
-    int dbg;               // diagnostic knob (timing probes only): 1 no A loads, 2 no stores, 4 no weights
     const float* A1;
     const float* A2;
     const float* B;
@@ -566,7 +565,7 @@ __global__ void __launch_bounds__(kX3Threads, 1)
     uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    if (!(p.dbg & 4)) {
+    {
         stage_weights(sBh, sBl, p.B, p.K1, p.K2, p.N, p.kb1, kbt, p.b_trans);
     }
     if (threadIdx.x == 0) {
@@ -594,7 +593,7 @@ __global__ void __launch_bounds__(kX3Threads, 1)
 #pragma unroll
             for (int i = 0; i < 8; i++) {
                 const int64_t row = (int64_t)tile * 128 + rsub + 16 * i;
-                v[i] = (row < p.M && k < Ks && !(p.dbg & 1)) ? __ldg(reinterpret_cast<const float4*>(A + row * Ks + k))
+                v[i] = (row < p.M && k < Ks) ? __ldg(reinterpret_cast<const float4*>(A + row * Ks + k))
                                                              : make_float4(0.f, 0.f, 0.f, 0.f);
             }
         };
@@ -647,7 +646,7 @@ __global__ void __launch_bounds__(kX3Threads, 1)
                     const uint32_t bl = tc::smem_u32(sBl + (size_t)kb * p.N * 128);
 #pragma unroll
                     for (int k = 0; k < 4; k++) {
-                        if (!(p.dbg & 8)) {
+                        {
                         tc::mma_f16(d, tc::smem_desc_sw128(al + k * 32, 0, 1024),
                                     tc::smem_desc_sw128(bh + k * 32, 0, 1024), idesc, (kb | k) != 0);
                         tc::mma_f16(d, tc::smem_desc_sw128(ah + k * 32, 0, 1024),
@@ -684,7 +683,7 @@ __global__ void __launch_bounds__(kX3Threads, 1)
             tc::mbar_wait(&tfull[acc], aphase);
             tc::fence_after();
             const uint32_t tb = tmem + (uint32_t)(acc * p.N) + tq;
-            for (int bx = 0; bx < ((p.dbg & 16) ? 0 : nb1 + nb2); bx++) {
+            for (int bx = 0; bx < nb1 + nb2; bx++) {
                 const bool first = bx < nb1;
                 const int cbase = first ? bx * 32 : (bx - nb1) * 32;          // column in C1 / C2
                 const int cend = first ? min(cbase + 32, p.n_split) : min(cbase + 32, p.N - p.n_split);
@@ -725,7 +724,7 @@ __global__ void __launch_bounds__(kX3Threads, 1)
                 }
                 tc::fence_proxy_async();              // staged box -> visible to the TMA engine
                 epi_bar();
-                if (leader && !(p.dbg & 2)) {
+                if (leader) {
                     tma_store_2d(first ? &tmC1 : &tmC2, obox, cbase, tile * 128);
                     bulk_commit();
                 }
@@ -1010,9 +1009,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 // bitwise deterministic.
 // A/B knobs (grappa_set_kernel_variant "tnstages" / "tnred"): ring depth (0 = fill shared
 // memory) and slab groups of the reduction (8 or 32)
-static int g_tn_stages = 4, g_tn_red = 8;   // 4 stages measured best (6-7 slower)
-void gemm_tn_set_stages(int v) { g_tn_stages = v; }
-void gemm_tn_set_red(int v) { g_tn_red = v == 32 ? 32 : 8; }
+// ring depth of the weight-gradient GEMM: 4 stages measured best (6-7 and a full-smem ring were
+// slower), and an 8-group fixed-order split-K reduction (32 groups measured no faster)
+constexpr int kTnStages = 4;
 template <int kRedGroups>
 __global__ void __launch_bounds__(32 * kRedGroups) k_tn_reduce(int64_t count, int N, int K1, int K2, int ft1,
                                                                int ftiles, int slabs, const float* __restrict__ ws,
@@ -1157,11 +1156,8 @@ bool gemm_x3_nn_supported(const GemmArgs& g) {
     return g.N % 16 == 0 && g.N <= 256 && g.n_split % 16 == 0 && g.K1 % 4 == 0 && g.K2 % 4 == 0 &&
            x3_stages(kbt, g.N) >= 2 && g.M < (1ll << 31);
 }
-static int g_x3_dbg = 0;
-void gemm_x3_set_dbg(int v) { g_x3_dbg = v; }
 grappa_status gemm_x3_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s) {
     TcX3 p;
-    p.dbg = g_x3_dbg;
     p.M = g.M; p.K1 = g.K1; p.K2 = g.K2; p.N = g.N;
     p.kb1 = (int)ceil_div(g.K1, 64); p.kb2 = (int)ceil_div(g.K2, 64);
     p.n_split = g.n_split; p.relu = g.relu; p.b_trans = g.b_trans;
@@ -1273,7 +1269,7 @@ grappa_status gemm_tc_tn(grappa_ctx* ctx, const GemmTNArgs& g, cudaStream_t s) {
     p.tmem_cols = pow2_cols(p.Nmma);
     const size_t st_bytes = 16384 + (size_t)p.nbox_b * 8192;
     p.stages = (int)std::min<size_t>(kTNMaxStages, (kMaxSmem - 1024 - 512) / st_bytes);
-    if (g_tn_stages > 0) p.stages = std::min(p.stages, g_tn_stages);
+    p.stages = std::min(p.stages, kTnStages);
     const size_t smem = 1024 + (size_t)p.stages * st_bytes + 512;
     static bool attr = false;
     if (!attr) {
@@ -1284,12 +1280,8 @@ grappa_status gemm_tc_tn(grappa_ctx* ctx, const GemmTNArgs& g, cudaStream_t s) {
     k_gemm_tc_tn<<<grid, kTcThreads, smem, s>>>(m1, m2, mb, p);
     GRAPPA_LAUNCHED(ctx);
     const int64_t count = (int64_t)(g.K1 + g.K2) * g.N;
-    if (g_tn_red == 32)
-        k_tn_reduce<32><<<(unsigned)ceil_div(count, 32), 32 * 32, 0, s>>>(count, g.N, g.K1, g.K2, p.ft1, ftiles,
-                                                                         p.slabs, g.ws, g.C);
-    else
-        k_tn_reduce<8><<<(unsigned)ceil_div(count, 32), 32 * 8, 0, s>>>(count, g.N, g.K1, g.K2, p.ft1, ftiles,
-                                                                       p.slabs, g.ws, g.C);
+    k_tn_reduce<8><<<(unsigned)ceil_div(count, 32), 32 * 8, 0, s>>>(count, g.N, g.K1, g.K2, p.ft1, ftiles,
+                                                                   p.slabs, g.ws, g.C);
     GRAPPA_LAUNCHED(ctx);
     return GRAPPA_OK;
 }

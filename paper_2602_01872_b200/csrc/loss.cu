@@ -109,12 +109,14 @@ using namespace grappa;
 extern "C" grappa_status grappa_loss(grappa_ctx* ctx, const grappa_part* part, const void* logits,
                                      int32_t num_classes, int32_t k_pad, void* dlogits,
                                      double* loss_dev, grappa_dtype dtype, void* stream) {
+    CallScope call_scope(ctx, stream);
     return grappa_loss_ex(ctx, part, logits, num_classes, k_pad, dlogits, loss_dev, dtype, 0u, stream);
 }
 
 extern "C" grappa_status grappa_loss_ex(grappa_ctx* ctx, const grappa_part* part, const void* logits,
                                         int32_t num_classes, int32_t k_pad, void* dlogits,
                                         double* loss_dev, grappa_dtype dtype, unsigned flags, void* stream) {
+    CallScope call_scope(ctx, stream);
     GRAPPA_ARG((flags & ~GRAPPA_LOSS_DZ_NORMED) == 0, GRAPPA_E_ARG, "grappa_loss_ex: flags 0x%x invalid", flags);
     GRAPPA_ARG(ctx && part && logits && dlogits && loss_dev, GRAPPA_E_ARG, "grappa_loss: null argument");
     GRAPPA_ARG(num_classes >= 1 && num_classes <= k_pad && k_pad <= kMaxKPad, GRAPPA_E_ARG,

@@ -51,6 +51,7 @@ using namespace grappa;
 extern "C" grappa_status grappa_partition(grappa_ctx* ctx, int64_t num_nodes, int32_t num_chunks,
                                           uint64_t seed, int32_t* chunk_of,
                                           int64_t* chunk_sizes, void* stream) {
+    CallScope call_scope(ctx, stream);
     GRAPPA_ARG(ctx && chunk_of && chunk_sizes, GRAPPA_E_ARG, "grappa_partition: null argument");
     GRAPPA_ARG(num_chunks >= 2 && (int64_t)num_chunks <= num_nodes, GRAPPA_E_ARG,
                "grappa_partition: need 2 <= C <= N (S:128-130), got C=%d N=%lld", num_chunks,

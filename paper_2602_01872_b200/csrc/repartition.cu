@@ -492,6 +492,7 @@ extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g
                                             int32_t base, int32_t swept, const uint8_t* train_mask,
                                             const int32_t* labels, grappa_part** inout,
                                             void* stream) {
+    CallScope call_scope(ctx, stream);
     return grappa_repartition_ex(ctx, g, feats, feat_dim, dtype, chunk_of, num_chunks, base, swept,
                                  train_mask, labels, 0u, inout, stream);
 }
@@ -678,6 +679,12 @@ static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const voi
     p->t_n_heavy = p->t_n_slots = 0;
     p->t_eid_ready = halo;            // induced-core: built lazily by the first GAT backward
     if (halo) {
+        // cub's radix sort takes an int item count
+        if (nnz >= ((int64_t)1 << 31)) {
+            set_error("grappa_repartition_ex: halo-1 transpose of %lld local edges exceeds the 2^31 sort limit",
+                      (long long)nnz);
+            return fail(GRAPPA_E_SUPPORT);
+        }
         RP_TRY(p->t_rowptr.grow((size_t)(n_local + 1) * 8));
         RP_TRY(p->t_col.grow((size_t)(nnz > 0 ? nnz : 1) * 4));
         RP_TRY(p->t_deg.grow((size_t)n_local * 4));
@@ -747,6 +754,7 @@ extern "C" grappa_status grappa_repartition_ex(grappa_ctx* ctx, const grappa_csr
                                                int32_t base, int32_t swept, const uint8_t* train_mask,
                                                const int32_t* labels, unsigned flags,
                                                grappa_part** inout, void* stream) {
+    CallScope call_scope(ctx, stream);
     GRAPPA_ARG(ctx && g && chunk_of && train_mask && inout, GRAPPA_E_ARG,
                "grappa_repartition: null argument");
     return repart_impl(ctx, g, feats, feat_dim, dtype, chunk_of, num_chunks, base, swept, train_mask, labels,
@@ -757,6 +765,7 @@ extern "C" grappa_status grappa_repartition_shards(grappa_ctx* ctx, const grappa
                                                    const grappa_shard* swept, const int32_t* chunk_of,
                                                    int64_t num_nodes, int32_t num_chunks, grappa_part** inout,
                                                    void* stream) {
+    CallScope call_scope(ctx, stream);
     GRAPPA_ARG(ctx && base && swept && chunk_of && inout, GRAPPA_E_ARG,
                "grappa_repartition_shards: null argument");
     const grappa_shard_info &A = base->info, &B = swept->info;

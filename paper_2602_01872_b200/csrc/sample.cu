@@ -242,6 +242,8 @@ struct grappa_batch {
 
 static grappa_status sort_pairs(DevBuf& tmp, const int32_t* kin, int32_t* kout, const int32_t* vin,
                                 int32_t* vout, int64_t n, int end_bit, cudaStream_t s) {
+    GRAPPA_ARG(n < ((int64_t)1 << 31), GRAPPA_E_SUPPORT, "sampler: %lld items exceed cub's int sort limit",
+               (long long)n);
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, (int)n, 0, end_bit, s);
     GRAPPA_TRY(tmp.grow(bytes));
@@ -251,6 +253,7 @@ static grappa_status sort_pairs(DevBuf& tmp, const int32_t* kin, int32_t* kout, 
 
 extern "C" grappa_status grappa_epoch_seeds(grappa_ctx* ctx, const grappa_part* part, uint64_t seed,
                                             int64_t epoch, int32_t* order, void* stream) {
+    CallScope call_scope(ctx, stream);
     GRAPPA_ARG(ctx && part && order, GRAPPA_E_ARG, "grappa_epoch_seeds: null argument");
     const grappa_part_info& I = part->info;
     cudaStream_t s = (cudaStream_t)stream;
@@ -263,6 +266,8 @@ extern "C" grappa_status grappa_epoch_seeds(grappa_ctx* ctx, const grappa_part* 
     k_seed_keys<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 4096), 256, 0, s>>>(n, I.seeds, I.core_global, seed,
                                                                                       (uint64_t)epoch, keys);
     GRAPPA_LAUNCHED(ctx);
+    GRAPPA_ARG(n < ((int64_t)1 << 31), GRAPPA_E_SUPPORT, "grappa_epoch_seeds: %lld seeds exceed the int sort limit",
+               (long long)n);
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, skeys, I.seeds, order, (int)n, 0, 64, s);
     GRAPPA_TRY(ctx->scan_ws.grow(bytes));
@@ -275,6 +280,7 @@ extern "C" grappa_status grappa_sample(grappa_ctx* ctx, const grappa_part* part,
                                        int32_t n_batch, const int32_t* fanouts, int32_t n_layers,
                                        uint64_t seed, int64_t epoch, int64_t batch_index,
                                        grappa_batch** inout, void* stream) {
+    CallScope call_scope(ctx, stream);
     GRAPPA_TRY(grappa_sample_async(ctx, part, batch, n_batch, fanouts, n_layers, seed, epoch, batch_index,
                                    inout, stream));
     return grappa_sample_wait(*inout);
@@ -284,6 +290,7 @@ extern "C" grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part*
                                              int32_t n_batch, const int32_t* fanouts, int32_t n_layers,
                                              uint64_t seed, int64_t epoch, int64_t batch_index,
                                              grappa_batch** inout, void* stream) {
+    CallScope call_scope(ctx, stream);
     GRAPPA_ARG(ctx && part && batch && fanouts && inout, GRAPPA_E_ARG, "grappa_sample: null argument");
     GRAPPA_ARG(n_layers >= 1 && n_layers <= kMaxLayers, GRAPPA_E_ARG, "grappa_sample: 1 <= n_layers <= %d", kMaxLayers);
     GRAPPA_ARG(n_batch >= 1, GRAPPA_E_ARG, "grappa_sample: empty batch (S:213)");
@@ -480,6 +487,7 @@ extern "C" grappa_status grappa_minibatch_step(grappa_ctx* ctx, const grappa_par
                                                const float* theta, float* grad, void* ws, size_t ws_bytes,
                                                double* loss_dev, void* const* hidden_out, grappa_dtype dt,
                                                void* stream) {
+    CallScope call_scope(ctx, stream);
     return grappa_minibatch_step_ex(ctx, part, b, L, dp, num_classes, theta, grad, ws, ws_bytes, loss_dev,
                                     hidden_out, dt, 0u, stream);
 }
@@ -489,6 +497,7 @@ extern "C" grappa_status grappa_minibatch_step_ex(grappa_ctx* ctx, const grappa_
                                                   const float* theta, float* grad, void* ws, size_t ws_bytes,
                                                   double* loss_dev, void* const* hidden_out, grappa_dtype dt,
                                                   unsigned flags, void* stream) {
+    CallScope call_scope(ctx, stream);
     GRAPPA_ARG((flags & ~GRAPPA_LAYER_NODE_LEVEL) == 0, GRAPPA_E_ARG,
                "grappa_minibatch_step_ex: flags 0x%x invalid", flags);
     const bool node = flags & GRAPPA_LAYER_NODE_LEVEL;

@@ -13,6 +13,7 @@
 // replicated path builds (tests/test_gpu_shard.py).
 #include <nccl.h>
 
+#include <string>
 #include "part.cuh"
 #include "scan.cuh"
 
@@ -159,6 +160,7 @@ extern "C" grappa_status grappa_shard_extract(grappa_ctx* ctx, const grappa_csr*
                                               int32_t feat_dim, grappa_dtype dtype, const int32_t* chunk_of,
                                               int32_t num_chunks, int32_t chunk, const uint8_t* train_mask,
                                               const int32_t* labels, grappa_shard** inout, void* stream) {
+    CallScope call_scope(ctx, stream);
     GRAPPA_ARG(ctx && g && chunk_of && train_mask && inout, GRAPPA_E_ARG, "grappa_shard_extract: null argument");
     GRAPPA_ARG(chunk >= 0 && chunk < num_chunks, GRAPPA_E_ARG, "grappa_shard_extract: chunk %d out of range", chunk);
     GRAPPA_ARG(feats == nullptr || (feat_dim > 0 && feat_dim % 16 == 0), GRAPPA_E_SHAPE,
@@ -250,6 +252,7 @@ extern "C" void grappa_shard_destroy(grappa_shard* sh) {
 
 extern "C" grappa_status grappa_shard_exchange(grappa_ctx* ctx, int32_t n_xfers, const grappa_shard_xfer* xfers,
                                                void* stream) {
+    CallScope call_scope(ctx, stream);
     GRAPPA_ARG(ctx && (n_xfers == 0 || xfers) && n_xfers >= 0, GRAPPA_E_ARG, "grappa_shard_exchange: null argument");
     GRAPPA_ARG(ctx->comm, GRAPPA_E_ARG, "grappa_shard_exchange: the ctx has no NCCL communicator");
     for (int32_t k = 0; k < n_xfers; k++) {
@@ -271,7 +274,7 @@ extern "C" grappa_status grappa_shard_exchange(grappa_ctx* ctx, int32_t n_xfers,
             hdr[k * 4 + 2] = I.nnz;
             hdr[k * 4 + 3] = (int64_t)I.feat_dim | ((int64_t)I.dtype << 32);
         }
-    GRAPPA_TRY(ctx->xf_hdr.grow((size_t)n_xfers * 32));
+    GRAPPA_TRY(ctx->xf_hdr.grow((size_t)n_xfers * 40));
     int64_t* d_hdr = (int64_t*)ctx->xf_hdr.p;
     GRAPPA_CUDA(cudaMemcpyAsync(d_hdr, hdr.data(), (size_t)n_xfers * 32, cudaMemcpyHostToDevice, s));
     SH_NCCL(ncclGroupStart());
@@ -282,25 +285,60 @@ extern "C" grappa_status grappa_shard_exchange(grappa_ctx* ctx, int32_t n_xfers,
     SH_NCCL(ncclGroupEnd());
     GRAPPA_CUDA(cudaMemcpyAsync(hdr.data(), d_hdr, (size_t)n_xfers * 32, cudaMemcpyDeviceToHost, s));
     GRAPPA_CUDA(cudaStreamSynchronize(s));
-    // size the receive shards
+    // size the receive shards; a receiver that cannot take a shard does not return yet: both sides
+    // of every transfer first agree on success (round 1b), so no sender is left in round 2 with a
+    // ncclSend nobody matches
     std::vector<grappa_shard*> rs((size_t)n_xfers, nullptr);
+    std::vector<int64_t> ok((size_t)n_xfers, 0);
+    grappa_status local = GRAPPA_OK;
+    std::string local_msg;
     for (int32_t k = 0; k < n_xfers; k++) {
         if (!xfers[k].recv) continue;
         const int64_t n_rows = hdr[k * 4 + 1], nnz = hdr[k * 4 + 2];
         const int32_t fd = (int32_t)(hdr[k * 4 + 3] & 0xffffffffll);
         const grappa_dtype dt = (grappa_dtype)(hdr[k * 4 + 3] >> 32);
-        GRAPPA_ARG(n_rows > 0 && nnz >= 0 && fd >= 0 && (dt == GRAPPA_F32 || dt == GRAPPA_BF16), GRAPPA_E_ARG,
-                   "grappa_shard_exchange: malformed header from rank %d", xfers[k].peer);
-        grappa_shard* sh = *xfers[k].recv ? *xfers[k].recv : new grappa_shard();
-        grappa_status st = shard_alloc(sh, n_rows, nnz, fd, dt);
-        if (st != GRAPPA_OK) {
-            if (!*xfers[k].recv) grappa_shard_destroy(sh);
-            return st;
+        grappa_status st = GRAPPA_OK;
+        if (local != GRAPPA_OK) {
+            st = local;
+        } else if (!(n_rows > 0 && nnz >= 0 && fd >= 0 && (dt == GRAPPA_F32 || dt == GRAPPA_BF16))) {
+            set_error("grappa_shard_exchange: malformed header from rank %d", xfers[k].peer);
+            st = GRAPPA_E_ARG;
+        } else {
+            grappa_shard* sh = *xfers[k].recv ? *xfers[k].recv : new grappa_shard();
+            st = shard_alloc(sh, n_rows, nnz, fd, dt);
+            if (st != GRAPPA_OK) {
+                if (!*xfers[k].recv) grappa_shard_destroy(sh);
+            } else {
+                shard_publish(sh, (int32_t)hdr[k * 4 + 0], n_rows, nnz, fd, dt);
+                *xfers[k].recv = sh;
+                rs[k] = sh;
+            }
         }
-        shard_publish(sh, (int32_t)hdr[k * 4 + 0], n_rows, nnz, fd, dt);
-        *xfers[k].recv = sh;
-        rs[k] = sh;
+        if (st != GRAPPA_OK && local == GRAPPA_OK) {
+            local = st;
+            local_msg = grappa_last_error();
+        }
+        ok[k] = st == GRAPPA_OK ? 1 : 0;
     }
+    // round 1b: every receiver tells its sender whether it can take the arrays
+    int64_t* d_ok = d_hdr + (size_t)n_xfers * 4;
+    GRAPPA_CUDA(cudaMemcpyAsync(d_ok, ok.data(), (size_t)n_xfers * 8, cudaMemcpyHostToDevice, s));
+    SH_NCCL(ncclGroupStart());
+    for (int32_t k = 0; k < n_xfers; k++) {
+        if (xfers[k].recv) SH_NCCL(ncclSend(d_ok + k, 1, ncclInt64, xfers[k].peer, comm, s));
+        else SH_NCCL(ncclRecv(d_ok + k, 1, ncclInt64, xfers[k].peer, comm, s));
+    }
+    SH_NCCL(ncclGroupEnd());
+    GRAPPA_CUDA(cudaMemcpyAsync(ok.data(), d_ok, (size_t)n_xfers * 8, cudaMemcpyDeviceToHost, s));
+    GRAPPA_CUDA(cudaStreamSynchronize(s));
+    if (local != GRAPPA_OK) {
+        set_error("%s", local_msg.c_str());
+        return local;
+    }
+    for (int32_t k = 0; k < n_xfers; k++)
+        GRAPPA_ARG(ok[k] == 1, GRAPPA_E_NCCL,
+                   "grappa_shard_exchange: rank %d could not receive transfer %d (its own error says why)",
+                   xfers[k].peer, k);
     // round 2: the arrays (sizes known on both sides from the header)
     SH_NCCL(ncclGroupStart());
     for (int32_t k = 0; k < n_xfers; k++) {
@@ -311,8 +349,13 @@ extern "C" grappa_status grappa_shard_exchange(grappa_ctx* ctx, int32_t n_xfers,
             {I.x, (size_t)I.n_rows * I.feat_dim * esz}, {I.labels, (size_t)I.n_rows * 4}, {I.train, (size_t)I.n_rows}};
         for (auto& a : arr) {
             if (a.bytes == 0) continue;
-            if (xfers[k].send) SH_NCCL(ncclSend(a.p, a.bytes, ncclUint8, xfers[k].peer, comm, s));
-            else SH_NCCL(ncclRecv(const_cast<void*>(a.p), a.bytes, ncclUint8, xfers[k].peer, comm, s));
+            if (xfers[k].send) {
+                SH_NCCL(ncclSend(a.p, a.bytes, ncclUint8, xfers[k].peer, comm, s));
+                if (xfers[k].peer != ctx->rank) ctx->comm_other_bytes += (int64_t)a.bytes;
+            }
+            else {
+                SH_NCCL(ncclRecv(const_cast<void*>(a.p), a.bytes, ncclUint8, xfers[k].peer, comm, s));
+            }
         }
     }
     SH_NCCL(ncclGroupEnd());

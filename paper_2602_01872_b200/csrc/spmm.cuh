@@ -36,32 +36,6 @@ struct SpmmArgs {
                                       // of the fused kernel; no mask / accumulate / relu)
 };
 
-// Fused aggregate -> transform (bf16, tcgen05):
-//   out[v] = epi( agg(X)[v] @ B ),  agg(X)[v] = rs[v] (self cs[v] X[v] + sum_u cs[u] X[u])
-//   B = W [K x N] (or W^T when b_trans, W stored [N x K]), epi = relu? / relu'(mask[v]) gate,
-//   agg_out (optional) receives agg(X) itself.  Same arithmetic as spmm() followed by
-//   gemm_nn() except that the aggregate is rounded to bf16 once, before the transform.
-struct AggMMArgs {
-    const void* X = nullptr;          // [n x K] bf16
-    int K = 0;
-    const float* row_scale = nullptr;
-    const float* col_scale = nullptr;
-    int self = 0;
-    const float* W = nullptr;         // fp32 master weights
-    int N = 0;
-    int b_trans = 0;
-    int relu = 0;
-    const void* mask = nullptr;       // [n x N] bf16 or null
-    void* out = nullptr;              // [n x N] bf16
-    void* agg_out = nullptr;          // [n x K] bf16 or null
-    void* hagg = nullptr;             // scratch [n_heavy x K] bf16
-    float* partial = nullptr;         // scratch [n_slots x K] fp32
-};
-bool spmm_mm_supported(const grappa_part* part, int K, int N, grappa_dtype dt);
-grappa_status spmm_mm(grappa_ctx* ctx, const grappa_part* part, const AggMMArgs& m, cudaStream_t s);
-void spmm_set_fuse(int v);
-void spmm_set_wide(int v);
-
 grappa_status spmm(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grappa_dtype dt,
                    cudaStream_t s);
 // the transpose operator A_loc^T (backward aggregations): A_loc itself for induced-core

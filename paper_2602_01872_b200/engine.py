@@ -126,7 +126,7 @@ class Trainer:
                  num_chunks: int, chunk_seed: int, corr: str = "resampling", lr: float = 0.003,
                  repartition_every: int = 10, dtype: str = "f32", num_workers: int | None = None,
                  stream=None, controller=None, halo: bool = False, capacity: bool = False,
-                 sharded: bool = False):
+                 sharded: bool = False, comm_dtype: str = "f32", eps: float = 1e-9, c_max: float = 10.0):
         self.ctx = ctx
         self.dev = torch.device("cuda", ctx.device)
         self.stream = stream or torch.cuda.current_stream(self.dev)
@@ -137,6 +137,8 @@ class Trainer:
         self.rank = ctx.rank
         self.corr = corr
         self.lr = lr
+        # a7 arguments: all-reduce payload dtype (fused scale/cast) and the R12 guards
+        self.comm_dtype, self.eps, self.c_max = comm_dtype, eps, c_max
         self.rep_every = repartition_every
         # optional §3.5 controller (paper_2602_01872_b200.controller.Controller): decides the
         # super-epoch switches instead of the fixed `repartition_every`
@@ -193,10 +195,16 @@ class Trainer:
             blk = np.concatenate([np.asarray(w, dtype=np.float32) for w in ws], axis=0)
             self.w_views[l].copy_(torch.from_numpy(blk))
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.graph = None                # CUDA graph of one epoch (run_epoch_graph), per super-epoch
         self.parts: dict = {}            # worker id -> Part (this rank's workers)
         self.t = None
         self.epoch = 0
         self.losses = []
+
+    def check(self):
+        """grappa_check on the training stream: E_NONFINITE if any aggregated gradient since the
+        last check was non-finite (its SGD step was skipped on the device), E_CUDA / E_NCCL."""
+        self.ctx.check(self.stream)
 
     # ------------------------------------------------------------------ partitions
     def my_workers(self):
@@ -204,7 +212,14 @@ class Trainer:
         return [(i, i * self.G + self.rank) for i, _, _ in phase_plan(self.W, self.G, self.rank)]
 
     def repartition(self, t: int):
-        """a3 for super-epoch t on every worker this rank owns."""
+        """a3 for super-epoch t on every worker this rank owns.  Drops any captured
+        epoch graph first: it holds the previous partitions' sizes, SpMM plans, tensor maps,
+        coverage factors and buffer pointers, so it must never be replayed on the new layout."""
+        self.graph = None
+        if self.t is not None:
+            # the switch synchronises anyway: surface a non-finite aggregate of the last
+            # super-epoch now (the device skipped those updates; S:424)
+            self.check()
         pairs = self.schedule[(t - 1) % len(self.schedule)]
         if self.capacity:
             return self._repartition_to_host(t, pairs)
@@ -350,7 +365,8 @@ class Trainer:
         else:
             self.grad.zero_()
         grappa_aggregate_grads(self.ctx, part, self.corr, self.grad, m_active,
-                               self.lr if lr is None else lr, self.theta, self.stream)
+                               self.lr if lr is None else lr, self.theta, self.stream, eps=self.eps,
+                               c_max=self.c_max, comm_dtype=self.comm_dtype)
         self._steps.append((part.factor(self.corr), 1.0) if part is not None else (0.0, 0.0))
 
     # ------------------------------------------------------------------ super-epochs
@@ -441,8 +457,7 @@ class Trainer:
         h0 = time.perf_counter()
         t = self.super_epoch()
         if t != self.t:
-            self.repartition(t)
-            self.graph = None
+            self.repartition(t)                 # drops the previous super-epoch's graph
         h1 = time.perf_counter()
         if getattr(self, "graph", None) is not None:
             self.graph.replay()
@@ -610,7 +625,7 @@ class MinibatchTrainer(Trainer):
                     self.grad.zero_()
                     c = 0.0
                 grappa_aggregate_grads_c(self.ctx, c, self.grad, m_active, self.lr, self.theta,
-                                         self.stream)
+                                         self.stream, comm_dtype=self.comm_dtype)
                 self._steps.append((c, 1.0) if part is not None else (0.0, 0.0))
                 if on_phase is not None:
                     on_phase()

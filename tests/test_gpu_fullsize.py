@@ -22,6 +22,8 @@ from oracle import model as Mo
 from oracle import partition as Po
 from oracle import train as Tr
 
+from _parity import assert_flips_bounded  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 
 
@@ -133,7 +135,8 @@ def test_fullsize_phase_update(setup):
     X = torch.from_numpy(ds.x[:, :wl.F]).to(torch.bfloat16).double().numpy()[part["core"]]
     W0 = [[np.asarray(w, np.float64)[:wl.dims[l], :wl.dims[l + 1]] for w in ws]
           for l, ws in enumerate(ds.weights)]
-    _, g, _, _ = Mo.partition_loss_grad(wl.arch, part, X, ds.y[part["core"]], W0, masks)
+    _, g, _, cache = Mo.partition_loss_grad(wl.arch, part, X, ds.y[part["core"]], W0, masks)
+    assert_flips_bounded(cache, "bf16", "fullsize phase")
     ref = Co.aggregate([Tr.partition_factor(wl.correction, part)], [g], 1)
     assert err(ghat, ref) <= 2e-2
     tr.theta.copy_(theta0)

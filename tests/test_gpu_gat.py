@@ -13,6 +13,8 @@ from oracle import model as Mo
 from oracle import partition as Po
 from oracle import train as Tr
 
+from _parity import assert_flips_bounded  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 TOL = {"f32": 1e-4, "bf16": 2e-2}
 
@@ -84,7 +86,7 @@ def test_gat_layer_parity(G, ctx, prod, f_in, f_out, dtype, halo):
     op = Mo.operator("gat", part.rowptr.cpu().numpy(), part.col.cpu().numpy(), n)
     H, W = _np(h_in), _np(w)
     Ws = [W[:f_in], W[f_in:]]
-    P, Z, Hn = Mo.layer_forward("gat", op, H, Ws, True, mask=(_np(h_out) > 0).astype(np.float64))
+    P, Z, Hn = Mo.layer_forward("gat", op, H, Ws, True)
     tol = TOL[dtype]
     assert err(_np(h_out), Hn) <= tol
     grads, dH = Mo.layer_backward("gat", op, H, P, Ws, _np(dz))
@@ -153,7 +155,8 @@ def test_gat_epoch_parity(G, ctx, prod, dtype, halo):
     for k in range(P):
         b, s = sched[0][k]
         part = Po.induced_partition(ds.rowptr, ds.col, chunk_of, b, s, ds.train, halo=halo)
-        _, g, _, _ = Mo.partition_loss_grad("gat", part, X[part["core"]], ds.y[part["core"]],
-                                            Mo.unflatten(thetas[k], shapes), masks[k])
+        _, g, _, cache = Mo.partition_loss_grad("gat", part, X[part["core"]], ds.y[part["core"]],
+                                                Mo.unflatten(thetas[k], shapes), masks[k])
+        assert_flips_bounded(cache, dtype, f"gat phase {k}")
         ref = Co.aggregate([Tr.partition_factor("uniform", part)], [g], 1)
         assert err(ghat[k], ref) <= TOL[dtype], k

@@ -14,6 +14,8 @@ from oracle import model as Mo
 from oracle import partition as Po
 from oracle import train as Tr
 
+from _parity import assert_flips_bounded  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 TOL = {"f32": 1e-4, "bf16": 2e-2}
 
@@ -125,7 +127,7 @@ def test_halo_layer_parity(G, ctx, prod, arch, f_in, f_out, dtype, flags):
     op = Mo.operator(arch, rp, cl, n, node_w)
     H, W = _np(h_in), _np(w)
     Ws = [W] if arch == "gcn" else [W[:f_in], W[f_in:]]
-    P, Z, Hn = Mo.layer_forward(arch, op, H, Ws, True, mask=(_np(h_out) > 0).astype(np.float64))
+    P, Z, Hn = Mo.layer_forward(arch, op, H, Ws, True)
     tol = TOL[dtype]
     assert err(_np(h_out), Hn) <= tol
     dz_ref = _np(dz_k) / nrm[:, None] if normed else _np(dz_k)
@@ -181,8 +183,9 @@ def test_halo_epoch_parity(G, ctx, prod):
     for k in range(P):
         b, s = sched[0][k]
         part = Po.induced_partition(ds.rowptr, ds.col, chunk_of, b, s, ds.train, halo=True)
-        _, g, _, _ = Mo.partition_loss_grad(wl.arch, part, X[part["core"]], ds.y[part["core"]],
-                                            Mo.unflatten(thetas[k], shapes), masks[k])
+        _, g, _, cache = Mo.partition_loss_grad(wl.arch, part, X[part["core"]], ds.y[part["core"]],
+                                                Mo.unflatten(thetas[k], shapes), masks[k])
+        assert_flips_bounded(cache, "f32", f"halo phase {k}")
         c = Tr.partition_factor("resampling", part)
         assert c == 1.0
         assert err(ghat[k], Co.aggregate([c], [g], 1)) <= 1e-4, k

@@ -15,6 +15,8 @@ from oracle import model as Mo
 from oracle import partition as Po
 from oracle import sampler as Sa
 
+from _parity import assert_flips_bounded  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 FAN = [6, 4, 3]        # input -> output layer (scaled-down {15, 10, 5})
 
@@ -106,6 +108,7 @@ def test_minibatch_step_parity(G, setup, dtype):
         X = torch.from_numpy(ds.x).to(torch.bfloat16).float().numpy().astype(np.float64)[ref["core"]][blocks[0]["src"]]
     masks = [(h.float().cpu().numpy() > 0).astype(np.float64) for h in hidden]
     lg, cache = Sa.sage_forward(blocks, X, W, masks)
+    assert_flips_bounded(cache, dtype, "minibatch step")
     K = wl.K
     L_ref, dZ = Mo.loss_and_dlogits(lg[:, :K], ds.y[ref["core"]][seeds], np.arange(len(seeds)))
     dZp = np.zeros_like(lg)

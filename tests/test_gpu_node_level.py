@@ -17,6 +17,8 @@ from oracle import partition as Po
 from oracle import sampler as Sa
 from oracle import train as Tr
 
+from _parity import assert_flips_bounded  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 TOL = {"f32": 1e-4, "bf16": 2e-2}
 
@@ -111,7 +113,7 @@ def test_layer_parity_node_level(G, ctx, prod, arch, f_in, f_out, dtype, normed)
     H = _np(h_in)
     W = _np(w)
     Ws = [W] if arch == "gcn" else [W[:f_in], W[f_in:]]
-    P, Z, Hn = Mo.layer_forward(arch, op, H, Ws, True, mask=(_np(h_out) > 0).astype(np.float64))
+    P, Z, Hn = Mo.layer_forward(arch, op, H, Ws, True)
     tol = TOL[dtype]
     assert err(_np(h_out), Hn) <= tol
     # the weighting is visible: the uncorrected operator is off by more than the tolerance
@@ -189,11 +191,12 @@ def test_epoch_parity_node_level(G, ctx, prod, dtype):
         b, s = sched[0][k]
         part = Po.induced_partition(ds.rowptr, ds.col, chunk_of, b, s, ds.train)
         nw = Co.node_weights(part["d_l"], part["d_g"])
-        _, g, _, _ = Mo.partition_loss_grad(wl.arch, part, X[part["core"]], ds.y[part["core"]],
-                                            Mo.unflatten(thetas[k], shapes), masks[k], node_w=nw)
+        _, g, _, cache = Mo.partition_loss_grad(wl.arch, part, X[part["core"]], ds.y[part["core"]],
+                                                Mo.unflatten(thetas[k], shapes), masks[k], node_w=nw)
+        assert_flips_bounded(cache, dtype, f"node-level phase {k}")
         # the node-level gradient differs from the uncorrected one (the weights act)
         _, g0, _, _ = Mo.partition_loss_grad(wl.arch, part, X[part["core"]], ds.y[part["core"]],
-                                             Mo.unflatten(thetas[k], shapes), masks[k])
+                                             Mo.unflatten(thetas[k], shapes))      # uncorrected, own ReLU
         assert err(g0, g) > 1e-3
         assert err(ghat[k], Co.aggregate([1.0], [g], 1)) <= TOL[dtype], k
     if dtype == "f32":
@@ -244,6 +247,7 @@ def test_minibatch_node_level(G, ctx, dtype):
     X = xs[ref["core"]][blocks[0]["src"]]
     masks = [(h.float().cpu().numpy() > 0).astype(np.float64) for h in hidden]
     lg, cache = Sa.sage_forward(blocks, X, W, masks, node_w=node_w)
+    assert_flips_bounded(cache, dtype, "node-level minibatch step")
     K = wl.K
     L_ref, dZ = Mo.loss_and_dlogits(lg[:, :K], ds.y[ref["core"]][seeds], np.arange(len(seeds)))
     dZp = np.zeros_like(lg)
@@ -280,7 +284,7 @@ def test_gcn_input_layer_aggregate_first(G, ctx, prod, dtype, node, f_in, f_out)
     node_w = Co.node_weights(part.d_l.cpu().numpy(), part.d_g.cpu().numpy()) if node else None
     op = Mo.operator("gcn", part.rowptr.cpu().numpy(), part.col.cpu().numpy(), n, node_w)
     H, W = _np(h_in), _np(w)
-    P, Z, Hn = Mo.layer_forward("gcn", op, H, [W], True, mask=(_np(h_out) > 0).astype(np.float64))
+    P, Z, Hn = Mo.layer_forward("gcn", op, H, [W], True)
     tol = TOL[dtype]
     assert err(_np(h_out), Hn) <= tol
     grads, _ = Mo.layer_backward("gcn", op, H, P, [W], _np(dz))
