@@ -25,7 +25,7 @@ _TORCH_DT = {F32: torch.float32, BF16: torch.bfloat16}
 
 
 def dtype_code(dt) -> int:
-    if dt in (F32, BF16):
+    if isinstance(dt, int):          # raw codes pass through (the library validates them)
         return dt
     return {torch.float32: F32, torch.bfloat16: BF16, "f32": F32, "fp32": F32,
             "bf16": BF16}[dt]

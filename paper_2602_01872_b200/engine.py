@@ -196,6 +196,10 @@ class Trainer:
             self.w_views[l].copy_(torch.from_numpy(blk))
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=self.dev)
         self.graph = None                # CUDA graph of one epoch (run_epoch_graph), per super-epoch
+        # test instrumentation: phase_probe(phase, worker) is called after every phase step of
+        # run_epoch_graph, on the stream the step ran on (inside the capture, so stream-ordered
+        # copies it enqueues are replayed with the graph); None in normal runs
+        self.phase_probe = None
         self.parts: dict = {}            # worker id -> Part (this rank's workers)
         self.t = None
         self.epoch = 0
@@ -484,11 +488,15 @@ class Trainer:
                         with torch.cuda.stream(main):
                             self.stream = main
                             self.phase_step(i, w, m_active)       # runs now
+                            if self.phase_probe is not None:
+                                self.phase_probe(i, w)
                     saved, self._steps = self._steps, []
                     l0 = self.ctx.launches()
                     self.stream = cap
                     self.phase_step(i, w, m_active)               # recorded for the replays
                     n_cap += self.ctx.launches() - l0
+                    if self.phase_probe is not None:              # its copies are captured too
+                        self.phase_probe(i, w)
                     cap_steps += self._steps
                     self._steps = saved
                 h2 = time.perf_counter()
