@@ -182,16 +182,28 @@ class Part:
             self.x = None
         return self
 
-    def host_image(self):
-        """Pinned host buffers for this partition's arrays (grappa_part_host) + the struct."""
+    def host_image(self, reuse: dict | None = None, headroom: float = 0.0):
+        """Pinned host buffers for this partition's arrays (grappa_part_host) + the struct.
+        reuse: the buffers of an earlier image (e.g. the previous super-epoch's partition of the
+        same worker) -- views of them are returned where they are large enough, so a switch
+        does not re-pin host memory; new buffers get `headroom` extra capacity."""
         I = self.info
         tdt = torch.bfloat16 if I.dtype == BF16 else torch.float32
-        pin = lambda n, dt: torch.empty(n, dtype=dt, pin_memory=True)
-        bufs = dict(rowptr=pin(I.n_core + 1, torch.int64), col=pin(I.nnz, torch.int32),
-                    d_l=pin(I.n_core, torch.int32), norm_gcn=pin(I.n_core, torch.float32),
-                    norm_sage=pin(I.n_core, torch.float32), seeds=pin(I.n_seeds, torch.int32),
-                    labels=pin(I.n_core, torch.int32), x=pin(I.n_core * I.feat_dim, tdt),
-                    node_w=pin(3 * I.n_core, torch.float32))
+        want = dict(rowptr=(I.n_core + 1, torch.int64), col=(I.nnz, torch.int32), d_l=(I.n_core, torch.int32),
+                    norm_gcn=(I.n_core, torch.float32), norm_sage=(I.n_core, torch.float32),
+                    seeds=(I.n_seeds, torch.int32), labels=(I.n_core, torch.int32),
+                    x=(I.n_core * I.feat_dim, tdt), node_w=(3 * I.n_core, torch.float32))
+        bufs = {}
+        for k, (n, dt) in want.items():
+            old = (reuse or {}).get(k)
+            base = getattr(old, "_grappa_base", old)
+            if base is not None and base.dtype == dt and base.numel() >= n:
+                v = base[:n]
+            else:
+                base = torch.empty(max(n, int(n * (1 + headroom))), dtype=dt, pin_memory=True)
+                v = base[:n]
+            v._grappa_base = base
+            bufs[k] = v
         st = _lib.PartHost(**{k: v.data_ptr() for k, v in bufs.items()})
         return bufs, st
 

@@ -97,6 +97,10 @@ ProfScope::ProfScope(grappa_ctx* c, cudaStream_t st, int cls, double bytes, doub
     ctx->prof.push_back(r);
 }
 
+void ProfScope::set_bytes(double bytes) {
+    if (idx >= 0) ctx->prof[idx].bytes = bytes;
+}
+
 ProfScope::~ProfScope() {
     if (idx >= 0) cudaEventRecord(ctx->prof[idx].b, s);
 }

@@ -143,6 +143,8 @@ struct ProfScope {
     int idx = -1;
     ProfScope(grappa_ctx* c, cudaStream_t st, int cls, double bytes, double flops);
     ~ProfScope();
+    // algorithmic bytes known only after the call has sized its outputs (repartition)
+    void set_bytes(double bytes);
 };
 
 // Device-wide exclusive scan helpers (scan.cu).  `count` elements of int32 `in` (or the

@@ -231,7 +231,9 @@ __global__ void k_row_finalize(int64_t n_core, const int32_t* __restrict__ task_
                                const int64_t* __restrict__ task_out, const int32_t* __restrict__ core_global,
                                const int64_t* __restrict__ g_rowptr, const int32_t* __restrict__ g_labels,
                                int64_t* rowptr, int32_t* d_l, int32_t* d_g, float* norm_gcn, float* norm_sage,
-                               float* node_w, int64_t w_stride, int32_t* labels) {
+                               float* node_w, int64_t w_stride, int32_t* labels,
+                               unsigned long long* __restrict__ sum_dg) {
+    unsigned long long my_dg = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_core;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t a = task_out[task_off[i]], b = task_out[task_off[i + 1]];
@@ -242,6 +244,7 @@ __global__ void k_row_finalize(int64_t n_core, const int32_t* __restrict__ task_
         d_l[i] = cnt;
         const int32_t dg = (int32_t)(g_rowptr[v + 1] - g_rowptr[v]);
         d_g[i] = dg;
+        my_dg += (unsigned long long)dg;
         const double ng = 1.0 / sqrt((double)cnt + 1.0), ns = cnt > 0 ? 1.0 / (double)cnt : 0.0;
         norm_gcn[i] = (float)ng;
         norm_sage[i] = (float)ns;
@@ -252,6 +255,10 @@ __global__ void k_row_finalize(int64_t n_core, const int32_t* __restrict__ task_
         node_w[2 * w_stride + i] = (float)(w * ns);
         labels[i] = g_labels ? g_labels[v] : 0;
     }
+    // sum of the core rows' global degrees (integer, order-free): the rows' source bytes for the
+    // algorithmic byte count of the profiling scope
+    my_dg = warp_sum(my_dg);
+    if ((threadIdx.x & 31) == 0 && my_dg) atomicAdd(sum_dg, my_dg);
 }
 
 // stable ballot compaction of every task's kept neighbours, relabelled to local ids
@@ -616,10 +623,12 @@ static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const voi
     GRAPPA_LAUNCHED(ctx);
     // 3. scans: task outputs (= local col offsets, total = nnz), then per-row finalize
     RP_TRY(device_scan(ctx, ReadTcount{tcount, d_stat + 5}, T_max, WriteTaskOut{task_out, d_stat}, s));
+    GRAPPA_CUDA(cudaMemsetAsync(d_stat + 7, 0, 8, s));      // sum of d_g (k_row_finalize)
     k_row_finalize<<<grid, 256, 0, s>>>(n_core, task_off, task_out, srow, G_rowptr, G_labels,
                                          (int64_t*)p->rowptr.p, (int32_t*)p->d_l.p, (int32_t*)p->d_g.p,
                                          (float*)p->norm_gcn.p, (float*)p->norm_sage.p,
-                                         (float*)p->node_w.p, n_local, (int32_t*)p->labels.p);
+                                         (float*)p->node_w.p, n_local, (int32_t*)p->labels.p,
+                                         (unsigned long long*)(d_stat + 7));
     GRAPPA_LAUNCHED(ctx);
     if (halo && n_halo > 0) {
         k_halo_rows<<<grid, 256, 0, s>>>(n_core, n_local, d_stat + 1, core_global, g->rowptr, labels,
@@ -661,7 +670,9 @@ static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const voi
     k_seed_stats_final<<<1, 32, 0, s>>>(nb, (SeedStats*)ctx->scan_ws.p, d_seedstats);
     GRAPPA_LAUNCHED(ctx);
     SeedStats hs;
-    if (cudaMemcpyAsync(&hs, d_seedstats, sizeof(hs), cudaMemcpyDeviceToHost, s) != cudaSuccess) {
+    int64_t sum_dg = 0;
+    if (cudaMemcpyAsync(&hs, d_seedstats, sizeof(hs), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(&sum_dg, d_stat + 7, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) {
         set_error("grappa_repartition: %s", cudaGetErrorString(cudaGetLastError()));
         return fail(GRAPPA_E_CUDA);
     }
@@ -725,6 +736,10 @@ static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const voi
                           d_stat + 3, &p->t_n_heavy, &p->t_n_slots));
     }
     GRAPPA_CUDA(cudaStreamSynchronize(s));
+    // algorithmic bytes (SURVEY §8(d) d.3 per core row: rowptr 8 + d_g source columns 4 d_g +
+    // kept columns 4 d_l + per-row outputs 24 + the feature row read and written 2 F s)
+    ps.set_bytes((double)n_core * (8.0 + 24.0 + 2.0 * (feats ? feat_dim * esz : 0)) + 4.0 * (double)sum_dg +
+                 4.0 * (double)nnz);
     // publish
     grappa_part_info& I = p->info;
     I.n_core = n_local; I.nnz = nnz; I.n_seeds = n_seeds; I.base = base; I.swept = swept;
