@@ -416,6 +416,11 @@ def run_grappa(args):
     probes = {"l2_gather_256B_64MiB": ctx.roofline_probe("l2_gather", 64 << 20, 256, iters=10, stream=stream),
               "l2_read_64MiB": ctx.roofline_probe("l2_read", 64 << 20, iters=10, stream=stream),
               "hbm_copy_2GiB": ctx.roofline_probe("hbm_copy", 2 << 30, iters=5, stream=stream)}
+    # the same probe at the footprint of this run's gathered table (rows of the widest SpMM of the
+    # largest partition; uniform random rows, so a lower bound on the hit rate the SpMM sees)
+    n_max = max([p.n_core for p in tr.parts.values()] + [1])
+    tab = ((n_max * max(spec.dims_pad[1:]) * (2 if args.dtype == "bf16" else 4)) >> 20) + 1
+    probes[f"l2_gather_256B_{tab}MiB"] = ctx.roofline_probe("l2_gather", tab << 20, 256, iters=10, stream=stream)
     l2_peak = probes["l2_gather_256B_64MiB"]
     sp_ms, sp_n, sp_b, _ = prof["spmm"]
     t_call = (sp_ms / sp_n / 1e3) if sp_n else None
@@ -464,7 +469,7 @@ def run_grappa(args):
             kernels[k]["frac_hbm"] = kernels[k]["GB/s"] / hbm
     for k in ("gemm", "gemm_tn"):
         if kernels[k]["TFLOP/s"]:
-            kernels[k]["frac_tensor_peak"] = kernels[k]["TFLOP/s"] * 1e3 / bf16_peak
+            kernels[k]["frac_tensor_peak"] = kernels[k]["TFLOP/s"] / bf16_peak
 
     # fp32 storage arm of the same workload (the paper states no precision; SURVEY §6 presumes
     # fp32): the same epochs on a second Trainer holding fp32 features/activations

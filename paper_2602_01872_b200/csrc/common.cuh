@@ -147,10 +147,6 @@ struct ProfScope {
     void set_bytes(double bytes);
 };
 
-// Device-wide exclusive scan helpers (scan.cu).  `count` elements of int32 `in` (or the
-// flag functor result) -> int64 exclusive prefix in `out` (out[count] = total), total also
-// returned in *d_total (device int64) when non-null.
-grappa_status scan_i32_to_i64(grappa_ctx* ctx, const int32_t* in, int64_t count, int64_t* out,
-                              cudaStream_t s);
+// Device-wide exclusive scans: device_scan in scan.cuh.
 
 }  // namespace grappa

@@ -1074,6 +1074,24 @@ static grappa_status make_map(CUtensorMap* m, const void* ptr, int64_t rows, int
     return GRAPPA_OK;
 }
 
+// row-gather map of a bf16 row-major [rows x cols] tensor for tile::gather4: box {cols, 1} (each
+// gather4 writes 4 whole rows contiguously), no swizzle (spmm_tma.cu)
+grappa_status tma_map_rows_bf16(CUtensorMap* m, const void* ptr, int64_t rows, int cols) {
+    GRAPPA_TRY(get_encoder());
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)(rows > 0 ? rows : 1)};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    cuuint32_t box[2] = {(cuuint32_t)cols, 1u};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled (row gather) failed (%d): rows=%lld cols=%d", (int)r, (long long)rows, cols);
+        return GRAPPA_E_CUDA;
+    }
+    return GRAPPA_OK;
+}
+
 // A ring + resident weights + 2 groups x nsb staging boxes + barriers; the deepest ring
 // (<= 8 stages) and double-buffered staging when they fit
 static size_t nn_smem_of(int kbt, int N, int stages, int nsb, int mask_tma) {

@@ -19,6 +19,22 @@ grappa_status shard_merge(grappa_ctx* ctx, const grappa_shard* sa, const grappa_
                           cudaStream_t s);
 }  // namespace grappa
 
+namespace grappa {
+// TMA-gather SpMM plan of one operator (spmm_tma.cu): the degree-ordered 16-row tiles of the
+// SpMM's row space (split-row segments, then rows by descending degree) assigned round-robin to
+// `grid` persistent CTAs and stored CTA-major, so each CTA streams one contiguous range of
+// "steps" (a step = one gathered row per tile row: the self row, then the j-th neighbour).
+struct TmaPlan {
+    DevBuf tsteps;      // int32 [grid * tpc]   steps of each tile (0 for padding tiles)
+    DevBuf toff;        // int64 [grid * tpc + 1] exclusive scan of tsteps
+    DevBuf tinfo;       // int2  [grid * tpc * 16] per tile row {out row | slot flag, degree}
+    DevBuf stream;      // int32 [sum tsteps * 16] gather row ids, step-major
+    int grid = 0;
+    int64_t tpc = 0;    // tiles per CTA
+    bool ready = false;
+};
+}  // namespace grappa
+
 // one chunk's rows (sharded mode): ids ascending, local rowptr from 0, global neighbour ids
 struct grappa_shard {
     grappa_shard_info info{};
@@ -51,4 +67,6 @@ struct grappa_part {
     // (k_gat_rev) on the first GAT backward in induced-core mode
     grappa::DevBuf t_eid;
     bool t_eid_ready = false;
+    // TMA-gather SpMM plans (built on first use; invalidated by repartition / image load)
+    grappa::TmaPlan tma, t_tma;
 };

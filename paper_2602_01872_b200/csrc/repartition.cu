@@ -689,6 +689,7 @@ static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const voi
     p->n_halo = n_halo;
     p->t_n_heavy = p->t_n_slots = 0;
     p->t_eid_ready = halo;            // induced-core: built lazily by the first GAT backward
+    p->tma.ready = p->t_tma.ready = false;   // TMA SpMM plans: rebuilt on first use
     if (halo) {
         // cub's radix sort takes an int item count
         if (nnz >= ((int64_t)1 << 31)) {
@@ -945,6 +946,7 @@ extern "C" grappa_status grappa_part_load(grappa_part** inout, const void* host,
     p->halo = h.halo != 0;
     p->n_halo = h.n_halo; p->t_n_heavy = h.t_n_heavy; p->t_n_slots = h.t_n_slots;
     p->t_eid_ready = p->halo;
+    p->tma.ready = p->t_tma.ready = false;
     grappa_part_info& I = p->info;
     I = h.info;
     I.rowptr = (int64_t*)p->rowptr.p; I.col = (int32_t*)p->col.p;

@@ -548,6 +548,38 @@ static grappa_status launch_t(grappa_ctx* ctx, const SpmmArgs& a, cudaStream_t s
     return GRAPPA_E_SHAPE;
 }
 
+// split-row combine for bf16 rows (the TMA kernel's fix-up: same launch as launch_grp's)
+grappa_status spmm_fixup(grappa_ctx* ctx, const SpmmArgs& a, cudaStream_t s) {
+    if (a.n_heavy > 0) {
+        k_spmm_fixup_blk<__nv_bfloat16><<<(unsigned)a.n_heavy, kFixWarps * 32, 0, s>>>(a, a.width / 8);
+        GRAPPA_LAUNCHED(ctx);
+    }
+    return GRAPPA_OK;
+}
+
+static double spmm_bytes(const SpmmArgs& a, grappa_dtype dt) {
+    const double es = dt == GRAPPA_BF16 ? 2.0 : 4.0, w = a.width, nnz = (double)a.nnz;
+    const double per_edge = 4.0 + (a.col_scale || a.edge_w ? 4.0 : 0.0) + w * es;
+    const bool self_coef = a.self && (a.self_sep ? a.self_scale != nullptr : a.col_scale != nullptr);
+    const double per_row = 8.0 + (a.row_scale ? 4.0 : 0.0) + (self_coef ? 4.0 : 0.0) +
+                           (a.nbr_scale ? 4.0 : 0.0) + (a.self ? w * es : 0.0) + w * es +
+                           (a.accumulate ? w * es : 0.0) + (a.mask ? w * es : 0.0);
+    return nnz * per_edge + (double)a.n * per_row;
+}
+
+// a partition operator: the TMA-gather kernel when selected and applicable (spmm_tma.cu), else
+// the row-group / warp-per-row kernels
+static grappa_status spmm_part(grappa_ctx* ctx, const grappa_part* part, bool transpose, SpmmArgs& a,
+                               grappa_dtype dt, cudaStream_t s) {
+    if (a.width % 8 != 0) {
+        set_error("spmm: width %d not a multiple of 8", a.width);
+        return GRAPPA_E_SHAPE;
+    }
+    ProfScope ps(ctx, s, GRAPPA_K_SPMM, spmm_bytes(a, dt), 2.0 * (double)a.nnz * a.width);
+    if (spmm_tma_eligible(ctx, a, dt)) return spmm_tma(ctx, part, transpose, a, s);
+    return dt == GRAPPA_BF16 ? launch_t<__nv_bfloat16>(ctx, a, s) : launch_t<float>(ctx, a, s);
+}
+
 grappa_status spmm(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grappa_dtype dt,
                    cudaStream_t s) {
     const grappa_part_info& I = part->info;
@@ -563,7 +595,7 @@ grappa_status spmm(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grappa_
     a.heavy_slot_off = (const int32_t*)part->heavy_slot_off.p;
     a.row_order = spmm_var(ctx) == 3 ? nullptr : (const int32_t*)part->row_order.p;
     a.row_desc = spmm_var(ctx) == 3 ? nullptr : (const int4*)part->row_desc.p;
-    return spmm_csr(ctx, a, dt, s);
+    return spmm_part(ctx, part, false, a, dt, s);
 }
 
 grappa_status spmm_t(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grappa_dtype dt,
@@ -582,7 +614,7 @@ grappa_status spmm_t(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grapp
     a.heavy_slot_off = (const int32_t*)part->t_heavy_slot_off.p;
     a.row_order = spmm_var(ctx) == 3 ? nullptr : (const int32_t*)part->t_row_order.p;
     a.row_desc = spmm_var(ctx) == 3 ? nullptr : (const int4*)part->t_row_desc.p;
-    return spmm_csr(ctx, a, dt, s);
+    return spmm_part(ctx, part, true, a, dt, s);
 }
 
 grappa_status spmm_csr(grappa_ctx* ctx, SpmmArgs a, grappa_dtype dt, cudaStream_t s) {
@@ -590,14 +622,7 @@ grappa_status spmm_csr(grappa_ctx* ctx, SpmmArgs a, grappa_dtype dt, cudaStream_
         set_error("spmm: width %d not a multiple of 8", a.width);
         return GRAPPA_E_SHAPE;
     }
-    struct { int64_t n_core, nnz; } I{a.n, a.nnz};
-    const double es = dt == GRAPPA_BF16 ? 2.0 : 4.0, w = a.width, nnz = (double)I.nnz;
-    const double per_edge = 4.0 + (a.col_scale || a.edge_w ? 4.0 : 0.0) + w * es;
-    const bool self_coef = a.self && (a.self_sep ? a.self_scale != nullptr : a.col_scale != nullptr);
-    const double per_row = 8.0 + (a.row_scale ? 4.0 : 0.0) + (self_coef ? 4.0 : 0.0) +
-                           (a.nbr_scale ? 4.0 : 0.0) + (a.self ? w * es : 0.0) + w * es +
-                           (a.accumulate ? w * es : 0.0) + (a.mask ? w * es : 0.0);
-    ProfScope ps(ctx, s, GRAPPA_K_SPMM, nnz * per_edge + (double)I.n_core * per_row, 2.0 * nnz * w);
+    ProfScope ps(ctx, s, GRAPPA_K_SPMM, spmm_bytes(a, dt), 2.0 * (double)a.nnz * a.width);
     return dt == GRAPPA_BF16 ? launch_t<__nv_bfloat16>(ctx, a, s) : launch_t<float>(ctx, a, s);
 }
 

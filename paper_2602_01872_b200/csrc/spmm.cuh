@@ -36,6 +36,13 @@ struct SpmmArgs {
                                       // of the fused kernel; no mask / accumulate / relu)
 };
 
+// TMA-gather kernel (spmm_tma.cu) for bf16 unweighted aggregations at widths 80..128; default when
+// eligible (ctx variant "spmm" 0); its split rows are combined by spmm_fixup (spmm.cu)
+bool spmm_tma_eligible(const grappa_ctx* ctx, const SpmmArgs& a, grappa_dtype dt);
+grappa_status spmm_tma(grappa_ctx* ctx, const grappa_part* part, bool transpose, const SpmmArgs& a,
+                       cudaStream_t s);
+grappa_status spmm_fixup(grappa_ctx* ctx, const SpmmArgs& a, cudaStream_t s);
+
 grappa_status spmm(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grappa_dtype dt,
                    cudaStream_t s);
 // the transpose operator A_loc^T (backward aggregations): A_loc itself for induced-core

@@ -33,6 +33,11 @@ def test_header_declares_the_boundary():
         assert core in names
 
 
+def test_library_resolves_every_symbol_at_load():
+    """RTLD_NOW: an undefined internal symbol fails here, not on the GPU box"""
+    ctypes.CDLL(LIB, mode=os.RTLD_NOW | os.RTLD_LOCAL)
+
+
 def test_every_declared_symbol_is_exported(lib):
     missing = [n for n in declared() if not hasattr(lib, n)]
     assert not missing, missing

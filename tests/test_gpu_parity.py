@@ -481,3 +481,43 @@ def test_bf16_graph_epochs_vs_oracle(G, ctx, eager_capture):
         # the SGD step the graph applied is lr times that update
         assert err(thetas[k] - thetas[k + 1], lr * ghat[k]) <= 1e-2, k
     print(f"{epochs * P} graph-replayed phases vs the oracle, {flips} ReLU decisions within the R16b bound")
+
+
+@pytest.mark.parametrize("width", [128, 112, 80, 96])
+@pytest.mark.parametrize("mode", ["plain", "node", "halo"])
+def test_spmm_tma_bitwise_equals_row_group(G, ctx, prod, width, mode):
+    """The TMA-gather SpMM (spmm_tma.cu, ctx variant "spmm" = 4, for bf16 unweighted aggregations
+    of 80..128 wide rows) sums every row's neighbours in the same edge order as the row-group
+    kernel and applies the same epilogue, so forward h_out (self term, row scale, node-level
+    neighbour scale, ReLU) and the backward dz_in / dW agree BIT FOR BIT with the row-group
+    kernel (the default, variant 0) -- on induced-core partitions (hub rows split into 256-edge segments)
+    and on halo-1 partitions (forward on A, backward on the stored transpose)."""
+    rp, col, x, y, tr = upload(prod)
+    ch = torch.empty(prod.wl.n, dtype=torch.int32, device="cuda")
+    G.grappa_partition(ctx, prod.wl.n, 8, gen.seed_of("chunks"), ch)
+    part = G.grappa_repartition(ctx, rp, col, x.to(torch.bfloat16), "bf16", ch, 8, 2, 5, tr, y,
+                                halo=(mode == "halo"))
+    assert part.info.n_heavy > 0 or mode == "halo"
+    n, f_in = part.n_core, 64
+    g = torch.Generator(device="cuda").manual_seed(width)
+    h_in = torch.randn(n, f_in, device="cuda", generator=g).relu().to(torch.bfloat16)
+    w = (torch.randn(f_in, width, device="cuda", generator=g) / 8).contiguous()
+    dz = (torch.randn(n, width, device="cuda", generator=g) * 1e-2).to(torch.bfloat16)
+    flags = G.LAYER_NODE_LEVEL if mode == "node" else 0
+    outs = []
+    for variant in (4, 0):
+        ctx.set_variant("spmm", variant)
+        ws = torch.empty(G.layer_ws_bytes(part, "gcn", f_in, width, "bf16"), dtype=torch.uint8, device="cuda")
+        h_out = torch.empty(n, width, device="cuda", dtype=torch.bfloat16)
+        G.grappa_layer_fwd_ex(ctx, part, "gcn", f_in, width, True, h_in, w, h_out, None, ws, "bf16", flags)
+        dw = torch.empty_like(w)
+        dz_in = torch.empty(n, f_in, device="cuda", dtype=torch.bfloat16)
+        G.grappa_layer_bwd_ex(ctx, part, "gcn", f_in, width, True, dz, h_in, w, None, dw, dz_in, ws, "bf16",
+                              flags | G.BWD_DZ_OUT_NORMED | G.BWD_DZ_IN_NORMED if mode != "node" else flags)
+        torch.cuda.synchronize()
+        outs.append((h_out.view(torch.int16).clone(), dz_in.view(torch.int16).clone(), dw.clone()))
+    ctx.set_variant("spmm", 0)
+    (a_h, a_dz, a_dw), (b_h, b_dz, b_dw) = outs
+    assert torch.equal(a_h, b_h)
+    assert torch.equal(a_dz, b_dz)
+    assert torch.equal(a_dw, b_dw)
