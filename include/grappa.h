@@ -187,6 +187,21 @@ grappa_status grappa_repartition_ex(grappa_ctx* ctx, const grappa_csr* g, const 
                                     int32_t num_chunks, int32_t base, int32_t swept,
                                     const uint8_t* train_mask, const int32_t* labels, unsigned flags,
                                     grappa_part** inout, void* stream);
+/* a3 for every partition of a super-epoch switch in one call (induced-core partitions from the
+ * replicated global CSR): partition k = chunk pair {bases[k], swepts[k]} (host int32[n_parts]),
+ * written to parts[k] (host array of n_parts grappa_part*; NULL entries -> created, others
+ * reused).  Each partition is bitwise the one grappa_repartition builds; the switch costs two host
+ * syncs in total (sizes after the counting pass, statistics at the end) instead of five per
+ * partition.  chunk_sizes: host int64[num_chunks], grappa_partition's output for this chunk map
+ * (core sizes are allocated from it and checked against the device counts).  Other arguments as
+ * grappa_repartition.  Errors: as grappa_repartition (E_EMPTY names the seedless pair), E_ARG if
+ * chunk_sizes disagree with chunk_of; on error no partition is published and created ones are
+ * destroyed. */
+grappa_status grappa_repartition_batch(grappa_ctx* ctx, const grappa_csr* g, const void* feats, int32_t feat_dim,
+                                       grappa_dtype dtype, const int32_t* chunk_of, int32_t num_chunks,
+                                       const int64_t* chunk_sizes, int32_t n_parts, const int32_t* bases,
+                                       const int32_t* swepts, const uint8_t* train_mask, const int32_t* labels,
+                                       grappa_part** parts, void* stream);
 grappa_status grappa_part_query(const grappa_part* part, grappa_part_info* out);
 void grappa_part_destroy(grappa_part* part);
 

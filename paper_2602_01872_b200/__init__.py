@@ -9,6 +9,7 @@ schedule, buffers) built on these calls.
 from __future__ import annotations
 
 import ctypes
+import sys
 
 import torch
 
@@ -63,7 +64,7 @@ def _torch_alloc(nbytes, stream, user):
 
 
 def _torch_free(ptr, nbytes, stream, user):
-    if ptr:
+    if ptr and not sys.is_finalizing():
         torch.cuda.caching_allocator_delete(int(ptr))
 
 
@@ -142,6 +143,8 @@ class Context:
             self.h = None
 
     def __del__(self):
+        if sys.is_finalizing():      # interpreter exit: the allocator callbacks may be gone; leak
+            return
         try:
             self.close()
         except Exception:
@@ -248,6 +251,8 @@ class Part:
             self.h = ctypes.c_void_p()
 
     def __del__(self):
+        if sys.is_finalizing():      # interpreter exit: the allocator callbacks may be gone; leak
+            return
         try:
             self.destroy()
         except Exception:
@@ -275,6 +280,32 @@ def grappa_repartition(ctx: Context, rowptr: torch.Tensor, col: torch.Tensor, fe
         num_chunks, base, swept, _lib.ptr(train_mask), _lib.ptr(labels),
         _lib.PART_HALO1 if halo else 0, ctypes.byref(part.h), _lib.stream_ptr(stream)))
     return part.refresh()
+
+
+def grappa_repartition_batch(ctx: Context, rowptr: torch.Tensor, col: torch.Tensor, feats, dtype,
+                             chunk_of: torch.Tensor, num_chunks: int, pairs, train_mask: torch.Tensor, labels,
+                             parts=None, stream=None, chunk_sizes=None) -> list:
+    """every partition of a switch (pairs = [(base, swept)] per partition) in one call; parts:
+    list of Part (or None) to reuse.  chunk_sizes: grappa_partition's output for chunk_of (computed
+    with torch on the device if not given)."""
+    g = _lib.Csr(rowptr.numel() - 1, col.numel(), rowptr.data_ptr(), col.data_ptr())
+    K = len(pairs)
+    if chunk_sizes is None:
+        chunk_sizes = torch.bincount(chunk_of.long(), minlength=num_chunks).cpu().tolist()
+    cs = (ctypes.c_int64 * num_chunks)(*[int(c) for c in chunk_sizes])
+    bs = (ctypes.c_int32 * K)(*[int(b) for b, _ in pairs])
+    ss = (ctypes.c_int32 * K)(*[int(s_) for _, s_ in pairs])
+    parts = list(parts) if parts is not None else [None] * K
+    parts = [p if p is not None else Part() for p in parts]
+    hs = (ctypes.c_void_p * K)(*[p.h.value for p in parts])
+    fdim = 0 if feats is None else feats.shape[1]
+    _lib.check("grappa_repartition_batch", ctx.lib.grappa_repartition_batch(
+        ctx.h, ctypes.byref(g), _lib.ptr(feats), fdim, dtype_code(dtype), _lib.ptr(chunk_of), num_chunks, cs, K, bs,
+        ss, _lib.ptr(train_mask), _lib.ptr(labels), hs, _lib.stream_ptr(stream)))
+    for p, h in zip(parts, hs):
+        p.h = ctypes.c_void_p(h)
+        p.refresh()
+    return parts
 
 
 class Shard:
@@ -309,6 +340,8 @@ class Shard:
             self.h = ctypes.c_void_p()
 
     def __del__(self):
+        if sys.is_finalizing():      # interpreter exit: the allocator callbacks may be gone; leak
+            return
         try:
             self.destroy()
         except Exception:
@@ -452,6 +485,8 @@ class Batch:
             self.h = ctypes.c_void_p()
 
     def __del__(self):
+        if sys.is_finalizing():      # interpreter exit: the allocator callbacks may be gone; leak
+            return
         try:
             self.destroy()
         except Exception:

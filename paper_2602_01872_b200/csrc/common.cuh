@@ -116,6 +116,11 @@ struct grappa_ctx {
     // cores; spmm 0 = row-group, 1 = warp per row, 2 = 8 loads in flight, 3 = natural row order;
     // pair 1 = separate GCN backward GEMMs
     int var_gemm = 0, var_spmm = 0, var_pair = 0;
+    // chunk map whose per-chunk counts are known (grappa_partition, or verified once by
+    // grappa_repartition_batch): the batched switch allocates from them without a sync
+    const int32_t* cmap_ptr = nullptr;
+    int64_t cmap_n = 0;
+    std::vector<int64_t> cmap_sizes;
     int64_t comm_grad_bytes = 0;   // gradient all-reduce payload bytes (grappa_comm_bytes)
     int64_t comm_other_bytes = 0;  // every other cross-GPU byte (shard / halo exchange)
 };

@@ -74,5 +74,9 @@ extern "C" grappa_status grappa_partition(grappa_ctx* ctx, int64_t num_nodes, in
     GRAPPA_CUDA(cudaMemcpyAsync(chunk_sizes, d_sizes, (size_t)num_chunks * 8,
                                 cudaMemcpyDeviceToHost, s));
     GRAPPA_CUDA(cudaStreamSynchronize(s));
+    // the batched repartition sizes its partitions from these counts (grappa_repartition_batch)
+    ctx->cmap_ptr = chunk_of;
+    ctx->cmap_n = num_nodes;
+    ctx->cmap_sizes.assign(chunk_sizes, chunk_sizes + num_chunks);
     return GRAPPA_OK;
 }

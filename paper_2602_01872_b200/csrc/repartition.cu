@@ -23,6 +23,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <vector>
 
 namespace grappa {
 
@@ -175,11 +176,20 @@ struct NumTasks {
         return d > kTaskLen ? (int32_t)ceil_div(d, kTaskLen) : 1;
     }
 };
+// task descriptors {core row, edge count, first edge lo, hi}: the count and fill passes read one
+// coalesced 16-byte record per task instead of the dependent row -> core id -> rowptr chain
 struct WriteTasks {
-    int32_t* task_off; int32_t* task_row; int64_t* stat;
+    int32_t* task_off; int4* task_desc; int64_t* stat;
+    const int32_t* core_global; const int64_t* g_rowptr;
     __device__ void operator()(int64_t i, int64_t p, int32_t k) const {
         task_off[i] = (int32_t)p;
-        for (int32_t j = 0; j < k; j++) task_row[p + j] = (int32_t)i;
+        const int32_t v = core_global ? core_global[i] : (int32_t)i;
+        const int64_t e0 = g_rowptr[v], e1 = g_rowptr[v + 1];
+        for (int32_t j = 0; j < k; j++) {
+            const int64_t a = e0 + (int64_t)j * kTaskLen;
+            const int32_t len = (int32_t)min((int64_t)kTaskLen, e1 - a);
+            task_desc[p + j] = make_int4((int)i, len, (int)(uint32_t)(a & 0xffffffffll), (int)(a >> 32));
+        }
     }
     __device__ void finish(int64_t n, int64_t total) const { task_off[n] = (int32_t)total; stat[5] = total; }
 };
@@ -194,35 +204,56 @@ struct WriteTaskOut {
 };
 
 // kept-neighbour count of every task (warp per task, ballot/popc)
-__global__ void k_task_count(const int64_t* __restrict__ d_T, const int32_t* __restrict__ task_row,
-                             const int32_t* __restrict__ task_off, const int32_t* __restrict__ core_global,
-                             const int64_t* __restrict__ g_rowptr, const int32_t* __restrict__ g_col,
-                             const int32_t* __restrict__ rank, int32_t* __restrict__ tcount) {
+// core membership bitmap of partition {b, s}: bit v = [chunk_of[v] in {b, s}] (warp per 32 nodes)
+__global__ void k_core_bitmap(int64_t n, const int32_t* __restrict__ chunk_of, int32_t b, int32_t s,
+                              uint32_t* __restrict__ bitmap) {
     const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < ceil_div(n, 32); w += nw) {
+        const int64_t v = w * 32 + lane;
+        int32_t c = -1;
+        if (v < n) c = chunk_of[v];
+        const unsigned m = __ballot_sync(0xffffffffu, c == b || c == s);
+        if (lane == 0) bitmap[w] = m;
+    }
+}
+__device__ __forceinline__ bool in_core(const uint32_t* __restrict__ bm, int32_t u) {
+    return (__ldg(bm + (u >> 5)) >> (u & 31)) & 1u;
+}
+
+// kept-neighbour count of every task: half a warp per task (2 tasks per warp in flight), 4 x 16
+// edges per round, membership from the core bitmap (ballot / popc).  (Two tasks per half-warp
+// measured slower: 6.9 vs 5.9 ms per products switch, registers.)
+__global__ void k_task_count(const int64_t* __restrict__ d_T, const int4* __restrict__ task_desc,
+                             const int32_t* __restrict__ g_col, const uint32_t* __restrict__ bitmap,
+                             int32_t* __restrict__ tcount) {
+    const int lane = threadIdx.x & 31, half = lane >> 4, sub = lane & 15;
+    const unsigned hmask = 0xffffu << (half * 16);
     const int64_t T = *d_T;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T; t += nwarps) {
-        const int32_t i = task_row[t];
-        const int32_t v = core_global ? core_global[i] : (int32_t)i;
-        const int64_t e0 = g_rowptr[v] + (t - task_off[i]) * (int64_t)kTaskLen;
-        const int64_t e1 = min(g_rowptr[v + 1], e0 + kTaskLen);
-        // 4 x 32 edges per round: the column loads, then the (dependent, L2-resident) rank
-        // probes, are issued together -- 4 probes in flight per lane instead of 1
+    const int64_t nh = ((int64_t)gridDim.x * blockDim.x) >> 4;
+    for (int64_t t0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5 << 1; t0 < T; t0 += nh) {
+        const int64_t t = t0 + half;
+        int32_t len = 0;
+        int64_t e0 = 0;
+        if (t < T) {
+            const int4 d = __ldg(task_desc + t);
+            len = d.y;
+            e0 = (int64_t)(uint32_t)d.z | ((int64_t)d.w << 32);
+        }
+        const int32_t lmax = __reduce_max_sync(0xffffffffu, len);
         int32_t cnt = 0;
-        for (int64_t b = e0; b < e1; b += 128) {
+        for (int32_t b = 0; b < lmax; b += 64) {
             int32_t u[4];
 #pragma unroll
             for (int k = 0; k < 4; k++) {
-                const int64_t e = b + k * 32 + lane;
-                u[k] = e < e1 ? g_col[e] : -1;
+                const int32_t e = b + k * 16 + sub;
+                u[k] = e < len ? __ldg(g_col + e0 + e) : -1;
             }
-            int32_t r[4];
 #pragma unroll
-            for (int k = 0; k < 4; k++) r[k] = u[k] >= 0 ? rank[u[k]] : -1;
-#pragma unroll
-            for (int k = 0; k < 4; k++) cnt += __popc(__ballot_sync(0xffffffffu, r[k] >= 0));
+            for (int k = 0; k < 4; k++)
+                cnt += __popc(__ballot_sync(0xffffffffu, u[k] >= 0 && in_core(bitmap, u[k])) & hmask);
         }
-        if (lane == 0) tcount[t] = cnt;
+        if (sub == 0 && t < T) tcount[t] = cnt;
     }
 }
 
@@ -261,35 +292,45 @@ __global__ void k_row_finalize(int64_t n_core, const int32_t* __restrict__ task_
     if ((threadIdx.x & 31) == 0 && my_dg) atomicAdd(sum_dg, my_dg);
 }
 
-// stable ballot compaction of every task's kept neighbours, relabelled to local ids
-__global__ void k_task_fill(const int64_t* __restrict__ d_T, const int32_t* __restrict__ task_row,
-                            const int32_t* __restrict__ task_off, const int64_t* __restrict__ task_out,
-                            const int32_t* __restrict__ core_global, const int64_t* __restrict__ g_rowptr,
-                            const int32_t* __restrict__ g_col, const int32_t* __restrict__ rank,
+// stable ballot compaction of every task's kept neighbours, relabelled to local ids (half a warp
+// per task, as k_task_count; rank is read for kept edges only)
+__global__ void k_task_fill(const int64_t* __restrict__ d_T, const int4* __restrict__ task_desc,
+                            const int64_t* __restrict__ task_out, const int32_t* __restrict__ g_col,
+                            const uint32_t* __restrict__ bitmap, const int32_t* __restrict__ rank,
                             int32_t* __restrict__ col) {
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, half = lane >> 4, sub = lane & 15;
+    const unsigned hmask = 0xffffu << (half * 16);
+    const unsigned below = ((1u << lane) - 1u) & hmask;
     const int64_t T = *d_T;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < T; t += nwarps) {
-        const int32_t i = task_row[t];
-        const int32_t v = core_global ? core_global[i] : (int32_t)i;
-        const int64_t e0 = g_rowptr[v] + (t - task_off[i]) * (int64_t)kTaskLen;
-        const int64_t e1 = min(g_rowptr[v + 1], e0 + kTaskLen);
-        int64_t out = task_out[t];
-        for (int64_t b = e0; b < e1; b += 128) {          // 4 probes in flight per lane (as above)
+    const int64_t nh = ((int64_t)gridDim.x * blockDim.x) >> 4;
+    for (int64_t t0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5 << 1; t0 < T; t0 += nh) {
+        const int64_t t = t0 + half;
+        int32_t len = 0;
+        int64_t e0 = 0, out = 0;
+        if (t < T) {
+            const int4 d = __ldg(task_desc + t);
+            len = d.y;
+            e0 = (int64_t)(uint32_t)d.z | ((int64_t)d.w << 32);
+            out = task_out[t];
+        }
+        const int32_t lmax = __reduce_max_sync(0xffffffffu, len);
+        for (int32_t b = 0; b < lmax; b += 64) {
             int32_t u[4];
 #pragma unroll
             for (int k = 0; k < 4; k++) {
-                const int64_t e = b + k * 32 + lane;
-                u[k] = e < e1 ? g_col[e] : -1;
+                const int32_t e = b + k * 16 + sub;
+                u[k] = e < len ? __ldg(g_col + e0 + e) : -1;
             }
+            bool keep[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) keep[k] = u[k] >= 0 && in_core(bitmap, u[k]);
             int32_t r[4];
 #pragma unroll
-            for (int k = 0; k < 4; k++) r[k] = u[k] >= 0 ? rank[u[k]] : -1;
+            for (int k = 0; k < 4; k++) r[k] = keep[k] ? __ldg(rank + u[k]) : -1;
 #pragma unroll
             for (int k = 0; k < 4; k++) {                  // stable: edge order kept
-                const unsigned m = __ballot_sync(0xffffffffu, r[k] >= 0);
-                if (r[k] >= 0) col[out + __popc(m & ((1u << lane) - 1u))] = r[k];
+                const unsigned m = __ballot_sync(0xffffffffu, keep[k]) & hmask;
+                if (keep[k]) col[out + __popc(m & below)] = r[k];
                 out += __popc(m);
             }
         }
@@ -310,14 +351,12 @@ __global__ void k_slot_tasks(int64_t n_heavy, const int32_t* heavy_rows, const i
 
 __global__ void k_gather_rows(int64_t n_core, int64_t row_bytes, const int32_t* __restrict__ core_global,
                               const uint4* __restrict__ src, uint4* __restrict__ dst) {
+    // one thread per 16-byte vector of the output (every lane busy whatever the row width)
     const int64_t vec = row_bytes / 16;
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < n_core; i += nwarps) {
-        const uint4* s = src + (int64_t)core_global[i] * vec;
-        uint4* d = dst + i * vec;
-        for (int64_t k = lane; k < vec; k += 32) d[k] = s[k];
+    const int64_t total = n_core * vec;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / vec, k = i - r * vec;
+        dst[i] = __ldg(src + (int64_t)__ldg(core_global + r) * vec + k);
     }
 }
 
@@ -337,10 +376,29 @@ __global__ void k_deg_hist(int64_t n, const int32_t* __restrict__ d_l, unsigned 
         if (sh[i]) atomicAdd(&bins[i], (unsigned long long)sh[i]);
 }
 
+// exclusive scan of the bucket counts by one warp (each lane a contiguous run of buckets)
 __global__ void k_deg_bins_scan(const unsigned long long* bins, unsigned long long* cursor) {
-    if (threadIdx.x == 0) {
-        unsigned long long run = 0;
-        for (int i = 0; i < kDegBuckets; i++) { cursor[i] = run; run += bins[i]; }
+    constexpr int kPer = (kDegBuckets + 31) / 32;
+    const int lane = threadIdx.x & 31;
+    unsigned long long v[kPer], sum = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; k++) {
+        const int i = lane * kPer + k;
+        v[k] = i < kDegBuckets ? bins[i] : 0ull;
+        sum += v[k];
+    }
+    unsigned long long incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    unsigned long long run = incl - sum;
+#pragma unroll
+    for (int k = 0; k < kPer; k++) {
+        const int i = lane * kPer + k;
+        if (i < kDegBuckets) cursor[i] = run;
+        run += v[k];
     }
 }
 
@@ -431,6 +489,12 @@ __global__ void k_seed_stats_final(int nb, const SeedStats* part, SeedStats* out
 
 using namespace grappa;
 
+// blocks of the fixed-order coverage-statistics reduction (the same for every path, so the f64
+// sums are identical whichever call built the partition)
+static int seed_stat_blocks(const grappa_ctx* ctx, int64_t n_seeds) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_seeds, 512), (int64_t)ctx->sm_count * 4));
+}
+
 static grappa_status rp_grid(grappa_ctx* ctx, int64_t rows, int threads, unsigned* grid) {
     int64_t warps_per_block = threads / 32;
     int64_t b = ceil_div(rows, warps_per_block);
@@ -445,6 +509,8 @@ static grappa_status rp_grid(grappa_ctx* ctx, int64_t rows, int threads, unsigne
 struct PlanBufs {
     DevBuf *heavy_rows, *heavy_slot_off, *slot_row, *slot_seg, *row_order, *row_desc;
 };
+static grappa_status plan_order(grappa_ctx* ctx, cudaStream_t s, int64_t n, const int64_t* rowptr,
+                                const int32_t* deg, PlanBufs b);
 static grappa_status build_plan(grappa_ctx* ctx, cudaStream_t s, int64_t n, const int64_t* rowptr,
                                 const int32_t* deg, PlanBufs b, int64_t* d_st, int64_t* n_heavy_out,
                                 int64_t* n_slots_out) {
@@ -472,6 +538,14 @@ static grappa_status build_plan(grappa_ctx* ctx, cudaStream_t s, int64_t n, cons
     // row order: counting sort by descending min(deg, kSegLen + 1)
     GRAPPA_TRY(b.row_order->grow((size_t)(n > 0 ? n : 1) * 4));
     GRAPPA_TRY(ctx->red_ws.grow((size_t)2 * kDegBuckets * 8));
+    *n_heavy_out = n_heavy;
+    *n_slots_out = n_slots;
+    return plan_order(ctx, s, n, rowptr, deg, b);
+}
+
+// degree-bucketed row order (counting sort) and the 16-byte row descriptors of a local CSR
+static grappa_status plan_order(grappa_ctx* ctx, cudaStream_t s, int64_t n, const int64_t* rowptr,
+                                const int32_t* deg, PlanBufs b) {
     unsigned long long* bins = (unsigned long long*)ctx->red_ws.p;
     GRAPPA_CUDA(cudaMemsetAsync(bins, 0, (size_t)kDegBuckets * 8, s));
     const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 8));
@@ -488,9 +562,29 @@ static grappa_status build_plan(grappa_ctx* ctx, cudaStream_t s, int64_t n, cons
     GRAPPA_TRY(b.row_desc->grow((size_t)(n > 0 ? n : 1) * 16));
     k_row_desc<<<g2, 256, 0, s>>>(n, (int32_t*)b.row_order->p, rowptr, (int4*)b.row_desc->p);
     GRAPPA_LAUNCHED(ctx);
-    *n_heavy_out = n_heavy;
-    *n_slots_out = n_slots;
     return GRAPPA_OK;
+}
+
+// build_plan with the split-row sizes known (batched switch): no host sync
+static grappa_status build_plan_sized(grappa_ctx* ctx, cudaStream_t s, int64_t n, const int64_t* rowptr,
+                                      const int32_t* deg, PlanBufs b, int64_t* d_st, int64_t n_heavy,
+                                      int64_t n_slots) {
+    GRAPPA_TRY(b.heavy_rows->grow((size_t)(n > 0 ? n : 1) * 4));
+    GRAPPA_TRY(b.heavy_slot_off->grow((size_t)(n_heavy + 1) * 4));
+    GRAPPA_TRY(b.slot_row->grow((size_t)(n_slots > 0 ? n_slots : 1) * 4));
+    GRAPPA_TRY(b.slot_seg->grow((size_t)(n_slots > 0 ? n_slots : 1) * 4));
+    if (n_heavy > 0) {
+        GRAPPA_TRY(device_scan(ctx, FlagHeavy{deg}, n, WriteCompact{(int32_t*)b.heavy_rows->p, d_st, 0}, s));
+        GRAPPA_TRY(device_scan(ctx, NumSeg{deg, (int32_t*)b.heavy_rows->p}, n_heavy,
+                               WriteSlotOff{(int32_t*)b.heavy_slot_off->p, d_st, 1}, s));
+        k_slot_tasks<<<(unsigned)std::min<int64_t>(ceil_div(n_heavy, 256), 1024), 256, 0, s>>>(
+            n_heavy, (int32_t*)b.heavy_rows->p, (int32_t*)b.heavy_slot_off->p, (int32_t*)b.slot_row->p,
+            (int32_t*)b.slot_seg->p);
+        GRAPPA_LAUNCHED(ctx);
+    }
+    GRAPPA_TRY(b.row_order->grow((size_t)(n > 0 ? n : 1) * 4));
+    GRAPPA_TRY(ctx->red_ws.grow((size_t)2 * kDegBuckets * 8));   // (already >= N * 4 in the batch)
+    return plan_order(ctx, s, n, rowptr, deg, b);
 }
 
 extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g, const void* feats,
@@ -539,9 +633,11 @@ static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const voi
     int64_t* d_stat = (int64_t*)ctx->small.p;
     SeedStats* d_seedstats = (SeedStats*)(d_stat + 8);
     // rank table (int32 [N]) + halo flags (uint8 [N], halo-1 only)
-    RP_TRY(ctx->red_ws.grow((size_t)N * sizeof(int32_t) + (halo ? (size_t)N : 0)));
+    const int64_t n_words = ceil_div(N, 32);
+    RP_TRY(ctx->red_ws.grow((size_t)N * sizeof(int32_t) + (size_t)n_words * 4 + (halo ? (size_t)N : 0)));
     int32_t* rank = (int32_t*)ctx->red_ws.p;
-    uint8_t* hflag = (uint8_t*)(rank + N);
+    uint32_t* bitmap = (uint32_t*)(rank + N);          // core membership (the per-edge test)
+    uint8_t* hflag = (uint8_t*)(bitmap + n_words);
     // 1. rank table.  core_global capacity: N (freed/reused across super-epochs)
     RP_TRY(p->core_global.grow((size_t)N * sizeof(int32_t)));
     RP_TRY(device_scan(ctx, FlagCore{chunk_of, base, swept}, N,
@@ -607,19 +703,20 @@ static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const voi
     // on the device and the task kernels grid-stride up to it -- no host sync needed)
     const int64_t T_max = n_core + G_nnz / kTaskLen + 1;
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
-    const size_t off_b = al((size_t)(n_core + 1) * 4), row_b = al((size_t)T_max * 4),
+    const size_t off_b = al((size_t)(n_core + 1) * 4), row_b = al((size_t)T_max * 16),
                  cnt_b = al((size_t)T_max * 4), out_b = al((size_t)(T_max + 1) * 8);
     RP_TRY(ctx->rp_ws.grow(off_b + row_b + cnt_b + out_b));
     int32_t* task_off = (int32_t*)ctx->rp_ws.p;
-    int32_t* task_row = (int32_t*)((char*)ctx->rp_ws.p + off_b);
+    int4* task_desc = (int4*)((char*)ctx->rp_ws.p + off_b);
     int32_t* tcount = (int32_t*)((char*)ctx->rp_ws.p + off_b + row_b);
     int64_t* task_out = (int64_t*)((char*)ctx->rp_ws.p + off_b + row_b + cnt_b);
     const int32_t* core_global = (const int32_t*)p->core_global.p;
     RP_TRY(device_scan(ctx, NumTasks{srow, G_rowptr}, n_core,
-                       WriteTasks{task_off, task_row, d_stat}, s));
+                       WriteTasks{task_off, task_desc, d_stat, srow, G_rowptr}, s));
     const unsigned tgrid = (unsigned)ctx->sm_count * 16;
-    k_task_count<<<tgrid, 256, 0, s>>>(d_stat + 5, task_row, task_off, srow, G_rowptr, G_col,
-                                        rank, tcount);
+    k_core_bitmap<<<(unsigned)ctx->sm_count * 16, 256, 0, s>>>(N, chunk_of, base, swept, bitmap);
+    GRAPPA_LAUNCHED(ctx);
+    k_task_count<<<tgrid, 256, 0, s>>>(d_stat + 5, task_desc, G_col, bitmap, tcount);
     GRAPPA_LAUNCHED(ctx);
     // 3. scans: task outputs (= local col offsets, total = nnz), then per-row finalize
     RP_TRY(device_scan(ctx, ReadTcount{tcount, d_stat + 5}, T_max, WriteTaskOut{task_out, d_stat}, s));
@@ -650,8 +747,7 @@ static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const voi
                "grappa_repartition: partition (%d,%d) has no seeds (S:213)", base, swept);
     // 4. fill
     RP_TRY(p->col.grow((size_t)(nnz > 0 ? nnz : 1) * 4));
-    k_task_fill<<<tgrid, 256, 0, s>>>(d_stat + 5, task_row, task_off, task_out, srow, G_rowptr,
-                                       G_col, rank, (int32_t*)p->col.p);
+    k_task_fill<<<tgrid, 256, 0, s>>>(d_stat + 5, task_desc, task_out, G_col, bitmap, rank, (int32_t*)p->col.p);
     GRAPPA_LAUNCHED(ctx);
     // 5. features (core and halo rows)
     if (feats && !sa) {
@@ -661,7 +757,7 @@ static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const voi
         GRAPPA_LAUNCHED(ctx);
     }
     // 6. coverage statistics over the seeds (R3; in halo-1 mode every seed has d_l = d_g, R33)
-    int nb = (int)std::min<int64_t>(ceil_div(n_seeds, 4096), (int64_t)ctx->sm_count * 4);
+    int nb = seed_stat_blocks(ctx, n_seeds);
     if (nb < 1) nb = 1;
     RP_TRY(ctx->scan_ws.grow((size_t)nb * sizeof(SeedStats)));
     k_seed_stats<<<nb, kStatThreads, 0, s>>>(n_seeds, (int32_t*)p->seeds.p, (int32_t*)p->d_l.p,
@@ -794,6 +890,275 @@ extern "C" grappa_status grappa_repartition_shards(grappa_ctx* ctx, const grappa
     return repart_impl(ctx, &gn, A.feat_dim ? (const void*)A.x : nullptr, A.feat_dim, A.dtype, chunk_of,
                        num_chunks, A.chunk, B.chunk, A.train, A.labels, 0u, base, swept, inout,
                        (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------ batched switch
+namespace grappa {
+// split rows of a local CSR: count (d > kSegLen) and slots (sum ceil(d / kSegLen)), integers
+__global__ void k_heavy_count(int64_t n, const int32_t* __restrict__ d_l, unsigned long long* out) {
+    unsigned long long h = 0, sl = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t d = d_l[i];
+        if (d > kSegLen) {
+            h++;
+            sl += (unsigned long long)ceil_div(d, kSegLen);
+        }
+    }
+    h = warp_sum(h);
+    sl = warp_sum(sl);
+    if ((threadIdx.x & 31) == 0 && (h | sl)) {
+        atomicAdd(out, h);
+        atomicAdd(out + 1, sl);
+    }
+}
+__global__ void k_chunk_hist(int64_t n, const int32_t* __restrict__ chunk_of, int C, unsigned long long* cnt) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = chunk_of[v];
+        if (c >= 0 && c < C) atomicAdd(&cnt[c], 1ull);
+    }
+}
+struct WriteRankOnly {
+    int32_t* rank;
+    __device__ void operator()(int64_t v, int64_t p, int32_t f) const { rank[v] = f ? (int32_t)p : -1; }
+    __device__ void finish(int64_t, int64_t) const {}
+};
+}  // namespace grappa
+
+// The switch's partitions extracted with two host syncs in total instead of five per partition:
+// phase A (every partition): rank table, task split + kept counts, task offsets, per-row
+// finalize (rowptr, degrees, norms, node weights, labels), seeds, split-row counts -- sizes stay
+// on the device; one sync reads them all; phase B (every partition): rank table again (cheap:
+// 8 bytes per node), stable fill of the local columns, features, coverage statistics, SpMM plan
+// with the now-known split-row sizes; one final sync publishes the statistics.  Core sizes come
+// from the caller's chunk sizes (grappa_partition's output), checked against the device counts.
+extern "C" grappa_status grappa_repartition_batch(grappa_ctx* ctx, const grappa_csr* g, const void* feats,
+                                                  int32_t feat_dim, grappa_dtype dtype, const int32_t* chunk_of,
+                                                  int32_t num_chunks, const int64_t* chunk_sizes, int32_t n_parts,
+                                                  const int32_t* bases, const int32_t* swepts,
+                                                  const uint8_t* train_mask, const int32_t* labels,
+                                                  grappa_part** parts, void* stream) {
+    CallScope call_scope(ctx, stream);
+    GRAPPA_ARG(ctx && g && chunk_of && chunk_sizes && bases && swepts && train_mask && parts && n_parts >= 1,
+               GRAPPA_E_ARG, "grappa_repartition_batch: null argument");
+    GRAPPA_ARG(feats == nullptr || (feat_dim > 0 && feat_dim % 16 == 0), GRAPPA_E_SHAPE,
+               "grappa_repartition_batch: feat_dim must be a positive multiple of 16");
+    GRAPPA_ARG(g->num_nodes > 0 && g->num_nodes < (1ll << 31), GRAPPA_E_ARG,
+               "grappa_repartition_batch: num_nodes out of int32 range");
+    const int K = n_parts;
+    std::vector<int64_t> ncore(K);
+    for (int k = 0; k < K; k++) {
+        GRAPPA_ARG(bases[k] != swepts[k], GRAPPA_E_ARG, "grappa_repartition_batch: base == swept (S:139)");
+        GRAPPA_ARG(bases[k] >= 0 && swepts[k] >= 0 && bases[k] < num_chunks && swepts[k] < num_chunks, GRAPPA_E_ARG,
+                   "grappa_repartition_batch: chunk id out of range");
+        ncore[k] = chunk_sizes[bases[k]] + chunk_sizes[swepts[k]];
+        GRAPPA_ARG(ncore[k] > 0 && ncore[k] <= g->num_nodes, GRAPPA_E_ARG, "grappa_repartition_batch: bad chunk sizes");
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t N = g->num_nodes;
+    const int64_t esz = dtype == GRAPPA_BF16 ? 2 : 4;
+    // the counts must describe this chunk map (every allocation below is sized from them): known
+    // from grappa_partition, else counted once on the device (one sync) and remembered
+    const bool known = ctx->cmap_ptr == chunk_of && ctx->cmap_n == N && (int)ctx->cmap_sizes.size() == num_chunks;
+    if (!known) {
+        GRAPPA_TRY(ctx->small.grow((size_t)num_chunks * 8));
+        unsigned long long* d_cnt = (unsigned long long*)ctx->small.p;
+        GRAPPA_CUDA(cudaMemsetAsync(d_cnt, 0, (size_t)num_chunks * 8, s));
+        k_chunk_hist<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(N, 256), (int64_t)ctx->sm_count * 8)),
+                       256, 0, s>>>(N, chunk_of, num_chunks, d_cnt);
+        GRAPPA_LAUNCHED(ctx);
+        std::vector<int64_t> cnt(num_chunks);
+        GRAPPA_CUDA(cudaMemcpyAsync(cnt.data(), d_cnt, (size_t)num_chunks * 8, cudaMemcpyDeviceToHost, s));
+        GRAPPA_CUDA(cudaStreamSynchronize(s));
+        ctx->cmap_ptr = chunk_of;
+        ctx->cmap_n = N;
+        ctx->cmap_sizes = cnt;
+    }
+    for (int c = 0; c < num_chunks; c++)
+        GRAPPA_ARG(ctx->cmap_sizes[c] == chunk_sizes[c], GRAPPA_E_ARG,
+                   "grappa_repartition_batch: chunk_sizes[%d] = %lld but the chunk map holds %lld nodes", c,
+                   (long long)chunk_sizes[c], (long long)ctx->cmap_sizes[c]);
+    ProfScope ps(ctx, s, GRAPPA_K_REPART, 0.0, 0.0);
+    // new partition objects (destroyed again if the batch fails)
+    std::vector<grappa_part*> P(K);
+    std::vector<bool> fresh(K);
+    for (int k = 0; k < K; k++) {
+        fresh[k] = parts[k] == nullptr;
+        P[k] = parts[k] ? parts[k] : new grappa_part();
+    }
+    auto fail = [&](grappa_status st) {
+        for (int k = 0; k < K; k++)
+            if (fresh[k]) grappa_part_destroy(P[k]);
+        return st;
+    };
+#define RB_TRY(expr)                               \
+    do {                                           \
+        grappa_status _s = (expr);                 \
+        if (_s != GRAPPA_OK) return fail(_s);      \
+    } while (0)
+#define RB_CUDA(expr)                                                                   \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess) {                                                        \
+            set_error("grappa_repartition_batch: %s", cudaGetErrorString(_e));          \
+            return fail(GRAPPA_E_CUDA);                                                 \
+        }                                                                               \
+    } while (0)
+    // device stats per partition: [0] n_core [1] nnz [2] n_seeds [3] n_heavy [4] n_slots [5] T
+    // [6] unused [7] sum d_g ; then the partitions' SeedStats
+    constexpr int kSt = 16;
+    RB_TRY(ctx->small.grow((size_t)K * kSt * 8 + (size_t)K * sizeof(SeedStats)));
+    int64_t* d_stat0 = (int64_t*)ctx->small.p;
+    SeedStats* d_ss0 = (SeedStats*)(d_stat0 + (size_t)K * kSt);
+    RB_CUDA(cudaMemsetAsync(d_stat0, 0, (size_t)K * kSt * 8, s));
+    // rank table (int32 [N]) + core membership bitmap (1 bit per node, L1/L2-resident: the per-edge
+    // test of the counting pass and the first test of the fill; rank is read for kept edges only)
+    const int64_t n_words = ceil_div(N, 32);
+    RB_TRY(ctx->red_ws.grow((size_t)N * sizeof(int32_t) + (size_t)n_words * 4));
+    int32_t* rank = (int32_t*)ctx->red_ws.p;
+    uint32_t* bitmap = (uint32_t*)(rank + N);
+    const unsigned bm_grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_words * 32, 256),
+                                                                             (int64_t)ctx->sm_count * 16));
+    // task tables of every partition (phase B reads them): one workspace, K slices
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    std::vector<int64_t> Tmax(K);
+    std::vector<size_t> ws_off(K + 1, 0);
+    for (int k = 0; k < K; k++) {
+        Tmax[k] = ncore[k] + g->nnz / kTaskLen + 1;
+        ws_off[k + 1] = ws_off[k] + al((size_t)(ncore[k] + 1) * 4) + al((size_t)Tmax[k] * 16) +
+                        al((size_t)Tmax[k] * 4) + al((size_t)(Tmax[k] + 1) * 8);
+    }
+    RB_TRY(ctx->rp_ws.grow(ws_off[K]));
+    struct TW { int32_t* off; int4* desc; int32_t* cnt; int64_t* out; };
+    std::vector<TW> tw(K);
+    for (int k = 0; k < K; k++) {
+        char* w = (char*)ctx->rp_ws.p + ws_off[k];
+        tw[k].off = (int32_t*)w; w += al((size_t)(ncore[k] + 1) * 4);
+        tw[k].desc = (int4*)w; w += al((size_t)Tmax[k] * 16);
+        tw[k].cnt = (int32_t*)w; w += al((size_t)Tmax[k] * 4);
+        tw[k].out = (int64_t*)w;
+    }
+    const unsigned tgrid = (unsigned)ctx->sm_count * 16;
+    // ---------------------------------------------------------------- phase A
+    for (int k = 0; k < K; k++) {
+        grappa_part* p = P[k];
+        int64_t* d_stat = d_stat0 + (size_t)k * kSt;
+        const int64_t n = ncore[k];
+        RB_TRY(p->core_global.grow((size_t)n * 4));
+        RB_TRY(p->d_l.grow(n * 4));
+        RB_TRY(p->d_g.grow(n * 4));
+        RB_TRY(p->norm_gcn.grow(n * 4));
+        RB_TRY(p->norm_sage.grow(n * 4));
+        RB_TRY(p->node_w.grow(n * 12));
+        RB_TRY(p->labels.grow(n * 4));
+        RB_TRY(p->rowptr.grow((n + 1) * 8));
+        RB_TRY(p->seeds.grow(n * 4));
+        RB_TRY(p->heavy_rows.grow((size_t)n * 4));
+        const int32_t* cg = (const int32_t*)p->core_global.p;
+        RB_TRY(device_scan(ctx, FlagCore{chunk_of, bases[k], swepts[k]}, N,
+                           WriteRank{rank, (int32_t*)p->core_global.p, d_stat}, s));
+        unsigned grid;
+        rp_grid(ctx, n, 256, &grid);
+        k_core_bitmap<<<bm_grid, 256, 0, s>>>(N, chunk_of, bases[k], swepts[k], bitmap);
+        GRAPPA_LAUNCHED(ctx);
+        RB_TRY(device_scan(ctx, NumTasks{cg, g->rowptr}, n, WriteTasks{tw[k].off, tw[k].desc, d_stat, cg, g->rowptr}, s));
+        k_task_count<<<tgrid, 256, 0, s>>>(d_stat + 5, tw[k].desc, g->col, bitmap, tw[k].cnt);
+        GRAPPA_LAUNCHED(ctx);
+        RB_TRY(device_scan(ctx, ReadTcount{tw[k].cnt, d_stat + 5}, Tmax[k], WriteTaskOut{tw[k].out, d_stat}, s));
+        k_row_finalize<<<grid, 256, 0, s>>>(n, tw[k].off, tw[k].out, cg, g->rowptr, labels, (int64_t*)p->rowptr.p,
+                                             (int32_t*)p->d_l.p, (int32_t*)p->d_g.p, (float*)p->norm_gcn.p,
+                                             (float*)p->norm_sage.p, (float*)p->node_w.p, n, (int32_t*)p->labels.p,
+                                             (unsigned long long*)(d_stat + 7));
+        GRAPPA_LAUNCHED(ctx);
+        RB_TRY(device_scan(ctx, FlagSeed{cg, train_mask}, n, WriteCompact{(int32_t*)p->seeds.p, d_stat, 2}, s));
+        k_heavy_count<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 4)),
+                        256, 0, s>>>(n, (const int32_t*)p->d_l.p, (unsigned long long*)(d_stat + 3));
+        GRAPPA_LAUNCHED(ctx);
+    }
+    std::vector<int64_t> st((size_t)K * kSt);
+    RB_CUDA(cudaMemcpyAsync(st.data(), d_stat0, (size_t)K * kSt * 8, cudaMemcpyDeviceToHost, s));
+    RB_CUDA(cudaStreamSynchronize(s));
+    for (int k = 0; k < K; k++) {
+        const int64_t* h = &st[(size_t)k * kSt];
+        if (h[0] != ncore[k]) {
+            set_error("grappa_repartition_batch: chunk_sizes disagree with chunk_of (%lld vs %lld core nodes)",
+                      (long long)ncore[k], (long long)h[0]);
+            return fail(GRAPPA_E_ARG);
+        }
+        if (h[2] == 0) {
+            set_error("grappa_repartition_batch: partition (%d,%d) has no seeds (S:213)", bases[k], swepts[k]);
+            return fail(GRAPPA_E_EMPTY);
+        }
+    }
+    // ---------------------------------------------------------------- phase B
+    double bytes = 0.0;
+    for (int k = 0; k < K; k++) {
+        grappa_part* p = P[k];
+        const int64_t* h = &st[(size_t)k * kSt];
+        const int64_t n = ncore[k], nnz = h[1], n_seeds = h[2], n_heavy = h[3], n_slots = h[4];
+        const int32_t* cg = (const int32_t*)p->core_global.p;
+        RB_TRY(device_scan(ctx, FlagCore{chunk_of, bases[k], swepts[k]}, N, WriteRankOnly{rank}, s));
+        RB_TRY(p->col.grow((size_t)(nnz > 0 ? nnz : 1) * 4));
+        k_core_bitmap<<<bm_grid, 256, 0, s>>>(N, chunk_of, bases[k], swepts[k], bitmap);
+        GRAPPA_LAUNCHED(ctx);
+        k_task_fill<<<tgrid, 256, 0, s>>>(d_stat0 + (size_t)k * kSt + 5, tw[k].desc, tw[k].out, g->col, bitmap, rank,
+                                           (int32_t*)p->col.p);
+        GRAPPA_LAUNCHED(ctx);
+        unsigned grid;
+        rp_grid(ctx, n, 256, &grid);
+        if (feats) {
+            RB_TRY(p->x.grow((size_t)n * feat_dim * esz));
+            k_gather_rows<<<grid, 256, 0, s>>>(n, feat_dim * esz, cg, (const uint4*)feats, (uint4*)p->x.p);
+            GRAPPA_LAUNCHED(ctx);
+        }
+        int nb = seed_stat_blocks(ctx, n_seeds);
+        if (nb < 1) nb = 1;
+        RB_TRY(ctx->scan_ws.grow((size_t)nb * sizeof(SeedStats)));
+        k_seed_stats<<<nb, kStatThreads, 0, s>>>(n_seeds, (int32_t*)p->seeds.p, (int32_t*)p->d_l.p,
+                                                  (int32_t*)p->d_g.p, (SeedStats*)ctx->scan_ws.p);
+        GRAPPA_LAUNCHED(ctx);
+        k_seed_stats_final<<<1, 32, 0, s>>>(nb, (SeedStats*)ctx->scan_ws.p, d_ss0 + k);
+        GRAPPA_LAUNCHED(ctx);
+        // SpMM plan with the known split-row sizes (no sync)
+        RB_TRY(build_plan_sized(ctx, s, n, (int64_t*)p->rowptr.p, (int32_t*)p->d_l.p,
+                                PlanBufs{&p->heavy_rows, &p->heavy_slot_off, &p->slot_row, &p->slot_seg,
+                                         &p->row_order, &p->row_desc},
+                                d_stat0 + (size_t)k * kSt + 8, n_heavy, n_slots));
+        p->halo = false;
+        p->n_halo = 0;
+        p->t_n_heavy = p->t_n_slots = 0;
+        p->t_eid_ready = false;
+        p->tma.ready = p->t_tma.ready = false;
+        grappa_part_info& I = p->info;
+        I = grappa_part_info{};
+        I.n_core = n; I.nnz = nnz; I.n_seeds = n_seeds; I.base = bases[k]; I.swept = swepts[k];
+        I.n_halo = 0;
+        I.feat_dim = feats ? feat_dim : 0; I.dtype = dtype;
+        I.rowptr = (int64_t*)p->rowptr.p; I.col = (int32_t*)p->col.p;
+        I.core_global = (int32_t*)p->core_global.p; I.d_l = (int32_t*)p->d_l.p; I.d_g = (int32_t*)p->d_g.p;
+        I.norm_gcn = (float*)p->norm_gcn.p; I.norm_sage = (float*)p->norm_sage.p;
+        I.node_w = (float*)p->node_w.p;
+        I.seeds = (int32_t*)p->seeds.p; I.labels = (int32_t*)p->labels.p; I.x = p->x.p;
+        I.n_heavy = n_heavy; I.n_slots = n_slots;
+        // algorithmic bytes (SURVEY §8(d) d.3 per core row): rowptr 8 + the d_g source columns + the
+        // d_l kept columns + outputs 24 + the feature row read and written
+        bytes += (double)n * (8.0 + 24.0 + 2.0 * (feats ? feat_dim * esz : 0)) + 4.0 * (double)h[7] + 4.0 * (double)nnz;
+    }
+    std::vector<SeedStats> hs(K);
+    RB_CUDA(cudaMemcpyAsync(hs.data(), d_ss0, (size_t)K * sizeof(SeedStats), cudaMemcpyDeviceToHost, s));
+    RB_CUDA(cudaStreamSynchronize(s));
+    for (int k = 0; k < K; k++) {
+        grappa_part_info& I = P[k]->info;
+        I.c_uniform = hs[k].sum_r / (double)I.n_seeds;
+        I.D = hs[k].D;
+        const double D = (double)hs[k].D;
+        I.c_resampling = D < 1e-9 ? 1.0 : std::min(1.0 / D, 10.0);
+        I.c_resampling_hm = hs[k].sum_dl > 0 ? (double)hs[k].sum_dl / (double)hs[k].sum_dg : 1.0;
+        parts[k] = P[k];
+    }
+    ps.set_bytes(bytes);
+    return GRAPPA_OK;
+#undef RB_TRY
+#undef RB_CUDA
 }
 
 static grappa_status part_copy(const grappa_part* p, const grappa_part_host* h, bool to_host, cudaStream_t s) {

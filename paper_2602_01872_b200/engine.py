@@ -23,7 +23,7 @@ import torch
 
 from . import (BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, F32, LAYER_INPUT, LAYER_NODE_LEVEL, Context, Part,
                Shard, grappa_aggregate_grads, grappa_layer_bwd, grappa_layer_bwd_ex, grappa_layer_fwd_ex,
-               grappa_loss, grappa_partition, grappa_repartition, grappa_repartition_shards,
+               grappa_loss, grappa_partition, grappa_repartition, grappa_repartition_batch, grappa_repartition_shards,
                grappa_shard_exchange, grappa_shard_extract, layer_saved_bytes, layer_ws_bytes)
 
 
@@ -229,13 +229,20 @@ class Trainer:
             return self._repartition_to_host(t, pairs)
         if self.sharded:
             return self._repartition_sharded(t, pairs)
-        for _, w in self.my_workers():
-            if w >= self.W:
-                continue
-            b, s = pairs[w]
-            self.parts[w] = grappa_repartition(self.ctx, self.rowptr, self.col, self.x, self.dt,
-                                               self.chunk_of, self.C, b, s, self.train, self.labels,
-                                               self.parts.get(w), self.stream, halo=self.halo)
+        mine = [w for _, w in self.my_workers() if w < self.W]
+        if self.halo:
+            for w in mine:
+                b, s = pairs[w]
+                self.parts[w] = grappa_repartition(self.ctx, self.rowptr, self.col, self.x, self.dt,
+                                                   self.chunk_of, self.C, b, s, self.train, self.labels,
+                                                   self.parts.get(w), self.stream, halo=True)
+        elif mine:
+            # every partition of this rank in one call: two host syncs per switch
+            got = grappa_repartition_batch(self.ctx, self.rowptr, self.col, self.x, self.dt, self.chunk_of, self.C,
+                                           [pairs[w] for w in mine], self.train, self.labels,
+                                           [self.parts.get(w) for w in mine], self.stream,
+                                           chunk_sizes=self.chunk_sizes)
+            self.parts.update(zip(mine, got))
         self.t = t
         self._alloc()
 

@@ -521,3 +521,43 @@ def test_spmm_tma_bitwise_equals_row_group(G, ctx, prod, width, mode):
     assert torch.equal(a_h, b_h)
     assert torch.equal(a_dz, b_dz)
     assert torch.equal(a_dw, b_dw)
+
+
+@pytest.mark.parametrize("C,dtype", [(8, "bf16"), (4, "f32"), (2, "bf16"), (80, "bf16")])
+def test_repartition_batch_bitexact(G, ctx, prod, C, dtype):
+    """grappa_repartition_batch (all partitions of a switch, two host syncs) builds every partition
+    bit for bit as grappa_repartition and the oracle do -- CSR, maps, degrees, norms, node weights,
+    seeds, labels, gathered features, split-row plan sizes, coverage statistics -- reusing the
+    previous switch's partition objects; chunk sizes that disagree with the map are rejected."""
+    rp, col, x, y, tr = upload(prod)
+    seed = gen.seed_of("chunks")
+    ch = torch.empty(prod.wl.n, dtype=torch.int32, device="cuda")
+    sizes = G.grappa_partition(ctx, prod.wl.n, C, seed, ch)
+    chunk_of = Po.make_chunks(prod.wl.n, C, seed)
+    xt = x.to(torch.bfloat16) if dtype == "bf16" else x
+    sched = Po.sweep_schedule(C, C)
+    parts = None
+    for t in range(min(2, len(sched))):
+        pairs = sched[t][:8]
+        parts = G.grappa_repartition_batch(ctx, rp, col, xt, dtype, ch, C, pairs, tr, y, parts, chunk_sizes=sizes)
+        for (b, s), p in zip(pairs, parts):
+            one = G.grappa_repartition(ctx, rp, col, xt, dtype, ch, C, b, s, tr, y)
+            ref = Po.induced_partition(prod.rowptr, prod.col, chunk_of, b, s, prod.train)
+            assert np.array_equal(p.rowptr.cpu().numpy(), ref["rowptr"])
+            assert np.array_equal(p.col.cpu().numpy(), ref["col"])
+            assert np.array_equal(p.seeds.cpu().numpy(), ref["seeds"])
+            for name in ("rowptr", "col", "core_global", "d_l", "d_g", "norm_gcn", "norm_sage", "seeds", "labels",
+                         "node_w"):
+                assert torch.equal(getattr(p, name), getattr(one, name)), name
+            assert torch.equal(p.x.view(torch.int16) if dtype == "bf16" else p.x,
+                               one.x.view(torch.int16) if dtype == "bf16" else one.x)
+            for f in ("n_core", "nnz", "n_seeds", "n_heavy", "n_slots", "D", "c_uniform", "c_resampling",
+                      "c_resampling_hm"):
+                assert getattr(p.info, f) == getattr(one.info, f), f
+    bad = list(sizes)
+    bad[sched[0][0][0]] += 1
+    with pytest.raises(G.GrappaError, match="E_ARG"):
+        G.grappa_repartition_batch(ctx, rp, col, xt, dtype, ch, C, sched[0][:8], tr, y, chunk_sizes=bad)
+    with pytest.raises(G.GrappaError, match="E_EMPTY"):
+        G.grappa_repartition_batch(ctx, rp, col, xt, dtype, ch, C, sched[0][:8], torch.zeros_like(tr), y,
+                                   chunk_sizes=sizes)
