@@ -138,9 +138,13 @@ def ncu_traffic(kclass: str):
     return (rec, d.get("window")) if rec else None
 
 
-def build_dataset(name: str):
+def build_dataset(name: str, rank: int = 0, world: int = 1, barrier=None):
+    """the workload's synthetic inputs; with several ranks on the node, rank 0 generates them
+    once and the others map its copy (gen.shared_dataset)"""
     import gen
     wl = gen.WORKLOADS[name]
+    if world > 1 and barrier is not None:
+        return wl, gen.shared_dataset(wl, rank, barrier)
     return wl, gen.make_dataset(wl)
 
 
@@ -313,9 +317,6 @@ def run_grappa(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 and "OMP_NUM_THREADS" not in os.environ:   # ranks generate inputs concurrently
-        os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 8) // int(
-            os.environ.get("LOCAL_WORLD_SIZE", world))))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -331,7 +332,7 @@ def run_grappa(args):
         ctx.set_variant(op, int(val))
 
     t_gen = time.perf_counter()
-    wl, ds = build_dataset(args.config)
+    wl, ds = build_dataset(args.config, rank, world, (lambda: dist.barrier()) if world > 1 else None)
     t_gen = time.perf_counter() - t_gen
     spec = ModelSpec(wl.arch, wl.dims, wl.dims_pad)
     stream = torch.cuda.current_stream(dev)
@@ -368,7 +369,9 @@ def run_grappa(args):
     # full-graph runs (~535 launches per products epoch; replay removes the host launch gaps);
     # multi-GPU runs replay only with --graph (the all-reduce would be captured too)
     # (GAT builds its transposed edge ids lazily in the first backward: eager unless --graph)
-    use_graph = ((args.graph or (world == 1 and not args.eager and spec.arch != "gat"))
+    # (multi-rank runs capture record-only: the NCCL all-reduce is a graph node, replayed in the
+    # same order on every rank)
+    use_graph = ((args.graph or (not args.eager and spec.arch != "gat"))
                  and not isinstance(tr, MinibatchTrainer) and not args.capacity)
     if use_graph:
         # the super-epoch's repartition + its first epoch (run eagerly while it is captured)
@@ -380,6 +383,7 @@ def run_grappa(args):
     # calls would add host work to host-bound loops); one extra profiled epoch follows
     ctx.profile(False)
     l0 = ctx.launches()
+    cb0 = ctx.comm_bytes()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     evs[0].record(stream)
     for k in range(args.steps):
@@ -393,8 +397,11 @@ def run_grappa(args):
     ms = evs[0].elapsed_time(evs[-1])
     per_epoch = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
     launches = ctx.launches() - l0
+    cb1 = ctx.comm_bytes()
     if use_graph:
         launches += tr.graph_launches * args.steps
+        # replayed all-reduces are not seen by the host counters: count the captured ones
+        cb1 = (cb1[0] + tr.graph_grad_bytes * args.steps, cb1[1])
     ctx.profile(True)                  # per-kernel times from one extra eager epoch
     tr.run_epoch()
     # the switch inside the timed region ran outside any profile window: time one more
@@ -484,6 +491,15 @@ def run_grappa(args):
     if not args.no_e2e and not isinstance(tr, MinibatchTrainer) and not args.capacity:
         e2e = measure_e2e(tr, stream, K, barrier, world, dist, nnz, use_graph)
 
+    # §8(e): the only per-iteration cross-GPU traffic is the gradient all-reduce;
+    # shard / halo exchanges happen at switches only.  At N > 1 also the all-reduce bus bandwidth
+    # through the product call (scale kernel + ncclAllReduce) at this model's gradient size.
+    comm = {"grad_bytes_per_step": (cb1[0] - cb0[0]) / K, "other_bytes_per_step": (cb1[1] - cb0[1]) / K,
+            "switches_timed": -(-K // wl.repartition_every),
+            "note": "bytes this rank sent per epoch; other = shard exchanges at super-epoch switches"}
+    if world > 1:
+        comm["allreduce"] = measure_allreduce(ctx, stream, tr.grad.numel(), world, dist, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_baseline(args.config, corr=args.corr, halo=args.halo)
@@ -511,7 +527,7 @@ def run_grappa(args):
                 "roofline": roofline, "kernels": kernels, "f32": f32,
                 "kernels_window": "1 eager epoch after the timed region",
                 "cpu_baseline": cpu,
-                "e2e": e2e, "gpu_launches": launches, "clocks": clk}
+                "e2e": e2e, "comm": comm, "gpu_launches": launches, "clocks": clk}
         s = json.dumps(line)
         print(s, flush=True)
         if args.out:
@@ -519,6 +535,34 @@ def run_grappa(args):
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_allreduce(ctx, stream, n_params, world, dist, dev, reps=50):
+    """algbw / busbw of the gradient all-reduce through grappa_aggregate_grads_c (lr = 0), at this
+    model's gradient size and at 64 MiB, CUDA events, max over ranks"""
+    import torch
+
+    import paper_2602_01872_b200 as G
+    out = {}
+    for n in (int(n_params), 16 << 20):
+        g = torch.ones(n, dtype=torch.float32, device=dev)
+        for _ in range(5):
+            G.grappa_aggregate_grads_c(ctx, 1.0, g, world, 0.0, None, stream)
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            G.grappa_aggregate_grads_c(ctx, 1.0, g, world, 0.0, None, stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        t = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        us = float(t.item()) * 1e3
+        alg = n * 4 / (us * 1e-6) / 1e9
+        out[f"{n * 4}B"] = {"us": us, "algbw_GBps": alg, "busbw_GBps": alg * 2 * (world - 1) / world,
+                            "peak_GBps": 900.0}
+    return out
 
 
 def measure_f32(args, ctx, ds, wl, spec, stream, barrier, world, dist, nnz, use_graph):

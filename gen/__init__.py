@@ -286,6 +286,35 @@ def make_dataset(wl: Workload, with_features: bool = True) -> Dataset:
     return Dataset(wl, rowptr, col, x, y, train, weights)
 
 
+def shared_dataset(wl: Workload, rank: int, barrier, root: str = "/dev/shm") -> Dataset:
+    """One copy of a dataset for all ranks of a node: rank 0 generates it and writes the arrays to
+    `root` (page cache, shared), the others wait at `barrier()` and map them read-only.  Avoids N
+    concurrent generations and N private host copies (8 x 57 GB of fp32 features at papers
+    scale).  Falls back to a private generation when `root` is not writable."""
+    import hashlib
+    key = hashlib.sha1(repr(sorted(wl.__dict__.items())).encode()).hexdigest()[:12]
+    base = os.path.join(root, f"grappa_{wl.name}_{key}")
+    names = ("rowptr", "col", "x", "y", "train")
+    ok = os.path.isdir(root) and os.access(root, os.W_OK)
+    if rank == 0:
+        ds = make_dataset(wl)
+        if ok:
+            try:
+                for n in names:
+                    np.save(f"{base}_{n}.tmp.npy", getattr(ds, n))
+                    os.replace(f"{base}_{n}.tmp.npy", f"{base}_{n}.npy")
+            except OSError:
+                ok = False
+        barrier()
+        return ds
+    barrier()
+    if ok and all(os.path.exists(f"{base}_{n}.npy") for n in names):
+        arr = {n: np.load(f"{base}_{n}.npy", mmap_mode="r") for n in names}
+        return Dataset(wl, arr["rowptr"], arr["col"], arr["x"], arr["y"], arr["train"],
+                       init_weights(wl, seed_of("init", wl.root)))
+    return make_dataset(wl)
+
+
 def init_weights(wl: Workload, seed: int) -> list:
     dims, dp = wl.dims, wl.dims_pad
     out = []

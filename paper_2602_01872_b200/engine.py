@@ -480,10 +480,13 @@ class Trainer:
         main = self.stream
         cap = torch.cuda.Stream(self.dev)
         cap.wait_stream(main)
-        n_cap, cap_steps = 0, []
+        n_cap, cap_steps, grad_b = 0, [], 0
         # small partitions (host-bound epochs): record only, then replay -- running the epoch
         # eagerly as well would double the host work that bounds them
-        eager = sum(p.nnz for p in self.parts.values()) >= getattr(self, "graph_eager_min_nnz", 4_000_000)
+        # multi-rank: record only (each communicator then sees one stream of collectives: the
+        # captured all-reduces replay in the same order on every rank)
+        eager = (self.G == 1 and
+                 sum(p.nnz for p in self.parts.values()) >= getattr(self, "graph_eager_min_nnz", 4_000_000))
         # capture_begin/end directly: torch.cuda.graph() would also run gc.collect() and
         # empty_cache(); relaxed mode lets the eager launches proceed during the capture
         with torch.cuda.stream(cap):
@@ -499,9 +502,11 @@ class Trainer:
                                 self.phase_probe(i, w)
                     saved, self._steps = self._steps, []
                     l0 = self.ctx.launches()
+                    b0 = self.ctx.comm_bytes()[0]
                     self.stream = cap
                     self.phase_step(i, w, m_active)               # recorded for the replays
                     n_cap += self.ctx.launches() - l0
+                    grad_b += self.ctx.comm_bytes()[0] - b0
                     if self.phase_probe is not None:              # its copies are captured too
                         self.phase_probe(i, w)
                     cap_steps += self._steps
@@ -517,6 +522,7 @@ class Trainer:
                   f"{1e3 * (h2 - h1):.1f} ms, capture_end {1e3 * (h3 - h2):.1f} ms", file=sys.stderr)
         self.graph = g
         self.graph_launches = n_cap
+        self.graph_grad_bytes = grad_b       # all-reduce payload bytes per replay (comm counters)
         self.graph_steps = cap_steps
         if not eager:
             g.replay()

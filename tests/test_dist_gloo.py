@@ -242,3 +242,30 @@ def test_two_rank_shard_exchange(C):
         p.join(timeout=300)
         assert p.exitcode == 0
     assert res == {0: True, 1: True}
+
+
+def _shared_worker(rank, world, port, root, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    wl = gen.small_workload("products", n=3001, scale=12, num_samples=30_000, depth=2, chunks=4, hidden=16)
+    ds = gen.shared_dataset(wl, rank, lambda: dist.barrier(), root=root)
+    d = {k: np.array(getattr(ds, k)) for k in ("rowptr", "col", "x", "y", "train")}
+    d["w"] = np.concatenate([np.asarray(w).ravel() for ws in ds.weights for w in ws])
+    out[rank] = d
+    dist.destroy_process_group()
+
+
+def test_shared_dataset_two_ranks(tmp_path):
+    """bench at N > 1: rank 0 generates the inputs once and the other ranks map its copy
+    (gen.shared_dataset) -- every rank sees exactly the generator's arrays"""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_shared_worker, args=(world, _port(), str(tmp_path), out), nprocs=world, join=True)
+    wl = gen.small_workload("products", n=3001, scale=12, num_samples=30_000, depth=2, chunks=4, hidden=16)
+    ref = gen.make_dataset(wl)
+    for r in range(world):
+        for k in ("rowptr", "col", "x", "y", "train"):
+            assert np.array_equal(out[r][k], getattr(ref, k)), (r, k)
+        assert np.array_equal(out[r]["w"], np.concatenate([np.asarray(w).ravel() for ws in ref.weights for w in ws]))
+    assert any(p.name.endswith("_col.npy") for p in tmp_path.iterdir())
