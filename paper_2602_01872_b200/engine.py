@@ -40,13 +40,14 @@ def sweep_schedule(C: int, W: int):
 
 
 def merge_step_factors(per_rank) -> list:
-    """per_rank[r] = [(c, active), ...] for the same lock-step sequence of optimizer steps;
-    returns per step the mean c over the ranks that were active (steps with none are dropped)"""
+    """per_rank[r] = [(partition, coverage, active), ...] for the same lock-step sequence of
+    optimizer steps; returns the (partition, coverage) observations in step order, ranks in
+    ascending order within a step (idle ranks dropped) -- the controller's input (R32)"""
     out = []
     for k in range(len(per_rank[0]) if per_rank else 0):
-        cs = [r[k][0] for r in per_rank if r[k][1] > 0]
-        if cs:
-            out.append(sum(cs) / len(cs))
+        for r in per_rank:
+            if r[k][2] > 0:
+                out.append((int(r[k][0]), float(r[k][1])))
     return out
 
 
@@ -378,7 +379,8 @@ class Trainer:
         grappa_aggregate_grads(self.ctx, part, self.corr, self.grad, m_active,
                                self.lr if lr is None else lr, self.theta, self.stream, eps=self.eps,
                                c_max=self.c_max, comm_dtype=self.comm_dtype)
-        self._steps.append((part.factor(self.corr), 1.0) if part is not None else (0.0, 0.0))
+        self._steps.append((float(worker), part.info.c_uniform, 1.0) if part is not None
+                           else (0.0, 0.0, 0.0))
 
     # ------------------------------------------------------------------ super-epochs
     def super_epoch(self) -> int:
@@ -386,23 +388,23 @@ class Trainer:
         return self.t_ctrl if self.controller is not None else 1 + self.epoch // self.rep_every
 
     def end_epoch(self):
-        """epoch boundary: feed the controller this epoch's per-step coverage factors (mean over
-        the active ranks of each step, identical on every rank) and advance the super-epoch if it
-        says so (§3.5, R32)"""
+        """epoch boundary: feed the controller this epoch's per-step (partition, coverage)
+        records of every active rank (gathered, so identical on every rank) and advance the
+        super-epoch if it says so (§3.5, R32)"""
         self.epoch += 1
         steps, self._steps = self._steps, []
         if self.controller is None:
             return
         if self.G > 1:
             import torch.distributed as dist
-            mine = torch.tensor(steps, dtype=torch.float64, device=self.dev).reshape(-1, 2)
+            mine = torch.tensor(steps, dtype=torch.float64, device=self.dev).reshape(-1, 3)
             every = [torch.empty_like(mine) for _ in range(self.G)]
             dist.all_gather(every, mine)
             seq = merge_step_factors([e.cpu().tolist() for e in every])
         else:
             seq = merge_step_factors([steps])
-        for c in seq:
-            self.controller.observe(c)
+        for p, c in seq:
+            self.controller.observe(p, c)
         if self.controller.end_epoch():
             self.t_ctrl += 1
 
@@ -642,12 +644,13 @@ class MinibatchTrainer(Trainer):
                     done[slot] = torch.cuda.Event()
                     done[slot].record(self.stream)
                     c = bt.factors[self.corr]
+                    cov = bt.factors["uniform"]          # the controller's coverage (R32)
                 else:
                     self.grad.zero_()
                     c = 0.0
                 grappa_aggregate_grads_c(self.ctx, c, self.grad, m_active, self.lr, self.theta,
                                          self.stream, comm_dtype=self.comm_dtype)
-                self._steps.append((c, 1.0) if part is not None else (0.0, 0.0))
+                self._steps.append((float(w), cov, 1.0) if part is not None else (0.0, 0.0, 0.0))
                 if on_phase is not None:
                     on_phase()
         self.end_epoch()

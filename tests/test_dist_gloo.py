@@ -100,9 +100,9 @@ def test_phase_plan():
 
 
 def _ctrl_worker(rank, world, port, out):
-    """each rank sees different coverage factors (its own partitions); after gathering the
-    per-step (c, active) lists once per epoch (Trainer.end_epoch) every rank must take the same
-    switch decisions, equal to the oracle controller fed the per-step mean over active ranks"""
+    """each rank sees different coverages (its own partitions); after gathering the per-step
+    (partition, coverage, active) lists once per epoch (Trainer.end_epoch) every rank must take
+    the same switch decisions, equal to the oracle controller fed every active partition's step"""
     from paper_2602_01872_b200.controller import Controller
     from paper_2602_01872_b200.engine import merge_step_factors
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -113,13 +113,14 @@ def _ctrl_worker(rank, world, port, out):
     for epoch in range(25):
         steps = []
         for i, w, m in phase_plan(3, world, rank):     # W = 3: rank 1 idle in phase 1
-            steps.append((float(rng.uniform(0.0, 1.0)), 1.0) if w is not None else (0.0, 0.0))
-        mine = torch.tensor(steps, dtype=torch.float64).reshape(-1, 2)
+            steps.append((float(w), float(rng.uniform(0.0, 0.35)), 1.0) if w is not None
+                         else (0.0, 0.0, 0.0))
+        mine = torch.tensor(steps, dtype=torch.float64).reshape(-1, 3)
         every = [torch.empty_like(mine) for _ in range(world)]
         dist.all_gather(every, mine)
         lists = [e.tolist() for e in every]
-        for c in merge_step_factors(lists):
-            ctrl.observe(c)
+        for p, c in merge_step_factors(lists):
+            ctrl.observe(p, c)
         decisions.append(ctrl.end_epoch())
         out.put((rank, epoch, lists))
     out.put((rank, "decisions", decisions))
@@ -151,8 +152,9 @@ def test_two_rank_controller_agrees():
     for epoch in range(25):
         per_rank = lists[epoch]
         for k in range(len(per_rank[0])):
-            cs = [r[k][0] for r in per_rank if r[k][1] > 0]
-            oc.observe(sum(cs) / len(cs))
+            for r in per_rank:
+                if r[k][2] > 0:
+                    oc.observe(int(r[k][0]), r[k][1])
         ref.append(oc.end_epoch())
     assert got[0] == ref and any(ref)
 
