@@ -446,11 +446,11 @@ def run_grappa(args):
         for k in ("lts_bytes_per_call", "issue_active_pct"):
             if k in rec:
                 traffic_src[k] = rec[k]
-    rep_ms = prof["repart"][0]
-    if prof["repart"][1]:
-        # per switch = the profiled extractions / switches they make up, times the switches timed
-        n_parts = sum(1 for _, w in tr.my_workers() if w < tr.W)
-        rep_ms = prof["repart"][0] / (prof["repart"][1] / n_parts) * (-(-K // wl.repartition_every))
+    # the profile window holds exactly one switch (the extra tr.repartition call above; the extra
+    # epoch stays in its super-epoch), whatever number of library calls it is made of (one batched
+    # call for replicated induced-core partitions, one per partition otherwise)
+    rep_ms_switch = prof["repart"][0]
+    rep_ms = rep_ms_switch * (-(-K // wl.repartition_every))
     roofline = {"bound": "l2", "achieved": achieved, "peak": l2_peak, "unit": "GB/s",
                 "frac": (achieved / l2_peak) if achieved else None,
                 "traffic": traffic, "traffic_source": traffic_src,
@@ -513,6 +513,7 @@ def run_grappa(args):
                            "nnz_global": nnz, "partitions": wl.chunks, "phases_per_epoch": -(-wl.chunks // world),
                            "repartitions_timed": -(-K // wl.repartition_every),
                            "repartition_ms_total": rep_ms,
+                           "repartition_ms_per_switch": rep_ms_switch,
                            "epoch_ms_excl_repartition": (ms - rep_ms) / K,
                            "epoch_ms": {"median": statistics.median(per_epoch), "min": min(per_epoch),
                                         "max": max(per_epoch), "note": "rank-local CUDA events; the "

@@ -202,6 +202,28 @@ grappa_status grappa_repartition_batch(grappa_ctx* ctx, const grappa_csr* g, con
                                        const int64_t* chunk_sizes, int32_t n_parts, const int32_t* bases,
                                        const int32_t* swepts, const uint8_t* train_mask, const int32_t* labels,
                                        grappa_part** parts, void* stream);
+/* Switch index of a (global CSR, chunk map) pair, built once per run (the chunk map is fixed for
+ * the whole run, "performed only once") and passed to grappa_repartition_batch_ix:
+ *   per-edge chunk bytes ec[e] = chunk_of[col[e]]  (device uint8 [nnz], library-owned) -- the
+ *       switch's "is this neighbour in {base, swept}" test becomes a coalesced byte stream;
+ *   per-chunk node counts and sums of the nodes' global degrees (host; bound the task tables).
+ * grappa_index_create: one kernel pass over the edges and one host sync.  The index refers to
+ * g->rowptr, g->col and chunk_of by address: the caller keeps them alive and unchanged while the
+ * index is used (grappa_repartition_batch_ix checks the addresses and sizes, not the contents).
+ * Errors: E_ARG (C outside [2, 255], N outside int32, null), E_NOMEM, E_CUDA.
+ * grappa_index_query copies the per-chunk counts / degree sums into host int64[C] (either NULL). */
+typedef struct grappa_index grappa_index;
+grappa_status grappa_index_create(grappa_ctx* ctx, const grappa_csr* g, const int32_t* chunk_of,
+                                  int32_t num_chunks, grappa_index** out, void* stream);
+grappa_status grappa_index_query(const grappa_index* ix, int64_t* chunk_sizes, int64_t* chunk_degrees);
+void grappa_index_destroy(grappa_index* ix);
+/* grappa_repartition_batch with a prebuilt index (chunk map and C taken from it): the same
+ * partitions, bitwise.  grappa_repartition_batch itself builds a temporary index per call. */
+grappa_status grappa_repartition_batch_ix(grappa_ctx* ctx, const grappa_csr* g, const void* feats,
+                                          int32_t feat_dim, grappa_dtype dtype, const grappa_index* ix,
+                                          const int64_t* chunk_sizes, int32_t n_parts, const int32_t* bases,
+                                          const int32_t* swepts, const uint8_t* train_mask,
+                                          const int32_t* labels, grappa_part** parts, void* stream);
 grappa_status grappa_part_query(const grappa_part* part, grappa_part_info* out);
 void grappa_part_destroy(grappa_part* part);
 
@@ -469,8 +491,8 @@ grappa_status grappa_epoch_seeds(grappa_ctx* ctx, const grappa_part* part, uint6
  * Floyd's algorithm over neighbour positions keyed by h(h(seed, epoch, batch_index, h), gid v, j)
  * (reading R24); hop 1 uses the LAST fanout (R25); sources = targets then new nodes in ascending
  * local id (R26).  batch: dev int32[n_batch] local seed ids; fanouts: host int32[n_layers]
- * (input -> output, each <= 16).  *inout NULL -> created, else reused.  Syncs once.
- * Errors: E_ARG (n_layers < 1, fanout < 1, n_batch < 1). */
+ * (input -> output, each <= 32).  *inout NULL -> created, else reused.  Syncs once.
+ * Errors: E_ARG (n_layers < 1 or > 8, fanout outside [1, 32], n_batch < 1). */
 grappa_status grappa_sample(grappa_ctx* ctx, const grappa_part* part, const int32_t* batch,
                             int32_t n_batch, const int32_t* fanouts, int32_t n_layers,
                             uint64_t seed, int64_t epoch, int64_t batch_index,

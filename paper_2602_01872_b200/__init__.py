@@ -282,16 +282,50 @@ def grappa_repartition(ctx: Context, rowptr: torch.Tensor, col: torch.Tensor, fe
     return part.refresh()
 
 
+class Index:
+    """grappa_index of (global CSR, chunk map): per-edge chunk bytes + per-chunk counts / degree
+    sums for grappa_repartition_batch_ix.  Keeps references to the tensors it indexes."""
+
+    def __init__(self, ctx: Context, rowptr: torch.Tensor, col: torch.Tensor, chunk_of: torch.Tensor,
+                 num_chunks: int, stream=None):
+        self.h = ctypes.c_void_p()
+        self.refs = (rowptr, col, chunk_of)
+        self.C = num_chunks
+        g = _lib.Csr(rowptr.numel() - 1, col.numel(), rowptr.data_ptr(), col.data_ptr())
+        _lib.check("grappa_index_create", ctx.lib.grappa_index_create(
+            ctx.h, ctypes.byref(g), _lib.ptr(chunk_of), num_chunks, ctypes.byref(self.h), _lib.stream_ptr(stream)))
+
+    def query(self):
+        cs, dg = (ctypes.c_int64 * self.C)(), (ctypes.c_int64 * self.C)()
+        _lib.check("grappa_index_query", load().grappa_index_query(self.h, cs, dg))
+        return list(cs), list(dg)
+
+    def destroy(self):
+        if self.h:
+            load().grappa_index_destroy(self.h)
+            self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        if sys.is_finalizing():
+            return
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
 def grappa_repartition_batch(ctx: Context, rowptr: torch.Tensor, col: torch.Tensor, feats, dtype,
                              chunk_of: torch.Tensor, num_chunks: int, pairs, train_mask: torch.Tensor, labels,
-                             parts=None, stream=None, chunk_sizes=None) -> list:
+                             parts=None, stream=None, chunk_sizes=None, index: "Index" = None) -> list:
     """every partition of a switch (pairs = [(base, swept)] per partition) in one call; parts:
     list of Part (or None) to reuse.  chunk_sizes: grappa_partition's output for chunk_of (computed
-    with torch on the device if not given)."""
+    with torch on the device if not given).  index: a prebuilt Index of (rowptr/col, chunk_of)
+    (grappa_repartition_batch_ix); None -> the library builds a temporary one."""
     g = _lib.Csr(rowptr.numel() - 1, col.numel(), rowptr.data_ptr(), col.data_ptr())
     K = len(pairs)
     if chunk_sizes is None:
-        chunk_sizes = torch.bincount(chunk_of.long(), minlength=num_chunks).cpu().tolist()
+        chunk_sizes = (index.query()[0] if index is not None
+                       else torch.bincount(chunk_of.long(), minlength=num_chunks).cpu().tolist())
     cs = (ctypes.c_int64 * num_chunks)(*[int(c) for c in chunk_sizes])
     bs = (ctypes.c_int32 * K)(*[int(b) for b, _ in pairs])
     ss = (ctypes.c_int32 * K)(*[int(s_) for _, s_ in pairs])
@@ -299,9 +333,14 @@ def grappa_repartition_batch(ctx: Context, rowptr: torch.Tensor, col: torch.Tens
     parts = [p if p is not None else Part() for p in parts]
     hs = (ctypes.c_void_p * K)(*[p.h.value for p in parts])
     fdim = 0 if feats is None else feats.shape[1]
-    _lib.check("grappa_repartition_batch", ctx.lib.grappa_repartition_batch(
-        ctx.h, ctypes.byref(g), _lib.ptr(feats), fdim, dtype_code(dtype), _lib.ptr(chunk_of), num_chunks, cs, K, bs,
-        ss, _lib.ptr(train_mask), _lib.ptr(labels), hs, _lib.stream_ptr(stream)))
+    if index is not None:
+        _lib.check("grappa_repartition_batch_ix", ctx.lib.grappa_repartition_batch_ix(
+            ctx.h, ctypes.byref(g), _lib.ptr(feats), fdim, dtype_code(dtype), index.h, cs, K, bs, ss,
+            _lib.ptr(train_mask), _lib.ptr(labels), hs, _lib.stream_ptr(stream)))
+    else:
+        _lib.check("grappa_repartition_batch", ctx.lib.grappa_repartition_batch(
+            ctx.h, ctypes.byref(g), _lib.ptr(feats), fdim, dtype_code(dtype), _lib.ptr(chunk_of), num_chunks, cs,
+            K, bs, ss, _lib.ptr(train_mask), _lib.ptr(labels), hs, _lib.stream_ptr(stream)))
     for p, h in zip(parts, hs):
         p.h = ctypes.c_void_p(h)
         p.refresh()

@@ -38,7 +38,8 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_part_save", "grappa_part_image_info", "grappa_part_load", "grappa_layer_saved_bytes_ex",
            "grappa_loss_ex", "grappa_shard_extract", "grappa_shard_query", "grappa_shard_destroy",
            "grappa_shard_exchange", "grappa_repartition_shards", "grappa_roofline_probe",
-           "grappa_ctx_create_ex", "grappa_comm_bytes", "grappa_repartition_batch"]
+           "grappa_ctx_create_ex", "grappa_comm_bytes", "grappa_repartition_batch",
+           "grappa_index_create", "grappa_index_query", "grappa_index_destroy", "grappa_repartition_batch_ix"]
 KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5, "sample": 6}
 
 
@@ -152,6 +153,11 @@ def load(path: str = LIB_PATH):
         "grappa_aggregate_grads": (st, [vp, vp, ctypes.c_int, dbl, dbl, vp, i64, i32, ctypes.c_int, f32, vp, vp]),
         "grappa_repartition_batch": (st, [vp, ctypes.POINTER(Csr), vp, i32, ctypes.c_int, vp, i32, vp, i32, vp, vp,
                                           vp, vp, vp, vp]),
+        "grappa_repartition_batch_ix": (st, [vp, ctypes.POINTER(Csr), vp, i32, ctypes.c_int, vp, vp, i32, vp, vp,
+                                             vp, vp, vp, vp]),
+        "grappa_index_create": (st, [vp, ctypes.POINTER(Csr), vp, i32, ctypes.POINTER(vp), vp]),
+        "grappa_index_query": (st, [vp, vp, vp]),
+        "grappa_index_destroy": (None, [vp]),
         "grappa_comm_bytes": (st, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
         "grappa_ctx_create_ex": (st, [ctypes.c_int, vp, ctypes.c_int, ctypes.c_int, ALLOC_FN, FREE_FN, vp,
                                       ctypes.POINTER(vp)]),

@@ -35,6 +35,17 @@ struct TmaPlan {
 };
 }  // namespace grappa
 
+// switch index of (global CSR, chunk map): per-edge chunk bytes and per-chunk counts / degree sums
+struct grappa_index {
+    const int64_t* rowptr = nullptr;
+    const int32_t* col = nullptr;
+    const int32_t* chunk_of = nullptr;
+    int64_t N = 0, nnz = 0;
+    int32_t C = 0;
+    grappa::DevBuf ec;                 // uint8 [nnz]: chunk_of[col[e]]
+    std::vector<int64_t> sizes, degs;  // per chunk: nodes, sum of their global degrees
+};
+
 // one chunk's rows (sharded mode): ids ascending, local rowptr from 0, global neighbour ids
 struct grappa_shard {
     grappa_shard_info info{};

@@ -29,6 +29,7 @@ namespace grappa {
 
 static size_t al256(size_t b) { return (b + 255) / 256 * 256; }
 
+
 struct FlagCore {
     const int32_t* chunk_of; int32_t b, s;
     __device__ int32_t operator()(int64_t v) const {
@@ -163,10 +164,11 @@ __global__ void k_row_deg(int64_t n, const int64_t* __restrict__ rowptr, int32_t
 }
 
 // Global rows are cut into tasks of at most kTaskLen edges (power-law hubs reach 10^5
-// neighbours; one warp per task keeps every warp's work bounded).  Tasks are numbered in
+// neighbours; a warp takes 32 tasks, so its work is bounded by 32 kTaskLen edges -- the tail
+// of a switch is the warp holding a hub's tasks).  Tasks are numbered in
 // (row, segment) order, so an exclusive scan of the per-task kept counts is directly each
 // task's output offset in the local `col` array -- and the local rowptr.
-constexpr int kTaskLen = 1024;
+constexpr int kTaskLen = 128;
 
 struct NumTasks {
     const int32_t* core_global; const int64_t* g_rowptr;
@@ -221,39 +223,86 @@ __device__ __forceinline__ bool in_core(const uint32_t* __restrict__ bm, int32_t
     return (__ldg(bm + (u >> 5)) >> (u & 31)) & 1u;
 }
 
-// kept-neighbour count of every task: half a warp per task (2 tasks per warp in flight), 4 x 16
-// edges per round, membership from the core bitmap (ballot / popc).  (Two tasks per half-warp
-// measured slower: 6.9 vs 5.9 ms per products switch, registers.)
-__global__ void k_task_count(const int64_t* __restrict__ d_T, const int4* __restrict__ task_desc,
-                             const int32_t* __restrict__ g_col, const uint32_t* __restrict__ bitmap,
-                             int32_t* __restrict__ tcount) {
-    const int lane = threadIdx.x & 31, half = lane >> 4, sub = lane & 15;
-    const unsigned hmask = 0xffffu << (half * 16);
+// Task processing (count and fill): a warp takes 32 consecutive tasks (one 16-byte descriptor
+// per lane, coalesced) and walks them kPackU at a time, all 32 lanes on one task's edges (lane j
+// takes edge j, j + 32, ...): the kPackU tasks' col loads and membership probes are independent
+// and in flight together, and a task's count is a warp-uniform popc of ballots -- no per-edge
+// owner search, no shared-memory bookkeeping.  (Half a warp per task, the former design, left
+// most lanes idle on products' short rows and had one dependent descriptor -> col -> bitmap chain
+// per task in flight.)  Halo-1 partitions keep every neighbour of a core row (keep_all).
+constexpr int kPackU = 4;
+// Edge membership in partition {b, s}.  EC: from the per-edge chunk bytes of the global CSR
+// (ec[e] = chunk_of[col[e]], built once per (graph, chunk map): a coalesced 1-byte stream
+// instead of a dependent random probe per edge); else from the core bitmap (sharded merged CSRs).
+struct Member {
+    const uint32_t* bitmap;
+    const uint8_t* ec;
+    int b, s, keep_all;
+};
+template <bool EC>
+__device__ __forceinline__ bool member(const Member& m, int64_t e, int32_t u) {
+    if (m.keep_all) return true;
+    if (EC) {
+        const int c = __ldg(m.ec + e);
+        return c == m.b || c == m.s;
+    }
+    return in_core(m.bitmap, u);
+}
+template <bool EC>
+__global__ void __launch_bounds__(256, 6) k_task_count(const int64_t* __restrict__ d_T,
+                                                    const int4* __restrict__ task_desc,
+                                                    const int32_t* __restrict__ g_col, Member mb,
+                                                    int32_t* __restrict__ tcount) {
+    const int lane = threadIdx.x & 31;
     const int64_t T = *d_T;
-    const int64_t nh = ((int64_t)gridDim.x * blockDim.x) >> 4;
-    for (int64_t t0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5 << 1; t0 < T; t0 += nh) {
-        const int64_t t = t0 + half;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; t0 < T; t0 += nwarps * 32) {
         int32_t len = 0;
         int64_t e0 = 0;
-        if (t < T) {
-            const int4 d = __ldg(task_desc + t);
+        if (t0 + lane < T) {
+            const int4 d = __ldg(task_desc + t0 + lane);
             len = d.y;
             e0 = (int64_t)(uint32_t)d.z | ((int64_t)d.w << 32);
         }
-        const int32_t lmax = __reduce_max_sync(0xffffffffu, len);
-        int32_t cnt = 0;
-        for (int32_t b = 0; b < lmax; b += 64) {
-            int32_t u[4];
+        if (mb.keep_all) {
+            if (t0 + lane < T) tcount[t0 + lane] = len;
+            continue;
+        }
+        const int nt = (int)min((int64_t)32, T - t0);
+        int32_t mine = 0;                       // lane i ends with task i's count
+        for (int i = 0; i < nt; i += kPackU) {
+            int32_t L[kPackU], c[kPackU];
+            int64_t E[kPackU];
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const int32_t e = b + k * 16 + sub;
-                u[k] = e < len ? __ldg(g_col + e0 + e) : -1;
+            for (int k = 0; k < kPackU; k++) {
+                L[k] = __shfl_sync(0xffffffffu, len, (i + k) & 31);
+                E[k] = __shfl_sync(0xffffffffu, e0, (i + k) & 31);
+                if (i + k >= nt) L[k] = 0;
+                c[k] = 0;
+            }
+            int32_t Lm = L[0];
+#pragma unroll
+            for (int k = 1; k < kPackU; k++) Lm = max(Lm, L[k]);
+            for (int32_t off = 0; off < Lm; off += 32) {
+                bool kp[kPackU];
+                if (EC) {        // only the chunk bytes are needed to count
+#pragma unroll
+                    for (int k = 0; k < kPackU; k++) kp[k] = off + lane < L[k] && member<true>(mb, E[k] + off + lane, 0);
+                } else {
+                    int32_t u[kPackU];
+#pragma unroll
+                    for (int k = 0; k < kPackU; k++) u[k] = off + lane < L[k] ? __ldg(g_col + E[k] + off + lane) : -1;
+#pragma unroll
+                    for (int k = 0; k < kPackU; k++) kp[k] = u[k] >= 0 && member<false>(mb, 0, u[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < kPackU; k++) c[k] += __popc(__ballot_sync(0xffffffffu, kp[k]));
             }
 #pragma unroll
-            for (int k = 0; k < 4; k++)
-                cnt += __popc(__ballot_sync(0xffffffffu, u[k] >= 0 && in_core(bitmap, u[k])) & hmask);
+            for (int k = 0; k < kPackU; k++)
+                if (lane == i + k) mine = c[k];
         }
-        if (sub == 0 && t < T) tcount[t] = cnt;
+        if (t0 + lane < T) tcount[t0 + lane] = mine;
     }
 }
 
@@ -292,46 +341,58 @@ __global__ void k_row_finalize(int64_t n_core, const int32_t* __restrict__ task_
     if ((threadIdx.x & 31) == 0 && my_dg) atomicAdd(sum_dg, my_dg);
 }
 
-// stable ballot compaction of every task's kept neighbours, relabelled to local ids (half a warp
-// per task, as k_task_count; rank is read for kept edges only)
-__global__ void k_task_fill(const int64_t* __restrict__ d_T, const int4* __restrict__ task_desc,
-                            const int64_t* __restrict__ task_out, const int32_t* __restrict__ g_col,
-                            const uint32_t* __restrict__ bitmap, const int32_t* __restrict__ rank,
-                            int32_t* __restrict__ col) {
-    const int lane = threadIdx.x & 31, half = lane >> 4, sub = lane & 15;
-    const unsigned hmask = 0xffffu << (half * 16);
-    const unsigned below = ((1u << lane) - 1u) & hmask;
+// stable compaction of every task's kept neighbours, relabelled to local ids (walked like
+// k_task_count; rank is read for kept edges only): a kept edge goes to its task's offset + the
+// task's kept edges before it (a warp-uniform running count + the popc of the lower lanes).
+template <bool EC>
+__global__ void __launch_bounds__(256, 6) k_task_fill(const int64_t* __restrict__ d_T,
+                                                   const int4* __restrict__ task_desc,
+                                                   const int64_t* __restrict__ task_out,
+                                                   const int32_t* __restrict__ g_col, Member mb,
+                                                   const int32_t* __restrict__ rank,
+                                                   int32_t* __restrict__ col) {
+    const int lane = threadIdx.x & 31;
+    const unsigned below = (1u << lane) - 1u;
     const int64_t T = *d_T;
-    const int64_t nh = ((int64_t)gridDim.x * blockDim.x) >> 4;
-    for (int64_t t0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5 << 1; t0 < T; t0 += nh) {
-        const int64_t t = t0 + half;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; t0 < T; t0 += nwarps * 32) {
         int32_t len = 0;
         int64_t e0 = 0, out = 0;
-        if (t < T) {
-            const int4 d = __ldg(task_desc + t);
+        if (t0 + lane < T) {
+            const int4 d = __ldg(task_desc + t0 + lane);
             len = d.y;
             e0 = (int64_t)(uint32_t)d.z | ((int64_t)d.w << 32);
-            out = task_out[t];
+            out = task_out[t0 + lane];
         }
-        const int32_t lmax = __reduce_max_sync(0xffffffffu, len);
-        for (int32_t b = 0; b < lmax; b += 64) {
-            int32_t u[4];
+        const int nt = (int)min((int64_t)32, T - t0);
+        for (int i = 0; i < nt; i += kPackU) {
+            int32_t L[kPackU];
+            int64_t E[kPackU], O[kPackU];
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const int32_t e = b + k * 16 + sub;
-                u[k] = e < len ? __ldg(g_col + e0 + e) : -1;
+            for (int k = 0; k < kPackU; k++) {
+                L[k] = __shfl_sync(0xffffffffu, len, (i + k) & 31);
+                E[k] = __shfl_sync(0xffffffffu, e0, (i + k) & 31);
+                O[k] = __shfl_sync(0xffffffffu, out, (i + k) & 31);
+                if (i + k >= nt) L[k] = 0;
             }
-            bool keep[4];
+            int32_t Lm = L[0];
 #pragma unroll
-            for (int k = 0; k < 4; k++) keep[k] = u[k] >= 0 && in_core(bitmap, u[k]);
-            int32_t r[4];
+            for (int k = 1; k < kPackU; k++) Lm = max(Lm, L[k]);
+            for (int32_t off = 0; off < Lm; off += 32) {
+                int32_t u[kPackU], r[kPackU];
+                bool keep[kPackU];
 #pragma unroll
-            for (int k = 0; k < 4; k++) r[k] = keep[k] ? __ldg(rank + u[k]) : -1;
+                for (int k = 0; k < kPackU; k++) u[k] = off + lane < L[k] ? __ldg(g_col + E[k] + off + lane) : -1;
 #pragma unroll
-            for (int k = 0; k < 4; k++) {                  // stable: edge order kept
-                const unsigned m = __ballot_sync(0xffffffffu, keep[k]) & hmask;
-                if (keep[k]) col[out + __popc(m & below)] = r[k];
-                out += __popc(m);
+                for (int k = 0; k < kPackU; k++) keep[k] = u[k] >= 0 && member<EC>(mb, E[k] + off + lane, u[k]);
+#pragma unroll
+                for (int k = 0; k < kPackU; k++) r[k] = keep[k] ? __ldg(rank + u[k]) : -1;
+#pragma unroll
+                for (int k = 0; k < kPackU; k++) {
+                    const unsigned bal = __ballot_sync(0xffffffffu, keep[k]);
+                    if (keep[k]) col[O[k] + __popc(bal & below)] = r[k];
+                    O[k] += __popc(bal);
+                }
             }
         }
     }
@@ -714,9 +775,15 @@ static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const voi
     RP_TRY(device_scan(ctx, NumTasks{srow, G_rowptr}, n_core,
                        WriteTasks{task_off, task_desc, d_stat, srow, G_rowptr}, s));
     const unsigned tgrid = (unsigned)ctx->sm_count * 16;
-    k_core_bitmap<<<(unsigned)ctx->sm_count * 16, 256, 0, s>>>(N, chunk_of, base, swept, bitmap);
-    GRAPPA_LAUNCHED(ctx);
-    k_task_count<<<tgrid, 256, 0, s>>>(d_stat + 5, task_desc, G_col, bitmap, tcount);
+    // membership: the core bitmap; halo-1 keeps every neighbour
+    const uint8_t* ec = nullptr;         // (the per-edge chunk bytes live in a grappa_index)
+    if (!halo) {
+        k_core_bitmap<<<(unsigned)ctx->sm_count * 16, 256, 0, s>>>(N, chunk_of, base, swept, bitmap);
+        GRAPPA_LAUNCHED(ctx);
+    }
+    const Member mb{bitmap, ec, base, swept, halo ? 1 : 0};
+    if (ec) k_task_count<true><<<tgrid, 256, 0, s>>>(d_stat + 5, task_desc, G_col, mb, tcount);
+    else k_task_count<false><<<tgrid, 256, 0, s>>>(d_stat + 5, task_desc, G_col, mb, tcount);
     GRAPPA_LAUNCHED(ctx);
     // 3. scans: task outputs (= local col offsets, total = nnz), then per-row finalize
     RP_TRY(device_scan(ctx, ReadTcount{tcount, d_stat + 5}, T_max, WriteTaskOut{task_out, d_stat}, s));
@@ -747,7 +814,8 @@ static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const voi
                "grappa_repartition: partition (%d,%d) has no seeds (S:213)", base, swept);
     // 4. fill
     RP_TRY(p->col.grow((size_t)(nnz > 0 ? nnz : 1) * 4));
-    k_task_fill<<<tgrid, 256, 0, s>>>(d_stat + 5, task_desc, task_out, G_col, bitmap, rank, (int32_t*)p->col.p);
+    if (ec) k_task_fill<true><<<tgrid, 256, 0, s>>>(d_stat + 5, task_desc, task_out, G_col, mb, rank, (int32_t*)p->col.p);
+    else k_task_fill<false><<<tgrid, 256, 0, s>>>(d_stat + 5, task_desc, task_out, G_col, mb, rank, (int32_t*)p->col.p);
     GRAPPA_LAUNCHED(ctx);
     // 5. features (core and halo rows)
     if (feats && !sa) {
@@ -912,10 +980,45 @@ __global__ void k_heavy_count(int64_t n, const int32_t* __restrict__ d_l, unsign
     }
 }
 __global__ void k_chunk_hist(int64_t n, const int32_t* __restrict__ chunk_of, int C, unsigned long long* cnt) {
+    __shared__ unsigned int sh[256];
+    const bool loc = C <= 256;
+    if (loc)
+        for (int i = threadIdx.x; i < C; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
         const int32_t c = chunk_of[v];
-        if (c >= 0 && c < C) atomicAdd(&cnt[c], 1ull);
+        if (c >= 0 && c < C) {
+            if (loc) atomicAdd(&sh[c], 1u);
+            else atomicAdd(&cnt[c], 1ull);
+        }
     }
+    __syncthreads();
+    if (loc)
+        for (int i = threadIdx.x; i < C; i += blockDim.x)
+            if (sh[i]) atomicAdd(&cnt[i], (unsigned long long)sh[i]);
+}
+// per-chunk sums of the nodes' global degrees (block-local shared sums for C <= 64)
+__global__ void k_chunk_deg(int64_t n, const int32_t* __restrict__ chunk_of, const int64_t* __restrict__ rowptr,
+                            int C, unsigned long long* sum) {
+    __shared__ unsigned long long sh[64];
+    const bool loc = C <= 64;
+    if (loc)
+        for (int i = threadIdx.x; i < C; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t c = chunk_of[v];
+        const unsigned long long d = (unsigned long long)(rowptr[v + 1] - rowptr[v]);
+        if (c >= 0 && c < C && d) atomicAdd(loc ? &sh[c] : &sum[c], d);
+    }
+    __syncthreads();
+    if (loc)
+        for (int i = threadIdx.x; i < C; i += blockDim.x)
+            if (sh[i]) atomicAdd(&sum[i], sh[i]);
+}
+__global__ void k_edge_chunk(int64_t nnz, const int32_t* __restrict__ col, const int32_t* __restrict__ chunk_of,
+                             uint8_t* __restrict__ ec) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
+        ec[e] = (uint8_t)__ldg(chunk_of + __ldg(col + e));
 }
 struct WriteRankOnly {
     int32_t* rank;
@@ -931,6 +1034,69 @@ struct WriteRankOnly {
 // 8 bytes per node), stable fill of the local columns, features, coverage statistics, SpMM plan
 // with the now-known split-row sizes; one final sync publishes the statistics.  Core sizes come
 // from the caller's chunk sizes (grappa_partition's output), checked against the device counts.
+extern "C" grappa_status grappa_index_create(grappa_ctx* ctx, const grappa_csr* g, const int32_t* chunk_of,
+                                             int32_t num_chunks, grappa_index** out, void* stream) {
+    CallScope call_scope(ctx, stream);
+    GRAPPA_ARG(ctx && g && chunk_of && out, GRAPPA_E_ARG, "grappa_index_create: null argument");
+    GRAPPA_ARG(num_chunks >= 2 && num_chunks <= 255, GRAPPA_E_ARG, "grappa_index_create: need 2 <= C <= 255");
+    GRAPPA_ARG(g->num_nodes > 0 && g->num_nodes < (1ll << 31) && g->nnz >= 0, GRAPPA_E_ARG,
+               "grappa_index_create: num_nodes out of int32 range");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t N = g->num_nodes;
+    grappa_index* ix = new grappa_index();
+    auto fail = [&](grappa_status st) {
+        grappa_index_destroy(ix);
+        return st;
+    };
+#define IX_TRY(expr)                          \
+    do {                                      \
+        grappa_status _s = (expr);            \
+        if (_s != GRAPPA_OK) return fail(_s); \
+    } while (0)
+    IX_TRY(ix->ec.grow((size_t)(g->nnz > 0 ? g->nnz : 1)));
+    if (g->nnz > 0) {
+        k_edge_chunk<<<(unsigned)std::min<int64_t>(ceil_div(g->nnz, 256), (int64_t)ctx->sm_count * 32), 256, 0, s>>>(
+            g->nnz, g->col, chunk_of, (uint8_t*)ix->ec.p);
+        GRAPPA_LAUNCHED(ctx);
+    }
+    IX_TRY(ctx->small.grow((size_t)num_chunks * 16));
+    unsigned long long* d_cnt = (unsigned long long*)ctx->small.p;
+    if (cudaMemsetAsync(d_cnt, 0, (size_t)num_chunks * 16, s) != cudaSuccess) return fail(GRAPPA_E_CUDA);
+    const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(N, 256), (int64_t)ctx->sm_count * 8));
+    k_chunk_hist<<<gr, 256, 0, s>>>(N, chunk_of, num_chunks, d_cnt);
+    GRAPPA_LAUNCHED(ctx);
+    k_chunk_deg<<<gr, 256, 0, s>>>(N, chunk_of, g->rowptr, num_chunks, d_cnt + num_chunks);
+    GRAPPA_LAUNCHED(ctx);
+    std::vector<int64_t> h((size_t)num_chunks * 2);
+    if (cudaMemcpyAsync(h.data(), d_cnt, (size_t)num_chunks * 16, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+        set_error("grappa_index_create: %s", cudaGetErrorString(cudaGetLastError()));
+        return fail(GRAPPA_E_CUDA);
+    }
+    ix->sizes.assign(h.begin(), h.begin() + num_chunks);
+    ix->degs.assign(h.begin() + num_chunks, h.end());
+    ix->rowptr = g->rowptr; ix->col = g->col; ix->chunk_of = chunk_of;
+    ix->N = N; ix->nnz = g->nnz; ix->C = num_chunks;
+    *out = ix;
+    return GRAPPA_OK;
+#undef IX_TRY
+}
+
+extern "C" void grappa_index_destroy(grappa_index* ix) {
+    if (!ix) return;
+    ix->ec.release();
+    delete ix;
+}
+
+extern "C" grappa_status grappa_index_query(const grappa_index* ix, int64_t* chunk_sizes, int64_t* chunk_degrees) {
+    GRAPPA_ARG(ix, GRAPPA_E_ARG, "grappa_index_query: null argument");
+    for (int c = 0; c < ix->C; c++) {
+        if (chunk_sizes) chunk_sizes[c] = ix->sizes[c];
+        if (chunk_degrees) chunk_degrees[c] = ix->degs[c];
+    }
+    return GRAPPA_OK;
+}
+
 extern "C" grappa_status grappa_repartition_batch(grappa_ctx* ctx, const grappa_csr* g, const void* feats,
                                                   int32_t feat_dim, grappa_dtype dtype, const int32_t* chunk_of,
                                                   int32_t num_chunks, const int64_t* chunk_sizes, int32_t n_parts,
@@ -938,14 +1104,37 @@ extern "C" grappa_status grappa_repartition_batch(grappa_ctx* ctx, const grappa_
                                                   const uint8_t* train_mask, const int32_t* labels,
                                                   grappa_part** parts, void* stream) {
     CallScope call_scope(ctx, stream);
-    GRAPPA_ARG(ctx && g && chunk_of && chunk_sizes && bases && swepts && train_mask && parts && n_parts >= 1,
+    GRAPPA_ARG(ctx && g && chunk_of, GRAPPA_E_ARG, "grappa_repartition_batch: null argument");
+    grappa_index* ix = nullptr;
+    GRAPPA_TRY(grappa_index_create(ctx, g, chunk_of, num_chunks, &ix, stream));
+    const grappa_status st = grappa_repartition_batch_ix(ctx, g, feats, feat_dim, dtype, ix, chunk_sizes, n_parts,
+                                                         bases, swepts, train_mask, labels, parts, stream);
+    cudaStreamSynchronize((cudaStream_t)stream);     // the index's buffer is in use until here
+    grappa_index_destroy(ix);
+    return st;
+}
+
+extern "C" grappa_status grappa_repartition_batch_ix(grappa_ctx* ctx, const grappa_csr* g, const void* feats,
+                                                     int32_t feat_dim, grappa_dtype dtype, const grappa_index* ix,
+                                                     const int64_t* chunk_sizes, int32_t n_parts,
+                                                     const int32_t* bases, const int32_t* swepts,
+                                                     const uint8_t* train_mask, const int32_t* labels,
+                                                     grappa_part** parts, void* stream) {
+    CallScope call_scope(ctx, stream);
+    GRAPPA_ARG(ctx && g && ix && chunk_sizes && bases && swepts && train_mask && parts && n_parts >= 1,
                GRAPPA_E_ARG, "grappa_repartition_batch: null argument");
     GRAPPA_ARG(feats == nullptr || (feat_dim > 0 && feat_dim % 16 == 0), GRAPPA_E_SHAPE,
                "grappa_repartition_batch: feat_dim must be a positive multiple of 16");
-    GRAPPA_ARG(g->num_nodes > 0 && g->num_nodes < (1ll << 31), GRAPPA_E_ARG,
-               "grappa_repartition_batch: num_nodes out of int32 range");
+    GRAPPA_ARG(ix->col == g->col && ix->rowptr == g->rowptr && ix->N == g->num_nodes && ix->nnz == g->nnz,
+               GRAPPA_E_ARG, "grappa_repartition_batch: the index was built for another graph");
+    const int32_t* chunk_of = ix->chunk_of;
+    const int32_t num_chunks = ix->C;
     const int K = n_parts;
     std::vector<int64_t> ncore(K);
+    for (int c = 0; c < num_chunks; c++)
+        GRAPPA_ARG(ix->sizes[c] == chunk_sizes[c], GRAPPA_E_ARG,
+                   "grappa_repartition_batch: chunk_sizes[%d] = %lld but the chunk map holds %lld nodes", c,
+                   (long long)chunk_sizes[c], (long long)ix->sizes[c]);
     for (int k = 0; k < K; k++) {
         GRAPPA_ARG(bases[k] != swepts[k], GRAPPA_E_ARG, "grappa_repartition_batch: base == swept (S:139)");
         GRAPPA_ARG(bases[k] >= 0 && swepts[k] >= 0 && bases[k] < num_chunks && swepts[k] < num_chunks, GRAPPA_E_ARG,
@@ -956,27 +1145,6 @@ extern "C" grappa_status grappa_repartition_batch(grappa_ctx* ctx, const grappa_
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t N = g->num_nodes;
     const int64_t esz = dtype == GRAPPA_BF16 ? 2 : 4;
-    // the counts must describe this chunk map (every allocation below is sized from them): known
-    // from grappa_partition, else counted once on the device (one sync) and remembered
-    const bool known = ctx->cmap_ptr == chunk_of && ctx->cmap_n == N && (int)ctx->cmap_sizes.size() == num_chunks;
-    if (!known) {
-        GRAPPA_TRY(ctx->small.grow((size_t)num_chunks * 8));
-        unsigned long long* d_cnt = (unsigned long long*)ctx->small.p;
-        GRAPPA_CUDA(cudaMemsetAsync(d_cnt, 0, (size_t)num_chunks * 8, s));
-        k_chunk_hist<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(N, 256), (int64_t)ctx->sm_count * 8)),
-                       256, 0, s>>>(N, chunk_of, num_chunks, d_cnt);
-        GRAPPA_LAUNCHED(ctx);
-        std::vector<int64_t> cnt(num_chunks);
-        GRAPPA_CUDA(cudaMemcpyAsync(cnt.data(), d_cnt, (size_t)num_chunks * 8, cudaMemcpyDeviceToHost, s));
-        GRAPPA_CUDA(cudaStreamSynchronize(s));
-        ctx->cmap_ptr = chunk_of;
-        ctx->cmap_n = N;
-        ctx->cmap_sizes = cnt;
-    }
-    for (int c = 0; c < num_chunks; c++)
-        GRAPPA_ARG(ctx->cmap_sizes[c] == chunk_sizes[c], GRAPPA_E_ARG,
-                   "grappa_repartition_batch: chunk_sizes[%d] = %lld but the chunk map holds %lld nodes", c,
-                   (long long)chunk_sizes[c], (long long)ctx->cmap_sizes[c]);
     ProfScope ps(ctx, s, GRAPPA_K_REPART, 0.0, 0.0);
     // new partition objects (destroyed again if the batch fails)
     std::vector<grappa_part*> P(K);
@@ -1010,20 +1178,20 @@ extern "C" grappa_status grappa_repartition_batch(grappa_ctx* ctx, const grappa_
     int64_t* d_stat0 = (int64_t*)ctx->small.p;
     SeedStats* d_ss0 = (SeedStats*)(d_stat0 + (size_t)K * kSt);
     RB_CUDA(cudaMemsetAsync(d_stat0, 0, (size_t)K * kSt * 8, s));
-    // rank table (int32 [N]) + core membership bitmap (1 bit per node, L1/L2-resident: the per-edge
-    // test of the counting pass and the first test of the fill; rank is read for kept edges only)
-    const int64_t n_words = ceil_div(N, 32);
-    RB_TRY(ctx->red_ws.grow((size_t)N * sizeof(int32_t) + (size_t)n_words * 4));
-    int32_t* rank = (int32_t*)ctx->red_ws.p;
-    uint32_t* bitmap = (uint32_t*)(rank + N);
-    const unsigned bm_grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_words * 32, 256),
-                                                                             (int64_t)ctx->sm_count * 16));
+    // rank table (int32 [N], read for kept edges only); membership from the per-edge chunk bytes
+    // one table per partition when K of them fit in 1 GiB (phase B then reuses phase A's), else
+    // one shared table recomputed in phase B
+    const bool keep_ranks = (double)K * (double)N * 4.0 <= (double)(1ll << 30);
+    RB_TRY(ctx->red_ws.grow((size_t)N * sizeof(int32_t) * (keep_ranks ? K : 1)));
+    int32_t* rank0 = (int32_t*)ctx->red_ws.p;
+    auto rank_of = [&](int k) { return keep_ranks ? rank0 + (size_t)k * N : rank0; };
     // task tables of every partition (phase B reads them): one workspace, K slices
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     std::vector<int64_t> Tmax(K);
     std::vector<size_t> ws_off(K + 1, 0);
     for (int k = 0; k < K; k++) {
-        Tmax[k] = ncore[k] + g->nnz / kTaskLen + 1;
+        // sum over core rows of max(1, ceil(d / L)) <= n + floor(sum d / L)
+        Tmax[k] = ncore[k] + (ix->degs[bases[k]] + ix->degs[swepts[k]]) / kTaskLen + 1;
         ws_off[k + 1] = ws_off[k] + al((size_t)(ncore[k] + 1) * 4) + al((size_t)Tmax[k] * 16) +
                         al((size_t)Tmax[k] * 4) + al((size_t)(Tmax[k] + 1) * 8);
     }
@@ -1038,6 +1206,7 @@ extern "C" grappa_status grappa_repartition_batch(grappa_ctx* ctx, const grappa_
         tw[k].out = (int64_t*)w;
     }
     const unsigned tgrid = (unsigned)ctx->sm_count * 16;
+    const uint8_t* ec = (const uint8_t*)ix->ec.p;
     // ---------------------------------------------------------------- phase A
     for (int k = 0; k < K; k++) {
         grappa_part* p = P[k];
@@ -1055,13 +1224,14 @@ extern "C" grappa_status grappa_repartition_batch(grappa_ctx* ctx, const grappa_
         RB_TRY(p->heavy_rows.grow((size_t)n * 4));
         const int32_t* cg = (const int32_t*)p->core_global.p;
         RB_TRY(device_scan(ctx, FlagCore{chunk_of, bases[k], swepts[k]}, N,
-                           WriteRank{rank, (int32_t*)p->core_global.p, d_stat}, s));
+                           WriteRank{rank_of(k), (int32_t*)p->core_global.p, d_stat}, s));
         unsigned grid;
         rp_grid(ctx, n, 256, &grid);
-        k_core_bitmap<<<bm_grid, 256, 0, s>>>(N, chunk_of, bases[k], swepts[k], bitmap);
-        GRAPPA_LAUNCHED(ctx);
         RB_TRY(device_scan(ctx, NumTasks{cg, g->rowptr}, n, WriteTasks{tw[k].off, tw[k].desc, d_stat, cg, g->rowptr}, s));
-        k_task_count<<<tgrid, 256, 0, s>>>(d_stat + 5, tw[k].desc, g->col, bitmap, tw[k].cnt);
+        {
+            const Member mb{nullptr, ec, bases[k], swepts[k], 0};
+            k_task_count<true><<<tgrid, 256, 0, s>>>(d_stat + 5, tw[k].desc, g->col, mb, tw[k].cnt);
+        }
         GRAPPA_LAUNCHED(ctx);
         RB_TRY(device_scan(ctx, ReadTcount{tw[k].cnt, d_stat + 5}, Tmax[k], WriteTaskOut{tw[k].out, d_stat}, s));
         k_row_finalize<<<grid, 256, 0, s>>>(n, tw[k].off, tw[k].out, cg, g->rowptr, labels, (int64_t*)p->rowptr.p,
@@ -1096,12 +1266,15 @@ extern "C" grappa_status grappa_repartition_batch(grappa_ctx* ctx, const grappa_
         const int64_t* h = &st[(size_t)k * kSt];
         const int64_t n = ncore[k], nnz = h[1], n_seeds = h[2], n_heavy = h[3], n_slots = h[4];
         const int32_t* cg = (const int32_t*)p->core_global.p;
-        RB_TRY(device_scan(ctx, FlagCore{chunk_of, bases[k], swepts[k]}, N, WriteRankOnly{rank}, s));
+        int32_t* rank = rank_of(k);
+        if (!keep_ranks)
+            RB_TRY(device_scan(ctx, FlagCore{chunk_of, bases[k], swepts[k]}, N, WriteRankOnly{rank}, s));
         RB_TRY(p->col.grow((size_t)(nnz > 0 ? nnz : 1) * 4));
-        k_core_bitmap<<<bm_grid, 256, 0, s>>>(N, chunk_of, bases[k], swepts[k], bitmap);
-        GRAPPA_LAUNCHED(ctx);
-        k_task_fill<<<tgrid, 256, 0, s>>>(d_stat0 + (size_t)k * kSt + 5, tw[k].desc, tw[k].out, g->col, bitmap, rank,
-                                           (int32_t*)p->col.p);
+        {
+            const Member mb{nullptr, ec, bases[k], swepts[k], 0};
+            k_task_fill<true><<<tgrid, 256, 0, s>>>(d_stat0 + (size_t)k * kSt + 5, tw[k].desc, tw[k].out, g->col, mb, rank,
+                                     (int32_t*)p->col.p);
+        }
         GRAPPA_LAUNCHED(ctx);
         unsigned grid;
         rp_grid(ctx, n, 256, &grid);

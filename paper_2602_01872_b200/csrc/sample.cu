@@ -23,7 +23,7 @@
 namespace grappa {
 
 constexpr int kMaxLayers = 8;
-constexpr int kMaxFanout = 16;
+constexpr int kMaxFanout = 32;   // P:489 fanouts {25,10}, {20,15,10,5}; kernels instantiated for <=16 and <=32
 
 __device__ __forceinline__ uint64_t smix(uint64_t x) {
     uint64_t z = x + 0x9E3779B97F4A7C15ull;
@@ -45,6 +45,7 @@ static uint64_t hmix(uint64_t x) {
 // hashed every neighbour).  One thread per target; picks in draw order (k_fill_block sorts).
 // The picked neighbours are also marked in the frontier bitmap here (cleared beforehand), which
 // saves the separate marking pass over the picks.
+template <int MAXF>
 __global__ void k_pick_floyd(const int64_t* __restrict__ d_nt, const int32_t* __restrict__ targets,
                              const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                              const int32_t* __restrict__ gid, int f, uint64_t key0, int32_t* __restrict__ picks,
@@ -65,27 +66,27 @@ __global__ void k_pick_floyd(const int64_t* __restrict__ d_nt, const int32_t* __
         }
         const uint64_t kv = key0;
         const uint64_t gv = (uint64_t)gid[v];
-        int64_t kept[kMaxFanout];
+        int64_t kept[MAXF];
 #pragma unroll
-        for (int k = 0; k < kMaxFanout; k++) {
+        for (int k = 0; k < MAXF; k++) {
             if (k >= f) break;
             const int64_t j = d - f + k;
             const uint64_t r = smix(kv ^ smix(gv ^ smix((uint64_t)j)));
             int64_t pos = (int64_t)__umul64hi(r, (uint64_t)(j + 1));
             bool dup = false;
 #pragma unroll
-            for (int q = 0; q < kMaxFanout; q++)
+            for (int q = 0; q < MAXF; q++)
                 if (q < k && kept[q] == pos) dup = true;
             if (dup) pos = j;
             kept[k] = pos;
         }
         // neighbour ids of the kept positions (independent loads, issued together)
-        int32_t u[kMaxFanout];
+        int32_t u[MAXF];
 #pragma unroll
-        for (int k = 0; k < kMaxFanout; k++)
+        for (int k = 0; k < MAXF; k++)
             if (k < f) u[k] = col[e0 + kept[k]];
 #pragma unroll
-        for (int k = 0; k < kMaxFanout; k++)
+        for (int k = 0; k < MAXF; k++)
             if (k < f) {
                 out[k] = u[k];
                 atomicOr(&bitmap[u[k] >> 5], 1u << (u[k] & 31));
@@ -136,6 +137,7 @@ struct WriteBRow {
 };
 
 // block CSR rows: positions of the picks, ascending; edge -> target id for the transpose sort
+template <int MAXF>
 __global__ void k_fill_block(const int64_t* __restrict__ d_nt, const int64_t* __restrict__ d_nnz,
                              int64_t cap_nnz, const int32_t* __restrict__ picks, const int32_t* __restrict__ cnt,
                              int f, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ where,
@@ -146,11 +148,11 @@ __global__ void k_fill_block(const int64_t* __restrict__ d_nt, const int64_t* __
     const int64_t nt = *d_nt, nnz = *d_nnz;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
         const int c = cnt[t];
-        int32_t p[kMaxFanout];
+        int32_t p[MAXF];
 #pragma unroll
-        for (int j = 0; j < kMaxFanout; j++) p[j] = j < c ? where[picks[t * f + j]] : 0x7fffffff;
+        for (int j = 0; j < MAXF; j++) p[j] = j < c ? where[picks[t * f + j]] : 0x7fffffff;
 #pragma unroll
-        for (int a = 1; a < kMaxFanout; a++)              // insertion sort, unrolled network
+        for (int a = 1; a < MAXF; a++)              // insertion sort, unrolled network
 #pragma unroll
             for (int b = a; b > 0; b--)
                 if (p[b] < p[b - 1]) { const int32_t x = p[b]; p[b] = p[b - 1]; p[b - 1] = x; }
@@ -340,9 +342,12 @@ extern "C" grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part*
         const uint64_t key0 = hmix(seed ^ hmix((uint64_t)epoch ^ hmix((uint64_t)batch_index ^ hmix((uint64_t)h))));
         const unsigned tgrid = (unsigned)std::min<int64_t>(ceil_div(cap_nnz, 256), (int64_t)ctx->sm_count * 16);
         GRAPPA_CUDA(cudaMemsetAsync(b->bitmap.p, 0, (size_t)nwords * 4, s));
-        k_pick_floyd<<<(unsigned)std::min<int64_t>(ceil_div(cap_t, 256), (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
-            d_nt, targets, I.rowptr, I.col, I.core_global, f, key0, (int32_t*)b->picks.p, (int32_t*)b->cnt.p,
-            (uint32_t*)b->bitmap.p);
+        {
+            auto kp = f <= 16 ? k_pick_floyd<16> : k_pick_floyd<32>;
+            kp<<<(unsigned)std::min<int64_t>(ceil_div(cap_t, 256), (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
+                d_nt, targets, I.rowptr, I.col, I.core_global, f, key0, (int32_t*)b->picks.p, (int32_t*)b->cnt.p,
+                (uint32_t*)b->bitmap.p);
+        }
         GRAPPA_LAUNCHED(ctx);
         k_unmark<<<(unsigned)std::min<int64_t>(ceil_div(cap_t, 256), 4096), 256, 0, s>>>(
             d_nt, targets, (uint32_t*)b->bitmap.p, (int32_t*)b->where.p, (int32_t*)B.src.p);
@@ -352,7 +357,7 @@ extern "C" grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part*
                                nullptr, &b->scan_ws));
         GRAPPA_TRY(device_scan(ctx, CntUpTo{(int32_t*)b->cnt.p, d_nt}, cap_t,
                                WriteBRow{(int64_t*)B.rowptr.p, d_nnz}, s, nullptr, &b->scan_ws));
-        k_fill_block<<<tgrid, 256, 0, s>>>(d_nt, d_nnz, cap_nnz, (int32_t*)b->picks.p, (int32_t*)b->cnt.p, f,
+        (f <= 16 ? k_fill_block<16> : k_fill_block<32>)<<<tgrid, 256, 0, s>>>(d_nt, d_nnz, cap_nnz, (int32_t*)b->picks.p, (int32_t*)b->cnt.p, f,
                                            (int64_t*)B.rowptr.p, (int32_t*)b->where.p, (int32_t*)B.col.p,
                                            (int32_t*)b->erow.p, (int32_t*)b->key_pad.p, (float*)B.inv_cnt.p,
                                            targets, I.d_l, I.d_g, (float*)B.inv_cnt_node.p);

@@ -23,7 +23,7 @@ import torch
 
 from . import (BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, F32, LAYER_INPUT, LAYER_NODE_LEVEL, Context, Part,
                Shard, grappa_aggregate_grads, grappa_layer_bwd, grappa_layer_bwd_ex, grappa_layer_fwd_ex,
-               grappa_loss, grappa_partition, grappa_repartition, grappa_repartition_batch, grappa_repartition_shards,
+               Index, grappa_loss, grappa_partition, grappa_repartition, grappa_repartition_batch, grappa_repartition_shards,
                grappa_shard_exchange, grappa_shard_extract, layer_saved_bytes, layer_ws_bytes)
 
 
@@ -239,10 +239,14 @@ class Trainer:
                                                    self.parts.get(w), self.stream, halo=True)
         elif mine:
             # every partition of this rank in one call: two host syncs per switch
+            # the switch index (per-edge chunk bytes of this graph under the run's chunk map) is
+            # built at the first switch and kept: graph and chunk map never change within a run
+            if getattr(self, "index", None) is None:
+                self.index = Index(self.ctx, self.rowptr, self.col, self.chunk_of, self.C, self.stream)
             got = grappa_repartition_batch(self.ctx, self.rowptr, self.col, self.x, self.dt, self.chunk_of, self.C,
                                            [pairs[w] for w in mine], self.train, self.labels,
                                            [self.parts.get(w) for w in mine], self.stream,
-                                           chunk_sizes=self.chunk_sizes)
+                                           chunk_sizes=self.chunk_sizes, index=self.index)
             self.parts.update(zip(mine, got))
         self.t = t
         self._alloc()

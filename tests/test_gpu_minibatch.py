@@ -59,13 +59,17 @@ def test_epoch_order_bitexact(G, setup):
         assert np.array_equal(order.cpu().numpy(), exp)
 
 
-@pytest.mark.parametrize("batch_index", [0, 5])
-def test_sampled_blocks_bitexact(G, setup, batch_index):
+@pytest.mark.parametrize("batch_index,fan", [(0, FAN), (5, FAN),
+                                             (2, [25, 10]),            # P:489 2-layer fanouts
+                                             (3, [20, 15, 10, 5]),     # P:489 4-layer fanouts
+                                             (1, [32, 17])])           # the cap; the <=32 kernels
+def test_sampled_blocks_bitexact(G, setup, batch_index, fan):
     ctx, wl, ds, ref, parts = setup
     p = parts["f32"]
     seeds = Sa.epoch_batches(ref, 9, 1, 300)[batch_index]
-    b = G.grappa_sample(ctx, p, torch.from_numpy(seeds.astype(np.int32)).cuda(), FAN, 9, 1, batch_index)
-    blocks = Sa.sample_batch(ref, seeds, FAN, 9, 1, batch_index)
+    b = G.grappa_sample(ctx, p, torch.from_numpy(seeds.astype(np.int32)).cuda(), fan, 9, 1, batch_index)
+    blocks = Sa.sample_batch(ref, seeds, fan, 9, 1, batch_index)
+    assert len(blocks) == len(fan) == len(b.blocks)
     for l, (gb, ob) in enumerate(zip(b.blocks, blocks)):
         assert gb["n_dst"] == ob["n_dst"] and gb["n_src"] == ob["n_src"], l
         assert np.array_equal(gb["src"].cpu().numpy(), ob["src"]), l
@@ -84,6 +88,13 @@ def test_sampled_blocks_bitexact(G, setup, batch_index):
     assert math.isclose(b.factors["uniform"], Co.c_uniform(d_l, d_g), rel_tol=1e-12)
     assert math.isclose(b.factors["resampling"], Co.c_resampling(d_l, d_g, s), rel_tol=1e-12)
     assert math.isclose(b.factors["resampling_hm"], Co.c_resampling_hm(d_l, d_g, s), rel_tol=1e-12)
+
+
+def test_fanout_cap_rejected(G, setup):
+    ctx, wl, ds, ref, parts = setup
+    seeds = torch.arange(10, dtype=torch.int32, device="cuda")
+    with pytest.raises(Exception, match="fanout"):
+        G.grappa_sample(ctx, parts["f32"], seeds, [33, 5], 9, 1, 0)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])

@@ -525,8 +525,9 @@ def test_spmm_tma_bitwise_equals_row_group(G, ctx, prod, width, mode):
 
 @pytest.mark.parametrize("C,dtype", [(8, "bf16"), (4, "f32"), (2, "bf16"), (80, "bf16")])
 def test_repartition_batch_bitexact(G, ctx, prod, C, dtype):
-    """grappa_repartition_batch (all partitions of a switch, two host syncs) builds every partition
-    bit for bit as grappa_repartition and the oracle do -- CSR, maps, degrees, norms, node weights,
+    """grappa_repartition_batch (all partitions of a switch, two host syncs; with the run's
+    grappa_index or a temporary one) builds every partition bit for bit as grappa_repartition and
+    the oracle do; the index's per-chunk counts and degree sums are exact -- CSR, maps, degrees, norms, node weights,
     seeds, labels, gathered features, split-row plan sizes, coverage statistics -- reusing the
     previous switch's partition objects; chunk sizes that disagree with the map are rejected."""
     rp, col, x, y, tr = upload(prod)
@@ -537,9 +538,14 @@ def test_repartition_batch_bitexact(G, ctx, prod, C, dtype):
     xt = x.to(torch.bfloat16) if dtype == "bf16" else x
     sched = Po.sweep_schedule(C, C)
     parts = None
-    for t in range(min(2, len(sched))):
+    index = G.Index(ctx, rp, col, ch, C)        # the engine's path: one index for the whole run
+    assert index.query()[0] == list(sizes)
+    deg = np.diff(prod.rowptr)
+    assert index.query()[1] == [int(deg[chunk_of == c].sum()) for c in range(C)]
+    for t in range(min(3, len(sched))):
         pairs = sched[t][:8]
-        parts = G.grappa_repartition_batch(ctx, rp, col, xt, dtype, ch, C, pairs, tr, y, parts, chunk_sizes=sizes)
+        parts = G.grappa_repartition_batch(ctx, rp, col, xt, dtype, ch, C, pairs, tr, y, parts, chunk_sizes=sizes,
+                                           index=index if t != 1 else None)
         for (b, s), p in zip(pairs, parts):
             one = G.grappa_repartition(ctx, rp, col, xt, dtype, ch, C, b, s, tr, y)
             ref = Po.induced_partition(prod.rowptr, prod.col, chunk_of, b, s, prod.train)
@@ -554,6 +560,9 @@ def test_repartition_batch_bitexact(G, ctx, prod, C, dtype):
             for f in ("n_core", "nnz", "n_seeds", "n_heavy", "n_slots", "D", "c_uniform", "c_resampling",
                       "c_resampling_hm"):
                 assert getattr(p.info, f) == getattr(one.info, f), f
+    with pytest.raises(G.GrappaError, match="E_ARG"):       # an index of another graph
+        G.grappa_repartition_batch(ctx, rp, col.clone(), xt, dtype, ch, C, sched[0][:8], tr, y, chunk_sizes=sizes,
+                                   index=index)
     bad = list(sizes)
     bad[sched[0][0][0]] += 1
     with pytest.raises(G.GrappaError, match="E_ARG"):
