@@ -44,8 +44,10 @@ def parse():
                     choices=["none", "uniform", "resampling", "resampling_hm", "node"],
                     help="override the config's estimator (node = node-level eq. (9), R30)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--capacity", action="store_true",
-                    help="capacity mode: partitions streamed per phase from pinned host images")
+    ap.add_argument("--capacity", nargs="?", const="images", default=None, choices=["images", "shards"],
+                    help="capacity mode: partitions streamed per phase from pinned host images ('images'), or "
+                         "chunk-shard images in host memory with the partition extracted per phase on the "
+                         "device ('shards': the global graph never reaches the GPU)")
     ap.add_argument("--sharded", action="store_true",
                     help="sharded mode (a3 (i)): each rank keeps its chunk shards only; swept shards "
                          "arrive by NCCL point-to-point at super-epoch switches")
@@ -338,7 +340,7 @@ def run_grappa(args):
     stream = torch.cuda.current_stream(dev)
     common = dict(corr=args.corr or wl.correction, lr=0.003, repartition_every=wl.repartition_every,
                   dtype=args.dtype, stream=stream, num_workers=wl.extra.get("workers"), halo=args.halo,
-                  capacity=args.capacity, sharded=args.sharded)
+                  capacity={None: False, "images": True, "shards": "shards"}[args.capacity], sharded=args.sharded)
     if wl.extra.get("mode") == "minibatch":
         tr = MinibatchTrainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights,
                               wl.chunks, gen.seed_of("chunks"), fanouts=wl.extra["fanouts"],
@@ -349,7 +351,9 @@ def run_grappa(args):
                      gen.seed_of("chunks"), **common)
     nnz = ds.nnz
     full_graph = not isinstance(tr, MinibatchTrainer)
-    keep_ds = ds if (args.dtype == "bf16" and full_graph and not args.no_f32) else None
+    # the fp32 arm accompanies the headline configuration only (replicated, induced-core, resident)
+    keep_ds = ds if (args.dtype == "bf16" and full_graph and not args.no_f32 and not args.capacity
+                     and not args.sharded and not args.halo) else None
     del ds
 
     def barrier():
@@ -394,6 +398,7 @@ def run_grappa(args):
         evs[k + 1].record(stream)
     barrier()
     clk = clocks.stop()
+    mem_peak = torch.cuda.max_memory_allocated(dev)
     ms = evs[0].elapsed_time(evs[-1])
     per_epoch = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
     launches = ctx.launches() - l0
@@ -519,10 +524,13 @@ def run_grappa(args):
                                         "max": max(per_epoch), "note": "rank-local CUDA events; the "
                                         "epoch holding the repartition is the max"},
                            "l2": "inputs larger than L2 (graph+features ~1.6 GB, activations ~2.8 GB); no flush",
-                           "capacity_mode": bool(args.capacity),
+                           "capacity_mode": args.capacity or False,
                            "sharded_mode": bool(args.sharded),
                            "cuda_graph": bool(use_graph),
-                           "capacity_h2d_bytes_per_epoch": int(sum(tr.img_bytes.values())) if args.capacity else 0,
+                           "capacity_h2d_bytes_per_epoch": (int(sum(tr.img_bytes.values())) if args.capacity == "images"
+                                                            else capacity_shard_bytes(tr) if args.capacity == "shards"
+                                                            else 0),
+                           "device_mem_peak_gb": round(mem_peak / 1e9, 3),
                            "parallelism": f"dp{world} (phase-parallel, gradient-only)",
                            "generate_s": round(t_gen, 1)},
                 "roofline": roofline, "kernels": kernels, "f32": f32,
@@ -536,6 +544,16 @@ def run_grappa(args):
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def capacity_shard_bytes(tr) -> int:
+    """H2D bytes per epoch of capacity mode from chunk shards: both shard images of every phase"""
+    tot = 0
+    for _, w in tr.my_workers():
+        if w < tr.W:
+            b, s = tr.pairs[w]
+            tot += int(tr.shard_imgs[b].numel()) + int(tr.shard_imgs[s].numel())
+    return tot
 
 
 def measure_allreduce(ctx, stream, n_params, world, dist, dev, reps=50):

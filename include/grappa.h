@@ -286,6 +286,32 @@ grappa_status grappa_repartition_shards(grappa_ctx* ctx, const grappa_shard* bas
                                         const int32_t* chunk_of, int64_t num_nodes, int32_t num_chunks,
                                         grappa_part** inout, void* stream);
 
+/* Host images of chunk shards -- the data loader of capacity mode from chunk shards (§8f row 3:
+ * Alg. 1 with M < P beyond HBM; "trades training time for memory capacity" P:395;
+ * partitions in CPU memory loaded onto the GPU P:410; RMAT-36 one partition at a time P:656).
+ * A shard image is one contiguous HOST buffer (caller-owned; pin it for asynchronous loads) with a
+ * 256-byte header and the arrays of grappa_shard_info (ids, rowptr from 0, global col, labels,
+ * train flags, x in the storage dtype), cut out of a HOST copy of the global graph, so the
+ * device never holds the global graph: per phase the two shards of the partition's chunk pair are
+ * loaded (grappa_shard_load) and the partition extracted from them (grappa_repartition_shards),
+ * bitwise the partition grappa_repartition builds.
+ *   grappa_shard_image_size   host rowptr [N+1], chunk map [N]: rows / edges of chunk `chunk` and
+ *                             the image size in bytes.  E_EMPTY for an empty chunk.
+ *   grappa_shard_image_build  write chunk `chunk`'s image (host fp32 feats [N x feat_dim], cast to
+ *                             dtype: bf16 rounds to nearest even; labels may be NULL; `threads` <=
+ *                             0 -> all host cores).  E_ARG if image_bytes is too small.
+ *   grappa_shard_load         (re)allocate *inout (NULL -> new shard) and enqueue the H2D copies of
+ *                             an image on stream; no host sync (the header is read on the host);
+ *                             the image must stay valid until the copies complete. */
+grappa_status grappa_shard_image_size(const int64_t* rowptr, int64_t num_nodes, const int32_t* chunk_of,
+                                      int32_t chunk, int32_t feat_dim, grappa_dtype dtype, int64_t* n_rows,
+                                      int64_t* nnz, size_t* bytes);
+grappa_status grappa_shard_image_build(const int64_t* rowptr, const int32_t* col, int64_t num_nodes,
+                                       const float* feats, int32_t feat_dim, grappa_dtype dtype,
+                                       const int32_t* chunk_of, int32_t chunk, const uint8_t* train_mask,
+                                       const int32_t* labels, void* image, size_t image_bytes, int32_t threads);
+grappa_status grappa_shard_load(grappa_ctx* ctx, const void* image, grappa_shard** inout, void* stream);
+
 /* Host-memory image of a partition's arrays (sizes as in grappa_part_info; any field may be
  * NULL = not transferred).  Used when partitions live in host memory between phases -- the
  * paper keeps partitions in CPU memory and loads them to the GPU; the bench's

@@ -399,6 +399,44 @@ def grappa_shard_extract(ctx: Context, rowptr: torch.Tensor, col: torch.Tensor, 
     return shard.refresh()
 
 
+def _np_ptr(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+def shard_image(rowptr, col, feats, dtype, chunk_of, chunk: int, train_mask, labels, threads: int = 0,
+                pin: bool = True) -> torch.Tensor:
+    """Host image of chunk `chunk`'s shard (grappa_shard_image_size / _build) from HOST numpy
+    arrays (rowptr int64 [N+1], col int32, feats fp32 [N x F_pad] or None, chunk_of int32 [N],
+    train_mask uint8, labels int32 or None), in a pinned uint8 tensor."""
+    import numpy as np
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    chunk_of = np.ascontiguousarray(chunk_of, dtype=np.int32)
+    train_mask = np.ascontiguousarray(train_mask, dtype=np.uint8)
+    labels = None if labels is None else np.ascontiguousarray(labels, dtype=np.int32)
+    feats = None if feats is None else np.ascontiguousarray(feats, dtype=np.float32)
+    N = rowptr.size - 1
+    fdim = 0 if feats is None else feats.shape[1]
+    n, m, nb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_size_t()
+    lib = load()
+    _lib.check("grappa_shard_image_size", lib.grappa_shard_image_size(
+        _np_ptr(rowptr), N, _np_ptr(chunk_of), chunk, fdim, dtype_code(dtype), ctypes.byref(n), ctypes.byref(m),
+        ctypes.byref(nb)))
+    img = torch.empty(nb.value, dtype=torch.uint8, pin_memory=pin)
+    _lib.check("grappa_shard_image_build", lib.grappa_shard_image_build(
+        _np_ptr(rowptr), _np_ptr(col), N, _np_ptr(feats), fdim, dtype_code(dtype), _np_ptr(chunk_of), chunk,
+        _np_ptr(train_mask), _np_ptr(labels), ctypes.c_void_p(img.data_ptr()), nb.value, threads))
+    return img
+
+
+def grappa_shard_load(ctx: Context, image: torch.Tensor, shard: Shard | None = None, stream=None) -> Shard:
+    """enqueue the H2D copies of a shard image into `shard` (new if None); no host sync"""
+    shard = shard or Shard()
+    _lib.check("grappa_shard_load", ctx.lib.grappa_shard_load(
+        ctx.h, ctypes.c_void_p(image.data_ptr()), ctypes.byref(shard.h), _lib.stream_ptr(stream)))
+    return shard.refresh()
+
+
 def grappa_shard_exchange(ctx: Context, sends, recvs, stream=None):
     """sends: [(peer, Shard)], recvs: [(peer, Shard)] (the receiving Shard objects are filled);
     listed in the order both sides agree on (engine.shard_plan)."""

@@ -39,7 +39,8 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_loss_ex", "grappa_shard_extract", "grappa_shard_query", "grappa_shard_destroy",
            "grappa_shard_exchange", "grappa_repartition_shards", "grappa_roofline_probe",
            "grappa_ctx_create_ex", "grappa_comm_bytes", "grappa_repartition_batch",
-           "grappa_index_create", "grappa_index_query", "grappa_index_destroy", "grappa_repartition_batch_ix"]
+           "grappa_index_create", "grappa_index_query", "grappa_index_destroy", "grappa_repartition_batch_ix",
+           "grappa_shard_image_size", "grappa_shard_image_build", "grappa_shard_load"]
 KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5, "sample": 6}
 
 
@@ -156,6 +157,11 @@ def load(path: str = LIB_PATH):
         "grappa_repartition_batch_ix": (st, [vp, ctypes.POINTER(Csr), vp, i32, ctypes.c_int, vp, vp, i32, vp, vp,
                                              vp, vp, vp, vp]),
         "grappa_index_create": (st, [vp, ctypes.POINTER(Csr), vp, i32, ctypes.POINTER(vp), vp]),
+        "grappa_shard_image_size": (st, [vp, i64, vp, i32, i32, ctypes.c_int, ctypes.POINTER(i64),
+                                         ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_size_t)]),
+        "grappa_shard_image_build": (st, [vp, vp, i64, vp, i32, ctypes.c_int, vp, i32, vp, vp, vp, ctypes.c_size_t,
+                                          i32]),
+        "grappa_shard_load": (st, [vp, vp, ctypes.POINTER(vp), vp]),
         "grappa_index_query": (st, [vp, vp, vp]),
         "grappa_index_destroy": (None, [vp]),
         "grappa_comm_bytes": (st, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]),

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import (BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, F32, LAYER_INPUT, LAYER_NODE_LEVEL, Context, Part,
-               Shard, grappa_aggregate_grads, grappa_layer_bwd, grappa_layer_bwd_ex, grappa_layer_fwd_ex,
+               Shard, grappa_aggregate_grads, grappa_shard_load, shard_image, grappa_layer_bwd, grappa_layer_bwd_ex, grappa_layer_fwd_ex,
                Index, grappa_loss, grappa_partition, grappa_repartition, grappa_repartition_batch, grappa_repartition_shards,
                grappa_shard_exchange, grappa_shard_extract, layer_saved_bytes, layer_ws_bytes)
 
@@ -147,11 +147,19 @@ class Trainer:
         self.halo = halo                 # halo-1 partitions (R33) instead of induced-core
         # capacity mode (Alg. 1 with M < P beyond HBM): partitions live as images in
         # pinned host memory and are streamed into one of two device slots per phase
+        # capacity="shards": the global graph never reaches the device -- every chunk's shard is
+        # an image in pinned host memory, and each phase loads its pair's two shards and extracts
+        # the partition from them on the device (device memory O(two chunks + one partition))
         self.capacity = capacity
+        self.cap_shards = capacity == "shards"
+        if capacity not in (False, True, "shards"):
+            raise ValueError("capacity must be False, True (partition images) or 'shards' (chunk-shard images)")
         # sharded mode (a3 (i)): keep only the owned chunk shards, exchange swept shards at switches
         self.sharded = sharded
         if sharded and (halo or capacity):
             raise ValueError("sharded mode builds induced-core partitions held in HBM (no halo / capacity)")
+        if self.cap_shards and halo:
+            raise ValueError("capacity mode from chunk shards builds induced-core partitions")
         self.host_imgs: dict = {}
         self.img_bytes: dict = {}
         self.cap_slots = None
@@ -161,6 +169,10 @@ class Trainer:
         self.tdt = torch.bfloat16 if self.dt == BF16 else torch.float32
         self.schedule = sweep_schedule(self.C, self.W)
         as_t = lambda a, dt: (a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))).to(self.dev, dt)
+        if self.cap_shards:
+            self._init_shard_images(ctx, rowptr, col, x, labels, train_mask, chunk_seed)
+            self._init_params(spec, weights)
+            return
         # replicated global graph + node data, resident in HBM for the whole run
         self.rowptr = as_t(rowptr, torch.int64)
         self.col = as_t(col, torch.int32)
@@ -183,6 +195,29 @@ class Trainer:
                            for c in range(self.C) if shard_owner(c, self.G) == self.rank}
             self.recv_slots = [Shard(), Shard()]
             self.rowptr = self.col = self.x = self.labels = self.train = None
+        self._init_params(spec, weights)
+
+    def _init_shard_images(self, ctx, rowptr, col, x, labels, train_mask, chunk_seed):
+        """capacity mode from chunk shards: the chunk map on the device (a1), every chunk's shard
+        cut out of the HOST graph into a pinned image (grappa_shard_image_build); no global array
+        is copied to the device"""
+        host = lambda a, dt: (a.cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)).astype(dt, copy=False)
+        rowptr, col = host(rowptr, np.int64), host(col, np.int32)
+        self.N = rowptr.size - 1
+        self.nnz_global = int(col.size)
+        self.chunk_of = torch.empty(self.N, dtype=torch.int32, device=self.dev)
+        self.chunk_sizes = grappa_partition(ctx, self.N, self.C, chunk_seed, self.chunk_of, self.stream)
+        cmap = self.chunk_of.cpu().numpy()
+        xf = host(x, np.float32)
+        self.shard_imgs = [shard_image(rowptr, col, xf, self.dt, cmap, c, host(train_mask, np.uint8),
+                                       host(labels, np.int32)) for c in range(self.C)]
+        self.shard_img_bytes = sum(int(im.numel()) for im in self.shard_imgs)
+        self.rowptr = self.col = self.x = self.labels = self.train = None
+        self.sh_slots = [[Shard(), Shard()], [Shard(), Shard()]]
+        self.cap_part = Part()
+        self.cap_stream = torch.cuda.Stream(self.dev)
+
+    def _init_params(self, spec, weights):
         # theta / grad: one flat fp32 buffer each -> one all-reduce per iteration
         shapes = spec.layer_shapes()
         self.theta = torch.zeros(spec.n_params(), dtype=torch.float32, device=self.dev)
@@ -226,6 +261,10 @@ class Trainer:
             # super-epoch now (the device skipped those updates)
             self.check()
         pairs = self.schedule[(t - 1) % len(self.schedule)]
+        if self.cap_shards:              # partitions are extracted per phase (_run_epoch_shards)
+            self.pairs = pairs
+            self.t = t
+            return None
         if self.capacity:
             return self._repartition_to_host(t, pairs)
         if self.sharded:
@@ -417,6 +456,8 @@ class Trainer:
         t = self.super_epoch()
         if t != self.t:
             self.repartition(t)
+        if self.cap_shards:
+            return self._run_epoch_shards(on_phase)
         if self.capacity:
             return self._run_epoch_capacity(on_phase)
         for i, w in self.my_workers():
@@ -456,6 +497,49 @@ class Trainer:
             self.phase_step(i, w, m_active)
             free[k % 2] = torch.cuda.Event()
             free[k % 2].record(self.stream)
+            if on_phase is not None:
+                on_phase()
+            ready = nxt
+        self.end_epoch()
+
+    def _run_epoch_shards(self, on_phase=None):
+        """capacity mode from chunk shards: phase k's two shard images are copied H2D into shard
+        slot k % 2 on a copy stream while phase k-1 computes; the phase then extracts its
+        partition from them on the device (grappa_repartition_shards: bitwise the resident
+        partition) into the single partition slot and trains on it"""
+        plan = self.my_workers()
+        extracted = [None, None]                  # slot's previous shards consumed by their extraction
+
+        def load(k):
+            _, w = plan[k]
+            if w >= self.W:
+                return None
+            if extracted[k % 2] is not None:
+                self.cap_stream.wait_event(extracted[k % 2])
+            b, s_ = self.pairs[w]
+            A, B = self.sh_slots[k % 2]
+            grappa_shard_load(self.ctx, self.shard_imgs[b], A, self.cap_stream)
+            grappa_shard_load(self.ctx, self.shard_imgs[s_], B, self.cap_stream)
+            ev = torch.cuda.Event()
+            ev.record(self.cap_stream)
+            return ev
+
+        self.cap_stream.wait_stream(self.stream)
+        ready = load(0) if plan else None
+        for k, (i, w) in enumerate(plan):
+            nxt = load(k + 1) if k + 1 < len(plan) else None
+            if ready is not None:
+                self.stream.wait_event(ready)
+                A, B = self.sh_slots[k % 2]
+                part = grappa_repartition_shards(self.ctx, A, B, self.chunk_of, self.C, self.cap_part, self.stream)
+                extracted[k % 2] = torch.cuda.Event()
+                extracted[k % 2].record(self.stream)
+                self.parts = {w: part}
+                self._alloc([self._sizes(part)])
+            else:
+                self.parts = {}
+            m_active = min(self.G, self.W - i * self.G)
+            self.phase_step(i, w, m_active)
             if on_phase is not None:
                 on_phase()
             ready = nxt

@@ -1,7 +1,9 @@
 """Capacity mode (Alg. 1 with partitions streamed from host memory, P:395,
 P:139): partition images round-trip bit-exactly (grappa_part_save / grappa_part_load),
 and an epoch that streams every phase's partition from pinned host memory into two device slots
-reproduces the resident-partition epoch bit for bit (same kernels, same inputs, same order)."""
+reproduces the resident-partition epoch bit for bit (same kernels, same inputs, same order); so does
+capacity mode from chunk shards (host shard images, partitions extracted per phase on the device).
+"""
 import pytest
 import torch
 
@@ -52,8 +54,11 @@ def test_image_roundtrip(G, prod, halo):
     ctx.close()
 
 
-@pytest.mark.parametrize("halo,dtype", [(False, "bf16"), (True, "f32")])
-def test_capacity_epoch_equals_resident(G, prod, halo, dtype):
+@pytest.mark.parametrize("halo,dtype,cap", [(False, "bf16", True), (True, "f32", True),
+                                            (False, "bf16", "shards"), (False, "f32", "shards")])
+def test_capacity_epoch_equals_resident(G, prod, halo, dtype, cap):
+    """cap=True: partition images; cap="shards": chunk-shard images in host memory, the partition
+    extracted per phase from its pair's two shards (the device never holds the global graph)"""
     from paper_2602_01872_b200.engine import ModelSpec, Trainer
     ctx = G.Context(0)
     ds = prod
@@ -62,7 +67,9 @@ def test_capacity_epoch_equals_resident(G, prod, halo, dtype):
     mk = lambda cap: Trainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights, wl.chunks,
                              gen.seed_of("chunks"), corr="uniform", lr=0.05, repartition_every=1,
                              dtype=dtype, halo=halo, capacity=cap)
-    a, b = mk(False), mk(True)
+    a, b = mk(False), mk(cap)
+    if cap == "shards":
+        assert b.rowptr is None and b.col is None and b.x is None       # no global array on the device
     for _ in range(2):                       # two super-epochs (repartition every epoch)
         a.run_epoch()
         b.run_epoch()

@@ -269,7 +269,9 @@ def _logical(trainer, flat):
                                                             ("arxiv", "resampling", 1, 10, False),
                                                             ("arxiv", "none", 2, 1, False),
                                                             ("prod", "uniform", 2, 1, True),
-                                                            ("arxiv", "resampling_hm", 1, 10, True)])
+                                                            ("arxiv", "resampling_hm", 1, 10, True),
+                                                            ("prod", "uniform", 2, 1, "shards"),
+                                                            ("arxiv", "resampling", 1, 10, "shards")])
 def test_epoch_parity(G, ctx, prod, arxiv, which, corr, epochs, rep, capacity):
     """Alg. 1 end to end on 1 GPU (P = 8 partitions, M = 1 per phase): theta after the run
     matches the oracle's phase loop.  lr is raised so the update is visible next to theta.
