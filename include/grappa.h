@@ -286,6 +286,29 @@ grappa_status grappa_repartition_shards(grappa_ctx* ctx, const grappa_shard* bas
                                         const int32_t* chunk_of, int64_t num_nodes, int32_t num_chunks,
                                         grappa_part** inout, void* stream);
 
+/* a3 from two shards with flags: 0 is grappa_repartition_shards; GRAPPA_PART_HALO1 builds the
+ * halo-1 partition (R33/R34) whose core part is complete but whose halo rows (features, global
+ * degree, label, node weight) are PENDING: they live in other chunks' shards and arrive with
+ * grappa_halo_exchange (layer calls reject a pending partition with E_ARG). */
+grappa_status grappa_repartition_shards_ex(grappa_ctx* ctx, const grappa_shard* base, const grappa_shard* swept,
+                                           const int32_t* chunk_of, int64_t num_nodes, int32_t num_chunks,
+                                           unsigned flags, grappa_part** inout, void* stream);
+/* Halo feature all-to-all of sharded halo-1 partitions ("Halo node features are pre-cached at
+ * super-epoch boundaries", "synchronize halo features", "Feature gathering during
+ * repartitioning uses all-to-all collectives").  COLLECTIVE over the ctx's communicator: every rank
+ * calls it once per partition build, in the same order; part = this rank's pending partition or
+ * NULL (a rank without one still answers requests).  shards: the n_shards chunk shards this rank
+ * owns (host array of handles); chunk_owner: host int32[C], the rank owning each chunk's shard;
+ * chunk_of: dev [N].  Rounds: per-owner request counts (one host sync), an ok word from every rank
+ * (both sides agree before any array moves), request ids (int32, ascending per owner), replies
+ * (feature row in the storage dtype, global degree, label per request) -- counted in
+ * grappa_comm_bytes' `other`.  Afterwards the partition is bitwise the replicated path's halo-1
+ * partition.  Errors: E_ARG (no communicator, C > 64, bad owner, a shard this rank does not own,
+ * mismatched feature format, a requested node absent from its owner's shards), E_NOMEM, E_NCCL. */
+grappa_status grappa_halo_exchange(grappa_ctx* ctx, grappa_part* part, int32_t n_shards,
+                                   const grappa_shard* const* shards, const int32_t* chunk_owner,
+                                   const int32_t* chunk_of, int32_t num_chunks, void* stream);
+
 /* Host images of chunk shards -- the data loader of capacity mode from chunk shards (§8f row 3:
  * Alg. 1 with M < P beyond HBM; "trades training time for memory capacity" P:395;
  * partitions in CPU memory loaded onto the GPU P:410; RMAT-36 one partition at a time P:656).

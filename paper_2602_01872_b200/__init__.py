@@ -456,12 +456,27 @@ def grappa_shard_exchange(ctx: Context, sends, recvs, stream=None):
 
 
 def grappa_repartition_shards(ctx: Context, base: Shard, swept: Shard, chunk_of: torch.Tensor, num_chunks: int,
-                              part: Part | None = None, stream=None) -> Part:
+                              part: Part | None = None, stream=None, halo: bool = False) -> Part:
+    """halo=True: a halo-1 partition whose halo rows are pending until grappa_halo_exchange"""
     part = part or Part()
-    _lib.check("grappa_repartition_shards", ctx.lib.grappa_repartition_shards(
-        ctx.h, base.h, swept.h, _lib.ptr(chunk_of), chunk_of.numel(), num_chunks, ctypes.byref(part.h),
-        _lib.stream_ptr(stream)))
+    _lib.check("grappa_repartition_shards_ex", ctx.lib.grappa_repartition_shards_ex(
+        ctx.h, base.h, swept.h, _lib.ptr(chunk_of), chunk_of.numel(), num_chunks, _lib.PART_HALO1 if halo else 0,
+        ctypes.byref(part.h), _lib.stream_ptr(stream)))
     return part.refresh()
+
+
+def grappa_halo_exchange(ctx: Context, part: Part | None, shards, chunk_owner, chunk_of: torch.Tensor,
+                         num_chunks: int, stream=None):
+    """collective halo feature all-to-all (every rank, once per partition build); shards: the Shard
+    objects this rank owns; chunk_owner: rank of each chunk's shard"""
+    hs = (ctypes.c_void_p * max(1, len(shards)))(*[sh.h.value for sh in shards])
+    own = (ctypes.c_int32 * num_chunks)(*[int(o) for o in chunk_owner])
+    _lib.check("grappa_halo_exchange", ctx.lib.grappa_halo_exchange(
+        ctx.h, part.h if part is not None else None, len(shards), ctypes.cast(hs, ctypes.c_void_p), own,
+        _lib.ptr(chunk_of), num_chunks, _lib.stream_ptr(stream)))
+    if part is not None:
+        part.refresh()
+    return part
 
 
 def layer_saved_bytes(part: Part, arch, f_in, f_out, dtype, flags: int = 0) -> int:

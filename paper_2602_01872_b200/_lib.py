@@ -40,7 +40,8 @@ SYMBOLS = ["grappa_version", "grappa_last_error", "grappa_nccl_unique_id", "grap
            "grappa_shard_exchange", "grappa_repartition_shards", "grappa_roofline_probe",
            "grappa_ctx_create_ex", "grappa_comm_bytes", "grappa_repartition_batch",
            "grappa_index_create", "grappa_index_query", "grappa_index_destroy", "grappa_repartition_batch_ix",
-           "grappa_shard_image_size", "grappa_shard_image_build", "grappa_shard_load"]
+           "grappa_shard_image_size", "grappa_shard_image_build", "grappa_shard_load",
+           "grappa_repartition_shards_ex", "grappa_halo_exchange"]
 KCLASS = {"spmm": 0, "gemm": 1, "gemm_tn": 2, "loss": 3, "agg": 4, "repart": 5, "sample": 6}
 
 
@@ -162,6 +163,8 @@ def load(path: str = LIB_PATH):
         "grappa_shard_image_build": (st, [vp, vp, i64, vp, i32, ctypes.c_int, vp, i32, vp, vp, vp, ctypes.c_size_t,
                                           i32]),
         "grappa_shard_load": (st, [vp, vp, ctypes.POINTER(vp), vp]),
+        "grappa_repartition_shards_ex": (st, [vp, vp, vp, vp, i64, i32, ctypes.c_uint, ctypes.POINTER(vp), vp]),
+        "grappa_halo_exchange": (st, [vp, vp, i32, vp, vp, vp, i32, vp]),
         "grappa_index_query": (st, [vp, vp, vp]),
         "grappa_index_destroy": (None, [vp]),
         "grappa_comm_bytes": (st, [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]),

@@ -323,6 +323,8 @@ extern "C" grappa_status grappa_layer_fwd_ex(grappa_ctx* ctx, const grappa_part*
     GRAPPA_ARG(arch != GRAPPA_GCN || !(flags & GRAPPA_LAYER_INPUT) || saved, GRAPPA_E_ARG,
                "grappa_layer_fwd_ex: GRAPPA_LAYER_INPUT (GCN) needs `saved` (grappa_layer_saved_bytes_ex)");
     GRAPPA_ARG(ctx && part && h_in && w && h_out && ws, GRAPPA_E_ARG, "grappa_layer_fwd: null argument");
+    GRAPPA_ARG(!part->halo_pending, GRAPPA_E_ARG,
+               "grappa_layer_fwd: the partition's halo rows are pending (grappa_halo_exchange first)");
     GRAPPA_TRY(check_dims("grappa_layer_fwd", f_in, f_out));
     GRAPPA_ARG(arch == GRAPPA_GCN || saved, GRAPPA_E_ARG, "grappa_layer_fwd: SAGE / GAT need `saved`");
     GRAPPA_ARG(arch == GRAPPA_GCN || arch == GRAPPA_SAGE || arch == GRAPPA_GAT, GRAPPA_E_ARG,

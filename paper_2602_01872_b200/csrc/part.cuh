@@ -70,6 +70,9 @@ struct grappa_part {
     // on its transpose, with the same SpMM plan structures (split rows, order, descriptors)
     bool halo = false;
     int64_t n_halo = 0;
+    // sharded halo-1 partition whose halo rows (features, global degree, label, node weight)
+    // still have to arrive from their chunks' owners (grappa_halo_exchange)
+    bool halo_pending = false;
     grappa::DevBuf t_rowptr, t_col, t_deg, t_heavy_rows, t_heavy_slot_off, t_slot_row, t_slot_seg,
         t_row_order, t_row_desc, t_tmp;
     int64_t t_n_heavy = 0, t_n_slots = 0;

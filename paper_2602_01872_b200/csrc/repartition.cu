@@ -97,6 +97,17 @@ __global__ void k_mark_halo(const int64_t* __restrict__ d_ncore, const int32_t* 
         }
     }
 }
+// the same marking over an explicit CSR with global neighbour ids (a chunk shard: sharded mode)
+__global__ void k_mark_halo_rows(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                 const int32_t* __restrict__ rank, uint8_t* __restrict__ flag) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps)
+        for (int64_t e = rp[i] + lane; e < rp[i + 1]; e += 32) {
+            const int32_t u = col[e];
+            if (rank[u] < 0) flag[u] = 1;
+        }
+}
 struct FlagHalo {
     const uint8_t* flag;
     __device__ int32_t operator()(int64_t v) const { return flag[v]; }
@@ -121,7 +132,9 @@ __global__ void k_halo_rows(int64_t n_core, int64_t n_local, const int64_t* __re
     for (int64_t i = n_core + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_local;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = core_global ? core_global[i] : (int32_t)i;
-        const int32_t dg = (int32_t)(g_rowptr[v + 1] - g_rowptr[v]);
+        // sharded mode: the halo node's global degree and label arrive with its features
+        // (grappa_halo_exchange); placeholders until then
+        const int32_t dg = g_rowptr ? (int32_t)(g_rowptr[v + 1] - g_rowptr[v]) : 0;
         rowptr[i + 1] = nnz;
         d_l[i] = 0;
         d_g[i] = dg;
@@ -706,9 +719,17 @@ static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const voi
     if (halo) {
         // 1b. halo = non-core neighbours of core rows; they extend the rank table after the core
         GRAPPA_CUDA(cudaMemsetAsync(hflag, 0, (size_t)N, s));
-        k_mark_halo<<<(unsigned)ctx->sm_count * 16, 256, 0, s>>>(d_stat, (int32_t*)p->core_global.p,
-                                                                  g->rowptr, g->col, rank, hflag);
-        GRAPPA_LAUNCHED(ctx);
+        if (sa) {        // the two shards' rows carry the core rows' global adjacency
+            for (const grappa_shard* sh : {sa, sb}) {
+                k_mark_halo_rows<<<(unsigned)ctx->sm_count * 16, 256, 0, s>>>(sh->info.n_rows, sh->info.rowptr,
+                                                                               sh->info.col, rank, hflag);
+                GRAPPA_LAUNCHED(ctx);
+            }
+        } else {
+            k_mark_halo<<<(unsigned)ctx->sm_count * 16, 256, 0, s>>>(d_stat, (int32_t*)p->core_global.p,
+                                                                      g->rowptr, g->col, rank, hflag);
+            GRAPPA_LAUNCHED(ctx);
+        }
         RP_TRY(device_scan(ctx, FlagHalo{hflag}, N, WriteHaloRank{rank, (int32_t*)p->core_global.p, d_stat}, s));
     } else {
         GRAPPA_CUDA(cudaMemsetAsync(d_stat + 6, 0, 8, s));
@@ -743,7 +764,7 @@ static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const voi
         int32_t* m_col = (int32_t*)w; w += a_col;
         int32_t* m_lab = (int32_t*)w; w += a_lab;
         uint8_t* m_tr = (uint8_t*)w;
-        if (feats) RP_TRY(p->x.grow((size_t)n_core * feat_dim * esz));
+        if (feats) RP_TRY(p->x.grow((size_t)n_local * feat_dim * esz));   // halo rows: grappa_halo_exchange
         RP_TRY(shard_merge(ctx, sa, sb, rank, n_core, m_src, m_deg, m_rowptr, m_col, m_lab, m_tr,
                            feats ? p->x.p : nullptr, feat_dim * esz, d_stat, s));
         srow = nullptr;
@@ -851,6 +872,7 @@ static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const voi
     // sources in ascending local id (deterministic).
     p->halo = halo;
     p->n_halo = n_halo;
+    p->halo_pending = halo && sa && n_halo > 0;   // halo features / degrees / labels: grappa_halo_exchange
     p->t_n_heavy = p->t_n_slots = 0;
     p->t_eid_ready = halo;            // induced-core: built lazily by the first GAT backward
     p->tma.ready = p->t_tma.ready = false;   // TMA SpMM plans: rebuilt on first use
@@ -945,6 +967,13 @@ extern "C" grappa_status grappa_repartition_shards(grappa_ctx* ctx, const grappa
                                                    const grappa_shard* swept, const int32_t* chunk_of,
                                                    int64_t num_nodes, int32_t num_chunks, grappa_part** inout,
                                                    void* stream) {
+    return grappa_repartition_shards_ex(ctx, base, swept, chunk_of, num_nodes, num_chunks, 0u, inout, stream);
+}
+
+extern "C" grappa_status grappa_repartition_shards_ex(grappa_ctx* ctx, const grappa_shard* base,
+                                                      const grappa_shard* swept, const int32_t* chunk_of,
+                                                      int64_t num_nodes, int32_t num_chunks, unsigned flags,
+                                                      grappa_part** inout, void* stream) {
     CallScope call_scope(ctx, stream);
     GRAPPA_ARG(ctx && base && swept && chunk_of && inout, GRAPPA_E_ARG,
                "grappa_repartition_shards: null argument");
@@ -956,7 +985,7 @@ extern "C" grappa_status grappa_repartition_shards(grappa_ctx* ctx, const grappa
     // only num_nodes is read from the CSR descriptor in sharded mode (rank table over N)
     grappa_csr gn{num_nodes, 0, nullptr, nullptr};
     return repart_impl(ctx, &gn, A.feat_dim ? (const void*)A.x : nullptr, A.feat_dim, A.dtype, chunk_of,
-                       num_chunks, A.chunk, B.chunk, A.train, A.labels, 0u, base, swept, inout,
+                       num_chunks, A.chunk, B.chunk, A.train, A.labels, flags, base, swept, inout,
                        (cudaStream_t)stream);
 }
 
@@ -1298,6 +1327,7 @@ extern "C" grappa_status grappa_repartition_batch_ix(grappa_ctx* ctx, const grap
                                 d_stat0 + (size_t)k * kSt + 8, n_heavy, n_slots));
         p->halo = false;
         p->n_halo = 0;
+        p->halo_pending = false;
         p->t_n_heavy = p->t_n_slots = 0;
         p->t_eid_ready = false;
         p->tma.ready = p->t_tma.ready = false;
@@ -1482,6 +1512,7 @@ extern "C" grappa_status grappa_part_load(grappa_part** inout, const void* host,
         GRAPPA_CUDA(cudaMemcpyAsync(a[i].buf->p, (const char*)host + h.off[i], a[i].bytes, cudaMemcpyHostToDevice, s));
     }
     p->halo = h.halo != 0;
+    p->halo_pending = false;
     p->n_halo = h.n_halo; p->t_n_heavy = h.t_n_heavy; p->t_n_slots = h.t_n_slots;
     p->t_eid_ready = p->halo;
     p->tma.ready = p->t_tma.ready = false;

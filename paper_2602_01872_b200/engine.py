@@ -24,7 +24,7 @@ import torch
 from . import (BF16, BWD_DZ_IN_NORMED, BWD_DZ_OUT_NORMED, F32, LAYER_INPUT, LAYER_NODE_LEVEL, Context, Part,
                Shard, grappa_aggregate_grads, grappa_shard_load, shard_image, grappa_layer_bwd, grappa_layer_bwd_ex, grappa_layer_fwd_ex,
                Index, grappa_loss, grappa_partition, grappa_repartition, grappa_repartition_batch, grappa_repartition_shards,
-               grappa_shard_exchange, grappa_shard_extract, layer_saved_bytes, layer_ws_bytes)
+               grappa_halo_exchange, grappa_shard_exchange, grappa_shard_extract, layer_saved_bytes, layer_ws_bytes)
 
 
 def sweep_schedule(C: int, W: int):
@@ -156,8 +156,8 @@ class Trainer:
             raise ValueError("capacity must be False, True (partition images) or 'shards' (chunk-shard images)")
         # sharded mode (a3 (i)): keep only the owned chunk shards, exchange swept shards at switches
         self.sharded = sharded
-        if sharded and (halo or capacity):
-            raise ValueError("sharded mode builds induced-core partitions held in HBM (no halo / capacity)")
+        if sharded and capacity:
+            raise ValueError("sharded mode holds its partitions in HBM (no capacity mode)")
         if self.cap_shards and halo:
             raise ValueError("capacity mode from chunk shards builds induced-core partitions")
         self.host_imgs: dict = {}
@@ -194,6 +194,7 @@ class Trainer:
                                                    self.C, c, self.train, self.labels, None, self.stream)
                            for c in range(self.C) if shard_owner(c, self.G) == self.rank}
             self.recv_slots = [Shard(), Shard()]
+            self.owners = [shard_owner(c, self.G) for c in range(self.C)]
             self.rowptr = self.col = self.x = self.labels = self.train = None
         self._init_params(spec, weights)
 
@@ -304,12 +305,20 @@ class Trainer:
             if sends or recvs:
                 grappa_shard_exchange(self.ctx, sends, recvs, self.stream)
             if w >= self.W:
+                if self.halo:            # collective: an idle rank still answers halo requests
+                    grappa_halo_exchange(self.ctx, None, list(self.shards.values()), self.owners, self.chunk_of,
+                                         self.C, self.stream)
                 continue
             b, s = pairs[w]
             sb = self.shards.get(b) or got[b]
             ss = self.shards.get(s) or got[s]
             self.parts[w] = grappa_repartition_shards(self.ctx, sb, ss, self.chunk_of, self.C, self.parts.get(w),
-                                                      self.stream)
+                                                      self.stream, halo=self.halo)
+            if self.halo:
+                # halo-1 (R33): the halo rows' features, degrees and labels from their chunks'
+                # owners -- the all-to-all of P:416, at the switch only
+                grappa_halo_exchange(self.ctx, self.parts[w], list(self.shards.values()), self.owners,
+                                     self.chunk_of, self.C, self.stream)
         self.t = t
         self._alloc()
 

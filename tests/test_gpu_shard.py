@@ -158,3 +158,71 @@ def test_sharded_training_equals_replicated(G, prod, dtype):
     assert torch.equal(a.theta, b.theta)
     assert a.losses == b.losses
     ctx.close()
+
+
+@pytest.mark.parametrize("dtype,nccl", [("f32", True), ("bf16", True), ("bf16", False)])
+def test_sharded_halo_partition_bitexact(G, prod, dtype, nccl):
+    """§8f row 2 in sharded mode: a halo-1 partition built from its pair's two
+    shards is pending until grappa_halo_exchange ships the halo rows' features, global degrees and
+    labels from their chunks' owners (here a 1-rank communicator's self transfers, or the local
+    path without one); afterwards it is bitwise the replicated halo-1 partition and the oracle's
+    halo sets and CSR"""
+    uid = G.Context.nccl_unique_id() if nccl else None
+    ctx = G.Context(0, rank=0, nranks=1, nccl_uid=uid) if nccl else G.Context(0)
+    ds = prod
+    C = 8
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    rp, col, x, y, tr = upload(ds, tdt)
+    ch, sh = shards_of(G, ctx, ds, C, dtype)
+    chunk_of = Po.make_chunks(ds.wl.n, C, gen.seed_of("chunks"))
+    for b, s in [(0, 3), (5, 2)]:
+        p = G.grappa_repartition_shards(ctx, sh[b], sh[s], ch, C, halo=True)
+        assert p.n_halo > 0
+        with pytest.raises(G.GrappaError, match="pending"):
+            h = torch.zeros(p.n_core, 16, device="cuda")
+            ws = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+            G.grappa_layer_fwd_ex(ctx, p, "gcn", 16, 16, True, h, torch.zeros(16, 16, device="cuda"), h.clone(),
+                                  None, ws, "f32", 0)
+        G.grappa_halo_exchange(ctx, p, [sh[c] for c in range(C)], [0] * C, ch, C)
+        one = G.grappa_repartition(ctx, rp, col, x, dtype, ch, C, b, s, tr, y, halo=True)
+        torch.cuda.synchronize()
+        for k in ("rowptr", "col", "core_global", "d_l", "d_g", "norm_gcn", "norm_sage", "seeds", "labels",
+                  "node_w", "t_rowptr", "t_col"):
+            assert torch.equal(getattr(p, k), getattr(one, k)), k
+        assert torch.equal(p.x.view(torch.int16) if dtype == "bf16" else p.x,
+                           one.x.view(torch.int16) if dtype == "bf16" else one.x)
+        ref = Po.induced_partition(ds.rowptr, ds.col, chunk_of, b, s, ds.train, halo=True)
+        assert np.array_equal(p.core_global.cpu().numpy(), ref["core"])
+        assert np.array_equal(p.col.cpu().numpy(), ref["col"])
+        assert np.array_equal(p.d_g.cpu().numpy(), ref["d_g"])
+    if nccl:
+        # a shard this rank does not own is refused before anything moves
+        q = G.grappa_repartition_shards(ctx, sh[0], sh[1], ch, C, halo=True)
+        with pytest.raises(G.GrappaError, match="E_ARG"):
+            G.grappa_halo_exchange(ctx, q, [sh[2]], [0, 0, 1] + [0] * (C - 3), ch, C)
+    ctx.check()
+    ctx.close()
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_sharded_halo_training_equals_replicated(G, prod, dtype):
+    """sharded halo-1 training (owned shards only; halo features exchanged at every switch)
+    reproduces the replicated halo-1 trainer's theta bit for bit over two switches"""
+    from paper_2602_01872_b200.engine import ModelSpec, Trainer
+    ctx = G.Context(0)
+    ds = prod
+    wl = ds.wl
+    spec = ModelSpec(wl.arch, wl.dims, wl.dims_pad)
+    mk = lambda sharded: Trainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights, wl.chunks,
+                                 gen.seed_of("chunks"), corr="uniform", lr=0.05, repartition_every=1,
+                                 dtype=dtype, sharded=sharded, halo=True)
+    a, b = mk(False), mk(True)
+    assert b.rowptr is None
+    for _ in range(2):
+        a.run_epoch()
+        b.run_epoch()
+    torch.cuda.synchronize()
+    ctx.check()
+    assert torch.equal(a.theta, b.theta)
+    assert a.losses == b.losses
+    ctx.close()
