@@ -90,11 +90,18 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def mark(self):
+        """start of the timed region: the sampler is started well before it (nvidia-smi's own
+        start-up takes the driver for a while and must not overlap timed epochs), and only the
+        samples taken between mark() and stop() are reported"""
+        self.t0 = time.monotonic()
 
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t1 = time.monotonic()
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -103,7 +110,9 @@ class ClockSampler:
         self.t.join(timeout=2)
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0 = getattr(self, "t0", None)
+        inside = [ln for t, ln in self.lines if t0 is None or t0 <= t <= t1 + 0.15]
+        for ln in inside or [ln for _, ln in self.lines[-3:]]:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -353,7 +362,7 @@ def run_grappa(args):
     full_graph = not isinstance(tr, MinibatchTrainer)
     # the fp32 arm accompanies the headline configuration only (replicated, induced-core, resident)
     keep_ds = ds if (args.dtype == "bf16" and full_graph and not args.no_f32 and not args.capacity
-                     and not args.sharded and not args.halo) else None
+                     and not args.sharded and not args.halo and args.config == "products") else None
     del ds
 
     def barrier():
@@ -361,14 +370,15 @@ def run_grappa(args):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
+    clocks = ClockSampler(local)         # started before the warm-up (see ClockSampler.mark)
+    clocks.start()
     for _ in range(args.warmup):
         tr.run_epoch()
     ctx.check(stream)
     # timed region starts on a super-epoch boundary -> includes ceil(K/N) repartitions
     tr.epoch = wl.repartition_every * (1 + tr.epoch // wl.repartition_every)
     barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks.mark()
     # CUDA-graph replay of the epoch (one capture per super-epoch): the default on one GPU for
     # full-graph runs (~535 launches per products epoch; replay removes the host launch gaps);
     # multi-GPU runs replay only with --graph (the all-reduce would be captured too)

@@ -193,6 +193,7 @@ extern "C" void grappa_ctx_destroy(grappa_ctx* c) {
     c->sh_ws.release();
     c->xf_hdr.release();
     c->comm_buf.release();
+    c->wimg.release();
     for (auto& r : c->prof) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);

@@ -112,6 +112,7 @@ struct grappa_ctx {
     void* h_pinned = nullptr;    // pinned host staging (64 KB)
     std::shared_ptr<const grappa::Allocator> alloc;   // caller allocator (null: cudaMalloc)
     grappa::DevBuf comm_buf;     // bf16 communication buffer of grappa_aggregate_grads
+    grappa::DevBuf wimg;         // streamed-weight image of the tcgen05 NN GEMM (large K)
     // test / A-B kernel selection (grappa_set_kernel_variant): gemm 0 = tensor cores, 1/2 = CUDA
     // cores; spmm 0 = row-group, 1 = warp per row, 2 = 8 loads in flight, 3 = natural row order;
     // pair 1 = separate GCN backward GEMMs

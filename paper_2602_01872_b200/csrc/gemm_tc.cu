@@ -51,6 +51,11 @@ struct TcNN {
     int mask_tma;          // relu'-gate boxes TMA-staged one tile ahead (else register prefetch)
     int nsb;               // staging boxes per epilogue group (1 or 2)
     uint32_t tmem_cols;
+    // weights too large to stay resident (K x N bf16 > the shared memory left by the ring, e.g.
+    // cora's K = 1440 input layer): the weight k-block travels with each A tile instead, from a
+    // global image already in the SW128 K-major layout (k_weight_image), by a plain bulk copy
+    int b_stream;
+    const uint8_t* bimg;
 };
 
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int x, int y) {
@@ -101,6 +106,40 @@ __device__ __forceinline__ void stage_weights(uint8_t* sB, uint8_t* sBlo, const 
         *reinterpret_cast<uint4*>(sB + off) = make_uint4(h[0], h[1], h[2], h[3]);
         if (sBlo) *reinterpret_cast<uint4*>(sBlo + off) = make_uint4(l[0], l[1], l[2], l[3]);
     }
+}
+
+// the same bf16 K-major SWIZZLE_128B image stage_weights writes to shared memory, written to global
+// memory once per call: k-block kb at byte kb * N * 128 (a multiple of 1024, so the swizzle of the
+// image equals the swizzle of a 1024-aligned shared-memory copy of it)
+__global__ void k_weight_image(const float* __restrict__ B, int K1, int K2, int N, int kb1, int kbt, int b_trans,
+                               uint8_t* __restrict__ img) {
+    const int Kt = K1 + K2;
+    const int total = kbt * 8 * N;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+        const int n = idx % N, kc = idx / N;
+        const int kb = kc >> 3, c8 = kc & 7;
+        int k0, kend;
+        if (kb < kb1) { k0 = kb * 64 + c8 * 8; kend = K1; }
+        else { k0 = K1 + (kb - kb1) * 64 + c8 * 8; kend = Kt; }
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const int k = k0 + j;
+            v[j] = k < kend ? __ldg(b_trans ? B + (int64_t)n * Kt + k : B + (int64_t)k * N + n) : 0.f;
+        }
+        uint32_t h[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const __nv_bfloat162 bh = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+            h[j] = *reinterpret_cast<const uint32_t*>(&bh);
+        }
+        *reinterpret_cast<uint4*>(img + (size_t)kb * N * 128 + tc::sw128_off(n, c8)) = make_uint4(h[0], h[1], h[2], h[3]);
+    }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(tc::smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(tc::smem_u32(bar))
+                 : "memory");
 }
 
 __device__ __forceinline__ void bulk_wait_read1() {
@@ -209,9 +248,11 @@ __global__ void __launch_bounds__(kNNThreads, 1)
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const int kbt = p.kb1 + p.kb2;
     const int stages = p.stages;
+    const uint32_t stB = p.b_stream ? (uint32_t)p.N * 128 : 0u;   // streamed weight k-block per stage
+    const uint32_t st_bytes = kNNStageBytes + stB;
     uint8_t* sA = smem;
-    uint8_t* sB = sA + stages * kNNStageBytes;
-    uint8_t* sOut = sB + (size_t)kbt * p.N * 128;                  // 2 groups x nsb boxes
+    uint8_t* sB = sA + (size_t)stages * st_bytes;                  // resident weights (not streamed)
+    uint8_t* sOut = sB + (p.b_stream ? 0 : (size_t)kbt * p.N * 128);   // 2 groups x nsb boxes
     uint8_t* sMask = sOut + 2 * p.nsb * kBoxBytes;                 // [group][buf] gate boxes
     uint64_t* full = (uint64_t*)(sMask + (p.mask_tma ? 4 * kBoxBytes : 0));
     uint64_t* empty = full + kMaxNNStages;
@@ -222,7 +263,7 @@ __global__ void __launch_bounds__(kNNThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     // weights -> shared memory once: bf16, K-major, SWIZZLE_128B, zero padded
-    stage_weights(sB, nullptr, p.B, p.K1, p.K2, p.N, p.kb1, kbt, p.b_trans);
+    if (!p.b_stream) stage_weights(sB, nullptr, p.B, p.K1, p.K2, p.N, p.kb1, kbt, p.b_trans);
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < stages; s++) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
         for (int a = 0; a < 2; a++) { tc::mbar_init(&tfull[a], 1); tc::mbar_init(&tempty[a], 8); }
@@ -245,10 +286,12 @@ __global__ void __launch_bounds__(kNNThreads, 1)
             for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
                 for (int kb = 0; kb < kbt; kb++) {
                     tc::mbar_wait(&empty[stage], phase ^ 1);
-                    tc::mbar_arrive_expect_tx(&full[stage], kNNStageBytes);
+                    tc::mbar_arrive_expect_tx(&full[stage], st_bytes);
                     const bool first = kb < p.kb1;
-                    tc::tma_load_2d(sA + stage * kNNStageBytes, first ? &tmA1 : &tmA2, &full[stage],
-                                    (first ? kb : kb - p.kb1) * 64, tile * 128);
+                    uint8_t* st = sA + (size_t)stage * st_bytes;
+                    tc::tma_load_2d(st, first ? &tmA1 : &tmA2, &full[stage], (first ? kb : kb - p.kb1) * 64,
+                                    tile * 128);
+                    if (p.b_stream) bulk_g2s(st + kNNStageBytes, p.bimg + (size_t)kb * stB, stB, &full[stage]);
                     if (++stage == stages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -265,8 +308,8 @@ __global__ void __launch_bounds__(kNNThreads, 1)
                 tc::mbar_wait(&full[stage], phase);
                 tc::fence_after();
                 if (lane == 0) {
-                    const uint32_t a0 = tc::smem_u32(sA + stage * kNNStageBytes);
-                    const uint32_t b0 = tc::smem_u32(sB + (size_t)kb * p.N * 128);
+                    const uint32_t a0 = tc::smem_u32(sA + (size_t)stage * st_bytes);
+                    const uint32_t b0 = p.b_stream ? a0 + kNNStageBytes : tc::smem_u32(sB + (size_t)kb * p.N * 128);
 #pragma unroll
                     for (int k = 0; k < 4; k++)
                         tc::mma_f16(d, tc::smem_desc_sw128(a0 + k * 32, 0, 1024),
@@ -1094,26 +1137,30 @@ grappa_status tma_map_rows_bf16(CUtensorMap* m, const void* ptr, int64_t rows, i
 
 // A ring + resident weights + 2 groups x nsb staging boxes + barriers; the deepest ring
 // (<= 8 stages) and double-buffered staging when they fit
-static size_t nn_smem_of(int kbt, int N, int stages, int nsb, int mask_tma) {
-    return 1024 + (size_t)stages * kNNStageBytes + (size_t)kbt * N * 128 + (size_t)2 * nsb * kBoxBytes +
+static size_t nn_smem_of(int kbt, int N, int stages, int nsb, int mask_tma, int b_stream = 0) {
+    const size_t stage = kNNStageBytes + (b_stream ? (size_t)N * 128 : 0);
+    return 1024 + (size_t)stages * stage + (b_stream ? 0 : (size_t)kbt * N * 128) + (size_t)2 * nsb * kBoxBytes +
            (mask_tma ? (size_t)4 * kBoxBytes : 0) + 256;
 }
-static bool nn_plan(int kbt, int N, int mask_tma, int* stages, int* nsb) {
-    for (int b = 2; b >= 1; b--)
-        for (int st = kMaxNNStages; st >= 2; st--)
-            if (nn_smem_of(kbt, N, st, b, mask_tma) <= (size_t)kMaxSmem && (b == 1 || st >= 4)) {
-                *stages = st;
-                *nsb = b;
-                return true;
-            }
+// resident weights when they fit next to a ring of >= 2 stages, else streamed weight k-blocks
+static bool nn_plan(int kbt, int N, int mask_tma, int* stages, int* nsb, int* b_stream) {
+    for (int bs = 0; bs <= 1; bs++)
+        for (int b = 2; b >= 1; b--)
+            for (int st = kMaxNNStages; st >= 2; st--)
+                if (nn_smem_of(kbt, N, st, b, mask_tma, bs) <= (size_t)kMaxSmem && (b == 1 || st >= 4)) {
+                    *stages = st;
+                    *nsb = b;
+                    *b_stream = bs;
+                    return true;
+                }
     return false;
 }
 
 bool gemm_tc_nn_supported(const GemmArgs& g) {
     const int kbt = (int)(ceil_div(g.K1, 64) + ceil_div(g.K2, 64));
-    int st, nsb;
+    int st, nsb, bs;
     return g.N % 16 == 0 && g.N <= 256 && g.n_split % 16 == 0 && g.K1 % 8 == 0 && g.K2 % 8 == 0 &&
-           nn_plan(kbt, g.N, 0, &st, &nsb) && g.M < (1ll << 31);
+           nn_plan(kbt, g.N, 0, &st, &nsb, &bs) && g.M < (1ll << 31);
 }
 
 static uint32_t pow2_cols(int c) {
@@ -1139,15 +1186,24 @@ grappa_status gemm_tc_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s) {
     p.num_tiles = (int)ceil_div(g.M, 128);
     p.tmem_cols = pow2_cols(2 * g.N);
     // relu'-gate through TMA when each epilogue group owns at most one gated box and it fits
-    p.mask_tma = p.has_mask && p.nb1 <= 2 && nn_plan(p.kb1 + p.kb2, g.N, 1, &p.stages, &p.nsb) ? 1 : 0;
-    if (!p.mask_tma && !nn_plan(p.kb1 + p.kb2, g.N, 0, &p.stages, &p.nsb)) {
+    p.mask_tma = p.has_mask && p.nb1 <= 2 && nn_plan(p.kb1 + p.kb2, g.N, 1, &p.stages, &p.nsb, &p.b_stream) ? 1 : 0;
+    if (!p.mask_tma && !nn_plan(p.kb1 + p.kb2, g.N, 0, &p.stages, &p.nsb, &p.b_stream)) {
         set_error("gemm_tc_nn: shape does not fit shared memory");
         return GRAPPA_E_SUPPORT;
+    }
+    p.bimg = nullptr;
+    if (p.b_stream) {            // the weight image, once per call (stream-ordered before the GEMM)
+        const int kbt = p.kb1 + p.kb2;
+        GRAPPA_TRY(ctx->wimg.grow((size_t)kbt * g.N * 128));
+        k_weight_image<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)kbt * 8 * g.N, 256), (int64_t)ctx->sm_count * 4),
+                         256, 0, s>>>(g.B, g.K1, g.K2, g.N, p.kb1, kbt, g.b_trans, (uint8_t*)ctx->wimg.p);
+        GRAPPA_LAUNCHED(ctx);
+        p.bimg = (const uint8_t*)ctx->wimg.p;
     }
     CUtensorMap mk;
     if (p.mask_tma) GRAPPA_TRY(make_map(&mk, g.mask, g.M, g.n_split, 128));
     else mk = c1;
-    const size_t smem = nn_smem_of(p.kb1 + p.kb2, g.N, p.stages, p.nsb, p.mask_tma);
+    const size_t smem = nn_smem_of(p.kb1 + p.kb2, g.N, p.stages, p.nsb, p.mask_tma, p.b_stream);
     static bool attr = false;
     if (!attr) {
         GRAPPA_CUDA(cudaFuncSetAttribute(k_gemm_tc_nn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));

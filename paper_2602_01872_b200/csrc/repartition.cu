@@ -816,7 +816,10 @@ static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const voi
                                          (unsigned long long*)(d_stat + 7));
     GRAPPA_LAUNCHED(ctx);
     if (halo && n_halo > 0) {
-        k_halo_rows<<<grid, 256, 0, s>>>(n_core, n_local, d_stat + 1, core_global, g->rowptr, labels,
+        // (sharded: the labels argument is the base shard's, indexed by shard row -- the halo rows'
+        // labels and degrees come with grappa_halo_exchange)
+        k_halo_rows<<<grid, 256, 0, s>>>(n_core, n_local, d_stat + 1, core_global, sa ? nullptr : g->rowptr,
+                                          sa ? nullptr : labels,
                                           (int64_t*)p->rowptr.p, (int32_t*)p->d_l.p, (int32_t*)p->d_g.p,
                                           (float*)p->norm_gcn.p, (float*)p->norm_sage.p,
                                           (float*)p->node_w.p, (int32_t*)p->labels.p);

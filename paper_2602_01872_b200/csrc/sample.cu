@@ -14,6 +14,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <cstring>
+#include <vector>
 
 #include "gemm.cuh"
 #include "part.cuh"
@@ -48,9 +49,10 @@ static uint64_t hmix(uint64_t x) {
 template <int MAXF>
 __global__ void k_pick_floyd(const int64_t* __restrict__ d_nt, const int32_t* __restrict__ targets,
                              const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                             const int32_t* __restrict__ gid, int f, uint64_t key0, int32_t* __restrict__ picks,
-                             int32_t* __restrict__ cnt, uint32_t* __restrict__ bitmap) {
+                             const int32_t* __restrict__ gid, int f, const uint64_t* __restrict__ d_key,
+                             int32_t* __restrict__ picks, int32_t* __restrict__ cnt, uint32_t* __restrict__ bitmap) {
     const int64_t nt = *d_nt;
+    const uint64_t key0 = *d_key;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = targets[t];
         const int64_t e0 = rowptr[v], d = rowptr[v + 1] - e0;
@@ -212,6 +214,23 @@ __global__ void k_batch_stats(int n, const int32_t* seeds, const int32_t* d_l, c
     }
 }
 
+// Per-call parameters of grappa_sample_async, written by the host into pinned memory and copied
+// to the device by the call itself, so that the call's launch sequence is identical from batch to
+// batch and can be replayed as a CUDA graph (the batch index and epoch only enter the hop keys,
+// the seed slice only enters k_sample_prep).
+struct SampleParams {
+    int64_t n_batch;
+    const int32_t* batch;
+    uint64_t key[kMaxLayers];   // h(seed, epoch, batch, hop) per hop
+};
+__global__ void k_sample_prep(const SampleParams* __restrict__ P, int32_t* __restrict__ seeds, int64_t* __restrict__ d_nt) {
+    const int64_t n = P->n_batch;
+    const int32_t* src = P->batch;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        seeds[i] = src[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) *d_nt = n;
+}
+
 // seeds' epoch keys: h(seed, epoch, gid) = mix(seed ^ mix(epoch ^ mix(gid)))
 __global__ void k_seed_keys(int64_t n, const int32_t* seeds, const int32_t* gid, uint64_t seed, uint64_t epoch,
                             uint64_t* keys) {
@@ -240,7 +259,38 @@ struct grappa_batch {
     void* host = nullptr;                   // int64 [3 kMaxLayers] + BatchStats
     cudaEvent_t done = nullptr;
     bool pending = false;
+    // graph replay of the launch sequence (see grappa_sample_async): parameters in pinned host
+    // memory (copied to `dparams` by the sequence), the seed copy, and the graph of the last key
+    SampleParams* hparams = nullptr;
+    DevBuf dparams, seedbuf;
+    // graphs of the last few keys (the phases of an epoch cycle through the partitions), each valid
+    // while none of the batch's buffers has moved since its capture (generation)
+    struct Cached {
+        std::vector<int64_t> key;
+        cudaGraphExec_t exec = nullptr;
+        int64_t launches = 0;
+        uint64_t gen = 0;
+        uint64_t used = 0;
+    };
+    std::vector<Cached> graphs;
+    std::vector<std::vector<int64_t>> seen;   // keys run eagerly once (capture on the next call)
+    uint64_t gen = 0, tick = 0;
 };
+static constexpr int kSampleGraphs = 16;
+// identity of every buffer the launch sequence touches: a change means a graph captured earlier
+// points at freed memory
+static uint64_t batch_layout(const grappa_batch* b) {
+    uint64_t h = 1469598103934665603ull;
+    auto mixp = [&](const void* p) { h = (h ^ (uint64_t)(uintptr_t)p) * 1099511628211ull; };
+    for (int l = 0; l < kMaxLayers; l++)
+        for (const DevBuf* d : {&b->blk[l].rowptr, &b->blk[l].col, &b->blk[l].trowptr, &b->blk[l].tcol,
+                                &b->blk[l].inv_cnt, &b->blk[l].src, &b->blk[l].inv_cnt_node})
+            mixp(d->p);
+    for (const DevBuf* d : {&b->picks, &b->cnt, &b->bitmap, &b->where, &b->erow, &b->key_pad, &b->skeys,
+                            &b->svals, &b->sort_tmp, &b->counts, &b->heavy_q, &b->scan_ws, &b->dparams, &b->seedbuf})
+        mixp(d->p);
+    return h;
+}
 
 static grappa_status sort_pairs(DevBuf& tmp, const int32_t* kin, int32_t* kout, const int32_t* vin,
                                 int32_t* vout, int64_t n, int end_bit, cudaStream_t s) {
@@ -288,35 +338,24 @@ extern "C" grappa_status grappa_sample(grappa_ctx* ctx, const grappa_part* part,
     return grappa_sample_wait(*inout);
 }
 
-extern "C" grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part* part, const int32_t* batch,
-                                             int32_t n_batch, const int32_t* fanouts, int32_t n_layers,
-                                             uint64_t seed, int64_t epoch, int64_t batch_index,
-                                             grappa_batch** inout, void* stream) {
-    CallScope call_scope(ctx, stream);
-    GRAPPA_ARG(ctx && part && batch && fanouts && inout, GRAPPA_E_ARG, "grappa_sample: null argument");
-    GRAPPA_ARG(n_layers >= 1 && n_layers <= kMaxLayers, GRAPPA_E_ARG, "grappa_sample: 1 <= n_layers <= %d", kMaxLayers);
-    GRAPPA_ARG(n_batch >= 1, GRAPPA_E_ARG, "grappa_sample: empty batch (S:213)");
-    for (int l = 0; l < n_layers; l++)
-        GRAPPA_ARG(fanouts[l] >= 1 && fanouts[l] <= kMaxFanout, GRAPPA_E_ARG,
-                   "grappa_sample: fanout must be in [1, %d]", kMaxFanout);
-    cudaStream_t s = (cudaStream_t)stream;
+// The launch sequence of one batch: params H2D (pinned -> device), seed copy, per hop: frontier
+// clear, Floyd pick (+ marking), unmark, two scans, block fill, radix-sort transpose, transpose
+// rowptr; then the batch statistics.  Every size comes from device counters or from the call key
+// (n_batch, fanouts, partition), so the sequence is the same for every batch of that key.
+static grappa_status sample_body(grappa_ctx* ctx, const grappa_part* part, grappa_batch* b, int32_t n_batch,
+                                 const int32_t* fanouts, int32_t n_layers, cudaStream_t s) {
     const grappa_part_info& I = part->info;
-    ProfScope ps(ctx, s, GRAPPA_K_SAMPLE, 0.0, 0.0);
-    grappa_batch* b = *inout ? *inout : new grappa_batch();
-    b->L = n_layers;
-    b->n_batch = n_batch;
     const int64_t nc = I.n_core;
-    // device counters: per hop n_t, n_s, nnz (3 x kMaxLayers int64) + stats
-    GRAPPA_TRY(b->counts.grow(3 * kMaxLayers * 8 + sizeof(BatchStats) + 64));
     int64_t* dc = (int64_t*)b->counts.p;
     BatchStats* dstat = (BatchStats*)(dc + 3 * kMaxLayers);
+    SampleParams* dp = (SampleParams*)b->dparams.p;
+    GRAPPA_CUDA(cudaMemcpyAsync(dp, b->hparams, sizeof(SampleParams), cudaMemcpyHostToDevice, s));
+    k_sample_prep<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_batch, 256), 64)), 256, 0, s>>>(
+        dp, (int32_t*)b->seedbuf.p, dc);
+    GRAPPA_LAUNCHED(ctx);
     const int64_t nwords = ceil_div(nc, 32);
-    GRAPPA_TRY(b->bitmap.grow((size_t)nwords * 4));
-    GRAPPA_TRY(b->where.grow((size_t)nc * 4));
-    int64_t n_t_host = n_batch;           // exact for hop 1
     int64_t cap_t = n_batch;
-    GRAPPA_CUDA(cudaMemcpyAsync(dc + 0, &n_t_host, 8, cudaMemcpyHostToDevice, s));
-    const int32_t* targets = batch;
+    const int32_t* targets = (const int32_t*)b->seedbuf.p;
     for (int h = 1; h <= n_layers; h++) {
         const int layer = n_layers - h;
         const int f = fanouts[layer];
@@ -338,15 +377,13 @@ extern "C" grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part*
         GRAPPA_TRY(b->erow.grow((size_t)cap_nnz * 4));
         GRAPPA_TRY(b->key_pad.grow((size_t)cap_nnz * 4));
         GRAPPA_TRY(b->skeys.grow((size_t)cap_nnz * 4));
-        // h(seed, epoch, batch, hop) = mix(seed ^ mix(epoch ^ mix(batch ^ mix(hop))))
-        const uint64_t key0 = hmix(seed ^ hmix((uint64_t)epoch ^ hmix((uint64_t)batch_index ^ hmix((uint64_t)h))));
         const unsigned tgrid = (unsigned)std::min<int64_t>(ceil_div(cap_nnz, 256), (int64_t)ctx->sm_count * 16);
         GRAPPA_CUDA(cudaMemsetAsync(b->bitmap.p, 0, (size_t)nwords * 4, s));
         {
             auto kp = f <= 16 ? k_pick_floyd<16> : k_pick_floyd<32>;
             kp<<<(unsigned)std::min<int64_t>(ceil_div(cap_t, 256), (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
-                d_nt, targets, I.rowptr, I.col, I.core_global, f, key0, (int32_t*)b->picks.p, (int32_t*)b->cnt.p,
-                (uint32_t*)b->bitmap.p);
+                d_nt, targets, I.rowptr, I.col, I.core_global, f, &dp->key[h - 1], (int32_t*)b->picks.p,
+                (int32_t*)b->cnt.p, (uint32_t*)b->bitmap.p);
         }
         GRAPPA_LAUNCHED(ctx);
         k_unmark<<<(unsigned)std::min<int64_t>(ceil_div(cap_t, 256), 4096), 256, 0, s>>>(
@@ -376,13 +413,132 @@ extern "C" grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part*
         cap_t = cap_s;
     }
     // batch coverage statistics over the seeds (hop 1 = output layer block)
-    k_batch_stats<<<1, 256, 0, s>>>(n_batch, batch, I.d_l, I.d_g, (int64_t*)b->blk[n_layers - 1].rowptr.p, dstat);
+    k_batch_stats<<<1, 256, 0, s>>>(n_batch, (const int32_t*)b->seedbuf.p, I.d_l, I.d_g,
+                                    (int64_t*)b->blk[n_layers - 1].rowptr.p, dstat);
     GRAPPA_LAUNCHED(ctx);
+    return GRAPPA_OK;
+}
+
+// Graph replay.  The ~45-launch sequence of a batch is launch-bound on the host (config 4 runs
+// 2416 batches per epoch); since it only depends on the call key (partition arrays and sizes,
+// n_batch, fanouts), the second call with a key captures it into a CUDA graph and later calls
+// replay it (one graph launch; the parameters travel through the pinned `hparams`).  A call with
+// another key runs eagerly and drops the graph (its buffers may move).  Results are the same
+// launches on the same data whichever way they run.
+extern "C" grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part* part, const int32_t* batch,
+                                             int32_t n_batch, const int32_t* fanouts, int32_t n_layers,
+                                             uint64_t seed, int64_t epoch, int64_t batch_index,
+                                             grappa_batch** inout, void* stream) {
+    CallScope call_scope(ctx, stream);
+    GRAPPA_ARG(ctx && part && batch && fanouts && inout, GRAPPA_E_ARG, "grappa_sample: null argument");
+    GRAPPA_ARG(n_layers >= 1 && n_layers <= kMaxLayers, GRAPPA_E_ARG, "grappa_sample: 1 <= n_layers <= %d", kMaxLayers);
+    GRAPPA_ARG(n_batch >= 1, GRAPPA_E_ARG, "grappa_sample: empty batch (S:213)");
+    for (int l = 0; l < n_layers; l++)
+        GRAPPA_ARG(fanouts[l] >= 1 && fanouts[l] <= kMaxFanout, GRAPPA_E_ARG,
+                   "grappa_sample: fanout must be in [1, %d]", kMaxFanout);
+    cudaStream_t s = (cudaStream_t)stream;
+    const grappa_part_info& I = part->info;
+    ProfScope ps(ctx, s, GRAPPA_K_SAMPLE, 0.0, 0.0);
+    grappa_batch* b = *inout ? *inout : new grappa_batch();
+    // the pinned parameters of the previous call on this batch object must have been consumed
+    if (b->pending) {
+        GRAPPA_CUDA(cudaEventSynchronize(b->done));
+        b->pending = false;
+    }
+    b->L = n_layers;
+    b->n_batch = n_batch;
+    const int64_t nc = I.n_core;
+    // device counters: per hop n_t, n_s, nnz (3 x kMaxLayers int64) + stats
+    GRAPPA_TRY(b->counts.grow(3 * kMaxLayers * 8 + sizeof(BatchStats) + 64));
+    GRAPPA_TRY(b->bitmap.grow((size_t)ceil_div(nc, 32) * 4));
+    GRAPPA_TRY(b->where.grow((size_t)nc * 4));
+    GRAPPA_TRY(b->dparams.grow(sizeof(SampleParams)));
+    GRAPPA_TRY(b->seedbuf.grow((size_t)n_batch * 4));
+    if (!b->hparams) GRAPPA_CUDA(cudaMallocHost((void**)&b->hparams, sizeof(SampleParams)));
     if (!b->host) {
         GRAPPA_CUDA(cudaMallocHost(&b->host, sizeof(int64_t) * 3 * kMaxLayers + sizeof(BatchStats)));
         GRAPPA_CUDA(cudaEventCreateWithFlags(&b->done, cudaEventDisableTiming));
     }
-    GRAPPA_CUDA(cudaMemcpyAsync(b->host, dc, sizeof(int64_t) * 3 * kMaxLayers + sizeof(BatchStats),
+    SampleParams& P = *b->hparams;
+    P.n_batch = n_batch;
+    P.batch = batch;
+    for (int h = 1; h <= n_layers; h++)
+        // h(seed, epoch, batch, hop) = mix(seed ^ mix(epoch ^ mix(batch ^ mix(hop))))
+        P.key[h - 1] = hmix(seed ^ hmix((uint64_t)epoch ^ hmix((uint64_t)batch_index ^ hmix((uint64_t)h))));
+    std::vector<int64_t> key = {(int64_t)(uintptr_t)part, (int64_t)(uintptr_t)I.rowptr, (int64_t)(uintptr_t)I.col,
+                                nc, I.nnz, n_batch, n_layers};
+    for (int l = 0; l < n_layers; l++) key.push_back(fanouts[l]);
+    // not on the legacy default stream (cannot be captured), not inside a caller's own capture,
+    // not while per-kernel-class profiling records events
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    const bool can_graph = !ctx->profiling && s != nullptr && s != cudaStreamLegacy && s != cudaStreamPerThread &&
+                           cudaStreamIsCapturing(s, &cst) == cudaSuccess && cst == cudaStreamCaptureStatusNone;
+    const uint64_t layout = batch_layout(b);
+    if (layout != b->gen) {                   // buffers moved: every cached graph is stale
+        for (auto& c : b->graphs) cudaGraphExecDestroy(c.exec);
+        b->graphs.clear();
+        b->gen = layout;
+    }
+    b->tick++;
+    grappa_batch::Cached* hit = nullptr;
+    for (auto& c : b->graphs)
+        if (c.key == key) hit = &c;
+    bool seen = false;
+    for (auto& k : b->seen)
+        if (k == key) seen = true;
+    if (can_graph && hit) {
+        hit->used = b->tick;
+        GRAPPA_CUDA(cudaGraphLaunch(hit->exec, s));
+        ctx->launches += hit->launches;
+    } else if (can_graph && seen) {
+        // capture the sequence (buffers already sized by the eager call with this key)
+        const int64_t l0 = ctx->launches;
+        GRAPPA_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        const grappa_status st = sample_body(ctx, part, b, n_batch, fanouts, n_layers, s);
+        cudaGraph_t g = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(s, &g);
+        grappa_batch::Cached c;
+        cudaError_t ie = cudaErrorUnknown;
+        if (st == GRAPPA_OK && ce == cudaSuccess && batch_layout(b) == b->gen) ie = cudaGraphInstantiate(&c.exec, g, 0);
+        if (g) cudaGraphDestroy(g);
+        if (ie != cudaSuccess) {
+            // the sequence could not be captured as it stands (e.g. a buffer had to grow inside
+            // the capture): run it eagerly; the next call with this key tries again
+            cudaGetLastError();
+            ctx->launches = l0;
+            GRAPPA_TRY(sample_body(ctx, part, b, n_batch, fanouts, n_layers, s));
+            b->gen = batch_layout(b);
+            for (auto& x : b->graphs) cudaGraphExecDestroy(x.exec);
+            b->graphs.clear();
+            goto published;
+        }
+        c.key = key;
+        c.launches = ctx->launches - l0;
+        c.gen = b->gen;
+        c.used = b->tick;
+        if ((int)b->graphs.size() >= kSampleGraphs) {     // drop the least recently used
+            size_t lru = 0;
+            for (size_t i = 1; i < b->graphs.size(); i++)
+                if (b->graphs[i].used < b->graphs[lru].used) lru = i;
+            cudaGraphExecDestroy(b->graphs[lru].exec);
+            b->graphs.erase(b->graphs.begin() + lru);
+        }
+        b->graphs.push_back(c);
+        GRAPPA_CUDA(cudaGraphLaunch(c.exec, s));
+    } else {
+        GRAPPA_TRY(sample_body(ctx, part, b, n_batch, fanouts, n_layers, s));
+        if (batch_layout(b) != b->gen) {             // this call moved buffers
+            for (auto& c : b->graphs) cudaGraphExecDestroy(c.exec);
+            b->graphs.clear();
+            b->gen = batch_layout(b);
+        }
+        if (!seen) {
+            b->seen.push_back(key);
+            if ((int)b->seen.size() > 4 * kSampleGraphs) b->seen.erase(b->seen.begin());
+        }
+    }
+published:
+    GRAPPA_CUDA(cudaMemcpyAsync(b->host, b->counts.p, sizeof(int64_t) * 3 * kMaxLayers + sizeof(BatchStats),
                                 cudaMemcpyDeviceToHost, s));
     GRAPPA_CUDA(cudaEventRecord(b->done, s));
     b->pending = true;
@@ -441,6 +597,10 @@ extern "C" void grappa_batch_destroy(grappa_batch* b) {
     if (!b) return;
     if (b->done) { cudaEventSynchronize(b->done); cudaEventDestroy(b->done); }
     if (b->host) cudaFreeHost(b->host);
+    if (b->hparams) cudaFreeHost(b->hparams);
+    for (auto& c : b->graphs) cudaGraphExecDestroy(c.exec);
+    b->dparams.release();
+    b->seedbuf.release();
     for (int l = 0; l < kMaxLayers; l++)
         for (DevBuf* d : {&b->blk[l].rowptr, &b->blk[l].col, &b->blk[l].trowptr, &b->blk[l].tcol,
                           &b->blk[l].inv_cnt, &b->blk[l].src, &b->blk[l].inv_cnt_node})

@@ -206,3 +206,30 @@ def test_sharded_minibatch_equals_replicated(G, setup):
     torch.cuda.synchronize()
     ctx.check()
     assert torch.equal(a.theta, b.theta)
+
+
+def test_sampler_graph_replay_bitexact(G, setup):
+    """grappa_sample_async on a side stream: the second call with a key captures the launch
+    sequence into a CUDA graph and later calls replay it with new parameters (pinned params ->
+    device).  Every call -- eager, capture, replays, and an eager call after a key change -- gives
+    blocks bit-exact with a fresh eager sample and with the oracle."""
+    ctx, wl, ds, ref, parts = setup
+    p = parts["f32"]
+    st = torch.cuda.Stream()
+    order = Sa.epoch_batches(ref, 9, 1, 300)
+    b = None
+    fan_seq = [FAN, FAN, FAN, FAN, [5, 4, 3], FAN, FAN]
+    for k, fan in enumerate(fan_seq):
+        seeds = torch.from_numpy(order[k % len(order)].astype(np.int32)).cuda()
+        l0 = ctx.launches()
+        with torch.cuda.stream(st):
+            b = G.grappa_sample_async(ctx, p, seeds, fan, 9, 1, k, b, stream=st)
+        G.grappa_sample_wait(b)
+        assert ctx.launches() > l0                   # replays count their captured launches
+        fresh = G.grappa_sample(ctx, p, seeds, fan, 9, 1, k)
+        blocks = Sa.sample_batch(ref, order[k % len(order)], fan, 9, 1, k)
+        for l, (gb, fb, ob) in enumerate(zip(b.blocks, fresh.blocks, blocks)):
+            for key in ("rowptr", "col", "t_rowptr", "t_col", "src", "inv_cnt"):
+                assert torch.equal(gb[key], fb[key]), (k, l, key)
+            assert np.array_equal(gb["col"].cpu().numpy(), ob["col"]), (k, l)
+        assert b.factors == fresh.factors

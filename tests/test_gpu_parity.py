@@ -148,7 +148,8 @@ def _np(t):
 
 @pytest.mark.parametrize("arch", ["gcn", "sage"])
 @pytest.mark.parametrize("f_in,f_out", [(112, 128), (128, 48), (128, 16), (16, 128), (256, 256),
-                                         (112, 256), (256, 48)])
+                                         (112, 256), (256, 48),
+                                         (1440, 128), (1440, 16)])   # cora's input layer: streamed weights
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_layer_parity(G, ctx, prod, arch, f_in, f_out, dtype):
     """Layer-local parity: the oracle sees the GPU's own (upcast) layer inputs."""
