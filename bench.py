@@ -458,7 +458,8 @@ def run_grappa(args):
         traffic_src = {"dram_per_algorithmic_byte": ratio, "window": nt[1],
                        "window_dram_bytes_per_call": rec["dram_bytes_per_call"],
                        "window_algorithmic_bytes_per_call": rec["algorithmic_bytes_per_call"]}
-        for k in ("lts_bytes_per_call", "issue_active_pct"):
+        for k in ("lts_bytes_per_call", "issue_active_pct", "l2_throughput_pct", "l1_throughput_pct", "l2_hit_pct",
+                  "warp_instructions_per_call"):
             if k in rec:
                 traffic_src[k] = rec[k]
     # the profile window holds exactly one switch (the extra tr.repartition call above; the extra

@@ -354,15 +354,16 @@ __global__ void k_row_finalize(int64_t n_core, const int32_t* __restrict__ task_
     if ((threadIdx.x & 31) == 0 && my_dg) atomicAdd(sum_dg, my_dg);
 }
 
-// stable compaction of every task's kept neighbours, relabelled to local ids (walked like
-// k_task_count; rank is read for kept edges only): a kept edge goes to its task's offset + the
-// task's kept edges before it (a warp-uniform running count + the popc of the lower lanes).
+// stable compaction of every task's kept neighbours (walked like k_task_count): a kept edge goes
+// to its task's offset + the task's kept edges before it (a warp-uniform running count + the popc
+// of the lower lanes).  It writes the GLOBAL neighbour id; k_relabel then maps every entry through
+// the rank table in one fully parallel pass -- the dependent rank probe per kept edge inside the
+// walk (col -> membership -> rank -> store) was what bounded the fill.
 template <bool EC>
 __global__ void __launch_bounds__(256, 6) k_task_fill(const int64_t* __restrict__ d_T,
                                                    const int4* __restrict__ task_desc,
                                                    const int64_t* __restrict__ task_out,
                                                    const int32_t* __restrict__ g_col, Member mb,
-                                                   const int32_t* __restrict__ rank,
                                                    int32_t* __restrict__ col) {
     const int lane = threadIdx.x & 31;
     const unsigned below = (1u << lane) - 1u;
@@ -392,23 +393,27 @@ __global__ void __launch_bounds__(256, 6) k_task_fill(const int64_t* __restrict_
 #pragma unroll
             for (int k = 1; k < kPackU; k++) Lm = max(Lm, L[k]);
             for (int32_t off = 0; off < Lm; off += 32) {
-                int32_t u[kPackU], r[kPackU];
+                int32_t u[kPackU];
                 bool keep[kPackU];
 #pragma unroll
                 for (int k = 0; k < kPackU; k++) u[k] = off + lane < L[k] ? __ldg(g_col + E[k] + off + lane) : -1;
 #pragma unroll
                 for (int k = 0; k < kPackU; k++) keep[k] = u[k] >= 0 && member<EC>(mb, E[k] + off + lane, u[k]);
 #pragma unroll
-                for (int k = 0; k < kPackU; k++) r[k] = keep[k] ? __ldg(rank + u[k]) : -1;
-#pragma unroll
                 for (int k = 0; k < kPackU; k++) {
                     const unsigned bal = __ballot_sync(0xffffffffu, keep[k]);
-                    if (keep[k]) col[O[k] + __popc(bal & below)] = r[k];
+                    if (keep[k]) col[O[k] + __popc(bal & below)] = u[k];
                     O[k] += __popc(bal);
                 }
             }
         }
     }
+}
+
+// global -> local neighbour ids of a partition's CSR through its rank table (independent loads)
+__global__ void k_relabel(int64_t nnz, const int32_t* __restrict__ rank, int32_t* __restrict__ col) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
+        col[e] = __ldg(rank + col[e]);
 }
 
 __global__ void k_slot_tasks(int64_t n_heavy, const int32_t* heavy_rows, const int32_t* slot_off,
@@ -838,8 +843,13 @@ static grappa_status repart_impl(grappa_ctx* ctx, const grappa_csr* g, const voi
                "grappa_repartition: partition (%d,%d) has no seeds (S:213)", base, swept);
     // 4. fill
     RP_TRY(p->col.grow((size_t)(nnz > 0 ? nnz : 1) * 4));
-    if (ec) k_task_fill<true><<<tgrid, 256, 0, s>>>(d_stat + 5, task_desc, task_out, G_col, mb, rank, (int32_t*)p->col.p);
-    else k_task_fill<false><<<tgrid, 256, 0, s>>>(d_stat + 5, task_desc, task_out, G_col, mb, rank, (int32_t*)p->col.p);
+    if (ec) k_task_fill<true><<<tgrid, 256, 0, s>>>(d_stat + 5, task_desc, task_out, G_col, mb, (int32_t*)p->col.p);
+    else k_task_fill<false><<<tgrid, 256, 0, s>>>(d_stat + 5, task_desc, task_out, G_col, mb, (int32_t*)p->col.p);
+    GRAPPA_LAUNCHED(ctx);
+    if (nnz > 0) {
+        k_relabel<<<(unsigned)std::min<int64_t>(ceil_div(nnz, 256), (int64_t)ctx->sm_count * 32), 256, 0, s>>>(
+            nnz, rank, (int32_t*)p->col.p);
+    }
     GRAPPA_LAUNCHED(ctx);
     // 5. features (core and halo rows)
     if (feats && !sa) {
@@ -1304,8 +1314,13 @@ extern "C" grappa_status grappa_repartition_batch_ix(grappa_ctx* ctx, const grap
         RB_TRY(p->col.grow((size_t)(nnz > 0 ? nnz : 1) * 4));
         {
             const Member mb{nullptr, ec, bases[k], swepts[k], 0};
-            k_task_fill<true><<<tgrid, 256, 0, s>>>(d_stat0 + (size_t)k * kSt + 5, tw[k].desc, tw[k].out, g->col, mb, rank,
-                                     (int32_t*)p->col.p);
+            k_task_fill<true><<<tgrid, 256, 0, s>>>(d_stat0 + (size_t)k * kSt + 5, tw[k].desc, tw[k].out, g->col, mb,
+                                                    (int32_t*)p->col.p);
+        }
+        GRAPPA_LAUNCHED(ctx);
+        if (nnz > 0) {
+            k_relabel<<<(unsigned)std::min<int64_t>(ceil_div(nnz, 256), (int64_t)ctx->sm_count * 32), 256, 0, s>>>(
+                nnz, rank, (int32_t*)p->col.p);
         }
         GRAPPA_LAUNCHED(ctx);
         unsigned grid;

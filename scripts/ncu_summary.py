@@ -24,7 +24,9 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "lts__t_bytes.sum",
         "l1tex__t_sector_hit_rate.pct", "smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct",
         "smsp__warp_issue_stalled_lg_throttle_per_warp_active.pct",
-        "smsp__warp_issue_stalled_barrier_per_warp_active.pct"]
+        "smsp__warp_issue_stalled_barrier_per_warp_active.pct",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed.sum",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active"]
 
 
 # kernel-name prefixes of each profiled class (a logical call = all of its launches)
@@ -79,6 +81,19 @@ def full(paths):
                         "dram_bytes_per_call": sum(out[k]["dram_bytes_total"] for k in ks) / n,
                         "algorithmic_bytes_per_call": calls["algorithmic_bytes"][cls] / n,
                         "ncu_time_per_call_s": sum(out[k]["time_total_s"] for k in ks) / n}
+            # time-weighted limiter evidence over the class's launches
+            tw = sum(out[k]["time_total_s"] for k in ks)
+            for key, metric in (("issue_active_pct", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                                ("l2_throughput_pct", "lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+                                ("l1_throughput_pct", "l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                                ("l2_hit_pct", "lts__t_sector_hit_rate.pct")):
+                if tw and all(metric in out[k] for k in ks):
+                    per[cls][key] = sum(out[k][metric] * out[k]["time_total_s"] for k in ks) / tw
+            if all("lts__t_bytes.sum" in out[k] for k in ks):
+                per[cls]["lts_bytes_per_call"] = sum(out[k]["lts__t_bytes.sum"] * out[k]["launches"] for k in ks) / n
+            if all("smsp__inst_executed.sum" in out[k] for k in ks):
+                per[cls]["warp_instructions_per_call"] = sum(out[k]["smsp__inst_executed.sum"] * out[k]["launches"]
+                                                             for k in ks) / n
         res["window"] = {k: calls[k] for k in ("config", "dtype", "worker")}
         res["per_call"] = per
     json.dump(res, sys.stdout, indent=1)
