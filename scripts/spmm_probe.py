@@ -34,6 +34,7 @@ def main():
     w = (torch.randn(width, width, device=d, generator=g) / 11).contiguous()
     out = torch.empty(n, width, device=d, dtype=torch.bfloat16)
     ws = torch.empty(G.layer_ws_bytes(part, "gcn", width, width, "bf16"), dtype=torch.uint8, device=d)
+    ref = None
     for v in variants:
         ctx.set_variant("spmm", v)
         for _ in range(2):
@@ -44,8 +45,14 @@ def main():
             G.grappa_layer_fwd(ctx, part, "gcn", width, width, True, h, w, out, None, ws, "bf16")
         ms, calls, by, _ = ctx.profile_read("spmm")
         ctx.profile(False)
+        torch.cuda.synchronize()
+        same = None
+        if ref is None:
+            ref = out.clone()
+        else:
+            same = torch.equal(out.view(torch.int16), ref.view(torch.int16))
         print(f"variant {v}: spmm {ms / calls * 1e3:.1f} us/call, {by / calls / 1e9:.3f} GB algorithmic, "
-              f"{by / (ms / 1e3) / 1e9:.0f} GB/s", flush=True)
+              f"{by / (ms / 1e3) / 1e9:.0f} GB/s, bitwise == first variant: {same}", flush=True)
     ctx.close()
 
 
