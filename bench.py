@@ -78,6 +78,9 @@ class ClockSampler:
         self.index, self.proc, self.lines = index, None, []
 
     def start(self):
+        if os.environ.get("GRAPPA_NO_CLOCKS") == "1":      # diagnostic: no sampler at all
+            self.proc = None
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",

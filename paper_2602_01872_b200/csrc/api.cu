@@ -194,6 +194,14 @@ extern "C" void grappa_ctx_destroy(grappa_ctx* c) {
     c->xf_hdr.release();
     c->comm_buf.release();
     c->wimg.release();
+    for (int i = 0; i < grappa_ctx::kRpStreams; i++) {
+        c->rp_scan[i].release();
+        c->rp_small[i].release();
+        c->rp_rank[i].release();
+        if (c->rp_s[i]) cudaStreamDestroy(c->rp_s[i]);
+    }
+    for (int i = 0; i <= grappa_ctx::kRpStreams; i++)
+        if (c->rp_ev[i]) cudaEventDestroy(c->rp_ev[i]);
     for (auto& r : c->prof) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);

@@ -113,6 +113,12 @@ struct grappa_ctx {
     std::shared_ptr<const grappa::Allocator> alloc;   // caller allocator (null: cudaMalloc)
     grappa::DevBuf comm_buf;     // bf16 communication buffer of grappa_aggregate_grads
     grappa::DevBuf wimg;         // streamed-weight image of the tcgen05 NN GEMM (large K)
+    // side streams of the batched switch (partitions extracted concurrently) and their own
+    // workspaces: scan partials, degree-bucket counters + seed-statistics partials, rank table
+    static constexpr int kRpStreams = 4;
+    cudaStream_t rp_s[kRpStreams] = {};
+    cudaEvent_t rp_ev[kRpStreams + 1] = {};
+    grappa::DevBuf rp_scan[kRpStreams], rp_small[kRpStreams], rp_rank[kRpStreams];
     // test / A-B kernel selection (grappa_set_kernel_variant): gemm 0 = tensor cores, 1/2 = CUDA
     // cores; spmm 0 = row-group, 1 = warp per row, 2 = 8 loads in flight, 3 = natural row order;
     // pair 1 = separate GCN backward GEMMs

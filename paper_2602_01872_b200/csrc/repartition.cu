@@ -589,7 +589,7 @@ struct PlanBufs {
     DevBuf *heavy_rows, *heavy_slot_off, *slot_row, *slot_seg, *row_order, *row_desc;
 };
 static grappa_status plan_order(grappa_ctx* ctx, cudaStream_t s, int64_t n, const int64_t* rowptr,
-                                const int32_t* deg, PlanBufs b);
+                                const int32_t* deg, PlanBufs b, unsigned long long* bins = nullptr);
 static grappa_status build_plan(grappa_ctx* ctx, cudaStream_t s, int64_t n, const int64_t* rowptr,
                                 const int32_t* deg, PlanBufs b, int64_t* d_st, int64_t* n_heavy_out,
                                 int64_t* n_slots_out) {
@@ -624,8 +624,8 @@ static grappa_status build_plan(grappa_ctx* ctx, cudaStream_t s, int64_t n, cons
 
 // degree-bucketed row order (counting sort) and the 16-byte row descriptors of a local CSR
 static grappa_status plan_order(grappa_ctx* ctx, cudaStream_t s, int64_t n, const int64_t* rowptr,
-                                const int32_t* deg, PlanBufs b) {
-    unsigned long long* bins = (unsigned long long*)ctx->red_ws.p;
+                                const int32_t* deg, PlanBufs b, unsigned long long* bins) {
+    if (!bins) bins = (unsigned long long*)ctx->red_ws.p;
     GRAPPA_CUDA(cudaMemsetAsync(bins, 0, (size_t)kDegBuckets * 8, s));
     const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 8));
     k_deg_hist<<<g2, 256, 0, s>>>(n, deg, bins);
@@ -645,25 +645,27 @@ static grappa_status plan_order(grappa_ctx* ctx, cudaStream_t s, int64_t n, cons
 }
 
 // build_plan with the split-row sizes known (batched switch): no host sync
+// (ws / bins: a side stream's own scan partials and bucket counters; null = the ctx's)
 static grappa_status build_plan_sized(grappa_ctx* ctx, cudaStream_t s, int64_t n, const int64_t* rowptr,
                                       const int32_t* deg, PlanBufs b, int64_t* d_st, int64_t n_heavy,
-                                      int64_t n_slots) {
+                                      int64_t n_slots, DevBuf* ws = nullptr, unsigned long long* bins = nullptr) {
     GRAPPA_TRY(b.heavy_rows->grow((size_t)(n > 0 ? n : 1) * 4));
     GRAPPA_TRY(b.heavy_slot_off->grow((size_t)(n_heavy + 1) * 4));
     GRAPPA_TRY(b.slot_row->grow((size_t)(n_slots > 0 ? n_slots : 1) * 4));
     GRAPPA_TRY(b.slot_seg->grow((size_t)(n_slots > 0 ? n_slots : 1) * 4));
     if (n_heavy > 0) {
-        GRAPPA_TRY(device_scan(ctx, FlagHeavy{deg}, n, WriteCompact{(int32_t*)b.heavy_rows->p, d_st, 0}, s));
+        GRAPPA_TRY(device_scan(ctx, FlagHeavy{deg}, n, WriteCompact{(int32_t*)b.heavy_rows->p, d_st, 0}, s,
+                               nullptr, ws));
         GRAPPA_TRY(device_scan(ctx, NumSeg{deg, (int32_t*)b.heavy_rows->p}, n_heavy,
-                               WriteSlotOff{(int32_t*)b.heavy_slot_off->p, d_st, 1}, s));
+                               WriteSlotOff{(int32_t*)b.heavy_slot_off->p, d_st, 1}, s, nullptr, ws));
         k_slot_tasks<<<(unsigned)std::min<int64_t>(ceil_div(n_heavy, 256), 1024), 256, 0, s>>>(
             n_heavy, (int32_t*)b.heavy_rows->p, (int32_t*)b.heavy_slot_off->p, (int32_t*)b.slot_row->p,
             (int32_t*)b.slot_seg->p);
         GRAPPA_LAUNCHED(ctx);
     }
     GRAPPA_TRY(b.row_order->grow((size_t)(n > 0 ? n : 1) * 4));
-    GRAPPA_TRY(ctx->red_ws.grow((size_t)2 * kDegBuckets * 8));   // (already >= N * 4 in the batch)
-    return plan_order(ctx, s, n, rowptr, deg, b);
+    if (!bins) GRAPPA_TRY(ctx->red_ws.grow((size_t)2 * kDegBuckets * 8));
+    return plan_order(ctx, s, n, rowptr, deg, b, bins);
 }
 
 extern "C" grappa_status grappa_repartition(grappa_ctx* ctx, const grappa_csr* g, const void* feats,
@@ -1196,6 +1198,8 @@ extern "C" grappa_status grappa_repartition_batch_ix(grappa_ctx* ctx, const grap
         P[k] = parts[k] ? parts[k] : new grappa_part();
     }
     auto fail = [&](grappa_status st) {
+        for (int j = 0; j < grappa_ctx::kRpStreams; j++)      // side streams may still use them
+            if (ctx->rp_s[j]) cudaStreamSynchronize(ctx->rp_s[j]);
         for (int k = 0; k < K; k++)
             if (fresh[k]) grappa_part_destroy(P[k]);
         return st;
@@ -1249,8 +1253,35 @@ extern "C" grappa_status grappa_repartition_batch_ix(grappa_ctx* ctx, const grap
     }
     const unsigned tgrid = (unsigned)ctx->sm_count * 16;
     const uint8_t* ec = (const uint8_t*)ix->ec.p;
+    // The partitions are independent: partition k runs on side stream k % NS with its own scan
+    // partials, bucket counters and (if not kept per partition) rank table, so the chains of
+    // small latency-bound kernels of different partitions overlap.  Fork after the stats memset,
+    // join before each host sync.
+    const int NS = std::min(K, (int)grappa_ctx::kRpStreams);
+    for (int j = 0; j < NS; j++)
+        if (!ctx->rp_s[j]) RB_CUDA(cudaStreamCreateWithFlags(&ctx->rp_s[j], cudaStreamNonBlocking));
+    for (int j = 0; j <= NS; j++)
+        if (!ctx->rp_ev[j]) RB_CUDA(cudaEventCreateWithFlags(&ctx->rp_ev[j], cudaEventDisableTiming));
+    auto fork = [&]() -> grappa_status {
+        GRAPPA_CUDA(cudaEventRecord(ctx->rp_ev[NS], s));
+        for (int j = 0; j < NS; j++) GRAPPA_CUDA(cudaStreamWaitEvent(ctx->rp_s[j], ctx->rp_ev[NS], 0));
+        return GRAPPA_OK;
+    };
+    auto join = [&]() -> grappa_status {
+        for (int j = 0; j < NS; j++) {
+            GRAPPA_CUDA(cudaEventRecord(ctx->rp_ev[j], ctx->rp_s[j]));
+            GRAPPA_CUDA(cudaStreamWaitEvent(s, ctx->rp_ev[j], 0));
+        }
+        return GRAPPA_OK;
+    };
+    if (!keep_ranks)
+        for (int j = 0; j < NS; j++) RB_TRY(ctx->rp_rank[j].grow((size_t)N * sizeof(int32_t)));
+    auto rank_k = [&](int k) { return keep_ranks ? rank_of(k) : (int32_t*)ctx->rp_rank[k % NS].p; };
+    RB_TRY(fork());
     // ---------------------------------------------------------------- phase A
     for (int k = 0; k < K; k++) {
+        cudaStream_t s = ctx->rp_s[k % NS];            // (shadows the call's stream)
+        DevBuf* sws = &ctx->rp_scan[k % NS];
         grappa_part* p = P[k];
         int64_t* d_stat = d_stat0 + (size_t)k * kSt;
         const int64_t n = ncore[k];
@@ -1266,26 +1297,30 @@ extern "C" grappa_status grappa_repartition_batch_ix(grappa_ctx* ctx, const grap
         RB_TRY(p->heavy_rows.grow((size_t)n * 4));
         const int32_t* cg = (const int32_t*)p->core_global.p;
         RB_TRY(device_scan(ctx, FlagCore{chunk_of, bases[k], swepts[k]}, N,
-                           WriteRank{rank_of(k), (int32_t*)p->core_global.p, d_stat}, s));
+                           WriteRank{rank_k(k), (int32_t*)p->core_global.p, d_stat}, s, nullptr, sws));
         unsigned grid;
         rp_grid(ctx, n, 256, &grid);
-        RB_TRY(device_scan(ctx, NumTasks{cg, g->rowptr}, n, WriteTasks{tw[k].off, tw[k].desc, d_stat, cg, g->rowptr}, s));
+        RB_TRY(device_scan(ctx, NumTasks{cg, g->rowptr}, n, WriteTasks{tw[k].off, tw[k].desc, d_stat, cg, g->rowptr}, s,
+                           nullptr, sws));
         {
             const Member mb{nullptr, ec, bases[k], swepts[k], 0};
             k_task_count<true><<<tgrid, 256, 0, s>>>(d_stat + 5, tw[k].desc, g->col, mb, tw[k].cnt);
         }
         GRAPPA_LAUNCHED(ctx);
-        RB_TRY(device_scan(ctx, ReadTcount{tw[k].cnt, d_stat + 5}, Tmax[k], WriteTaskOut{tw[k].out, d_stat}, s));
+        RB_TRY(device_scan(ctx, ReadTcount{tw[k].cnt, d_stat + 5}, Tmax[k], WriteTaskOut{tw[k].out, d_stat}, s,
+                           nullptr, sws));
         k_row_finalize<<<grid, 256, 0, s>>>(n, tw[k].off, tw[k].out, cg, g->rowptr, labels, (int64_t*)p->rowptr.p,
                                              (int32_t*)p->d_l.p, (int32_t*)p->d_g.p, (float*)p->norm_gcn.p,
                                              (float*)p->norm_sage.p, (float*)p->node_w.p, n, (int32_t*)p->labels.p,
                                              (unsigned long long*)(d_stat + 7));
         GRAPPA_LAUNCHED(ctx);
-        RB_TRY(device_scan(ctx, FlagSeed{cg, train_mask}, n, WriteCompact{(int32_t*)p->seeds.p, d_stat, 2}, s));
+        RB_TRY(device_scan(ctx, FlagSeed{cg, train_mask}, n, WriteCompact{(int32_t*)p->seeds.p, d_stat, 2}, s,
+                           nullptr, sws));
         k_heavy_count<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->sm_count * 4)),
                         256, 0, s>>>(n, (const int32_t*)p->d_l.p, (unsigned long long*)(d_stat + 3));
         GRAPPA_LAUNCHED(ctx);
     }
+    RB_TRY(join());
     std::vector<int64_t> st((size_t)K * kSt);
     RB_CUDA(cudaMemcpyAsync(st.data(), d_stat0, (size_t)K * kSt * 8, cudaMemcpyDeviceToHost, s));
     RB_CUDA(cudaStreamSynchronize(s));
@@ -1303,14 +1338,17 @@ extern "C" grappa_status grappa_repartition_batch_ix(grappa_ctx* ctx, const grap
     }
     // ---------------------------------------------------------------- phase B
     double bytes = 0.0;
+    RB_TRY(fork());
     for (int k = 0; k < K; k++) {
+        cudaStream_t s = ctx->rp_s[k % NS];
+        DevBuf* sws = &ctx->rp_scan[k % NS];
         grappa_part* p = P[k];
         const int64_t* h = &st[(size_t)k * kSt];
         const int64_t n = ncore[k], nnz = h[1], n_seeds = h[2], n_heavy = h[3], n_slots = h[4];
         const int32_t* cg = (const int32_t*)p->core_global.p;
-        int32_t* rank = rank_of(k);
+        int32_t* rank = rank_k(k);
         if (!keep_ranks)
-            RB_TRY(device_scan(ctx, FlagCore{chunk_of, bases[k], swepts[k]}, N, WriteRankOnly{rank}, s));
+            RB_TRY(device_scan(ctx, FlagCore{chunk_of, bases[k], swepts[k]}, N, WriteRankOnly{rank}, s, nullptr, sws));
         RB_TRY(p->col.grow((size_t)(nnz > 0 ? nnz : 1) * 4));
         {
             const Member mb{nullptr, ec, bases[k], swepts[k], 0};
@@ -1332,17 +1370,21 @@ extern "C" grappa_status grappa_repartition_batch_ix(grappa_ctx* ctx, const grap
         }
         int nb = seed_stat_blocks(ctx, n_seeds);
         if (nb < 1) nb = 1;
-        RB_TRY(ctx->scan_ws.grow((size_t)nb * sizeof(SeedStats)));
+        // this stream's small workspace: degree-bucket counters, then the seed-statistics partials
+        const size_t bins_b = (size_t)2 * kDegBuckets * 8;
+        RB_TRY(ctx->rp_small[k % NS].grow(bins_b + (size_t)nb * sizeof(SeedStats)));
+        unsigned long long* bins = (unsigned long long*)ctx->rp_small[k % NS].p;
+        SeedStats* sp = (SeedStats*)((char*)ctx->rp_small[k % NS].p + bins_b);
         k_seed_stats<<<nb, kStatThreads, 0, s>>>(n_seeds, (int32_t*)p->seeds.p, (int32_t*)p->d_l.p,
-                                                  (int32_t*)p->d_g.p, (SeedStats*)ctx->scan_ws.p);
+                                                  (int32_t*)p->d_g.p, sp);
         GRAPPA_LAUNCHED(ctx);
-        k_seed_stats_final<<<1, 32, 0, s>>>(nb, (SeedStats*)ctx->scan_ws.p, d_ss0 + k);
+        k_seed_stats_final<<<1, 32, 0, s>>>(nb, sp, d_ss0 + k);
         GRAPPA_LAUNCHED(ctx);
         // SpMM plan with the known split-row sizes (no sync)
         RB_TRY(build_plan_sized(ctx, s, n, (int64_t*)p->rowptr.p, (int32_t*)p->d_l.p,
                                 PlanBufs{&p->heavy_rows, &p->heavy_slot_off, &p->slot_row, &p->slot_seg,
                                          &p->row_order, &p->row_desc},
-                                d_stat0 + (size_t)k * kSt + 8, n_heavy, n_slots));
+                                d_stat0 + (size_t)k * kSt + 8, n_heavy, n_slots, sws, bins));
         p->halo = false;
         p->n_halo = 0;
         p->halo_pending = false;
@@ -1364,6 +1406,7 @@ extern "C" grappa_status grappa_repartition_batch_ix(grappa_ctx* ctx, const grap
         // d_l kept columns + outputs 24 + the feature row read and written
         bytes += (double)n * (8.0 + 24.0 + 2.0 * (feats ? feat_dim * esz : 0)) + 4.0 * (double)h[7] + 4.0 * (double)nnz;
     }
+    RB_TRY(join());
     std::vector<SeedStats> hs(K);
     RB_CUDA(cudaMemcpyAsync(hs.data(), d_ss0, (size_t)K * sizeof(SeedStats), cudaMemcpyDeviceToHost, s));
     RB_CUDA(cudaStreamSynchronize(s));

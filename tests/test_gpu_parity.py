@@ -573,3 +573,43 @@ def test_repartition_batch_bitexact(G, ctx, prod, C, dtype):
     with pytest.raises(G.GrappaError, match="E_EMPTY"):
         G.grappa_repartition_batch(ctx, rp, col, xt, dtype, ch, C, sched[0][:8], torch.zeros_like(tr), y,
                                    chunk_sizes=sizes)
+
+
+def test_controller_drives_switches(G, ctx, prod):
+    """§3.5 controller in the training loop (R32): the trainer feeds every phase's coverage
+    (c_uniform of its partition) to the controller and switches super-epochs when it says so; the
+    switch epochs equal those of the oracle controller fed the oracle partitions' coverages."""
+    from oracle.controller import Controller as OC
+    from paper_2602_01872_b200.controller import Controller
+    from paper_2602_01872_b200.engine import ModelSpec, Trainer
+    ds = prod
+    wl = ds.wl
+    spec = ModelSpec(wl.arch, wl.dims, wl.dims_pad)
+    # a deficit threshold between the partitions' coverages makes some partitions fire early
+    P = wl.chunks
+    chunk_of = Po.make_chunks(wl.n, P, gen.seed_of("chunks"))
+    sched = Po.sweep_schedule(P, P)
+    cov = {}
+    for t in range(len(sched)):
+        for w, (b, s) in enumerate(sched[t]):
+            part = Po.induced_partition(ds.rowptr, ds.col, chunk_of, b, s, ds.train)
+            cov[(t, w)] = Co.c_uniform(part["d_l"][part["seeds"]], part["d_g"][part["seeds"]])
+    vals = sorted(cov.values())
+    m = len(vals) // 2
+    thr = 1.0 - 0.5 * (vals[m - 1] + vals[m])       # between two coverages: no ties at 1e-12
+    mk = lambda: Controller(epochs_total=40, num_chunks=P, deficit_threshold=thr, streak_threshold=2)
+    tr = Trainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights, P, gen.seed_of("chunks"),
+                 corr="uniform", lr=0.0, controller=mk())
+    got = []
+    for _ in range(6):
+        tr.run_epoch()
+        got.append(tr.t)
+    oc = OC(40, P, deficit_threshold=thr, streak_threshold=2)
+    t, ref = 1, []
+    for _ in range(6):
+        ref.append(t)
+        for w in range(P):
+            oc.observe(w, cov[((t - 1) % len(sched), w)])
+        if oc.end_epoch():
+            t += 1
+    assert got == ref and len(set(ref)) > 1, (got, ref)
