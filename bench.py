@@ -387,6 +387,10 @@ def run_grappa(args):
     # timed region starts on a super-epoch boundary -> includes ceil(K/N) repartitions
     tr.epoch = wl.repartition_every * (1 + tr.epoch // wl.repartition_every)
     barrier()
+    if os.environ.get("GRAPPA_BENCH_NOGC") == "1":     # diagnostic: no Python GC pauses while timed
+        import gc
+        gc.collect()
+        gc.disable()
     clocks.mark()
     # CUDA-graph replay of the epoch (one capture per super-epoch): the default on one GPU for
     # full-graph runs (~535 launches per products epoch; replay removes the host launch gaps);

@@ -194,6 +194,7 @@ extern "C" void grappa_ctx_destroy(grappa_ctx* c) {
     c->xf_hdr.release();
     c->comm_buf.release();
     c->wimg.release();
+    c->loss_ws.release();
     for (int i = 0; i < grappa_ctx::kRpStreams; i++) {
         c->rp_scan[i].release();
         c->rp_small[i].release();

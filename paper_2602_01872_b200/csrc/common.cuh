@@ -113,6 +113,7 @@ struct grappa_ctx {
     std::shared_ptr<const grappa::Allocator> alloc;   // caller allocator (null: cudaMalloc)
     grappa::DevBuf comm_buf;     // bf16 communication buffer of grappa_aggregate_grads
     grappa::DevBuf wimg;         // streamed-weight image of the tcgen05 NN GEMM (large K)
+    grappa::DevBuf loss_ws;      // loss partial sums (kept apart from the repartition scratch)
     // side streams of the batched switch (partitions extracted concurrently) and their own
     // workspaces: scan partials, degree-bucket counters + seed-statistics partials, rank table
     static constexpr int kRpStreams = 4;

@@ -87,8 +87,10 @@ grappa_status loss_rows(grappa_ctx* ctx, int64_t n_seeds, const int32_t* rows, c
                  5.0 * n_seeds * K);
     GRAPPA_CUDA(cudaMemsetAsync(dlogits, 0, (size_t)n_rows * k_pad * esz, s));
     const int64_t nb = ceil_div(n_seeds, kLossThreads / 32);
-    GRAPPA_TRY(ctx->red_ws.grow((size_t)nb * sizeof(double)));
-    double* part_sums = (double*)ctx->red_ws.p;
+    // the loss's own scratch: a captured epoch graph references it, and a switch prefetched on a
+    // side stream (engine) may reuse the repartition workspaces while that graph runs
+    GRAPPA_TRY(ctx->loss_ws.grow((size_t)nb * sizeof(double)));
+    double* part_sums = (double*)ctx->loss_ws.p;
     if (dtype == GRAPPA_BF16)
         k_loss<__nv_bfloat16><<<(unsigned)nb, kLossThreads, 0, s>>>(
             n_seeds, rows, lidx, labels, (const __nv_bfloat16*)logits, K, k_pad, (__nv_bfloat16*)dlogits,

@@ -321,6 +321,10 @@ __device__ __forceinline__ void grp_accumulate(const T* __restrict__ X, const in
     const int WV = G;
     const int maxdeg = __reduce_max_sync(0xffffffffu, deg);
     const int CH = G * R;
+    // unweighted gathers: row s of this lane's 16-byte column at base_lane + s * row bytes (one
+    // IMAD.WIDE.U32 per gathered vector instead of the signed 64-bit index arithmetic)
+    const uint64_t base_lane = reinterpret_cast<uint64_t>(X) + (uint64_t)sub * 16;
+    const uint32_t rowb = (uint32_t)WV * 16;
     for (int off = 0; off < maxdeg; off += CH) {
         int idx[R];
         float wt[R];
@@ -346,7 +350,8 @@ __device__ __forceinline__ void grp_accumulate(const T* __restrict__ X, const in
                     const int s = __shfl_sync(0xffffffffu, idx[r], srcl);
                     const bool ok = jj < G && off + r * G + jj < deg;
                     if (ok) v[u] = WT ? Vec<T>::load(X + ((int64_t)s * WV + sub) * E)
-                                      : Vec<T>::load_ordered(X + ((int64_t)s * WV + sub) * E);
+                                      : Vec<T>::load_ordered(reinterpret_cast<const T*>(
+                                            base_lane + (uint64_t)(uint32_t)s * rowb));
                     else v[u] = {};
                 }
                 if (WT) {

@@ -257,6 +257,7 @@ class Trainer:
         epoch graph first: it holds the previous partitions' sizes, SpMM plans, tensor maps,
         coverage factors and buffer pointers, so it must never be replayed on the new layout."""
         self.graph = None
+        self.next_graph = None
         if self.t is not None:
             # the switch synchronises anyway: surface a non-finite aggregate of the last
             # super-epoch now (the device skipped those updates; S:424)
@@ -560,32 +561,64 @@ class Trainer:
         partitions the first epoch of a super-epoch runs eagerly on the main stream while the same
         launches are recorded on a capture stream, so the GPU works through that epoch while the
         host records (capturing alone would leave the GPU idle for the recording +
-        instantiation); on small ones (host-bound epochs) it is recorded only, then replayed."""
+        instantiation); on small ones (host-bound epochs) it is recorded only, then replayed.
+
+        Prefetched switch (fixed-period super-epochs, replicated induced-core partitions): while
+        the GPU replays the LAST epoch of a super-epoch, the host extracts the next super-epoch's
+        partitions into the second partition set on a side stream and records their epoch graph;
+        the next epoch then only swaps the sets and replays.  The switch's host work (its syncs,
+        the ~535 recorded launches) overlaps the GPU instead of pacing it."""
         import os
         import time
         tm = os.environ.get("GRAPPA_GRAPH_TIMING") == "1"     # diagnostic host timings (stderr)
         h0 = time.perf_counter()
         t = self.super_epoch()
         if t != self.t:
-            self.repartition(t)                 # drops the previous super-epoch's graph
+            nxt = getattr(self, "next_graph", None)
+            if nxt is not None and nxt["t"] == t:
+                self._swap_in(nxt)
+            else:
+                self.repartition(t)                 # drops the previous super-epoch's graph
         h1 = time.perf_counter()
         if getattr(self, "graph", None) is not None:
             self.graph.replay()
             if self.controller is not None:    # the captured steps' factors (fixed per super-epoch)
                 self._steps = list(self.graph_steps)
+            self._maybe_prefetch(tm)
             self.end_epoch()
             return
-        g = torch.cuda.CUDAGraph()
-        main = self.stream
-        cap = torch.cuda.Stream(self.dev)
-        cap.wait_stream(main)
-        n_cap, cap_steps, grad_b = 0, [], 0
         # small partitions (host-bound epochs): record only, then replay -- running the epoch
         # eagerly as well would double the host work that bounds them
         # multi-rank: record only (each communicator then sees one stream of collectives: the
         # captured all-reduces replay in the same order on every rank)
         eager = (self.G == 1 and
                  sum(p.nnz for p in self.parts.values()) >= getattr(self, "graph_eager_min_nnz", 4_000_000))
+        g, n_cap, cap_steps, grad_b, h2 = self._capture(eager)
+        h3 = time.perf_counter()
+        if tm:
+            import sys
+            print(f"[graph] repartition {1e3 * (h1 - h0):.1f} ms, record{' + eager' if eager else ''} "
+                  f"{1e3 * (h2 - h1):.1f} ms, capture_end {1e3 * (h3 - h2):.1f} ms", file=sys.stderr)
+        self.graph = g
+        self.graph_launches = n_cap
+        self.graph_grad_bytes = grad_b       # all-reduce payload bytes per replay (comm counters)
+        self.graph_steps = cap_steps
+        if not eager:
+            g.replay()
+            self._steps += cap_steps
+        self._maybe_prefetch(tm)
+        self.end_epoch()
+
+    def _capture(self, eager: bool):
+        """record one epoch of the current self.parts into a CUDA graph (and run it eagerly on the
+        main stream at the same time if `eager`); returns (graph, launches, step factors, grad bytes,
+        host time at the end of the recording)"""
+        import time
+        g = torch.cuda.CUDAGraph()
+        main = self.stream
+        cap = torch.cuda.Stream(self.dev)
+        cap.wait_stream(main)
+        n_cap, cap_steps, grad_b = 0, [], 0
         # capture_begin/end directly: torch.cuda.graph() would also run gc.collect() and
         # empty_cache(); relaxed mode lets the eager launches proceed during the capture
         with torch.cuda.stream(cap):
@@ -614,19 +647,67 @@ class Trainer:
             finally:
                 self.stream = main
                 g.capture_end()
-        h3 = time.perf_counter()
+        return g, n_cap, cap_steps, grad_b, h2
+
+    def _prefetch_ok(self) -> bool:
+        return (getattr(self, "prefetch_switch", True) and self.controller is None and not self.halo
+                and not self.capacity and not self.sharded and self.rep_every >= 1)
+
+    def _maybe_prefetch(self, tm=False):
+        """after launching the replay of the last epoch of a super-epoch: build the next one's
+        partitions into the other set on a side stream and record their graph (see
+        run_epoch_graph)"""
+        import time
+        if not self._prefetch_ok():
+            return
+        t1 = 1 + (self.epoch + 1) // self.rep_every
+        if t1 == self.t or (getattr(self, "next_graph", None) or {}).get("t") == t1:
+            return
+        h0 = time.perf_counter()
+        mine = [w for _, w in self.my_workers() if w < self.W]
+        pairs = self.schedule[(t1 - 1) % len(self.schedule)]
+        if getattr(self, "pf_stream", None) is None:
+            self.pf_stream = torch.cuda.Stream(self.dev)
+            self.alt_parts = {}
+        if getattr(self, "alt_free", None) is not None:
+            self.pf_stream.wait_event(self.alt_free)      # the other set's last graph has finished
+        if getattr(self, "index", None) is None:
+            self.index = Index(self.ctx, self.rowptr, self.col, self.chunk_of, self.C, self.stream)
+        got = grappa_repartition_batch(self.ctx, self.rowptr, self.col, self.x, self.dt, self.chunk_of, self.C,
+                                       [pairs[w] for w in mine], self.train, self.labels,
+                                       [self.alt_parts.get(w) for w in mine], self.pf_stream,
+                                       chunk_sizes=self.chunk_sizes, index=self.index)
+        nparts = dict(zip(mine, got))
+        h1 = time.perf_counter()
+        # buffers for both sets (the running graph's tensors stay valid: any reallocation is
+        # stream-ordered after it on the main stream), then record the next epoch on the new set
+        self._alloc([self._sizes(p) for p in list(self.parts.values()) + list(nparts.values())])
+        self.stream.wait_stream(self.pf_stream)            # the new partitions before their graph
+        cur = self.parts
+        self.parts = nparts
+        try:
+            g, n_cap, cap_steps, grad_b, _ = self._capture(eager=False)
+        finally:
+            self.parts = cur
+        self.next_graph = dict(t=t1, parts=nparts, graph=g, launches=n_cap, steps=cap_steps, grad_bytes=grad_b)
         if tm:
             import sys
-            print(f"[graph] repartition {1e3 * (h1 - h0):.1f} ms, record{' + eager' if eager else ''} "
-                  f"{1e3 * (h2 - h1):.1f} ms, capture_end {1e3 * (h3 - h2):.1f} ms", file=sys.stderr)
-        self.graph = g
-        self.graph_launches = n_cap
-        self.graph_grad_bytes = grad_b       # all-reduce payload bytes per replay (comm counters)
-        self.graph_steps = cap_steps
-        if not eager:
-            g.replay()
-            self._steps += cap_steps
-        self.end_epoch()
+            print(f"[graph] prefetch of super-epoch {t1}: repartition {1e3 * (h1 - h0):.1f} ms, record "
+                  f"{1e3 * (time.perf_counter() - h1):.1f} ms (overlapping the replay)", file=sys.stderr)
+
+    def _swap_in(self, nxt):
+        """switch to the prefetched super-epoch: its partitions and graph become current; the
+        previous set is reused by the next prefetch once its last replay is done"""
+        self.check()             # surface a non-finite aggregate of the last super-epoch (S:424)
+        self.alt_parts, self.parts = self.parts, nxt["parts"]
+        self.alt_free = torch.cuda.Event()
+        self.alt_free.record(self.stream)
+        self.graph = nxt["graph"]
+        self.graph_launches = nxt["launches"]
+        self.graph_grad_bytes = nxt["grad_bytes"]
+        self.graph_steps = nxt["steps"]
+        self.t = nxt["t"]
+        self.next_graph = None
 
     @property
     def nnz(self):
