@@ -677,13 +677,13 @@ def measure_e2e(tr, stream, K, barrier, world, dist, nnz, use_graph=False):
             host[w] = (bufs, st, nb)
             counters["d2h"] += nb
 
-    def enqueue_epoch(s):
+    def enqueue_epoch(s, himg):
         ready = {}
         copy.wait_stream(s)
         for i, w in plan:                           # grappa_part_upload from host buffers
-            if w in host:
+            if w in himg:
                 with torch.cuda.stream(copy):
-                    tr.parts[w].upload(host[w][1], copy)
+                    tr.parts[w].upload(himg[w][1], copy)
                     ready[w] = torch.cuda.Event()
                     ready[w].record(copy)
         tr.stream = s
@@ -694,36 +694,75 @@ def measure_e2e(tr, stream, K, barrier, world, dist, nnz, use_graph=False):
         loss_host.copy_(tr.loss_dev, non_blocking=True)
         tr.stream = stream
 
+    def capture(himg):
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(tr.dev)
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            g.capture_begin(capture_error_mode="relaxed")
+            try:
+                enqueue_epoch(cap, himg)
+            finally:
+                g.capture_end()
+        tr._steps = []
+        return g
+
     graph = None
+    # prefetched switch (as Trainer.run_epoch_graph): during the last replay of a super-epoch the
+    # next partitions are extracted into the second partition set on a side stream, downloaded
+    # into the second set of pinned host images on that stream, and their epoch graph (uploads
+    # included) recorded; the switch epoch then swaps and replays
+    prefetch = use_graph and tr._prefetch_ok()
+    host_alt, nxt = {}, {}
+
+    def prefetch_next():
+        t1 = 1 + (tr.epoch + 1) // rep
+        if not prefetch or t1 == tr.t or nxt.get("t") == t1:
+            return
+        nparts = tr.build_next_parts(t1)
+        for w, p in nparts.items():
+            old = host_alt.get(w, (None,))[0]
+            bufs, st = p.host_image(reuse=old, headroom=0.25)
+            p.download(st, tr.pf_stream)
+            host_alt[w] = (bufs, st, sum(b.numel() * b.element_size() for b in bufs.values()))
+            counters["d2h"] += host_alt[w][2]
+        tr._alloc([tr._sizes(p) for p in list(tr.parts.values()) + list(nparts.values())])
+        stream.wait_stream(tr.pf_stream)            # images and partitions before their graph
+        cur = tr.parts
+        tr.parts = nparts
+        try:
+            g = capture(host_alt)
+        finally:
+            tr.parts = cur
+        nxt.update(t=t1, parts=nparts, graph=g)
 
     def switch_if_due():
-        nonlocal graph
+        nonlocal graph, host, host_alt
         t = tr.super_epoch()
         if t == tr.t and host:
+            return
+        if t != tr.t and nxt.get("t") == t:        # prefetched: swap the sets
+            tr.check()
+            tr.alt_parts, tr.parts = tr.parts, nxt["parts"]
+            host, host_alt = host_alt, host
+            tr.alt_free = torch.cuda.Event()
+            tr.alt_free.record(stream)
+            tr.t = t
+            graph = nxt["graph"]
+            nxt.clear()
             return
         if t != tr.t:
             tr.repartition(t)                       # a3 on the device (syncs)
         refresh_images()
-        graph = None
-        if use_graph:
-            g = torch.cuda.CUDAGraph()
-            cap = torch.cuda.Stream(tr.dev)
-            cap.wait_stream(stream)
-            with torch.cuda.stream(cap):
-                g.capture_begin(capture_error_mode="relaxed")
-                try:
-                    enqueue_epoch(cap)
-                finally:
-                    g.capture_end()
-            tr._steps = []
-            graph = g
+        graph = capture(host) if use_graph else None
 
     def one_epoch():
         switch_if_due()
         if graph is not None:
             graph.replay()
+            prefetch_next()
         else:
-            enqueue_epoch(stream)
+            enqueue_epoch(stream, host)
         counters["h2d"] += sum(host[w][2] for _, w in plan if w in host)
         tr._steps = []
         tr.end_epoch()
@@ -732,6 +771,10 @@ def measure_e2e(tr, stream, K, barrier, world, dist, nnz, use_graph=False):
     # (switch + capture), then K timed epochs holding ceil(K / rep) switches
     tr.epoch = rep * (1 + tr.epoch // rep)
     one_epoch()
+    if prefetch:          # pin the second set of host images before timing (reused thereafter)
+        for w, p in tr.parts.items():
+            bufs, st = p.host_image(headroom=0.25)
+            host_alt[w] = (bufs, st, 0)
     barrier()
     counters["h2d"] = counters["d2h"] = 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

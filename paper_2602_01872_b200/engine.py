@@ -664,20 +664,7 @@ class Trainer:
         if t1 == self.t or (getattr(self, "next_graph", None) or {}).get("t") == t1:
             return
         h0 = time.perf_counter()
-        mine = [w for _, w in self.my_workers() if w < self.W]
-        pairs = self.schedule[(t1 - 1) % len(self.schedule)]
-        if getattr(self, "pf_stream", None) is None:
-            self.pf_stream = torch.cuda.Stream(self.dev)
-            self.alt_parts = {}
-        if getattr(self, "alt_free", None) is not None:
-            self.pf_stream.wait_event(self.alt_free)      # the other set's last graph has finished
-        if getattr(self, "index", None) is None:
-            self.index = Index(self.ctx, self.rowptr, self.col, self.chunk_of, self.C, self.stream)
-        got = grappa_repartition_batch(self.ctx, self.rowptr, self.col, self.x, self.dt, self.chunk_of, self.C,
-                                       [pairs[w] for w in mine], self.train, self.labels,
-                                       [self.alt_parts.get(w) for w in mine], self.pf_stream,
-                                       chunk_sizes=self.chunk_sizes, index=self.index)
-        nparts = dict(zip(mine, got))
+        nparts = self.build_next_parts(t1)
         h1 = time.perf_counter()
         # buffers for both sets (the running graph's tensors stay valid: any reallocation is
         # stream-ordered after it on the main stream), then record the next epoch on the new set
@@ -694,6 +681,24 @@ class Trainer:
             import sys
             print(f"[graph] prefetch of super-epoch {t1}: repartition {1e3 * (h1 - h0):.1f} ms, record "
                   f"{1e3 * (time.perf_counter() - h1):.1f} ms (overlapping the replay)", file=sys.stderr)
+
+    def build_next_parts(self, t1: int) -> dict:
+        """the partitions of super-epoch t1 in the second partition set, extracted on the side
+        stream `pf_stream` (concurrently with work on the main stream); returns worker -> Part"""
+        mine = [w for _, w in self.my_workers() if w < self.W]
+        pairs = self.schedule[(t1 - 1) % len(self.schedule)]
+        if getattr(self, "pf_stream", None) is None:
+            self.pf_stream = torch.cuda.Stream(self.dev)
+            self.alt_parts = {}
+        if getattr(self, "alt_free", None) is not None:
+            self.pf_stream.wait_event(self.alt_free)      # the other set's last graph has finished
+        if getattr(self, "index", None) is None:
+            self.index = Index(self.ctx, self.rowptr, self.col, self.chunk_of, self.C, self.stream)
+        got = grappa_repartition_batch(self.ctx, self.rowptr, self.col, self.x, self.dt, self.chunk_of, self.C,
+                                       [pairs[w] for w in mine], self.train, self.labels,
+                                       [self.alt_parts.get(w) for w in mine], self.pf_stream,
+                                       chunk_sizes=self.chunk_sizes, index=self.index)
+        return dict(zip(mine, got))
 
     def _swap_in(self, nxt):
         """switch to the prefetched super-epoch: its partitions and graph become current; the
