@@ -513,8 +513,13 @@ grappa_status grappa_comm_bytes(const grappa_ctx* ctx, int64_t* grad_bytes, int6
  * from the local partition only), P:382 (Alg. 1 isolated_sampling), P:489 (B = 1000,
  * fanouts {15,10,5}).  Readings R23-R28:
  *   epoch order  seeds sorted by (h(seed, epoch, gid), gid)
- *   hop h        each target v keeps the min(f_h, d_l(v)) local neighbours u with the
- *                smallest (h(h(seed, epoch, batch, h), gid(v), gid(u)), gid(u))
+ *   hop h        each target v keeps min(f_h, d_l(v)) distinct local neighbours, uniform
+ *                without replacement, drawn by Floyd's algorithm over neighbour positions
+ *                (R24; keys h(h(seed, epoch, batch, h), gid(v), j))
+ *   fanouts      each in [1, 32] (P:489's {15,10,5}, {25,10}, {20,15,10,5})
+ *   replay       grappa_sample_async replays the batch's launch sequence as a CUDA graph from
+ *                the second call with the same (partition, n_batch, fanouts) on a non-default
+ *                stream (per-call values through pinned memory); results are identical
  *   sources      targets (prefix, same order) then new nodes in ascending local id
  *   fanouts      listed input -> output layer: hop 1 (the seeds) uses fanouts[L-1]
  * GraphSAGE only (config 4 is SAGE-3). */
