@@ -650,8 +650,10 @@ class Trainer:
         return g, n_cap, cap_steps, grad_b, h2
 
     def _prefetch_ok(self) -> bool:
+        # one rank only: recording a graph with NCCL all-reduces while the previous graph's
+        # all-reduces run on the same communicator has not been exercised on multi-GPU hardware
         return (getattr(self, "prefetch_switch", True) and self.controller is None and not self.halo
-                and not self.capacity and not self.sharded and self.rep_every >= 1)
+                and not self.capacity and not self.sharded and self.rep_every >= 1 and self.G == 1)
 
     def _maybe_prefetch(self, tm=False):
         """after launching the replay of the last epoch of a super-epoch: build the next one's
