@@ -653,10 +653,11 @@ def measure_f32(args, ctx, ds, wl, spec, stream, barrier, world, dist, nnz, use_
 
 def measure_e2e(tr, stream, K, barrier, world, dist, nnz, use_graph=False):
     """Public-API epochs with the step inputs on the host (partitions parked in pinned host
-    memory between phases, as the paper keeps them in CPU memory, P:139 / P:410): before each
-    phase the partition's inputs (local CSR, features, labels, norms, seeds) are copied H2D from
+    memory between phases, as the paper keeps them in CPU memory, P:139 / P:410): every epoch
+    each partition's inputs (local CSR, features, labels, norms, seeds) are copied H2D from
     pinned host memory into its device buffers (grappa_part_upload, on a copy stream overlapping
-    the previous phase) and the epoch's loss is read back D2H.  Super-epoch switches happen at the
+    compute: partition k before phase k, the first phase's partition during the previous
+    epoch) and the epoch's loss is read back D2H.  Super-epoch switches happen at the
     same cadence as in the device-resident run and are inside the timed region: the repartition
     (a3) of every partition, the D2H refresh of the host images, and (use_graph) the capture of
     the new super-epoch's epoch graph; the other epochs replay it (copies as memcpy nodes)."""
@@ -678,19 +679,31 @@ def measure_e2e(tr, stream, K, barrier, world, dist, nnz, use_graph=False):
             counters["d2h"] += nb
 
     def enqueue_epoch(s, himg):
+        # uploads on the copy stream: the partitions of phases 1.. before their phases, and the
+        # partition of phase 0 for the NEXT epoch as soon as this epoch's phase 0 is done (its
+        # upload then overlaps phases 1..; consecutive epochs are ordered, so the next epoch's
+        # phase 0 finds it in place).  Every partition is still uploaded once per epoch.
         ready = {}
         copy.wait_stream(s)
-        for i, w in plan:                           # grappa_part_upload from host buffers
+        first = plan[0][1] if plan else None
+        for i, w in plan[1:]:                       # grappa_part_upload from host buffers
             if w in himg:
                 with torch.cuda.stream(copy):
                     tr.parts[w].upload(himg[w][1], copy)
                     ready[w] = torch.cuda.Event()
                     ready[w].record(copy)
         tr.stream = s
-        for i, w in plan:
+        for k, (i, w) in enumerate(plan):
             if w in ready:
                 s.wait_event(ready[w])
             tr.phase_step(i, w, min(tr.G, tr.W - i * tr.G))
+            if k == 0 and first in himg:
+                done0 = torch.cuda.Event()
+                done0.record(s)
+                copy.wait_event(done0)
+                with torch.cuda.stream(copy):
+                    tr.parts[first].upload(himg[first][1], copy)
+        s.wait_stream(copy)                         # the epoch ends with its uploads
         loss_host.copy_(tr.loss_dev, non_blocking=True)
         tr.stream = stream
 

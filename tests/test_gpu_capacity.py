@@ -105,3 +105,36 @@ def test_graph_epochs_equal_eager(G, prod, dtype, eager_min):
     assert torch.equal(a.theta, b.theta)
     assert a.losses == b.losses if hasattr(a, "losses") else True
     ctx.close()
+
+
+@pytest.mark.parametrize("use_graph", [False, True])
+def test_e2e_epochs_equal_resident(G, prod, use_graph):
+    """bench.measure_e2e (the end-to-end number: every partition uploaded from pinned host images
+    each epoch, the first phase's partition during the previous epoch, the loss read back; with
+    use_graph the epochs are graph replays and switches are prefetched) trains exactly what the
+    device-resident loop trains: theta bitwise equal after 1 + K epochs across super-epoch
+    switches"""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from paper_2602_01872_b200.engine import ModelSpec, Trainer
+    ctx = G.Context(0)
+    ds = prod
+    wl = ds.wl
+    spec = ModelSpec(wl.arch, wl.dims, wl.dims_pad)
+    mk = lambda: Trainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights, wl.chunks,
+                         gen.seed_of("chunks"), corr="uniform", lr=0.05, repartition_every=2, dtype="bf16")
+    a, b = mk(), mk()
+    stream = torch.cuda.current_stream()
+    K = 5
+    r = bench.measure_e2e(a, stream, K, torch.cuda.synchronize, 1, None, ds.nnz, use_graph=use_graph)
+    assert r["h2d_bytes_per_step"] > 0
+    b.epoch = 2                                  # measure_e2e starts on the next boundary
+    for _ in range(1 + K):
+        b.run_epoch()
+    torch.cuda.synchronize()
+    ctx.check()
+    assert a.epoch == b.epoch
+    assert torch.equal(a.theta, b.theta)
+    ctx.close()
