@@ -465,8 +465,10 @@ extern "C" grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part*
     for (int h = 1; h <= n_layers; h++)
         // h(seed, epoch, batch, hop) = mix(seed ^ mix(epoch ^ mix(batch ^ mix(hop))))
         P.key[h - 1] = hmix(seed ^ hmix((uint64_t)epoch ^ hmix((uint64_t)batch_index ^ hmix((uint64_t)h))));
+    // every partition array the sequence reads, by address, and every size it is launched with
     std::vector<int64_t> key = {(int64_t)(uintptr_t)part, (int64_t)(uintptr_t)I.rowptr, (int64_t)(uintptr_t)I.col,
-                                nc, I.nnz, n_batch, n_layers};
+                                (int64_t)(uintptr_t)I.core_global, (int64_t)(uintptr_t)I.d_l,
+                                (int64_t)(uintptr_t)I.d_g, nc, I.nnz, n_batch, n_layers};
     for (int l = 0; l < n_layers; l++) key.push_back(fanouts[l]);
     // not on the legacy default stream (cannot be captured), not inside a caller's own capture,
     // not while per-kernel-class profiling records events
