@@ -116,7 +116,7 @@ struct grappa_ctx {
     grappa::DevBuf loss_ws;      // loss partial sums (kept apart from the repartition scratch)
     // side streams of the batched switch (partitions extracted concurrently) and their own
     // workspaces: scan partials, degree-bucket counters + seed-statistics partials, rank table
-    static constexpr int kRpStreams = 4;
+    static constexpr int kRpStreams = 8;
     cudaStream_t rp_s[kRpStreams] = {};
     cudaEvent_t rp_ev[kRpStreams + 1] = {};
     grappa::DevBuf rp_scan[kRpStreams], rp_small[kRpStreams], rp_rank[kRpStreams];
