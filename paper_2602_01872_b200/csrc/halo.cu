@@ -299,10 +299,14 @@ extern "C" grappa_status grappa_halo_exchange(grappa_ctx* ctx, grappa_part* part
             (int32_t*)part->labels.p, (float*)part->node_w.p);
         GRAPPA_LAUNCHED(ctx);
     }
+    // every rank learns whether any server met a request it does not hold (the requester's halo
+    // rows would otherwise hold whatever that server sent)
+    if (!local_only) HX_NCCL(ncclAllReduce(d_bad, d_bad, 1, ncclInt32, ncclMax, comm, s));
     int bad = 0;
     GRAPPA_CUDA(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, s));
     GRAPPA_CUDA(cudaStreamSynchronize(s));
-    GRAPPA_ARG(!bad, GRAPPA_E_ARG, "grappa_halo_exchange: a requested halo node is not in its owner's shards");
+    GRAPPA_ARG(!bad, GRAPPA_E_ARG,
+               "grappa_halo_exchange: a requested halo node is not in its owner's shards (on some rank)");
     if (part) part->halo_pending = false;
     return GRAPPA_OK;
 }

@@ -195,11 +195,19 @@ def test_sharded_halo_partition_bitexact(G, prod, dtype, nccl):
         assert np.array_equal(p.core_global.cpu().numpy(), ref["core"])
         assert np.array_equal(p.col.cpu().numpy(), ref["col"])
         assert np.array_equal(p.d_g.cpu().numpy(), ref["d_g"])
+    q = G.grappa_repartition_shards(ctx, sh[0], sh[1], ch, C, halo=True)
     if nccl:
         # a shard this rank does not own is refused before anything moves
-        q = G.grappa_repartition_shards(ctx, sh[0], sh[1], ch, C, halo=True)
         with pytest.raises(G.GrappaError, match="E_ARG"):
             G.grappa_halo_exchange(ctx, q, [sh[2]], [0, 0, 1] + [0] * (C - 3), ch, C)
+    # an owner that does not hold the requested rows: reported (on every rank), the partition
+    # stays pending
+    with pytest.raises(G.GrappaError, match="not in its owner"):
+        G.grappa_halo_exchange(ctx, q, [sh[0], sh[1]], [0] * C, ch, C)
+    with pytest.raises(G.GrappaError, match="pending"):
+        h = torch.zeros(q.n_core, 16, device="cuda")
+        G.grappa_layer_fwd_ex(ctx, q, "gcn", 16, 16, True, h, torch.zeros(16, 16, device="cuda"), h.clone(),
+                              None, torch.empty(1 << 20, dtype=torch.uint8, device="cuda"), "f32", 0)
     ctx.check()
     ctx.close()
 
