@@ -39,6 +39,22 @@ static uint64_t hmix(uint64_t x) {
     return z ^ (z >> 31);
 }
 
+// Per-call parameters of grappa_sample_async, written by the host into pinned memory and copied
+// to the device by the call itself, so that the call's launch sequence is identical from batch to
+// batch and can be replayed as a CUDA graph (the batch index and epoch only enter the hop keys,
+// the seed slice only enters k_sample_prep).
+struct SampleParams {
+    int64_t n_batch;
+    const int32_t* batch;
+    uint64_t key[kMaxLayers];   // h(seed, epoch, batch, hop) per hop
+    // the partition the batch is drawn from (parameters too, so one recorded sequence serves
+    // every partition whose size fits the buffers: the phases of an epoch cycle through them)
+    const int64_t* rowptr;
+    const int32_t* col;
+    const int32_t* gid;
+    const int32_t* d_l;
+    const int32_t* d_g;
+};
 // R24: per target, f distinct local neighbour positions by Floyd's algorithm -- for j = d-f .. d-1
 // draw t = floor(h(key0, gid(v), j) (j+1) / 2^64) uniform on [0, j] and keep t, or j if t is
 // already kept: every f-subset equally likely (uniform without replacement), O(f) work per
@@ -48,11 +64,13 @@ static uint64_t hmix(uint64_t x) {
 // saves the separate marking pass over the picks.
 template <int MAXF>
 __global__ void k_pick_floyd(const int64_t* __restrict__ d_nt, const int32_t* __restrict__ targets,
-                             const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                             const int32_t* __restrict__ gid, int f, const uint64_t* __restrict__ d_key,
+                             const SampleParams* __restrict__ P, int f, int hop,
                              int32_t* __restrict__ picks, int32_t* __restrict__ cnt, uint32_t* __restrict__ bitmap) {
     const int64_t nt = *d_nt;
-    const uint64_t key0 = *d_key;
+    const uint64_t key0 = P->key[hop];
+    const int64_t* __restrict__ rowptr = P->rowptr;
+    const int32_t* __restrict__ col = P->col;
+    const int32_t* __restrict__ gid = P->gid;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = targets[t];
         const int64_t e0 = rowptr[v], d = rowptr[v + 1] - e0;
@@ -145,8 +163,9 @@ __global__ void k_fill_block(const int64_t* __restrict__ d_nt, const int64_t* __
                              int f, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ where,
                              int32_t* __restrict__ col, int32_t* __restrict__ erow, int32_t* __restrict__ key_pad,
                              float* __restrict__ inv_cnt, const int32_t* __restrict__ targets,
-                             const int32_t* __restrict__ d_l, const int32_t* __restrict__ d_g,
-                             float* __restrict__ inv_cnt_node) {
+                             const SampleParams* __restrict__ P, float* __restrict__ inv_cnt_node) {
+    const int32_t* __restrict__ d_l = P->d_l;
+    const int32_t* __restrict__ d_g = P->d_g;
     const int64_t nt = *d_nt, nnz = *d_nnz;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
         const int c = cnt[t];
@@ -188,8 +207,10 @@ __global__ void k_trowptr(const int64_t* __restrict__ d_ns, const int64_t* __res
 struct BatchStats {
     double sum_r, D, num, den;
 };
-__global__ void k_batch_stats(int n, const int32_t* seeds, const int32_t* d_l, const int32_t* d_g,
+__global__ void k_batch_stats(int n, const int32_t* seeds, const SampleParams* __restrict__ P,
                               const int64_t* brow, BatchStats* out) {
+    const int32_t* d_l = P->d_l;
+    const int32_t* d_g = P->d_g;
     __shared__ BatchStats sh[256];
     BatchStats a{0, 0, 0, 0};
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -214,15 +235,6 @@ __global__ void k_batch_stats(int n, const int32_t* seeds, const int32_t* d_l, c
     }
 }
 
-// Per-call parameters of grappa_sample_async, written by the host into pinned memory and copied
-// to the device by the call itself, so that the call's launch sequence is identical from batch to
-// batch and can be replayed as a CUDA graph (the batch index and epoch only enter the hop keys,
-// the seed slice only enters k_sample_prep).
-struct SampleParams {
-    int64_t n_batch;
-    const int32_t* batch;
-    uint64_t key[kMaxLayers];   // h(seed, epoch, batch, hop) per hop
-};
 __global__ void k_sample_prep(const SampleParams* __restrict__ P, int32_t* __restrict__ seeds, int64_t* __restrict__ d_nt) {
     const int64_t n = P->n_batch;
     const int32_t* src = P->batch;
@@ -275,6 +287,7 @@ struct grappa_batch {
     std::vector<Cached> graphs;
     std::vector<std::vector<int64_t>> seen;   // keys run eagerly once (capture on the next call)
     uint64_t gen = 0, tick = 0;
+    int64_t nc_cap = 0;                        // node capacity of the buffers / launches
 };
 static constexpr int kSampleGraphs = 16;
 // identity of every buffer the launch sequence touches: a change means a graph captured earlier
@@ -342,10 +355,10 @@ extern "C" grappa_status grappa_sample(grappa_ctx* ctx, const grappa_part* part,
 // clear, Floyd pick (+ marking), unmark, two scans, block fill, radix-sort transpose, transpose
 // rowptr; then the batch statistics.  Every size comes from device counters or from the call key
 // (n_batch, fanouts, partition), so the sequence is the same for every batch of that key.
-static grappa_status sample_body(grappa_ctx* ctx, const grappa_part* part, grappa_batch* b, int32_t n_batch,
+static grappa_status sample_body(grappa_ctx* ctx, grappa_batch* b, int64_t nc, int32_t n_batch,
                                  const int32_t* fanouts, int32_t n_layers, cudaStream_t s) {
-    const grappa_part_info& I = part->info;
-    const int64_t nc = I.n_core;
+    // nc: the node capacity the buffers and launches are sized for (>= the partition's n_core;
+    // bitmap words past the partition stay zero, so scanning them adds nothing)
     int64_t* dc = (int64_t*)b->counts.p;
     BatchStats* dstat = (BatchStats*)(dc + 3 * kMaxLayers);
     SampleParams* dp = (SampleParams*)b->dparams.p;
@@ -382,8 +395,7 @@ static grappa_status sample_body(grappa_ctx* ctx, const grappa_part* part, grapp
         {
             auto kp = f <= 16 ? k_pick_floyd<16> : k_pick_floyd<32>;
             kp<<<(unsigned)std::min<int64_t>(ceil_div(cap_t, 256), (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
-                d_nt, targets, I.rowptr, I.col, I.core_global, f, &dp->key[h - 1], (int32_t*)b->picks.p,
-                (int32_t*)b->cnt.p, (uint32_t*)b->bitmap.p);
+                d_nt, targets, dp, f, h - 1, (int32_t*)b->picks.p, (int32_t*)b->cnt.p, (uint32_t*)b->bitmap.p);
         }
         GRAPPA_LAUNCHED(ctx);
         k_unmark<<<(unsigned)std::min<int64_t>(ceil_div(cap_t, 256), 4096), 256, 0, s>>>(
@@ -397,7 +409,7 @@ static grappa_status sample_body(grappa_ctx* ctx, const grappa_part* part, grapp
         (f <= 16 ? k_fill_block<16> : k_fill_block<32>)<<<tgrid, 256, 0, s>>>(d_nt, d_nnz, cap_nnz, (int32_t*)b->picks.p, (int32_t*)b->cnt.p, f,
                                            (int64_t*)B.rowptr.p, (int32_t*)b->where.p, (int32_t*)B.col.p,
                                            (int32_t*)b->erow.p, (int32_t*)b->key_pad.p, (float*)B.inv_cnt.p,
-                                           targets, I.d_l, I.d_g, (float*)B.inv_cnt_node.p);
+                                           targets, dp, (float*)B.inv_cnt_node.p);
         GRAPPA_LAUNCHED(ctx);
         int end_bit = 1;
         while (((int64_t)1 << end_bit) - 1 <= cap_s) end_bit++;
@@ -413,7 +425,7 @@ static grappa_status sample_body(grappa_ctx* ctx, const grappa_part* part, grapp
         cap_t = cap_s;
     }
     // batch coverage statistics over the seeds (hop 1 = output layer block)
-    k_batch_stats<<<1, 256, 0, s>>>(n_batch, (const int32_t*)b->seedbuf.p, I.d_l, I.d_g,
+    k_batch_stats<<<1, 256, 0, s>>>(n_batch, (const int32_t*)b->seedbuf.p, dp,
                                     (int64_t*)b->blk[n_layers - 1].rowptr.p, dstat);
     GRAPPA_LAUNCHED(ctx);
     return GRAPPA_OK;
@@ -447,7 +459,10 @@ extern "C" grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part*
     }
     b->L = n_layers;
     b->n_batch = n_batch;
-    const int64_t nc = I.n_core;
+    // node capacity of the launch sequence: grows with 1/8 headroom, so one recorded sequence
+    // serves every partition of a run (their sizes differ by a few %)
+    if (I.n_core > b->nc_cap) b->nc_cap = I.n_core + I.n_core / 8;
+    const int64_t nc = b->nc_cap;
     // device counters: per hop n_t, n_s, nnz (3 x kMaxLayers int64) + stats
     GRAPPA_TRY(b->counts.grow(3 * kMaxLayers * 8 + sizeof(BatchStats) + 64));
     GRAPPA_TRY(b->bitmap.grow((size_t)ceil_div(nc, 32) * 4));
@@ -462,13 +477,16 @@ extern "C" grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part*
     SampleParams& P = *b->hparams;
     P.n_batch = n_batch;
     P.batch = batch;
+    P.rowptr = I.rowptr;
+    P.col = I.col;
+    P.gid = I.core_global;
+    P.d_l = I.d_l;
+    P.d_g = I.d_g;
     for (int h = 1; h <= n_layers; h++)
         // h(seed, epoch, batch, hop) = mix(seed ^ mix(epoch ^ mix(batch ^ mix(hop))))
         P.key[h - 1] = hmix(seed ^ hmix((uint64_t)epoch ^ hmix((uint64_t)batch_index ^ hmix((uint64_t)h))));
-    // every partition array the sequence reads, by address, and every size it is launched with
-    std::vector<int64_t> key = {(int64_t)(uintptr_t)part, (int64_t)(uintptr_t)I.rowptr, (int64_t)(uintptr_t)I.col,
-                                (int64_t)(uintptr_t)I.core_global, (int64_t)(uintptr_t)I.d_l,
-                                (int64_t)(uintptr_t)I.d_g, nc, I.nnz, n_batch, n_layers};
+    // every size the sequence is launched with (the partition itself is a parameter)
+    std::vector<int64_t> key = {nc, n_batch, n_layers};
     for (int l = 0; l < n_layers; l++) key.push_back(fanouts[l]);
     // not on the legacy default stream (cannot be captured), not inside a caller's own capture,
     // not while per-kernel-class profiling records events
@@ -496,7 +514,7 @@ extern "C" grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part*
         // capture the sequence (buffers already sized by the eager call with this key)
         const int64_t l0 = ctx->launches;
         GRAPPA_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        const grappa_status st = sample_body(ctx, part, b, n_batch, fanouts, n_layers, s);
+        const grappa_status st = sample_body(ctx, b, nc, n_batch, fanouts, n_layers, s);
         cudaGraph_t g = nullptr;
         const cudaError_t ce = cudaStreamEndCapture(s, &g);
         grappa_batch::Cached c;
@@ -508,7 +526,7 @@ extern "C" grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part*
             // the capture): run it eagerly; the next call with this key tries again
             cudaGetLastError();
             ctx->launches = l0;
-            GRAPPA_TRY(sample_body(ctx, part, b, n_batch, fanouts, n_layers, s));
+            GRAPPA_TRY(sample_body(ctx, b, nc, n_batch, fanouts, n_layers, s));
             b->gen = batch_layout(b);
             for (auto& x : b->graphs) cudaGraphExecDestroy(x.exec);
             b->graphs.clear();
@@ -528,7 +546,7 @@ extern "C" grappa_status grappa_sample_async(grappa_ctx* ctx, const grappa_part*
         b->graphs.push_back(c);
         GRAPPA_CUDA(cudaGraphLaunch(c.exec, s));
     } else {
-        GRAPPA_TRY(sample_body(ctx, part, b, n_batch, fanouts, n_layers, s));
+        GRAPPA_TRY(sample_body(ctx, b, nc, n_batch, fanouts, n_layers, s));
         if (batch_layout(b) != b->gen) {             // this call moved buffers
             for (auto& c : b->graphs) cudaGraphExecDestroy(c.exec);
             b->graphs.clear();
