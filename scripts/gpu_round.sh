@@ -36,7 +36,7 @@ if [ "${SIDE:-1}" != "0" ]; then
   for spec in "f32:--dtype f32 $nb" "sharded:--sharded $nb" "halo:--halo $nb" "sharded_halo:--sharded --halo $nb" \
               "node:--corr node $nb" "capshards:--capacity shards $nb" "rmat26_capshards:--config rmat26 --capacity shards $nb" \
               "rmat24:--config rmat24 $nb" "rmat26:--config rmat26 $nb" "arxiv:--config arxiv" "cora:--config cora" \
-              "gat:--config products_gat $nb" "capacity:--capacity $nb" "papers:--config papers --steps 2 --warmup 1 $nb"; do
+              "gat:--config products_gat $nb" "capacity:--capacity $nb" "papers:--config papers --steps 4 --warmup 1 $nb"; do
     name=${spec%%:*}; a=${spec#*:}
     timeout 1200 python bench.py $a > gpurun_out/${TAG}_bench_${name}.json 2> gpurun_out/${TAG}_bench_${name}.err
     echo "bench $name exit $?"; python -c "import json,sys; d=json.load(open(sys.argv[1])); c=d['config']; print(d['ms_per_step'], c['epoch_ms']['median'], (d.get('e2e') or {}).get('ms_per_step'), c.get('repartition_ms_per_switch'), c.get('device_mem_peak_gb'))" gpurun_out/${TAG}_bench_${name}.json
