@@ -631,7 +631,8 @@ typedef enum {
  *   op "spmm": 0 = row-group kernel (rows of <= 32 vectors) over the degree-bucketed row order
  *              (default), 1 = warp per row, 2 = row-group with 8 loads in flight, 3 = row-group
  *              over the natural row order, 4 = TMA row gathers into a shared-memory ring (spmm_tma.cu; bf16
- *              unweighted widths 80..128 only, others fall back to 0).
+ *              unweighted widths 80..128 only, others fall back to 0), 5 = row-group with the
+ *              previous per-edge-predicated unweighted schedule (same sums, bitwise).
  *   op "pair": 0 = GCN backward computes dz_in and dW in one pass over dT and h_in (bf16,
  *              default), 1 = the two separate GEMMs.
  * Returns E_ARG for a null ctx, an unknown op or an out-of-range variant. */

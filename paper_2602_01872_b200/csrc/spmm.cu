@@ -85,10 +85,11 @@ __device__ __forceinline__ void ffma2(float& a0, float& a1, float w, float x0, f
         : "+f"(a0), "+f"(a1)
         : "f"(x0), "f"(x1), "f"(w));
 }
-// dispatch knob (tests / A-B timing) for narrow rows: 0 = row-group kernel with 4 feature
-// loads in flight per lane (default; measured best), 1 = warp-per-row kernel, 2 = row-group
+// dispatch knob (tests / A-B timing) for narrow rows: 0 = row-group kernel, unweighted gathers
+// through grp_accumulate_lean (default; measured best), 1 = warp-per-row kernel, 2 = row-group
 // kernel with 8 loads in flight (more registers, fewer resident warps: slower on B200),
-// 3 = row-group kernel over the rows in natural order (no degree bucketing)
+// 3 = row-group kernel over the rows in natural order (no degree bucketing), 4 = TMA row gather
+// (spmm_tma.cu), 5 = row-group kernel with the previous unweighted schedule (grp_accumulate)
 static inline int spmm_var(const grappa_ctx* c) { return c ? c->var_spmm : 0; }
 
 // Gather-sum of edges [e0, e1) of one row into acc (lanes of slot `slot`, sub-lane `sub`).
@@ -379,11 +380,74 @@ __device__ __forceinline__ void grp_accumulate(const T* __restrict__ X, const in
     }
 }
 
+// Predicated gather-add of one 16-byte vector: `ok` guards both the load and the adds, so a
+// masked-off edge costs neither a zeroing move nor a wasted add (ISETP once, shared by both).
+__device__ __forceinline__ void pred_gather_add(float (&acc)[8], const __nv_bfloat16* p, bool ok) {
+    uint32_t x0, x1, x2, x3;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+                 "@q ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%5];\n\t}"
+                 : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3) : "r"((int)ok), "l"(p));
+    asm volatile("{\n\t.reg .pred q;\n\t.reg .b16 l0, h0, l1, h1, l2, h2, l3, h3;\n\t"
+                 "setp.ne.b32 q, %12, 0;\n\t"
+                 "mov.b32 {l0, h0}, %8;\n\tmov.b32 {l1, h1}, %9;\n\t"
+                 "mov.b32 {l2, h2}, %10;\n\tmov.b32 {l3, h3}, %11;\n\t"
+                 "@q add.rn.f32.bf16 %0, l0, %0;\n\t@q add.rn.f32.bf16 %1, h0, %1;\n\t"
+                 "@q add.rn.f32.bf16 %2, l1, %2;\n\t@q add.rn.f32.bf16 %3, h1, %3;\n\t"
+                 "@q add.rn.f32.bf16 %4, l2, %4;\n\t@q add.rn.f32.bf16 %5, h2, %5;\n\t"
+                 "@q add.rn.f32.bf16 %6, l3, %6;\n\t@q add.rn.f32.bf16 %7, h3, %7;\n\t}"
+                 : "+f"(acc[0]), "+f"(acc[1]), "+f"(acc[2]), "+f"(acc[3]), "+f"(acc[4]), "+f"(acc[5]),
+                   "+f"(acc[6]), "+f"(acc[7])
+                 : "r"(x0), "r"(x1), "r"(x2), "r"(x3), "r"((int)ok));
+}
+__device__ __forceinline__ void pred_gather_add(float (&acc)[4], const float* p, bool ok) {
+    if (ok) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+        acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
+    }
+}
+
+// Unweighted gather-accumulate (every GCN call after R29, SAGE forward): same rows, lanes and
+// summation order as grp_accumulate<.., false> (bitwise the same sums), but the edges of a
+// G-edge sub-chunk are walked in groups of UL with compile-time offsets and one predicate per
+// edge that guards both the load and its adds, and the next sub-chunk's column index is loaded
+// while this one is gathered: a gathered vector costs a shuffle, a compare, an IMAD.WIDE, the
+// load and its 8 adds (~14 issue slots) instead of ~20-24 (per-edge lane / bound arithmetic,
+// selects, zeroing moves; the kernel is issue-bound).  Measured on a products partition (bf16
+// 128 wide): 346 -> 222 us per call with UL = 2 at 32 registers (UL = 1: 247, 3: 237, UL = 4 at
+// 40 registers: 240; the whole 32-edge sub-chunk unrolled spilled).
+template <typename T, int UL>
+__device__ __forceinline__ void grp_accumulate_lean(const T* __restrict__ X, const int32_t* __restrict__ col,
+                                                    int64_t e0, int deg, int G, int slot, int sub,
+                                                    float (&acc)[Vec<T>::EPV]) {
+    const int maxdeg = __reduce_max_sync(0xffffffffu, deg);
+    const uint64_t base_lane = reinterpret_cast<uint64_t>(X) + (uint64_t)sub * 16;
+    const uint32_t rowb = (uint32_t)G * 16;
+    const int slotG = slot * G;
+    const int32_t* cl = col + e0 + sub;
+    int idx = sub < deg ? __ldg(cl) : 0;
+    for (int off = 0; off < maxdeg; off += G) {
+        // the next sub-chunk's index is in flight while this one's rows are gathered
+        const int nidx = off + G + sub < deg ? __ldg(cl + off + G) : 0;
+        const int jmax = min(G, maxdeg - off);          // warp-uniform
+        const int rem = min(G, deg - off);              // this lane's valid edges here
+#pragma unroll 1
+        for (int jb = 0; jb < jmax; jb += UL) {
+            const int lb = slotG + jb, rb = rem - jb;
+#pragma unroll
+            for (int u = 0; u < UL; u++) {
+                const uint32_t s = (uint32_t)__shfl_sync(0xffffffffu, idx, lb + u);
+                pred_gather_add(acc, reinterpret_cast<const T*>(base_lane + (uint64_t)s * rowb), u < rb);
+            }
+        }
+        idx = nidx;
+    }
+}
+
 // Narrow rows: every group of G = W/EPV lanes owns a different row, so a warp carries
 // P = 32/G independent rows and their dependent load chains (rowptr -> col -> scale /
 // feature row) overlap; no cross-group reduction is needed.
-template <typename T, int R, int U, bool WT>
-__global__ void __launch_bounds__(256) k_spmm_grp(SpmmArgs a, int G, int P) {
+template <typename T, int R, int U, bool WT, bool LEAN = false, int MB = 1>
+__global__ void __launch_bounds__(256, MB) k_spmm_grp(SpmmArgs a, int G, int P) {
     constexpr int E = Vec<T>::EPV;
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -418,8 +482,12 @@ __global__ void __launch_bounds__(256) k_spmm_grp(SpmmArgs a, int G, int P) {
     float acc[E];
 #pragma unroll
     for (int q = 0; q < E; q++) acc[q] = 0.f;
-    grp_accumulate<T, R, U, WT>(reinterpret_cast<const T*>(a.X), a.col, a.col_scale, e0, (int)(e1 - e0),
-                                G, slot, sub, acc, a.edge_w);
+    if (LEAN)
+        grp_accumulate_lean<T, U>(reinterpret_cast<const T*>(a.X), a.col, e0, (int)(e1 - e0), G, slot,
+                                          sub, acc);
+    else
+        grp_accumulate<T, R, U, WT>(reinterpret_cast<const T*>(a.X), a.col, a.col_scale, e0, (int)(e1 - e0),
+                                    G, slot, sub, acc, a.edge_w);
     if (orow < 0) return;
     if (to_partial) {
         float* dst = a.partial + ((int64_t)orow * WV + sub) * E;
@@ -506,7 +574,8 @@ static grappa_status launch_grp(grappa_ctx* ctx, const SpmmArgs& a, int G, cudaS
             else k_spmm_grp<T, R, 8, false><<<grid, 256, 0, s>>>(a, G, P);
         } else {
             if (a.col_scale || a.edge_w) k_spmm_grp<T, R, 4, true><<<grid, 256, 0, s>>>(a, G, P);
-            else k_spmm_grp<T, R, 4, false><<<grid, 256, 0, s>>>(a, G, P);
+            else if (spmm_var(ctx) == 5) k_spmm_grp<T, R, 4, false><<<grid, 256, 0, s>>>(a, G, P);
+            else k_spmm_grp<T, R, 2, false, true, 8><<<grid, 256, 0, s>>>(a, G, P);
         }
         GRAPPA_LAUNCHED(ctx);
     }

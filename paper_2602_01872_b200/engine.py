@@ -370,7 +370,9 @@ class Trainer:
         if sizes is None:
             sizes = [self._sizes(p) for p in self.parts.values()]
         n_max = max([1] + [z[0] for z in sizes])
+        changed = False
         if getattr(self, "_n_cap", 0) < n_max:
+            changed = True
             self._n_cap = n_cap = n_max + n_max // 8
             self.H = [None] + [torch.empty(n_cap, sp.dims_pad[l], dtype=self.tdt, device=self.dev)
                                for l in range(1, sp.depth + 1)]
@@ -384,10 +386,17 @@ class Trainer:
             old = self.saved[l] if getattr(self, "saved", None) else None
             if sb and (old is None or old.numel() < sb):
                 old = torch.empty(sb + sb // 8, dtype=torch.uint8, device=self.dev)
+                changed = True
             saved.append(old if sb else None)
         if getattr(self, "ws", None) is None or self.ws.numel() < ws:
             self.ws = torch.empty(ws + ws // 8, dtype=torch.uint8, device=self.dev)
+            changed = True
         self.saved = saved
+        if changed:
+            # a captured epoch holds the old buffers' pointers: never replay it on the new ones
+            # (the prefetch path reallocates after its last replay was launched and installs
+            # the freshly recorded graph at the switch)
+            self.graph = None
 
     # ------------------------------------------------------------------ one iteration
     def forward_backward(self, part: Part):
