@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(256, MB) k_spmm_grp(SpmmArgs a, int G, int P) 
     for (int q = 0; q < E; q++) acc[q] = 0.f;
     if (LEAN)
         grp_accumulate_lean<T, U>(reinterpret_cast<const T*>(a.X), a.col, e0, (int)(e1 - e0), G, slot,
-                                          sub, acc);
+                                  sub, acc);
     else
         grp_accumulate<T, R, U, WT>(reinterpret_cast<const T*>(a.X), a.col, a.col_scale, e0, (int)(e1 - e0),
                                     G, slot, sub, acc, a.edge_w);
@@ -573,6 +573,9 @@ static grappa_status launch_grp(grappa_ctx* ctx, const SpmmArgs& a, int G, cudaS
             if (a.col_scale || a.edge_w) k_spmm_grp<T, R, 8, true><<<grid, 256, 0, s>>>(a, G, P);
             else k_spmm_grp<T, R, 8, false><<<grid, 256, 0, s>>>(a, G, P);
         } else {
+            // weighted gathers keep grp_accumulate: a lean weighted walk (weight loaded one
+            // sub-chunk ahead and shuffled with the index, predicated FFMA2) measured no faster
+            // (GCN input layer 378 -> 402 us per products call; node-level epoch 41.7 -> 42.4 ms)
             if (a.col_scale || a.edge_w) k_spmm_grp<T, R, 4, true><<<grid, 256, 0, s>>>(a, G, P);
             else if (spmm_var(ctx) == 5) k_spmm_grp<T, R, 4, false><<<grid, 256, 0, s>>>(a, G, P);
             else k_spmm_grp<T, R, 2, false, true, 8><<<grid, 256, 0, s>>>(a, G, P);

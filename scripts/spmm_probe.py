@@ -1,6 +1,8 @@
 """SpMM kernel probe on a products-shaped partition (bf16, GCN hidden layer 128 -> 128): times
 the aggregation per kernel variant with the library's profiling scopes (CUDA events).
-Usage: python scripts/spmm_probe.py [reps] [variants, e.g. 0,2] [width]"""
+Usage: python scripts/spmm_probe.py [reps] [variants, e.g. 0,2] [width] [flags]
+flags: grappa_layer_fwd_ex flags, e.g. 8 = GCN input layer (aggregate-first: the weighted
+gather over the source norms at width f_in), 4 = node-level (weighted by d_l/d_g)"""
 import os
 import sys
 
@@ -17,6 +19,7 @@ def main():
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
     variants = [int(v) for v in (sys.argv[2] if len(sys.argv) > 2 else "0,2").split(",")]
     width = int(sys.argv[3]) if len(sys.argv) > 3 else 128
+    flags = int(sys.argv[4]) if len(sys.argv) > 4 else 0
     G.load()
     wl = gen.WORKLOADS["products"]
     ds = gen.make_dataset(wl)
@@ -33,16 +36,18 @@ def main():
     h = torch.randn(n, width, device=d, generator=g).to(torch.bfloat16)
     w = (torch.randn(width, width, device=d, generator=g) / 11).contiguous()
     out = torch.empty(n, width, device=d, dtype=torch.bfloat16)
-    ws = torch.empty(G.layer_ws_bytes(part, "gcn", width, width, "bf16"), dtype=torch.uint8, device=d)
+    ws = torch.empty(G.layer_ws_bytes(part, "gcn", width, width, "bf16") * 2, dtype=torch.uint8, device=d)
+    saved = torch.empty(max(1, G.layer_saved_bytes(part, "gcn", width, width, "bf16", flags)), dtype=torch.uint8,
+                        device=d)
     ref = None
     for v in variants:
         ctx.set_variant("spmm", v)
         for _ in range(2):
-            G.grappa_layer_fwd(ctx, part, "gcn", width, width, True, h, w, out, None, ws, "bf16")
+            G.grappa_layer_fwd_ex(ctx, part, "gcn", width, width, True, h, w, out, saved, ws, "bf16", flags)
         torch.cuda.synchronize()
         ctx.profile(True)
         for _ in range(reps):
-            G.grappa_layer_fwd(ctx, part, "gcn", width, width, True, h, w, out, None, ws, "bf16")
+            G.grappa_layer_fwd_ex(ctx, part, "gcn", width, width, True, h, w, out, saved, ws, "bf16", flags)
         ms, calls, by, _ = ctx.profile_read("spmm")
         ctx.profile(False)
         torch.cuda.synchronize()
