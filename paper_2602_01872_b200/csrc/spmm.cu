@@ -89,7 +89,11 @@ __device__ __forceinline__ void ffma2(float& a0, float& a1, float w, float x0, f
 // through grp_accumulate_lean (default; measured best), 1 = warp-per-row kernel, 2 = row-group
 // kernel with 8 loads in flight (more registers, fewer resident warps: slower on B200),
 // 3 = row-group kernel over the rows in natural order (no degree bucketing), 4 = TMA row gather
-// (spmm_tma.cu), 5 = row-group kernel with the previous unweighted schedule (grp_accumulate)
+// (spmm_tma.cu), 5 = row-group kernel with the previous unweighted schedule (grp_accumulate).
+// Measured and not kept: a persistent grid-stride version of the lean kernel (255 vs 220 us per
+// products call: static row-group assignment loses the block scheduler's balancing) and a
+// packed epilogue (FMUL2 / FFMA2, ReLU folded into the bf16 pack) with a division-free slot
+// split (242 vs 220 us: more live registers, spills at the 32-register bound).
 static inline int spmm_var(const grappa_ctx* c) { return c ? c->var_spmm : 0; }
 
 // Gather-sum of edges [e0, e1) of one row into acc (lanes of slot `slot`, sub-lane `sub`).

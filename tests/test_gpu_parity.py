@@ -334,7 +334,8 @@ def test_epoch_parity(G, ctx, prod, arxiv, which, corr, epochs, rep, capacity):
                                                ("gcn", "gemm", "f32", 1), ("sage", "gemm", "f32", 1),
                                                ("gcn", "spmm", "bf16", 1), ("sage", "spmm", "f32", 1),
                                                ("gcn", "spmm", "bf16", 3), ("gcn", "spmm", "bf16", 2),
-                                               ("gcn", "spmm", "bf16", 5), ("sage", "spmm", "f32", 5)])
+                                               ("gcn", "spmm", "bf16", 5), ("sage", "spmm", "f32", 5),
+                                               ("sage", "spmm", "bf16", 5)])
 def test_kernel_variants_agree(G, ctx, prod, arch, op, dtype, alt):
     """Alternative implementations agree on the same layer and inputs: bf16 tcgen05 GEMMs vs
     the CUDA-core GEMMs; the split-fp32 tcgen05 GEMMs (fp32 storage) vs the FFMA ones (1e-5); the
