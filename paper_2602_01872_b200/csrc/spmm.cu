@@ -93,7 +93,12 @@ __device__ __forceinline__ void ffma2(float& a0, float& a1, float w, float x0, f
 // Measured and not kept: a persistent grid-stride version of the lean kernel (255 vs 220 us per
 // products call: static row-group assignment loses the block scheduler's balancing) and a
 // packed epilogue (FMUL2 / FFMA2, ReLU folded into the bf16 pack) with a division-free slot
-// split (242 vs 220 us: more live registers, spills at the 32-register bound).
+// split (242 vs 220 us: more live registers, spills at the 32-register bound); the split-row
+// combine fused into this kernel (last-arriving segment sums its row; 436 us: the fence and
+// counter path inflated every launch); a tensor-core aggregation (8 targets per warp, their edge
+// lists walked 16 at a time, neighbour rows staged by cp.async, D += S^T B with B the 0/1
+// edge-to-target matrix via ldmatrix.trans + mma.sync m16n8k16; correct to 1e-6) at 506 us:
+// latency-bound on the staged chunk, ~2.3x slower at equal bytes in flight.
 static inline int spmm_var(const grappa_ctx* c) { return c ? c->var_spmm : 0; }
 
 // Gather-sum of edges [e0, e1) of one row into acc (lanes of slot `slot`, sub-lane `sub`).

@@ -56,6 +56,9 @@ def main():
             ref = out.clone()
         else:
             same = torch.equal(out.view(torch.int16), ref.view(torch.int16))
+            if not same:
+                e = ((out.float() - ref.float()).abs().max() / ref.float().abs().max()).item()
+                same = f"False (max rel diff {e:.2e})"
         print(f"variant {v}: spmm {ms / calls * 1e3:.1f} us/call, {by / calls / 1e9:.3f} GB algorithmic, "
               f"{by / (ms / 1e3) / 1e9:.0f} GB/s, bitwise == first variant: {same}", flush=True)
     ctx.close()
