@@ -395,10 +395,27 @@ __global__ void __launch_bounds__(256, 6) k_task_fill(const int64_t* __restrict_
             for (int32_t off = 0; off < Lm; off += 32) {
                 int32_t u[kPackU];
                 bool keep[kPackU];
+                if (EC) {
+                    // the chunk byte and the neighbour id are independent loads: issue all 2 x kPackU
+                    // together (a membership test behind the id load serialised the two latencies)
+                    bool in[kPackU];
+                    int c[kPackU];
 #pragma unroll
-                for (int k = 0; k < kPackU; k++) u[k] = off + lane < L[k] ? __ldg(g_col + E[k] + off + lane) : -1;
+                    for (int k = 0; k < kPackU; k++) in[k] = off + lane < L[k];
 #pragma unroll
-                for (int k = 0; k < kPackU; k++) keep[k] = u[k] >= 0 && member<EC>(mb, E[k] + off + lane, u[k]);
+                    for (int k = 0; k < kPackU; k++) {
+                        u[k] = in[k] ? __ldg(g_col + E[k] + off + lane) : -1;
+                        c[k] = in[k] ? (int)__ldg(mb.ec + E[k] + off + lane) : -1;
+                    }
+#pragma unroll
+                    for (int k = 0; k < kPackU; k++)
+                        keep[k] = in[k] && (mb.keep_all || c[k] == mb.b || c[k] == mb.s);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < kPackU; k++) u[k] = off + lane < L[k] ? __ldg(g_col + E[k] + off + lane) : -1;
+#pragma unroll
+                    for (int k = 0; k < kPackU; k++) keep[k] = u[k] >= 0 && member<EC>(mb, E[k] + off + lane, u[k]);
+                }
 #pragma unroll
                 for (int k = 0; k < kPackU; k++) {
                     const unsigned bal = __ballot_sync(0xffffffffu, keep[k]);
