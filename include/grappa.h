@@ -414,7 +414,9 @@ grappa_status grappa_layer_fwd(grappa_ctx* ctx, const grappa_part* part, grappa_
  *     GCN then evaluates aggregate-first, Z = (Ahat h_in) W: the forward keeps P = Ahat h_in in
  *     `saved` (size: grappa_layer_saved_bytes_ex with this flag), and the backward is dW = P^T dz
  *     alone -- no aggregation (a re-association of the same products, reading R29; one bf16
- *     rounding of P instead of one of h_in W).  The backward takes no normalised-gradient flags.
+ *     rounding of P instead of one of h_in W).  P is formed as N (h'_v + sum_u h'_u) from the
+ *     pre-scaled rows h' = N h_in (rounded to the storage dtype; reading R29c), so the gather
+ *     carries no per-edge weight.  The backward takes no normalised-gradient flags.
  *     No effect for SAGE / GAT (SAGE is aggregate-first already). */
 #define GRAPPA_LAYER_INPUT 8u
 size_t grappa_layer_saved_bytes_ex(const grappa_part* part, grappa_arch arch, int32_t f_in,

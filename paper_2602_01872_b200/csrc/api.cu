@@ -284,7 +284,8 @@ extern "C" size_t grappa_layer_ws_bytes(const grappa_part* part, grappa_arch arc
     const int64_t n = part->info.n_core, slots = std::max<int64_t>(part->info.n_slots, part->t_n_slots);
     const size_t es = esz_of(dtype);
     const int wmax = f_in > f_out ? f_in : f_out;
-    size_t node = (size_t)n * (arch == GRAPPA_GCN ? f_out : f_in) * es;       // T / dT / dM
+    // T / dT / dM; GCN: also the input layer's pre-scaled rows N h_in (width f_in)
+    size_t node = (size_t)n * (arch == GRAPPA_GCN ? wmax : f_in) * es;
     size_t partial = (size_t)slots * wmax * 4;
     size_t splitk = gemm_tn_ws_bytes(n, f_in, arch == GRAPPA_GCN ? 0 : f_in, f_out);
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
@@ -302,7 +303,7 @@ static WsLayout carve(const grappa_part* part, grappa_arch arch, int f_in, int f
     const size_t es = esz_of(dt);
     const int wmax = f_in > f_out ? f_in : f_out;
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
-    size_t node = al((size_t)n * (arch == GRAPPA_GCN ? f_out : f_in) * es);
+    size_t node = al((size_t)n * (arch == GRAPPA_GCN ? wmax : f_in) * es);   // as grappa_layer_ws_bytes
     size_t partial = al((size_t)slots * wmax * 4);
     char* b = (char*)ws;
     return WsLayout{b, (float*)(b + node), (float*)(b + node + partial)};
@@ -352,8 +353,11 @@ extern "C" grappa_status grappa_layer_fwd_ex(grappa_ctx* ctx, const grappa_part*
     if (arch == GRAPPA_GCN && (flags & GRAPPA_LAYER_INPUT)) {
         // input layer, aggregate-first: P = Ahat h_in (kept in `saved`), h_out = act(P W); its
         // backward is then dW = P^T dz with no aggregation at all (no dh_in for the input)
+        // (R29c) the source normalisation is applied once per row, h' = N h_in rounded to the
+        // storage dtype, so the aggregation gathers unweighted rows: P = N (h'_v + sum h'_u)
+        GRAPPA_TRY(row_scale(ctx, h_in, I.n_core, f_in, I.norm_gcn, L.node, dtype, s));
         SpmmArgs a;
-        a.X = h_in; a.width = f_in; a.row_scale = I.norm_gcn; a.col_scale = I.norm_gcn; a.nbr_scale = w_node;
+        a.X = L.node; a.width = f_in; a.row_scale = I.norm_gcn; a.col_scale = nullptr; a.nbr_scale = w_node;
         a.self = 1; a.out = saved; a.partial = L.partial;
         GRAPPA_TRY(spmm(ctx, part, a, dtype, s));
         GemmArgs g;

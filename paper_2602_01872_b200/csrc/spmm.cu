@@ -643,6 +643,41 @@ grappa_status spmm_fixup(grappa_ctx* ctx, const SpmmArgs& a, cudaStream_t s) {
     return GRAPPA_OK;
 }
 
+// out[v] = scale[v] * X[v] (rounded to the storage dtype), 16 bytes per thread: the GCN input
+// layer's source normalisation applied once per row, so its aggregation gathers unweighted rows
+// (R29c) instead of loading scale[u] per edge (the weighted walk: 378 us per products call at
+// width 112, the unweighted one ~205 us + this pass ~45 us)
+template <typename T>
+__global__ void k_row_scale(int64_t n, int wv, const T* __restrict__ X, const float* __restrict__ scale,
+                            T* __restrict__ out) {
+    constexpr int E = Vec<T>::EPV;
+    const int64_t total = n * wv;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = i / wv;
+        const float sc = __ldg(scale + v);
+        float f[E];
+        Vec<T>::to_f(Vec<T>::load(X + i * E), f);
+#pragma unroll
+        for (int q = 0; q < E; q++) f[q] *= sc;
+        Vec<T>::store(out + i * E, f);
+    }
+}
+
+grappa_status row_scale(grappa_ctx* ctx, const void* X, int64_t n, int width, const float* scale, void* out,
+                        grappa_dtype dt, cudaStream_t s) {
+    if (n <= 0) return GRAPPA_OK;
+    const int E = dt == GRAPPA_BF16 ? 8 : 4;
+    const int wv = width / E;
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n * wv, 256), (int64_t)ctx->sm_count * 16);
+    if (dt == GRAPPA_BF16)
+        k_row_scale<__nv_bfloat16><<<grid, 256, 0, s>>>(n, wv, (const __nv_bfloat16*)X, scale, (__nv_bfloat16*)out);
+    else
+        k_row_scale<float><<<grid, 256, 0, s>>>(n, wv, (const float*)X, scale, (float*)out);
+    GRAPPA_LAUNCHED(ctx);
+    return GRAPPA_OK;
+}
+
 static double spmm_bytes(const SpmmArgs& a, grappa_dtype dt) {
     const double es = dt == GRAPPA_BF16 ? 2.0 : 4.0, w = a.width, nnz = (double)a.nnz;
     const double per_edge = 4.0 + (a.col_scale || a.edge_w ? 4.0 : 0.0) + w * es;

@@ -52,5 +52,8 @@ grappa_status spmm_t(grappa_ctx* ctx, const grappa_part* part, SpmmArgs a, grapp
 // same kernel on an explicit CSR (a.n rows, a.nnz, a.rowptr, a.col, optional split rows);
 // used for the rectangular mini-batch blocks and their transposes
 grappa_status spmm_csr(grappa_ctx* ctx, SpmmArgs a, grappa_dtype dt, cudaStream_t s);
+// out[v] = scale[v] * X[v] over n rows of `width` elements (rounded to dt)
+grappa_status row_scale(grappa_ctx* ctx, const void* X, int64_t n, int width, const float* scale, void* out,
+                        grappa_dtype dt, cudaStream_t s);
 
 }  // namespace grappa
