@@ -98,7 +98,8 @@ __device__ __forceinline__ void ffma2(float& a0, float& a1, float w, float x0, f
 // counter path inflated every launch); a tensor-core aggregation (8 targets per warp, their edge
 // lists walked 16 at a time, neighbour rows staged by cp.async, D += S^T B with B the 0/1
 // edge-to-target matrix via ldmatrix.trans + mma.sync m16n8k16; correct to 1e-6) at 506 us:
-// latency-bound on the staged chunk, ~2.3x slower at equal bytes in flight.
+// latency-bound on the staged chunk, ~2.3x slower at equal bytes in flight; the row's own
+// vector and row scale requested before the gathers (244 vs 222 us: spills at 32 registers).
 static inline int spmm_var(const grappa_ctx* c) { return c ? c->var_spmm : 0; }
 
 // Gather-sum of edges [e0, e1) of one row into acc (lanes of slot `slot`, sub-lane `sub`).
