@@ -457,11 +457,13 @@ __device__ __forceinline__ void grp_accumulate_lean(const T* __restrict__ X, con
 // P = 32/G independent rows and their dependent load chains (rowptr -> col -> scale /
 // feature row) overlap; no cross-group reduction is needed.
 template <typename T, int R, int U, bool WT, bool LEAN = false, int MB = 1>
-__global__ void __launch_bounds__(256, MB) k_spmm_grp(SpmmArgs a, int G, int P) {
+__global__ void __launch_bounds__(256, MB) k_spmm_grp(SpmmArgs a, int G, int P, unsigned gmagic) {
     constexpr int E = Vec<T>::EPV;
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int slot = lane / G, sub = lane - slot * G;
+    // lane / G without an integer division (lane < 32, G <= 32): lane * gmagic >> 16 with
+    // gmagic = ceil(2^16 / G) (host) is exact, the rounding term is below 32 / 2^16
+    const int slot = (int)(((unsigned)lane * gmagic) >> 16), sub = lane - slot * G;
     const int WV = G;
     const int64_t vrow = warp * P + slot;
     int64_t e0 = 0, e1 = 0, orow = -1;
@@ -579,16 +581,17 @@ static grappa_status launch_grp(grappa_ctx* ctx, const SpmmArgs& a, int G, cudaS
     const int64_t vrows = a.n + a.n_slots;   // split-row segments first, then the rows
     if (vrows > 0) {
         const unsigned grid = (unsigned)ceil_div(ceil_div(vrows, P), 8);
+        const unsigned gm = (65536u + (unsigned)G - 1u) / (unsigned)G;
         if (spmm_var(ctx) == 2) {
-            if (a.col_scale || a.edge_w) k_spmm_grp<T, R, 8, true><<<grid, 256, 0, s>>>(a, G, P);
-            else k_spmm_grp<T, R, 8, false><<<grid, 256, 0, s>>>(a, G, P);
+            if (a.col_scale || a.edge_w) k_spmm_grp<T, R, 8, true><<<grid, 256, 0, s>>>(a, G, P, gm);
+            else k_spmm_grp<T, R, 8, false><<<grid, 256, 0, s>>>(a, G, P, gm);
         } else {
             // weighted gathers keep grp_accumulate: a lean weighted walk (weight loaded one
             // sub-chunk ahead and shuffled with the index, predicated FFMA2) measured no faster
             // (GCN input layer 378 -> 402 us per products call; node-level epoch 41.7 -> 42.4 ms)
-            if (a.col_scale || a.edge_w) k_spmm_grp<T, R, 4, true><<<grid, 256, 0, s>>>(a, G, P);
-            else if (spmm_var(ctx) == 5) k_spmm_grp<T, R, 4, false><<<grid, 256, 0, s>>>(a, G, P);
-            else k_spmm_grp<T, R, 2, false, true, 8><<<grid, 256, 0, s>>>(a, G, P);
+            if (a.col_scale || a.edge_w) k_spmm_grp<T, R, 4, true><<<grid, 256, 0, s>>>(a, G, P, gm);
+            else if (spmm_var(ctx) == 5) k_spmm_grp<T, R, 4, false><<<grid, 256, 0, s>>>(a, G, P, gm);
+            else k_spmm_grp<T, R, 2, false, true, 8><<<grid, 256, 0, s>>>(a, G, P, gm);
         }
         GRAPPA_LAUNCHED(ctx);
     }
