@@ -637,6 +637,10 @@ typedef enum {
  *              previous per-edge-predicated unweighted schedule (same sums, bitwise).
  *   op "pair": 0 = GCN backward computes dz_in and dW in one pass over dT and h_in (bf16,
  *              default), 1 = the two separate GEMMs.
+ *   op "wstream": tcgen05 transform GEMM's weight operand: 0 = converted once into a bf16
+ *              image and streamed per k-block when the call has <= 2 row tiles per SM, else
+ *              resident in shared memory (default), 1 = always streamed, 2 = resident whenever
+ *              it fits.  Same products and fp32 accumulation order either way (bitwise).
  * Returns E_ARG for a null ctx, an unknown op or an out-of-range variant. */
 grappa_status grappa_set_kernel_variant(grappa_ctx* ctx, const char* op, int variant);
 

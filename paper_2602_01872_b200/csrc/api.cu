@@ -219,6 +219,7 @@ extern "C" grappa_status grappa_set_kernel_variant(grappa_ctx* ctx, const char* 
     if (!strcmp(op, "gemm") && variant >= 0 && variant <= 2) { ctx->var_gemm = variant; return GRAPPA_OK; }
     if (!strcmp(op, "spmm") && variant >= 0 && variant <= 5) { ctx->var_spmm = variant; return GRAPPA_OK; }
     if (!strcmp(op, "pair") && variant >= 0 && variant <= 1) { ctx->var_pair = variant; return GRAPPA_OK; }
+    if (!strcmp(op, "wstream") && variant >= 0 && variant <= 2) { ctx->var_gemm_stream = variant; return GRAPPA_OK; }
     set_error("grappa_set_kernel_variant: unknown op '%s' or variant %d", op, variant);
     return GRAPPA_E_ARG;
 }

@@ -124,6 +124,7 @@ struct grappa_ctx {
     // cores; spmm 0 = row-group, 1 = warp per row, 2 = 8 loads in flight, 3 = natural row order;
     // pair 1 = separate GCN backward GEMMs
     int var_gemm = 0, var_spmm = 0, var_pair = 0;
+    int var_gemm_stream = 0;     // tcgen05 NN weight: 0 = streamed image when <= 2 tiles per SM, 1 = always, 2 = never
     // chunk map whose per-chunk counts are known (grappa_partition, or verified once by
     // grappa_repartition_batch): the batched switch allocates from them without a sync
     const int32_t* cmap_ptr = nullptr;

@@ -1143,8 +1143,8 @@ static size_t nn_smem_of(int kbt, int N, int stages, int nsb, int mask_tma, int 
            (mask_tma ? (size_t)4 * kBoxBytes : 0) + 256;
 }
 // resident weights when they fit next to a ring of >= 2 stages, else streamed weight k-blocks
-static bool nn_plan(int kbt, int N, int mask_tma, int* stages, int* nsb, int* b_stream) {
-    for (int bs = 0; bs <= 1; bs++)
+static bool nn_plan(int kbt, int N, int mask_tma, int* stages, int* nsb, int* b_stream, int prefer_stream = 0) {
+    for (int bs = prefer_stream; bs <= 1; bs++)
         for (int b = 2; b >= 1; b--)
             for (int st = kMaxNNStages; st >= 2; st--)
                 if (nn_smem_of(kbt, N, st, b, mask_tma, bs) <= (size_t)kMaxSmem && (b == 1 || st >= 4)) {
@@ -1185,9 +1185,15 @@ grappa_status gemm_tc_nn(grappa_ctx* ctx, const GemmArgs& g, cudaStream_t s) {
     p.nb1 = (int)ceil_div(g.n_split, 64); p.nb2 = (int)ceil_div(g.N - g.n_split, 64);
     p.num_tiles = (int)ceil_div(g.M, 128);
     p.tmem_cols = pow2_cols(2 * g.N);
+    // few tiles per CTA (mini-batch blocks): the per-CTA fp32 -> bf16 staging of the whole weight
+    // is not amortised (ncu: ~half of a 19 us call at M = 10^4), so the weight is converted once
+    // into the SW128 image (k_weight_image) and streamed per k-block by bulk copies instead
+    const int prefer_stream = (ctx->var_gemm_stream == 1 || (ctx->var_gemm_stream == 0 &&
+                               p.num_tiles <= 2 * (int64_t)ctx->sm_count)) ? 1 : 0;
     // relu'-gate through TMA when each epilogue group owns at most one gated box and it fits
-    p.mask_tma = p.has_mask && p.nb1 <= 2 && nn_plan(p.kb1 + p.kb2, g.N, 1, &p.stages, &p.nsb, &p.b_stream) ? 1 : 0;
-    if (!p.mask_tma && !nn_plan(p.kb1 + p.kb2, g.N, 0, &p.stages, &p.nsb, &p.b_stream)) {
+    p.mask_tma = p.has_mask && p.nb1 <= 2 &&
+                 nn_plan(p.kb1 + p.kb2, g.N, 1, &p.stages, &p.nsb, &p.b_stream, prefer_stream) ? 1 : 0;
+    if (!p.mask_tma && !nn_plan(p.kb1 + p.kb2, g.N, 0, &p.stages, &p.nsb, &p.b_stream, prefer_stream)) {
         set_error("gemm_tc_nn: shape does not fit shared memory");
         return GRAPPA_E_SUPPORT;
     }
