@@ -118,6 +118,7 @@ struct grappa_ctx {
     // workspaces: scan partials, degree-bucket counters + seed-statistics partials, rank table
     static constexpr int kRpStreams = 8;
     cudaStream_t rp_s[kRpStreams] = {};
+    int rp_prio = 0;             // priority the side streams were created with (the caller's)
     cudaEvent_t rp_ev[kRpStreams + 1] = {};
     grappa::DevBuf rp_scan[kRpStreams], rp_small[kRpStreams], rp_rank[kRpStreams];
     // test / A-B kernel selection (grappa_set_kernel_variant): gemm 0 = tensor cores, 1/2 = CUDA

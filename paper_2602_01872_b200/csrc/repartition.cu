@@ -1275,8 +1275,19 @@ extern "C" grappa_status grappa_repartition_batch_ix(grappa_ctx* ctx, const grap
     // small latency-bound kernels of different partitions overlap.  Fork after the stats memset,
     // join before each host sync.
     const int NS = std::min(K, (int)grappa_ctx::kRpStreams);
-    for (int j = 0; j < NS; j++)
-        if (!ctx->rp_s[j]) RB_CUDA(cudaStreamCreateWithFlags(&ctx->rp_s[j], cudaStreamNonBlocking));
+    // the side streams take the caller stream's priority (a prefetched switch runs on a
+    // high-priority stream so its kernels are scheduled ahead of the epoch being replayed)
+    int prio = 0;
+    RB_CUDA(cudaStreamGetPriority(s, &prio));
+    for (int j = 0; j < NS; j++) {
+        if (ctx->rp_s[j] && ctx->rp_prio != prio) {
+            RB_CUDA(cudaStreamSynchronize(ctx->rp_s[j]));
+            RB_CUDA(cudaStreamDestroy(ctx->rp_s[j]));
+            ctx->rp_s[j] = nullptr;
+        }
+        if (!ctx->rp_s[j]) RB_CUDA(cudaStreamCreateWithPriority(&ctx->rp_s[j], cudaStreamNonBlocking, prio));
+    }
+    ctx->rp_prio = prio;
     for (int j = 0; j <= NS; j++)
         if (!ctx->rp_ev[j]) RB_CUDA(cudaEventCreateWithFlags(&ctx->rp_ev[j], cudaEventDisableTiming));
     auto fork = [&]() -> grappa_status {

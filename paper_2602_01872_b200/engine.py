@@ -699,7 +699,9 @@ class Trainer:
         mine = [w for _, w in self.my_workers() if w < self.W]
         pairs = self.schedule[(t1 - 1) % len(self.schedule)]
         if getattr(self, "pf_stream", None) is None:
-            self.pf_stream = torch.cuda.Stream(self.dev)
+            # high priority: the switch's kernels are scheduled ahead of the replay they
+            # overlap, so the host's size syncs return after the switch's own GPU work
+            self.pf_stream = torch.cuda.Stream(self.dev, priority=-1)
             self.alt_parts = {}
         if getattr(self, "alt_free", None) is not None:
             self.pf_stream.wait_event(self.alt_free)      # the other set's last graph has finished
