@@ -22,6 +22,9 @@ t = time.time()
 ds = gen.make_dataset(wl)
 print("gen", round(time.time() - t, 1), "s  nnz", ds.nnz, flush=True)
 ctx = G.Context(0)
+for kv in filter(None, os.environ.get("GRAPPA_VARIANTS", "").split(",")):   # e.g. tnrows=2,wstream=2
+    k, v = kv.split("=")
+    ctx.set_variant(k, int(v))
 spec = ModelSpec(wl.arch, wl.dims, wl.dims_pad)
 t = time.time()
 tr = MinibatchTrainer(ctx, ds.rowptr, ds.col, ds.x, ds.y, ds.train, spec, ds.weights, 8, gen.seed_of("chunks"),
