@@ -289,14 +289,17 @@ extern "C" size_t grappa_layer_ws_bytes(const grappa_part* part, grappa_arch arc
     size_t node = (size_t)n * (arch == GRAPPA_GCN ? wmax : f_in) * es;
     size_t partial = (size_t)slots * wmax * 4;
     size_t splitk = gemm_tn_ws_bytes(n, f_in, arch == GRAPPA_GCN ? 0 : f_in, f_out);
+    // GCN node-level backward: the pre-weighted rows w_u dz_u (R30c)
+    size_t node2 = arch == GRAPPA_GCN ? (size_t)n * f_out * es : 0;
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
-    return al(node) + al(partial) + al(splitk);
+    return al(node) + al(partial) + al(splitk) + al(node2);
 }
 
 struct WsLayout {
     void* node;
     float* partial;
     float* splitk;
+    void* node2;
 };
 static WsLayout carve(const grappa_part* part, grappa_arch arch, int f_in, int f_out,
                       grappa_dtype dt, void* ws) {
@@ -306,8 +309,9 @@ static WsLayout carve(const grappa_part* part, grappa_arch arch, int f_in, int f
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     size_t node = al((size_t)n * (arch == GRAPPA_GCN ? wmax : f_in) * es);   // as grappa_layer_ws_bytes
     size_t partial = al((size_t)slots * wmax * 4);
+    size_t splitk = al(gemm_tn_ws_bytes(n, f_in, arch == GRAPPA_GCN ? 0 : f_in, f_out));
     char* b = (char*)ws;
-    return WsLayout{b, (float*)(b + node), (float*)(b + node + partial)};
+    return WsLayout{b, (float*)(b + node), (float*)(b + node + partial), b + node + partial + splitk};
 }
 
 static grappa_status check_dims(const char* who, int f_in, int f_out) {
@@ -443,7 +447,14 @@ extern "C" grappa_status grappa_layer_bwd_ex(grappa_ctx* ctx, const grappa_part*
         SpmmArgs a;
         a.X = dz_out; a.width = f_out; a.row_scale = I.norm_gcn; a.col_scale = out_normed ? nullptr : I.norm_gcn;
         if (node) {
-            a.col_scale = out_normed ? I.node_w : I.node_w + I.n_core;
+            // (R30c) the neighbour weight w_u (w_u n_u unnormalised) is applied once per row:
+            // dz' = w dz rounded to the storage dtype, gathered unweighted; the self term reads
+            // the unweighted dz_v
+            GRAPPA_TRY(row_scale(ctx, dz_out, I.n_core, f_out, out_normed ? I.node_w : I.node_w + I.n_core,
+                                 L.node2, dtype, s));
+            a.X = L.node2;
+            a.X_self = dz_out;
+            a.col_scale = nullptr;
             a.self_sep = 1;
             a.self_scale = out_normed ? nullptr : I.norm_gcn;
         }

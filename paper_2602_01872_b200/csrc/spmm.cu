@@ -174,7 +174,7 @@ template <typename T, int CPL>
 __device__ __forceinline__ void epilogue(const SpmmArgs& a, int64_t v, int64_t ov, int sub, int G,
                                          int WV, float (&acc)[CPL][Vec<T>::EPV]) {
     constexpr int E = Vec<T>::EPV;
-    const T* X = reinterpret_cast<const T*>(a.X);
+    const T* X = reinterpret_cast<const T*>(a.X_self ? a.X_self : a.X);   // the self term's rows
     T* out = reinterpret_cast<T*>(a.out);
     const T* mask = reinterpret_cast<const T*>(a.mask);
     const float rs = a.row_scale ? a.row_scale[v] : 1.f;

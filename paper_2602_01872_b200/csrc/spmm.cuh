@@ -19,6 +19,8 @@ struct SpmmArgs {
     const int4* row_desc = nullptr;        // optional {v, deg, e0 lo, e0 hi} in that order
     // caller
     const void* X = nullptr;          // [n x width] dtype
+    const void* X_self = nullptr;     // rows of the self term if not X (node-level backward: X holds
+                                      // the pre-weighted rows w_u dz_u, the self term is unweighted)
     int width = 0;                    // elements per row (multiple of 4)
     const float* row_scale = nullptr; // rs[v] or null (1)
     const float* col_scale = nullptr; // cs[u] or null (1); also weights the self term

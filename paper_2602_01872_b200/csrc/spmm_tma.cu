@@ -390,7 +390,7 @@ bool spmm_tma_eligible(const grappa_ctx* ctx, const SpmmArgs& a, grappa_dtype dt
     // bf16 rows of 80..128 elements (two rows per consumer warp), unweighted neighbour sum with a
     // plain self term: every GCN hidden-layer aggregation of the normalised chain (R29)
     return ctx && ctx->var_spmm == 4 && dt == GRAPPA_BF16 && a.width % 16 == 0 && a.width >= 80 &&
-           a.width <= 128 && !a.col_scale && !a.edge_w && !a.accumulate && !a.mask && !a.self_sep &&
+           a.width <= 128 && !a.col_scale && !a.edge_w && !a.accumulate && !a.mask && !a.self_sep && !a.X_self &&
            !a.out_compact && a.n > 0 && a.n < (1ll << 31);
 }
 
