@@ -407,7 +407,9 @@ grappa_status grappa_layer_fwd(grappa_ctx* ctx, const grappa_part* part, grappa_
  *     every target's aggregated neighbour message is multiplied by w_v = d_l/d_g:
  *       GCN  Ahat_w = N (diag(w) A_loc + I) N   (self term unweighted)
  *       SAGE M = diag(w) D_l^-1 A_loc h_in       (= local sum / d_g)
- *     and the backward is the exact transpose (Ahat_w^T = N (A_loc diag(w) + I) N).
+ *     and the backward is the exact transpose (Ahat_w^T = N (A_loc diag(w) + I) N); GCN
+ *     evaluates it from dz' = w dz rounded to the storage dtype (reading R30c), so the gather
+ *     is unweighted (ws: grappa_layer_ws_bytes holds dz').
  *     Pair it with GRAPPA_CORR_NODE in the aggregation (batch factor 1).               */
 #define GRAPPA_LAYER_NODE_LEVEL 4u
 /*   GRAPPA_LAYER_INPUT : the model's first layer (its backward is called with dz_in = NULL).
