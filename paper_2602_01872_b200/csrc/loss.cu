@@ -24,8 +24,10 @@ template <typename T>
 __global__ void __launch_bounds__(kLossThreads) k_loss(int64_t n_seeds, const int32_t* rows,
                                                        const int32_t* lidx, const int32_t* labels,
                                                        const T* logits, int K, int kpad, T* dlogits,
-                                                       double* part, const float* __restrict__ rscale) {
+                                                       double* part, const float* __restrict__ rscale,
+                                                       unsigned* done, double inv_n, double* out) {
     __shared__ double wsum[kLossThreads / 32];
+    __shared__ bool last;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t k = (int64_t)blockIdx.x * (kLossThreads / 32) + wid;
     double my = 0.0;
@@ -57,6 +59,26 @@ __global__ void __launch_bounds__(kLossThreads) k_loss(int64_t n_seeds, const in
         double s = 0.0;
         for (int w = 0; w < kLossThreads / 32; w++) s += wsum[w];
         part[blockIdx.x] = s;
+        // the block that completes the count combines the partials (k_loss_final's fixed order,
+        // so the value is the two-launch one bit for bit) and resets the count
+        __threadfence();
+        last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int nb = (int)gridDim.x;
+    const int per = (nb + 255) / 256;
+    double s = 0.0;
+    for (int b = threadIdx.x * per, e = min(nb, b + per); b < e; b++) s += __ldcg(part + b);
+    s = warp_sum(s);
+    if (lane == 0) wsum[wid] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; w++) t += wsum[w];
+        *out = t * inv_n;
+        *done = 0u;
     }
 }
 
@@ -89,17 +111,26 @@ grappa_status loss_rows(grappa_ctx* ctx, int64_t n_seeds, const int32_t* rows, c
     const int64_t nb = ceil_div(n_seeds, kLossThreads / 32);
     // the loss's own scratch: a captured epoch graph references it, and a switch prefetched on a
     // side stream (engine) may reuse the repartition workspaces while that graph runs
-    GRAPPA_TRY(ctx->loss_ws.grow((size_t)nb * sizeof(double)));
-    double* part_sums = (double*)ctx->loss_ws.p;
+    // [arrival count (zero between calls) | nb partial sums]
+    void* before = ctx->loss_ws.p;
+    GRAPPA_TRY(ctx->loss_ws.grow((size_t)(nb + 1) * sizeof(double)));
+    unsigned* done = (unsigned*)ctx->loss_ws.p;
+    if (ctx->loss_ws.p != before) GRAPPA_CUDA(cudaMemsetAsync(done, 0, sizeof(double), s));
+    double* part_sums = (double*)ctx->loss_ws.p + 1;
+    if (n_seeds <= 0) {
+        k_loss_final<<<1, 256, 0, s>>>(0, part_sums, 0.0, loss_dev);
+        GRAPPA_LAUNCHED(ctx);
+        return GRAPPA_OK;
+    }
+    const double inv_n = 1.0 / (double)n_seeds;
     if (dtype == GRAPPA_BF16)
         k_loss<__nv_bfloat16><<<(unsigned)nb, kLossThreads, 0, s>>>(
             n_seeds, rows, lidx, labels, (const __nv_bfloat16*)logits, K, k_pad, (__nv_bfloat16*)dlogits,
-            part_sums, rscale);
+            part_sums, rscale, done, inv_n, loss_dev);
     else
         k_loss<float><<<(unsigned)nb, kLossThreads, 0, s>>>(n_seeds, rows, lidx, labels, (const float*)logits,
-                                                            K, k_pad, (float*)dlogits, part_sums, rscale);
-    GRAPPA_LAUNCHED(ctx);
-    k_loss_final<<<1, 256, 0, s>>>((int)nb, part_sums, 1.0 / (double)n_seeds, loss_dev);
+                                                            K, k_pad, (float*)dlogits, part_sums, rscale, done,
+                                                            inv_n, loss_dev);
     GRAPPA_LAUNCHED(ctx);
     return GRAPPA_OK;
 }

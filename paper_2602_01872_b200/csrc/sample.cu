@@ -744,13 +744,13 @@ extern "C" grappa_status grappa_minibatch_step_ex(grappa_ctx* ctx, const grappa_
         g.M = B.n_dst; g.K1 = dp[l + 1]; g.N = 2 * dp[l]; g.A1 = dz; g.B = theta + woff[l]; g.b_trans = 1;
         g.n_split = dp[l]; g.C1 = dz_in; g.C2 = w + lay.dM;
         GRAPPA_TRY(gemm_nn(ctx, g, dt, s));
-        if (B.n_src > B.n_dst)
-            GRAPPA_CUDA(cudaMemsetAsync(dz_in + (size_t)B.n_dst * dp[l] * es, 0,
-                                        (size_t)(B.n_src - B.n_dst) * dp[l] * es, s));
+        // source-only rows (n_dst .. n_src) have no dh_s term: the SpMM writes them instead of
+        // accumulating (no zero fill of dz_in's tail)
         SpmmArgs a;
         a.n = B.n_src; a.nnz = B.nnz; a.rowptr = (const int64_t*)B.trowptr.p; a.col = (const int32_t*)B.tcol.p;
         a.X = w + lay.dM; a.width = dp[l];
         a.col_scale = (const float*)(node ? B.inv_cnt_node.p : B.inv_cnt.p); a.accumulate = 1;
+        a.acc_rows = B.n_dst;
         a.mask = w + lay.H[l]; a.out = dz_in;
         GRAPPA_TRY(spmm_csr(ctx, a, dt, s));
         dz = dz_in;

@@ -204,7 +204,7 @@ __device__ __forceinline__ void epilogue(const SpmmArgs& a, int64_t v, int64_t o
         }
 #pragma unroll
         for (int q = 0; q < E; q++) r[q] *= rs;
-        if (a.accumulate) {
+        if (a.accumulate && v < a.acc_rows) {
             float f[E];
             Vec<T>::to_f(Vec<T>::load_rw(out + ooff), f);
 #pragma unroll

@@ -31,6 +31,8 @@ struct SpmmArgs {
     const float* self_scale = nullptr;
     int relu = 0;
     int accumulate = 0;
+    int64_t acc_rows = INT64_MAX;     // accumulate into out rows < acc_rows only (rows past it are
+                                      // written: a block transpose's source-only rows)
     const void* mask = nullptr;       // [n x width] dtype or null
     void* out = nullptr;              // [n x width] dtype
     float* partial = nullptr;         // [n_slots x width] fp32 scratch
