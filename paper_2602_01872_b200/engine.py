@@ -693,6 +693,21 @@ class Trainer:
             print(f"[graph] prefetch of super-epoch {t1}: repartition {1e3 * (h1 - h0):.1f} ms, record "
                   f"{1e3 * (time.perf_counter() - h1):.1f} ms (overlapping the replay)", file=sys.stderr)
 
+    def warm_prefetch(self):
+        """pay the prefetched switch's one-time costs before a timed region: the second partition
+        set's buffers, the switch index (grappa_index), the prefetch stream and the library's
+        side streams at its priority.  Extracts the next super-epoch's partitions into the second
+        set once (kept as that set's buffers for the real prefetch) and sizes the activation
+        buffers for both sets; call it before the epoch graph is captured.  Without it the first
+        prefetch -- 0.1-1 s of host time in first-touch allocations -- fell inside the timed
+        epochs."""
+        if not self._prefetch_ok():
+            return
+        nparts = self.build_next_parts(self.t + 1)
+        self.pf_stream.synchronize()
+        self.alt_parts = dict(nparts)
+        self._alloc([self._sizes(p) for p in list(self.parts.values()) + list(nparts.values())])
+
     def build_next_parts(self, t1: int) -> dict:
         """the partitions of super-epoch t1 in the second partition set, extracted on the side
         stream `pf_stream` (concurrently with work on the main stream); returns worker -> Part"""
@@ -701,7 +716,8 @@ class Trainer:
         if getattr(self, "pf_stream", None) is None:
             # high priority: the switch's kernels are scheduled ahead of the replay they
             # overlap, so the host's size syncs return after the switch's own GPU work
-            self.pf_stream = torch.cuda.Stream(self.dev, priority=-1)
+            import os
+            self.pf_stream = torch.cuda.Stream(self.dev, priority=int(os.environ.get("GRAPPA_PF_PRIORITY", "-1")))
             self.alt_parts = {}
         if getattr(self, "alt_free", None) is not None:
             self.pf_stream.wait_event(self.alt_free)      # the other set's last graph has finished

@@ -13,7 +13,7 @@ timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_
 echo "bench exit $?"; tail -c 600 gpurun_out/${TAG}_bench.json
 timeout 600 python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/${TAG}_bench_ref.json 2> gpurun_out/${TAG}_bench_ref.err
 echo "ref exit $?"; tail -c 300 gpurun_out/${TAG}_bench_ref.json
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline \
   > gpurun_out/${TAG}_bench_under_ncu.log 2>&1
 echo "ncu launches exit $?"
