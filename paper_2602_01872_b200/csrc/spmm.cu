@@ -93,7 +93,9 @@ __device__ __forceinline__ void ffma2(float& a0, float& a1, float w, float x0, f
 // Measured and not kept: a persistent grid-stride version of the lean kernel (255 vs 220 us per
 // products call: static row-group assignment loses the block scheduler's balancing) and a
 // packed epilogue (FMUL2 / FFMA2, ReLU folded into the bf16 pack) with a division-free slot
-// split (242 vs 220 us: more live registers, spills at the 32-register bound); the split-row
+// split (242 vs 220 us: more live registers, spills at the 32-register bound); a warp-per-
+// split-row fix-up, 8 rows per block (the call 220 -> 241 us: a hub's 100+ segments summed by one
+// warp became the tail); the split-row
 // combine fused into this kernel (last-arriving segment sums its row; 436 us: the fence and
 // counter path inflated every launch); a tensor-core aggregation (8 targets per warp, their edge
 // lists walked 16 at a time, neighbour rows staged by cp.async, D += S^T B with B the 0/1
